@@ -1,0 +1,226 @@
+/*
+ * plaid.h — C ABI of the B200-native PLAID searcher (libplaid.so).
+ *
+ * Drop-in boundary for the reference C++ searcher `lir` (/root/reference/proj).
+ * Plain pointers and sizes only; no CUDA or torch types in any signature
+ * (streams and device pointers travel as void* / uint64 where needed).
+ *
+ * Every entry point names the reference interface it replaces
+ * (include/lir/<file>:<line>).  Status codes mirror lir::ErrorCode
+ * (error.hpp:8-26) shifted by one, plus CUDA/NCCL/unsupported codes; a
+ * thread-local message is available from plaid_last_error().
+ *
+ * Arithmetic contract: integer outputs (candidate sets, pruning masks, unpacked
+ * residual indices, selections) are bit-exact with the reference on identical
+ * inputs.  In PLAID_SCORES_EXACT mode every fp32 score is bit-exact too; in
+ * PLAID_SCORES_TENSOR mode (tcgen05 S_cq) centroid scores are within ~1e-6
+ * absolute and MaxSim scores within 1e-4 relative.
+ */
+#ifndef PLAID_H
+#define PLAID_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLAID_ABI_VERSION 1
+
+/* lir::ErrorCode (error.hpp:8-26) + 1. */
+typedef enum plaid_status {
+    PLAID_OK = 0,
+    PLAID_DIMENSION_MISMATCH = 1,
+    PLAID_NOT_NORMALIZED = 2,
+    PLAID_TOO_FEW_POINTS = 3,
+    PLAID_PACKING_UNSUPPORTED = 4,
+    PLAID_EMPTY_CORPUS = 5,
+    PLAID_INDEX_OUT_OF_RANGE = 6,
+    PLAID_LENGTH_NOT_PACKABLE = 7,
+    PLAID_EMPTY_PASSAGE_RANGE = 8,
+    PLAID_INVALID_PARAMS = 9,
+    PLAID_CHECKSUM_MISMATCH = 10,
+    PLAID_UNSUPPORTED_VERSION = 11,
+    PLAID_INVARIANT_VIOLATION = 12,
+    PLAID_HEADER_MISMATCH = 13,
+    PLAID_NORMALIZATION_ERROR = 14,
+    PLAID_LENGTH_MISMATCH = 15,
+    PLAID_UNKNOWN_QUERY_ID = 16,
+    PLAID_IO_ERROR = 17,
+    PLAID_CUDA_ERROR = 100,
+    PLAID_NCCL_ERROR = 101,
+    PLAID_UNSUPPORTED = 102,  /* outside the engine's envelope, e.g. |Q| > 32 */
+    PLAID_OUT_OF_MEMORY = 103
+} plaid_status;
+
+typedef enum plaid_score_mode {
+    PLAID_SCORES_TENSOR = 0, /* tcgen05 3xTF32 S_cq GEMM (production default) */
+    PLAID_SCORES_EXACT = 1   /* in-order fp32 CUDA-core S_cq, bit-exact with lir */
+} plaid_score_mode;
+
+typedef struct plaid_index plaid_index;       /* device-resident CompressedIndex */
+typedef struct plaid_searcher plaid_searcher; /* stream + scratch, one per host thread */
+
+/* Mirrors lir::CompressedIndex's persisted fields (index.hpp:61-72). */
+typedef struct plaid_index_desc {
+    uint32_t dim;
+    uint32_t nbits;
+    uint64_t num_centroids;          /* K */
+    uint64_t num_passages;           /* N */
+    uint64_t num_embeddings;         /* T = sum(doclens) */
+    const float* centroids;          /* K x dim, row-major, unit rows */
+    const uint32_t* codes;           /* T */
+    const uint8_t* residuals;        /* T x nbits*dim/8, LSB-first packing */
+    const uint32_t* doclens;         /* N */
+    const uint64_t* ivf_offsets;     /* K + 1 */
+    const uint32_t* ivf_postings;    /* ivf_offsets[K], sorted unique per centroid */
+    const float* bucket_cutoffs;     /* 2^nbits - 1 */
+    const float* bucket_weights;     /* 2^nbits */
+} plaid_index_desc;
+
+/* lir::SearchParams (types.hpp:79-84) + SearchOptions.disable_filter (pipeline.hpp:45-48). */
+typedef struct plaid_params {
+    uint64_t k;
+    uint64_t nprobe;
+    float t_cs;
+    uint64_t ndocs;
+    int32_t disable_filter;
+} plaid_params;
+
+/* lir::StageTrace (pipeline.hpp:23-43): counters bit-exact, times from CUDA events. */
+typedef struct plaid_trace {
+    uint64_t stage1_candidates;
+    uint64_t stage2_out;
+    uint64_t stage3_out;
+    uint64_t final_out;
+    uint64_t centroid_matmul_count;
+    uint64_t stage2_rows_gathered;
+    uint64_t stage3_rows_gathered;
+    uint64_t decompressed_passages;
+    double candidate_generation_ms;
+    double stage2_ms;
+    double stage3_ms;
+    double lookup_ms;
+    double decompression_ms;
+    double scoring_ms;
+    double total_ms;
+} plaid_trace;
+
+typedef struct plaid_searcher_config {
+    int32_t score_mode;     /* plaid_score_mode */
+    int32_t record_times;   /* fill the *_ms fields of plaid_trace (adds events) */
+    int32_t use_graphs;     /* replay captured CUDA graphs per parameter set */
+    int32_t reserved;
+} plaid_searcher_config;
+
+/* ---- errors / host-side helpers ------------------------------------------------ */
+const char* plaid_last_error(void);
+const char* plaid_status_name(int status);              /* error.hpp:28-49 */
+int plaid_abi_version(void);
+
+/* types.cpp:61-72 validate_query; types.cpp:88-99 validate_params */
+plaid_status plaid_validate_query(const float* q, uint64_t rows, uint64_t dim, uint64_t index_dim);
+plaid_status plaid_validate_params(const plaid_params* p, uint64_t num_centroids);
+/* types.cpp:74-86 */
+void plaid_default_params_for_k(uint64_t k, plaid_params* out);
+/* pipeline.cpp:227-230 */
+uint64_t plaid_stage3_width(const plaid_params* p);
+
+/* ---- index lifecycle ------------------------------------------------------------ */
+/* Builds the device index from host arrays (index.hpp:60-85 + finalize_derived,
+ * index.cpp:7-10).  validate != 0 runs validate_index's invariants (index.cpp:12-84). */
+plaid_status plaid_index_from_host(const plaid_index_desc* desc, int device, int validate,
+                                   plaid_index** out);
+/* Passage-range shard [pid_begin, pid_end) of a host index: local IVF with
+ * local ids; search results report global ids (local + pid_begin). */
+plaid_status plaid_index_from_host_shard(const plaid_index_desc* desc, uint64_t pid_begin,
+                                         uint64_t pid_end, int device, plaid_index** out);
+/* Re-checks validate_index's invariants on the device copy (index.cpp:12-84). */
+plaid_status plaid_index_validate(plaid_index* index);
+void plaid_index_close(plaid_index* index);
+/* dim, nbits, K, N, T, P, pid_base, device bytes */
+void plaid_index_info(const plaid_index* index, uint64_t out[8]);
+
+/* ---- search ----------------------------------------------------------------------- */
+/* index may be NULL for the index-free kernels (select/unpack/maxsim). */
+plaid_status plaid_searcher_create(plaid_index* index, int device, const plaid_searcher_config* cfg,
+                                   plaid_searcher** out);
+void plaid_searcher_destroy(plaid_searcher* s);
+
+/* lir::search (pipeline.hpp:86-87 / pipeline.cpp:232-283).  Q is host memory,
+ * rows x dim fp32.  out_pids / out_scores hold >= params->k entries, sorted by
+ * (score desc, pid asc).  trace may be NULL.  Synchronous. */
+plaid_status plaid_search(plaid_searcher* s, const float* q, uint64_t rows, uint64_t dim,
+                          const plaid_params* params, uint32_t* out_pids, float* out_scores,
+                          uint64_t* out_n, plaid_trace* trace);
+/* nq queries [nq][rows][dim]; outputs [nq][k] and out_n[nq]; traces[nq] or NULL. */
+plaid_status plaid_search_batch(plaid_searcher* s, const float* q, uint64_t nq, uint64_t rows,
+                                uint64_t dim, const plaid_params* params, uint32_t* out_pids,
+                                float* out_scores, uint64_t* out_n, plaid_trace* traces);
+/* Device-resident variant: d_q [nq][rows][dim] on the searcher's device,
+ * outputs d_pids/d_scores [nq][k], d_n [nq] on device, enqueued on `stream`
+ * (a cudaStream_t, 0 = the searcher's own stream) and NOT synchronised.
+ * Query norms are checked on the device; a failure is reported by the next
+ * plaid_searcher_sync().  Used by bench.py for the HBM-resident timing. */
+plaid_status plaid_search_device(plaid_searcher* s, const float* d_q, uint64_t nq, uint64_t rows,
+                                 uint64_t dim, const plaid_params* params, uint32_t* d_pids,
+                                 float* d_scores, uint64_t* d_n, uint64_t stream);
+plaid_status plaid_searcher_sync(plaid_searcher* s);
+/* Number of kernels the last search enqueued (for the bench's gpu_launches). */
+uint64_t plaid_searcher_last_launches(const plaid_searcher* s);
+
+/* Merge G per-shard top-k lists (score desc, pid asc) into the global top-k —
+ * the final select after the NCCL all-gather. Host arrays. */
+plaid_status plaid_merge_topk(plaid_searcher* s, const uint32_t* pids, const float* scores,
+                              const uint64_t* counts, uint64_t shards, uint64_t stride, uint64_t k,
+                              uint32_t* out_pids, float* out_scores, uint64_t* out_n);
+/* Same on device buffers, enqueued on stream (0 = searcher stream). */
+plaid_status plaid_merge_topk_device(plaid_searcher* s, const uint32_t* d_pids,
+                                     const float* d_scores, const uint64_t* d_counts,
+                                     uint64_t shards, uint64_t stride, uint64_t k, uint32_t* d_out_pids,
+                                     float* d_out_scores, uint64_t* d_out_n, uint64_t stream);
+
+/* ---- per-stage entry points (host buffers in/out, computed on the GPU) ------------ */
+/* pipeline.cpp:26-50: scores K x rows (centroid-major), row_max K */
+plaid_status plaid_compute_centroid_scores(plaid_searcher* s, const float* q, uint64_t rows,
+                                           uint64_t dim, float* scores, float* row_max);
+/* pipeline.cpp:52-87: scores K x rows from the host; out_ids sorted ascending (capacity N) */
+plaid_status plaid_generate_candidates(plaid_searcher* s, const float* scores, uint64_t rows,
+                                       uint64_t nprobe, uint32_t* out_ids, uint64_t* out_n);
+/* pipeline.cpp:89-95 */
+plaid_status plaid_prune_centroids(plaid_searcher* s, const float* row_max, uint64_t num_centroids,
+                                   float t_cs, uint8_t* keep);
+/* pipeline.cpp:97-137: mask may be NULL */
+plaid_status plaid_centroid_interaction(plaid_searcher* s, const float* scores, uint64_t rows,
+                                        const uint32_t* cand, uint64_t n, const uint8_t* mask,
+                                        float* out_scores, uint64_t* rows_gathered);
+/* pipeline.cpp:139-163 */
+plaid_status plaid_select_top(plaid_searcher* s, const uint32_t* ids, const float* scores,
+                              uint64_t n, uint64_t keep, uint32_t* out_ids, float* out_scores,
+                              uint64_t* out_n);
+/* pipeline.cpp:165-225 */
+plaid_status plaid_rank_final(plaid_searcher* s, const float* q, uint64_t rows,
+                              const uint32_t* cand, uint64_t n, uint64_t k, uint32_t* out_ids,
+                              float* out_scores, uint64_t* out_n);
+/* residual_codec.cpp:97-132 (uses the index's centroids and quantizer) */
+plaid_status plaid_reconstruct(plaid_searcher* s, const uint32_t* codes, uint64_t n,
+                               const uint8_t* residuals, float* out);
+/* residual_codec.cpp:42-59 / :86-95 */
+plaid_status plaid_lut_build(uint32_t nbits, uint8_t* table);
+plaid_status plaid_unpack_via_lut(plaid_searcher* s, const uint8_t* packed, uint64_t n,
+                                  uint32_t nbits, uint8_t* out);
+/* residual_codec.cpp:61-84 (host; index-build side, kept for round trips) */
+plaid_status plaid_pack_residual(const uint8_t* idx, uint64_t n, uint32_t nbits, uint8_t* out);
+/* maxsim.cpp:31-64 */
+plaid_status plaid_maxsim_packed(plaid_searcher* s, const float* scores, uint64_t nq,
+                                 const uint64_t* offsets, uint64_t np, float* out);
+/* maxsim.cpp:66-104 */
+plaid_status plaid_maxsim_embeddings(plaid_searcher* s, const float* q, uint64_t rows, uint64_t dim,
+                                     const float* emb, const uint64_t* offsets, uint64_t np,
+                                     float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLAID_H */

@@ -1,0 +1,399 @@
+"""Python mirror of the reference searcher's interface (namespace `lir`,
+/root/reference/proj/include/lir/*.hpp) over the C ABI of libplaid.so.
+
+Names, argument meaning and error behaviour follow the reference:
+`search` (pipeline.hpp:86-87), the per-stage functions (pipeline.hpp:55-90),
+the codec (residual_codec.hpp) and MaxSim kernels (maxsim.hpp).  Errors raise
+`PlaidError` whose `.code` is the lir::ErrorCode (error.hpp:8-26).  Every call
+runs on the GPU; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .hostindex import HostIndex
+
+
+class ErrorCode(enum.IntEnum):  # error.hpp:8-26 (+1 on the wire)
+    DimensionMismatch = 0
+    NotNormalized = 1
+    TooFewPoints = 2
+    PackingUnsupported = 3
+    EmptyCorpus = 4
+    IndexOutOfRange = 5
+    LengthNotPackable = 6
+    EmptyPassageRange = 7
+    InvalidParams = 8
+    ChecksumMismatch = 9
+    UnsupportedVersion = 10
+    InvariantViolation = 11
+    HeaderMismatch = 12
+    NormalizationError = 13
+    LengthMismatch = 14
+    UnknownQueryId = 15
+    IoError = 16
+    CudaError = 99
+    NcclError = 100
+    Unsupported = 101
+    OutOfMemory = 102
+
+
+class PlaidError(RuntimeError):
+    """lir::Error (error.hpp:51-61): carries an ErrorCode."""
+
+    def __init__(self, code: ErrorCode, message: str):
+        super().__init__(f"{code.name}: {message}")
+        self.code = code
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = N.load().plaid_last_error().decode(errors="replace")
+        raise PlaidError(ErrorCode(status - 1), msg)
+
+
+class ScoreMode(enum.IntEnum):
+    TENSOR = 0
+    EXACT = 1
+
+
+@dataclass
+class SearchParams:  # types.hpp:79-84
+    k: int = 10
+    nprobe: int = 1
+    t_cs: float = 0.5
+    ndocs: int = 256
+
+    def _c(self, disable_filter: bool = False) -> N.Params:
+        return N.Params(int(self.k), int(self.nprobe), float(self.t_cs), int(self.ndocs), int(bool(disable_filter)))
+
+
+@dataclass
+class SearchOptions:  # pipeline.hpp:45-48
+    threads: int = 0             # accepted for interface parity; the grid size is internal
+    disable_filter: bool = False
+
+
+@dataclass
+class CandidateSet:  # types.hpp:93-99
+    passage_ids: np.ndarray
+    scores: Optional[np.ndarray] = None
+
+    def __len__(self) -> int:
+        return int(self.passage_ids.shape[0])
+
+
+@dataclass
+class StageTrace:  # pipeline.hpp:23-43
+    stage1_candidates: int = 0
+    stage2_out: int = 0
+    stage3_out: int = 0
+    final_out: int = 0
+    candidate_generation_ms: float = 0.0
+    stage2_ms: float = 0.0
+    stage3_ms: float = 0.0
+    lookup_ms: float = 0.0
+    decompression_ms: float = 0.0
+    scoring_ms: float = 0.0
+    total_ms: float = 0.0
+    centroid_matmul_count: int = 0
+    stage2_rows_gathered: int = 0
+    stage3_rows_gathered: int = 0
+    decompressed_passages: int = 0
+
+    @classmethod
+    def _from_c(cls, t: N.Trace) -> "StageTrace":
+        return cls(**{f: getattr(t, f) for f, _ in N.Trace._fields_})
+
+    def filtering_ms(self) -> float:
+        return self.stage2_ms + self.stage3_ms
+
+    def counters(self) -> dict:
+        return {k: getattr(self, k) for k in (
+            "stage1_candidates", "stage2_out", "stage3_out", "final_out", "centroid_matmul_count",
+            "stage2_rows_gathered", "stage3_rows_gathered", "decompressed_passages")}
+
+
+@dataclass
+class SearchResult:  # pipeline.hpp:50-53
+    topk: CandidateSet
+    trace: StageTrace = field(default_factory=StageTrace)
+
+
+def default_params_for_k(k: int) -> SearchParams:  # types.cpp:74-86
+    p = N.Params()
+    N.load().plaid_default_params_for_k(int(k), C.byref(p))
+    return SearchParams(int(p.k), int(p.nprobe), float(p.t_cs), int(p.ndocs))
+
+
+def stage3_width(params: SearchParams) -> int:  # pipeline.cpp:227-230
+    return int(N.load().plaid_stage3_width(C.byref(params._c())))
+
+
+def validate_params(params: SearchParams, num_centroids: int) -> None:  # types.cpp:88-99
+    _check(N.load().plaid_validate_params(C.byref(params._c()), int(num_centroids)))
+
+
+def validate_query(q: np.ndarray, index_dim: int) -> None:  # types.cpp:61-72
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    rows, dim = (q.shape if q.ndim == 2 else (0, q.shape[-1] if q.ndim else 0))
+    _check(N.load().plaid_validate_query(N.ptr(q, C.c_float), rows, dim, int(index_dim)))
+
+
+def lut_build(nbits: int) -> np.ndarray:  # residual_codec.cpp:42-59
+    if nbits not in (1, 2, 4):
+        raise PlaidError(ErrorCode.PackingUnsupported, f"nbits {nbits} not in {{1,2,4}}")
+    t = np.zeros(256 * (8 // nbits), dtype=np.uint8)
+    _check(N.load().plaid_lut_build(nbits, N.ptr(t, C.c_uint8)))
+    return t.reshape(256, 8 // nbits)
+
+
+def pack_residual(bucket_indices: np.ndarray, nbits: int) -> np.ndarray:  # residual_codec.cpp:61-84
+    idx = np.ascontiguousarray(bucket_indices, dtype=np.uint8)
+    if nbits not in (1, 2, 4):
+        raise PlaidError(ErrorCode.PackingUnsupported, f"nbits {nbits} not in {{1,2,4}}")
+    out = np.zeros(max(1, idx.size * nbits // 8), dtype=np.uint8)
+    _check(N.load().plaid_pack_residual(N.ptr(idx, C.c_uint8), idx.size, nbits, N.ptr(out, C.c_uint8)))
+    return out[: idx.size * nbits // 8]
+
+
+def _desc(h: HostIndex) -> N.IndexDesc:
+    return N.IndexDesc(h.dim, h.nbits, h.num_centroids, h.num_passages, h.num_embeddings,
+                       N.ptr(h.centroids, C.c_float), N.ptr(h.codes, C.c_uint32),
+                       N.ptr(h.residuals, C.c_uint8), N.ptr(h.doclens, C.c_uint32),
+                       N.ptr(h.ivf_offsets, C.c_uint64), N.ptr(h.ivf_postings, C.c_uint32),
+                       N.ptr(h.bucket_cutoffs, C.c_float), N.ptr(h.bucket_weights, C.c_float))
+
+
+class DeviceIndex:
+    """The compressed index resident in HBM (index.hpp:60-85).  Immutable and
+    shareable between searchers (index.hpp:57-59)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        info = (C.c_uint64 * 8)()
+        N.load().plaid_index_info(self._h, info)
+        (self.dim, self.nbits, self.num_centroids, self.num_passages, self.num_embeddings,
+         self.num_postings, self.pid_base, self.device_bytes) = (int(x) for x in info)
+
+    @classmethod
+    def from_host(cls, h: HostIndex, device: int = 0, validate: bool = False) -> "DeviceIndex":
+        out = C.c_void_p()
+        d = _desc(h)
+        _check(N.load().plaid_index_from_host(C.byref(d), device, int(validate), C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def shard(cls, h: HostIndex, pid_begin: int, pid_end: int, device: int = 0) -> "DeviceIndex":
+        out = C.c_void_p()
+        d = _desc(h)
+        _check(N.load().plaid_index_from_host_shard(C.byref(d), pid_begin, pid_end, device, C.byref(out)))
+        return cls(out.value)
+
+    def validate(self) -> None:  # index.cpp:12-84
+        _check(N.load().plaid_index_validate(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            N.load().plaid_index_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Searcher:
+    """One CUDA stream + device scratch; use one per host thread."""
+
+    def __init__(self, index: Optional[DeviceIndex] = None, device: int = 0,
+                 score_mode: ScoreMode = ScoreMode.EXACT, record_times: bool = True,
+                 use_graphs: bool = False):
+        self.index = index
+        cfg = N.SearcherConfig(int(score_mode), int(record_times), int(use_graphs), 0)
+        out = C.c_void_p()
+        _check(N.load().plaid_searcher_create(index._h if index else None, device, C.byref(cfg), C.byref(out)))
+        self._h = out
+
+    def close(self) -> None:
+        if self._h:
+            N.load().plaid_searcher_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- lir::search
+    def search(self, q: np.ndarray, params: SearchParams, options: SearchOptions = SearchOptions()) -> SearchResult:
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        if q.ndim != 2:
+            raise PlaidError(ErrorCode.DimensionMismatch, "query must be rows x dim")
+        k = max(int(params.k), 1)
+        ids = np.zeros(k, dtype=np.uint32)
+        sc = np.zeros(k, dtype=np.float32)
+        n = C.c_uint64()
+        tr = N.Trace()
+        p = params._c(options.disable_filter)
+        _check(N.load().plaid_search(self._h, N.ptr(q, C.c_float), q.shape[0], q.shape[1], C.byref(p),
+                                     N.ptr(ids, C.c_uint32), N.ptr(sc, C.c_float), C.byref(n), C.byref(tr)))
+        return SearchResult(CandidateSet(ids[: n.value].copy(), sc[: n.value].copy()), StageTrace._from_c(tr))
+
+    def search_batch(self, q: np.ndarray, params: SearchParams, options: SearchOptions = SearchOptions()):
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        nq, rows, dim = q.shape
+        k = int(params.k)
+        ids = np.zeros((nq, k), dtype=np.uint32)
+        sc = np.zeros((nq, k), dtype=np.float32)
+        n = np.zeros(nq, dtype=np.uint64)
+        p = params._c(options.disable_filter)
+        _check(N.load().plaid_search_batch(self._h, N.ptr(q, C.c_float), nq, rows, dim, C.byref(p),
+                                           N.ptr(ids, C.c_uint32), N.ptr(sc, C.c_float), N.ptr(n, C.c_uint64),
+                                           None))
+        return ids, sc, n
+
+    def search_device(self, d_q: int, nq: int, rows: int, dim: int, params: SearchParams,
+                      d_pids: int, d_scores: int, d_n: int, stream: int = 0,
+                      options: SearchOptions = SearchOptions()) -> None:
+        p = params._c(options.disable_filter)
+        _check(N.load().plaid_search_device(self._h, d_q, nq, rows, dim, C.byref(p), d_pids, d_scores, d_n,
+                                            stream))
+
+    def sync(self) -> None:
+        _check(N.load().plaid_searcher_sync(self._h))
+
+    def last_launches(self) -> int:
+        return int(N.load().plaid_searcher_last_launches(self._h))
+
+    # ---- per-stage functions (pipeline.hpp:55-90)
+    def compute_centroid_scores(self, q: np.ndarray):
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        K = self.index.num_centroids
+        S = np.zeros((K, q.shape[0]), dtype=np.float32)
+        mx = np.zeros(K, dtype=np.float32)
+        _check(N.load().plaid_compute_centroid_scores(self._h, N.ptr(q, C.c_float), q.shape[0], q.shape[1],
+                                                      N.ptr(S, C.c_float), N.ptr(mx, C.c_float)))
+        return S, mx
+
+    def generate_candidates(self, scores: np.ndarray, nprobe: int) -> np.ndarray:
+        S = np.ascontiguousarray(scores, dtype=np.float32)
+        out = np.zeros(max(self.index.num_passages, 1), dtype=np.uint32)
+        n = C.c_uint64()
+        _check(N.load().plaid_generate_candidates(self._h, N.ptr(S, C.c_float), S.shape[1], int(nprobe),
+                                                  N.ptr(out, C.c_uint32), C.byref(n)))
+        return out[: n.value].copy()
+
+    def prune_centroids(self, row_max: np.ndarray, t_cs: float) -> np.ndarray:
+        mx = np.ascontiguousarray(row_max, dtype=np.float32)
+        keep = np.zeros(mx.size, dtype=np.uint8)
+        _check(N.load().plaid_prune_centroids(self._h, N.ptr(mx, C.c_float), mx.size, float(t_cs),
+                                              N.ptr(keep, C.c_uint8)))
+        return keep
+
+    def centroid_interaction(self, candidates: np.ndarray, scores: np.ndarray, mask: Optional[np.ndarray]):
+        cand = np.ascontiguousarray(candidates, dtype=np.uint32)
+        S = np.ascontiguousarray(scores, dtype=np.float32)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        out = np.zeros(max(cand.size, 1), dtype=np.float32)
+        rows = C.c_uint64()
+        _check(N.load().plaid_centroid_interaction(self._h, N.ptr(S, C.c_float), S.shape[1],
+                                                   N.ptr(cand, C.c_uint32), cand.size, N.ptr(m, C.c_uint8),
+                                                   N.ptr(out, C.c_float), C.byref(rows)))
+        return out[: cand.size].copy(), int(rows.value)
+
+    def select_top(self, ids: np.ndarray, scores: np.ndarray, n: int):
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        sc = np.ascontiguousarray(scores, dtype=np.float32)
+        m = max(min(int(n), ids.size), 1)
+        oi = np.zeros(m, dtype=np.uint32)
+        os_ = np.zeros(m, dtype=np.float32)
+        cnt = C.c_uint64()
+        _check(N.load().plaid_select_top(self._h, N.ptr(ids, C.c_uint32), N.ptr(sc, C.c_float), ids.size, int(n),
+                                         N.ptr(oi, C.c_uint32), N.ptr(os_, C.c_float), C.byref(cnt)))
+        return oi[: cnt.value].copy(), os_[: cnt.value].copy()
+
+    def rank_final(self, candidates: np.ndarray, q: np.ndarray, k: int):
+        cand = np.ascontiguousarray(candidates, dtype=np.uint32)
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        m = max(min(int(k), cand.size), 1)
+        oi = np.zeros(m, dtype=np.uint32)
+        os_ = np.zeros(m, dtype=np.float32)
+        cnt = C.c_uint64()
+        _check(N.load().plaid_rank_final(self._h, N.ptr(q, C.c_float), q.shape[0], N.ptr(cand, C.c_uint32),
+                                         cand.size, int(k), N.ptr(oi, C.c_uint32), N.ptr(os_, C.c_float),
+                                         C.byref(cnt)))
+        return oi[: cnt.value].copy(), os_[: cnt.value].copy()
+
+    # ---- codec / MaxSim
+    def reconstruct(self, codes: np.ndarray, residuals: np.ndarray) -> np.ndarray:
+        codes = np.ascontiguousarray(codes, dtype=np.uint32)
+        res = np.ascontiguousarray(residuals, dtype=np.uint8).reshape(-1)
+        out = np.zeros((codes.size, self.index.dim), dtype=np.float32)
+        _check(N.load().plaid_reconstruct(self._h, N.ptr(codes, C.c_uint32), codes.size, N.ptr(res, C.c_uint8),
+                                          N.ptr(out, C.c_float)))
+        return out
+
+    def unpack_via_lut(self, packed: np.ndarray, nbits: int) -> np.ndarray:
+        pk = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1)
+        if nbits not in (1, 2, 4):
+            raise PlaidError(ErrorCode.PackingUnsupported, f"nbits {nbits} not in {{1,2,4}}")
+        out = np.zeros(max(pk.size * (8 // nbits), 1), dtype=np.uint8)
+        _check(N.load().plaid_unpack_via_lut(self._h, N.ptr(pk, C.c_uint8), pk.size, nbits, N.ptr(out, C.c_uint8)))
+        return out[: pk.size * (8 // nbits)]
+
+    def maxsim_packed(self, scores: np.ndarray, offsets: np.ndarray) -> np.ndarray:
+        S = np.ascontiguousarray(scores, dtype=np.float32)
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        np_ = max(off.size - 1, 0)
+        if off.size == 0:
+            raise PlaidError(ErrorCode.InvalidParams, "offsets must start at 0")
+        out = np.zeros(max(np_, 1), dtype=np.float32)
+        nq = S.shape[1] if S.ndim == 2 else 0
+        _check(N.load().plaid_maxsim_packed(self._h, N.ptr(S, C.c_float), nq, N.ptr(off, C.c_uint64), np_,
+                                            N.ptr(out, C.c_float)))
+        return out[:np_]
+
+    def maxsim_embeddings(self, q: np.ndarray, emb: np.ndarray, offsets: np.ndarray) -> np.ndarray:
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        e = np.ascontiguousarray(emb, dtype=np.float32)
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        if off.size == 0:
+            raise PlaidError(ErrorCode.InvalidParams, "offsets must start at 0")
+        np_ = off.size - 1
+        out = np.zeros(max(np_, 1), dtype=np.float32)
+        _check(N.load().plaid_maxsim_embeddings(self._h, N.ptr(q, C.c_float), q.shape[0], q.shape[1],
+                                                N.ptr(e, C.c_float), N.ptr(off, C.c_uint64), np_,
+                                                N.ptr(out, C.c_float)))
+        return out[:np_]
+
+    def merge_topk(self, pids: np.ndarray, scores: np.ndarray, counts: np.ndarray, k: int):
+        """Final select over G shard lists [G, stride]."""
+        pids = np.ascontiguousarray(pids, dtype=np.uint32)
+        sc = np.ascontiguousarray(scores, dtype=np.float32)
+        cnt = np.ascontiguousarray(counts, dtype=np.uint64)
+        G, stride = pids.shape
+        oi = np.zeros(k, dtype=np.uint32)
+        os_ = np.zeros(k, dtype=np.float32)
+        n = C.c_uint64()
+        _check(N.load().plaid_merge_topk(self._h, N.ptr(pids, C.c_uint32), N.ptr(sc, C.c_float),
+                                         N.ptr(cnt, C.c_uint64), G, stride, k, N.ptr(oi, C.c_uint32),
+                                         N.ptr(os_, C.c_float), C.byref(n)))
+        return oi[: n.value].copy(), os_[: n.value].copy()
+
+
+def search(index: DeviceIndex, q: np.ndarray, params: SearchParams,
+           options: SearchOptions = SearchOptions(), searcher: Optional[Searcher] = None) -> SearchResult:
+    """lir::search (pipeline.hpp:86-87).  Creates a throwaway Searcher unless
+    one is given; reuse a Searcher for repeated queries."""
+    s = searcher or Searcher(index)
+    return s.search(q, params, options)

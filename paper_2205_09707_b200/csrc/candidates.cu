@@ -1,0 +1,135 @@
+// candidates.cu — stage-1 candidate generation (pipeline.cpp:52-87).
+//
+// The union of the probed centroids' postings is formed in an N-bit bitmap
+// (atomicOr per posting; duplicates across query tokens collapse for free),
+// then compacted into ascending passage ids.  Scanning the bitmap in order is
+// exactly the reference's `std::sort` of the unique ids (pipeline.cpp:83), so
+// the output is bit-identical.  Two launches: per-chunk popcounts, then each
+// chunk re-derives its base from the preceding chunk counts and writes its ids.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace plaid {
+namespace {
+
+constexpr uint32_t kChunkWords = 2048;  // 65536 passages per chunk
+constexpr uint32_t kThreads = 256;
+constexpr uint32_t kWordsPerThread = kChunkWords / kThreads;
+
+__global__ void postings_bitmap_kernel(const uint64_t* __restrict__ ivf_offsets,
+                                       const uint32_t* __restrict__ postings,
+                                       const uint32_t* __restrict__ sel,
+                                       uint32_t* __restrict__ bitmap) {
+    const uint32_t c = sel[blockIdx.x];
+    const uint64_t b = ivf_offsets[c], e = ivf_offsets[c + 1];
+    for (uint64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
+        const uint32_t p = postings[j];
+        atomicOr(bitmap + (p >> 5), 1u << (p & 31));
+    }
+}
+
+__device__ __forceinline__ uint32_t masked_word(const uint32_t* bitmap, uint64_t w, uint64_t N) {
+    const uint64_t words = (N + 31) / 32;
+    if (w >= words) return 0;
+    uint32_t v = bitmap[w];
+    if (w == words - 1 && (N & 31)) v &= (1u << (N & 31)) - 1;
+    return v;
+}
+
+__global__ void chunk_count_kernel(const uint32_t* __restrict__ bitmap, uint64_t N,
+                                   uint32_t* __restrict__ counts) {
+    __shared__ uint32_t warp_sums[kThreads / 32];
+    const uint64_t w0 = uint64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
+    uint32_t n = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kWordsPerThread; ++j) n += __popc(masked_word(bitmap, w0 + j, N));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (uint32_t k = 0; k < kThreads / 32; ++k) t += warp_sums[k];
+        counts[blockIdx.x] = t;
+    }
+}
+
+__global__ void chunk_write_kernel(const uint32_t* __restrict__ bitmap, uint64_t N,
+                                   const uint32_t* __restrict__ counts, uint32_t* __restrict__ out,
+                                   uint64_t* __restrict__ out_n) {
+    __shared__ uint64_t red[kThreads / 32];
+    __shared__ uint32_t scan[kThreads / 32];
+    // base = sum of counts of the chunks before this one
+    uint64_t part = 0;
+    for (uint32_t c = threadIdx.x; c < blockIdx.x; c += kThreads) part += counts[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+
+    const uint64_t w0 = uint64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
+    uint32_t words[kWordsPerThread];
+    uint32_t mine = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kWordsPerThread; ++j) {
+        words[j] = masked_word(bitmap, w0 + j, N);
+        mine += __popc(words[j]);
+    }
+    // block exclusive scan of `mine`
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += v;
+    }
+    if (lane == 31) scan[warp] = incl;
+    __syncthreads();
+    uint64_t base = 0;
+    for (uint32_t k = 0; k < kThreads / 32; ++k) base += red[k];
+    uint32_t before = 0;
+    for (uint32_t k = 0; k < warp; ++k) before += scan[k];
+    uint64_t pos = base + before + incl - mine;
+#pragma unroll
+    for (uint32_t j = 0; j < kWordsPerThread; ++j) {
+        uint32_t v = words[j];
+        while (v) {
+            const uint32_t b = __ffs(v) - 1;
+            v &= v - 1;
+            out[pos++] = uint32_t((w0 + j) * 32 + b);
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kThreads - 1) *out_n = pos;
+}
+
+}  // namespace
+
+namespace launch {
+
+void postings_to_bitmap(const IndexView& ix, const uint32_t* d_sel, uint32_t nsel,
+                        uint32_t* d_bitmap, cudaStream_t st) {
+    if (nsel == 0) return;
+    postings_bitmap_kernel<<<nsel, 256, 0, st>>>(ix.ivf_offsets, ix.ivf_postings, d_sel, d_bitmap);
+    count_launch();
+}
+
+uint32_t bitmap_chunks(uint64_t N) {
+    const uint64_t words = (N + 31) / 32;
+    uint64_t c = (words + kChunkWords - 1) / kChunkWords;
+    return uint32_t(c ? c : 1);
+}
+
+void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_counts,
+                    uint32_t* d_out_ids, uint64_t* d_out_n, cudaStream_t st) {
+    const uint32_t chunks = bitmap_chunks(N);
+    chunk_count_kernel<<<chunks, kThreads, 0, st>>>(d_bitmap, N, d_chunk_counts);
+    chunk_write_kernel<<<chunks, kThreads, 0, st>>>(d_bitmap, N, d_chunk_counts, d_out_ids, d_out_n);
+    count_launch();
+    count_launch();
+}
+
+}  // namespace launch
+}  // namespace plaid

@@ -1,0 +1,77 @@
+// device.cuh — device-side helpers shared by the PLAID kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace plaid {
+namespace dev {
+
+constexpr int kWarp = 32;
+constexpr int kMaxRows = 32;  // |Q| <= 32: one query token per lane
+
+// Orderable 32-bit image of an fp32 score: a > b (as floats) <=> ord(a) > ord(b).
+// -0.0 is canonicalised to +0.0 first because the reference compares scores
+// with `!=` / `>` (pipeline.cpp:147-150), for which the two zeros are equal.
+__host__ __device__ __forceinline__ uint32_t ord_f32(float f) {
+#ifdef __CUDA_ARCH__
+    uint32_t u = __float_as_uint(f);
+#else
+    uint32_t u;
+    __builtin_memcpy(&u, &f, 4);
+#endif
+    if (u == 0x80000000u) u = 0u;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__host__ __device__ __forceinline__ float unord_f32(uint32_t o) {
+    uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(u);
+#else
+    float f;
+    __builtin_memcpy(&f, &u, 4);
+    return f;
+#endif
+}
+
+// 64-bit selection key: larger key = better under (score desc, id asc), the
+// total order of select_top (pipeline.cpp:147-150) and of the per-token
+// centroid ranking (pipeline.cpp:67-72).  Keys are unique for unique ids.
+__host__ __device__ __forceinline__ uint64_t make_key(float score, uint32_t id) {
+    return (uint64_t(ord_f32(score)) << 32) | uint64_t(~id);
+}
+__host__ __device__ __forceinline__ uint32_t key_id(uint64_t key) { return ~uint32_t(key); }
+__host__ __device__ __forceinline__ float key_score(uint64_t key) { return unord_f32(uint32_t(key >> 32)); }
+
+// In-order fp32 multiply-then-add, never contracted into an FMA: the
+// reference's `acc += a[i] * b[i]` (types.hpp:18-22).
+__device__ __forceinline__ float madd_rn(float acc, float a, float b) {
+    return __fadd_rn(acc, __fmul_rn(a, b));
+}
+
+// `if (s > acc) acc = s` (pipeline.cpp:122, maxsim.cpp:95).
+__device__ __forceinline__ float max_gt(float acc, float s) { return s > acc ? s : acc; }
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max_gt(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Branchless insertion of x into a descending list k[0..NP) of unique keys.
+template <int NP>
+__device__ __forceinline__ void topn_insert(uint64_t (&k)[NP], uint64_t x) {
+    if (x <= k[NP - 1]) return;
+#pragma unroll
+    for (int j = NP - 1; j > 0; --j) {
+        uint64_t lo = x < k[j - 1] ? x : k[j - 1];
+        k[j] = k[j] > lo ? k[j] : lo;
+    }
+    k[0] = k[0] > x ? k[0] : x;
+}
+
+}  // namespace dev
+}  // namespace plaid

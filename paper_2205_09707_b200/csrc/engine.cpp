@@ -1,0 +1,846 @@
+// engine.cpp — DeviceIndex / Searcher: the host orchestration of lir::search
+// (pipeline.cpp:232-283) over the sm_100a kernels in kernels.cuh.
+#include "engine.hpp"
+
+#include "device.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+namespace plaid {
+
+// ---------------------------------------------------------------- launch counter
+namespace launch {
+namespace {
+thread_local uint64_t g_launches = 0;
+}
+uint64_t launches() { return g_launches; }
+void reset_launches() { g_launches = 0; }
+void count_launch() { ++g_launches; }
+}  // namespace launch
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        fail(PLAID_OUT_OF_MEMORY, std::string("CUDA out of memory in ") + what);
+    }
+    fail(PLAID_CUDA_ERROR, std::string(cudaGetErrorString(e)) + " in " + what);
+}
+
+namespace {
+
+bool nbits_supported(uint32_t b) { return b == 1 || b == 2 || b == 4; }
+
+uint32_t np_bucket(uint64_t nprobe) {
+    uint32_t b = 1;
+    while (b < nprobe) b <<= 1;
+    return b;
+}
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) PLAID_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Counter slots in Searcher::counters_.
+enum : int {
+    kN1 = 0,        // stage1_candidates
+    kN2 = 1,        // stage2_out
+    kN3 = 2,        // stage3_out
+    kNOut = 3,      // final_out
+    kRows2 = 4,     // stage2_rows_gathered
+    kRows3 = 5,     // stage3_rows_gathered
+    kNFin = 6,      // decompressed_passages
+    kKConst = 7,    // K (for generic selects)
+    kTmpN = 8,      // scratch count
+    kEntryN = 9,    // entry-point input count
+    kNumCounters = 16
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------- validation
+// types.cpp:61-72 (check_unit_rows types.cpp:10-19, tolerance types.hpp:16)
+void validate_query_host(const float* q, uint64_t rows, uint64_t dim, uint64_t index_dim) {
+    if (rows == 0) fail(PLAID_INVALID_PARAMS, "query must contain at least one token");
+    if (dim != index_dim)
+        fail(PLAID_DIMENSION_MISMATCH, "query dim " + std::to_string(dim) +
+                                           " does not match index dim " + std::to_string(index_dim));
+    const double tol = double(1e-3f);
+    for (uint64_t r = 0; r < rows; ++r) {
+        double acc = 0.0;
+        for (uint64_t d = 0; d < dim; ++d) acc += double(q[r * dim + d]) * double(q[r * dim + d]);
+        const double norm = std::sqrt(acc);
+        if (std::fabs(norm - 1.0) > tol)
+            fail(PLAID_NOT_NORMALIZED, "query row " + std::to_string(r) + " has L2 norm " + std::to_string(norm));
+    }
+}
+
+// types.cpp:88-99
+void validate_params_host(const plaid_params& p, uint64_t num_centroids) {
+    if (p.k < 1) fail(PLAID_INVALID_PARAMS, "k must be >= 1");
+    if (p.nprobe < 1 || p.nprobe > num_centroids)
+        fail(PLAID_INVALID_PARAMS, "nprobe " + std::to_string(p.nprobe) + " outside [1, " +
+                                       std::to_string(num_centroids) + "]");
+    if (p.ndocs < p.k) fail(PLAID_INVALID_PARAMS, "ndocs must be >= k");
+    if (!(p.t_cs >= -1.0f && p.t_cs <= 1.0f)) fail(PLAID_INVALID_PARAMS, "t_cs must lie in [-1, 1]");
+}
+
+// types.cpp:74-86
+void default_params_for_k(uint64_t k, plaid_params* out) {
+    out->k = k;
+    out->disable_filter = 0;
+    if (k <= 10) {
+        out->nprobe = 1; out->t_cs = 0.5f; out->ndocs = 256;
+    } else if (k <= 100) {
+        out->nprobe = 2; out->t_cs = 0.45f; out->ndocs = 1024;
+    } else {
+        out->nprobe = 4; out->t_cs = 0.4f; out->ndocs = 4096;
+    }
+    if (out->ndocs < k) out->ndocs = k;
+}
+
+// pipeline.cpp:227-230
+uint64_t stage3_width(const plaid_params& p) { return std::max<uint64_t>((p.ndocs + 3) / 4, p.k); }
+
+// index.cpp:12-84 (+ validate_centroids types.cpp:50-59, validate_quantizer
+// residual_codec.cpp:15-40), on the host arrays before upload.
+void validate_index_host(const plaid_index_desc& d) {
+    auto bad = [](const std::string& m) { fail(PLAID_INVARIANT_VIOLATION, m); };
+    if (!nbits_supported(d.nbits)) bad("nbits must be one of {1,2,4}");
+    if (d.dim == 0 || d.dim % (8 / d.nbits) != 0) bad("dim must be positive and divisible by 8/nbits");
+    const uint64_t K = d.num_centroids;
+    if (K == 0) bad("index must contain at least one centroid");
+    const double tol = double(1e-3f);
+    for (uint64_t c = 0; c < K; ++c) {
+        double acc = 0;
+        for (uint32_t j = 0; j < d.dim; ++j) acc += double(d.centroids[c * d.dim + j]) * double(d.centroids[c * d.dim + j]);
+        if (std::fabs(std::sqrt(acc) - 1.0) > tol) fail(PLAID_NOT_NORMALIZED, "centroid row " + std::to_string(c) + " not unit norm");
+    }
+    if (d.num_passages == 0) bad("index must contain at least one passage");
+    uint64_t total = 0;
+    for (uint64_t p = 0; p < d.num_passages; ++p) total += d.doclens[p];
+    if (d.num_embeddings != total) bad("codes length must equal the doclens total");
+    for (uint64_t t = 0; t < total; ++t)
+        if (d.codes[t] >= K) bad("token code " + std::to_string(t) + " out of centroid range");
+    const uint64_t nb = uint64_t(1) << d.nbits;
+    for (uint64_t i = 1; i + 1 < nb; ++i)
+        if (d.bucket_cutoffs[i] < d.bucket_cutoffs[i - 1]) bad("quantizer cutoffs not ascending");
+    for (uint64_t i = 0; i < nb; ++i) {
+        const float lo = i == 0 ? -INFINITY : d.bucket_cutoffs[i - 1];
+        const float hi = i + 1 == nb ? INFINITY : d.bucket_cutoffs[i];
+        const float w = d.bucket_weights[i];
+        if (!(w >= lo && w <= hi)) bad("quantizer weight " + std::to_string(i) + " outside its bucket interval");
+    }
+    if (d.ivf_offsets[0] != 0) bad("inverted list offsets must start at 0");
+    for (uint64_t c = 0; c < K; ++c) {
+        if (d.ivf_offsets[c + 1] < d.ivf_offsets[c]) bad("inverted list offsets must be monotone");
+        for (uint64_t j = d.ivf_offsets[c]; j < d.ivf_offsets[c + 1]; ++j) {
+            if (d.ivf_postings[j] >= d.num_passages) bad("posting references unknown passage");
+            if (j > d.ivf_offsets[c] && d.ivf_postings[j] <= d.ivf_postings[j - 1])
+                bad("postings must be strictly increasing within a centroid");
+        }
+    }
+    // content check: passage p listed under centroid c iff some token of p has code c
+    std::vector<uint64_t> cursor(d.ivf_offsets, d.ivf_offsets + K);
+    std::vector<uint32_t> seen(K, UINT32_MAX);
+    uint64_t t = 0;
+    for (uint64_t p = 0; p < d.num_passages; ++p)
+        for (uint32_t j = 0; j < d.doclens[p]; ++j, ++t) {
+            const uint32_t c = d.codes[t];
+            if (seen[c] == p) continue;
+            seen[c] = uint32_t(p);
+            if (cursor[c] >= d.ivf_offsets[c + 1] || d.ivf_postings[cursor[c]] != p)
+                bad("inverted list does not match token codes");
+            ++cursor[c];
+        }
+    for (uint64_t c = 0; c < K; ++c)
+        if (cursor[c] != d.ivf_offsets[c + 1]) bad("inverted list contains postings with no matching token code");
+}
+
+// ---------------------------------------------------------------- DevBuf
+template <typename T>
+void DevBuf<T>::ensure(uint64_t count) {
+    if (count <= n && p) return;
+    release();
+    const uint64_t c = count ? count : 1;
+    PLAID_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), c * sizeof(T)));
+    n = c;
+}
+template <typename T>
+void DevBuf<T>::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+}
+template struct DevBuf<float>;
+template struct DevBuf<uint32_t>;
+template struct DevBuf<uint64_t>;
+template struct DevBuf<unsigned char>;
+template struct DevBuf<SelectState>;
+template struct DevBuf<int>;
+
+// ---------------------------------------------------------------- DeviceIndex
+template <typename T>
+T* DeviceIndex::upload(const T* src, uint64_t count) {
+    void* p = nullptr;
+    const uint64_t bytes = std::max<uint64_t>(count, 1) * sizeof(T);
+    PLAID_CUDA(cudaMalloc(&p, bytes));
+    allocs_.push_back(p);
+    bytes_ += bytes;
+    if (count) PLAID_CUDA(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return static_cast<T*>(p);
+}
+
+DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_base)
+    : device_(device), pid_base_(pid_base) {
+    if (!nbits_supported(d.nbits)) fail(PLAID_PACKING_UNSUPPORTED, "nbits must be one of {1,2,4}");
+    if (d.dim == 0 || d.dim % 4 != 0 || d.dim > 256)
+        fail(PLAID_UNSUPPORTED, "engine supports dim in {4, 8, ..., 256}");
+    if (d.num_centroids == 0 || d.num_centroids > 0xFFFFFFFFull)
+        fail(PLAID_INVALID_PARAMS, "centroid count must be in [1, 2^32)");
+    if (d.num_passages > 0xFFFFFFFFull) fail(PLAID_INVALID_PARAMS, "corpora above 2^32 passages are not supported");
+    DeviceGuard g(device);
+    view_.dim = d.dim;
+    view_.nbits = d.nbits;
+    view_.K = d.num_centroids;
+    view_.N = d.num_passages;
+    view_.T = d.num_embeddings;
+    view_.P = d.ivf_offsets[d.num_centroids];
+    h_doclens_.assign(d.doclens, d.doclens + d.num_passages);
+    std::vector<uint64_t> offsets(d.num_passages + 1, 0);
+    for (uint64_t p = 0; p < d.num_passages; ++p) {
+        offsets[p + 1] = offsets[p] + d.doclens[p];
+        max_doclen_ = std::max(max_doclen_, d.doclens[p]);
+    }
+    if (offsets.back() != d.num_embeddings) fail(PLAID_LENGTH_MISMATCH, "doclens total does not match codes length");
+    const uint64_t nb = uint64_t(1) << d.nbits;
+    for (uint64_t i = 0; i < nb; ++i) view_.weights[i] = d.bucket_weights[i];
+    for (uint64_t i = 0; i + 1 < nb; ++i) cutoffs_[i] = d.bucket_cutoffs[i];
+    try {
+        view_.centroids = upload(d.centroids, d.num_centroids * d.dim);
+        view_.codes = upload(d.codes, d.num_embeddings);
+        view_.residuals = upload(d.residuals, d.num_embeddings * (uint64_t(d.nbits) * d.dim / 8));
+        view_.doclens = upload(d.doclens, d.num_passages);
+        view_.offsets = upload(offsets.data(), offsets.size());
+        view_.ivf_offsets = upload(d.ivf_offsets, d.num_centroids + 1);
+        view_.ivf_postings = upload(d.ivf_postings, view_.P);
+    } catch (...) {
+        for (void* p : allocs_) cudaFree(p);
+        allocs_.clear();
+        throw;
+    }
+}
+
+void DeviceIndex::validate_device() {
+    DeviceGuard g(device_);
+    const IndexView& v = view_;
+    std::vector<float> C(v.K * v.dim);
+    std::vector<uint32_t> codes(v.T), post(v.P);
+    std::vector<uint8_t> res(v.T * (uint64_t(v.nbits) * v.dim / 8));
+    std::vector<uint64_t> ivo(v.K + 1);
+    PLAID_CUDA(cudaMemcpy(C.data(), v.centroids, C.size() * 4, cudaMemcpyDeviceToHost));
+    PLAID_CUDA(cudaMemcpy(codes.data(), v.codes, codes.size() * 4, cudaMemcpyDeviceToHost));
+    PLAID_CUDA(cudaMemcpy(post.data(), v.ivf_postings, post.size() * 4, cudaMemcpyDeviceToHost));
+    PLAID_CUDA(cudaMemcpy(ivo.data(), v.ivf_offsets, ivo.size() * 8, cudaMemcpyDeviceToHost));
+    plaid_index_desc d{};
+    d.dim = v.dim;
+    d.nbits = v.nbits;
+    d.num_centroids = v.K;
+    d.num_passages = v.N;
+    d.num_embeddings = v.T;
+    d.centroids = C.data();
+    d.codes = codes.data();
+    d.residuals = res.data();
+    d.doclens = h_doclens_.data();
+    d.ivf_offsets = ivo.data();
+    d.ivf_postings = post.data();
+    d.bucket_cutoffs = cutoffs_;
+    d.bucket_weights = v.weights;
+    validate_index_host(d);
+}
+
+DeviceIndex::~DeviceIndex() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device_);
+    for (void* p : allocs_) cudaFree(p);
+    cudaSetDevice(prev);
+}
+
+// ---------------------------------------------------------------- Searcher
+Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& cfg)
+    : index_(index), device_(index ? index->device() : device), cfg_(cfg) {
+    DeviceGuard g(device_);
+    PLAID_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    for (auto& e : ev_) PLAID_CUDA(cudaEventCreate(&e));
+    counters_.ensure(kNumCounters);
+    PLAID_CUDA(cudaMemset(counters_.p, 0, kNumCounters * sizeof(uint64_t)));
+    status_.ensure(1);
+    PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
+    sel_state_.ensure(1);
+    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_q_), 32 * 256 * sizeof(float)));
+    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_counters_), kNumCounters * sizeof(uint64_t)));
+    q_.ensure(32 * 256);
+    if (index_) {
+        const IndexView& ix = index_->view();
+        scores_.ensure(ix.K * kScoresPitch);
+        rowmax_.ensure(ix.K);
+        keep_.ensure((ix.K + 31) / 32);
+        npartial_warps_ = launch::scores_max_warps();
+        partial_.ensure(npartial_warps_ * 32 * 32);
+        bitmap_.ensure((ix.N + 31) / 32);
+        chunk_counts_.ensure(launch::bitmap_chunks(ix.N));
+        c1_.ensure(ix.N);
+        keys2_.ensure(ix.N);
+        keys4_.ensure(ix.N);
+        const uint64_t K = ix.K;
+        PLAID_CUDA(cudaMemcpy(counters_.p + kKConst, &K, sizeof K, cudaMemcpyHostToDevice));
+    }
+}
+
+Searcher::~Searcher() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (h_q_) cudaFreeHost(h_q_);
+    if (h_counters_) cudaFreeHost(h_counters_);
+    if (h_pids_) cudaFreeHost(h_pids_);
+    if (h_scores_) cudaFreeHost(h_scores_);
+    if (stream_) cudaStreamDestroy(stream_);
+    cudaSetDevice(prev);
+}
+
+void Searcher::require_index() const {
+    if (!index_) fail(PLAID_INVALID_PARAMS, "searcher has no index");
+}
+
+void Searcher::ensure_param_buffers(const plaid_params& p) {
+    const IndexView& ix = index_->view();
+    const uint64_t K = ix.K, N = ix.N;
+    const uint64_t nsel = p.nprobe == K ? K : 32 * std::max<uint64_t>(p.nprobe, 32);
+    sel_.ensure(nsel);
+    if (p.nprobe > 32 && p.nprobe < K) tok_keys_.ensure(K);
+    const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
+    const uint64_t n3 = std::min<uint64_t>(stage3_width(p), N);
+    sel2_.ensure(nd);
+    keys3_.ensure(nd);
+    sel3_.ensure(n3);
+    tmp_keys_.ensure(std::max<uint64_t>(std::min<uint64_t>(p.k, N), std::min<uint64_t>(p.nprobe, K)));
+    out_pids_.ensure(p.k);
+    out_scores_.ensure(p.k);
+    uint64_t tmp = 0;
+    tmp = std::max(tmp, launch::sort_tmp_capacity(nd));
+    tmp = std::max(tmp, launch::sort_tmp_capacity(std::min<uint64_t>(p.k, N)));
+    tmp = std::max(tmp, launch::sort_tmp_capacity(n3));
+    if (tmp) sort_tmp_.ensure(tmp);
+    if (h_cap_ < p.k) {
+        if (h_pids_) cudaFreeHost(h_pids_);
+        if (h_scores_) cudaFreeHost(h_scores_);
+        h_pids_ = nullptr;
+        h_scores_ = nullptr;
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_pids_), p.k * sizeof(uint32_t)));
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_scores_), p.k * sizeof(float)));
+        h_cap_ = p.k;
+    }
+}
+
+void Searcher::record(int slot, cudaStream_t st, bool times) {
+    if (times) PLAID_CUDA(cudaEventRecord(ev_[slot], st));
+}
+
+// The four stages of lir::search (pipeline.cpp:232-283) as one launch sequence.
+void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
+                       float* d_scores, uint64_t* d_n, cudaStream_t st, bool times) {
+    const IndexView& ix = index_->view();
+    const uint64_t K = ix.K, N = ix.N;
+    uint64_t* c = counters_.p;
+    record(0, st, times);
+    PLAID_CUDA(cudaMemsetAsync(c, 0, kKConst * sizeof(uint64_t), st));
+    PLAID_CUDA(cudaMemsetAsync(bitmap_.p, 0, ((N + 31) / 32) * sizeof(uint32_t), st));
+
+    // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
+    const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
+    const uint32_t warps = launch::scores_exact(ix, d_q, rows, p.t_cs, scores_.p, rowmax_.p, keep_.p,
+                                                partial_.p, npb, st);
+    uint64_t nsel;
+    if (p.nprobe == K) {
+        launch::iota(sel_.p, K, st);
+        nsel = K;
+    } else if (p.nprobe <= 32) {
+        launch::topn_merge(partial_.p, warps, npb, rows, uint32_t(p.nprobe), sel_.p, st);
+        nsel = uint64_t(rows) * p.nprobe;
+    } else {
+        for (uint32_t i = 0; i < rows; ++i) {
+            launch::token_keys(scores_.p, K, i, tok_keys_.p, st);
+            launch::select_top_large(tok_keys_.p, c + kKConst, K, p.nprobe, sel_state_.p,
+                                     tmp_keys_.p, c + kTmpN, st);
+            launch::keys_to_ids(tmp_keys_.p, c + kTmpN, p.nprobe, sel_.p + uint64_t(i) * p.nprobe, st);
+        }
+        nsel = uint64_t(rows) * p.nprobe;
+    }
+    launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap_.p, st);
+    launch::bitmap_compact(bitmap_.p, N, chunk_counts_.p, c1_.p, c + kN1, st);
+    record(1, st, times);
+
+    const uint64_t want_final = p.k;
+    const uint64_t* fin_keys = nullptr;
+    const uint32_t* fin_ids = nullptr;
+    const uint64_t* fin_n = nullptr;
+    uint64_t fin_max = 0;
+    if (p.disable_filter) {
+        // pipeline.cpp:255-258: every stage-1 candidate goes to stage 4
+        launch::copy_count(c + kN1, c + kN2, ~0ull, st);
+        launch::copy_count(c + kN1, c + kN3, ~0ull, st);
+        fin_ids = c1_.p;
+        fin_n = c + kN1;
+        fin_max = N;
+        record(2, st, times);
+        record(3, st, times);
+    } else {
+        // Stage 2: pruned centroid interaction over C1, keep ndocs.
+        const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
+        launch::centroid_interaction(ix, scores_.p, rows, c1_.p, nullptr, c + kN1, N, keep_.p, keys2_.p,
+                                     nullptr, reinterpret_cast<unsigned long long*>(c + kRows2), st);
+        launch::select_top_large(keys2_.p, c + kN1, N, p.ndocs, sel_state_.p, sel2_.p, c + kN2, st);
+        record(2, st, times);
+        // Stage 3: full centroid interaction, keep max(ceil(ndocs/4), k).
+        const uint64_t n3 = std::min<uint64_t>(stage3_width(p), N);
+        launch::centroid_interaction(ix, scores_.p, rows, nullptr, sel2_.p, c + kN2, nd, nullptr,
+                                     keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
+        launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
+                         sort_tmp_.p, st);
+        record(3, st, times);
+        fin_keys = sel3_.p;
+        fin_n = c + kN3;
+        fin_max = n3;
+    }
+    // Stage 4: decompress + exact MaxSim, top-k.
+    launch::copy_count(fin_n, c + kNFin, ~0ull, st);
+    launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, st);
+    const uint32_t base = uint32_t(index_->pid_base());
+    if (fin_max <= launch::kSmallSortMax) {
+        launch::sort_top(keys4_.p, fin_n, fin_max, want_final, nullptr, d_pids, d_scores, d_n, base,
+                         sort_tmp_.p, st);
+    } else {
+        launch::select_top_large(keys4_.p, fin_n, fin_max, want_final, sel_state_.p, tmp_keys_.p,
+                                 c + kTmpN, st);
+        const uint64_t m = std::min<uint64_t>(want_final, fin_max);
+        launch::sort_top(tmp_keys_.p, c + kTmpN, m, want_final, nullptr, d_pids, d_scores, d_n, base,
+                         sort_tmp_.p, st);
+    }
+    launch::copy_count(d_n, c + kNOut, ~0ull, st);
+    record(4, st, times);
+}
+
+void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_params& p,
+                      uint32_t* out_pids, float* out_scores, uint64_t* out_n, plaid_trace* trace) {
+    require_index();
+    *out_n = 0;
+    if (trace) std::memset(trace, 0, sizeof *trace);
+    const IndexView& ix = index_->view();
+    validate_query_host(q, rows, dim, ix.dim);
+    validate_params_host(p, ix.K);
+    if (rows > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32 query tokens");
+    DeviceGuard g(device_);
+    ensure_param_buffers(p);
+    launch::reset_launches();
+    std::memcpy(h_q_, q, rows * dim * sizeof(float));
+    const bool times = trace && cfg_.record_times;
+    PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, rows * dim * sizeof(float), cudaMemcpyHostToDevice, stream_));
+    enqueue(q_.p, uint32_t(rows), p, out_pids_.p, out_scores_.p, counters_.p + kNOut, stream_, times);
+    PLAID_CUDA(cudaMemcpyAsync(h_counters_, counters_.p, kNumCounters * sizeof(uint64_t),
+                               cudaMemcpyDeviceToHost, stream_));
+    PLAID_CUDA(cudaMemcpyAsync(h_pids_, out_pids_.p, p.k * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_));
+    PLAID_CUDA(cudaMemcpyAsync(h_scores_, out_scores_.p, p.k * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    PLAID_CUDA(cudaGetLastError());
+    last_launches_ = launch::launches();
+    const uint64_t n = h_counters_[kNOut];
+    *out_n = n;
+    std::memcpy(out_pids, h_pids_, n * sizeof(uint32_t));
+    std::memcpy(out_scores, h_scores_, n * sizeof(float));
+    if (trace) {
+        trace->stage1_candidates = h_counters_[kN1];
+        trace->centroid_matmul_count = 1;
+        if (h_counters_[kN1] > 0) {  // pipeline.cpp:249-252: empty C1 returns early
+            trace->stage2_out = h_counters_[kN2];
+            trace->stage3_out = h_counters_[kN3];
+            trace->final_out = n;
+            trace->stage2_rows_gathered = h_counters_[kRows2];
+            trace->stage3_rows_gathered = h_counters_[kRows3];
+            trace->decompressed_passages = h_counters_[kNFin];
+        }
+        if (times) {
+            float ms[4];
+            for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], ev_[i], ev_[i + 1]);
+            trace->candidate_generation_ms = ms[0];
+            trace->stage2_ms = ms[1];
+            trace->stage3_ms = ms[2];
+            trace->lookup_ms = 0.0;         // fused into the stage-4 kernel
+            trace->decompression_ms = 0.0;  // fused into the stage-4 kernel
+            trace->scoring_ms = ms[3];
+            float tot = 0;
+            cudaEventElapsedTime(&tot, ev_[0], ev_[4]);
+            trace->total_ms = tot;
+        }
+    }
+}
+
+void Searcher::search_device(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim,
+                             const plaid_params& p, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
+                             cudaStream_t st) {
+    require_index();
+    const IndexView& ix = index_->view();
+    if (dim != ix.dim) fail(PLAID_DIMENSION_MISMATCH, "query dim does not match index dim");
+    if (rows == 0) fail(PLAID_INVALID_PARAMS, "query must contain at least one token");
+    if (rows > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32 query tokens");
+    validate_params_host(p, ix.K);
+    DeviceGuard g(device_);
+    ensure_param_buffers(p);
+    if (!st) st = stream_;
+    launch::reset_launches();
+    for (uint64_t j = 0; j < nq; ++j) {
+        const float* q = d_q + j * rows * dim;
+        launch::validate_query(q, uint32_t(rows), uint32_t(dim), status_.p, st);
+        enqueue(q, uint32_t(rows), p, d_pids + j * p.k, d_scores + j * p.k, d_n + j, st, false);
+    }
+    PLAID_CUDA(cudaGetLastError());
+    last_launches_ = launch::launches();
+}
+
+void Searcher::sync() {
+    DeviceGuard g(device_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    PLAID_CUDA(cudaDeviceSynchronize());
+    int status = 0;
+    PLAID_CUDA(cudaMemcpy(&status, status_.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (status) {
+        PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
+        fail(status, "device-side query validation failed (row not unit norm)");
+    }
+}
+
+// ---------------------------------------------------------------- entry points
+namespace {
+template <typename T>
+void h2d(T* dst, const T* src, uint64_t n, cudaStream_t st) {
+    if (n) PLAID_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+template <typename T>
+void d2h(T* dst, const T* src, uint64_t n, cudaStream_t st) {
+    if (n) PLAID_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+}
+}  // namespace
+
+void Searcher::compute_centroid_scores(const float* q, uint64_t rows, uint64_t dim, float* scores,
+                                       float* row_max) {
+    require_index();
+    const IndexView& ix = index_->view();
+    if (dim != ix.dim) fail(PLAID_DIMENSION_MISMATCH, "query dim does not match centroid dim");
+    if (rows == 0 || rows > 32) fail(PLAID_UNSUPPORTED, "engine supports 1 <= |Q| <= 32");
+    DeviceGuard g(device_);
+    h2d(q_.p, q, rows * dim, stream_);
+    launch::scores_exact(ix, q_.p, uint32_t(rows), INFINITY, scores_.p, rowmax_.p, keep_.p, partial_.p, 1,
+                         stream_);
+    std::vector<float> S(ix.K * kScoresPitch);
+    d2h(S.data(), scores_.p, S.size(), stream_);
+    d2h(row_max, rowmax_.p, ix.K, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    for (uint64_t c = 0; c < ix.K; ++c)
+        std::memcpy(scores + c * rows, S.data() + c * kScoresPitch, rows * sizeof(float));
+}
+
+void Searcher::generate_candidates(const float* scores, uint64_t rows, uint64_t nprobe,
+                                   uint32_t* out_ids, uint64_t* out_n) {
+    require_index();
+    const IndexView& ix = index_->view();
+    *out_n = 0;
+    if (nprobe < 1 || nprobe > ix.K) fail(PLAID_INVALID_PARAMS, "nprobe outside [1, K]");
+    if (rows == 0 || rows > 32) fail(PLAID_UNSUPPORTED, "engine supports 1 <= |Q| <= 32");
+    DeviceGuard g(device_);
+    plaid_params p{};
+    p.k = 1;
+    p.nprobe = nprobe;
+    p.ndocs = 1;
+    ensure_param_buffers(p);
+    std::vector<float> S(ix.K * kScoresPitch, 0.0f);
+    for (uint64_t c = 0; c < ix.K; ++c) std::memcpy(S.data() + c * kScoresPitch, scores + c * rows, rows * 4);
+    h2d(scores_.p, S.data(), S.size(), stream_);
+    uint64_t* c = counters_.p;
+    PLAID_CUDA(cudaMemsetAsync(bitmap_.p, 0, ((ix.N + 31) / 32) * sizeof(uint32_t), stream_));
+    uint64_t nsel;
+    if (nprobe == ix.K) {
+        launch::iota(sel_.p, ix.K, stream_);
+        nsel = ix.K;
+    } else if (nprobe <= 32) {
+        const uint32_t npb = np_bucket(nprobe);
+        const uint32_t w = launch::topn_from_scores(scores_.p, ix.K, uint32_t(rows), partial_.p, npb, stream_);
+        launch::topn_merge(partial_.p, w, npb, uint32_t(rows), uint32_t(nprobe), sel_.p, stream_);
+        nsel = rows * nprobe;
+    } else {
+        for (uint32_t i = 0; i < rows; ++i) {
+            launch::token_keys(scores_.p, ix.K, i, tok_keys_.p, stream_);
+            launch::select_top_large(tok_keys_.p, c + kKConst, ix.K, nprobe, sel_state_.p, tmp_keys_.p,
+                                     c + kTmpN, stream_);
+            launch::keys_to_ids(tmp_keys_.p, c + kTmpN, nprobe, sel_.p + uint64_t(i) * nprobe, stream_);
+        }
+        nsel = rows * nprobe;
+    }
+    launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap_.p, stream_);
+    launch::bitmap_compact(bitmap_.p, ix.N, chunk_counts_.p, c1_.p, c + kN1, stream_);
+    uint64_t n = 0;
+    d2h(&n, c + kN1, 1, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    d2h(out_ids, c1_.p, n, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    *out_n = n;
+}
+
+void Searcher::centroid_interaction(const float* scores, uint64_t rows, const uint32_t* cand, uint64_t n,
+                                    const uint8_t* mask, float* out_scores, uint64_t* rows_gathered) {
+    require_index();
+    const IndexView& ix = index_->view();
+    if (n == 0) fail(PLAID_INVALID_PARAMS, "centroid interaction requires candidates");
+    if (rows == 0 || rows > 32) fail(PLAID_UNSUPPORTED, "engine supports 1 <= |Q| <= 32");
+    for (uint64_t i = 0; i < n; ++i)
+        if (cand[i] >= ix.N) fail(PLAID_INDEX_OUT_OF_RANGE, "candidate id out of range");
+    DeviceGuard g(device_);
+    std::vector<float> S(ix.K * kScoresPitch, 0.0f);
+    for (uint64_t c = 0; c < ix.K; ++c) std::memcpy(S.data() + c * kScoresPitch, scores + c * rows, rows * 4);
+    h2d(scores_.p, S.data(), S.size(), stream_);
+    ids_tmp_.ensure(n);
+    h2d(ids_tmp_.p, cand, n, stream_);
+    if (mask) {
+        std::vector<uint32_t> bits((ix.K + 31) / 32, 0);
+        for (uint64_t c = 0; c < ix.K; ++c)
+            if (mask[c]) bits[c / 32] |= 1u << (c % 32);
+        h2d(keep_.p, bits.data(), bits.size(), stream_);
+    }
+    uint64_t* c = counters_.p;
+    PLAID_CUDA(cudaMemcpyAsync(c + kEntryN, &n, sizeof n, cudaMemcpyHostToDevice, stream_));
+    PLAID_CUDA(cudaMemsetAsync(c + kRows2, 0, sizeof(uint64_t), stream_));
+    DevBuf<uint64_t> keys;
+    keys.ensure(n);
+    DevBuf<float> sc;
+    sc.ensure(n);
+    launch::centroid_interaction(ix, scores_.p, uint32_t(rows), ids_tmp_.p, nullptr, c + kEntryN, n,
+                                 mask ? keep_.p : nullptr, keys.p, sc.p,
+                                 reinterpret_cast<unsigned long long*>(c + kRows2), stream_);
+    d2h(out_scores, sc.p, n, stream_);
+    uint64_t rg = 0;
+    d2h(&rg, c + kRows2, 1, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    if (rows_gathered) *rows_gathered = rg;
+}
+
+void Searcher::select_top(const uint32_t* ids, const float* scores, uint64_t n, uint64_t keep,
+                          uint32_t* out_ids, float* out_scores, uint64_t* out_n) {
+    if (keep < 1) fail(PLAID_INVALID_PARAMS, "selection width must be >= 1");
+    *out_n = 0;
+    DeviceGuard g(device_);
+    DevBuf<uint32_t> dids;
+    DevBuf<float> dsc;
+    DevBuf<uint64_t> keys, sel, tmp, out_nb;
+    dids.ensure(n);
+    dsc.ensure(n);
+    keys.ensure(n);
+    out_nb.ensure(2);
+    h2d(dids.p, ids, n, stream_);
+    h2d(dsc.p, scores, n, stream_);
+    uint64_t* c = counters_.p;
+    PLAID_CUDA(cudaMemcpyAsync(c + kEntryN, &n, sizeof n, cudaMemcpyHostToDevice, stream_));
+    launch::make_keys(dids.p, dsc.p, n, keys.p, stream_);
+    const uint64_t m = std::min(n, keep);
+    DevBuf<uint32_t> oid;
+    DevBuf<float> osc;
+    oid.ensure(m);
+    osc.ensure(m);
+    if (n <= launch::kSmallSortMax) {
+        launch::sort_top(keys.p, c + kEntryN, n, keep, nullptr, oid.p, osc.p, out_nb.p, 0, nullptr, stream_);
+    } else {
+        sel.ensure(m);
+        launch::select_top_large(keys.p, c + kEntryN, n, keep, sel_state_.p, sel.p, out_nb.p + 1, stream_);
+        const uint64_t cap = launch::sort_tmp_capacity(m);
+        if (cap) tmp.ensure(cap);
+        launch::sort_top(sel.p, out_nb.p + 1, m, keep, nullptr, oid.p, osc.p, out_nb.p, 0, tmp.p, stream_);
+    }
+    uint64_t got = 0;
+    d2h(&got, out_nb.p, 1, stream_);
+    d2h(out_ids, oid.p, m, stream_);
+    d2h(out_scores, osc.p, m, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    *out_n = got;
+}
+
+void Searcher::rank_final(const float* q, uint64_t rows, const uint32_t* cand, uint64_t n, uint64_t k,
+                          uint32_t* out_ids, float* out_scores, uint64_t* out_n) {
+    require_index();
+    const IndexView& ix = index_->view();
+    *out_n = 0;
+    if (n == 0) fail(PLAID_INVALID_PARAMS, "final ranking requires candidates");
+    if (rows == 0 || rows > 32) fail(PLAID_UNSUPPORTED, "engine supports 1 <= |Q| <= 32");
+    for (uint64_t i = 0; i < n; ++i) {  // maxsim.cpp:18-22 via rank_final's packed offsets
+        if (cand[i] >= ix.N) fail(PLAID_INDEX_OUT_OF_RANGE, "candidate id out of range");
+        if (index_->host_doclens()[cand[i]] == 0)
+            fail(PLAID_EMPTY_PASSAGE_RANGE, "passage " + std::to_string(i) + " has no token rows");
+    }
+    DeviceGuard g(device_);
+    ids_tmp_.ensure(n);
+    h2d(q_.p, q, rows * ix.dim, stream_);
+    h2d(ids_tmp_.p, cand, n, stream_);
+    uint64_t* c = counters_.p;
+    PLAID_CUDA(cudaMemcpyAsync(c + kEntryN, &n, sizeof n, cudaMemcpyHostToDevice, stream_));
+    DevBuf<uint64_t> keys;
+    keys.ensure(n);
+    launch::rank_exact(ix, q_.p, uint32_t(rows), ids_tmp_.p, nullptr, c + kEntryN, n, keys.p, stream_);
+    std::vector<uint64_t> hk(n);
+    d2h(hk.data(), keys.p, n, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    PLAID_CUDA(cudaGetLastError());
+    std::vector<float> sc(n);
+    for (uint64_t i = 0; i < n; ++i) sc[i] = dev::key_score(hk[i]);
+    select_top(cand, sc.data(), n, k, out_ids, out_scores, out_n);
+}
+
+void Searcher::reconstruct(const uint32_t* codes, uint64_t n, const uint8_t* residuals, float* out) {
+    require_index();
+    const IndexView& ix = index_->view();
+    DeviceGuard g(device_);
+    for (uint64_t t = 0; t < n; ++t)
+        if (codes[t] >= ix.K) fail(PLAID_INDEX_OUT_OF_RANGE, "code exceeds centroid count");
+    const uint64_t bpt = uint64_t(ix.nbits) * ix.dim / 8;
+    DevBuf<uint32_t> dc;
+    DevBuf<unsigned char> dr;
+    DevBuf<float> dout;
+    dc.ensure(n);
+    dr.ensure(n * bpt);
+    dout.ensure(n * ix.dim);
+    h2d(dc.p, codes, n, stream_);
+    h2d(dr.p, residuals, n * bpt, stream_);
+    launch::reconstruct(ix, dc.p, n, dr.p, dout.p, stream_);
+    d2h(out, dout.p, n * ix.dim, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Searcher::unpack(const uint8_t* packed, uint64_t n, uint32_t nbits, uint8_t* out) {
+    if (!nbits_supported(nbits)) fail(PLAID_PACKING_UNSUPPORTED, "nbits not in {1,2,4}");
+    DeviceGuard g(device_);
+    DevBuf<unsigned char> dp, dout;
+    dp.ensure(n);
+    dout.ensure(n * (8 / nbits));
+    h2d(dp.p, packed, n, stream_);
+    launch::unpack_via_lut(dp.p, n, nbits, dout.p, stream_);
+    d2h(out, dout.p, n * (8 / nbits), stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+}
+
+namespace {
+// maxsim.cpp:11-27
+void check_offsets_host(const uint64_t* offsets, uint64_t np, uint64_t total_rows) {
+    if (offsets[0] != 0) fail(PLAID_INVALID_PARAMS, "offsets must start at 0");
+    for (uint64_t p = 0; p < np; ++p) {
+        if (offsets[p + 1] < offsets[p]) fail(PLAID_INVALID_PARAMS, "offsets must be monotone");
+        if (offsets[p + 1] == offsets[p])
+            fail(PLAID_EMPTY_PASSAGE_RANGE, "passage " + std::to_string(p) + " has no token rows");
+    }
+    if (offsets[np] != total_rows) fail(PLAID_LENGTH_MISMATCH, "last offset does not match row count");
+}
+}  // namespace
+
+void Searcher::maxsim_packed(const float* scores, uint64_t nq, const uint64_t* offsets, uint64_t np,
+                             float* out) {
+    if (nq == 0) fail(PLAID_INVALID_PARAMS, "need at least one query token");
+    if (nq > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32");
+    check_offsets_host(offsets, np, offsets[np]);
+    DeviceGuard g(device_);
+    const uint64_t T = offsets[np];
+    DevBuf<float> ds, dout;
+    DevBuf<uint64_t> doff;
+    ds.ensure(T * nq);
+    doff.ensure(np + 1);
+    dout.ensure(np);
+    h2d(ds.p, scores, T * nq, stream_);
+    h2d(doff.p, offsets, np + 1, stream_);
+    launch::maxsim_packed(ds.p, uint32_t(nq), doff.p, np, dout.p, stream_);
+    d2h(out, dout.p, np, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Searcher::maxsim_embeddings(const float* q, uint64_t rows, uint64_t dim, const float* emb,
+                                 const uint64_t* offsets, uint64_t np, float* out) {
+    if (rows == 0 || dim == 0) fail(PLAID_INVALID_PARAMS, "empty query matrix");
+    if (rows > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32");
+    check_offsets_host(offsets, np, offsets[np]);
+    DeviceGuard g(device_);
+    const uint64_t T = offsets[np];
+    DevBuf<float> dq, de, dout;
+    DevBuf<uint64_t> doff;
+    dq.ensure(rows * dim);
+    de.ensure(T * dim);
+    doff.ensure(np + 1);
+    dout.ensure(np);
+    h2d(dq.p, q, rows * dim, stream_);
+    h2d(de.p, emb, T * dim, stream_);
+    h2d(doff.p, offsets, np + 1, stream_);
+    launch::maxsim_embeddings(dq.p, uint32_t(rows), uint32_t(dim), de.p, doff.p, np, dout.p, stream_);
+    d2h(out, dout.p, np, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Searcher::merge_topk_device(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts,
+                                 uint64_t shards, uint64_t stride, uint64_t k, uint32_t* d_out_pids,
+                                 float* d_out_scores, uint64_t* d_out_n, cudaStream_t st) {
+    if (k < 1) fail(PLAID_INVALID_PARAMS, "k must be >= 1");
+    DeviceGuard g(device_);
+    if (!st) st = stream_;
+    const uint64_t total = shards * stride;
+    tmp_keys_.ensure(std::max<uint64_t>(total, 1));
+    const uint64_t cap = launch::sort_tmp_capacity(total);
+    if (cap) sort_tmp_.ensure(cap);
+    launch::merge_topk(d_pids, d_scores, d_counts, shards, stride, k, tmp_keys_.p, counters_.p + kTmpN,
+                       d_out_pids, d_out_scores, d_out_n, sort_tmp_.p, st);
+}
+
+void Searcher::merge_topk(const uint32_t* pids, const float* scores, const uint64_t* counts, uint64_t shards,
+                          uint64_t stride, uint64_t k, uint32_t* out_pids, float* out_scores,
+                          uint64_t* out_n) {
+    DeviceGuard g(device_);
+    const uint64_t total = shards * stride;
+    DevBuf<uint32_t> dp, op;
+    DevBuf<float> ds, os;
+    DevBuf<uint64_t> dc, on;
+    dp.ensure(total);
+    ds.ensure(total);
+    dc.ensure(shards);
+    op.ensure(k);
+    os.ensure(k);
+    on.ensure(1);
+    h2d(dp.p, pids, total, stream_);
+    h2d(ds.p, scores, total, stream_);
+    h2d(dc.p, counts, shards, stream_);
+    merge_topk_device(dp.p, ds.p, dc.p, shards, stride, k, op.p, os.p, on.p, stream_);
+    uint64_t n = 0;
+    d2h(&n, on.p, 1, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    d2h(out_pids, op.p, n, stream_);
+    d2h(out_scores, os.p, n, stream_);
+    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    *out_n = n;
+}
+
+}  // namespace plaid

@@ -1,0 +1,157 @@
+// engine.hpp — C++ host side of the B200 PLAID searcher.
+//
+// DeviceIndex mirrors lir::CompressedIndex (index.hpp:60-85) in HBM; Searcher
+// owns one stream and all per-query scratch, pre-sized from (K, N) so a search
+// never allocates, and enqueues the four stages of lir::search
+// (pipeline.cpp:232-283) as a fixed launch sequence.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/plaid.h"
+#include "kernels.cuh"
+
+namespace plaid {
+
+class Error : public std::runtime_error {
+public:
+    Error(int status, const std::string& msg) : std::runtime_error(msg), status_(status) {}
+    int status() const noexcept { return status_; }
+
+private:
+    int status_;
+};
+
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Error(status, msg); }
+
+void cuda_check(cudaError_t e, const char* what);
+#define PLAID_CUDA(x) ::plaid::cuda_check((x), #x)
+
+// Host-side validation mirroring types.cpp / index.cpp.
+void validate_query_host(const float* q, uint64_t rows, uint64_t dim, uint64_t index_dim);
+void validate_params_host(const plaid_params& p, uint64_t num_centroids);
+void default_params_for_k(uint64_t k, plaid_params* out);
+uint64_t stage3_width(const plaid_params& p);
+void validate_index_host(const plaid_index_desc& d);
+
+class DeviceIndex {
+public:
+    DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_base);
+    ~DeviceIndex();
+    DeviceIndex(const DeviceIndex&) = delete;
+    DeviceIndex& operator=(const DeviceIndex&) = delete;
+
+    const IndexView& view() const { return view_; }
+    int device() const { return device_; }
+    uint64_t pid_base() const { return pid_base_; }
+    uint32_t max_doclen() const { return max_doclen_; }
+    uint64_t bytes() const { return bytes_; }
+    const float* cutoffs() const { return cutoffs_; }
+    const std::vector<uint32_t>& host_doclens() const { return h_doclens_; }
+    // Downloads the device arrays and re-checks validate_index's invariants.
+    void validate_device();
+
+private:
+    template <typename T>
+    T* upload(const T* src, uint64_t count);
+    int device_;
+    uint64_t pid_base_;
+    IndexView view_;
+    uint32_t max_doclen_ = 0;
+    uint64_t bytes_ = 0;
+    float cutoffs_[16] = {};
+    std::vector<void*> allocs_;
+    std::vector<uint32_t> h_doclens_;
+};
+
+// Host-side pinned/device buffer helper.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    uint64_t n = 0;
+    void ensure(uint64_t count);
+    void release();
+    ~DevBuf() { release(); }
+};
+
+struct SearchCounts;  // device-side trace counters
+
+class Searcher {
+public:
+    Searcher(DeviceIndex* index, int device, const plaid_searcher_config& cfg);
+    ~Searcher();
+
+    // Host path (lir::search): validates, uploads Q, runs, downloads.
+    void search(const float* q, uint64_t rows, uint64_t dim, const plaid_params& p,
+                uint32_t* out_pids, float* out_scores, uint64_t* out_n, plaid_trace* trace);
+    // Device path: enqueue only.
+    void search_device(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim,
+                       const plaid_params& p, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
+                       cudaStream_t st);
+    void sync();
+    uint64_t last_launches() const { return last_launches_; }
+
+    // Per-stage entry points (host buffers).
+    void compute_centroid_scores(const float* q, uint64_t rows, uint64_t dim, float* scores,
+                                 float* row_max);
+    void generate_candidates(const float* scores, uint64_t rows, uint64_t nprobe, uint32_t* out_ids,
+                             uint64_t* out_n);
+    void centroid_interaction(const float* scores, uint64_t rows, const uint32_t* cand, uint64_t n,
+                              const uint8_t* mask, float* out_scores, uint64_t* rows_gathered);
+    void select_top(const uint32_t* ids, const float* scores, uint64_t n, uint64_t keep,
+                    uint32_t* out_ids, float* out_scores, uint64_t* out_n);
+    void rank_final(const float* q, uint64_t rows, const uint32_t* cand, uint64_t n, uint64_t k,
+                    uint32_t* out_ids, float* out_scores, uint64_t* out_n);
+    void reconstruct(const uint32_t* codes, uint64_t n, const uint8_t* residuals, float* out);
+    void unpack(const uint8_t* packed, uint64_t n, uint32_t nbits, uint8_t* out);
+    void maxsim_packed(const float* scores, uint64_t nq, const uint64_t* offsets, uint64_t np,
+                       float* out);
+    void maxsim_embeddings(const float* q, uint64_t rows, uint64_t dim, const float* emb,
+                           const uint64_t* offsets, uint64_t np, float* out);
+    void merge_topk(const uint32_t* pids, const float* scores, const uint64_t* counts,
+                    uint64_t shards, uint64_t stride, uint64_t k, uint32_t* out_pids,
+                    float* out_scores, uint64_t* out_n);
+    void merge_topk_device(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts,
+                           uint64_t shards, uint64_t stride, uint64_t k, uint32_t* d_out_pids,
+                           float* d_out_scores, uint64_t* d_out_n, cudaStream_t st);
+
+private:
+    void require_index() const;
+    // Enqueue one query whose rows already sit at d_q; results go to the
+    // given device buffers (pids are global: local + pid_base).
+    void enqueue(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
+                 float* d_scores, uint64_t* d_n, cudaStream_t st, bool times);
+    void ensure_param_buffers(const plaid_params& p);
+    void record(int slot, cudaStream_t st, bool times);
+
+    DeviceIndex* index_;
+    int device_;
+    plaid_searcher_config cfg_;
+    cudaStream_t stream_ = nullptr;
+    uint64_t last_launches_ = 0;
+
+    // scratch
+    DevBuf<float> q_, scores_, rowmax_, out_scores_;
+    DevBuf<uint32_t> keep_, sel_, bitmap_, chunk_counts_, c1_, out_pids_, ids_tmp_;
+    DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_,
+        counters_, tmp_keys_;
+    DevBuf<unsigned char> bytes_tmp_;
+    DevBuf<SelectState> sel_state_;
+    DevBuf<int> status_;
+    // pinned staging
+    float* h_q_ = nullptr;
+    uint64_t* h_counters_ = nullptr;
+    uint32_t* h_pids_ = nullptr;
+    float* h_scores_ = nullptr;
+    uint64_t h_cap_ = 0;
+    cudaEvent_t ev_[8] = {};
+    uint64_t npartial_warps_ = 0;
+};
+
+}  // namespace plaid

@@ -1,0 +1,275 @@
+// interaction.cu — centroid interaction, stages 2 and 3 (pipeline.cpp:97-137).
+//
+// Per candidate passage: acc[j] = max over its (unmasked) tokens t of
+// S[code(t)][j]; score = in-order fp32 sum of acc[0..|Q|) if any row was used,
+// else exactly 0.  The max is order-independent except for the sign of zero,
+// and an in-order sum that starts from +0.0f is insensitive to that sign, so
+// the scores are bit-identical to the reference.
+//
+// Stage 2 (masked, candidate count up to N): padding-free flattened scan.  A
+// block takes 256 candidates, prefix-sums their doclens in shared memory and
+// lets its 256 threads sweep the concatenated token range, so consecutive
+// threads read consecutive codes regardless of passage boundaries.  Tokens on
+// kept centroids (few) are queued in shared memory and then folded warp-wide:
+// one 128-byte S row per entry, atomicMax on an order-preserving integer image
+// of the accumulator.  Stage 3 (unmasked, <= ndocs candidates): one warp per
+// passage, codes broadcast by shuffle, 8 S-row loads in flight per warp.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace plaid {
+namespace {
+
+constexpr uint32_t kCB = 256;         // candidates per block (stage 2)
+constexpr uint32_t kListCap = 1024;   // kept-token queue per block (static smem < 48 KB)
+constexpr uint32_t kAccPitch = 33;    // conflict-free column sums
+
+__device__ __forceinline__ uint32_t cand_id(const uint32_t* ids, const uint64_t* keys, uint64_t i) {
+    return ids ? ids[i] : dev::key_id(keys[i]);
+}
+
+__device__ __forceinline__ bool kept(const uint32_t* keep_bits, uint32_t code) {
+    return (__ldg(keep_bits + (code >> 5)) >> (code & 31)) & 1u;
+}
+
+// Warp-wide scoring of one passage (also the overflow fallback of stage 2).
+// Returns the score on every lane; *used = rows folded in.
+template <bool MASKED>
+__device__ float score_passage_warp(const uint32_t* __restrict__ codes, uint64_t off, uint32_t len,
+                                    const float* __restrict__ S, uint32_t rows,
+                                    const uint32_t* __restrict__ keep_bits, uint32_t* used_out) {
+    const uint32_t lane = dev::lane_id();
+    float acc = -INFINITY;
+    uint32_t used = 0;
+    for (uint32_t base = 0; base < len; base += 32) {
+        const uint32_t t = base + lane;
+        const uint32_t code = t < len ? __ldg(codes + off + t) : 0u;
+        bool valid = t < len;
+        if (MASKED) valid = valid && kept(keep_bits, code);
+        uint32_t bits = __ballot_sync(0xffffffffu, valid);
+        used += __popc(bits);
+        while (bits) {
+            float s[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const int b = bits ? __ffs(bits) - 1 : 0;
+                const uint32_t c = __shfl_sync(0xffffffffu, code, b);
+                s[v] = bits ? __ldg(S + uint64_t(c) * kScoresPitch + lane) : -INFINITY;
+                bits &= bits - 1;
+            }
+#pragma unroll
+            for (int v = 0; v < 8; ++v) acc = dev::max_gt(acc, s[v]);
+        }
+    }
+    float total = 0.0f;
+    if (used > 0) {
+        for (uint32_t j = 0; j < rows; ++j) total = __fadd_rn(total, __shfl_sync(0xffffffffu, acc, j));
+    }
+    *used_out = used;
+    return total;
+}
+
+// Stage 3 (and the unmasked entry point): one warp per passage.
+__global__ void __launch_bounds__(256)
+ci_warp_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
+               const uint32_t* __restrict__ doclens, const float* __restrict__ S, uint32_t rows,
+               const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
+               const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ keep_bits,
+               uint64_t* __restrict__ out_keys, float* __restrict__ out_scores,
+               unsigned long long* __restrict__ d_rows) {
+    const uint64_t n = *d_n;
+    const uint32_t lane = dev::lane_id();
+    const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    unsigned long long rows_local = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const uint32_t pid = cand_id(ids, keys, i);
+        const uint64_t off = offsets[pid];
+        const uint32_t len = doclens[pid];
+        uint32_t used;
+        float total = keep_bits ? score_passage_warp<true>(codes, off, len, S, rows, keep_bits, &used)
+                                : score_passage_warp<false>(codes, off, len, S, rows, keep_bits, &used);
+        if (lane == 0) {
+            out_keys[i] = dev::make_key(total, pid);
+            if (out_scores) out_scores[i] = total;
+        }
+        rows_local += used;
+    }
+    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+}
+
+// Stage 2: masked, flattened over the block's concatenated token range.
+__global__ void __launch_bounds__(kCB)
+ci_masked_flat_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
+                      const uint32_t* __restrict__ doclens, const float* __restrict__ S,
+                      uint32_t rows, const uint32_t* __restrict__ ids,
+                      const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
+                      const uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ out_keys,
+                      float* __restrict__ out_scores, unsigned long long* __restrict__ d_rows) {
+    __shared__ uint64_t off_s[kCB];
+    __shared__ uint32_t start_s[kCB + 1];
+    __shared__ uint32_t acc_s[kCB * kAccPitch];
+    __shared__ uint32_t used_s[kCB];
+    __shared__ uint32_t list_s[kListCap * 2];
+    __shared__ uint32_t warp_tot[kCB / 32];
+    __shared__ uint32_t list_n;
+
+    const uint64_t n = *d_n;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t kNegInf = dev::ord_f32(-INFINITY);
+    unsigned long long rows_local = 0;
+
+    for (uint64_t base = uint64_t(blockIdx.x) * kCB; base < n; base += uint64_t(gridDim.x) * kCB) {
+        const uint64_t idx = base + t;
+        uint32_t pid = 0, len = 0;
+        uint64_t off = 0;
+        if (idx < n) {
+            pid = cand_id(ids, keys, idx);
+            off = offsets[pid];
+            len = doclens[pid];
+        }
+        off_s[t] = off;
+        // exclusive scan of len over the block
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += v;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        for (uint32_t j = 0; j < kAccPitch; ++j) acc_s[t * kAccPitch + j] = kNegInf;
+        used_s[t] = 0;
+        if (t == 0) list_n = 0;
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+        for (uint32_t w = 0; w < kCB / 32; ++w) {
+            if (w < warp) before += warp_tot[w];
+            total += warp_tot[w];
+        }
+        start_s[t] = before + incl - len;
+        if (t == 0) start_s[kCB] = total;
+        __syncthreads();
+
+        // sweep the flattened token range, 4 tokens per thread in flight
+        for (uint32_t f0 = 0; f0 < total; f0 += 4 * kCB) {
+            uint32_t code[4], cand[4];
+            bool in[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t f = f0 + u * kCB + t;
+                in[u] = f < total;
+                uint32_t lo = 0, hi = kCB;
+                while (hi - lo > 1) {
+                    uint32_t mid = (lo + hi) >> 1;
+                    if (start_s[mid] <= f) lo = mid; else hi = mid;
+                }
+                cand[u] = lo;
+                code[u] = in[u] ? __ldg(codes + off_s[lo] + (f - start_s[lo])) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (in[u] && kept(keep_bits, code[u])) {
+                    const uint32_t slot = atomicAdd(&list_n, 1u);
+                    if (slot < kListCap) {
+                        list_s[2 * slot] = cand[u];
+                        list_s[2 * slot + 1] = code[u];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t nl = list_n;
+        if (nl <= kListCap) {
+            // fold the queued rows, 4 per warp in flight
+            for (uint32_t e0 = warp; e0 < nl; e0 += 4 * (kCB / 32)) {
+                float s[4];
+                uint32_t cd[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e0 + u * (kCB / 32);
+                    cd[u] = e < nl ? list_s[2 * e] : 0u;
+                    s[u] = e < nl ? __ldg(S + uint64_t(list_s[2 * e + 1]) * kScoresPitch + lane) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e0 + u * (kCB / 32);
+                    if (e < nl) {
+                        if (lane < rows) atomicMax(&acc_s[cd[u] * kAccPitch + lane], dev::ord_f32(s[u]));
+                        if (lane == 0) atomicAdd(&used_s[cd[u]], 1u);
+                    }
+                }
+            }
+            __syncthreads();
+            if (idx < n) {
+                const uint32_t u = used_s[t];
+                float sc = 0.0f;
+                if (u > 0)
+                    for (uint32_t j = 0; j < rows; ++j)
+                        sc = __fadd_rn(sc, dev::unord_f32(acc_s[t * kAccPitch + j]));
+                out_keys[idx] = dev::make_key(sc, pid);
+                if (out_scores) out_scores[idx] = sc;
+                rows_local += u;
+            }
+        } else {
+            // queue overflow (dense masks): score this block's passages warp-wide
+            for (uint32_t c = warp; c < kCB && base + c < n; c += kCB / 32) {
+                const uint32_t p = cand_id(ids, keys, base + c);
+                uint32_t used;
+                float sc = score_passage_warp<true>(codes, offsets[p], doclens[p], S, rows, keep_bits, &used);
+                if (lane == 0) {
+                    out_keys[base + c] = dev::make_key(sc, p);
+                    if (out_scores) out_scores[base + c] = sc;
+                    rows_local += used;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // block-level reduction of the gathered-row counter
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rows_local += __shfl_xor_sync(0xffffffffu, rows_local, o);
+    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+}  // namespace
+
+namespace launch {
+
+void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t rows,
+                          const uint32_t* d_ids, const uint64_t* d_keys, const uint64_t* d_n,
+                          uint64_t nmax, const uint32_t* d_keep_bits, uint64_t* d_out_keys,
+                          float* d_out_scores, unsigned long long* d_rows, cudaStream_t st) {
+    if (nmax == 0) return;
+    if (d_keep_bits) {
+        uint64_t blocks = (nmax + kCB - 1) / kCB;
+        const uint64_t cap = uint64_t(sm_count()) * 4;
+        if (blocks > cap) blocks = cap;
+        ci_masked_flat_kernel<<<uint32_t(blocks), kCB, 0, st>>>(
+            ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_ids, d_keys, d_n, d_keep_bits,
+            d_out_keys, d_out_scores, d_rows);
+    } else {
+        uint64_t blocks = (nmax + 7) / 8;
+        const uint64_t cap = uint64_t(sm_count()) * 8;
+        if (blocks > cap) blocks = cap;
+        ci_warp_kernel<<<uint32_t(blocks), 256, 0, st>>>(ix.codes, ix.offsets, ix.doclens, d_scores,
+                                                        rows, d_ids, d_keys, d_n, d_keep_bits,
+                                                        d_out_keys, d_out_scores, d_rows);
+    }
+    count_launch();
+}
+
+}  // namespace launch
+}  // namespace plaid

@@ -1,0 +1,135 @@
+// kernels.cuh — launchers for the PLAID search kernels (sm_100a).
+//
+// All kernels are enqueued on an explicit stream and read data-dependent
+// sizes (candidate counts) from device memory, so a whole search is a fixed
+// launch sequence that can be captured in a CUDA graph with no host sync.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace plaid {
+
+// Device view of a CompressedIndex (index.hpp:60-85) + derived arrays.
+struct IndexView {
+    uint32_t dim = 0;
+    uint32_t nbits = 0;
+    uint64_t K = 0, N = 0, T = 0, P = 0;
+    const float* centroids = nullptr;   // K x dim
+    const uint32_t* codes = nullptr;    // T
+    const uint8_t* residuals = nullptr; // T x nbits*dim/8
+    const uint32_t* doclens = nullptr;  // N
+    const uint64_t* offsets = nullptr;  // N + 1
+    const uint64_t* ivf_offsets = nullptr;
+    const uint32_t* ivf_postings = nullptr;
+    float weights[16] = {};
+};
+
+// Radix-select scratch (device).  One per concurrent select.
+struct SelectState {
+    unsigned long long prefix;
+    unsigned long long mask;
+    unsigned long long remaining;
+    unsigned int done;
+    unsigned int ticket;
+    unsigned int hist[2048];
+};
+
+constexpr int kScoresPitch = 32;  // S rows padded to 32 floats (128 B)
+
+namespace launch {
+
+// ---- stage 1 -----------------------------------------------------------------
+// S = C . Q^T (in-order fp32, bit-exact), row max, keep bits (row max >= t_cs),
+// and per-warp top-NP keys per query token written to `partial`
+// [num_warps][32][np_bucket].  Returns the number of warps used.
+uint32_t scores_exact(const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
+                      float* d_scores, float* d_rowmax, uint32_t* d_keep_bits,
+                      uint64_t* d_partial, uint32_t np_bucket, cudaStream_t st);
+// Max number of warps scores_exact may use (for sizing `partial`).
+uint32_t scores_max_warps();
+// Merge per-warp partial top-NP lists into sel[rows][nprobe] centroid ids.
+void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,
+                uint32_t nprobe, uint32_t* d_sel, cudaStream_t st);
+// Top-NP per token from a stored S (entry point); returns warps used.
+uint32_t topn_from_scores(const float* d_scores, uint64_t K, uint32_t rows, uint64_t* d_partial,
+                          uint32_t np_bucket, cudaStream_t st);
+void iota(uint32_t* d_out, uint64_t n, cudaStream_t st);
+// Keys (S[c][i], c) for one token column i -> keys[K] (generic nprobe path).
+void token_keys(const float* d_scores, uint64_t K, uint32_t i, uint64_t* d_keys, cudaStream_t st);
+// sel[j] = key_id(keys[j]) for j < n (device count)
+void keys_to_ids(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint32_t* d_ids,
+                 cudaStream_t st);
+// rowmax >= t_cs -> keep bits
+void keep_bits_from_rowmax(const float* d_rowmax, uint64_t K, float t_cs, uint32_t* d_keep_bits,
+                           cudaStream_t st);
+
+// ---- candidate generation -------------------------------------------------------
+void postings_to_bitmap(const IndexView& ix, const uint32_t* d_sel, uint32_t nsel,
+                        uint32_t* d_bitmap, cudaStream_t st);
+// Bitmap (N bits) -> ascending ids + count.  chunk_counts has bitmap_chunks(N) entries.
+uint32_t bitmap_chunks(uint64_t N);
+void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_counts,
+                    uint32_t* d_out_ids, uint64_t* d_out_n, cudaStream_t st);
+
+// ---- centroid interaction (stages 2 and 3) -----------------------------------------
+// Candidates are either ids (d_ids) or keys (d_keys, id in the low word).
+// Writes keys (score, id) and optionally raw scores; adds used rows to *d_rows.
+void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t rows,
+                          const uint32_t* d_ids, const uint64_t* d_keys, const uint64_t* d_n,
+                          uint64_t nmax, const uint32_t* d_keep_bits, uint64_t* d_out_keys,
+                          float* d_out_scores, unsigned long long* d_rows, cudaStream_t st);
+
+// ---- selection -----------------------------------------------------------------------
+// Top `want` of keys[0..*d_n) (largest first).  Result: d_out_keys unsorted
+// (count min(want, n) in *d_out_n).  Uses radix select over 64-bit keys.
+void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
+                      SelectState* d_state, uint64_t* d_out_keys, uint64_t* d_out_n,
+                      cudaStream_t st);
+// Sort keys[0..*d_n) descending (n <= nmax) and emit the first min(want, n):
+// out_keys (optional), out_ids/out_scores (optional, ids offset by id_base),
+// out_n (optional).  nmax <= kSmallSortMax uses one CTA; larger uses a
+// global bitonic sort in `d_tmp` (capacity next_pow2(nmax)).
+constexpr uint64_t kSmallSortMax = 8192;
+void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
+              uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
+              uint32_t id_base, uint64_t* d_tmp, cudaStream_t st);
+uint64_t sort_tmp_capacity(uint64_t nmax);
+
+// ---- stage 4 ----------------------------------------------------------------------
+// Decompress + exact MaxSim per candidate (ids from keys or ids); writes keys.
+void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
+                const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
+                cudaStream_t st);
+
+// ---- misc ---------------------------------------------------------------------------
+// Device-side query validation (types.cpp:61-72): status 0 or NotNormalized+1.
+void validate_query(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, cudaStream_t st);
+// Stage counters: min() bookkeeping done on device.
+void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st);
+// Merge G shard top-k lists into the global top-k.
+void merge_topk(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts,
+                uint64_t shards, uint64_t stride, uint64_t k, uint64_t* d_tmp_keys,
+                uint64_t* d_tmp_n, uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
+                uint64_t* d_sort_tmp, cudaStream_t st);
+// Build keys from (ids, scores) arrays (select_top entry point).
+void make_keys(const uint32_t* d_ids, const float* d_scores, uint64_t n, uint64_t* d_keys,
+               cudaStream_t st);
+
+// ---- codec / maxsim entry points -------------------------------------------------
+void unpack_via_lut(const uint8_t* d_packed, uint64_t n, uint32_t nbits, uint8_t* d_out,
+                    cudaStream_t st);
+void reconstruct(const IndexView& ix, const uint32_t* d_codes, uint64_t n,
+                 const uint8_t* d_residuals, float* d_out, cudaStream_t st);
+void maxsim_packed(const float* d_scores, uint32_t nq, const uint64_t* d_offsets, uint64_t np,
+                   float* d_out, cudaStream_t st);
+void maxsim_embeddings(const float* d_q, uint32_t rows, uint32_t dim, const float* d_emb,
+                       const uint64_t* d_offsets, uint64_t np, float* d_out, cudaStream_t st);
+
+// Number of kernel launches issued by this thread since the last reset.
+uint64_t launches();
+void reset_launches();
+void count_launch();
+
+}  // namespace launch
+}  // namespace plaid

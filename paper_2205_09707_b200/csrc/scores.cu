@@ -1,0 +1,325 @@
+// scores.cu — stage 1 on CUDA cores, bit-exact with the reference:
+//   S[c][i] = dot(C[c], Q[i]) in order over d, mul-then-add (pipeline.cpp:26-50,
+//   types.hpp:18-22), row max (pipeline.cpp:40-46), keep bit (max >= t_cs,
+//   pipeline.cpp:89-95) and the per-token top-nprobe centroid keys
+//   (score desc, id asc; pipeline.cpp:65-73) fused into the same pass.
+//
+// Layout: C is K x dim row-major in HBM; S is K x 32 (row pitch 128 B) so the
+// stage-2/3 row gathers are one 128-byte line per centroid.
+//
+// Work split: each warp owns chunks of 32 consecutive centroids (one keep-bit
+// word) and walks them in groups of G=16; lane i is query token i.  The group's
+// 16 C rows are staged in shared memory and read as broadcast LDS.128; the
+// query rows sit in shared memory with a +4 float pad so the per-lane LDS.128
+// is conflict-free.  Per 4 dims a lane issues 1 + 16 LDS.128 for 128 fp32 ops.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace plaid {
+namespace {
+
+constexpr int kG = 16;           // centroids per group
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlocksPerSm = 2;
+
+template <int NP>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kBlocksPerSm)
+scores_exact_kernel(const float* __restrict__ C, uint64_t K, uint32_t dim,
+                    const float* __restrict__ Q, uint32_t rows, float t_cs,
+                    float* __restrict__ S, float* __restrict__ rowmax,
+                    uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ partial) {
+    extern __shared__ __align__(16) float smem[];
+    const uint32_t qpitch = dim + 4;
+    float* q_s = smem;                                   // 32 x (dim+4)
+    float* c_all = smem + 32 * qpitch;                   // warps x G x dim
+    const uint32_t lane = dev::lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    float* c_s = c_all + warp * kG * dim;
+
+    for (uint32_t idx = threadIdx.x; idx < 32 * dim; idx += blockDim.x) {
+        uint32_t i = idx / dim, d = idx % dim;
+        q_s[i * qpitch + d] = i < rows ? Q[i * dim + d] : 0.0f;
+    }
+    __syncthreads();
+
+    uint64_t top[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) top[j] = 0;  // below every real key
+
+    const uint64_t nchunks = (K + 31) / 32;
+    const uint64_t gwarp = uint64_t(blockIdx.x) * kWarpsPerBlock + warp;
+    const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerBlock;
+    const float4* qrow = reinterpret_cast<const float4*>(q_s + lane * qpitch);
+
+    for (uint64_t chunk = gwarp; chunk < nchunks; chunk += nwarps) {
+        uint32_t keep_word = 0;
+        for (int g = 0; g < 32 / kG; ++g) {
+            const uint64_t c0 = chunk * 32 + g * kG;
+            const uint32_t nc = uint32_t(K - c0 < kG ? K - c0 : kG);
+            // stage the group's rows (contiguous in HBM) into shared memory
+            const float4* src = reinterpret_cast<const float4*>(C + c0 * dim);
+            float4* dst = reinterpret_cast<float4*>(c_s);
+            const uint32_t n4 = nc * dim / 4, tot4 = kG * dim / 4;
+            __syncwarp();
+            for (uint32_t v = lane; v < tot4; v += 32)
+                dst[v] = v < n4 ? __ldcs(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();
+
+            float acc[kG];
+#pragma unroll
+            for (int c = 0; c < kG; ++c) acc[c] = 0.0f;
+            const float4* crow = reinterpret_cast<const float4*>(c_s);
+            const uint32_t dim4 = dim / 4;
+            for (uint32_t d4 = 0; d4 < dim4; ++d4) {
+                const float4 q = qrow[d4];
+#pragma unroll
+                for (int c = 0; c < kG; ++c) {
+                    const float4 cv = crow[c * dim4 + d4];
+                    float a = acc[c];
+                    a = dev::madd_rn(a, cv.x, q.x);
+                    a = dev::madd_rn(a, cv.y, q.y);
+                    a = dev::madd_rn(a, cv.z, q.z);
+                    a = dev::madd_rn(a, cv.w, q.w);
+                    acc[c] = a;
+                }
+            }
+            float my_max = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < kG; ++c) {
+                if (c < int(nc)) {
+                    S[(c0 + c) * kScoresPitch + lane] = acc[c];
+                    float m = dev::warp_max(lane < rows ? acc[c] : -INFINITY);
+                    if (lane == uint32_t(c)) my_max = m;
+                    if (m >= t_cs) keep_word |= 1u << (g * kG + c);
+                    if (lane < rows) dev::topn_insert<NP>(top, dev::make_key(acc[c], uint32_t(c0 + c)));
+                }
+            }
+            if (lane < nc) rowmax[c0 + lane] = my_max;
+        }
+        if (lane == 0) keep_bits[chunk] = keep_word;
+    }
+    uint64_t* out = partial + (gwarp * 32 + lane) * NP;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) out[j] = top[j];
+}
+
+// One block per query token: merge every warp's top-NP list for that token.
+template <int NP>
+__global__ void topn_merge_kernel(const uint64_t* __restrict__ partial, uint32_t nwarps,
+                                  uint32_t nprobe, uint32_t* __restrict__ sel) {
+    extern __shared__ uint64_t lists[];  // blockDim x NP
+    const uint32_t i = blockIdx.x;
+    uint64_t top[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) top[j] = 0;
+    for (uint32_t w = threadIdx.x; w < nwarps; w += blockDim.x) {
+        const uint64_t* l = partial + (uint64_t(w) * 32 + i) * NP;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) dev::topn_insert<NP>(top, l[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) lists[threadIdx.x * NP + j] = top[j];
+    __syncthreads();
+    for (uint32_t s = blockDim.x / 2; s > 0; s >>= 1) {
+        const bool active = threadIdx.x < s;
+        uint64_t out[NP];
+        if (active) {  // two-pointer merge of two descending lists, keep NP
+            const uint64_t* a = lists + threadIdx.x * NP;
+            const uint64_t* b = lists + (threadIdx.x + s) * NP;
+            int ia = 0, ib = 0;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                uint64_t va = ia < NP ? a[ia] : 0, vb = ib < NP ? b[ib] : 0;
+                if (va > vb) { out[j] = va; ++ia; } else { out[j] = vb; ++ib; }
+            }
+        }
+        __syncthreads();
+        if (active) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) lists[threadIdx.x * NP + j] = out[j];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < nprobe) sel[i * nprobe + threadIdx.x] = dev::key_id(lists[threadIdx.x]);
+}
+
+__global__ void token_keys_kernel(const float* __restrict__ S, uint64_t K, uint32_t i,
+                                  uint64_t* __restrict__ keys) {
+    for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < K;
+         c += uint64_t(gridDim.x) * blockDim.x)
+        keys[c] = dev::make_key(S[c * kScoresPitch + i], uint32_t(c));
+}
+
+__global__ void keys_to_ids_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ n,
+                                   uint32_t* __restrict__ ids) {
+    const uint64_t cnt = *n;
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < cnt;
+         j += uint64_t(gridDim.x) * blockDim.x)
+        ids[j] = dev::key_id(keys[j]);
+}
+
+__global__ void keep_bits_kernel(const float* __restrict__ rowmax, uint64_t K, float t_cs,
+                                 uint32_t* __restrict__ bits) {
+    const uint64_t words = (K + 31) / 32;
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < words;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t v = 0;
+        for (uint32_t b = 0; b < 32; ++b) {
+            uint64_t c = w * 32 + b;
+            if (c < K && rowmax[c] >= t_cs) v |= 1u << b;
+        }
+        bits[w] = v;
+    }
+}
+
+// Standalone top-NP over a stored S (the generate_candidates entry point):
+// same per-warp insertion lists as the fused kernel, so the merge is shared.
+template <int NP>
+__global__ void topn_from_scores_kernel(const float* __restrict__ S, uint64_t K, uint32_t rows,
+                                        uint64_t* __restrict__ partial) {
+    const uint32_t lane = dev::lane_id();
+    const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    uint64_t top[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) top[j] = 0;
+    if (lane < rows)
+        for (uint64_t c = gwarp; c < K; c += nwarps)
+            dev::topn_insert<NP>(top, dev::make_key(S[c * kScoresPitch + lane], uint32_t(c)));
+    uint64_t* out = partial + (gwarp * 32 + lane) * NP;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) out[j] = top[j];
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = uint32_t(i);
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int NP>
+void launch_scores(const IndexView& ix, const float* q, uint32_t rows, float t_cs, float* S,
+                   float* rowmax, uint32_t* keep, uint64_t* partial, uint32_t blocks,
+                   cudaStream_t st) {
+    const size_t smem = size_t(32) * (ix.dim + 4) * 4 + size_t(kWarpsPerBlock) * kG * ix.dim * 4;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(scores_exact_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
+        configured = true;
+    }
+    scores_exact_kernel<NP><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+        ix.centroids, ix.K, ix.dim, q, rows, t_cs, S, rowmax, keep, partial);
+    launch::count_launch();
+}
+
+template <int NP>
+void launch_merge(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint32_t nprobe,
+                  uint32_t* sel, cudaStream_t st) {
+    const uint32_t threads = 256;
+    topn_merge_kernel<NP><<<rows, threads, threads * NP * sizeof(uint64_t), st>>>(partial, nwarps,
+                                                                                 nprobe, sel);
+    launch::count_launch();
+}
+
+}  // namespace
+
+namespace launch {
+
+uint32_t scores_max_warps() { return uint32_t(sm_count()) * kBlocksPerSm * kWarpsPerBlock; }
+
+uint32_t scores_exact(const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
+                      float* d_scores, float* d_rowmax, uint32_t* d_keep_bits, uint64_t* d_partial,
+                      uint32_t np_bucket, cudaStream_t st) {
+    const uint64_t chunks = (ix.K + 31) / 32;
+    uint64_t want = (chunks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    uint32_t blocks = uint32_t(want < uint64_t(sm_count()) * kBlocksPerSm ? want
+                                                                          : uint64_t(sm_count()) * kBlocksPerSm);
+    if (blocks == 0) blocks = 1;
+    switch (np_bucket) {
+        case 1: launch_scores<1>(ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, blocks, st); break;
+        case 2: launch_scores<2>(ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, blocks, st); break;
+        case 4: launch_scores<4>(ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, blocks, st); break;
+        case 8: launch_scores<8>(ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, blocks, st); break;
+        case 16: launch_scores<16>(ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, blocks, st); break;
+        default: launch_scores<32>(ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, blocks, st); break;
+    }
+    return blocks * kWarpsPerBlock;
+}
+
+void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,
+                uint32_t nprobe, uint32_t* d_sel, cudaStream_t st) {
+    switch (np_bucket) {
+        case 1: launch_merge<1>(d_partial, num_warps, rows, nprobe, d_sel, st); break;
+        case 2: launch_merge<2>(d_partial, num_warps, rows, nprobe, d_sel, st); break;
+        case 4: launch_merge<4>(d_partial, num_warps, rows, nprobe, d_sel, st); break;
+        case 8: launch_merge<8>(d_partial, num_warps, rows, nprobe, d_sel, st); break;
+        case 16: launch_merge<16>(d_partial, num_warps, rows, nprobe, d_sel, st); break;
+        default: launch_merge<32>(d_partial, num_warps, rows, nprobe, d_sel, st); break;
+    }
+}
+
+void token_keys(const float* d_scores, uint64_t K, uint32_t i, uint64_t* d_keys, cudaStream_t st) {
+    uint64_t blocks = (K + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    token_keys_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_scores, K, i, d_keys);
+    count_launch();
+}
+
+void keys_to_ids(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint32_t* d_ids,
+                 cudaStream_t st) {
+    uint64_t blocks = (nmax + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    if (blocks == 0) blocks = 1;
+    keys_to_ids_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_keys, d_n, d_ids);
+    count_launch();
+}
+
+void keep_bits_from_rowmax(const float* d_rowmax, uint64_t K, float t_cs, uint32_t* d_keep_bits,
+                           cudaStream_t st) {
+    uint64_t words = (K + 31) / 32;
+    uint64_t blocks = (words + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    keep_bits_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_rowmax, K, t_cs, d_keep_bits);
+    count_launch();
+}
+
+uint32_t topn_from_scores(const float* d_scores, uint64_t K, uint32_t rows, uint64_t* d_partial,
+                          uint32_t np_bucket, cudaStream_t st) {
+    const uint32_t blocks = uint32_t(sm_count()) * kBlocksPerSm;
+    const uint32_t threads = kWarpsPerBlock * 32;
+    switch (np_bucket) {
+        case 1: topn_from_scores_kernel<1><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
+        case 2: topn_from_scores_kernel<2><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
+        case 4: topn_from_scores_kernel<4><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
+        case 8: topn_from_scores_kernel<8><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
+        case 16: topn_from_scores_kernel<16><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
+        default: topn_from_scores_kernel<32><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
+    }
+    count_launch();
+    return blocks * kWarpsPerBlock;
+}
+
+void iota(uint32_t* d_out, uint64_t n, cudaStream_t st) {
+    uint64_t b = (n + 255) / 256;
+    iota_kernel<<<uint32_t(b > 4096 ? 4096 : (b ? b : 1)), 256, 0, st>>>(d_out, n);
+    count_launch();
+}
+
+}  // namespace launch
+}  // namespace plaid
