@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py — PLAID four-stage search on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl plaid|reference]
+                    [--config cfg2] [--score-mode exact|tensor] [--cpu-seconds S]
+
+One step = one query through all four stages (single-query latency mode,
+BASELINE.json configs[1]: synthetic MS MARCO v1 scale, 8.8M passages, 2^18
+centroids, nbits=2, k=1000 with default_params_for_k).  Inputs are resident in
+HBM when the timed region starts; L2 is flushed (256 MiB write) before every
+step, outside the timed interval.  Each step is bracketed by CUDA events on
+the launching stream; the job time is the max over ranks of the summed step
+times, `value` = queries / that time.
+
+Multi-GPU (torchrun, one process per GPU): every rank holds a passage-range
+shard of the same size (weak scaling: the index grows with N), runs the full
+pipeline on its shard and the per-shard top-k lists are merged with an NCCL
+all-gather + a device-side merge — all inside the timed step.
+
+`--impl reference` times the reference's own CPU searcher (oracle/_ref, the
+unmodified /root/reference sources compiled by oracle/Makefile) on the box's
+host cores, on the same synthetic index and queries; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    "cfg1": dict(N=10_000, K=4096, nbits=2, mean_len=64, k=10,
+                 desc="synthetic 10k-passage index (~64 tok/passage, dim 128, 4096 centroids, nbits=2), k=10"),
+    "cfg2": dict(N=8_800_000, K=1 << 18, nbits=2, mean_len=68, k=1000,
+                 desc="synthetic MS MARCO v1-scale: 8.8M passages (~600M embeddings), 2^18 centroids, "
+                      "nbits=2, k=1000, single-query latency"),
+    "cfg3": dict(N=8_800_000, K=1 << 18, nbits=1, mean_len=68, k=100,
+                 desc="same MS MARCO-scale index, nbits=1, k=100"),
+    "cfg4": dict(N=2_400_000, K=1 << 16, nbits=2, mean_len=136, k=10,
+                 desc="synthetic LoTTE-pooled-scale: 2.4M passages, 2^16 centroids, nbits=2, k=10, ndocs=256"),
+    "small": dict(N=200_000, K=1 << 14, nbits=2, mean_len=68, k=1000, desc="smoke-size index"),
+}
+METRIC = "queries/sec @k=1000 & p50 latency vs HBM/tensor roofline, 1/2/4/8 B200"
+QLEN, DIM = 32, 128
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_index(cfg: dict, rank: int, seed: int = 0):
+    import paper_2205_09707_b200 as P
+
+    t = time.time()
+    h = P.generate_index(cfg["N"], cfg["K"], dim=DIM, nbits=cfg["nbits"], mean_len=cfg["mean_len"],
+                         spread=16, seed=seed, pid_base=rank * cfg["N"])
+    log(f"[rank {rank}] generated shard: N={h.num_passages} T={h.num_embeddings} P={len(h.ivf_postings)} "
+        f"({h.nbytes() / 1e9:.1f} GB) in {time.time() - t:.1f}s")
+    return h
+
+
+def params_for(cfg: dict):
+    import paper_2205_09707_b200 as P
+
+    p = P.default_params_for_k(cfg["k"])
+    if "ndocs" in cfg:
+        p.ndocs = cfg["ndocs"]
+    return p
+
+
+def cpu_reference_run(h, qs, params, steps, warmup, threads):
+    """Latency mode: sequential lir::search, threads = all host cores."""
+    import oracle
+
+    ref = oracle.get("ref")
+    t = time.time()
+    ref.ref_handle(h)
+    log(f"reference index built in {time.time() - t:.1f}s")
+    nq = qs.shape[0]
+    for i in range(warmup):
+        ref.search(h, qs[i % nq], params, threads=threads)
+    lat = []
+    for i in range(steps):
+        t0 = time.perf_counter()
+        ref.search(h, qs[(warmup + i) % nq], params, threads=threads)
+        lat.append(time.perf_counter() - t0)
+    ref.release(h)
+    return lat
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    if not oracle.available("ref"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liblir_ref.so not built"}))
+        return
+    import paper_2205_09707_b200 as P
+
+    h = make_index(cfg, 0)
+    qs = P.generate_queries(h, max(args.steps + args.warmup, 1), qlen=QLEN, seed=1234)
+    params = params_for(cfg)
+    threads = os.cpu_count() or 1
+    lat = cpu_reference_run(h, qs, params, args.steps, args.warmup, threads)
+    total = sum(lat)
+    qps = args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "p50_ms": 1e3 * statistics.median(lat), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 generator, SURVEY.md §8d)",
+        "config": config_block(cfg, params, args, 1),
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} sequential queries, lir::search latency mode, "
+                                   f"SearchOptions.threads={threads}"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def config_block(cfg, params, args, world):
+    return {"workload": f"{args.config}: {cfg['desc']}", "passages_per_gpu": cfg["N"],
+            "passages_total": cfg["N"] * world, "centroids": cfg["K"], "nbits": cfg["nbits"], "dim": DIM,
+            "query_tokens": QLEN, "k": params.k, "nprobe": params.nprobe, "t_cs": params.t_cs,
+            "ndocs": params.ndocs, "batch": 1, "l2_flush": "256 MiB write before every step (untimed)",
+            "score_mode": args.score_mode, "parallelism": f"passage-range shards x{world}"}
+
+
+def run_plaid(args, cfg):
+    import torch
+
+    import paper_2205_09707_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    h = make_index(cfg, rank)
+    params = params_for(cfg)
+    nq = max(args.steps + args.warmup, 8)
+    # queries: generated from shard 0's passages, identical on every rank
+    if rank == 0:
+        qs = P.generate_queries(h, nq, qlen=QLEN, seed=1234)
+    else:
+        qs = np.zeros((nq, QLEN, DIM), dtype=np.float32)
+    dq = torch.from_numpy(qs).cuda()
+    if dist is not None:
+        dist.broadcast(dq, 0)
+        qs = dq.cpu().numpy()
+
+    t = time.time()
+    idx = P.DeviceIndex.from_host_at(h, pid_base=rank * cfg["N"], device=local)
+    log(f"[rank {rank}] index resident on cuda:{local}: {idx.device_bytes / 1e9:.1f} GB in {time.time() - t:.1f}s")
+    mode = P.ScoreMode.EXACT if args.score_mode == "exact" else P.ScoreMode.TENSOR
+    s = P.Searcher(idx, device=local, score_mode=mode, record_times=True)
+
+    k = params.k
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    d_pids = torch.zeros(k, dtype=torch.int32, device="cuda")
+    d_scores = torch.zeros(k, dtype=torch.float32, device="cuda")
+    d_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if world > 1:
+        g_pids = torch.zeros(world, k, dtype=torch.int32, device="cuda")
+        g_scores = torch.zeros(world, k, dtype=torch.float32, device="cuda")
+        g_n = torch.zeros(world, dtype=torch.int64, device="cuda")
+        m_pids = torch.zeros(k, dtype=torch.int32, device="cuda")
+        m_scores = torch.zeros(k, dtype=torch.float32, device="cuda")
+        m_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(i):
+        q = dq[i % nq]
+        s.search_device(q.data_ptr(), 1, QLEN, DIM, params, d_pids.data_ptr(), d_scores.data_ptr(),
+                        d_n.data_ptr(), stream=sh)
+        if world > 1:
+            dist.all_gather_into_tensor(g_pids.view(-1), d_pids)
+            dist.all_gather_into_tensor(g_scores.view(-1), d_scores)
+            dist.all_gather_into_tensor(g_n, d_n)
+            s.merge_topk_device(g_pids.data_ptr(), g_scores.data_ptr(), g_n.data_ptr(), world, k, k,
+                                m_pids.data_ptr(), m_scores.data_ptr(), m_n.data_ptr(), stream=sh)
+
+    for i in range(args.warmup):
+        flush.zero_()
+        step(i)
+    torch.cuda.synchronize()
+    s.sync()
+
+    phases = {n: [] for n in P.Searcher.PHASES}
+    launches = 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step(args.warmup + i)
+        ev[i][1].record(stream)
+        ev[i][1].synchronize()
+        for n, v in s.phase_ms().items():
+            phases[n].append(v)
+        launches += s.last_launches()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    s.sync()
+    step_ms = torch.tensor([a.elapsed_time(b) for a, b in ev], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    step_ms = step_ms.cpu().numpy()
+    total_s = float(step_ms.sum()) / 1e3
+    value = args.steps / total_s
+
+    # ---- end to end through the C ABI with host buffers (H2D of Q, D2H of top-k inside)
+    e2e_lat = []
+    if world == 1:
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = s.search(qs[(args.warmup + i) % nq], params)
+            e2e_lat.append(time.perf_counter() - t0)
+        trace = r.trace
+    else:
+        hq = torch.from_numpy(qs).pin_memory()
+        hp = torch.zeros(k, dtype=torch.int32).pin_memory()
+        hs = torch.zeros(k, dtype=torch.float32).pin_memory()
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            dq[0].copy_(hq[(args.warmup + i) % nq], non_blocking=True)
+            step(0)
+            hp.copy_(m_pids, non_blocking=True)
+            hs.copy_(m_scores, non_blocking=True)
+            torch.cuda.synchronize()
+            e2e_lat.append(time.perf_counter() - t0)
+        trace = None
+        lat_t = torch.tensor(e2e_lat, dtype=torch.float64, device="cuda")
+        dist.all_reduce(lat_t, op=dist.ReduceOp.MAX)
+        e2e_lat = lat_t.cpu().tolist()
+    e2e_value = args.steps / sum(e2e_lat)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (largest mean phase)
+    hbm_peak, tf_peak, peak_kind = measured_peaks()
+    mean_ph = {n: float(np.mean(v)) for n, v in phases.items()}
+    dom = max(mean_ph, key=mean_ph.get)
+    K = cfg["K"]
+    tr = trace.counters() if trace is not None else {}
+    alg_bytes = {
+        # C read once + S written once + row max; keep bits/top lists are negligible
+        "scores": 512 * K + 128 * K + 4 * K,
+        "stage4_rank": None,
+        "stage2_interaction": None,
+    }
+    ab = alg_bytes.get(dom)
+    roof = None
+    if ab:
+        ach = ab / (mean_ph[dom] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                "algorithmic_bytes": ab, "mean_ms": mean_ph[dom]}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": hbm_peak, "unit": "GB/s",
+                "frac": None, "traffic": None, "peak_kind": peak_kind, "mean_ms": mean_ph[dom]}
+
+    # ---- CPU baseline: the reference's own searcher on this host, bounded sample
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            per_q = 0.5 if cfg["N"] > 1_000_000 else 0.02
+            nsample = max(3, min(64, int(args.cpu_seconds / per_q)))
+            lat = cpu_reference_run(h, qs, params, nsample, 1, threads)
+            cpu = {"value": nsample / sum(lat), "unit": "queries/s", "cores": threads, "kind": "reference",
+                   "sample": f"{nsample} sequential queries of the same workload, lir::search latency mode, "
+                             f"SearchOptions.threads={threads}", "p50_ms": 1e3 * statistics.median(lat)}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
+        "p50_ms": float(np.median(step_ms)), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 generator, SURVEY.md §8d)",
+        "config": config_block(cfg, params, args, world),
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": QLEN * DIM * 4,
+                "d2h_bytes_per_step": k * 8 + 128, "p50_ms": 1e3 * statistics.median(e2e_lat)},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "phases_ms": mean_ph,
+        "trace": tr,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="plaid", choices=["plaid", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--score-mode", default="exact", choices=["exact", "tensor"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_plaid(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

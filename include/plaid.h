@@ -132,6 +132,10 @@ uint64_t plaid_stage3_width(const plaid_params* p);
  * index.cpp:7-10).  validate != 0 runs validate_index's invariants (index.cpp:12-84). */
 plaid_status plaid_index_from_host(const plaid_index_desc* desc, int device, int validate,
                                    plaid_index** out);
+/* Same, for a desc that already is one passage-range shard of a larger index
+ * (local ids, local IVF): results report local id + pid_base. */
+plaid_status plaid_index_from_host_at(const plaid_index_desc* desc, uint64_t pid_base, int device,
+                                      plaid_index** out);
 /* Passage-range shard [pid_begin, pid_end) of a host index: local IVF with
  * local ids; search results report global ids (local + pid_begin). */
 plaid_status plaid_index_from_host_shard(const plaid_index_desc* desc, uint64_t pid_begin,
@@ -169,6 +173,11 @@ plaid_status plaid_search_device(plaid_searcher* s, const float* d_q, uint64_t n
 plaid_status plaid_searcher_sync(plaid_searcher* s);
 /* Number of kernels the last search enqueued (for the bench's gpu_launches). */
 uint64_t plaid_searcher_last_launches(const plaid_searcher* s);
+/* CUDA-event durations (ms) of the last enqueued query's phases, measured on
+ * the launching stream (record_times must be set): [0] S_cq kernel,
+ * [1] top-nprobe + candidate generation, [2] stage-2 interaction, [3] stage-2
+ * select, [4] stage 3, [5] stage-4 decompress+MaxSim kernel, [6] final top-k. */
+plaid_status plaid_searcher_phase_ms(plaid_searcher* s, double out[7]);
 
 /* Merge G per-shard top-k lists (score desc, pid asc) into the global top-k —
  * the final select after the NCCL all-gather. Host arrays. */

@@ -55,7 +55,8 @@ SIGNATURES = {
     "plaid_default_params_for_k": (None, [C.c_uint64, C.POINTER(Params)]),
     "plaid_stage3_width": (C.c_uint64, [C.POINTER(Params)]),
     "plaid_index_from_host": (C.c_int, [C.POINTER(IndexDesc), C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
-    "plaid_index_from_host_shard": (C.c_int, [C.POINTER(IndexDesc), C.c_uint64, C.c_uint64, C.c_int,
+    "plaid_index_from_host_at": (C.c_int, [C.POINTER(IndexDesc), C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]),
+    "plaid_index_from_host_shard":(C.c_int, [C.POINTER(IndexDesc), C.c_uint64, C.c_uint64, C.c_int,
                                               C.POINTER(C.c_void_p)]),
     "plaid_index_validate": (C.c_int, [C.c_void_p]),
     "plaid_index_close": (None, [C.c_void_p]),
@@ -70,6 +71,7 @@ SIGNATURES = {
                                       C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     "plaid_searcher_sync": (C.c_int, [C.c_void_p]),
     "plaid_searcher_last_launches": (C.c_uint64, [C.c_void_p]),
+    "plaid_searcher_phase_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "plaid_merge_topk": (C.c_int, [C.c_void_p, u32p, f32p, u64p, C.c_uint64, C.c_uint64, C.c_uint64,
                                    u32p, f32p, u64p]),
     "plaid_merge_topk_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,

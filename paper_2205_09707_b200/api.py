@@ -190,6 +190,14 @@ class DeviceIndex:
         return cls(out.value)
 
     @classmethod
+    def from_host_at(cls, h: HostIndex, pid_base: int, device: int = 0) -> "DeviceIndex":
+        """`h` is already the shard [pid_base, pid_base + N) with local ids."""
+        out = C.c_void_p()
+        d = _desc(h)
+        _check(N.load().plaid_index_from_host_at(C.byref(d), int(pid_base), device, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
     def shard(cls, h: HostIndex, pid_begin: int, pid_end: int, device: int = 0) -> "DeviceIndex":
         out = C.c_void_p()
         d = _desc(h)
@@ -269,11 +277,26 @@ class Searcher:
         _check(N.load().plaid_search_device(self._h, d_q, nq, rows, dim, C.byref(p), d_pids, d_scores, d_n,
                                             stream))
 
+    def merge_topk_device(self, d_pids: int, d_scores: int, d_counts: int, shards: int, stride: int, k: int,
+                          d_out_pids: int, d_out_scores: int, d_out_n: int, stream: int = 0) -> None:
+        """Device-side final select over G gathered shard lists."""
+        _check(N.load().plaid_merge_topk_device(self._h, d_pids, d_scores, d_counts, shards, stride, k,
+                                                d_out_pids, d_out_scores, d_out_n, stream))
+
     def sync(self) -> None:
         _check(N.load().plaid_searcher_sync(self._h))
 
     def last_launches(self) -> int:
         return int(N.load().plaid_searcher_last_launches(self._h))
+
+    PHASES = ("scores", "candidates", "stage2_interaction", "stage2_select", "stage3", "stage4_rank",
+              "final_select")
+
+    def phase_ms(self) -> dict:
+        """CUDA-event phase durations of the last enqueued query (record_times)."""
+        out = (C.c_double * 7)()
+        _check(N.load().plaid_searcher_phase_ms(self._h, out))
+        return dict(zip(self.PHASES, list(out)))
 
     # ---- per-stage functions (pipeline.hpp:55-90)
     def compute_centroid_scores(self, q: np.ndarray):

@@ -120,6 +120,25 @@ plaid_status plaid_index_from_host(const plaid_index_desc* desc, int device, int
     });
 }
 
+plaid_status plaid_index_from_host_at(const plaid_index_desc* desc, uint64_t pid_base, int device,
+                                      plaid_index** out) {
+    return guarded([&] {
+        need(desc, "desc");
+        need(out, "out");
+        *out = nullptr;
+        if (pid_base + desc->num_passages > 0xFFFFFFFFull)
+            plaid::fail(PLAID_INVALID_PARAMS, "global passage ids must fit in 32 bits");
+        auto* h = new plaid_index();
+        try {
+            h->impl = std::make_unique<plaid::DeviceIndex>(*desc, device, pid_base);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
 // Passage-range shard: [pid_begin, pid_end) with a local IVF (postings rebased
 // to local ids; each centroid's slice is a contiguous run of its sorted list).
 plaid_status plaid_index_from_host_shard(const plaid_index_desc* desc, uint64_t pid_begin,
@@ -250,6 +269,13 @@ plaid_status plaid_searcher_sync(plaid_searcher* s) {
 }
 
 uint64_t plaid_searcher_last_launches(const plaid_searcher* s) { return s->impl->last_launches(); }
+
+plaid_status plaid_searcher_phase_ms(plaid_searcher* s, double out[7]) {
+    return guarded([&] {
+        need(s, "searcher");
+        s->impl->phase_ms(out);
+    });
+}
 
 plaid_status plaid_merge_topk(plaid_searcher* s, const uint32_t* pids, const float* scores,
                               const uint64_t* counts, uint64_t shards, uint64_t stride, uint64_t k,

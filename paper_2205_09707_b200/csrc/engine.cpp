@@ -18,7 +18,16 @@ thread_local uint64_t g_launches = 0;
 }
 uint64_t launches() { return g_launches; }
 void reset_launches() { g_launches = 0; }
-void count_launch() { ++g_launches; }
+// Every launcher calls this right after its <<<>>>: a failed launch (bad
+// config, missing smem opt-in) surfaces here instead of as stale results.
+void count_launch() {
+    ++g_launches;
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(PLAID_CUDA_ERROR, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+    }
+}
 }  // namespace launch
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -377,6 +386,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
     const uint32_t warps = launch::scores_exact(ix, d_q, rows, p.t_cs, scores_.p, rowmax_.p, keep_.p,
                                                 partial_.p, npb, st);
+    record(1, st, times);
     uint64_t nsel;
     if (p.nprobe == K) {
         launch::iota(sel_.p, K, st);
@@ -395,7 +405,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     }
     launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap_.p, st);
     launch::bitmap_compact(bitmap_.p, N, chunk_counts_.p, c1_.p, c + kN1, st);
-    record(1, st, times);
+    record(2, st, times);
 
     const uint64_t want_final = p.k;
     const uint64_t* fin_keys = nullptr;
@@ -409,22 +419,24 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         fin_ids = c1_.p;
         fin_n = c + kN1;
         fin_max = N;
-        record(2, st, times);
         record(3, st, times);
+        record(4, st, times);
+        record(5, st, times);
     } else {
         // Stage 2: pruned centroid interaction over C1, keep ndocs.
         const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
         launch::centroid_interaction(ix, scores_.p, rows, c1_.p, nullptr, c + kN1, N, keep_.p, keys2_.p,
                                      nullptr, reinterpret_cast<unsigned long long*>(c + kRows2), st);
+        record(3, st, times);
         launch::select_top_large(keys2_.p, c + kN1, N, p.ndocs, sel_state_.p, sel2_.p, c + kN2, st);
-        record(2, st, times);
+        record(4, st, times);
         // Stage 3: full centroid interaction, keep max(ceil(ndocs/4), k).
         const uint64_t n3 = std::min<uint64_t>(stage3_width(p), N);
         launch::centroid_interaction(ix, scores_.p, rows, nullptr, sel2_.p, c + kN2, nd, nullptr,
                                      keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
         launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
                          sort_tmp_.p, st);
-        record(3, st, times);
+        record(5, st, times);
         fin_keys = sel3_.p;
         fin_n = c + kN3;
         fin_max = n3;
@@ -432,6 +444,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     // Stage 4: decompress + exact MaxSim, top-k.
     launch::copy_count(fin_n, c + kNFin, ~0ull, st);
     launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, st);
+    record(6, st, times);
     const uint32_t base = uint32_t(index_->pid_base());
     if (fin_max <= launch::kSmallSortMax) {
         launch::sort_top(keys4_.p, fin_n, fin_max, want_final, nullptr, d_pids, d_scores, d_n, base,
@@ -444,7 +457,20 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
                          sort_tmp_.p, st);
     }
     launch::copy_count(d_n, c + kNOut, ~0ull, st);
-    record(4, st, times);
+    record(7, st, times);
+}
+
+// Phase durations of the last enqueued query (record_times): K1, candidate
+// generation, stage-2 interaction, stage-2 select, stage 3, stage-4 kernel,
+// final select.
+void Searcher::phase_ms(double* out) {
+    DeviceGuard g(device_);
+    PLAID_CUDA(cudaEventSynchronize(ev_[7]));
+    for (int i = 0; i < 7; ++i) {
+        float ms = 0;
+        PLAID_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+        out[i] = ms;
+    }
 }
 
 void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_params& p,
@@ -486,17 +512,15 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
             trace->decompressed_passages = h_counters_[kNFin];
         }
         if (times) {
-            float ms[4];
-            for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], ev_[i], ev_[i + 1]);
-            trace->candidate_generation_ms = ms[0];
-            trace->stage2_ms = ms[1];
-            trace->stage3_ms = ms[2];
-            trace->lookup_ms = 0.0;         // fused into the stage-4 kernel
-            trace->decompression_ms = 0.0;  // fused into the stage-4 kernel
-            trace->scoring_ms = ms[3];
-            float tot = 0;
-            cudaEventElapsedTime(&tot, ev_[0], ev_[4]);
-            trace->total_ms = tot;
+            double ms[7];
+            phase_ms(ms);
+            trace->candidate_generation_ms = ms[0] + ms[1];
+            trace->stage2_ms = ms[2] + ms[3];
+            trace->stage3_ms = ms[4];
+            trace->lookup_ms = 0.0;  // fused into the stage-4 kernel
+            trace->decompression_ms = ms[5];  // fused decompress + MaxSim kernel
+            trace->scoring_ms = ms[6];        // final top-k select
+            trace->total_ms = ms[0] + ms[1] + ms[2] + ms[3] + ms[4] + ms[5] + ms[6];
         }
     }
 }
@@ -517,7 +541,8 @@ void Searcher::search_device(const float* d_q, uint64_t nq, uint64_t rows, uint6
     for (uint64_t j = 0; j < nq; ++j) {
         const float* q = d_q + j * rows * dim;
         launch::validate_query(q, uint32_t(rows), uint32_t(dim), status_.p, st);
-        enqueue(q, uint32_t(rows), p, d_pids + j * p.k, d_scores + j * p.k, d_n + j, st, false);
+        enqueue(q, uint32_t(rows), p, d_pids + j * p.k, d_scores + j * p.k, d_n + j, st,
+                cfg_.record_times != 0);
     }
     PLAID_CUDA(cudaGetLastError());
     last_launches_ = launch::launches();

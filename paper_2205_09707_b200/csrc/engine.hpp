@@ -96,6 +96,7 @@ public:
                        cudaStream_t st);
     void sync();
     uint64_t last_launches() const { return last_launches_; }
+    void phase_ms(double* out);
 
     // Per-stage entry points (host buffers).
     void compute_centroid_scores(const float* q, uint64_t rows, uint64_t dim, float* scores,

@@ -232,8 +232,13 @@ template <int NP>
 void launch_merge(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint32_t nprobe,
                   uint32_t* sel, cudaStream_t st) {
     const uint32_t threads = 256;
-    topn_merge_kernel<NP><<<rows, threads, threads * NP * sizeof(uint64_t), st>>>(partial, nwarps,
-                                                                                 nprobe, sel);
+    const size_t smem = threads * NP * sizeof(uint64_t);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(topn_merge_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = true;
+    }
+    topn_merge_kernel<NP><<<rows, threads, smem, st>>>(partial, nwarps, nprobe, sel);
     launch::count_launch();
 }
 

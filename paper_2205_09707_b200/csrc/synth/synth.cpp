@@ -110,11 +110,13 @@ void synth_centroids(uint64_t K, uint32_t dim, uint64_t seed, float* out, int th
     });
 }
 
-void synth_doclens(uint64_t N, uint32_t min_len, uint32_t max_len, uint64_t seed, uint32_t* out,
-                   int threads) {
+// Streams are keyed by the GLOBAL passage id (pid_base + p), so a passage-range
+// shard generated on its own is byte-identical to the same range of the full index.
+void synth_doclens(uint64_t N, uint64_t pid_base, uint32_t min_len, uint32_t max_len, uint64_t seed,
+                   uint32_t* out, int threads) {
     parallel_range(N, threads, [&](uint64_t b, uint64_t e, unsigned) {
         for (uint64_t p = b; p < e; ++p) {
-            Rng r(stream_seed(seed, p));
+            Rng r(stream_seed(seed, pid_base + p));
             out[p] = min_len + uint32_t(r.below(uint64_t(max_len - min_len) + 1));
         }
     });
@@ -127,11 +129,11 @@ uint64_t synth_offsets(const uint32_t* doclens, uint64_t N, uint64_t* offsets) {
     return offsets[N];
 }
 
-void synth_codes(const uint32_t* doclens, const uint64_t* offsets, uint64_t N, uint64_t K,
-                 double repeat_prob, uint64_t seed, uint32_t* codes, int threads) {
+void synth_codes(const uint32_t* doclens, const uint64_t* offsets, uint64_t N, uint64_t pid_base,
+                 uint64_t K, double repeat_prob, uint64_t seed, uint32_t* codes, int threads) {
     parallel_range(N, threads, [&](uint64_t b, uint64_t e, unsigned) {
         for (uint64_t p = b; p < e; ++p) {
-            Rng r(stream_seed(seed, p));
+            Rng r(stream_seed(seed, pid_base + p));
             uint32_t* c = codes + offsets[p];
             for (uint32_t t = 0; t < doclens[p]; ++t) {
                 if (t > 0 && r.unit() < repeat_prob)
@@ -143,15 +145,22 @@ void synth_codes(const uint32_t* doclens, const uint64_t* offsets, uint64_t N, u
     });
 }
 
-void synth_residuals(uint64_t T, uint64_t bytes_per_token, uint64_t seed, uint8_t* out, int threads) {
-    parallel_range(T, threads, [&](uint64_t b, uint64_t e, unsigned) {
-        for (uint64_t t = b; t < e; ++t) {
-            Rng r(stream_seed(seed, t));
-            uint8_t* o = out + t * bytes_per_token;
-            for (uint64_t i = 0; i < bytes_per_token; i += 8) {
-                uint64_t v = r.next();
-                uint64_t n = std::min<uint64_t>(8, bytes_per_token - i);
-                for (uint64_t j = 0; j < n; ++j) o[i + j] = uint8_t(v >> (8 * j));
+// One stream per passage covers all of its tokens' packed residual bytes.
+void synth_residuals(const uint64_t* offsets, uint64_t N, uint64_t pid_base, uint64_t bytes_per_token,
+                     uint64_t seed, uint8_t* out, int threads) {
+    parallel_range(N, threads, [&](uint64_t b, uint64_t e, unsigned) {
+        for (uint64_t p = b; p < e; ++p) {
+            Rng r(stream_seed(seed, pid_base + p));
+            uint8_t* o = out + offsets[p] * bytes_per_token;
+            const uint64_t n = (offsets[p + 1] - offsets[p]) * bytes_per_token;
+            uint64_t i = 0;
+            for (; i + 8 <= n; i += 8) {
+                const uint64_t v = r.next();
+                std::memcpy(o + i, &v, 8);  // little-endian host
+            }
+            if (i < n) {
+                const uint64_t v = r.next();
+                for (uint64_t j = 0; i + j < n; ++j) o[i + j] = uint8_t(v >> (8 * j));
             }
         }
     });

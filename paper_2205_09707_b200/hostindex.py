@@ -26,11 +26,11 @@ def _lib():
         _synth = C.CDLL(str(_SYNTH))
         vp, u64, u32, i32, dbl = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_double
         _synth.synth_centroids.argtypes = [u64, u32, u64, vp, i32]
-        _synth.synth_doclens.argtypes = [u64, u32, u32, u64, vp, i32]
+        _synth.synth_doclens.argtypes = [u64, u64, u32, u32, u64, vp, i32]
         _synth.synth_offsets.argtypes = [vp, u64, vp]
         _synth.synth_offsets.restype = u64
-        _synth.synth_codes.argtypes = [vp, vp, u64, u64, dbl, u64, vp, i32]
-        _synth.synth_residuals.argtypes = [u64, u64, u64, vp, i32]
+        _synth.synth_codes.argtypes = [vp, vp, u64, u64, u64, dbl, u64, vp, i32]
+        _synth.synth_residuals.argtypes = [vp, u64, u64, u64, u64, vp, i32]
         _synth.synth_ivf_count.argtypes = [vp, vp, u64, u64, vp, i32]
         _synth.synth_ivf_count.restype = vp
         _synth.synth_ivf_fill.argtypes = [vp, vp, vp, vp, vp]
@@ -135,25 +135,28 @@ def quantizer(nbits: int) -> tuple[np.ndarray, np.ndarray]:
 
 def generate_index(num_passages: int, num_centroids: int, dim: int = 128, nbits: int = 2,
                    mean_len: int = 64, spread: int = 16, repeat: float = 0.28, seed: int = 0,
-                   threads: int = 0) -> HostIndex:
+                   threads: int = 0, pid_base: int = 0) -> HostIndex:
     """Synthetic index per SURVEY.md §8d: doclens uniform in [mean-spread,
     mean+spread], codes with a `repeat` chance of re-using an earlier code of
     the same passage (~0.72 postings/token), uniform residual bytes, and the
-    fixed quantizer.  Fully determined by the arguments."""
+    fixed quantizer.  Fully determined by the arguments.  With pid_base > 0 the
+    result is the passage range [pid_base, pid_base + num_passages) of the
+    larger index with the same parameters (every stream is keyed by global
+    passage id); its IVF is local to the range, with local ids."""
     lib = _lib()
     N, K = int(num_passages), int(num_centroids)
     cents = np.empty((K, dim), dtype=np.float32)
     lib.synth_centroids(K, dim, 11 + seed, _p(cents), threads)
     lo, hi = max(1, mean_len - spread), mean_len + spread
     doclens = np.empty(N, dtype=np.uint32)
-    lib.synth_doclens(N, lo, hi, 5 + seed, _p(doclens), threads)
+    lib.synth_doclens(N, pid_base, lo, hi, 5 + seed, _p(doclens), threads)
     off = np.empty(N + 1, dtype=np.uint64)
     T = lib.synth_offsets(_p(doclens), N, _p(off))
     codes = np.empty(T, dtype=np.uint32)
-    lib.synth_codes(_p(doclens), _p(off), N, K, float(repeat), 99 + seed, _p(codes), threads)
+    lib.synth_codes(_p(doclens), _p(off), N, pid_base, K, float(repeat), 99 + seed, _p(codes), threads)
     bpt = nbits * dim // 8
     res = np.empty(T * bpt, dtype=np.uint8)
-    lib.synth_residuals(T, bpt, 7 + seed, _p(res), threads)
+    lib.synth_residuals(_p(off), N, pid_base, bpt, 7 + seed, _p(res), threads)
     ivf_off = np.zeros(K + 1, dtype=np.uint64)
     st = lib.synth_ivf_count(_p(codes), _p(off), N, K, _p(ivf_off), threads)
     post = np.empty(int(ivf_off[-1]), dtype=np.uint32)
