@@ -234,7 +234,10 @@ def run_plaid(args, cfg):
     s = P.Searcher(idx, device=local, score_mode=mode, record_times=True)
 
     k = params.k
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the kernels, the L2 flush and the timing
+    # events all go to it, so CUDA events bracket exactly the enqueued search
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
     d_pids = torch.zeros(k, dtype=torch.int32, device="cuda")
     d_scores = torch.zeros(k, dtype=torch.float32, device="cuda")
