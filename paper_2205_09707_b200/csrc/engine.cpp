@@ -294,8 +294,12 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
     DeviceGuard g(device_);
     PLAID_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     for (auto& e : ev_) PLAID_CUDA(cudaEventCreate(&e));
-    counters_.ensure(kNumCounters);
-    PLAID_CUDA(cudaMemset(counters_.p, 0, kNumCounters * sizeof(uint64_t)));
+    const uint64_t words = index_ ? (index_->view().N + 31) / 32 : 0;
+    zero_.ensure(2 * kNumCounters + 2 * words);
+    PLAID_CUDA(cudaMemset(zero_.p, 0, zero_.n * sizeof(uint32_t)));
+    counters_.p = reinterpret_cast<uint64_t*>(zero_.p);
+    bitmap_.p = zero_.p + 2 * kNumCounters;
+    kconst_.ensure(1);
     status_.ensure(1);
     PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
     sel_state_.ensure(1);
@@ -309,13 +313,12 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         keep_.ensure((ix.K + 31) / 32);
         npartial_warps_ = launch::scores_max_warps();
         partial_.ensure(npartial_warps_ * 32 * 32);
-        bitmap_.ensure((ix.N + 31) / 32);
         chunk_counts_.ensure(launch::bitmap_chunks(ix.N));
         c1_.ensure(ix.N);
         keys2_.ensure(ix.N);
         keys4_.ensure(ix.N);
         const uint64_t K = ix.K;
-        PLAID_CUDA(cudaMemcpy(counters_.p + kKConst, &K, sizeof K, cudaMemcpyHostToDevice));
+        PLAID_CUDA(cudaMemcpy(kconst_.p, &K, sizeof K, cudaMemcpyHostToDevice));
     }
 }
 
@@ -378,9 +381,12 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     const IndexView& ix = index_->view();
     const uint64_t K = ix.K, N = ix.N;
     uint64_t* c = counters_.p;
+    uint32_t* bitmap = bitmap_.p;
+    uint32_t* owners = bitmap_.p + (N + 31) / 32;
     record(0, st, times);
-    PLAID_CUDA(cudaMemsetAsync(c, 0, kKConst * sizeof(uint64_t), st));
-    PLAID_CUDA(cudaMemsetAsync(bitmap_.p, 0, ((N + 31) / 32) * sizeof(uint32_t), st));
+    // one memset clears the per-query counters, the candidate bitmap and the
+    // kept-owner bitmap (contiguous in zero_)
+    PLAID_CUDA(cudaMemsetAsync(zero_.p, 0, zero_.n * sizeof(uint32_t), st));
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
@@ -397,14 +403,14 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     } else {
         for (uint32_t i = 0; i < rows; ++i) {
             launch::token_keys(scores_.p, K, i, tok_keys_.p, st);
-            launch::select_top_large(tok_keys_.p, c + kKConst, K, p.nprobe, sel_state_.p,
+            launch::select_top_large(tok_keys_.p, kconst_.p, K, p.nprobe, sel_state_.p,
                                      tmp_keys_.p, c + kTmpN, st);
             launch::keys_to_ids(tmp_keys_.p, c + kTmpN, p.nprobe, sel_.p + uint64_t(i) * p.nprobe, st);
         }
         nsel = uint64_t(rows) * p.nprobe;
     }
-    launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap_.p, st);
-    launch::bitmap_compact(bitmap_.p, N, chunk_counts_.p, c1_.p, c + kN1, st);
+    launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap, st);
+    launch::bitmap_compact(bitmap, N, chunk_counts_.p, c1_.p, c + kN1, st);
     record(2, st, times);
 
     const uint64_t want_final = p.k;
@@ -414,8 +420,6 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     uint64_t fin_max = 0;
     if (p.disable_filter) {
         // pipeline.cpp:255-258: every stage-1 candidate goes to stage 4
-        launch::copy_count(c + kN1, c + kN2, ~0ull, st);
-        launch::copy_count(c + kN1, c + kN3, ~0ull, st);
         fin_ids = c1_.p;
         fin_n = c + kN1;
         fin_max = N;
@@ -423,16 +427,18 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         record(4, st, times);
         record(5, st, times);
     } else {
-        // Stage 2: pruned centroid interaction over C1, keep ndocs.
+        // Stage 2: pruned centroid interaction over C1, keep ndocs.  Only the
+        // candidates owning a kept token are read (see kept_owners).
         const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
-        launch::centroid_interaction(ix, scores_.p, rows, c1_.p, nullptr, c + kN1, N, keep_.p, keys2_.p,
-                                     nullptr, reinterpret_cast<unsigned long long*>(c + kRows2), st);
+        launch::kept_owners(ix, keep_.p, owners, st);
+        launch::centroid_interaction(ix, scores_.p, rows, c1_.p, nullptr, c + kN1, N, keep_.p, owners,
+                                     keys2_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows2), st);
         record(3, st, times);
         launch::select_top_large(keys2_.p, c + kN1, N, p.ndocs, sel_state_.p, sel2_.p, c + kN2, st);
         record(4, st, times);
         // Stage 3: full centroid interaction, keep max(ceil(ndocs/4), k).
         const uint64_t n3 = std::min<uint64_t>(stage3_width(p), N);
-        launch::centroid_interaction(ix, scores_.p, rows, nullptr, sel2_.p, c + kN2, nd, nullptr,
+        launch::centroid_interaction(ix, scores_.p, rows, nullptr, sel2_.p, c + kN2, nd, nullptr, nullptr,
                                      keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
         launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
                          sort_tmp_.p, st);
@@ -442,7 +448,6 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         fin_max = n3;
     }
     // Stage 4: decompress + exact MaxSim, top-k.
-    launch::copy_count(fin_n, c + kNFin, ~0ull, st);
     launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, st);
     record(6, st, times);
     const uint32_t base = uint32_t(index_->pid_base());
@@ -456,7 +461,6 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         launch::sort_top(tmp_keys_.p, c + kTmpN, m, want_final, nullptr, d_pids, d_scores, d_n, base,
                          sort_tmp_.p, st);
     }
-    launch::copy_count(d_n, c + kNOut, ~0ull, st);
     record(7, st, times);
 }
 
@@ -504,12 +508,13 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
         trace->stage1_candidates = h_counters_[kN1];
         trace->centroid_matmul_count = 1;
         if (h_counters_[kN1] > 0) {  // pipeline.cpp:249-252: empty C1 returns early
-            trace->stage2_out = h_counters_[kN2];
-            trace->stage3_out = h_counters_[kN3];
+            const bool df = p.disable_filter != 0;  // pipeline.cpp:255-258
+            trace->stage2_out = df ? h_counters_[kN1] : h_counters_[kN2];
+            trace->stage3_out = df ? h_counters_[kN1] : h_counters_[kN3];
             trace->final_out = n;
             trace->stage2_rows_gathered = h_counters_[kRows2];
             trace->stage3_rows_gathered = h_counters_[kRows3];
-            trace->decompressed_passages = h_counters_[kNFin];
+            trace->decompressed_passages = trace->stage3_out;
         }
         if (times) {
             double ms[7];
@@ -620,7 +625,7 @@ void Searcher::generate_candidates(const float* scores, uint64_t rows, uint64_t 
     } else {
         for (uint32_t i = 0; i < rows; ++i) {
             launch::token_keys(scores_.p, ix.K, i, tok_keys_.p, stream_);
-            launch::select_top_large(tok_keys_.p, c + kKConst, ix.K, nprobe, sel_state_.p, tmp_keys_.p,
+            launch::select_top_large(tok_keys_.p, kconst_.p, ix.K, nprobe, sel_state_.p, tmp_keys_.p,
                                      c + kTmpN, stream_);
             launch::keys_to_ids(tmp_keys_.p, c + kTmpN, nprobe, sel_.p + uint64_t(i) * nprobe, stream_);
         }
@@ -663,8 +668,14 @@ void Searcher::centroid_interaction(const float* scores, uint64_t rows, const ui
     keys.ensure(n);
     DevBuf<float> sc;
     sc.ensure(n);
+    uint32_t* owners = nullptr;
+    if (mask) {  // same owner filter as the pipeline's stage 2
+        owners = bitmap_.p + (ix.N + 31) / 32;
+        PLAID_CUDA(cudaMemsetAsync(owners, 0, ((ix.N + 31) / 32) * sizeof(uint32_t), stream_));
+        launch::kept_owners(ix, keep_.p, owners, stream_);
+    }
     launch::centroid_interaction(ix, scores_.p, uint32_t(rows), ids_tmp_.p, nullptr, c + kEntryN, n,
-                                 mask ? keep_.p : nullptr, keys.p, sc.p,
+                                 mask ? keep_.p : nullptr, owners, keys.p, sc.p,
                                  reinterpret_cast<unsigned long long*>(c + kRows2), stream_);
     d2h(out_scores, sc.p, n, stream_);
     uint64_t rg = 0;

@@ -139,9 +139,18 @@ private:
 
     // scratch
     DevBuf<float> q_, scores_, rowmax_, out_scores_;
-    DevBuf<uint32_t> keep_, sel_, bitmap_, chunk_counts_, c1_, out_pids_, ids_tmp_;
+    DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, out_pids_, ids_tmp_;
     DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_,
-        counters_, tmp_keys_;
+        tmp_keys_, kconst_;
+    // zero_ = [16 u64 counters | candidate bitmap (N bits) | kept-owner bitmap
+    // (N bits)], cleared by a single memset per query.
+    DevBuf<uint32_t> zero_;
+    template <typename T>
+    struct View {
+        T* p = nullptr;
+    };
+    View<uint64_t> counters_;
+    View<uint32_t> bitmap_;
     DevBuf<unsigned char> bytes_tmp_;
     DevBuf<SelectState> sel_state_;
     DevBuf<int> status_;

@@ -107,8 +107,9 @@ ci_masked_flat_kernel(const uint32_t* __restrict__ codes, const uint64_t* __rest
                       const uint32_t* __restrict__ doclens, const float* __restrict__ S,
                       uint32_t rows, const uint32_t* __restrict__ ids,
                       const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
-                      const uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ out_keys,
-                      float* __restrict__ out_scores, unsigned long long* __restrict__ d_rows) {
+                      const uint32_t* __restrict__ keep_bits, const uint32_t* __restrict__ owners,
+                      uint64_t* __restrict__ out_keys, float* __restrict__ out_scores,
+                      unsigned long long* __restrict__ d_rows) {
     __shared__ uint64_t off_s[kCB];
     __shared__ uint32_t start_s[kCB + 1];
     __shared__ uint32_t acc_s[kCB * kAccPitch];
@@ -128,8 +129,13 @@ ci_masked_flat_kernel(const uint32_t* __restrict__ codes, const uint64_t* __rest
         uint64_t off = 0;
         if (idx < n) {
             pid = cand_id(ids, keys, idx);
-            off = offsets[pid];
-            len = doclens[pid];
+            // A passage that owns no token on a kept centroid (absent from every
+            // kept centroid's posting list) has used == 0 and scores exactly 0
+            // (pipeline.cpp:127-131): its codes need not be read at all.
+            if (!owners || ((__ldg(owners + (pid >> 5)) >> (pid & 31)) & 1u)) {
+                off = offsets[pid];
+                len = doclens[pid];
+            }
         }
         off_s[t] = off;
         // exclusive scan of len over the block
@@ -234,6 +240,36 @@ ci_masked_flat_kernel(const uint32_t* __restrict__ codes, const uint64_t* __rest
     if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
 }
 
+// owners |= postings of every kept centroid: the passages that own at least
+// one token on a kept centroid (IVF content invariant, index.cpp:64-83).  Each
+// warp takes 32 keep-bit words (one per lane) and walks the set bits'
+// posting lists cooperatively.
+__global__ void kept_owners_kernel(const uint32_t* __restrict__ keep_bits, uint64_t K,
+                                   const uint64_t* __restrict__ ivf_offsets,
+                                   const uint32_t* __restrict__ postings, uint32_t* __restrict__ owners) {
+    const uint32_t lane = dev::lane_id();
+    const uint64_t words = (K + 31) / 32;
+    const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t w0 = (uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < words;
+         w0 += nw * 32) {
+        const uint32_t mine = w0 + lane < words ? keep_bits[w0 + lane] : 0u;
+        uint32_t nz = __ballot_sync(0xffffffffu, mine != 0);
+        while (nz) {
+            const int l = __ffs(nz) - 1;
+            nz &= nz - 1;
+            uint32_t bits = __shfl_sync(0xffffffffu, mine, l);
+            while (bits) {
+                const uint64_t c = (w0 + l) * 32 + (__ffs(bits) - 1);
+                bits &= bits - 1;
+                for (uint64_t j = ivf_offsets[c] + lane; j < ivf_offsets[c + 1]; j += 32) {
+                    const uint32_t p = postings[j];
+                    atomicOr(owners + (p >> 5), 1u << (p & 31));
+                }
+            }
+        }
+    }
+}
+
 int sm_count() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -248,17 +284,27 @@ int sm_count() {
 
 namespace launch {
 
+void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_owners, cudaStream_t st) {
+    const uint64_t tasks = ((ix.K + 31) / 32 + 31) / 32;  // one warp per 32 keep words
+    uint64_t blocks = (tasks + 7) / 8;
+    if (blocks == 0) blocks = 1;
+    kept_owners_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_keep_bits, ix.K, ix.ivf_offsets, ix.ivf_postings,
+                                                         d_owners);
+    count_launch();
+}
+
 void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t rows,
                           const uint32_t* d_ids, const uint64_t* d_keys, const uint64_t* d_n,
-                          uint64_t nmax, const uint32_t* d_keep_bits, uint64_t* d_out_keys,
-                          float* d_out_scores, unsigned long long* d_rows, cudaStream_t st) {
+                          uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_owners,
+                          uint64_t* d_out_keys, float* d_out_scores, unsigned long long* d_rows,
+                          cudaStream_t st) {
     if (nmax == 0) return;
     if (d_keep_bits) {
         uint64_t blocks = (nmax + kCB - 1) / kCB;
         const uint64_t cap = uint64_t(sm_count()) * 4;
         if (blocks > cap) blocks = cap;
         ci_masked_flat_kernel<<<uint32_t(blocks), kCB, 0, st>>>(
-            ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_ids, d_keys, d_n, d_keep_bits,
+            ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_ids, d_keys, d_n, d_keep_bits, d_owners,
             d_out_keys, d_out_scores, d_rows);
     } else {
         uint64_t blocks = (nmax + 7) / 8;

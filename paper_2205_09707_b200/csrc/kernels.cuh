@@ -25,14 +25,12 @@ struct IndexView {
     float weights[16] = {};
 };
 
-// Radix-select scratch (device).  One per concurrent select.
+// Radix-select scratch (device): one histogram per digit pass plus a grid
+// barrier.  Zeroed by the launcher before every select.
 struct SelectState {
-    unsigned long long prefix;
-    unsigned long long mask;
-    unsigned long long remaining;
-    unsigned int done;
-    unsigned int ticket;
-    unsigned int hist[2048];
+    unsigned int hist[6][2048];
+    unsigned int bar_count;
+    unsigned int bar_gen;
 };
 
 constexpr int kScoresPitch = 32;  // S rows padded to 32 floats (128 B)
@@ -75,10 +73,15 @@ void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_coun
 // ---- centroid interaction (stages 2 and 3) -----------------------------------------
 // Candidates are either ids (d_ids) or keys (d_keys, id in the low word).
 // Writes keys (score, id) and optionally raw scores; adds used rows to *d_rows.
+// d_owners (optional, masked only): N-bit set of passages owning a kept token
+// (kept_owners); candidates outside it are scored 0 without reading codes.
 void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t rows,
                           const uint32_t* d_ids, const uint64_t* d_keys, const uint64_t* d_n,
-                          uint64_t nmax, const uint32_t* d_keep_bits, uint64_t* d_out_keys,
-                          float* d_out_scores, unsigned long long* d_rows, cudaStream_t st);
+                          uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_owners,
+                          uint64_t* d_out_keys, float* d_out_scores, unsigned long long* d_rows,
+                          cudaStream_t st);
+// owners |= postings(c) for every kept centroid c (owners zeroed by the caller).
+void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_owners, cudaStream_t st);
 
 // ---- selection -----------------------------------------------------------------------
 // Top `want` of keys[0..*d_n) (largest first).  Result: d_out_keys unsorted

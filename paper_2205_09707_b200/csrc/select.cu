@@ -2,13 +2,15 @@
 //
 // Keys pack (ord(score) << 32 | ~id), so "largest key first" is exactly the
 // reference's (score desc, id asc) order and every key is unique.  Two paths:
-//   * select_top_large: multi-CTA radix select (6 digit passes of <= 11 bits
-//     over the 64-bit key; the last CTA of each pass picks the digit, so there
-//     is no host round trip) followed by a compaction of the keys >= the
-//     threshold.  Used for stage 2 where the input is the whole candidate set.
-//   * sort_top: one CTA bitonic sort in shared memory (<= 8192 keys), or a
-//     global-memory bitonic network beyond that; emits the first `want` keys
-//     as (id, score) pairs in order.
+//   * select_top_large: ONE cooperative kernel doing an MSB radix select over
+//     the 64-bit keys (digit passes of 11,11,11,11,11,9 bits; a grid barrier
+//     after each pass, then every CTA derives the same digit from the global
+//     histogram, so there is no host round trip and no extra launch), then a
+//     compaction of the keys >= the threshold (unordered).  Used for stage 2,
+//     whose input is the whole candidate set.
+//   * sort_top: one CTA bitonic sort in shared memory (<= 8192 keys; one
+//     comparator per thread per step), or a global-memory bitonic network
+//     beyond that; emits the first `want` keys as (id, score) pairs in order.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -21,93 +23,107 @@ namespace {
 
 constexpr uint32_t kBins = 2048;
 constexpr int kPasses = 6;
+constexpr uint32_t kSelThreads = 512;
 __host__ __device__ constexpr int pass_shift(int p) { return p < 5 ? 53 - 11 * p : 0; }
 __host__ __device__ constexpr int pass_bits(int p) { return p < 5 ? 11 : 9; }
 
-__global__ void sel_init_kernel(SelectState* st, const uint64_t* __restrict__ d_n, uint64_t want,
-                                uint64_t* __restrict__ out_n) {
-    const uint64_t n = *d_n;
-    for (uint32_t b = threadIdx.x; b < kBins; b += blockDim.x) st->hist[b] = 0;
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident).
+__device__ __forceinline__ void grid_sync(unsigned int* count, unsigned int* gen) {
+    __syncthreads();
     if (threadIdx.x == 0) {
-        st->prefix = 0;
-        st->mask = 0;
-        st->remaining = n < want ? n : want;
-        st->done = n <= want ? 1u : 0u;
-        st->ticket = 0;
-        *out_n = 0;
+        volatile unsigned int* vgen = gen;
+        const unsigned int g = *vgen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*vgen == g) __nanosleep(20);
+        }
+        __threadfence();
     }
+    __syncthreads();
 }
 
-__global__ void __launch_bounds__(256)
-sel_pass_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
-                SelectState* st, int pass) {
+__global__ void __launch_bounds__(kSelThreads)
+radix_select_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
+                    SelectState* st, uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
     __shared__ uint32_t h[kBins];
-    __shared__ uint32_t part[256];
-    __shared__ bool last;
-    if (*((volatile unsigned int*)&st->done)) return;
-    const int shift = pass_shift(pass);
-    const uint32_t nb = 1u << pass_bits(pass);
-    const uint64_t prefix = st->prefix, mask = st->mask;
-    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
-    __syncthreads();
+    __shared__ uint32_t part[kSelThreads];
+    __shared__ unsigned long long s_prefix, s_mask, s_rem;
+    __shared__ int s_done;
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint64_t n = *d_n;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t k = keys[i];
-        if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & (nb - 1)], 1u);
+    if (tid == 0) {
+        s_prefix = 0;
+        s_mask = 0;
+        s_rem = n < want ? n : want;
+        s_done = n <= want;
+    }
+    const uint64_t stride = uint64_t(gridDim.x) * kSelThreads;
+    for (int pass = 0; pass < kPasses; ++pass) {
+        __syncthreads();
+        if (s_done) break;
+        const int shift = pass_shift(pass);
+        const uint32_t nb = 1u << pass_bits(pass);
+        const uint64_t prefix = s_prefix, mask = s_mask;
+        for (uint32_t b = tid; b < nb; b += kSelThreads) h[b] = 0;
+        __syncthreads();
+        for (uint64_t i0 = uint64_t(blockIdx.x) * kSelThreads; i0 < n; i0 += stride) {
+            const uint64_t i = i0 + tid;
+            const uint64_t k = i < n ? __ldcg(keys + i) : 0;
+            const bool valid = i < n && (k & mask) == prefix;
+            const uint32_t bin = valid ? uint32_t(k >> shift) & (nb - 1) : 0xFFFFFFFFu;
+            // warp-aggregated: the many equal keys of a dense bucket (e.g. the
+            // all-masked zero scores of stage 2) cost one atomic per warp
+            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+            if (valid && lane == uint32_t(__ffs(peers) - 1)) atomicAdd(&h[bin], uint32_t(__popc(peers)));
+        }
+        __syncthreads();
+        for (uint32_t b = tid; b < nb; b += kSelThreads)
+            if (h[b]) atomicAdd(&st->hist[pass][b], h[b]);
+        grid_sync(&st->bar_count, &st->bar_gen);
+        // every CTA: the bin (from the top) holding the s_rem-th largest key
+        const uint32_t per = nb / kSelThreads;  // 4 or 1
+        uint32_t mine = 0;
+        for (uint32_t j = 0; j < per; ++j) mine += __ldcg(&st->hist[pass][nb - 1 - (tid * per + j)]);
+        // block inclusive scan of `mine` (descending-bin order)
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += v;
+        }
+        if (lane == 31) part[tid >> 5] = incl;
+        __syncthreads();
+        uint32_t before = 0;
+        for (uint32_t w = 0; w < (tid >> 5); ++w) before += part[w];
+        const uint64_t cum0 = uint64_t(before) + incl - mine;  // keys in bins above mine
+        const uint64_t rem = s_rem;
+        __syncthreads();
+        if (cum0 < rem && rem <= cum0 + mine) {
+            uint64_t cum = cum0;
+            for (uint32_t j = 0; j < per; ++j) {
+                const uint32_t bin = nb - 1 - (tid * per + j);
+                const uint32_t cnt = __ldcg(&st->hist[pass][bin]);
+                if (cum + cnt >= rem) {
+                    s_rem = rem - cum;
+                    s_prefix = prefix | (uint64_t(bin) << shift);
+                    s_mask = mask | (uint64_t(nb - 1) << shift);
+                    s_done = cnt == rem - cum;
+                    break;
+                }
+                cum += cnt;
+            }
+        }
     }
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
-        if (h[b]) atomicAdd(&st->hist[b], h[b]);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&st->ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    // Last CTA: find the digit holding the remaining-th largest key.
-    const uint32_t per = nb / blockDim.x;  // bins per thread (8 or 2)
-    // thread t owns bins [nb - (t+1)*per, nb - t*per) (descending order)
-    uint32_t s = 0;
-    for (uint32_t j = 0; j < per; ++j) s += __ldcg(&st->hist[nb - 1 - (threadIdx.x * per + j)]);
-    part[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint64_t rem = st->remaining;
-        uint64_t cum = 0;
-        uint32_t t = 0;
-        for (; t < blockDim.x; ++t) {
-            if (cum + part[t] >= rem) break;
-            cum += part[t];
-        }
-        uint32_t bin = 0;
-        uint32_t cnt = 0;
-        for (uint32_t j = 0; j < per; ++j) {
-            bin = nb - 1 - (t * per + j);
-            cnt = __ldcg(&st->hist[bin]);
-            if (cum + cnt >= rem) break;
-            cum += cnt;
-        }
-        const uint64_t left = rem - cum;
-        st->remaining = left;
-        st->prefix = prefix | (uint64_t(bin) << shift);
-        st->mask = mask | (uint64_t(nb - 1) << shift);
-        if (cnt == left) st->done = 1u;
-        st->ticket = 0;
-    }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < kBins; b += blockDim.x) st->hist[b] = 0;
-}
-
-__global__ void __launch_bounds__(256)
-sel_compact_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
-                   const SelectState* st, uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
-    const uint64_t thr = st->prefix;
-    const uint64_t n = *d_n;
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x); i0 < n; i0 += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t i = i0 + threadIdx.x;
-        const uint64_t k = i < n ? keys[i] : 0;
+    // compaction of every key >= threshold (exactly min(want, n) keys)
+    const uint64_t thr = s_prefix;
+    for (uint64_t i0 = uint64_t(blockIdx.x) * kSelThreads; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + tid;
+        const uint64_t k = i < n ? __ldcg(keys + i) : 0;
         const bool take = i < n && k >= thr;
         const uint32_t ballot = __ballot_sync(0xffffffffu, take);
         if (!ballot) continue;
@@ -118,12 +134,25 @@ sel_compact_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict
     }
 }
 
-// Emit the first min(want, n) keys of a descending array.
+// Emit the j-th key of a descending array.
 __device__ __forceinline__ void emit(uint64_t j, uint64_t key, uint64_t* out_keys, uint32_t* out_ids,
                                      float* out_scores, uint32_t id_base) {
     if (out_keys) out_keys[j] = key;
     if (out_ids) out_ids[j] = dev::key_id(key) + id_base;
     if (out_scores) out_scores[j] = dev::key_score(key);
+}
+
+// Bitonic network step over s[0..npad): comparator p (< npad/2) joins
+// i = insert a 0 bit at position log2(j) of p, and i + j.
+__device__ __forceinline__ void bitonic_pair(uint64_t* s, uint32_t p, uint32_t j, uint32_t k) {
+    const uint32_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+    const uint32_t ixj = i + j;
+    const uint64_t a = s[i], b = s[ixj];
+    const bool desc = (i & k) == 0;
+    if (desc ? (a < b) : (a > b)) {
+        s[i] = b;
+        s[ixj] = a;
+    }
 }
 
 __global__ void __launch_bounds__(1024)
@@ -134,19 +163,10 @@ sort_small_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict_
     const uint64_t n = *d_n;
     for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) s[i] = i < n ? keys[i] : 0ull;
     __syncthreads();
+    const uint32_t half = npad >> 1;
     for (uint32_t k = 2; k <= npad; k <<= 1) {
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) {
-                const uint32_t ixj = i ^ j;
-                if (ixj > i) {
-                    const uint64_t a = s[i], b = s[ixj];
-                    const bool desc = (i & k) == 0;
-                    if (desc ? (a < b) : (a > b)) {
-                        s[i] = b;
-                        s[ixj] = a;
-                    }
-                }
-            }
+            for (uint32_t p = threadIdx.x; p < half; p += blockDim.x) bitonic_pair(s, p, j, k);
             __syncthreads();
         }
     }
@@ -164,16 +184,15 @@ __global__ void pad_copy_kernel(const uint64_t* __restrict__ keys, const uint64_
 }
 
 __global__ void bitonic_step_kernel(uint64_t* __restrict__ s, uint64_t npad, uint64_t j, uint64_t k) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < npad;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t ixj = i ^ j;
-        if (ixj > i) {
-            const uint64_t a = s[i], b = s[ixj];
-            const bool desc = (i & k) == 0;
-            if (desc ? (a < b) : (a > b)) {
-                s[i] = b;
-                s[ixj] = a;
-            }
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < npad / 2;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+        const uint64_t ixj = i + j;
+        const uint64_t a = s[i], b = s[ixj];
+        const bool desc = (i & k) == 0;
+        if (desc ? (a < b) : (a > b)) {
+            s[i] = b;
+            s[ixj] = a;
         }
     }
 }
@@ -257,14 +276,19 @@ namespace launch {
 void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
                       SelectState* d_state, uint64_t* d_out_keys, uint64_t* d_out_n,
                       cudaStream_t st) {
-    sel_init_kernel<<<1, 256, 0, st>>>(d_state, d_n, want, d_out_n);
-    count_launch();
-    const uint32_t grid = grid_for(nmax, 256, uint32_t(sm_count()) * 4);
-    for (int p = 0; p < kPasses; ++p) {
-        sel_pass_kernel<<<grid, 256, 0, st>>>(d_keys, d_n, d_state, p);
-        count_launch();
+    // state (histograms, barrier counter) and the output count start at zero
+    cudaMemsetAsync(d_state, 0, sizeof(SelectState), st);
+    cudaMemsetAsync(d_out_n, 0, sizeof(uint64_t), st);
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, radix_select_kernel, kSelThreads, 0);
+        if (per_sm < 1) per_sm = 1;
+        if (per_sm > 2) per_sm = 2;
     }
-    sel_compact_kernel<<<grid, 256, 0, st>>>(d_keys, d_n, d_state, d_out_keys, d_out_n);
+    const uint32_t grid = grid_for(nmax, kSelThreads * 4, uint32_t(sm_count() * per_sm));
+    void* args[] = {(void*)&d_keys, (void*)&d_n, (void*)&want, (void*)&d_state, (void*)&d_out_keys,
+                    (void*)&d_out_n};
+    cudaLaunchCooperativeKernel((const void*)radix_select_kernel, dim3(grid), dim3(kSelThreads), args, 0, st);
     count_launch();
 }
 
@@ -282,8 +306,9 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
                                  int(kSmallSortMax * sizeof(uint64_t)));
             configured = true;
         }
-        sort_small_kernel<<<1, 1024, smem, st>>>(d_keys, d_n, npad, want, d_out_keys, d_out_ids,
-                                                 d_out_scores, d_out_n, id_base);
+        const uint32_t threads = npad / 2 < 1024 ? (npad / 2 < 32 ? 32 : npad / 2) : 1024;
+        sort_small_kernel<<<1, threads, smem, st>>>(d_keys, d_n, npad, want, d_out_keys, d_out_ids,
+                                                    d_out_scores, d_out_n, id_base);
         count_launch();
         return;
     }

@@ -79,3 +79,36 @@ def test_disable_filter(small, port):
     assert np.array_equal(got.topk.passage_ids, ids)
     assert np.array_equal(bits(got.topk.scores), bits(sc))
     assert got.trace.counters() == tr
+
+
+@pytest.mark.parametrize("n,keep", [(20000, 4096), (100000, 1000), (100000, 9000), (50000, 60000), (9000, 8200)])
+def test_select_top_large_ties(port, n, keep):
+    """Radix-select + global sort paths, with heavy score ties (tie -> lower pid)."""
+    rng = np.random.default_rng(n + keep)
+    s = P.Searcher(None)
+    ids = rng.permutation(n * 3)[:n].astype(np.uint32)
+    sc = rng.choice(np.array([0.0, -0.0, 1.5, 2.25, -3.0, 7.0], dtype=np.float32), size=n)
+    sc[: n // 3] = rng.standard_normal(n // 3).astype(np.float32)
+    a = s.select_top(ids, sc, keep)
+    b = port.select_top(ids, sc, keep)
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[1], b[1])
+
+
+def test_merge_topk(port):
+    rng = np.random.default_rng(5)
+    s = P.Searcher(None)
+    G, k = 4, 100
+    pids = np.zeros((G, k), np.uint32)
+    sc = np.zeros((G, k), np.float32)
+    counts = np.array([100, 37, 0, 100], np.uint64)
+    allp, alls = [], []
+    for g in range(G):
+        c = int(counts[g])
+        p = (rng.permutation(10000)[:c] + g * 10000).astype(np.uint32)
+        v = rng.standard_normal(c).astype(np.float32)
+        pids[g, :c], sc[g, :c] = p, v
+        allp.append(p), alls.append(v)
+    a = s.merge_topk(pids, sc, counts, k)
+    b = port.select_top(np.concatenate(allp), np.concatenate(alls), k)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
