@@ -28,6 +28,9 @@ void count_launch() {
         fail(PLAID_CUDA_ERROR, std::string("kernel launch failed: ") + cudaGetErrorString(e));
     }
 }
+void fail_cuda_driver(int code, const char* what) {
+    fail(PLAID_CUDA_ERROR, std::string(what) + " failed with CUresult " + std::to_string(code));
+}
 }  // namespace launch
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -319,7 +322,16 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         keys4_.ensure(ix.N);
         const uint64_t K = ix.K;
         PLAID_CUDA(cudaMemcpy(kconst_.p, &K, sizeof K, cudaMemcpyHostToDevice));
+        tensor_ = cfg_.score_mode == PLAID_SCORES_TENSOR && launch::tensor_scores_supported(ix);
+        if (tensor_) launch::make_centroid_tensor_map(ix, tmap_);
     }
+}
+
+uint32_t Searcher::launch_scores(const float* d_q, uint32_t rows, float t_cs, uint32_t npb, cudaStream_t st) {
+    const IndexView& ix = index_->view();
+    if (tensor_)
+        return launch::scores_tensor(tmap_, ix, d_q, rows, t_cs, scores_.p, rowmax_.p, keep_.p, partial_.p, npb, st);
+    return launch::scores_exact(ix, d_q, rows, t_cs, scores_.p, rowmax_.p, keep_.p, partial_.p, npb, st);
 }
 
 Searcher::~Searcher() {
@@ -390,8 +402,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
-    const uint32_t warps = launch::scores_exact(ix, d_q, rows, p.t_cs, scores_.p, rowmax_.p, keep_.p,
-                                                partial_.p, npb, st);
+    const uint32_t warps = launch_scores(d_q, rows, p.t_cs, npb, st);
     record(1, st, times);
     uint64_t nsel;
     if (p.nprobe == K) {
@@ -585,8 +596,7 @@ void Searcher::compute_centroid_scores(const float* q, uint64_t rows, uint64_t d
     if (rows == 0 || rows > 32) fail(PLAID_UNSUPPORTED, "engine supports 1 <= |Q| <= 32");
     DeviceGuard g(device_);
     h2d(q_.p, q, rows * dim, stream_);
-    launch::scores_exact(ix, q_.p, uint32_t(rows), INFINITY, scores_.p, rowmax_.p, keep_.p, partial_.p, 1,
-                         stream_);
+    launch_scores(q_.p, uint32_t(rows), INFINITY, 1, stream_);
     std::vector<float> S(ix.K * kScoresPitch);
     d2h(S.data(), scores_.p, S.size(), stream_);
     d2h(row_max, rowmax_.p, ix.K, stream_);

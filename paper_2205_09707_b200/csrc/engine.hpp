@@ -162,6 +162,10 @@ private:
     uint64_t h_cap_ = 0;
     cudaEvent_t ev_[8] = {};
     uint64_t npartial_warps_ = 0;
+    bool tensor_ = false;                   // tcgen05 S_cq path active
+    alignas(64) unsigned char tmap_[128];   // CUtensorMap over the centroids
+    // S_cq + row max + keep bits + per-warp top lists, in the configured mode
+    uint32_t launch_scores(const float* d_q, uint32_t rows, float t_cs, uint32_t npb, cudaStream_t st);
 };
 
 }  // namespace plaid

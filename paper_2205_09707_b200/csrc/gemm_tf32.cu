@@ -1,0 +1,381 @@
+// gemm_tf32.cu — stage-1 S_cq = C . Q^T on the 5th-gen tensor cores (tcgen05),
+// the production score path (PLAID_SCORES_TENSOR).  Replaces the reference's
+// scalar compute_centroid_scores (pipeline.cpp:26-50).
+//
+// Precision: 3xTF32.  Each fp32 operand is split in shared memory into
+// hi = x with the low 13 mantissa bits cleared and lo = x - hi (exact), and
+// S = C_hi.Q_hi + C_hi.Q_lo + C_lo.Q_hi accumulated in fp32 in TMEM, which is
+// fp32-accurate (~1e-6 absolute on unit-vector dots) while the HBM traffic
+// stays one fp32 read of C.  Decisions that depend on S (top-nprobe, t_cs)
+// then differ from the reference only for scores within that tolerance.
+//
+// Structure (persistent, one CTA per SM, 10 warps):
+//   warp 0      TMA producer: 128-centroid x 32-dim fp32 boxes (16 KB,
+//               SWIZZLE_128B) into a 5-stage ring;
+//   warps 2-5   splitters: rewrite each landed chunk in place as hi and write
+//               lo beside it (elementwise, so the swizzled layout is kept);
+//   warp 1      MMA issuer (one thread): 3 x 4 tcgen05.mma.kind::tf32
+//               (M=128, N=32, K=8) per chunk into one of two TMEM
+//               accumulators (2 x 32 columns), tcgen05.commit frees the stage;
+//   warps 6-9   epilogue: tcgen05.ld 32x32b.x32 (thread = centroid row, 32
+//               query-token scores in registers) -> S row (128 B store), row
+//               max, keep bit (ballot -> one 32-bit word per warp), and the
+//               per-token top-nprobe keys after a 32x32 smem transpose (lane =
+//               query token), exactly like the CUDA-core kernel.
+// Q (32 x 128) is split into hi/lo once per CTA and stays resident.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace plaid {
+namespace {
+
+constexpr int kStages = 5;
+constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 32 fp32
+constexpr uint32_t kQChunkBytes = 32 * 128;  // 32 rows x 32 fp32
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 64;           // two 32-column accumulators
+constexpr int kDim = 128;
+constexpr int kChunks = kDim / 32;
+
+// shared-memory carve-up (offsets from a 1024-B aligned base)
+constexpr uint32_t kOffA = 0;
+constexpr uint32_t kOffLo = kOffA + kStages * kChunkBytes;
+constexpr uint32_t kOffQHi = kOffLo + kStages * kChunkBytes;
+constexpr uint32_t kOffQLo = kOffQHi + kChunks * kQChunkBytes;
+constexpr uint32_t kOffTr = kOffQLo + kChunks * kQChunkBytes;  // 4 warps x 32 x 33 floats
+constexpr uint32_t kOffBar = kOffTr + 4 * 32 * 33 * 4;
+constexpr uint32_t kNumBars = 3 * kStages + 4;
+constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (SM100 layout:
+// start>>4 @0, LBO>>4 @16 (unused for swizzled K-major), SBO>>4 @32 = 1024 B
+// between 8-row groups, version 1 @46, layout 2 = SWIZZLE_128B @61).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
+    uint64_t d = uint64_t((addr >> 4) & 0x3FFFu);
+    d |= uint64_t(1) << 16;
+    d |= uint64_t(1024 >> 4) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N=32, M=128.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t split_hi(uint32_t x) { return x & 0xFFFFE000u; }
+
+// lo rounded to the nearest tf32 (the tensor core would otherwise truncate
+// its low 13 bits, a one-sided error that biases every dot product)
+__device__ __forceinline__ float tf32_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// hi/lo of one float4, written to hi_dst (may alias src) and lo_dst
+__device__ __forceinline__ void split4(float4 v, float4* hi_dst, float4* lo_dst) {
+    float4 h, l;
+    h.x = __uint_as_float(split_hi(__float_as_uint(v.x)));
+    h.y = __uint_as_float(split_hi(__float_as_uint(v.y)));
+    h.z = __uint_as_float(split_hi(__float_as_uint(v.z)));
+    h.w = __uint_as_float(split_hi(__float_as_uint(v.w)));
+    l.x = tf32_rn(__fsub_rn(v.x, h.x));
+    l.y = tf32_rn(__fsub_rn(v.y, h.y));
+    l.z = tf32_rn(__fsub_rn(v.z, h.z));
+    l.w = tf32_rn(__fsub_rn(v.w, h.w));
+    *hi_dst = h;
+    *lo_dst = l;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kThreads, 1)
+scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const float* __restrict__ Q,
+                   uint32_t rows, float t_cs, float* __restrict__ S, float* __restrict__ rowmax,
+                   uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ partial) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t base = smem_u32(smem);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t bar0 = base + kOffBar;
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto split_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * kStages + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * kStages + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * kStages + 2 + a); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + kNumBars * 8);
+
+    const uint64_t ntiles = (K + 127) / 128;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(split_bar(s), 128);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&cmap)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // Q -> hi/lo, SWIZZLE_128B K-major: row r, 16-byte granule j of chunk kc at
+    // kc*4096 + r*128 + ((j ^ (r & 7)) << 4)
+    for (uint32_t e = threadIdx.x; e < 32 * (kDim / 4); e += kThreads) {
+        const uint32_t r = e / (kDim / 4), g = e % (kDim / 4);
+        const uint32_t kc = g / 8, j = g % 8;
+        float4 v = r < rows ? reinterpret_cast<const float4*>(Q + uint64_t(r) * kDim)[g]
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        const uint32_t off = kc * kQChunkBytes + r * 128 + ((j ^ (r & 7)) << 4);
+        split4(v, reinterpret_cast<float4*>(smem + kOffQHi + off), reinterpret_cast<float4*>(smem + kOffQLo + off));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+                for (int kc = 0; kc < kChunks; ++kc, ++g) {
+                    const int s = g % kStages;
+                    const uint32_t ph = (g / kStages) & 1;
+                    mbar_wait(empty_bar(s), ph ^ 1);
+                    mbar_expect_tx(full_bar(s), kChunkBytes);
+                    tma_load_2d(base + kOffA + s * kChunkBytes, &cmap, kc * 32, int(t * 128), full_bar(s));
+                }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        uint32_t g = 0, lt = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            mbar_wait(tempty_bar(acc), aph ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t d = tmem_base + acc * 32;
+            for (int kc = 0; kc < kChunks; ++kc, ++g) {
+                const int s = g % kStages;
+                const uint32_t ph = (g / kStages) & 1;
+                mbar_wait(split_bar(s), ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    const uint32_t ahi = base + kOffA + s * kChunkBytes, alo = base + kOffLo + s * kChunkBytes;
+                    const uint32_t bhi = base + kOffQHi + kc * kQChunkBytes, blo = base + kOffQLo + kc * kQChunkBytes;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t o = kk * 32;  // 8 tf32 along K
+                        mma_tf32(d, umma_desc(ahi + o), umma_desc(bhi + o), (kc | kk) != 0);
+                        mma_tf32(d, umma_desc(ahi + o), umma_desc(blo + o), 1);
+                        mma_tf32(d, umma_desc(alo + o), umma_desc(bhi + o), 1);
+                    }
+                    mma_commit(empty_bar(s));
+                    if (kc == kChunks - 1) mma_commit(tfull_bar(acc));
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp < 6) {
+        // ---------------- splitters (128 threads)
+        const uint32_t tid = threadIdx.x - 64;
+        uint32_t g = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+            for (int kc = 0; kc < kChunks; ++kc, ++g) {
+                const int s = g % kStages;
+                const uint32_t ph = (g / kStages) & 1;
+                mbar_wait(full_bar(s), ph);
+                float4* a = reinterpret_cast<float4*>(smem + kOffA + s * kChunkBytes);
+                float4* lo = reinterpret_cast<float4*>(smem + kOffLo + s * kChunkBytes);
+                float4 v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = a[tid + j * 128];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) split4(v[j], a + tid + j * 128, lo + tid + j * 128);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(split_bar(s));
+            }
+    } else {
+        // ---------------- epilogue (warps 6..9 -> TMEM lane quarters 2,3,0,1)
+        const uint32_t q = warp & 3;
+        const uint32_t ew = warp - 6;
+        float* tr = reinterpret_cast<float*>(smem + kOffTr) + ew * 32 * 33;
+        uint64_t top[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) top[j] = 0;
+        uint32_t lt = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            mbar_wait(tfull_bar(acc), aph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t r[32];
+            const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * 32;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(tempty_bar(acc));
+
+            const uint64_t c0 = t * 128 + q * 32;
+            const uint64_t c = c0 + lane;
+            const bool valid = c < K;
+            float m = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (uint32_t(j) < rows) m = dev::max_gt(m, __uint_as_float(r[j]));
+            const uint32_t kw = __ballot_sync(0xffffffffu, valid && m >= t_cs);
+            if (lane == 0 && c0 < K) keep_bits[c0 >> 5] = kw;
+            if (valid) {
+                rowmax[c] = m;
+                float4* dst = reinterpret_cast<float4*>(S + c * kScoresPitch);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            }
+            // transpose the warp's 32 x 32 block: lane = query token
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = __uint_as_float(r[j]);
+            __syncwarp();
+            if (lane < rows) {
+                for (uint32_t rr = 0; rr < 32; ++rr)
+                    if (c0 + rr < K) dev::topn_insert<NP>(top, dev::make_key(tr[rr * 33 + lane], uint32_t(c0 + rr)));
+            }
+            __syncwarp();
+        }
+        uint64_t* out = partial + ((uint64_t(blockIdx.x) * 4 + ew) * 32 + lane) * NP;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) out[j] = top[j];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int NP>
+void launch_tf32(const CUtensorMap& map, const IndexView& ix, const float* q, uint32_t rows, float t_cs,
+                 float* S, float* rowmax, uint32_t* keep, uint64_t* partial, uint32_t grid, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(scores_tf32_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        configured = true;
+    }
+    scores_tf32_kernel<NP><<<grid, kThreads, kSmemBytes, st>>>(map, ix.K, q, rows, t_cs, S, rowmax, keep, partial);
+    launch::count_launch();
+}
+
+}  // namespace
+
+namespace launch {
+
+bool tensor_scores_supported(const IndexView& ix) { return ix.dim == kDim && ix.K < (1ull << 31); }
+
+uint32_t scores_tensor_max_warps() { return uint32_t(sm_count()) * 4; }
+
+void make_centroid_tensor_map(const IndexView& ix, void* out_map) {
+    CUtensorMap* map = static_cast<CUtensorMap*>(out_map);
+    const cuuint64_t dims[2] = {cuuint64_t(kDim), cuuint64_t(ix.K)};
+    const cuuint64_t strides[1] = {cuuint64_t(kDim) * sizeof(float)};
+    const cuuint32_t box[2] = {32, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                              const_cast<float*>(ix.centroids), dims, strides, box, estr,
+                                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail_cuda_driver(int(r), "cuTensorMapEncodeTiled");
+}
+
+uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
+                       float* d_scores, float* d_rowmax, uint32_t* d_keep_bits, uint64_t* d_partial,
+                       uint32_t np_bucket, cudaStream_t st) {
+    const CUtensorMap& map = *static_cast<const CUtensorMap*>(cmap);
+    const uint64_t ntiles = (ix.K + 127) / 128;
+    uint32_t grid = uint32_t(ntiles < uint64_t(sm_count()) ? ntiles : uint64_t(sm_count()));
+    if (grid == 0) grid = 1;
+    switch (np_bucket) {
+        case 1: launch_tf32<1>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
+        case 2: launch_tf32<2>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
+        case 4: launch_tf32<4>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
+        case 8: launch_tf32<8>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
+        case 16: launch_tf32<16>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
+        default: launch_tf32<32>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
+    }
+    return grid * 4;
+}
+
+}  // namespace launch
+}  // namespace plaid

@@ -46,6 +46,15 @@ uint32_t scores_exact(const IndexView& ix, const float* d_q, uint32_t rows, floa
                       uint64_t* d_partial, uint32_t np_bucket, cudaStream_t st);
 // Max number of warps scores_exact may use (for sizing `partial`).
 uint32_t scores_max_warps();
+// tcgen05/TMA 3xTF32 variant (gemm_tf32.cu); same outputs, dim == 128 only.
+// `cmap` is a CUtensorMap (128 B) made by make_centroid_tensor_map.
+bool tensor_scores_supported(const IndexView& ix);
+void make_centroid_tensor_map(const IndexView& ix, void* out_map);
+uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
+                       float* d_scores, float* d_rowmax, uint32_t* d_keep_bits, uint64_t* d_partial,
+                       uint32_t np_bucket, cudaStream_t st);
+uint32_t scores_tensor_max_warps();
+[[noreturn]] void fail_cuda_driver(int code, const char* what);
 // Merge per-warp partial top-NP lists into sel[rows][nprobe] centroid ids.
 void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,
                 uint32_t nprobe, uint32_t* d_sel, cudaStream_t st);

@@ -95,6 +95,51 @@ def test_select_top_large_ties(port, n, keep):
     assert np.array_equal(a[1], b[1])
 
 
+def compose_with_scores(port, h, q, S, mx, p):
+    """The reference pipeline (pipeline.cpp:232-283) run by the oracle stage by
+    stage, but on a given centroid-score table S (e.g. the tensor-core one)."""
+    c1 = port.generate_candidates(h, S, p.nprobe)
+    keep = port.prune_centroids(mx, p.t_cs)
+    s2, r2 = port.centroid_interaction(h, c1, S, keep)
+    k2, _ = port.select_top(c1, s2, p.ndocs)
+    s3, r3 = port.centroid_interaction(h, k2, S, None)
+    k3, _ = port.select_top(k2, s3, P.stage3_width(p))
+    ids, sc = port.rank_final(h, k3, q, p.k)
+    return ids, sc, dict(stage1_candidates=len(c1), stage2_out=len(k2), stage3_out=len(k3), final_out=len(ids),
+                         centroid_matmul_count=1, stage2_rows_gathered=r2, stage3_rows_gathered=r3,
+                         decompressed_passages=len(k3))
+
+
+@pytest.fixture(scope="module")
+def tensor_searcher(small):
+    h, qs, idx, _ = small
+    return P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+
+
+def test_tensor_scores_accuracy(small, tensor_searcher, port):
+    """tcgen05 3xTF32 S_cq vs the in-order fp32 reference dot products."""
+    h, qs, idx, _ = small
+    for q in qs:
+        S, mx = tensor_searcher.compute_centroid_scores(q)
+        S0, mx0 = port.compute_centroid_scores(h, q)
+        assert np.abs(S - S0).max() < 5e-6
+        assert np.abs(mx - mx0).max() < 5e-6
+
+
+@pytest.mark.parametrize("k", [10, 100, 1000])
+def test_tensor_search_consistent(small, tensor_searcher, port, k):
+    """Given the tensor-core S, every later stage is bit-exact with the oracle."""
+    h, qs, idx, _ = small
+    p = P.default_params_for_k(k)
+    for q in qs:
+        S, mx = tensor_searcher.compute_centroid_scores(q)
+        got = tensor_searcher.search(q, p)
+        ids, sc, tr = compose_with_scores(port, h, q, S, mx, p)
+        assert np.array_equal(got.topk.passage_ids, ids)
+        assert np.array_equal(bits(got.topk.scores), bits(sc))
+        assert got.trace.counters() == tr
+
+
 def test_merge_topk(port):
     rng = np.random.default_rng(5)
     s = P.Searcher(None)
