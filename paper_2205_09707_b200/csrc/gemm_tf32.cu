@@ -3,26 +3,30 @@
 // scalar compute_centroid_scores (pipeline.cpp:26-50).
 //
 // Precision: 3xTF32.  Each fp32 operand is split in shared memory into
-// hi = x with the low 13 mantissa bits cleared and lo = x - hi (exact), and
-// S = C_hi.Q_hi + C_hi.Q_lo + C_lo.Q_hi accumulated in fp32 in TMEM, which is
-// fp32-accurate (~1e-6 absolute on unit-vector dots) while the HBM traffic
-// stays one fp32 read of C.  Decisions that depend on S (top-nprobe, t_cs)
-// then differ from the reference only for scores within that tolerance.
+// hi = x with the low 13 mantissa bits cleared and lo = tf32_rn(x - hi), and
+// S = C_hi.Q_hi + C_hi.Q_lo + C_lo.Q_hi accumulated in fp32 in TMEM: ~2e-6
+// absolute on unit-vector dots (tests/test_gpu_parity.py), while the HBM
+// traffic stays one fp32 read of C.  Decisions that depend on S (top-nprobe,
+// t_cs) can differ from the reference only for scores that close to the
+// boundary.
 //
-// Structure (persistent, one CTA per SM, 10 warps):
+// Structure (persistent, one CTA per SM, 10 warps, two decoupled rings):
 //   warp 0      TMA producer: 128-centroid x 32-dim fp32 boxes (16 KB,
-//               SWIZZLE_128B) into a 5-stage ring;
-//   warps 2-5   splitters: rewrite each landed chunk in place as hi and write
-//               lo beside it (elementwise, so the swizzled layout is kept);
+//               SWIZZLE_128B) into a 6-stage raw ring;
+//   warps 2-5   splitters: read a landed raw chunk into registers, release
+//               the raw slot at once, write hi and lo (same swizzled layout,
+//               the split is elementwise) into a 2-stage operand ring;
 //   warp 1      MMA issuer (one thread): 3 x 4 tcgen05.mma.kind::tf32
 //               (M=128, N=32, K=8) per chunk into one of two TMEM
-//               accumulators (2 x 32 columns), tcgen05.commit frees the stage;
-//   warps 6-9   epilogue: tcgen05.ld 32x32b.x32 (thread = centroid row, 32
-//               query-token scores in registers) -> S row (128 B store), row
-//               max, keep bit (ballot -> one 32-bit word per warp), and the
-//               per-token top-nprobe keys after a 32x32 smem transpose (lane =
-//               query token), exactly like the CUDA-core kernel.
-// Q (32 x 128) is split into hi/lo once per CTA and stays resident.
+//               accumulators (2 x 32 columns); tcgen05.commit frees the
+//               operand slot / publishes the accumulator;
+//   warps 6-9   epilogue: tcgen05.ld 32x32b.x32 (thread = centroid row, its
+//               32 query-token scores in registers) -> S row (128 B store),
+//               row max, keep bit (ballot -> one 32-bit word per warp), and
+//               the per-token top-nprobe keys after a 32x32 smem transpose
+//               (lane = query token), as in the CUDA-core kernel.
+// The raw ring is released by the splitters, not by the MMA, so HBM streaming
+// never waits on tensor-core completion.  Q (32 x 128) is split once per CTA.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -34,7 +38,8 @@
 namespace plaid {
 namespace {
 
-constexpr int kStages = 5;
+constexpr int kRaw = 6;                      // raw (TMA) ring depth
+constexpr int kOps = 2;                      // hi/lo operand ring depth
 constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 32 fp32
 constexpr uint32_t kQChunkBytes = 32 * 128;  // 32 rows x 32 fp32
 constexpr int kThreads = 320;
@@ -43,13 +48,14 @@ constexpr int kDim = 128;
 constexpr int kChunks = kDim / 32;
 
 // shared-memory carve-up (offsets from a 1024-B aligned base)
-constexpr uint32_t kOffA = 0;
-constexpr uint32_t kOffLo = kOffA + kStages * kChunkBytes;
-constexpr uint32_t kOffQHi = kOffLo + kStages * kChunkBytes;
+constexpr uint32_t kOffRaw = 0;
+constexpr uint32_t kOffHi = kOffRaw + kRaw * kChunkBytes;
+constexpr uint32_t kOffLo = kOffHi + kOps * kChunkBytes;
+constexpr uint32_t kOffQHi = kOffLo + kOps * kChunkBytes;
 constexpr uint32_t kOffQLo = kOffQHi + kChunks * kQChunkBytes;
 constexpr uint32_t kOffTr = kOffQLo + kChunks * kQChunkBytes;  // 4 warps x 32 x 33 floats
 constexpr uint32_t kOffBar = kOffTr + 4 * 32 * 33 * 4;
-constexpr uint32_t kNumBars = 3 * kStages + 4;
+constexpr uint32_t kNumBars = 2 * kRaw + 2 * kOps + 4;
 constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -122,9 +128,7 @@ __device__ __forceinline__ float tf32_rn(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-// hi/lo of one float4, written to hi_dst (may alias src) and lo_dst
-__device__ __forceinline__ void split4(float4 v, float4* hi_dst, float4* lo_dst) {
-    float4 h, l;
+__device__ __forceinline__ void split4(float4 v, float4& h, float4& l) {
     h.x = __uint_as_float(split_hi(__float_as_uint(v.x)));
     h.y = __uint_as_float(split_hi(__float_as_uint(v.y)));
     h.z = __uint_as_float(split_hi(__float_as_uint(v.z)));
@@ -133,8 +137,6 @@ __device__ __forceinline__ void split4(float4 v, float4* hi_dst, float4* lo_dst)
     l.y = tf32_rn(__fsub_rn(v.y, h.y));
     l.z = tf32_rn(__fsub_rn(v.z, h.z));
     l.w = tf32_rn(__fsub_rn(v.w, h.w));
-    *hi_dst = h;
-    *lo_dst = l;
 }
 
 template <int NP>
@@ -142,25 +144,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const float* __restrict__ Q,
                    uint32_t rows, float t_cs, float* __restrict__ S, float* __restrict__ rowmax,
                    uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ partial) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    // align within the shared window (pointer stays in the shared address space)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t base = smem_u32(smem);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bar0 = base + kOffBar;
-    auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto split_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * kStages + s); };
-    auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * kStages + a); };
-    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * kStages + 2 + a); };
+    auto raw_full = [&](int s) { return bar0 + 8u * s; };
+    auto raw_empty = [&](int s) { return bar0 + 8u * (kRaw + s); };
+    auto ops_full = [&](int s) { return bar0 + 8u * (2 * kRaw + s); };
+    auto ops_empty = [&](int s) { return bar0 + 8u * (2 * kRaw + kOps + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kRaw + 2 * kOps + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kRaw + 2 * kOps + 2 + a); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + kNumBars * 8);
 
     const uint64_t ntiles = (K + 127) / 128;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(full_bar(s), 1);
-            mbar_init(split_bar(s), 128);
-            mbar_init(empty_bar(s), 1);
+        for (int s = 0; s < kRaw; ++s) {
+            mbar_init(raw_full(s), 1);
+            mbar_init(raw_empty(s), 128);
+        }
+        for (int s = 0; s < kOps; ++s) {
+            mbar_init(ops_full(s), 128);
+            mbar_init(ops_empty(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
@@ -182,7 +189,10 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
         float4 v = r < rows ? reinterpret_cast<const float4*>(Q + uint64_t(r) * kDim)[g]
                             : make_float4(0.f, 0.f, 0.f, 0.f);
         const uint32_t off = kc * kQChunkBytes + r * 128 + ((j ^ (r & 7)) << 4);
-        split4(v, reinterpret_cast<float4*>(smem + kOffQHi + off), reinterpret_cast<float4*>(smem + kOffQLo + off));
+        float4 h, l;
+        split4(v, h, l);
+        *reinterpret_cast<float4*>(smem + kOffQHi + off) = h;
+        *reinterpret_cast<float4*>(smem + kOffQLo + off) = l;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -196,11 +206,11 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             uint32_t g = 0;
             for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
                 for (int kc = 0; kc < kChunks; ++kc, ++g) {
-                    const int s = g % kStages;
-                    const uint32_t ph = (g / kStages) & 1;
-                    mbar_wait(empty_bar(s), ph ^ 1);
-                    mbar_expect_tx(full_bar(s), kChunkBytes);
-                    tma_load_2d(base + kOffA + s * kChunkBytes, &cmap, kc * 32, int(t * 128), full_bar(s));
+                    const int s = g % kRaw;
+                    const uint32_t ph = (g / kRaw) & 1;
+                    mbar_wait(raw_empty(s), ph ^ 1);
+                    mbar_expect_tx(raw_full(s), kChunkBytes);
+                    tma_load_2d(base + kOffRaw + s * kChunkBytes, &cmap, kc * 32, int(t * 128), raw_full(s));
                 }
         }
     } else if (warp == 1) {
@@ -212,12 +222,12 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t d = tmem_base + acc * 32;
             for (int kc = 0; kc < kChunks; ++kc, ++g) {
-                const int s = g % kStages;
-                const uint32_t ph = (g / kStages) & 1;
-                mbar_wait(split_bar(s), ph);
+                const int s = g % kOps;
+                const uint32_t ph = (g / kOps) & 1;
+                mbar_wait(ops_full(s), ph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
-                    const uint32_t ahi = base + kOffA + s * kChunkBytes, alo = base + kOffLo + s * kChunkBytes;
+                    const uint32_t ahi = base + kOffHi + s * kChunkBytes, alo = base + kOffLo + s * kChunkBytes;
                     const uint32_t bhi = base + kOffQHi + kc * kQChunkBytes, blo = base + kOffQLo + kc * kQChunkBytes;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
@@ -226,7 +236,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                         mma_tf32(d, umma_desc(ahi + o), umma_desc(blo + o), 1);
                         mma_tf32(d, umma_desc(alo + o), umma_desc(bhi + o), 1);
                     }
-                    mma_commit(empty_bar(s));
+                    mma_commit(ops_empty(s));
                     if (kc == kChunks - 1) mma_commit(tfull_bar(acc));
                 }
                 __syncwarp();
@@ -238,18 +248,28 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
         uint32_t g = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
             for (int kc = 0; kc < kChunks; ++kc, ++g) {
-                const int s = g % kStages;
-                const uint32_t ph = (g / kStages) & 1;
-                mbar_wait(full_bar(s), ph);
-                float4* a = reinterpret_cast<float4*>(smem + kOffA + s * kChunkBytes);
-                float4* lo = reinterpret_cast<float4*>(smem + kOffLo + s * kChunkBytes);
-                float4 v[8];
+                const int s = g % kRaw;
+                const uint32_t ph = (g / kRaw) & 1;
+                const int o = g % kOps;
+                const uint32_t oph = (g / kOps) & 1;
+                mbar_wait(raw_full(s), ph);
+                const float4* a = reinterpret_cast<const float4*>(smem + kOffRaw + s * kChunkBytes);
+                float4 h[8], l[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = a[tid + j * 128];
+                for (int j = 0; j < 8; ++j) split4(a[tid + j * 128], h[j], l[j]);
+                // the split consumed every loaded value, so the raw slot can go
+                // back to the TMA producer before the outputs are written
+                mbar_arrive(raw_empty(s));
+                mbar_wait(ops_empty(o), oph ^ 1);
+                float4* hi = reinterpret_cast<float4*>(smem + kOffHi + o * kChunkBytes);
+                float4* lo = reinterpret_cast<float4*>(smem + kOffLo + o * kChunkBytes);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) split4(v[j], a + tid + j * 128, lo + tid + j * 128);
+                for (int j = 0; j < 8; ++j) {
+                    hi[tid + j * 128] = h[j];
+                    lo[tid + j * 128] = l[j];
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(split_bar(s));
+                mbar_arrive(ops_full(o));
             }
     } else {
         // ---------------- epilogue (warps 6..9 -> TMEM lane quarters 2,3,0,1)
@@ -301,8 +321,12 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = __uint_as_float(r[j]);
             __syncwarp();
             if (lane < rows) {
-                for (uint32_t rr = 0; rr < 32; ++rr)
-                    if (c0 + rr < K) dev::topn_insert<NP>(top, dev::make_key(tr[rr * 33 + lane], uint32_t(c0 + rr)));
+                const uint32_t nv = K - c0 < 32 ? uint32_t(K - c0) : 32u;
+                // cheap pre-filter: only keys above the current NP-th best
+                for (uint32_t rr = 0; rr < nv; ++rr) {
+                    const uint64_t key = dev::make_key(tr[rr * 33 + lane], uint32_t(c0 + rr));
+                    if (key > top[NP - 1]) dev::topn_insert<NP>(top, key);
+                }
             }
             __syncwarp();
         }
