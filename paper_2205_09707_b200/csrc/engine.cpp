@@ -77,7 +77,8 @@ enum : int {
     kKConst = 7,    // K (for generic selects)
     kTmpN = 8,      // scratch count
     kEntryN = 9,    // entry-point input count
-    kNumCounters = 16
+    kGthr = 16,     // 32 u32 per-token top-nprobe bounds (tensor S_cq kernel)
+    kNumCounters = 32
 };
 
 }  // namespace
@@ -330,7 +331,8 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
 uint32_t Searcher::launch_scores(const float* d_q, uint32_t rows, float t_cs, uint32_t npb, cudaStream_t st) {
     const IndexView& ix = index_->view();
     if (tensor_)
-        return launch::scores_tensor(tmap_, ix, d_q, rows, t_cs, scores_.p, rowmax_.p, keep_.p, partial_.p, npb, st);
+        return launch::scores_tensor(tmap_, ix, d_q, rows, t_cs, scores_.p, rowmax_.p, keep_.p, partial_.p, npb,
+                                     reinterpret_cast<uint32_t*>(counters_.p + kGthr), st);
     return launch::scores_exact(ix, d_q, rows, t_cs, scores_.p, rowmax_.p, keep_.p, partial_.p, npb, st);
 }
 
@@ -596,6 +598,7 @@ void Searcher::compute_centroid_scores(const float* q, uint64_t rows, uint64_t d
     if (rows == 0 || rows > 32) fail(PLAID_UNSUPPORTED, "engine supports 1 <= |Q| <= 32");
     DeviceGuard g(device_);
     h2d(q_.p, q, rows * dim, stream_);
+    PLAID_CUDA(cudaMemsetAsync(counters_.p + kGthr, 0, 16 * sizeof(uint64_t), stream_));
     launch_scores(q_.p, uint32_t(rows), INFINITY, 1, stream_);
     std::vector<float> S(ix.K * kScoresPitch);
     d2h(S.data(), scores_.p, S.size(), stream_);

@@ -2,35 +2,36 @@
 // the production score path (PLAID_SCORES_TENSOR).  Replaces the reference's
 // scalar compute_centroid_scores (pipeline.cpp:26-50).
 //
-// Precision: 3xTF32.  Each fp32 operand is split in shared memory into
-// hi = x with the low 13 mantissa bits cleared and lo = tf32_rn(x - hi), and
-// S = C_hi.Q_hi + C_hi.Q_lo + C_lo.Q_hi accumulated in fp32 in TMEM: ~2e-6
+// Precision: 3xTF32.  Each fp32 operand is split into hi = x with the low 13
+// mantissa bits cleared and lo = tf32_rn(x - hi), and
+// S = C_hi.Q_hi + C_hi.Q_lo + C_lo.Q_hi is accumulated in fp32 in TMEM: ~2e-6
 // absolute on unit-vector dots (tests/test_gpu_parity.py), while the HBM
 // traffic stays one fp32 read of C.  Decisions that depend on S (top-nprobe,
-// t_cs) can differ from the reference only for scores that close to the
+// t_cs) can differ from the reference only for scores that close to a
 // boundary.
 //
-// Structure (persistent, one CTA per SM, 10 warps, two decoupled rings):
+// Structure (persistent, one CTA per SM, 10 warps):
 //   warp 0      TMA producer: 128-centroid x 32-dim fp32 boxes (16 KB,
-//               SWIZZLE_128B) into a 6-stage raw ring;
-//   warps 2-5   splitters: read a landed raw chunk into registers, release
-//               the raw slot at once, write hi and lo (same swizzled layout,
-//               the split is elementwise) into a 2-stage operand ring;
-//   warp 1      MMA issuer (one thread): 3 x 4 tcgen05.mma.kind::tf32
-//               (M=128, N=32, K=8) per chunk into one of two TMEM
-//               accumulators (2 x 32 columns); tcgen05.commit frees the
-//               operand slot / publishes the accumulator;
-//   warps 6-9   epilogue: tcgen05.ld 32x32b.x32 (thread = centroid row, its
-//               32 query-token scores in registers) -> S row (128 B store),
-//               row max, keep bit (ballot -> one 32-bit word per warp), and
-//               the per-token top-nprobe keys after a 32x32 smem transpose
-//               (lane = query token), as in the CUDA-core kernel.
-// The raw ring is released by the splitters, not by the MMA, so HBM streaming
-// never waits on tensor-core completion.  Q (32 x 128) is split once per CTA.
+//               SWIZZLE_128B) into a 10-stage ring (160 KB in flight);
+//   warps 2-5   splitters: thread = centroid row; read the row's 32 floats of
+//               a landed box (conflict-free LDS.128 through the swizzle),
+//               release the smem slot, split, and write hi/lo straight into
+//               TMEM (tcgen05.st 32x32b.x32: lane = row, column = k) — the A
+//               operand never goes back to shared memory;
+//   warp 1      MMA issuer (one thread): per chunk 3 x 4 tcgen05.mma.kind::tf32
+//               M=128 N=32 K=8 with A from TMEM and B = Q_hi/Q_lo from smem,
+//               into four K-split accumulators (independent MMA chains);
+//   warps 6-9   epilogue: tcgen05.ld of the four accumulators, S = sum, then
+//               the S row store (128 B), row max, keep bit (ballot -> one
+//               32-bit word per warp), and the per-token top-nprobe keys via a
+//               per-token score threshold + ballot (inserts are rare).
+// TMEM: [0,256) two accumulator buffers x 4 x 32 columns; [256,384) two
+// operand slots x (32 hi + 32 lo) columns.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -38,25 +39,41 @@
 namespace plaid {
 namespace {
 
-constexpr int kRaw = 6;                      // raw (TMA) ring depth
-constexpr int kOps = 2;                      // hi/lo operand ring depth
+constexpr int kRaw = 10;                     // TMA ring depth
+constexpr int kOps = 2;                      // TMEM operand slots
 constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 32 fp32
 constexpr uint32_t kQChunkBytes = 32 * 128;  // 32 rows x 32 fp32
 constexpr int kThreads = 320;
-constexpr uint32_t kTmemCols = 64;           // two 32-column accumulators
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kAccCols = 128;           // 4 K-split accumulators x 32 columns
+constexpr uint32_t kOpsCol0 = 256;           // first operand-slot column
 constexpr int kDim = 128;
 constexpr int kChunks = kDim / 32;
 
 // shared-memory carve-up (offsets from a 1024-B aligned base)
 constexpr uint32_t kOffRaw = 0;
-constexpr uint32_t kOffHi = kOffRaw + kRaw * kChunkBytes;
-constexpr uint32_t kOffLo = kOffHi + kOps * kChunkBytes;
-constexpr uint32_t kOffQHi = kOffLo + kOps * kChunkBytes;
+constexpr uint32_t kOffQHi = kOffRaw + kRaw * kChunkBytes;
 constexpr uint32_t kOffQLo = kOffQHi + kChunks * kQChunkBytes;
 constexpr uint32_t kOffTr = kOffQLo + kChunks * kQChunkBytes;  // 4 warps x 32 x 33 floats
 constexpr uint32_t kOffBar = kOffTr + 4 * 32 * 33 * 4;
 constexpr uint32_t kNumBars = 2 * kRaw + 2 * kOps + 4;
 constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
+
+// Debug timeline (dbg & 16): globaltimer stamps of CTA 0's pipeline events
+// and every CTA's begin/end (read back with plaid_debug_tf32_trace).
+__device__ unsigned long long g_tf32_trace[8 * 256];
+__device__ unsigned long long g_tf32_cta[2 * 256];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_stamp(uint32_t dbg, int slot, uint32_t i) {
+    if ((dbg & 16) && blockIdx.x == 0 && i < 256) g_tf32_trace[slot * 256 + i] = gtime();
+}
+__device__ __forceinline__ void cta_stamp(uint32_t dbg, int which) {
+    if ((dbg & 16) && threadIdx.x == 0 && blockIdx.x < 256) g_tf32_cta[which * 256 + blockIdx.x] = gtime();
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -78,9 +95,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 
@@ -107,12 +124,13 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
 // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N=32, M=128.
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
 
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+// D[tmem] (+)= A[tmem] . B[smem]
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(kIdesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -120,30 +138,46 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                  : "memory");
 }
 
+// 32 consecutive TMEM columns of this warp's 32 lanes -> r[0..31] (waits).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// r[0..31] -> 32 consecutive TMEM columns of this warp's 32 lanes (no wait).
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
 __device__ __forceinline__ uint32_t split_hi(uint32_t x) { return x & 0xFFFFE000u; }
 
 // lo rounded to the nearest tf32 (the tensor core would otherwise truncate
 // its low 13 bits, a one-sided error that biases every dot product)
-__device__ __forceinline__ float tf32_rn(float x) {
-    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
-
-__device__ __forceinline__ void split4(float4 v, float4& h, float4& l) {
-    h.x = __uint_as_float(split_hi(__float_as_uint(v.x)));
-    h.y = __uint_as_float(split_hi(__float_as_uint(v.y)));
-    h.z = __uint_as_float(split_hi(__float_as_uint(v.z)));
-    h.w = __uint_as_float(split_hi(__float_as_uint(v.w)));
-    l.x = tf32_rn(__fsub_rn(v.x, h.x));
-    l.y = tf32_rn(__fsub_rn(v.y, h.y));
-    l.z = tf32_rn(__fsub_rn(v.z, h.z));
-    l.w = tf32_rn(__fsub_rn(v.w, h.w));
+__device__ __forceinline__ uint32_t split_lo(uint32_t x) {
+    const float lo = __fsub_rn(__uint_as_float(x), __uint_as_float(split_hi(x)));
+    return (__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u;
 }
 
 template <int NP>
 __global__ void __launch_bounds__(kThreads, 1)
 scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const float* __restrict__ Q,
                    uint32_t rows, float t_cs, float* __restrict__ S, float* __restrict__ rowmax,
-                   uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ partial) {
+                   uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ partial, uint32_t* __restrict__ gthr,
+                   uint32_t dbg) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     // align within the shared window (pointer stays in the shared address space)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -159,6 +193,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + kNumBars * 8);
 
     const uint64_t ntiles = (K + 127) / 128;
+    cta_stamp(dbg, 0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRaw; ++s) {
@@ -186,13 +221,12 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
     for (uint32_t e = threadIdx.x; e < 32 * (kDim / 4); e += kThreads) {
         const uint32_t r = e / (kDim / 4), g = e % (kDim / 4);
         const uint32_t kc = g / 8, j = g % 8;
-        float4 v = r < rows ? reinterpret_cast<const float4*>(Q + uint64_t(r) * kDim)[g]
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        uint4 v = r < rows ? reinterpret_cast<const uint4*>(Q + uint64_t(r) * kDim)[g] : make_uint4(0, 0, 0, 0);
         const uint32_t off = kc * kQChunkBytes + r * 128 + ((j ^ (r & 7)) << 4);
-        float4 h, l;
-        split4(v, h, l);
-        *reinterpret_cast<float4*>(smem + kOffQHi + off) = h;
-        *reinterpret_cast<float4*>(smem + kOffQLo + off) = l;
+        *reinterpret_cast<uint4*>(smem + kOffQHi + off) =
+            make_uint4(split_hi(v.x), split_hi(v.y), split_hi(v.z), split_hi(v.w));
+        *reinterpret_cast<uint4*>(smem + kOffQLo + off) =
+            make_uint4(split_lo(v.x), split_lo(v.y), split_lo(v.z), split_lo(v.w));
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -209,6 +243,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                     const int s = g % kRaw;
                     const uint32_t ph = (g / kRaw) & 1;
                     mbar_wait(raw_empty(s), ph ^ 1);
+                    trace_stamp(dbg, 0, g);
                     mbar_expect_tx(raw_full(s), kChunkBytes);
                     tma_load_2d(base + kOffRaw + s * kChunkBytes, &cmap, kc * 32, int(t * 128), raw_full(s));
                 }
@@ -220,21 +255,28 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
             mbar_wait(tempty_bar(acc), aph ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d = tmem_base + acc * 32;
+            const uint32_t d = tmem_base + acc * kAccCols;
             for (int kc = 0; kc < kChunks; ++kc, ++g) {
                 const int s = g % kOps;
                 const uint32_t ph = (g / kOps) & 1;
                 mbar_wait(ops_full(s), ph);
+                if (lane == 0) trace_stamp(dbg, 4, g);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
-                    const uint32_t ahi = base + kOffHi + s * kChunkBytes, alo = base + kOffLo + s * kChunkBytes;
+                    const uint32_t ahi = tmem_base + kOpsCol0 + s * 64, alo = ahi + 32;
                     const uint32_t bhi = base + kOffQHi + kc * kQChunkBytes, blo = base + kOffQLo + kc * kQChunkBytes;
+                    // four independent accumulators (one per K-step kk): no
+                    // MMA ever waits on the previous one's result
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t o = kk * 32;  // 8 tf32 along K
-                        mma_tf32(d, umma_desc(ahi + o), umma_desc(bhi + o), (kc | kk) != 0);
-                        mma_tf32(d, umma_desc(ahi + o), umma_desc(blo + o), 1);
-                        mma_tf32(d, umma_desc(alo + o), umma_desc(bhi + o), 1);
+                    for (int kk = 0; kk < 4; ++kk)
+                        mma_tf32_ts(d + kk * 32, ahi + kk * 8, umma_desc(bhi + kk * 32), kc != 0);
+                    if (!(dbg & 2)) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_tf32_ts(d + kk * 32, ahi + kk * 8, umma_desc(blo + kk * 32), 1);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_tf32_ts(d + kk * 32, alo + kk * 8, umma_desc(bhi + kk * 32), 1);
                     }
                     mma_commit(ops_empty(s));
                     if (kc == kChunks - 1) mma_commit(tfull_bar(acc));
@@ -243,8 +285,9 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             }
         }
     } else if (warp < 6) {
-        // ---------------- splitters (128 threads)
-        const uint32_t tid = threadIdx.x - 64;
+        // ---------------- splitters: thread = row (TMEM lane quarter warp % 4)
+        const uint32_t row = (warp & 3) * 32 + lane;
+        const uint32_t lane_off = ((warp & 3) * 32) << 16;
         uint32_t g = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
             for (int kc = 0; kc < kChunks; ++kc, ++g) {
@@ -253,49 +296,67 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                 const int o = g % kOps;
                 const uint32_t oph = (g / kOps) & 1;
                 mbar_wait(raw_full(s), ph);
-                const float4* a = reinterpret_cast<const float4*>(smem + kOffRaw + s * kChunkBytes);
-                float4 h[8], l[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) split4(a[tid + j * 128], h[j], l[j]);
-                // the split consumed every loaded value, so the raw slot can go
-                // back to the TMA producer before the outputs are written
-                mbar_arrive(raw_empty(s));
-                mbar_wait(ops_empty(o), oph ^ 1);
-                float4* hi = reinterpret_cast<float4*>(smem + kOffHi + o * kChunkBytes);
-                float4* lo = reinterpret_cast<float4*>(smem + kOffLo + o * kChunkBytes);
+                if (warp == 2 && lane == 0) trace_stamp(dbg, 1, g);
+                // the row's 8 granules, un-swizzled: granule j at (j ^ (row & 7))
+                const uint4* src = reinterpret_cast<const uint4*>(smem + kOffRaw + s * kChunkBytes + row * 128);
+                uint32_t hi[32], lo[32];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    hi[tid + j * 128] = h[j];
-                    lo[tid + j * 128] = l[j];
+                    const uint4 v = src[j ^ (row & 7)];
+                    hi[4 * j + 0] = split_hi(v.x);
+                    hi[4 * j + 1] = split_hi(v.y);
+                    hi[4 * j + 2] = split_hi(v.z);
+                    hi[4 * j + 3] = split_hi(v.w);
+                    lo[4 * j + 0] = split_lo(v.x);
+                    lo[4 * j + 1] = split_lo(v.y);
+                    lo[4 * j + 2] = split_lo(v.z);
+                    lo[4 * j + 3] = split_lo(v.w);
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                // every loaded value has been consumed: the smem slot is free
+                mbar_arrive(raw_empty(s));
+                mbar_wait(ops_empty(o), oph ^ 1);
+                if (warp == 2 && lane == 0) trace_stamp(dbg, 2, g);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t col = tmem_base + lane_off + kOpsCol0 + o * 64;
+                if (!(dbg & 4)) {
+                    tmem_st32(col, hi);
+                    tmem_st32(col + 32, lo);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(ops_full(o));
+                if (warp == 2 && lane == 0) trace_stamp(dbg, 3, g);
             }
     } else {
         // ---------------- epilogue (warps 6..9 -> TMEM lane quarters 2,3,0,1)
         const uint32_t q = warp & 3;
-        const uint32_t ew = warp - 6;
-        float* tr = reinterpret_cast<float*>(smem + kOffTr) + ew * 32 * 33;
         uint64_t top[NP];
 #pragma unroll
         for (int j = 0; j < NP; ++j) top[j] = 0;
+        // thr: score of this lane's (token's) NP-th best key (-inf until the
+        // list is full); later centroids of this warp have larger ids, so they
+        // can only enter the list with a strictly larger score
+        float thr = -INFINITY;
+        float* tr = reinterpret_cast<float*>(smem + kOffTr) + (warp - 6) * 32 * 33;
         uint32_t lt = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
             const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
             mbar_wait(tfull_bar(acc), aph);
+            if (warp == 6 && lane == 0) trace_stamp(dbg, 5, lt);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // S = D0 + D1 + D2 + D3 (the K-split accumulators)
+            const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * kAccCols;
             uint32_t r[32];
-            const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * 32;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float v[32];
+            tmem_ld32(taddr, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll
+            for (int a = 1; a < 4; ++a) {
+                tmem_ld32(taddr + a * 32, r);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], __uint_as_float(r[j]));
+            }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(tempty_bar(acc));
 
@@ -305,32 +366,44 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             float m = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                if (uint32_t(j) < rows) m = dev::max_gt(m, __uint_as_float(r[j]));
+                if (uint32_t(j) < rows) m = dev::max_gt(m, v[j]);
             const uint32_t kw = __ballot_sync(0xffffffffu, valid && m >= t_cs);
             if (lane == 0 && c0 < K) keep_bits[c0 >> 5] = kw;
-            if (valid) {
+            if (valid && !(dbg & 8)) {
                 rowmax[c] = m;
                 float4* dst = reinterpret_cast<float4*>(S + c * kScoresPitch);
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
-            // transpose the warp's 32 x 32 block: lane = query token
+            if (warp == 6 && lane == 0) trace_stamp(dbg, 7, lt);
+            // per-token top-NP after a 32x32 transpose: lane = query token,
+            // scanning this warp's 32 centroids; a float threshold filters
+            // out all but the (rare) keys that enter the list
 #pragma unroll
-            for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = v[j];
             __syncwarp();
             if (lane < rows) {
-                const uint32_t nv = K - c0 < 32 ? uint32_t(K - c0) : 32u;
-                // cheap pre-filter: only keys above the current NP-th best
+                // grid-wide bound: some warp already holds NP keys scoring >=
+                // gb for this token, so a score below gb cannot reach the
+                // global top-NP (ties at gb are kept)
+                const uint32_t go = __ldcg(gthr + lane);
+                const float gb = go ? dev::unord_f32(go) : -INFINITY;
+                const uint32_t nv = (dbg & 1) ? 1u : (K - c0 < 32 ? uint32_t(K - c0) : 32u);
+                const float thr0 = thr;
+#pragma unroll 8
                 for (uint32_t rr = 0; rr < nv; ++rr) {
-                    const uint64_t key = dev::make_key(tr[rr * 33 + lane], uint32_t(c0 + rr));
-                    if (key > top[NP - 1]) dev::topn_insert<NP>(top, key);
+                    const float sc = tr[rr * 33 + lane];
+                    if (sc > thr && sc >= gb) {
+                        dev::topn_insert<NP>(top, dev::make_key(sc, uint32_t(c0 + rr)));
+                        if (top[NP - 1]) thr = dev::key_score(top[NP - 1]);
+                    }
                 }
+                if (thr > thr0 && thr > gb) atomicMax(gthr + lane, dev::ord_f32(thr));
             }
             __syncwarp();
+            if (warp == 6 && lane == 0) trace_stamp(dbg, 6, lt);
         }
-        uint64_t* out = partial + ((uint64_t(blockIdx.x) * 4 + ew) * 32 + lane) * NP;
+        uint64_t* out = partial + ((uint64_t(blockIdx.x) * 4 + (warp - 6)) * 32 + lane) * NP;
 #pragma unroll
         for (int j = 0; j < NP; ++j) out[j] = top[j];
     }
@@ -338,6 +411,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
     __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+    cta_stamp(dbg, 1);
 }
 
 int sm_count() {
@@ -352,13 +426,19 @@ int sm_count() {
 
 template <int NP>
 void launch_tf32(const CUtensorMap& map, const IndexView& ix, const float* q, uint32_t rows, float t_cs,
-                 float* S, float* rowmax, uint32_t* keep, uint64_t* partial, uint32_t grid, cudaStream_t st) {
+                 float* S, float* rowmax, uint32_t* keep, uint64_t* partial, uint32_t* gthr, uint32_t grid,
+                 cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(scores_tf32_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         configured = true;
     }
-    scores_tf32_kernel<NP><<<grid, kThreads, kSmemBytes, st>>>(map, ix.K, q, rows, t_cs, S, rowmax, keep, partial);
+    static const uint32_t dbg = [] {
+        const char* e = getenv("PLAID_TF32_DBG");
+        return e ? uint32_t(atoi(e)) : 0u;
+    }();
+    scores_tf32_kernel<NP><<<grid, kThreads, kSmemBytes, st>>>(map, ix.K, q, rows, t_cs, S, rowmax, keep, partial, gthr,
+                                                               dbg);
     launch::count_launch();
 }
 
@@ -385,21 +465,29 @@ void make_centroid_tensor_map(const IndexView& ix, void* out_map) {
 
 uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
                        float* d_scores, float* d_rowmax, uint32_t* d_keep_bits, uint64_t* d_partial,
-                       uint32_t np_bucket, cudaStream_t st) {
+                       uint32_t np_bucket, uint32_t* d_gthr, cudaStream_t st) {
     const CUtensorMap& map = *static_cast<const CUtensorMap*>(cmap);
     const uint64_t ntiles = (ix.K + 127) / 128;
     uint32_t grid = uint32_t(ntiles < uint64_t(sm_count()) ? ntiles : uint64_t(sm_count()));
     if (grid == 0) grid = 1;
     switch (np_bucket) {
-        case 1: launch_tf32<1>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
-        case 2: launch_tf32<2>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
-        case 4: launch_tf32<4>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
-        case 8: launch_tf32<8>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
-        case 16: launch_tf32<16>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
-        default: launch_tf32<32>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, grid, st); break;
+        case 1: launch_tf32<1>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 2: launch_tf32<2>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 4: launch_tf32<4>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 8: launch_tf32<8>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 16: launch_tf32<16>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        default: launch_tf32<32>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
     }
     return grid * 4;
 }
 
 }  // namespace launch
 }  // namespace plaid
+
+// Debug: copy the pipeline timeline (see trace_stamp / cta_stamp) to the host:
+// out[0..2048) = CTA 0 events, out[2048..2560) = per-CTA begin/end.
+extern "C" int plaid_debug_tf32_trace(unsigned long long* out) {
+    int rc = int(cudaMemcpyFromSymbol(out, plaid::g_tf32_trace, sizeof(plaid::g_tf32_trace)));
+    if (!rc) rc = int(cudaMemcpyFromSymbol(out + 8 * 256, plaid::g_tf32_cta, sizeof(plaid::g_tf32_cta)));
+    return rc;
+}

@@ -50,9 +50,10 @@ uint32_t scores_max_warps();
 // `cmap` is a CUtensorMap (128 B) made by make_centroid_tensor_map.
 bool tensor_scores_supported(const IndexView& ix);
 void make_centroid_tensor_map(const IndexView& ix, void* out_map);
+// d_gthr: 32 u32 per-token grid-wide top-nprobe bounds, zeroed before the launch.
 uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
                        float* d_scores, float* d_rowmax, uint32_t* d_keep_bits, uint64_t* d_partial,
-                       uint32_t np_bucket, cudaStream_t st);
+                       uint32_t np_bucket, uint32_t* d_gthr, cudaStream_t st);
 uint32_t scores_tensor_max_warps();
 [[noreturn]] void fail_cuda_driver(int code, const char* what);
 // Merge per-warp partial top-NP lists into sel[rows][nprobe] centroid ids.
