@@ -70,7 +70,7 @@ def build_plaid(verbose: bool = False, jobs: int = 8) -> Path:
         list(ex.map(lambda c: _run(c, verbose), jobs_list))
     so = LIB / "libplaid.so"
     if jobs_list or _stale(so, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(so), *map(str, objs), "-lcuda"], verbose)
+        _run([NVCC, *ARCH, "-shared", "-o", str(so), *map(str, objs)], verbose)
     return so
 
 

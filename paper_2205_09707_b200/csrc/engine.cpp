@@ -315,7 +315,7 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         scores_.ensure(ix.K * kScoresPitch);
         rowmax_.ensure(ix.K);
         keep_.ensure((ix.K + 31) / 32);
-        npartial_warps_ = launch::scores_max_warps();
+        npartial_warps_ = std::max(launch::scores_max_warps(), launch::scores_tensor_max_warps());
         partial_.ensure(npartial_warps_ * 32 * 32);
         chunk_counts_.ensure(launch::bitmap_chunks(ix.N));
         c1_.ensure(ix.N);
@@ -331,7 +331,7 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
 uint32_t Searcher::launch_scores(const float* d_q, uint32_t rows, float t_cs, uint32_t npb, cudaStream_t st) {
     const IndexView& ix = index_->view();
     if (tensor_)
-        return launch::scores_tensor(tmap_, ix, d_q, rows, t_cs, scores_.p, rowmax_.p, keep_.p, partial_.p, npb,
+        return launch::scores_tensor(tmap_, ix, d_q, rows, t_cs, scores_.p, keep_.p, partial_.p, npb,
                                      reinterpret_cast<uint32_t*>(counters_.p + kGthr), st);
     return launch::scores_exact(ix, d_q, rows, t_cs, scores_.p, rowmax_.p, keep_.p, partial_.p, npb, st);
 }
@@ -602,10 +602,17 @@ void Searcher::compute_centroid_scores(const float* q, uint64_t rows, uint64_t d
     launch_scores(q_.p, uint32_t(rows), INFINITY, 1, stream_);
     std::vector<float> S(ix.K * kScoresPitch);
     d2h(S.data(), scores_.p, S.size(), stream_);
-    d2h(row_max, rowmax_.p, ix.K, stream_);
+    if (!tensor_) d2h(row_max, rowmax_.p, ix.K, stream_);
     PLAID_CUDA(cudaStreamSynchronize(stream_));
-    for (uint64_t c = 0; c < ix.K; ++c)
+    for (uint64_t c = 0; c < ix.K; ++c) {
         std::memcpy(scores + c * rows, S.data() + c * kScoresPitch, rows * sizeof(float));
+        if (tensor_) {  // the tensor kernel emits keep bits, not row maxima (pipeline.cpp:40-46)
+            float m = -INFINITY;
+            for (uint64_t i = 0; i < rows; ++i)
+                if (S[c * kScoresPitch + i] > m) m = S[c * kScoresPitch + i];
+            row_max[c] = m;
+        }
+    }
 }
 
 void Searcher::generate_candidates(const float* scores, uint64_t rows, uint64_t nprobe,
@@ -632,7 +639,9 @@ void Searcher::generate_candidates(const float* scores, uint64_t rows, uint64_t 
         nsel = ix.K;
     } else if (nprobe <= 32) {
         const uint32_t npb = np_bucket(nprobe);
-        const uint32_t w = launch::topn_from_scores(scores_.p, ix.K, uint32_t(rows), partial_.p, npb, stream_);
+        PLAID_CUDA(cudaMemsetAsync(counters_.p + kGthr, 0, 16 * sizeof(uint64_t), stream_));
+        const uint32_t w = launch::topn_from_scores(scores_.p, ix.K, uint32_t(rows), partial_.p, npb,
+                                                    reinterpret_cast<uint32_t*>(counters_.p + kGthr), stream_);
         launch::topn_merge(partial_.p, w, npb, uint32_t(rows), uint32_t(nprobe), sel_.p, stream_);
         nsel = rows * nprobe;
     } else {

@@ -1,32 +1,43 @@
 // gemm_tf32.cu — stage-1 S_cq = C . Q^T on the 5th-gen tensor cores (tcgen05),
 // the production score path (PLAID_SCORES_TENSOR).  Replaces the reference's
-// scalar compute_centroid_scores (pipeline.cpp:26-50).
+// scalar compute_centroid_scores (pipeline.cpp:26-50) and fuses the two
+// consumers of S that follow it: the per-token top-nprobe selection
+// (pipeline.cpp:52-88) and the t_cs keep mask of centroid pruning
+// (pipeline.cpp:90-110).
 //
 // Precision: 3xTF32.  Each fp32 operand is split into hi = x with the low 13
-// mantissa bits cleared and lo = tf32_rn(x - hi), and
+// mantissa bits cleared and lo = tf32_rn(x - hi) (rounded: the tensor core
+// truncates fp32 operands to tf32, tools/tf32_round.cu), and
 // S = C_hi.Q_hi + C_hi.Q_lo + C_lo.Q_hi is accumulated in fp32 in TMEM: ~2e-6
-// absolute on unit-vector dots (tests/test_gpu_parity.py), while the HBM
-// traffic stays one fp32 read of C.  Decisions that depend on S (top-nprobe,
-// t_cs) can differ from the reference only for scores that close to a
-// boundary.
+// absolute on unit-vector dots (tests/test_gpu_parity.py), while HBM traffic
+// stays one fp32 read of C.
 //
-// Structure (persistent, one CTA per SM, 10 warps):
+// Structure (persistent, one CTA per SM, 16 warps):
 //   warp 0      TMA producer: 128-centroid x 32-dim fp32 boxes (16 KB,
-//               SWIZZLE_128B) into a 10-stage ring (160 KB in flight);
-//   warps 2-5   splitters: thread = centroid row; read the row's 32 floats of
-//               a landed box (conflict-free LDS.128 through the swizzle),
-//               release the smem slot, split, and write hi/lo straight into
-//               TMEM (tcgen05.st 32x32b.x32: lane = row, column = k) — the A
-//               operand never goes back to shared memory;
-//   warp 1      MMA issuer (one thread): per chunk 3 x 4 tcgen05.mma.kind::tf32
-//               M=128 N=32 K=8 with A from TMEM and B = Q_hi/Q_lo from smem,
-//               into four K-split accumulators (independent MMA chains);
-//   warps 6-9   epilogue: tcgen05.ld of the four accumulators, S = sum, then
-//               the S row store (128 B), row max, keep bit (ballot -> one
-//               32-bit word per warp), and the per-token top-nprobe keys via a
-//               per-token score threshold + ballot (inserts are rare).
-// TMEM: [0,256) two accumulator buffers x 4 x 32 columns; [256,384) two
-// operand slots x (32 hi + 32 lo) columns.
+//               SWIZZLE_128B) into a 9-stage ring (144 KB in flight);
+//   warps 4-7   converters: thread = centroid row; read the row's 32 floats
+//               of a landed box (conflict-free LDS.128 through the swizzle),
+//               release the slot, split, and write C_hi / C_lo straight into
+//               TMEM (tcgen05.st: lane = row, column = k) — the MMA A operand;
+//   warp 1      MMA issuer (one thread): per 8-dim step one M=128 N=64 MMA
+//               C_hi . [Q_hi | Q_lo] and one N=32 MMA C_lo . Q_hi into the
+//               same accumulator, B = Q from shared memory (8 KB per chunk);
+//   warps 8-15  epilogue, two groups of four taking alternate tiles (group g
+//               owns accumulator g): tcgen05.ld of the 64 accumulator
+//               columns, S = hi + lo products, the keep bit (row max >= t_cs
+//               -> one ballot -> one 32-bit word), a 32x32 transpose through
+//               shared memory, then lane = token: the S row stores (one
+//               coalesced 128-byte row per centroid) and the per-token
+//               top-nprobe (score, id) list, where a float threshold plus
+//               CTA- and grid-wide bounds make inserts rare;
+//   warps 2-3   idle.
+// Shared-memory traffic per 128-centroid tile is ~200 KB (TMA write, converter
+// read, MMA B reads, transpose): ~0.8 us at 128 B/clk, under the ~1.5 us the
+// tile takes to stream from HBM when all 148 SMs pull at once.  (The first
+// design, with C as the smem B operand split in shared memory, moved ~384 KB
+// per tile and was shared-memory bound at ~2 us per tile.)
+// TMEM: [0,128) two 64-column accumulators; [128,512) six operand slots of
+// 32 C_hi + 32 C_lo columns.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -39,28 +50,36 @@
 namespace plaid {
 namespace {
 
-constexpr int kRaw = 10;                     // TMA ring depth
-constexpr int kOps = 2;                      // TMEM operand slots
+constexpr int kRaw = 9;                      // TMA ring depth
+constexpr int kOps = 6;                      // TMEM operand slots
 constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 32 fp32
-constexpr uint32_t kQChunkBytes = 32 * 128;  // 32 rows x 32 fp32
-constexpr int kThreads = 320;
+constexpr uint32_t kQChunkBytes = 64 * 128;  // [Q_hi; Q_lo] 64 rows x 32 fp32
+constexpr int kThreads = 512;
+constexpr int kEpiWarps = 8;                 // warps 8..15
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAccCols = 128;           // 4 K-split accumulators x 32 columns
-constexpr uint32_t kOpsCol0 = 256;           // first operand-slot column
+constexpr uint32_t kAccCols = 64;            // 32 hi-product + 32 lo-product columns
+constexpr uint32_t kOpsCol0 = 128;           // first operand-slot column
 constexpr int kDim = 128;
 constexpr int kChunks = kDim / 32;
 
 // shared-memory carve-up (offsets from a 1024-B aligned base)
 constexpr uint32_t kOffRaw = 0;
-constexpr uint32_t kOffQHi = kOffRaw + kRaw * kChunkBytes;
-constexpr uint32_t kOffQLo = kOffQHi + kChunks * kQChunkBytes;
-constexpr uint32_t kOffTr = kOffQLo + kChunks * kQChunkBytes;  // 4 warps x 32 x 33 floats
-constexpr uint32_t kOffBar = kOffTr + 4 * 32 * 33 * 4;
+constexpr uint32_t kOffQ = kOffRaw + kRaw * kChunkBytes;
+constexpr uint32_t kOffTr = kOffQ + kChunks * kQChunkBytes;  // 4 warps x 32 x 33 floats
+constexpr uint32_t kOffBar = kOffTr + kEpiWarps * 32 * 33 * 4;
 constexpr uint32_t kNumBars = 2 * kRaw + 2 * kOps + 4;
-constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + alignment slack
+constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;  // tmem slot (16 B) + CTA bounds (128 B)
+constexpr uint32_t kSmemBytes = kOffMisc + 16 + 128 + 1024;  // + alignment slack
 
-// Debug timeline (dbg & 16): globaltimer stamps of CTA 0's pipeline events
-// and every CTA's begin/end (read back with plaid_debug_tf32_trace).
+// kind::tf32 instruction descriptors: D f32, A/B tf32, both K-major, M=128.
+constexpr uint32_t idesc_tf32(uint32_t n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+constexpr uint32_t kIdesc64 = idesc_tf32(64);
+constexpr uint32_t kIdesc32 = idesc_tf32(32);
+
+// Debug timeline (PLAID_TF32_DBG=16): globaltimer stamps of CTA 0's pipeline
+// events and every CTA's begin/end (read back with plaid_debug_tf32_trace).
 __device__ unsigned long long g_tf32_trace[8 * 256];
 __device__ unsigned long long g_tf32_cta[2 * 256];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -95,9 +114,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity), "r"(0x989680u)
+        "r"(parity)
         : "memory");
 }
 
@@ -121,16 +140,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
     return d;
 }
 
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N=32, M=128.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
-
 // D[tmem] (+)= A[tmem] . B[smem]
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                       uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(kIdesc), "r"(accumulate));
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -138,7 +155,7 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                  : "memory");
 }
 
-// 32 consecutive TMEM columns of this warp's 32 lanes -> r[0..31] (waits).
+// 32 consecutive TMEM columns of this warp's 32 lanes -> r[0..31] (no wait).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -148,10 +165,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// r[0..31] -> 32 consecutive TMEM columns of this warp's 32 lanes (no wait).
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// r[0..31] -> 32 consecutive TMEM columns of this warp's 32 lanes.
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -165,8 +183,8 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 
 __device__ __forceinline__ uint32_t split_hi(uint32_t x) { return x & 0xFFFFE000u; }
 
-// lo rounded to the nearest tf32 (the tensor core would otherwise truncate
-// its low 13 bits, a one-sided error that biases every dot product)
+// x - trunc_tf32(x) rounded to the nearest tf32 (an unrounded lo would be
+// truncated again by the tensor core and bias every dot product downwards)
 __device__ __forceinline__ uint32_t split_lo(uint32_t x) {
     const float lo = __fsub_rn(__uint_as_float(x), __uint_as_float(split_hi(x)));
     return (__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u;
@@ -175,11 +193,9 @@ __device__ __forceinline__ uint32_t split_lo(uint32_t x) {
 template <int NP>
 __global__ void __launch_bounds__(kThreads, 1)
 scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const float* __restrict__ Q,
-                   uint32_t rows, float t_cs, float* __restrict__ S, float* __restrict__ rowmax,
-                   uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ partial, uint32_t* __restrict__ gthr,
-                   uint32_t dbg) {
+                   uint32_t rows, float t_cs, float* __restrict__ S, uint32_t* __restrict__ keep_bits,
+                   uint64_t* __restrict__ partial, uint32_t* __restrict__ gthr, uint32_t dbg) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    // align within the shared window (pointer stays in the shared address space)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t base = smem_u32(smem);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -190,43 +206,45 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
     auto ops_empty = [&](int s) { return bar0 + 8u * (2 * kRaw + kOps + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kRaw + 2 * kOps + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kRaw + 2 * kOps + 2 + a); };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + kNumBars * 8);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffMisc);
+    // CTA-wide per-token bound (ordered float bits, 0 = none)
+    volatile uint32_t* cthr = reinterpret_cast<volatile uint32_t*>(smem + kOffMisc + 16);
 
     const uint64_t ntiles = (K + 127) / 128;
     cta_stamp(dbg, 0);
-
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRaw; ++s) {
             mbar_init(raw_full(s), 1);
-            mbar_init(raw_empty(s), 128);
+            mbar_init(raw_empty(s), 4);  // one arrive per converter warp
         }
         for (int s = 0; s < kOps; ++s) {
-            mbar_init(ops_full(s), 128);
+            mbar_init(ops_full(s), 4);
             mbar_init(ops_empty(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), 128);
+            mbar_init(tempty_bar(a), kEpiWarps / 2);  // the 4 warps of group a
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&cmap)) : "memory");
     }
+    if (threadIdx.x < 32) cthr[threadIdx.x] = 0;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // Q -> hi/lo, SWIZZLE_128B K-major: row r, 16-byte granule j of chunk kc at
-    // kc*4096 + r*128 + ((j ^ (r & 7)) << 4)
-    for (uint32_t e = threadIdx.x; e < 32 * (kDim / 4); e += kThreads) {
-        const uint32_t r = e / (kDim / 4), g = e % (kDim / 4);
-        const uint32_t kc = g / 8, j = g % 8;
-        uint4 v = r < rows ? reinterpret_cast<const uint4*>(Q + uint64_t(r) * kDim)[g] : make_uint4(0, 0, 0, 0);
-        const uint32_t off = kc * kQChunkBytes + r * 128 + ((j ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(smem + kOffQHi + off) =
-            make_uint4(split_hi(v.x), split_hi(v.y), split_hi(v.z), split_hi(v.w));
-        *reinterpret_cast<uint4*>(smem + kOffQLo + off) =
-            make_uint4(split_lo(v.x), split_lo(v.y), split_lo(v.z), split_lo(v.w));
+    // B operand [Q_hi; Q_lo] (row n < 32: Q_hi of token n, else Q_lo of token
+    // n - 32; zero rows past `rows`), SWIZZLE_128B K-major: row n, 16-byte
+    // granule j of chunk kc at kc*8192 + n*128 + ((j ^ (n & 7)) << 4)
+    for (uint32_t e = threadIdx.x; e < 64 * (kDim / 4); e += kThreads) {
+        const uint32_t n = e / (kDim / 4), g = e % (kDim / 4);
+        const uint32_t kc = g / 8, j = g % 8, tok = n & 31;
+        const uint4 v = tok < rows ? reinterpret_cast<const uint4*>(Q + uint64_t(tok) * kDim)[g] : make_uint4(0, 0, 0, 0);
+        const uint32_t off = kc * kQChunkBytes + n * 128 + ((j ^ (n & 7)) << 4);
+        *reinterpret_cast<uint4*>(smem + kOffQ + off) =
+            n < 32 ? make_uint4(split_hi(v.x), split_hi(v.y), split_hi(v.z), split_hi(v.w))
+                   : make_uint4(split_lo(v.x), split_lo(v.y), split_lo(v.z), split_lo(v.w));
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -241,8 +259,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
                 for (int kc = 0; kc < kChunks; ++kc, ++g) {
                     const int s = g % kRaw;
-                    const uint32_t ph = (g / kRaw) & 1;
-                    mbar_wait(raw_empty(s), ph ^ 1);
+                    mbar_wait(raw_empty(s), ((g / kRaw) & 1) ^ 1);
                     trace_stamp(dbg, 0, g);
                     mbar_expect_tx(raw_full(s), kChunkBytes);
                     tma_load_2d(base + kOffRaw + s * kChunkBytes, &cmap, kc * 32, int(t * 128), raw_full(s));
@@ -252,31 +269,24 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
         // ---------------- MMA issuer
         uint32_t g = 0, lt = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
-            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
-            mbar_wait(tempty_bar(acc), aph ^ 1);
+            const uint32_t acc = lt & 1;
+            mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t d = tmem_base + acc * kAccCols;
             for (int kc = 0; kc < kChunks; ++kc, ++g) {
                 const int s = g % kOps;
-                const uint32_t ph = (g / kOps) & 1;
-                mbar_wait(ops_full(s), ph);
+                mbar_wait(ops_full(s), (g / kOps) & 1);
                 if (lane == 0) trace_stamp(dbg, 4, g);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
                     const uint32_t ahi = tmem_base + kOpsCol0 + s * 64, alo = ahi + 32;
-                    const uint32_t bhi = base + kOffQHi + kc * kQChunkBytes, blo = base + kOffQLo + kc * kQChunkBytes;
-                    // four independent accumulators (one per K-step kk): no
-                    // MMA ever waits on the previous one's result
+                    const uint32_t bq = base + kOffQ + kc * kQChunkBytes;
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        mma_tf32_ts(d + kk * 32, ahi + kk * 8, umma_desc(bhi + kk * 32), kc != 0);
-                    if (!(dbg & 2)) {
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            mma_tf32_ts(d + kk * 32, ahi + kk * 8, umma_desc(blo + kk * 32), 1);
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            mma_tf32_ts(d + kk * 32, alo + kk * 8, umma_desc(bhi + kk * 32), 1);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        // D[:, 0:32] += C_hi.Q_hi, D[:, 32:64] += C_hi.Q_lo
+                        mma_ts(d, ahi + kk * 8, umma_desc(bq + kk * 32), kIdesc64, (kc | kk) != 0);
+                        // D[:, 0:32] += C_lo.Q_hi (B = the first 32 rows)
+                        mma_ts(d, alo + kk * 8, umma_desc(bq + kk * 32), kIdesc32, 1);
                     }
                     mma_commit(ops_empty(s));
                     if (kc == kChunks - 1) mma_commit(tfull_bar(acc));
@@ -284,19 +294,16 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                 __syncwarp();
             }
         }
-    } else if (warp < 6) {
-        // ---------------- splitters: thread = row (TMEM lane quarter warp % 4)
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- converters: thread = row (TMEM lane quarter warp % 4)
         const uint32_t row = (warp & 3) * 32 + lane;
         const uint32_t lane_off = ((warp & 3) * 32) << 16;
         uint32_t g = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
             for (int kc = 0; kc < kChunks; ++kc, ++g) {
-                const int s = g % kRaw;
-                const uint32_t ph = (g / kRaw) & 1;
-                const int o = g % kOps;
-                const uint32_t oph = (g / kOps) & 1;
-                mbar_wait(raw_full(s), ph);
-                if (warp == 2 && lane == 0) trace_stamp(dbg, 1, g);
+                const int s = g % kRaw, o = g % kOps;
+                mbar_wait(raw_full(s), (g / kRaw) & 1);
+                if (warp == 4 && lane == 0) trace_stamp(dbg, 1, g);
                 // the row's 8 granules, un-swizzled: granule j at (j ^ (row & 7))
                 const uint4* src = reinterpret_cast<const uint4*>(smem + kOffRaw + s * kChunkBytes + row * 128);
                 uint32_t hi[32], lo[32];
@@ -312,100 +319,119 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                     lo[4 * j + 2] = split_lo(v.z);
                     lo[4 * j + 3] = split_lo(v.w);
                 }
-                // every loaded value has been consumed: the smem slot is free
-                mbar_arrive(raw_empty(s));
-                mbar_wait(ops_empty(o), oph ^ 1);
-                if (warp == 2 && lane == 0) trace_stamp(dbg, 2, g);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(raw_empty(s));  // slot consumed
+                mbar_wait(ops_empty(o), ((g / kOps) & 1) ^ 1);
+                if (warp == 4 && lane == 0) trace_stamp(dbg, 2, g);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t col = tmem_base + lane_off + kOpsCol0 + o * 64;
-                if (!(dbg & 4)) {
-                    tmem_st32(col, hi);
-                    tmem_st32(col + 32, lo);
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                }
+                tmem_st32(col, hi);
+                tmem_st32(col + 32, lo);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(ops_full(o));
-                if (warp == 2 && lane == 0) trace_stamp(dbg, 3, g);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(ops_full(o));
+                if (warp == 4 && lane == 0) trace_stamp(dbg, 3, g);
             }
-    } else {
-        // ---------------- epilogue (warps 6..9 -> TMEM lane quarters 2,3,0,1)
-        const uint32_t q = warp & 3;
-        uint64_t top[NP];
+    } else if (warp >= 8) {
+        // ---------------- epilogue: two groups of 4 warps take alternate tiles
+        // (group = accumulator); thread = centroid row (lane quarter q)
+        const uint32_t q = warp & 3, ew = warp - 8, grp = ew >> 2;
+        // lane = query token after the transpose: this warp's best NP
+        // (score, centroid) pairs for it, descending.  Centroids arrive in
+        // increasing id order, so a later one enters only with a strictly
+        // larger score (reference tie order).  thr: the NP-th score (-inf
+        // until full); gb: a bound some list in the grid already reached
+        // (ties at gb are kept)
+        float top_s[NP];
+        uint32_t top_i[NP];
 #pragma unroll
-        for (int j = 0; j < NP; ++j) top[j] = 0;
-        // thr: score of this lane's (token's) NP-th best key (-inf until the
-        // list is full); later centroids of this warp have larger ids, so they
-        // can only enter the list with a strictly larger score
-        float thr = -INFINITY;
-        float* tr = reinterpret_cast<float*>(smem + kOffTr) + (warp - 6) * 32 * 33;
-        uint32_t lt = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
-            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
-            mbar_wait(tfull_bar(acc), aph);
-            if (warp == 6 && lane == 0) trace_stamp(dbg, 5, lt);
+        for (int j = 0; j < NP; ++j) top_s[j] = -INFINITY, top_i[j] = 0;
+        float gb = -INFINITY;
+        const bool tok = lane < rows;
+        float* tr = reinterpret_cast<float*>(smem + kOffTr) + ew * 32 * 33;
+        uint32_t lt = grp;
+        for (uint64_t t = blockIdx.x + uint64_t(grp) * gridDim.x; t < ntiles; t += 2ull * gridDim.x, lt += 2) {
+            const uint32_t acc = grp;
+            mbar_wait(tfull_bar(acc), (lt >> 1) & 1);
+            if (ew == 0 && lane == 0) trace_stamp(dbg, 5, lt);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            // S = D0 + D1 + D2 + D3 (the K-split accumulators)
             const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * kAccCols;
-            uint32_t r[32];
-            float v[32];
-            tmem_ld32(taddr, r);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-#pragma unroll
-            for (int a = 1; a < 4; ++a) {
-                tmem_ld32(taddr + a * 32, r);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], __uint_as_float(r[j]));
-            }
+            uint32_t rh[32], rl[32];
+            tmem_ld32(taddr, rh);
+            tmem_ld32(taddr + 32, rl);
+            tmem_ld_wait();
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(tempty_bar(acc));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar(acc));
 
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(__uint_as_float(rh[j]), __uint_as_float(rl[j]));
             const uint64_t c0 = t * 128 + q * 32;
             const uint64_t c = c0 + lane;
             const bool valid = c < K;
             float m = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                if (uint32_t(j) < rows) m = dev::max_gt(m, v[j]);
+                if (uint32_t(j) < rows) m = fmaxf(m, v[j]);
             const uint32_t kw = __ballot_sync(0xffffffffu, valid && m >= t_cs);
             if (lane == 0 && c0 < K) keep_bits[c0 >> 5] = kw;
-            if (valid && !(dbg & 8)) {
-                rowmax[c] = m;
-                float4* dst = reinterpret_cast<float4*>(S + c * kScoresPitch);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
-            if (warp == 6 && lane == 0) trace_stamp(dbg, 7, lt);
-            // per-token top-NP after a 32x32 transpose: lane = query token,
-            // scanning this warp's 32 centroids; a float threshold filters
-            // out all but the (rare) keys that enter the list
+            // 32x32 transpose: tr[centroid][token], pitch 33 (conflict-free both ways)
 #pragma unroll
             for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = v[j];
             __syncwarp();
-            if (lane < rows) {
-                // grid-wide bound: some warp already holds NP keys scoring >=
-                // gb for this token, so a score below gb cannot reach the
-                // global top-NP (ties at gb are kept)
-                const uint32_t go = __ldcg(gthr + lane);
-                const float gb = go ? dev::unord_f32(go) : -INFINITY;
-                const uint32_t nv = (dbg & 1) ? 1u : (K - c0 < 32 ? uint32_t(K - c0) : 32u);
-                const float thr0 = thr;
-#pragma unroll 8
-                for (uint32_t rr = 0; rr < nv; ++rr) {
-                    const float sc = tr[rr * 33 + lane];
-                    if (sc > thr && sc >= gb) {
-                        dev::topn_insert<NP>(top, dev::make_key(sc, uint32_t(c0 + rr)));
-                        if (top[NP - 1]) thr = dev::key_score(top[NP - 1]);
-                    }
-                }
-                if (thr > thr0 && thr > gb) atomicMax(gthr + lane, dev::ord_f32(thr));
+            if (tok) {
+                const uint32_t cb = cthr[lane];
+                if (cb) gb = fmaxf(gb, dev::unord_f32(cb));
             }
-            __syncwarp();
-            if (warp == 6 && lane == 0) trace_stamp(dbg, 6, lt);
-        }
-        uint64_t* out = partial + ((uint64_t(blockIdx.x) * 4 + (warp - 6)) * 32 + lane) * NP;
+            const float thr0 = top_s[NP - 1];
+            const uint32_t nv = K - c0 < 32 ? uint32_t(K - c0) : 32u;
+            uint32_t cand = 0;
+            // S rows from the transposed tile: one coalesced 128-byte row per
+            // centroid (lane = token)
 #pragma unroll
-        for (int j = 0; j < NP; ++j) out[j] = top[j];
+            for (int r = 0; r < 32; ++r) {
+                const float sc = tr[r * 33 + lane];
+                cand |= (uint32_t(r) < nv && tok && sc > thr0 && sc >= gb) ? (1u << r) : 0u;
+                if (uint32_t(r) < nv) S[(c0 + r) * kScoresPitch + lane] = sc;
+            }
+            // per-lane inserts, rare once the bounds have risen
+            while (cand) {
+                const int r = __ffs(cand) - 1;
+                cand &= cand - 1;
+                const float sc = tr[r * 33 + lane];
+                if (sc > top_s[NP - 1] && sc >= gb) {
+                    const uint32_t id = uint32_t(c0 + r);
+                    // shift-insert; every position reads only old values
+#pragma unroll
+                    for (int j = NP - 1; j > 0; --j) {
+                        const bool up = sc > top_s[j - 1], here = sc > top_s[j];
+                        top_i[j] = up ? top_i[j - 1] : (here ? id : top_i[j]);
+                        top_s[j] = up ? top_s[j - 1] : (here ? sc : top_s[j]);
+                    }
+                    if (sc > top_s[0]) top_s[0] = sc, top_i[0] = id;
+                }
+            }
+            const float thr = top_s[NP - 1];
+            __syncwarp();
+            // bounds: CTA-wide in shared memory every tile; one warp trades it
+            // with the grid-wide `gthr` every 4th of its tiles (one L2 line
+            // that every CTA hits, so per-tile traffic there would serialise)
+            if (tok && thr > thr0 && thr > gb) {
+                atomicMax(const_cast<uint32_t*>(&cthr[lane]), dev::ord_f32(thr));
+                gb = thr;
+            }
+            if (ew == kEpiWarps - 1 && (lt & 7) == 7 && tok) {
+                const uint32_t mine = cthr[lane];
+                const uint32_t go = mine ? atomicMax(gthr + lane, mine) : __ldcg(gthr + lane);
+                if (go > mine) atomicMax(const_cast<uint32_t*>(&cthr[lane]), go);
+            }
+            if (ew == 0 && lane == 0) trace_stamp(dbg, 6, lt);
+        }
+        uint64_t* out = partial + ((uint64_t(blockIdx.x) * kEpiWarps + ew) * 32 + lane) * NP;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) out[j] = top_s[j] == -INFINITY ? 0 : dev::make_key(top_s[j], top_i[j]);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -425,9 +451,8 @@ int sm_count() {
 }
 
 template <int NP>
-void launch_tf32(const CUtensorMap& map, const IndexView& ix, const float* q, uint32_t rows, float t_cs,
-                 float* S, float* rowmax, uint32_t* keep, uint64_t* partial, uint32_t* gthr, uint32_t grid,
-                 cudaStream_t st) {
+void launch_tf32(const CUtensorMap& map, const IndexView& ix, const float* q, uint32_t rows, float t_cs, float* S,
+                 uint32_t* keep, uint64_t* partial, uint32_t* gthr, uint32_t grid, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(scores_tf32_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -437,8 +462,7 @@ void launch_tf32(const CUtensorMap& map, const IndexView& ix, const float* q, ui
         const char* e = getenv("PLAID_TF32_DBG");
         return e ? uint32_t(atoi(e)) : 0u;
     }();
-    scores_tf32_kernel<NP><<<grid, kThreads, kSmemBytes, st>>>(map, ix.K, q, rows, t_cs, S, rowmax, keep, partial, gthr,
-                                                               dbg);
+    scores_tf32_kernel<NP><<<grid, kThreads, kSmemBytes, st>>>(map, ix.K, q, rows, t_cs, S, keep, partial, gthr, dbg);
     launch::count_launch();
 }
 
@@ -448,37 +472,50 @@ namespace launch {
 
 bool tensor_scores_supported(const IndexView& ix) { return ix.dim == kDim && ix.K < (1ull << 31); }
 
-uint32_t scores_tensor_max_warps() { return uint32_t(sm_count()) * 4; }
-
 void make_centroid_tensor_map(const IndexView& ix, void* out_map) {
     CUtensorMap* map = static_cast<CUtensorMap*>(out_map);
     const cuuint64_t dims[2] = {cuuint64_t(kDim), cuuint64_t(ix.K)};
     const cuuint64_t strides[1] = {cuuint64_t(kDim) * sizeof(float)};
     const cuuint32_t box[2] = {32, 128};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                                              const_cast<float*>(ix.centroids), dims, strides, box, estr,
-                                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // through the runtime's driver entry point: the library does not link
+    // libcuda, so it loads (and exports its ABI) on hosts without a driver
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<EncodeFn>(fn);
+    }();
+    if (!encode) fail_cuda_driver(int(CUDA_ERROR_NOT_FOUND), "cuGetProcAddress(cuTensorMapEncodeTiled)");
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ix.centroids), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail_cuda_driver(int(r), "cuTensorMapEncodeTiled");
 }
 
+uint32_t scores_tensor_max_warps() { return uint32_t(sm_count()) * kEpiWarps; }
+
 uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
-                       float* d_scores, float* d_rowmax, uint32_t* d_keep_bits, uint64_t* d_partial,
-                       uint32_t np_bucket, uint32_t* d_gthr, cudaStream_t st) {
+                       float* d_scores, uint32_t* d_keep_bits, uint64_t* d_partial, uint32_t np_bucket,
+                       uint32_t* d_gthr, cudaStream_t st) {
     const CUtensorMap& map = *static_cast<const CUtensorMap*>(cmap);
     const uint64_t ntiles = (ix.K + 127) / 128;
     uint32_t grid = uint32_t(ntiles < uint64_t(sm_count()) ? ntiles : uint64_t(sm_count()));
     if (grid == 0) grid = 1;
     switch (np_bucket) {
-        case 1: launch_tf32<1>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 2: launch_tf32<2>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 4: launch_tf32<4>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 8: launch_tf32<8>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 16: launch_tf32<16>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        default: launch_tf32<32>(map, ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 1: launch_tf32<1>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 2: launch_tf32<2>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 4: launch_tf32<4>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 8: launch_tf32<8>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        case 16: launch_tf32<16>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
+        default: launch_tf32<32>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
     }
-    return grid * 4;
+    return grid * kEpiWarps;
 }
 
 }  // namespace launch

@@ -50,18 +50,21 @@ uint32_t scores_max_warps();
 // `cmap` is a CUtensorMap (128 B) made by make_centroid_tensor_map.
 bool tensor_scores_supported(const IndexView& ix);
 void make_centroid_tensor_map(const IndexView& ix, void* out_map);
-// d_gthr: 32 u32 per-token grid-wide top-nprobe bounds, zeroed before the launch.
+// S, keep bits and per-warp top-NP lists (no row max: the pipeline only needs
+// the keep bits).  d_gthr: 32 u32 grid-wide per-token bounds, zeroed before
+// the launch.  Returns the number of partial lists written.
 uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
-                       float* d_scores, float* d_rowmax, uint32_t* d_keep_bits, uint64_t* d_partial,
-                       uint32_t np_bucket, uint32_t* d_gthr, cudaStream_t st);
+                       float* d_scores, uint32_t* d_keep_bits, uint64_t* d_partial, uint32_t np_bucket,
+                       uint32_t* d_gthr, cudaStream_t st);
 uint32_t scores_tensor_max_warps();
 [[noreturn]] void fail_cuda_driver(int code, const char* what);
 // Merge per-warp partial top-NP lists into sel[rows][nprobe] centroid ids.
 void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,
                 uint32_t nprobe, uint32_t* d_sel, cudaStream_t st);
-// Top-NP per token from a stored S (entry point); returns warps used.
+// Top-NP per token from a stored S; returns warps used (<= scores_max_warps()).
+// d_gthr (optional): 32 u32 grid-wide per-token bounds, zeroed beforehand.
 uint32_t topn_from_scores(const float* d_scores, uint64_t K, uint32_t rows, uint64_t* d_partial,
-                          uint32_t np_bucket, cudaStream_t st);
+                          uint32_t np_bucket, uint32_t* d_gthr, cudaStream_t st);
 void iota(uint32_t* d_out, uint64_t n, cudaStream_t st);
 // Keys (S[c][i], c) for one token column i -> keys[K] (generic nprobe path).
 void token_keys(const float* d_scores, uint64_t K, uint32_t i, uint64_t* d_keys, cudaStream_t st);

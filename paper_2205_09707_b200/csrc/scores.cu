@@ -177,20 +177,49 @@ __global__ void keep_bits_kernel(const float* __restrict__ rowmax, uint64_t K, f
     }
 }
 
-// Standalone top-NP over a stored S (the generate_candidates entry point):
-// same per-warp insertion lists as the fused kernel, so the merge is shared.
+// Top-NP per query token over a stored S (pipeline.cpp:65-73): warp = a
+// contiguous range of centroids, lane = query token, one coalesced 128-byte S
+// row per step (8 in flight).  A float bar filters the stream: the lane's own
+// NP-th score (strict: later ids lose ties) and a grid-wide bound gthr[token]
+// (some warp already holds NP keys scoring >= it, so lower scores cannot reach
+// the global top-NP; ties are kept).  Inserts are therefore rare.  Per-warp
+// lists go to `partial` for topn_merge.
 template <int NP>
-__global__ void topn_from_scores_kernel(const float* __restrict__ S, uint64_t K, uint32_t rows,
-                                        uint64_t* __restrict__ partial) {
+__global__ void __launch_bounds__(256)
+topn_from_scores_kernel(const float* __restrict__ S, uint64_t K, uint32_t rows, uint64_t* __restrict__ partial,
+                        uint32_t* __restrict__ gthr) {
     const uint32_t lane = dev::lane_id();
     const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t per = (K + nwarps - 1) / nwarps;
+    const uint64_t b = gwarp * per, e = b + per < K ? b + per : K;
     uint64_t top[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) top[j] = 0;
-    if (lane < rows)
-        for (uint64_t c = gwarp; c < K; c += nwarps)
-            dev::topn_insert<NP>(top, dev::make_key(S[c * kScoresPitch + lane], uint32_t(c)));
+    float thr = -INFINITY, gb = -INFINITY;
+    if (lane < rows) {
+        for (uint64_t c0 = b; c0 < e; c0 += 8) {
+            if (gthr && ((c0 - b) & 63) == 0) {
+                const uint32_t go = __ldcg(gthr + lane);
+                if (go) gb = dev::unord_f32(go);
+            }
+            float s[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[u] = c0 + u < e ? __ldcg(S + (c0 + u) * kScoresPitch + lane) : -INFINITY;
+            const float thr0 = thr;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (s[u] > thr && s[u] >= gb) {
+                    dev::topn_insert<NP>(top, dev::make_key(s[u], uint32_t(c0 + u)));
+                    if (top[NP - 1]) thr = dev::key_score(top[NP - 1]);
+                }
+            }
+            if (gthr && thr > thr0 && thr > gb) {
+                atomicMax(gthr + lane, dev::ord_f32(thr));
+                gb = thr;
+            }
+        }
+    }
     uint64_t* out = partial + (gwarp * 32 + lane) * NP;
 #pragma unroll
     for (int j = 0; j < NP; ++j) out[j] = top[j];
@@ -305,16 +334,16 @@ void keep_bits_from_rowmax(const float* d_rowmax, uint64_t K, float t_cs, uint32
 }
 
 uint32_t topn_from_scores(const float* d_scores, uint64_t K, uint32_t rows, uint64_t* d_partial,
-                          uint32_t np_bucket, cudaStream_t st) {
+                          uint32_t np_bucket, uint32_t* d_gthr, cudaStream_t st) {
     const uint32_t blocks = uint32_t(sm_count()) * kBlocksPerSm;
     const uint32_t threads = kWarpsPerBlock * 32;
     switch (np_bucket) {
-        case 1: topn_from_scores_kernel<1><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
-        case 2: topn_from_scores_kernel<2><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
-        case 4: topn_from_scores_kernel<4><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
-        case 8: topn_from_scores_kernel<8><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
-        case 16: topn_from_scores_kernel<16><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
-        default: topn_from_scores_kernel<32><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial); break;
+        case 1: topn_from_scores_kernel<1><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
+        case 2: topn_from_scores_kernel<2><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
+        case 4: topn_from_scores_kernel<4><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
+        case 8: topn_from_scores_kernel<8><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
+        case 16: topn_from_scores_kernel<16><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
+        default: topn_from_scores_kernel<32><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
     }
     count_launch();
     return blocks * kWarpsPerBlock;
