@@ -157,3 +157,17 @@ def test_merge_topk(port):
     a = s.merge_topk(pids, sc, counts, k)
     b = port.select_top(np.concatenate(allp), np.concatenate(alls), k)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_golden_gpu(golden):
+    """CUDA path (EXACT mode, through the C ABI) against the reference's own
+    golden outputs (tests/golden/make_golden.py)."""
+    idx = P.DeviceIndex.from_host(golden.index, validate=True)
+    s = P.Searcher(idx)
+    for qi, q in enumerate(golden.queries):
+        for pi, p in enumerate(golden.params):
+            r = s.search(q, p)
+            e_ids, e_bits, e_tr = golden.expected(qi, pi)
+            assert np.array_equal(r.topk.passage_ids, e_ids), (golden.name, qi, pi)
+            assert np.array_equal(bits(r.topk.scores), e_bits), (golden.name, qi, pi)
+            assert r.trace.counters() == e_tr, (golden.name, qi, pi)
