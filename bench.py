@@ -243,24 +243,19 @@ def run_plaid(args, cfg):
     d_scores = torch.zeros(k, dtype=torch.float32, device="cuda")
     d_n = torch.zeros(1, dtype=torch.int64, device="cuda")
     if world > 1:
-        g_pids = torch.zeros(world, k, dtype=torch.int32, device="cuda")
-        g_scores = torch.zeros(world, k, dtype=torch.float32, device="cuda")
-        g_n = torch.zeros(world, dtype=torch.int64, device="cuda")
-        m_pids = torch.zeros(k, dtype=torch.int32, device="cuda")
-        m_scores = torch.zeros(k, dtype=torch.float32, device="cuda")
-        m_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+        from paper_2205_09707_b200.sharded import ShardedSearcher
+
+        ss = ShardedSearcher(s, k, device=torch.device("cuda", local))
+        m_pids, m_scores = ss.out_pids, ss.out_scores
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step(i):
         q = dq[i % nq]
-        s.search_device(q.data_ptr(), 1, QLEN, DIM, params, d_pids.data_ptr(), d_scores.data_ptr(),
-                        d_n.data_ptr(), stream=sh)
         if world > 1:
-            dist.all_gather_into_tensor(g_pids.view(-1), d_pids)
-            dist.all_gather_into_tensor(g_scores.view(-1), d_scores)
-            dist.all_gather_into_tensor(g_n, d_n)
-            s.merge_topk_device(g_pids.data_ptr(), g_scores.data_ptr(), g_n.data_ptr(), world, k, k,
-                                m_pids.data_ptr(), m_scores.data_ptr(), m_n.data_ptr(), stream=sh)
+            ss.search(q, params, stream=sh)  # local search, all-gather of k (pid, score), merge
+        else:
+            s.search_device(q.data_ptr(), 1, QLEN, DIM, params, d_pids.data_ptr(), d_scores.data_ptr(),
+                            d_n.data_ptr(), stream=sh)
 
     for i in range(args.warmup):
         flush.zero_()

@@ -238,6 +238,7 @@ DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_bas
         max_doclen_ = std::max(max_doclen_, d.doclens[p]);
     }
     if (offsets.back() != d.num_embeddings) fail(PLAID_LENGTH_MISMATCH, "doclens total does not match codes length");
+    view_.max_doclen = max_doclen_;
     const uint64_t nb = uint64_t(1) << d.nbits;
     for (uint64_t i = 0; i < nb; ++i) view_.weights[i] = d.bucket_weights[i];
     for (uint64_t i = 0; i + 1 < nb; ++i) cutoffs_[i] = d.bucket_cutoffs[i];
@@ -366,6 +367,18 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
     sel2_.ensure(nd);
     keys3_.ensure(nd);
     sel3_.ensure(n3);
+    if (ix.dim == 128 && n3 <= launch::kStreamMaxPassages) {
+        const uint64_t toks = n3 * ix.max_doclen;
+        vhat_.ensure(toks * 128);
+        tok_pass_.ensure(toks);
+        pref_.ensure(n3 + 1);
+        if (run_.n < n3 * 32) {
+            run_.ensure(n3 * 32);
+            PLAID_CUDA(cudaMemset(run_.p, 0, run_.n * sizeof(uint32_t)));
+        }
+        rank_scratch_ = {vhat_.p, tok_pass_.p, pref_.p, run_.p, std::min<uint64_t>(vhat_.n / 128, tok_pass_.n),
+                         std::min<uint64_t>({pref_.n - 1, run_.n / 32, launch::kStreamMaxPassages})};
+    }
     tmp_keys_.ensure(std::max<uint64_t>(std::min<uint64_t>(p.k, N), std::min<uint64_t>(p.nprobe, K)));
     out_pids_.ensure(p.k);
     out_scores_.ensure(p.k);
@@ -461,7 +474,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         fin_max = n3;
     }
     // Stage 4: decompress + exact MaxSim, top-k.
-    launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, st);
+    launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, &rank_scratch_, st);
     record(6, st, times);
     const uint32_t base = uint32_t(index_->pid_base());
     if (fin_max <= launch::kSmallSortMax) {
@@ -765,7 +778,7 @@ void Searcher::rank_final(const float* q, uint64_t rows, const uint32_t* cand, u
     PLAID_CUDA(cudaMemcpyAsync(c + kEntryN, &n, sizeof n, cudaMemcpyHostToDevice, stream_));
     DevBuf<uint64_t> keys;
     keys.ensure(n);
-    launch::rank_exact(ix, q_.p, uint32_t(rows), ids_tmp_.p, nullptr, c + kEntryN, n, keys.p, stream_);
+    launch::rank_exact(ix, q_.p, uint32_t(rows), ids_tmp_.p, nullptr, c + kEntryN, n, keys.p, nullptr, stream_);
     std::vector<uint64_t> hk(n);
     d2h(hk.data(), keys.p, n, stream_);
     PLAID_CUDA(cudaStreamSynchronize(stream_));

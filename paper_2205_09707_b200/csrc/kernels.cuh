@@ -15,6 +15,7 @@ struct IndexView {
     uint32_t dim = 0;
     uint32_t nbits = 0;
     uint64_t K = 0, N = 0, T = 0, P = 0;
+    uint32_t max_doclen = 0;
     const float* centroids = nullptr;   // K x dim
     const uint32_t* codes = nullptr;    // T
     const uint8_t* residuals = nullptr; // T x nbits*dim/8
@@ -114,9 +115,22 @@ uint64_t sort_tmp_capacity(uint64_t nmax);
 
 // ---- stage 4 ----------------------------------------------------------------------
 // Decompress + exact MaxSim per candidate (ids from keys or ids); writes keys.
+// With d = 128 and a finalist list that fits `scratch` (rank128.cu: the
+// packed token-stream path), otherwise one fused kernel per finalist.
+struct RankScratch {
+    float* vhat = nullptr;        // tok_cap x 128 decompressed rows
+    uint32_t* tok_pass = nullptr; // tok_cap: finalist of each stream token
+    uint32_t* pref = nullptr;     // pass_cap + 1: stream offset of each finalist
+    uint32_t* run = nullptr;      // pass_cap x 32 running maxima; all zero between searches
+    uint64_t tok_cap = 0, pass_cap = 0;
+};
+constexpr uint64_t kStreamMaxPassages = 16384;
 void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
                 const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
-                cudaStream_t st);
+                const RankScratch* scratch, cudaStream_t st);
+bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
+                    const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
+                    const RankScratch& s, cudaStream_t st);
 
 // ---- misc ---------------------------------------------------------------------------
 // Device-side query validation (types.cpp:61-72): status 0 or NotNormalized+1.

@@ -147,6 +147,140 @@ rank_exact_kernel(const float* __restrict__ C, const uint32_t* __restrict__ code
     }
 }
 
+// ---- d = 128 fast path ---------------------------------------------------------
+// One warp per finalist passage, lane = QUERY token: each lane keeps its
+// query row q_i (128 fp32) in registers for the whole kernel, so the
+// per-passage max over tokens is thread-local and no lane idles on short
+// passages.  Per chunk of <= 32 passage tokens:
+//   1. decompress (lane = 4 dims, coalesced 512-byte centroid rows, the
+//      lane's 4 bucket indices from one residual byte at b=2) into the warp's
+//      shared-memory tile v[t][d] (pitch 132: conflict-free for both the
+//      row-per-lane and the broadcast access below);
+//   2. lane = token: in-order fp64 norm of its row and in-place scaling
+//      (residual_codec.cpp:124-129);
+//   3. lane = query: for each token, the in-order fp32 dot q_i . v_t with v_t
+//      broadcast from shared memory (LDS.128), two tokens interleaved so two
+//      dependent add chains are in flight; run_i = max(run_i, dot).
+// Then score = in-order fp32 sum of run_i over i (maxsim.cpp:89-99).
+constexpr uint32_t kR128Warps = 4;
+constexpr uint32_t kR128Pitch = 132;
+constexpr uint32_t kR128Chunk = 32;
+
+template <int NB>
+__global__ void __launch_bounds__(kR128Warps * 32, 3)
+rank128_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
+               const uint8_t* __restrict__ residuals, const uint32_t* __restrict__ doclens,
+               const uint64_t* __restrict__ offsets, Weights W, const float* __restrict__ Q, uint32_t rows,
+               const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
+               const uint64_t* __restrict__ d_n, uint64_t* __restrict__ out_keys) {
+    extern __shared__ __align__(16) float sm[];
+    __shared__ float w_s[16];
+    constexpr uint32_t kBpt = NB * 128 / 8;  // residual bytes per token
+    const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5;
+    float* v_s = sm + warp * kR128Chunk * kR128Pitch;
+    if (threadIdx.x < 16) w_s[threadIdx.x] = W.w[threadIdx.x];
+    __syncthreads();
+
+    float q[128];
+    {
+        const float4* qr = reinterpret_cast<const float4*>(Q + uint64_t(lane < rows ? lane : 0) * 128);
+#pragma unroll
+        for (int d4 = 0; d4 < 32; ++d4) {
+            const float4 x = lane < rows ? __ldg(qr + d4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            q[4 * d4] = x.x, q[4 * d4 + 1] = x.y, q[4 * d4 + 2] = x.z, q[4 * d4 + 3] = x.w;
+        }
+    }
+    const uint64_t n = *d_n;
+    const uint64_t nwarps = uint64_t(gridDim.x) * kR128Warps;
+    // passage p -> CTA p % grid: consecutive finalists land on different SMs
+    for (uint64_t p = uint64_t(warp) * gridDim.x + blockIdx.x; p < n; p += nwarps) {
+        const uint32_t pid = ids ? ids[p] : dev::key_id(keys[p]);
+        const uint64_t off = offsets[pid];
+        const uint32_t len = doclens[pid];
+        float run = -INFINITY;
+        for (uint32_t t0 = 0; t0 < len; t0 += kR128Chunk) {
+            const uint32_t nt = len - t0 < kR128Chunk ? len - t0 : kR128Chunk;
+            const uint32_t code_l = lane < nt ? __ldg(codes + off + t0 + lane) : 0u;
+            // 1. decompress: v = C[code] + w[idx], lane = dims 4*lane .. 4*lane+3
+#pragma unroll 8
+            for (uint32_t tt = 0; tt < nt; ++tt) {
+                const uint32_t code = __shfl_sync(0xffffffffu, code_l, tt);
+                const float4 c = __ldg(reinterpret_cast<const float4*>(C + uint64_t(code) * 128) + lane);
+                const uint8_t* rb = residuals + (off + t0 + tt) * kBpt;
+                uint32_t bits, sh;
+                if (NB == 1) {
+                    bits = __ldg(rb + (lane >> 1));
+                    sh = (lane & 1) * 4;
+                } else if (NB == 2) {
+                    bits = __ldg(rb + lane);
+                    sh = 0;
+                } else {
+                    bits = __ldg(reinterpret_cast<const uint16_t*>(rb) + lane);
+                    sh = 0;
+                }
+                constexpr uint32_t mask = (1u << NB) - 1;
+                float4 v;
+                v.x = __fadd_rn(c.x, w_s[(bits >> (sh + 0 * NB)) & mask]);
+                v.y = __fadd_rn(c.y, w_s[(bits >> (sh + 1 * NB)) & mask]);
+                v.z = __fadd_rn(c.z, w_s[(bits >> (sh + 2 * NB)) & mask]);
+                v.w = __fadd_rn(c.w, w_s[(bits >> (sh + 3 * NB)) & mask]);
+                reinterpret_cast<float4*>(v_s + tt * kR128Pitch)[lane] = v;
+            }
+            __syncwarp();
+            // 2. lane = token: in-order fp64 norm, then v *= inv
+            if (lane < nt) {
+                float4* row = reinterpret_cast<float4*>(v_s + lane * kR128Pitch);
+                double acc = 0.0;
+#pragma unroll 8
+                for (int d4 = 0; d4 < 32; ++d4) {
+                    const float4 x = row[d4];
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.x), double(x.x)));
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.y), double(x.y)));
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.z), double(x.z)));
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.w), double(x.w)));
+                }
+                if (acc > 0.0) {
+                    const float inv = float(1.0 / sqrt(acc));
+#pragma unroll 8
+                    for (int d4 = 0; d4 < 32; ++d4) {
+                        float4 x = row[d4];
+                        x.x = __fmul_rn(x.x, inv), x.y = __fmul_rn(x.y, inv);
+                        x.z = __fmul_rn(x.z, inv), x.w = __fmul_rn(x.w, inv);
+                        row[d4] = x;
+                    }
+                }
+            }
+            __syncwarp();
+            // 3. lane = query: in-order dots against broadcast token rows
+            for (uint32_t tt = 0; tt < nt; tt += 2) {
+                const uint32_t t1 = tt + 1 < nt ? tt + 1 : tt;
+                const float4* r0 = reinterpret_cast<const float4*>(v_s + tt * kR128Pitch);
+                const float4* r1 = reinterpret_cast<const float4*>(v_s + t1 * kR128Pitch);
+                float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll
+                for (int d4 = 0; d4 < 32; ++d4) {
+                    const float4 a = r0[d4], b = r1[d4];
+                    s0 = dev::madd_rn(s0, q[4 * d4 + 0], a.x);
+                    s1 = dev::madd_rn(s1, q[4 * d4 + 0], b.x);
+                    s0 = dev::madd_rn(s0, q[4 * d4 + 1], a.y);
+                    s1 = dev::madd_rn(s1, q[4 * d4 + 1], b.y);
+                    s0 = dev::madd_rn(s0, q[4 * d4 + 2], a.z);
+                    s1 = dev::madd_rn(s1, q[4 * d4 + 2], b.z);
+                    s0 = dev::madd_rn(s0, q[4 * d4 + 3], a.w);
+                    s1 = dev::madd_rn(s1, q[4 * d4 + 3], b.w);
+                }
+                run = dev::max_gt(run, s0);
+                run = dev::max_gt(run, s1);  // t1 == tt on an odd tail: same value
+            }
+            __syncwarp();
+        }
+        // in-order sum over query tokens
+        float total = 0.0f;
+        for (uint32_t i = 0; i < rows; ++i) total = __fadd_rn(total, __shfl_sync(0xffffffffu, run, i));
+        if (lane == 0) out_keys[p] = dev::make_key(total, pid);
+    }
+}
+
 // ---- per-stage entry points -------------------------------------------------
 
 __global__ void unpack_kernel(const uint8_t* __restrict__ packed, uint64_t n, uint32_t nbits,
@@ -231,10 +365,31 @@ namespace launch {
 
 void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
                 const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
-                cudaStream_t st) {
+                const RankScratch* scratch, cudaStream_t st) {
     if (nmax == 0) return;
     Weights W;
     for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
+    if (ix.dim == 128 && rows <= 32 && scratch && rank_stream128(ix, d_q, rows, d_ids, d_keys, d_n, nmax, d_out_keys, *scratch, st))
+        return;
+    if (ix.dim == 128 && rows <= 32) {
+        const size_t smem = size_t(kR128Warps) * kR128Chunk * kR128Pitch * sizeof(float);
+        static bool cfg128 = false;
+        if (!cfg128) {
+            cudaFuncSetAttribute(rank128_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            cudaFuncSetAttribute(rank128_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            cudaFuncSetAttribute(rank128_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            cfg128 = true;
+        }
+        // 3 CTAs (12 warps) per SM, one warp per finalist
+        uint64_t blocks = uint64_t(sm_count()) * 3;
+        if (blocks > nmax) blocks = nmax;
+        auto k = ix.nbits == 1 ? rank128_kernel<1> : ix.nbits == 2 ? rank128_kernel<2> : rank128_kernel<4>;
+        k<<<uint32_t(blocks), kR128Warps * 32, smem, st>>>(ix.centroids, ix.codes, ix.residuals, ix.doclens,
+                                                           ix.offsets, W, d_q, rows, d_ids, d_keys, d_n,
+                                                           d_out_keys);
+        count_launch();
+        return;
+    }
     const size_t smem = size_t(32 + kTile) * (ix.dim + 4) * sizeof(float);
     static bool configured = false;
     if (!configured) {

@@ -1,0 +1,357 @@
+// rank128.cu — stage 4 for d = 128 (pipeline.cpp:165-225): residual
+// decompression (residual_codec.cpp:97-132) and exact MaxSim
+// (maxsim.cpp:66-104) over the finalists' tokens as ONE packed stream.
+//
+// The finalists' tokens are laid end to end (passage p's tokens start at
+// pref[p], an exclusive scan of their doclens), and every kernel works on
+// full 32-token tiles of that stream, so no lane idles on a passage tail and
+// the grid is sized by tokens, not passages:
+//   K1 finalist_scan   one CTA: pref[] over the (<= 16384) finalists;
+//   K2 decompress      warp per tile: centroid rows fetched with cp.async
+//                      (lane = 16 bytes of every row), the token's packed
+//                      residual row in registers, then lane = token: v =
+//                      C + w[idx], the in-order fp64 norm and v *= inv —
+//                      bit-for-bit the reference arithmetic; rows written
+//                      to vhat[stream position] (coalesced 512-byte rows) and
+//                      tok_pass[g] = finalist of stream token g;
+//   K3 maxsim          CTA per tile (persistent, double-buffered cp.async
+//                      tile loads): lane = token, warp w = query tokens
+//                      8w..8w+7, eight independent in-order fp32 dot chains
+//                      per lane (q broadcast from shared memory); then a
+//                      segmented max across the lanes of each passage and one
+//                      atomicMax per (passage, query) segment into run[p][i]
+//                      (order-preserving uint image of the float);
+//   K4 finalize        thread per finalist: score = in-order fp32 sum of
+//                      run[p][i] over i, the 64-bit (score, pid) key, and
+//                      run[p][*] reset to 0 for the next search.
+// HBM/L2 traffic per finalist token: 4 B code + 16*b B residuals + 512 B
+// centroid row (shared rows hit L2) + a 512-byte vhat row written and read
+// back (L2-resident at these sizes).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace plaid {
+namespace {
+
+constexpr uint32_t kPitch = 132;  // floats per shared-memory row (conflict-free LDS.128 both ways)
+constexpr uint32_t kDecWarps = 4;
+constexpr uint32_t kMsWarps = 4;  // x 8 query tokens = 32
+constexpr uint32_t kMsTile = 64;  // stream tokens per maxsim tile (two per lane)
+
+struct Weights16 {
+    float w[16];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ uint32_t finalist_pid(const uint32_t* ids, const uint64_t* keys, uint64_t p) {
+    return ids ? ids[p] : dev::key_id(keys[p]);
+}
+
+// ---- K1: exclusive scan of finalist lengths -----------------------------------------
+__global__ void __launch_bounds__(1024)
+finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
+                     const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ doclens,
+                     uint32_t* __restrict__ pref) {
+    __shared__ uint32_t warp_sums[32];
+    const uint32_t n = uint32_t(*d_n);
+    const uint32_t per = (n + 1023) / 1024;
+    const uint32_t b = threadIdx.x * per, e = b + per < n ? b + per : n;
+    uint32_t local = 0;
+    for (uint32_t p = b; p < e; ++p) local += doclens[finalist_pid(ids, keys, p)];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += y;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = warp_sums[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= uint32_t(o)) wi += y;
+        }
+        warp_sums[lane] = wi - w;  // exclusive
+    }
+    __syncthreads();
+    uint32_t run = warp_sums[warp] + incl - local;
+    for (uint32_t p = b; p < e; ++p) {
+        pref[p] = run;
+        run += doclens[finalist_pid(ids, keys, p)];
+    }
+    if (threadIdx.x == 1023) pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)
+}
+
+// finalist p with pref[p] <= g < pref[p + 1]
+__device__ __forceinline__ uint32_t find_finalist(const uint32_t* __restrict__ pref, uint32_t n, uint32_t g) {
+    uint32_t lo = 0, hi = n;  // invariant: pref[lo] <= g < pref[hi]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(pref + mid) <= g) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ---- K2: decompress + normalise the token stream ------------------------------------
+template <int NB>
+__global__ void __launch_bounds__(kDecWarps * 32)
+stream_decompress_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
+                         const uint8_t* __restrict__ residuals, const uint64_t* __restrict__ offsets, Weights16 W,
+                         const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
+                         const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ pref,
+                         float* __restrict__ vhat, uint32_t* __restrict__ tok_pass) {
+    extern __shared__ __align__(16) float sm[];
+    __shared__ float w_s[16];
+    constexpr uint32_t kBpt = NB * 128 / 8;
+    const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5;
+    float* tile = sm + warp * 32 * kPitch;
+    if (threadIdx.x < 16) w_s[threadIdx.x] = W.w[threadIdx.x];
+    __syncthreads();
+    const uint32_t n = uint32_t(*d_n);
+    const uint32_t T = pref[n];
+    const uint32_t ntiles = (T + 31) / 32;
+    for (uint32_t tl = blockIdx.x * kDecWarps + warp; tl < ntiles; tl += gridDim.x * kDecWarps) {
+        const uint32_t g = tl * 32 + lane;
+        const bool valid = g < T;
+        uint64_t tok = 0;
+        uint32_t code = 0;
+        if (valid) {
+            const uint32_t p = find_finalist(pref, n, g);
+            tok_pass[g] = p;
+            tok = offsets[finalist_pid(ids, keys, p)] + (g - pref[p]);
+            code = __ldg(codes + tok);
+        }
+        const uint32_t nv = T - tl * 32 < 32 ? T - tl * 32 : 32;
+        for (uint32_t t = 0; t < nv; ++t) {
+            const uint32_t ct = __shfl_sync(0xffffffffu, code, t);
+            cp_async16(tile + t * kPitch + 4 * lane, C + uint64_t(ct) * 128 + 4 * lane);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        uint32_t rb[kBpt / 4];
+        if (valid) {
+            const uint4* src = reinterpret_cast<const uint4*>(residuals + tok * kBpt);
+#pragma unroll
+            for (uint32_t i = 0; i < kBpt / 16; ++i) {
+                const uint4 x = __ldg(src + i);
+                rb[4 * i] = x.x, rb[4 * i + 1] = x.y, rb[4 * i + 2] = x.z, rb[4 * i + 3] = x.w;
+            }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        if (valid) {
+            float4* row = reinterpret_cast<float4*>(tile + lane * kPitch);
+            constexpr uint32_t mask = (1u << NB) - 1;
+            double acc = 0.0;
+#pragma unroll
+            for (int d4 = 0; d4 < 32; ++d4) {
+                // dims 4*d4 .. 4*d4+3 <- 4*NB bits from bit 4*d4*NB (LSB-first packing)
+                const uint32_t word = rb[(4 * d4 * NB) / 32] >> ((4 * d4 * NB) % 32);
+                float4 x = row[d4];
+                x.x = __fadd_rn(x.x, w_s[(word >> (0 * NB)) & mask]);
+                x.y = __fadd_rn(x.y, w_s[(word >> (1 * NB)) & mask]);
+                x.z = __fadd_rn(x.z, w_s[(word >> (2 * NB)) & mask]);
+                x.w = __fadd_rn(x.w, w_s[(word >> (3 * NB)) & mask]);
+                row[d4] = x;
+                acc = __dadd_rn(acc, __dmul_rn(double(x.x), double(x.x)));
+                acc = __dadd_rn(acc, __dmul_rn(double(x.y), double(x.y)));
+                acc = __dadd_rn(acc, __dmul_rn(double(x.z), double(x.z)));
+                acc = __dadd_rn(acc, __dmul_rn(double(x.w), double(x.w)));
+            }
+            if (acc > 0.0) {
+                const float inv = float(1.0 / sqrt(acc));
+#pragma unroll
+                for (int d4 = 0; d4 < 32; ++d4) {
+                    float4 x = row[d4];
+                    x.x = __fmul_rn(x.x, inv), x.y = __fmul_rn(x.y, inv);
+                    x.z = __fmul_rn(x.z, inv), x.w = __fmul_rn(x.w, inv);
+                    row[d4] = x;
+                }
+            }
+        }
+        __syncwarp();
+        float4* dst = reinterpret_cast<float4*>(vhat + uint64_t(tl) * 32 * 128);
+        for (uint32_t t = 0; t < nv; ++t) dst[t * 32 + lane] = reinterpret_cast<const float4*>(tile + t * kPitch)[lane];
+        __syncwarp();
+    }
+}
+
+// ---- K3: exact MaxSim over stream tiles ----------------------------------------------
+__global__ void __launch_bounds__(kMsWarps * 32)
+stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict__ tok_pass,
+                     const uint32_t* __restrict__ pref, const uint64_t* __restrict__ d_n,
+                     const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
+    extern __shared__ __align__(16) float sm[];
+    float* q_s = sm;                      // 32 x kPitch
+    float* tile = sm + 32 * kPitch;       // kMsTile x kPitch
+    const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5;
+    const uint32_t n = uint32_t(*d_n);
+    const uint32_t T = pref[n];
+    const uint32_t ntiles = (T + kMsTile - 1) / kMsTile;
+    if (blockIdx.x >= ntiles) return;
+    for (uint32_t i = threadIdx.x; i < 32 * 32; i += kMsWarps * 32) {
+        const uint32_t r = i >> 5, c = i & 31;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < rows) v = __ldg(reinterpret_cast<const float4*>(Q + r * 128) + c);
+        reinterpret_cast<float4*>(q_s + r * kPitch)[c] = v;
+    }
+    const uint32_t i0 = warp * 8;
+    for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        const uint32_t g0 = tl * kMsTile;
+        const uint32_t nv = T - g0 < kMsTile ? T - g0 : kMsTile;
+        {
+            const float* src = vhat + uint64_t(g0) * 128;
+            for (uint32_t i = threadIdx.x; i < nv * 32; i += kMsWarps * 32) {
+                const uint32_t r = i >> 5, c = i & 31;
+                cp_async16(tile + r * kPitch + 4 * c, src + r * 128 + 4 * c);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        // lane scores tokens g0 + lane and g0 + 32 + lane
+        const bool valid0 = lane < nv, valid1 = 32 + lane < nv;
+        const uint32_t p0 = valid0 ? tok_pass[g0 + lane] : 0xFFFFFFFFu;
+        const uint32_t p1 = valid1 ? tok_pass[g0 + 32 + lane] : 0xFFFFFFFEu;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (i0 < rows) {
+            float a[8], c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = 0.0f, c[u] = 0.0f;
+            const float4* vr0 = reinterpret_cast<const float4*>(tile + lane * kPitch);
+            const float4* vr1 = reinterpret_cast<const float4*>(tile + (32 + lane) * kPitch);
+#pragma unroll 2
+            for (uint32_t d4 = 0; d4 < 32; ++d4) {
+                const float4 v = vr0[d4], w = vr1[d4];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const float4 q = reinterpret_cast<const float4*>(q_s + (i0 + u) * kPitch)[d4];
+                    float x = a[u], y = c[u];
+                    x = dev::madd_rn(x, q.x, v.x);
+                    y = dev::madd_rn(y, q.x, w.x);
+                    x = dev::madd_rn(x, q.y, v.y);
+                    y = dev::madd_rn(y, q.y, w.y);
+                    x = dev::madd_rn(x, q.z, v.z);
+                    y = dev::madd_rn(y, q.z, w.z);
+                    x = dev::madd_rn(x, q.w, v.w);
+                    y = dev::madd_rn(y, q.w, w.w);
+                    a[u] = x, c[u] = y;
+                }
+            }
+            // segmented max over the lanes of each finalist (its lanes are
+            // contiguous); the segment's last lane publishes
+            const uint32_t pn0 = __shfl_down_sync(0xffffffffu, p0, 1);
+            const uint32_t pn1 = __shfl_down_sync(0xffffffffu, p1, 1);
+            const bool tail0 = valid0 && (lane == 31 || pn0 != p0);
+            const bool tail1 = valid1 && (lane == 31 || pn1 != p1);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                float m0 = a[u], m1 = c[u];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float y0 = __shfl_up_sync(0xffffffffu, m0, o);
+                    const float y1 = __shfl_up_sync(0xffffffffu, m1, o);
+                    const uint32_t q0 = __shfl_up_sync(0xffffffffu, p0, o);
+                    const uint32_t q1 = __shfl_up_sync(0xffffffffu, p1, o);
+                    if (lane >= uint32_t(o) && q0 == p0) m0 = dev::max_gt(m0, y0);
+                    if (lane >= uint32_t(o) && q1 == p1) m1 = dev::max_gt(m1, y1);
+                }
+                if (i0 + u < rows) {
+                    if (tail0) atomicMax(run + uint64_t(p0) * 32 + i0 + u, dev::ord_f32(m0));
+                    if (tail1) atomicMax(run + uint64_t(p1) * 32 + i0 + u, dev::ord_f32(m1));
+                }
+            }
+        }
+        __syncthreads();  // tile fully read before it is refilled
+    }
+}
+
+// ---- K4: per-finalist score ---------------------------------------------------------
+__global__ void finalize_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
+                                const uint64_t* __restrict__ d_n, uint32_t rows, uint32_t* __restrict__ run,
+                                uint64_t* __restrict__ out_keys) {
+    const uint64_t n = *d_n;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x) {
+        uint4* r4 = reinterpret_cast<uint4*>(run + p * 32);
+        uint32_t v[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint4 x = r4[j];
+            v[4 * j] = x.x, v[4 * j + 1] = x.y, v[4 * j + 2] = x.z, v[4 * j + 3] = x.w;
+            r4[j] = make_uint4(0, 0, 0, 0);
+        }
+        float total = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (uint32_t(i) < rows) total = __fadd_rn(total, dev::unord_f32(v[i]));
+        out_keys[p] = dev::make_key(total, finalist_pid(ids, keys, p));
+    }
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+}  // namespace
+
+namespace launch {
+
+bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
+                    const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
+                    const RankScratch& s, cudaStream_t st) {
+    if (ix.dim != 128 || rows > 32 || nmax > s.pass_cap || nmax * ix.max_doclen > s.tok_cap ||
+        nmax * ix.max_doclen >= (1ull << 32))
+        return false;
+    Weights16 W;
+    for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
+    static bool cfg = false;
+    const size_t dsm = size_t(kDecWarps) * 32 * kPitch * sizeof(float);
+    const size_t msm = size_t(32 + kMsTile) * kPitch * sizeof(float);
+    if (!cfg) {
+        cudaFuncSetAttribute(stream_decompress_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
+        cudaFuncSetAttribute(stream_decompress_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
+        cudaFuncSetAttribute(stream_decompress_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
+        cudaFuncSetAttribute(stream_maxsim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(msm));
+        cfg = true;
+    }
+    finalist_scan_kernel<<<1, 1024, 0, st>>>(d_ids, d_keys, d_n, ix.doclens, s.pref);
+    count_launch();
+    const uint64_t max_tiles = (nmax * ix.max_doclen + 31) / 32;
+    uint64_t db = (max_tiles + kDecWarps - 1) / kDecWarps;
+    if (db > uint64_t(sm_count()) * 3) db = uint64_t(sm_count()) * 3;
+    auto dk = ix.nbits == 1 ? stream_decompress_kernel<1>
+                            : ix.nbits == 2 ? stream_decompress_kernel<2> : stream_decompress_kernel<4>;
+    dk<<<uint32_t(db), kDecWarps * 32, dsm, st>>>(ix.centroids, ix.codes, ix.residuals, ix.offsets, W, d_ids, d_keys,
+                                                  d_n, s.pref, s.vhat, s.tok_pass);
+    count_launch();
+    uint64_t mb = (nmax * ix.max_doclen + kMsTile - 1) / kMsTile;
+    if (mb > uint64_t(sm_count()) * 4) mb = uint64_t(sm_count()) * 4;
+    stream_maxsim_kernel<<<uint32_t(mb), kMsWarps * 32, msm, st>>>(s.vhat, s.tok_pass, s.pref, d_n, d_q, rows, s.run);
+    count_launch();
+    const uint32_t fb = uint32_t((nmax + 255) / 256);
+    finalize_kernel<<<fb, 256, 0, st>>>(d_ids, d_keys, d_n, rows, s.run, d_out_keys);
+    count_launch();
+    return true;
+}
+
+}  // namespace launch
+}  // namespace plaid

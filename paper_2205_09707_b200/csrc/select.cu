@@ -175,6 +175,55 @@ sort_small_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict_
     if (threadIdx.x == 0 && out_n) *out_n = m;
 }
 
+// Sort by rank (n <= kSmallSortMax): keys are unique, so the position of key
+// x in the descending order is the number of keys greater than x.  Every CTA
+// stages all n keys in shared memory and each thread ranks one key against
+// them (broadcast reads, two keys per 128-bit load); keys with rank < want
+// are written straight to their slot.  O(n^2) compares, but spread over the
+// whole GPU it beats a single-CTA bitonic network (78 barrier-separated
+// steps at n = 4096) by an order of magnitude.
+// A CTA ranks 32 keys with 4 threads each (thread q of a key scans quarter q
+// of the array); quarters start one 16-byte pair apart in bank space, so the
+// four addresses of a warp-wide load never share a bank.
+constexpr uint32_t kRankThreads = 128;
+constexpr uint32_t kRankPerCta = kRankThreads / 4;
+
+__host__ __device__ constexpr uint32_t rank_quarter_pairs(uint32_t n) {
+    return (((n + 1) / 2 + 3) / 4 + 7) / 8 * 8;  // pairs per quarter, a multiple of 8
+}
+
+__global__ void __launch_bounds__(kRankThreads)
+sort_rank_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
+                 uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids, float* __restrict__ out_scores,
+                 uint64_t* __restrict__ out_n, uint32_t id_base) {
+    extern __shared__ __align__(16) uint64_t s[];
+    const uint32_t n = uint32_t(*d_n);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && out_n) *out_n = n < want ? n : want;
+    if (blockIdx.x * kRankPerCta >= n) return;
+    const uint32_t npq = rank_quarter_pairs(n);
+    // pair k of quarter q lives at pair slot q * (npq + 1) + k
+    for (uint32_t i = threadIdx.x; i < 4 * (npq + 1); i += kRankThreads) {
+        const uint32_t q = i / (npq + 1), k = i % (npq + 1);
+        const uint32_t e = 2 * (q * npq + k);
+        const bool real = k < npq;
+        s[2 * i] = real && e < n ? __ldcg(keys + e) : 0ull;
+        s[2 * i + 1] = real && e + 1 < n ? __ldcg(keys + e + 1) : 0ull;
+    }
+    __syncthreads();
+    const uint32_t me = blockIdx.x * kRankPerCta + (threadIdx.x >> 2), q = threadIdx.x & 3;
+    const uint64_t x = me < n ? __ldcg(keys + me) : ~0ull;
+    uint32_t rank = 0;
+    const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(s) + q * (npq + 1);
+#pragma unroll 8
+    for (uint32_t j = 0; j < npq; ++j) {
+        const ulonglong2 v = s2[j];
+        rank += (v.x > x) + (v.y > x);
+    }
+    rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+    rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+    if (q == 0 && me < n && rank < want) emit(rank, x, out_keys, out_ids, out_scores, id_base);
+}
+
 __global__ void pad_copy_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
                                 uint64_t npad, uint64_t* __restrict__ tmp) {
     const uint64_t n = *d_n;
@@ -297,6 +346,20 @@ uint64_t sort_tmp_capacity(uint64_t nmax) { return nmax <= kSmallSortMax ? 0 : n
 void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
               uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
               uint32_t id_base, uint64_t* d_tmp, cudaStream_t st) {
+    if (nmax <= kSmallSortMax && nmax >= 256) {
+        const size_t smem = size_t(4) * (rank_quarter_pairs(uint32_t(nmax)) + 1) * 16;
+        static bool rank_cfg = false;
+        if (!rank_cfg) {
+            cudaFuncSetAttribute(sort_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(4 * (rank_quarter_pairs(uint32_t(kSmallSortMax)) + 1) * 16));
+            rank_cfg = true;
+        }
+        const uint32_t grid = uint32_t((nmax + kRankPerCta - 1) / kRankPerCta);
+        sort_rank_kernel<<<grid, kRankThreads, smem, st>>>(d_keys, d_n, want, d_out_keys, d_out_ids, d_out_scores,
+                                                          d_out_n, id_base);
+        count_launch();
+        return;
+    }
     if (nmax <= kSmallSortMax) {
         const uint32_t npad = uint32_t(next_pow2(nmax < 2 ? 2 : nmax));
         const size_t smem = size_t(npad) * sizeof(uint64_t);
