@@ -50,6 +50,21 @@ __device__ __forceinline__ float madd_rn(float acc, float a, float b) {
     return __fadd_rn(acc, __fmul_rn(a, b));
 }
 
+// (a.x * s, a.y * s), each rounded to nearest: one FMUL2 on sm_100.  Only
+// the multiply is packed — ptxas contracts a packed mul.rn.f32x2 feeding a
+// packed add.rn.f32x2 into FFMA2 (checked with cuobjdump), which would break
+// the reference's separately rounded multiply-then-add, so the adds stay
+// scalar __fadd_rn.
+__device__ __forceinline__ float2 mul2_rn(float2 a, float s) {
+    unsigned long long r;
+    const float2 b = make_float2(s, s);
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
 // `if (s > acc) acc = s` (pipeline.cpp:122, maxsim.cpp:95).
 __device__ __forceinline__ float max_gt(float acc, float s) { return s > acc ? s : acc; }
 

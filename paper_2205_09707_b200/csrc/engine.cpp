@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 
 namespace plaid {
 
@@ -77,6 +78,7 @@ enum : int {
     kKConst = 7,    // K (for generic selects)
     kTmpN = 8,      // scratch count
     kEntryN = 9,    // entry-point input count
+    kKeptN = 10,    // stage 2: kept centroids, their postings, queued owners (3 slots)
     kGthr = 16,     // 32 u32 per-token top-nprobe bounds (tensor S_cq kernel)
     kNumCounters = 32
 };
@@ -216,6 +218,51 @@ T* DeviceIndex::upload(const T* src, uint64_t count) {
     return static_cast<T*>(p);
 }
 
+// mult[j] for posting j = (centroid c, passage p): how many tokens of p have
+// code c, saturated at 255 (kernels recount a saturated entry from the codes).
+// Stage 2 scores candidates from the kept centroids' posting lists and needs
+// it for the reference's gathered-row counter (pipeline.cpp:108, :133).  One
+// pass over the codes per passage range; ranges run on all host threads.
+static std::vector<uint8_t> posting_multiplicity(const plaid_index_desc& d, const std::vector<uint64_t>& offsets) {
+    const uint64_t K = d.num_centroids, N = d.num_passages;
+    const uint64_t P = d.ivf_offsets[K];
+    std::vector<uint8_t> mult(P, 0);
+    if (P == 0 || N == 0) return mult;
+    unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+    if (nt > 32) nt = 32;
+    if (uint64_t(nt) * 4096 > N) nt = unsigned(std::max<uint64_t>(1, N / 4096));
+    auto work = [&](uint64_t pb, uint64_t pe) {
+        std::vector<uint64_t> cursor(K);
+        std::vector<uint32_t> seen(K, UINT32_MAX);
+        std::vector<uint64_t> at(K, UINT64_MAX);
+        for (uint64_t c = 0; c < K; ++c) {
+            const uint32_t* b = d.ivf_postings + d.ivf_offsets[c];
+            const uint32_t* e = d.ivf_postings + d.ivf_offsets[c + 1];
+            cursor[c] = uint64_t(std::lower_bound(b, e, uint32_t(pb)) - d.ivf_postings);
+        }
+        for (uint64_t p = pb; p < pe; ++p)
+            for (uint64_t t = offsets[p]; t < offsets[p + 1]; ++t) {
+                const uint32_t c = d.codes[t];
+                if (c >= K) continue;
+                if (seen[c] != uint32_t(p)) {
+                    seen[c] = uint32_t(p);
+                    const uint64_t j = cursor[c];
+                    if (j < d.ivf_offsets[c + 1] && d.ivf_postings[j] == p) {
+                        at[c] = j;
+                        ++cursor[c];
+                    } else {
+                        at[c] = UINT64_MAX;  // inconsistent IVF (validate_index reports it)
+                    }
+                }
+                if (at[c] != UINT64_MAX && mult[at[c]] < 255) ++mult[at[c]];
+            }
+    };
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nt; ++i) th.emplace_back(work, N * i / nt, N * (i + 1) / nt);
+    for (auto& x : th) x.join();
+    return mult;
+}
+
 DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_base)
     : device_(device), pid_base_(pid_base) {
     if (!nbits_supported(d.nbits)) fail(PLAID_PACKING_UNSUPPORTED, "nbits must be one of {1,2,4}");
@@ -250,6 +297,8 @@ DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_bas
         view_.offsets = upload(offsets.data(), offsets.size());
         view_.ivf_offsets = upload(d.ivf_offsets, d.num_centroids + 1);
         view_.ivf_postings = upload(d.ivf_postings, view_.P);
+        const std::vector<uint8_t> mult = posting_multiplicity(d, offsets);
+        view_.ivf_mult = upload(mult.data(), mult.size());
     } catch (...) {
         for (void* p : allocs_) cudaFree(p);
         allocs_.clear();
@@ -320,6 +369,10 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         partial_.ensure(npartial_warps_ * 32 * 32);
         chunk_counts_.ensure(launch::bitmap_chunks(ix.N));
         c1_.ensure(ix.N);
+        slot_of_.ensure(ix.N);
+        kept_list_.ensure(ix.K);
+        acc2_.ensure(ix.N * 32);
+        PLAID_CUDA(cudaMemset(acc2_.p, 0, acc2_.n * sizeof(uint32_t)));
         keys2_.ensure(ix.N);
         keys4_.ensure(ix.N);
         const uint64_t K = ix.K;
@@ -376,8 +429,15 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
             run_.ensure(n3 * 32);
             PLAID_CUDA(cudaMemset(run_.p, 0, run_.n * sizeof(uint32_t)));
         }
-        rank_scratch_ = {vhat_.p, tok_pass_.p, pref_.p, run_.p, std::min<uint64_t>(vhat_.n / 128, tok_pass_.n),
-                         std::min<uint64_t>({pref_.n - 1, run_.n / 32, launch::kStreamMaxPassages})};
+        fin_base_.ensure(n3);
+        rank_scratch_.vhat = vhat_.p;
+        rank_scratch_.tok_pass = tok_pass_.p;
+        rank_scratch_.pref = pref_.p;
+        rank_scratch_.run = run_.p;
+        rank_scratch_.fin_base = fin_base_.p;
+        rank_scratch_.tok_cap = std::min<uint64_t>(vhat_.n / 128, tok_pass_.n);
+        rank_scratch_.pass_cap =
+            std::min<uint64_t>({pref_.n - 1, run_.n / 32, fin_base_.n, launch::kStreamMaxPassages});
     }
     tmp_keys_.ensure(std::max<uint64_t>(std::min<uint64_t>(p.k, N), std::min<uint64_t>(p.nprobe, K)));
     out_pids_.ensure(p.k);
@@ -456,9 +516,9 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         // Stage 2: pruned centroid interaction over C1, keep ndocs.  Only the
         // candidates owning a kept token are read (see kept_owners).
         const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
-        launch::kept_owners(ix, keep_.p, owners, st);
-        launch::centroid_interaction(ix, scores_.p, rows, c1_.p, nullptr, c + kN1, N, keep_.p, owners,
-                                     keys2_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows2), st);
+        launch::stage2_masked(ix, scores_.p, rows, c1_.p, c + kN1, N, keep_.p, bitmap, owners, kept_list_.p,
+                              slot_of_.p, acc2_.p, reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p,
+                              reinterpret_cast<unsigned long long*>(c + kRows2), st);
         record(3, st, times);
         launch::select_top_large(keys2_.p, c + kN1, N, p.ndocs, sel_state_.p, sel2_.p, c + kN2, st);
         record(4, st, times);

@@ -139,9 +139,10 @@ private:
 
     // scratch
     DevBuf<float> q_, scores_, rowmax_, out_scores_, vhat_;
-    DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, out_pids_, ids_tmp_, tok_pass_, pref_, run_;
+    DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, out_pids_, ids_tmp_, tok_pass_, pref_, run_, slot_of_,
+        kept_list_, acc2_;
     launch::RankScratch rank_scratch_;
-    DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_,
+    DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_,
         tmp_keys_, kconst_;
     // zero_ = [16 u64 counters | candidate bitmap (N bits) | kept-owner bitmap
     // (N bits)], cleared by a single memset per query.

@@ -27,6 +27,7 @@ namespace {
 constexpr uint32_t kCB = 256;         // candidates per block (stage 2)
 constexpr uint32_t kListCap = 1024;   // kept-token queue per block (static smem < 48 KB)
 constexpr uint32_t kAccPitch = 33;    // conflict-free column sums
+constexpr uint64_t kListsPerCandidate = 4;  // kept postings per C1 candidate above which ci_all runs
 
 __device__ __forceinline__ uint32_t cand_id(const uint32_t* ids, const uint64_t* keys, uint64_t i) {
     return ids ? ids[i] : dev::key_id(keys[i]);
@@ -270,6 +271,172 @@ __global__ void kept_owners_kernel(const uint32_t* __restrict__ keep_bits, uint6
     }
 }
 
+// ---- stage 2 from the kept centroids' posting lists ------------------------------------
+// Stage 2's score for candidate p is sum_i max over p's tokens on KEPT
+// centroids of S[code][i] (0 if there is none, pipeline.cpp:127-131).  A max
+// only needs the set of distinct kept codes of p, and p owns code c exactly
+// when p is in postings(c) (IVF content invariant, index.cpp:64-83).  So the
+// stage is driven by the kept centroids' posting lists, never reading codes:
+//   keep_list        kept centroid ids + the total length of their lists;
+//   slot_scatter     slot_of[pid] = position of pid in C1;
+//   ivf_accumulate   a block per kept centroid: S[c] in registers (lane =
+//                    query token), for each posting in C1 one warp-wide
+//                    atomicMax of the 32 order-preserving score images into
+//                    acc[slot], the slot's used bit, and the posting's token
+//                    multiplicity (index-derived ivf_mult) into the
+//                    gathered-row counter;
+//   stage2_finalize  thread per candidate: in-order fp32 sum of acc[slot]
+//                    (exactly 0 when unused), the key, acc reset to 0.
+// Work is proportional to the kept (centroid, candidate) pairs.  When the kept
+// lists are long (t_cs near -1 keeps most centroids) a warp-per-candidate
+// pass over the codes (ci_all) takes over; the choice is made on the device.
+__global__ void keep_list_kernel(const uint32_t* __restrict__ keep_bits, uint64_t K,
+                                 const uint64_t* __restrict__ ivf_offsets, uint32_t* __restrict__ list,
+                                 unsigned long long* __restrict__ counts /* [0] kept, [1] postings */) {
+    const uint32_t lane = dev::lane_id();
+    const uint64_t words = (K + 31) / 32;
+    for (uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; w0 < words;
+         w0 += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = w0 + lane;
+        uint32_t bits = w < words ? keep_bits[w] : 0u;
+        if (w == words - 1 && (K & 31)) bits &= (1u << (K & 31)) - 1;
+        const uint32_t cnt = __popc(bits);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (!tot) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(counts, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        uint32_t slot = uint32_t(base) + incl - cnt;
+        unsigned long long post = 0;
+        while (bits) {
+            const uint32_t c = uint32_t(w * 32 + (__ffs(bits) - 1));
+            bits &= bits - 1;
+            list[slot++] = c;
+            post += ivf_offsets[c + 1] - ivf_offsets[c];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) post += __shfl_xor_sync(0xffffffffu, post, o);
+        if (lane == 0) atomicAdd(counts + 1, post);
+    }
+}
+
+__device__ __forceinline__ bool use_lists(const unsigned long long* counts, uint64_t n1) {
+    return counts[1] <= kListsPerCandidate * (n1 + 1024);
+}
+
+__global__ void slot_scatter_kernel(const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
+                                    uint32_t* __restrict__ slot_of) {
+    const uint64_t n = *d_n1;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        slot_of[c1[i]] = uint32_t(i);
+}
+
+__global__ void __launch_bounds__(256)
+ivf_accumulate_kernel(const uint32_t* __restrict__ list, const unsigned long long* __restrict__ counts,
+                      const uint64_t* __restrict__ d_n1, const uint64_t* __restrict__ ivf_offsets,
+                      const uint32_t* __restrict__ postings, const uint8_t* __restrict__ mult,
+                      const uint32_t* __restrict__ cand_bits, const uint32_t* __restrict__ slot_of,
+                      const float* __restrict__ S, uint32_t rows, const uint32_t* __restrict__ codes,
+                      const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ doclens,
+                      uint32_t* __restrict__ acc, uint32_t* __restrict__ used_bits,
+                      unsigned long long* __restrict__ d_rows) {
+    if (!use_lists(counts, *d_n1)) return;
+    const uint64_t kept = counts[0];
+    const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    unsigned long long rows_local = 0;
+    // few kept centroids with long lists: every list is split over `parts` blocks
+    const uint64_t parts = kept && gridDim.x > kept ? gridDim.x / kept : 1;
+    for (uint64_t item = blockIdx.x; item < kept * parts; item += gridDim.x) {
+        const uint64_t k = item % kept, part = item / kept;
+        const uint32_t c = list[k];
+        const uint32_t ord_s = dev::ord_f32(__ldg(S + uint64_t(c) * kScoresPitch + lane));
+        const uint64_t e = ivf_offsets[c + 1];
+        for (uint64_t j0 = ivf_offsets[c] + (part * nwarp + warp) * 32; j0 < e; j0 += parts * nwarp * 32) {
+            const uint64_t j = j0 + lane;
+            uint32_t slot = 0;
+            bool in = false;
+            if (j < e) {
+                const uint32_t p = __ldg(postings + j);
+                in = (__ldg(cand_bits + (p >> 5)) >> (p & 31)) & 1u;
+                if (in) {
+                    slot = __ldg(slot_of + p);
+                    atomicOr(used_bits + (slot >> 5), 1u << (slot & 31));
+                    uint32_t m = __ldg(mult + j);
+                    if (m == 255) {  // saturated: recount from the codes
+                        m = 0;
+                        const uint64_t o = offsets[p];
+                        for (uint32_t t = 0; t < doclens[p]; ++t) m += codes[o + t] == c;
+                    }
+                    rows_local += m;
+                }
+            }
+            uint32_t b = __ballot_sync(0xffffffffu, in);
+            while (b) {
+                const int l = __ffs(b) - 1;
+                b &= b - 1;
+                const uint32_t s = __shfl_sync(0xffffffffu, slot, l);
+                if (lane < rows) atomicMax(acc + uint64_t(s) * 32 + lane, ord_s);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rows_local += __shfl_xor_sync(0xffffffffu, rows_local, o);
+    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+}
+
+__global__ void stage2_finalize_kernel(const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
+                                       const unsigned long long* __restrict__ counts, uint32_t rows,
+                                       uint32_t* __restrict__ acc, const uint32_t* __restrict__ used_bits,
+                                       uint64_t* __restrict__ keys_out) {
+    const uint64_t n = *d_n1;
+    if (!use_lists(counts, n)) return;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        float sc = 0.0f;
+        if ((used_bits[i >> 5] >> (i & 31)) & 1u) {
+            uint4* a4 = reinterpret_cast<uint4*>(acc + i * 32);
+            uint32_t v[32];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint4 x = a4[q];
+                v[4 * q] = x.x, v[4 * q + 1] = x.y, v[4 * q + 2] = x.z, v[4 * q + 3] = x.w;
+                a4[q] = make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (uint32_t(q) < rows) sc = __fadd_rn(sc, dev::unord_f32(v[q]));
+        }
+        keys_out[i] = dev::make_key(sc, c1[i]);
+    }
+}
+
+// fallback when the kept lists are long: warp per candidate over its codes
+__global__ void __launch_bounds__(256)
+ci_all_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
+              const uint32_t* __restrict__ doclens, const float* __restrict__ S, uint32_t rows,
+              const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
+              const unsigned long long* __restrict__ counts, const uint32_t* __restrict__ keep_bits,
+              uint64_t* __restrict__ keys_out, unsigned long long* __restrict__ d_rows) {
+    const uint64_t n = *d_n1;
+    if (use_lists(counts, n)) return;
+    const uint32_t lane = dev::lane_id();
+    const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    unsigned long long rows_local = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const uint32_t pid = c1[i];
+        uint32_t used;
+        const float total = score_passage_warp<true>(codes, offsets[pid], doclens[pid], S, rows, keep_bits, &used);
+        if (lane == 0) keys_out[i] = dev::make_key(total, pid);
+        rows_local += used;
+    }
+    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+}
+
 int sm_count() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -290,6 +457,33 @@ void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_o
     if (blocks == 0) blocks = 1;
     kept_owners_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_keep_bits, ix.K, ix.ivf_offsets, ix.ivf_postings,
                                                          d_owners);
+    count_launch();
+}
+
+void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, const uint32_t* d_c1,
+                   const uint64_t* d_n1, uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_cand_bits,
+                   uint32_t* d_used_bits, uint32_t* d_kept_list, uint32_t* d_slot_of, uint32_t* d_acc,
+                   unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows, cudaStream_t st) {
+    const uint32_t sms = uint32_t(sm_count());
+    const uint64_t words = (ix.K + 31) / 32;
+    uint64_t kb = (words + 255) / 256;
+    if (kb == 0) kb = 1;
+    keep_list_kernel<<<uint32_t(kb), 256, 0, st>>>(d_keep_bits, ix.K, ix.ivf_offsets, d_kept_list, d_counts2);
+    count_launch();
+    if (nmax == 0) return;
+    uint64_t sb = (nmax + 255) / 256;
+    if (sb > uint64_t(sms) * 8) sb = uint64_t(sms) * 8;
+    slot_scatter_kernel<<<uint32_t(sb), 256, 0, st>>>(d_c1, d_n1, d_slot_of);
+    count_launch();
+    ivf_accumulate_kernel<<<sms * 8, 256, 0, st>>>(d_kept_list, d_counts2, d_n1, ix.ivf_offsets, ix.ivf_postings,
+                                                   ix.ivf_mult, d_cand_bits, d_slot_of, d_scores, rows, ix.codes,
+                                                   ix.offsets, ix.doclens, d_acc, d_used_bits, d_rows);
+    count_launch();
+    stage2_finalize_kernel<<<uint32_t(sb), 256, 0, st>>>(d_c1, d_n1, d_counts2, rows, d_acc, d_used_bits,
+                                                         d_out_keys);
+    count_launch();
+    ci_all_kernel<<<sms * 8, 256, 0, st>>>(ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_c1, d_n1, d_counts2,
+                                           d_keep_bits, d_out_keys, d_rows);
     count_launch();
 }
 

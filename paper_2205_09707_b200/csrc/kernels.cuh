@@ -23,6 +23,7 @@ struct IndexView {
     const uint64_t* offsets = nullptr;  // N + 1
     const uint64_t* ivf_offsets = nullptr;
     const uint32_t* ivf_postings = nullptr;
+    const uint8_t* ivf_mult = nullptr;  // P: tokens of the passage with the posting's code (<= 255, saturating)
     float weights[16] = {};
 };
 
@@ -96,6 +97,15 @@ void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t r
                           cudaStream_t st);
 // owners |= postings(c) for every kept centroid c (owners zeroed by the caller).
 void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_owners, cudaStream_t st);
+// Stage 2 over C1 (ids d_c1 ascending, count *d_n1 <= nmax, membership
+// bitmap d_cand_bits): keys for every candidate, from the kept centroids'
+// posting lists (interaction.cu).  Scratch: d_used_bits (nmax bits, zeroed),
+// d_counts2 (2 zeroed counters), d_kept_list (K), d_slot_of (N), d_acc
+// (nmax x 32, all zero between calls).
+void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, const uint32_t* d_c1,
+                   const uint64_t* d_n1, uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_cand_bits,
+                   uint32_t* d_used_bits, uint32_t* d_kept_list, uint32_t* d_slot_of, uint32_t* d_acc,
+                   unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows, cudaStream_t st);
 
 // ---- selection -----------------------------------------------------------------------
 // Top `want` of keys[0..*d_n) (largest first).  Result: d_out_keys unsorted
@@ -122,6 +132,7 @@ struct RankScratch {
     uint32_t* tok_pass = nullptr; // tok_cap: finalist of each stream token
     uint32_t* pref = nullptr;     // pass_cap + 1: stream offset of each finalist
     uint32_t* run = nullptr;      // pass_cap x 32 running maxima; all zero between searches
+    uint64_t* fin_base = nullptr; // pass_cap: index token of stream position g is fin_base[p] + g
     uint64_t tok_cap = 0, pass_cap = 0;
 };
 constexpr uint64_t kStreamMaxPassages = 16384;

@@ -62,7 +62,8 @@ __device__ __forceinline__ uint32_t finalist_pid(const uint32_t* ids, const uint
 __global__ void __launch_bounds__(1024)
 finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
                      const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ doclens,
-                     uint32_t* __restrict__ pref) {
+                     const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pref,
+                     uint64_t* __restrict__ fin_base) {
     __shared__ uint32_t warp_sums[32];
     const uint32_t n = uint32_t(*d_n);
     const uint32_t per = (n + 1023) / 1024;
@@ -90,30 +91,44 @@ finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restric
     __syncthreads();
     uint32_t run = warp_sums[warp] + incl - local;
     for (uint32_t p = b; p < e; ++p) {
+        const uint32_t pid = finalist_pid(ids, keys, p);
         pref[p] = run;
-        run += doclens[finalist_pid(ids, keys, p)];
+        fin_base[p] = offsets[pid] - run;  // index token = fin_base[p] + stream position
+        run += doclens[pid];
     }
     if (threadIdx.x == 1023) pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)
 }
 
-// finalist p with pref[p] <= g < pref[p + 1]
-__device__ __forceinline__ uint32_t find_finalist(const uint32_t* __restrict__ pref, uint32_t n, uint32_t g) {
-    uint32_t lo = 0, hi = n;  // invariant: pref[lo] <= g < pref[hi]
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(pref + mid) <= g) lo = mid;
-        else hi = mid;
+// Warp-cooperative: the finalist of stream token g (this lane's) for a tile
+// starting at g0.  A 32-ary search finds p0 (pref[p0] <= g0 < pref[p0 + 1])
+// in ceil(log32 n) rounds of one load per lane; the tile's 32 tokens then lie
+// in finalists p0 .. p0 + 31 (each has >= 1 token), whose ends one load per
+// lane brings in.
+__device__ __forceinline__ uint32_t tile_finalists(const uint32_t* __restrict__ pref, uint32_t n, uint32_t g0,
+                                                   uint32_t g) {
+    const uint32_t lane = dev::lane_id();
+    uint32_t lo = 0, span = n;  // pref[lo] <= g0 < pref[lo + span]
+    while (span > 1) {
+        const uint32_t step = (span + 31) / 32;
+        const uint32_t probe = lo + lane * step;
+        const bool le = probe < lo + span && __ldg(pref + probe) <= g0;
+        const uint32_t last = 31 - __clz(__ballot_sync(0xffffffffu, le));  // lane 0 always qualifies
+        lo += last * step;
+        span = (last + 1) * step <= span ? step : span - last * step;
     }
-    return lo;
+    const uint32_t e = lo + 1 + lane <= n ? __ldg(pref + lo + 1 + lane) : 0xFFFFFFFFu;  // end of finalist lo + lane
+    uint32_t p = lo;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) p += __shfl_sync(0xffffffffu, e, j) <= g;
+    return p;
 }
 
 // ---- K2: decompress + normalise the token stream ------------------------------------
 template <int NB>
 __global__ void __launch_bounds__(kDecWarps * 32)
 stream_decompress_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
-                         const uint8_t* __restrict__ residuals, const uint64_t* __restrict__ offsets, Weights16 W,
-                         const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
-                         const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ pref,
+                         const uint8_t* __restrict__ residuals, Weights16 W, const uint64_t* __restrict__ d_n,
+                         const uint32_t* __restrict__ pref, const uint64_t* __restrict__ fin_base,
                          float* __restrict__ vhat, uint32_t* __restrict__ tok_pass) {
     extern __shared__ __align__(16) float sm[];
     __shared__ float w_s[16];
@@ -130,10 +145,10 @@ stream_decompress_kernel(const float* __restrict__ C, const uint32_t* __restrict
         const bool valid = g < T;
         uint64_t tok = 0;
         uint32_t code = 0;
+        const uint32_t p = tile_finalists(pref, n, tl * 32, g);
         if (valid) {
-            const uint32_t p = find_finalist(pref, n, g);
             tok_pass[g] = p;
-            tok = offsets[finalist_pid(ids, keys, p)] + (g - pref[p]);
+            tok = fin_base[p] + g;
             code = __ldg(codes + tok);
         }
         const uint32_t nv = T - tl * 32 < 32 ? T - tl * 32 : 32;
@@ -196,18 +211,23 @@ stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict_
                      const uint32_t* __restrict__ pref, const uint64_t* __restrict__ d_n,
                      const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
     extern __shared__ __align__(16) float sm[];
-    float* q_s = sm;                      // 32 x kPitch
-    float* tile = sm + 32 * kPitch;       // kMsTile x kPitch
+    // query pairs interleaved: qp[g][d] = (q_{2g}[d], q_{2g+1}[d]) so one
+    // FMUL2 forms both products of a token dim with a query pair
+    float2* qp = reinterpret_cast<float2*>(sm);  // 16 x 128 float2
+    float* tile = sm + 32 * kPitch;              // kMsTile x kPitch
     const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5;
     const uint32_t n = uint32_t(*d_n);
     const uint32_t T = pref[n];
     const uint32_t ntiles = (T + kMsTile - 1) / kMsTile;
     if (blockIdx.x >= ntiles) return;
-    for (uint32_t i = threadIdx.x; i < 32 * 32; i += kMsWarps * 32) {
-        const uint32_t r = i >> 5, c = i & 31;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < rows) v = __ldg(reinterpret_cast<const float4*>(Q + r * 128) + c);
-        reinterpret_cast<float4*>(q_s + r * kPitch)[c] = v;
+    for (uint32_t i = threadIdx.x; i < 16 * 32; i += kMsWarps * 32) {
+        const uint32_t g = i >> 5, d4 = i & 31;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 x = 2 * g < rows ? __ldg(reinterpret_cast<const float4*>(Q + 2 * g * 128) + d4) : z;
+        const float4 y = 2 * g + 1 < rows ? __ldg(reinterpret_cast<const float4*>(Q + (2 * g + 1) * 128) + d4) : z;
+        float4* dst = reinterpret_cast<float4*>(qp + g * 128 + 4 * d4);
+        dst[0] = make_float4(x.x, y.x, x.y, y.y);
+        dst[1] = make_float4(x.z, y.z, x.w, y.w);
     }
     const uint32_t i0 = warp * 8;
     for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
@@ -233,22 +253,26 @@ stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict_
             for (int u = 0; u < 8; ++u) a[u] = 0.0f, c[u] = 0.0f;
             const float4* vr0 = reinterpret_cast<const float4*>(tile + lane * kPitch);
             const float4* vr1 = reinterpret_cast<const float4*>(tile + (32 + lane) * kPitch);
+            const float4* q4 = reinterpret_cast<const float4*>(qp + (i0 / 2) * 128);
 #pragma unroll 2
             for (uint32_t d4 = 0; d4 < 32; ++d4) {
                 const float4 v = vr0[d4], w = vr1[d4];
+                const float vv[4] = {v.x, v.y, v.z, v.w}, ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const float4 q = reinterpret_cast<const float4*>(q_s + (i0 + u) * kPitch)[d4];
-                    float x = a[u], y = c[u];
-                    x = dev::madd_rn(x, q.x, v.x);
-                    y = dev::madd_rn(y, q.x, w.x);
-                    x = dev::madd_rn(x, q.y, v.y);
-                    y = dev::madd_rn(y, q.y, w.y);
-                    x = dev::madd_rn(x, q.z, v.z);
-                    y = dev::madd_rn(y, q.z, w.z);
-                    x = dev::madd_rn(x, q.w, v.w);
-                    y = dev::madd_rn(y, q.w, w.w);
-                    a[u] = x, c[u] = y;
+                for (int gp = 0; gp < 4; ++gp) {
+                    // (q_u, q_u+1) at dims 4*d4 .. 4*d4+3, u = i0 + 2*gp
+                    const float4 qa = q4[gp * 64 + 2 * d4], qb = q4[gp * 64 + 2 * d4 + 1];
+                    const float2 qq[4] = {make_float2(qa.x, qa.y), make_float2(qa.z, qa.w),
+                                          make_float2(qb.x, qb.y), make_float2(qb.z, qb.w)};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        // products rounded once each (FMUL2), then the in-order adds
+                        const float2 p0 = dev::mul2_rn(qq[e], vv[e]), p1 = dev::mul2_rn(qq[e], ww[e]);
+                        a[2 * gp] = __fadd_rn(a[2 * gp], p0.x);
+                        a[2 * gp + 1] = __fadd_rn(a[2 * gp + 1], p0.y);
+                        c[2 * gp] = __fadd_rn(c[2 * gp], p1.x);
+                        c[2 * gp + 1] = __fadd_rn(c[2 * gp + 1], p1.y);
+                    }
                 }
             }
             // segmented max over the lanes of each finalist (its lanes are
@@ -333,15 +357,15 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
         cudaFuncSetAttribute(stream_maxsim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(msm));
         cfg = true;
     }
-    finalist_scan_kernel<<<1, 1024, 0, st>>>(d_ids, d_keys, d_n, ix.doclens, s.pref);
+    finalist_scan_kernel<<<1, 1024, 0, st>>>(d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref, s.fin_base);
     count_launch();
     const uint64_t max_tiles = (nmax * ix.max_doclen + 31) / 32;
     uint64_t db = (max_tiles + kDecWarps - 1) / kDecWarps;
     if (db > uint64_t(sm_count()) * 3) db = uint64_t(sm_count()) * 3;
     auto dk = ix.nbits == 1 ? stream_decompress_kernel<1>
                             : ix.nbits == 2 ? stream_decompress_kernel<2> : stream_decompress_kernel<4>;
-    dk<<<uint32_t(db), kDecWarps * 32, dsm, st>>>(ix.centroids, ix.codes, ix.residuals, ix.offsets, W, d_ids, d_keys,
-                                                  d_n, s.pref, s.vhat, s.tok_pass);
+    dk<<<uint32_t(db), kDecWarps * 32, dsm, st>>>(ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref, s.fin_base,
+                                                  s.vhat, s.tok_pass);
     count_launch();
     uint64_t mb = (nmax * ix.max_doclen + kMsTile - 1) / kMsTile;
     if (mb > uint64_t(sm_count()) * 4) mb = uint64_t(sm_count()) * 4;

@@ -171,3 +171,41 @@ def test_golden_gpu(golden):
             assert np.array_equal(r.topk.passage_ids, e_ids), (golden.name, qi, pi)
             assert np.array_equal(bits(r.topk.scores), e_bits), (golden.name, qi, pi)
             assert r.trace.counters() == e_tr, (golden.name, qi, pi)
+
+
+@pytest.mark.parametrize("params", [(10, 3, 0.3, 64), (50, 8, -1.0, 800), (7, 2, 0.9, 16), (20, 5, 0.45, 20),
+                                    (100, 512, 0.2, 4000)])
+def test_search_params_sweep_gpu(small, port, params):
+    """Stage 2 through the kept-list path and its long-list fallback (t_cs=-1)."""
+    h, qs, idx, s = small
+    p = P.SearchParams(*params)
+    for q in qs[:3]:
+        got = s.search(q, p)
+        ids, sc, tr = port.search(h, q, p)
+        assert np.array_equal(got.topk.passage_ids, ids)
+        assert np.array_equal(bits(got.topk.scores), bits(sc))
+        assert got.trace.counters() == tr
+
+
+def test_saturated_multiplicity(port):
+    """A passage repeating one code > 255 times: the gathered-row counter
+    still matches the reference (saturated ivf_mult entries are recounted)."""
+    rng = np.random.default_rng(3)
+    K, dim = 16, 128
+    C = rng.standard_normal((K, dim)).astype(np.float32)
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    doclens = np.array([300, 20, 40, 300], np.uint32)
+    codes = np.concatenate([np.full(300, 3), rng.integers(0, K, 20), rng.integers(0, K, 40),
+                            np.concatenate([np.full(280, 7), rng.integers(0, K, 20)])]).astype(np.uint32)
+    ivo, post = P.build_inverted_list(codes, doclens, K)
+    cut, w = P.hostindex.quantizer(2)
+    res = rng.integers(0, 256, size=codes.size * 32, dtype=np.uint8)
+    h = P.HostIndex(dim, 2, C, codes, res, doclens, ivo, post, cut, w)
+    s = P.Searcher(P.DeviceIndex.from_host(h, validate=True))
+    q = np.stack([C[3], C[7]] + [C[i % K] for i in range(30)]).astype(np.float32)
+    for prm in (P.SearchParams(4, 2, 0.5, 4), P.SearchParams(4, 16, -1.0, 16), P.SearchParams(2, 4, 0.9, 4)):
+        got = s.search(q, prm)
+        ids, sc, tr = port.search(h, q, prm)
+        assert np.array_equal(got.topk.passage_ids, ids)
+        assert np.array_equal(bits(got.topk.scores), bits(sc))
+        assert got.trace.counters() == tr
