@@ -327,28 +327,28 @@ def run_plaid(args, cfg):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (largest mean phase)
+    # ---- roofline of the dominant kernel: the S_cq kernel (the largest single
+    # launch of a search; the engine's "scores" phase events bracket it alone).
+    # Algorithmic bytes per launch: C read once (512 B per
+    # centroid at d=128), S written once (128 B per centroid), keep bits (1 bit
+    # per centroid) and Q (16 KiB).  3xTF32 FLOPs (3 * 2*K*d*|Q| = 6.4 GFLOP at
+    # cfg2) take ~6 us at the dense tf32 rate, so the kernel is HBM-bound.
     hbm_peak, tf_peak, peak_kind = measured_peaks()
     mean_ph = {n: float(np.mean(v)) for n, v in phases.items()}
-    dom = max(mean_ph, key=mean_ph.get)
     K = cfg["K"]
     tr = trace.counters() if trace is not None else {}
-    alg_bytes = {
-        # C read once + S written once + row max; keep bits/top lists are negligible
-        "scores": 512 * K + 128 * K + 4 * K,
-        "stage4_rank": None,
-        "stage2_interaction": None,
-    }
-    ab = alg_bytes.get(dom)
-    roof = None
-    if ab:
-        ach = ab / (mean_ph[dom] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ach / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                "algorithmic_bytes": ab, "mean_ms": mean_ph[dom]}
-    else:
-        roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": hbm_peak, "unit": "GB/s",
-                "frac": None, "traffic": None, "peak_kind": peak_kind, "mean_ms": mean_ph[dom]}
+    ab = 512 * K + 128 * K + K // 8 + QLEN * DIM * 4
+    ach = ab / (mean_ph["scores"] * 1e-3) / 1e9
+    kname = "scores_tf32_kernel" if args.score_mode == "tensor" else "scores_exact_kernel"
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        t = json.loads(tf.read_text()).get(f"{args.config}/{kname}")
+        traffic = t.get("dram_bytes_per_launch") if t else None
+    roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ach / hbm_peak, "traffic": traffic, "peak_kind": f"{peak_kind} (copy bandwidth, burst)",
+            "algorithmic_bytes_per_launch": ab, "mean_ms": mean_ph["scores"],
+            "share_of_step": mean_ph["scores"] / (1e3 * total_s / args.steps)}
 
     # ---- CPU baseline: the reference's own searcher on this host, bounded sample
     cpu = None
@@ -392,7 +392,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="plaid", choices=["plaid", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--score-mode", default="exact", choices=["exact", "tensor"])
+    ap.add_argument("--score-mode", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -96,6 +96,9 @@ def build_all(verbose: bool = False) -> None:
     build_synth(verbose)
     build_oracle(verbose)
     build_plaid(verbose)
+    if Path("/root/reference/proj/src").is_dir():
+        # drop-in demonstration: reference lir code calling libplaid (test infra)
+        _run(["make", "-s", "-C", str(ROOT / "oracle"), "dropin"], verbose)
 
 
 if __name__ == "__main__":

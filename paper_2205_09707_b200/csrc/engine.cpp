@@ -470,10 +470,11 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     uint64_t* c = counters_.p;
     uint32_t* bitmap = bitmap_.p;
     uint32_t* owners = bitmap_.p + (N + 31) / 32;
-    record(0, st, times);
     // one memset clears the per-query counters, the candidate bitmap and the
-    // kept-owner bitmap (contiguous in zero_)
+    // stage-2 used bitmap (contiguous in zero_); the "scores" phase then
+    // brackets the S_cq kernel alone
     PLAID_CUDA(cudaMemsetAsync(zero_.p, 0, zero_.n * sizeof(uint32_t), st));
+    record(0, st, times);
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;

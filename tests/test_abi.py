@@ -116,3 +116,14 @@ def test_compute_fails_loudly_without_gpu():
     with pytest.raises(P.PlaidError) as e:
         P.Searcher(None)
     assert e.value.code == P.ErrorCode.CudaError
+
+
+DROPIN = ROOT / "oracle" / "_ref" / "lir_dropin"
+
+
+@pytest.mark.skipif(HAS_GPU or not DROPIN.exists(), reason="no-GPU behaviour of the lir drop-in binary")
+def test_lir_dropin_fails_loudly_without_gpu():
+    """Reference lir code linked against libplaid through include/plaid_lir.hpp
+    (oracle/lir_dropin.cpp): without a GPU the engine refuses, no CPU answer."""
+    r = subprocess.run([str(DROPIN)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and r.stdout.startswith("NOGPU")

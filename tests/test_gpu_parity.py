@@ -209,3 +209,18 @@ def test_saturated_multiplicity(port):
         assert np.array_equal(got.topk.passage_ids, ids)
         assert np.array_equal(bits(got.topk.scores), bits(sc))
         assert got.trace.counters() == tr
+
+
+def test_lir_dropin_binary():
+    """The drop-in demonstration: reference `lir` code (compiled reference
+    sources) swaps lir::search for plaid_lir::Engine::search unchanged, and
+    both return identical ids, score bits and trace counters."""
+    import subprocess
+    from pathlib import Path
+
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "lir_dropin"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/lir_dropin not built (needs the reference sources at build time)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("OK")
