@@ -204,6 +204,7 @@ template struct DevBuf<uint32_t>;
 template struct DevBuf<uint64_t>;
 template struct DevBuf<unsigned char>;
 template struct DevBuf<SelectState>;
+template struct DevBuf<SelectHist>;
 template struct DevBuf<int>;
 
 // ---------------------------------------------------------------- DeviceIndex
@@ -370,6 +371,8 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         chunk_counts_.ensure(launch::bitmap_chunks(ix.N));
         c1_.ensure(ix.N);
         slot_of_.ensure(ix.N);
+        bkeys_.ensure(ix.N);
+        sel_hist_.ensure(1);
         kept_list_.ensure(ix.K);
         acc2_.ensure(ix.N * 32);
         PLAID_CUDA(cudaMemset(acc2_.p, 0, acc2_.n * sizeof(uint32_t)));
@@ -521,7 +524,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
                               slot_of_.p, acc2_.p, reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p,
                               reinterpret_cast<unsigned long long*>(c + kRows2), st);
         record(3, st, times);
-        launch::select_top_large(keys2_.p, c + kN1, N, p.ndocs, sel_state_.p, sel2_.p, c + kN2, st);
+        launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st);
         record(4, st, times);
         // Stage 3: full centroid interaction, keep max(ceil(ndocs/4), k).
         const uint64_t n3 = std::min<uint64_t>(stage3_width(p), N);

@@ -142,7 +142,7 @@ private:
     DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, out_pids_, ids_tmp_, tok_pass_, pref_, run_, slot_of_,
         kept_list_, acc2_;
     launch::RankScratch rank_scratch_;
-    DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_,
+    DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_, bkeys_,
         tmp_keys_, kconst_;
     // zero_ = [16 u64 counters | candidate bitmap (N bits) | kept-owner bitmap
     // (N bits)], cleared by a single memset per query.
@@ -155,6 +155,7 @@ private:
     View<uint32_t> bitmap_;
     DevBuf<unsigned char> bytes_tmp_;
     DevBuf<SelectState> sel_state_;
+    DevBuf<SelectHist> sel_hist_;
     DevBuf<int> status_;
     // pinned staging
     float* h_q_ = nullptr;

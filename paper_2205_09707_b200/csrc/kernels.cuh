@@ -5,6 +5,7 @@
 // launch sequence that can be captured in a CUDA graph with no host sync.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -33,6 +34,22 @@ struct SelectState {
     unsigned int hist[6][2048];
     unsigned int bar_count;
     unsigned int bar_gen;
+    unsigned int bnd_n;                // keys in the boundary bucket (see radix_select_kernel)
+    unsigned int pad;
+    unsigned long long bnd[1024];      // not zeroed: only [0, bnd_n) is read
+};
+constexpr size_t kSelectStateZeroBytes = offsetof(SelectState, bnd);
+
+// Histogram select scratch (select_top_hist): a 65536-bin histogram of the
+// keys' top 16 bits and the control words; zeroed by the launcher.
+struct SelectHist {
+    unsigned int hist[65536];
+    unsigned long long above;   // keys in buckets above the boundary bucket
+    unsigned long long bcount;  // keys in the boundary bucket
+    unsigned long long rem;     // boundary keys still to take
+    unsigned int bucket;        // boundary bucket (top 16 key bits)
+    unsigned int take_all;      // n <= want
+    unsigned long long bn;      // boundary keys written to the side buffer
 };
 
 constexpr int kScoresPitch = 32;  // S rows padded to 32 floats (128 B)
@@ -113,6 +130,12 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
 void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
                       SelectState* d_state, uint64_t* d_out_keys, uint64_t* d_out_n,
                       cudaStream_t st);
+// Same result as select_top_large without grid barriers: histogram of the top
+// 16 key bits, one-CTA bucket search, compaction (keys above the boundary
+// bucket -> out, bucket keys -> d_bkeys, capacity nmax), exact resolution of
+// the bucket by rank (<= 8192 keys) or a one-CTA radix pass (larger).
+void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, SelectHist* d_st,
+                     uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st);
 // Sort keys[0..*d_n) descending (n <= nmax) and emit the first min(want, n):
 // out_keys (optional), out_ids/out_scores (optional, ids offset by id_base),
 // out_n (optional).  nmax <= kSmallSortMax uses one CTA; larger uses a

@@ -13,6 +13,7 @@
 //     beyond that; emits the first `want` keys as (id, score) pairs in order.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "device.cuh"
@@ -24,6 +25,8 @@ namespace {
 constexpr uint32_t kBins = 2048;
 constexpr int kPasses = 6;
 constexpr uint32_t kSelThreads = 512;
+constexpr uint32_t kBoundaryCap = 1024;  // boundary-bucket keys resolved in one CTA (fits h[] as u64)
+static_assert(kBoundaryCap * 8 <= kBins * 4, "boundary keys reuse the histogram's shared memory");
 __host__ __device__ constexpr int pass_shift(int p) { return p < 5 ? 53 - 11 * p : 0; }
 __host__ __device__ constexpr int pass_bits(int p) { return p < 5 ? 11 : 9; }
 
@@ -49,10 +52,10 @@ __device__ __forceinline__ void grid_sync(unsigned int* count, unsigned int* gen
 __global__ void __launch_bounds__(kSelThreads)
 radix_select_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
                     SelectState* st, uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
-    __shared__ uint32_t h[kBins];
+    __shared__ __align__(16) uint32_t h[kBins];
     __shared__ uint32_t part[kSelThreads];
     __shared__ unsigned long long s_prefix, s_mask, s_rem;
-    __shared__ int s_done;
+    __shared__ int s_done, s_small;
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint64_t n = *d_n;
     if (tid == 0) {
@@ -60,11 +63,12 @@ radix_select_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restric
         s_mask = 0;
         s_rem = n < want ? n : want;
         s_done = n <= want;
+        s_small = 0;
     }
     const uint64_t stride = uint64_t(gridDim.x) * kSelThreads;
     for (int pass = 0; pass < kPasses; ++pass) {
         __syncthreads();
-        if (s_done) break;
+        if (s_done || s_small) break;
         const int shift = pass_shift(pass);
         const uint32_t nb = 1u << pass_bits(pass);
         const uint64_t prefix = s_prefix, mask = s_mask;
@@ -112,6 +116,9 @@ radix_select_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restric
                     s_prefix = prefix | (uint64_t(bin) << shift);
                     s_mask = mask | (uint64_t(nb - 1) << shift);
                     s_done = cnt == rem - cum;
+                    // a small boundary bucket is resolved exactly in one CTA
+                    // instead of by further passes over all n keys
+                    s_small = cnt <= kBoundaryCap;
                     break;
                 }
                 cum += cnt;
@@ -119,6 +126,44 @@ radix_select_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restric
         }
     }
     __syncthreads();
+    if (s_small && !s_done) {
+        // keys above the boundary bucket are all in; the bucket's keys (at
+        // most kBoundaryCap) go to st->bnd and CTA 0 keeps their top s_rem
+        const uint64_t prefix = s_prefix, mask = s_mask;
+        for (uint64_t i0 = uint64_t(blockIdx.x) * kSelThreads; i0 < n; i0 += stride) {
+            const uint64_t i = i0 + tid;
+            const uint64_t k = i < n ? __ldcg(keys + i) : 0;
+            const uint64_t top = k & mask;
+            const bool above = i < n && top > prefix, inb = i < n && top == prefix;
+            const uint32_t ba = __ballot_sync(0xffffffffu, above), bb = __ballot_sync(0xffffffffu, inb);
+            if (ba) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd((unsigned long long*)out_n, (unsigned long long)__popc(ba));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (above) out[base + __popc(ba & ((1u << lane) - 1))] = k;
+            }
+            if (bb) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&st->bnd_n, uint32_t(__popc(bb)));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (inb) st->bnd[base + __popc(bb & ((1u << lane) - 1))] = k;
+            }
+        }
+        grid_sync(&st->bar_count, &st->bar_gen);
+        if (blockIdx.x != 0) return;
+        unsigned long long* sb = reinterpret_cast<unsigned long long*>(h);  // kBins u32 = kBoundaryCap u64
+        const uint32_t nbd = __ldcg(&st->bnd_n);
+        for (uint32_t j = tid; j < nbd; j += kSelThreads) sb[j] = __ldcg(&st->bnd[j]);
+        __syncthreads();
+        const uint64_t rem = s_rem;
+        for (uint32_t j = tid; j < nbd; j += kSelThreads) {
+            const unsigned long long x = sb[j];
+            uint32_t rank = 0;
+            for (uint32_t m = 0; m < nbd; ++m) rank += sb[m] > x;
+            if (rank < rem) out[atomicAdd((unsigned long long*)out_n, 1ull)] = x;
+        }
+        return;
+    }
     // compaction of every key >= threshold (exactly min(want, n) keys)
     const uint64_t thr = s_prefix;
     for (uint64_t i0 = uint64_t(blockIdx.x) * kSelThreads; i0 < n; i0 += stride) {
@@ -318,15 +363,208 @@ uint64_t next_pow2(uint64_t v) {
     return p;
 }
 
+// ---- histogram select (no grid barriers) ----------------------------------------------
+constexpr uint32_t kHistBucketShift = 48;  // top 16 key bits = sign, exponent, 7 mantissa bits of the score
+constexpr uint32_t kRankCap = 8192;       // boundary buckets up to this size are ranked in parallel
+
+// The bucket of score 0 (all-masked stage-2 candidates): counted per block in
+// shared memory so that bucket costs one global atomic per block.
+constexpr uint32_t kZeroBucket = 0x8000u;
+
+__global__ void hist16_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
+                              SelectHist* __restrict__ st) {
+    __shared__ uint32_t zeros;
+    if (threadIdx.x == 0) zeros = 0;
+    __syncthreads();
+    const uint64_t n = *d_n;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
+         i0 += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = i0 + lane;
+        const uint32_t b = i < n ? uint32_t(__ldcg(keys + i) >> kHistBucketShift) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        if (i < n && lane == uint32_t(__ffs(peers) - 1)) {
+            if (b == kZeroBucket) atomicAdd(&zeros, uint32_t(__popc(peers)));
+            else atomicAdd(&st->hist[b], uint32_t(__popc(peers)));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && zeros) atomicAdd(&st->hist[kZeroBucket], zeros);
+}
+
+// One CTA: the bucket (from the top) holding the want-th largest key.  Warp
+// w sums buckets [2048 w, 2048 w + 2048) with coalesced loads; the warp whose
+// range holds the target walks it from the top, 32 buckets per step.
+__global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restrict__ d_n, uint64_t want,
+                                                         SelectHist* __restrict__ st) {
+    __shared__ unsigned long long warp_tot[32];
+    const uint64_t n = *d_n;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (n <= want) {
+        if (t == 0) st->take_all = 1;
+        return;
+    }
+    const uint32_t* hw = st->hist + warp * 2048;
+    unsigned long long mine = 0;
+#pragma unroll 8
+    for (uint32_t j = 0; j < 64; ++j) mine += hw[j * 32 + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) warp_tot[warp] = mine;
+    __syncthreads();
+    // keys in the warps' ranges above this one (higher buckets = higher warps)
+    unsigned long long above = 0;
+    for (uint32_t w = warp + 1; w < 32; ++w) above += warp_tot[w];
+    if (!(above < want && want <= above + warp_tot[warp])) return;
+    for (int j = 63; j >= 0; --j) {
+        const uint32_t c = hw[j * 32 + lane];
+        // inclusive sum from the top lane down (bucket 32 j + 31 first)
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_down_sync(0xffffffffu, incl, o);
+            if (lane + o < 32) incl += y;
+        }
+        const uint32_t chunk = __shfl_sync(0xffffffffu, incl, 0);
+        if (above + chunk >= want) {
+            const bool hit = above + incl >= want && above + incl - c < want;
+            if (hit) {
+                st->bucket = warp * 2048 + j * 32 + lane;
+                st->above = above + incl - c;
+                st->bcount = c;
+                st->rem = want - (above + incl - c);
+            }
+            return;
+        }
+        above += chunk;
+    }
+}
+
+__global__ void hist_compact_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
+                                    SelectHist* __restrict__ st, uint64_t* __restrict__ bkeys,
+                                    uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
+    const uint64_t n = *d_n;
+    const bool all = st->take_all;
+    const uint32_t bucket = st->bucket;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
+         i0 += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = i0 + lane;
+        const uint64_t k = i < n ? __ldcg(keys + i) : 0;
+        const uint32_t b = uint32_t(k >> kHistBucketShift);
+        const bool above = i < n && (all || b > bucket), inb = i < n && !all && b == bucket;
+        const uint32_t ba = __ballot_sync(0xffffffffu, above), bb = __ballot_sync(0xffffffffu, inb);
+        if (ba) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd((unsigned long long*)out_n, (unsigned long long)__popc(ba));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (above) out[base + __popc(ba & ((1u << lane) - 1))] = k;
+        }
+        if (bb) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&st->bn, (unsigned long long)__popc(bb));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (inb) bkeys[base + __popc(bb & ((1u << lane) - 1))] = k;
+        }
+    }
+}
+
+// Boundary bucket: keys are unique, so the top `rem` are those with fewer
+// than `rem` bucket keys above them.  Up to kRankCap keys: every CTA stages
+// the bucket in shared memory and ranks 32 of them (4 threads per key).
+// Larger buckets (massive score ties, e.g. the all-masked zeros of stage 2):
+// CTA 0 runs an MSB radix select over the bucket's low 48 bits.
+__global__ void __launch_bounds__(128)
+hist_resolve_kernel(SelectHist* __restrict__ st, const uint64_t* __restrict__ bkeys, uint64_t* __restrict__ out,
+                    uint64_t* __restrict__ out_n) {
+    extern __shared__ __align__(16) uint64_t s[];
+    if (st->take_all) return;
+    const uint32_t nb = uint32_t(st->bcount);
+    const uint64_t rem = st->rem;
+    const uint32_t t = threadIdx.x;
+    if (nb <= kRankCap) {
+        if (blockIdx.x * 32 >= nb) return;
+        for (uint32_t i = t; i < nb; i += 128) s[i] = __ldcg(bkeys + i);
+        __syncthreads();
+        const uint32_t me = blockIdx.x * 32 + (t >> 2), q = t & 3;
+        const uint64_t x = me < nb ? s[me] : ~0ull;
+        uint32_t rank = 0;
+        for (uint32_t j = q; j < nb; j += 4) rank += s[j] > x;
+        rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+        rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+        if (q == 0 && me < nb && rank < rem) out[atomicAdd((unsigned long long*)out_n, 1ull)] = x;
+        return;
+    }
+    if (blockIdx.x != 0) return;
+    // one-CTA radix over bits 47..0, 8 bits per pass
+    uint32_t* h = reinterpret_cast<uint32_t*>(s);
+    __shared__ unsigned long long s_prefix, s_rem;
+    unsigned long long prefix = 0, mask = 0;
+    if (t == 0) s_rem = rem;
+    for (int shift = 40; shift >= 0; shift -= 8) {
+        for (uint32_t b = t; b < 256; b += 128) h[b] = 0;
+        __syncthreads();
+        for (uint32_t i = t; i < nb; i += 128) {
+            const uint64_t k = __ldcg(bkeys + i) & 0xFFFFFFFFFFFFull;
+            if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        if (t == 0) {
+            unsigned long long cum = 0, r = s_rem;
+            for (int b = 255; b >= 0; --b) {
+                if (cum + h[b] >= r) {
+                    s_prefix = prefix | (uint64_t(b) << shift);
+                    s_rem = r - cum;
+                    break;
+                }
+                cum += h[b];
+            }
+        }
+        __syncthreads();
+        prefix = s_prefix;
+        mask |= uint64_t(255) << shift;
+    }
+    // threshold key (bucket bits + resolved low bits): exactly rem keys >= it
+    const uint64_t thr = (uint64_t(st->bucket) << kHistBucketShift) | prefix;
+    for (uint32_t i = t; i < nb; i += 128) {
+        const uint64_t k = __ldcg(bkeys + i);
+        if (k >= thr) out[atomicAdd((unsigned long long*)out_n, 1ull)] = k;
+    }
+}
+
 }  // namespace
 
 namespace launch {
+
+void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, SelectHist* d_st,
+                     uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st) {
+    cudaMemsetAsync(d_st, 0, sizeof(SelectHist), st);
+    cudaMemsetAsync(d_out_n, 0, sizeof(uint64_t), st);
+    if (nmax == 0) return;
+    const uint32_t grid = grid_for(nmax, 256, uint32_t(sm_count()) * 8);
+    hist16_kernel<<<grid, 256, 0, st>>>(d_keys, d_n, d_st);
+    count_launch();
+    hist_find_kernel<<<1, 1024, 0, st>>>(d_n, want, d_st);
+    count_launch();
+    hist_compact_kernel<<<grid, 256, 0, st>>>(d_keys, d_n, d_st, d_bkeys, d_out_keys, d_out_n);
+    count_launch();
+    static bool cfg = false;
+    if (!cfg) {
+        cudaFuncSetAttribute(hist_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kRankCap * sizeof(uint64_t)));
+        cfg = true;
+    }
+    const uint64_t rb = std::min<uint64_t>((std::min<uint64_t>(nmax, kRankCap) + 31) / 32, kRankCap / 32);
+    hist_resolve_kernel<<<uint32_t(rb ? rb : 1), 128, kRankCap * sizeof(uint64_t), st>>>(d_st, d_bkeys, d_out_keys,
+                                                                                       d_out_n);
+    count_launch();
+}
 
 void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
                       SelectState* d_state, uint64_t* d_out_keys, uint64_t* d_out_n,
                       cudaStream_t st) {
     // state (histograms, barrier counter) and the output count start at zero
-    cudaMemsetAsync(d_state, 0, sizeof(SelectState), st);
+    cudaMemsetAsync(d_state, 0, kSelectStateZeroBytes, st);
     cudaMemsetAsync(d_out_n, 0, sizeof(uint64_t), st);
     static int per_sm = 0;
     if (!per_sm) {

@@ -224,3 +224,20 @@ def test_lir_dropin_binary():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().endswith("OK")
+
+
+def test_stage2_select_massive_ties(port):
+    """Stage-2 select when the ndocs boundary falls among > 8192 equal (zero)
+    scores: the histogram select's one-CTA radix fallback (select.cu)."""
+    h = P.generate_index(40000, 1024, dim=128, nbits=2, mean_len=20, spread=8, seed=9)
+    qs = P.generate_queries(h, 2, seed=5)
+    s = P.Searcher(P.DeviceIndex.from_host(h))
+    for prm in (P.SearchParams(50, 256, 0.9, 30000), P.SearchParams(50, 64, 0.95, 9000),
+                P.SearchParams(10, 16, 0.3, 200)):
+        for q in qs:
+            got = s.search(q, prm)
+            ids, sc, tr = port.search(h, q, prm)
+            assert tr["stage1_candidates"] > 8192 or prm.ndocs == 200
+            assert np.array_equal(got.topk.passage_ids, ids)
+            assert np.array_equal(bits(got.topk.scores), bits(sc))
+            assert got.trace.counters() == tr
