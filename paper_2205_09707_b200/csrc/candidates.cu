@@ -24,6 +24,7 @@ __global__ void postings_bitmap_kernel(const uint64_t* __restrict__ ivf_offsets,
                                        const uint32_t* __restrict__ postings,
                                        const uint32_t* __restrict__ sel,
                                        uint32_t* __restrict__ bitmap) {
+    dev::pdl_wait();
     const uint32_t c = sel[blockIdx.x];
     const uint64_t b = ivf_offsets[c], e = ivf_offsets[c + 1];
     for (uint64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
@@ -42,6 +43,7 @@ __device__ __forceinline__ uint32_t masked_word(const uint32_t* bitmap, uint64_t
 
 __global__ void chunk_count_kernel(const uint32_t* __restrict__ bitmap, uint64_t N,
                                    uint32_t* __restrict__ counts) {
+    dev::pdl_wait();
     __shared__ uint32_t warp_sums[kThreads / 32];
     const uint64_t w0 = uint64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
     uint32_t n = 0;
@@ -61,6 +63,7 @@ __global__ void chunk_count_kernel(const uint32_t* __restrict__ bitmap, uint64_t
 __global__ void chunk_write_kernel(const uint32_t* __restrict__ bitmap, uint64_t N,
                                    const uint32_t* __restrict__ counts, uint32_t* __restrict__ out,
                                    uint64_t* __restrict__ out_n) {
+    dev::pdl_wait();
     __shared__ uint64_t red[kThreads / 32];
     __shared__ uint32_t scan[kThreads / 32];
     // base = sum of counts of the chunks before this one
@@ -112,7 +115,7 @@ namespace launch {
 void postings_to_bitmap(const IndexView& ix, const uint32_t* d_sel, uint32_t nsel,
                         uint32_t* d_bitmap, cudaStream_t st) {
     if (nsel == 0) return;
-    postings_bitmap_kernel<<<nsel, 256, 0, st>>>(ix.ivf_offsets, ix.ivf_postings, d_sel, d_bitmap);
+    ::plaid::launch::pdl(postings_bitmap_kernel, nsel, 256, 0, st, ix.ivf_offsets, ix.ivf_postings, d_sel, d_bitmap);
     count_launch();
 }
 
@@ -125,8 +128,8 @@ uint32_t bitmap_chunks(uint64_t N) {
 void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_counts,
                     uint32_t* d_out_ids, uint64_t* d_out_n, cudaStream_t st) {
     const uint32_t chunks = bitmap_chunks(N);
-    chunk_count_kernel<<<chunks, kThreads, 0, st>>>(d_bitmap, N, d_chunk_counts);
-    chunk_write_kernel<<<chunks, kThreads, 0, st>>>(d_bitmap, N, d_chunk_counts, d_out_ids, d_out_n);
+    ::plaid::launch::pdl(chunk_count_kernel, chunks, kThreads, 0, st, d_bitmap, N, d_chunk_counts);
+    ::plaid::launch::pdl(chunk_write_kernel, chunks, kThreads, 0, st, d_bitmap, N, d_chunk_counts, d_out_ids, d_out_n);
     count_launch();
     count_launch();
 }

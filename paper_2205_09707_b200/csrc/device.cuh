@@ -76,6 +76,13 @@ __device__ __forceinline__ float warp_max(float v) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: every kernel is launched with
+// programmatic stream serialization (launch::pdl) so its launch and block
+// scheduling overlap the previous kernel's tail; it must not touch memory the
+// previous kernels write before this wait (a no-op without a PDL edge).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Branchless insertion of x into a descending list k[0..NP) of unique keys.
 template <int NP>
 __device__ __forceinline__ void topn_insert(uint64_t (&k)[NP], uint64_t x) {

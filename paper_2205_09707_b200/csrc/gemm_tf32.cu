@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const float* __restrict__ Q,
                    uint32_t rows, float t_cs, float* __restrict__ S, uint32_t* __restrict__ keep_bits,
                    uint64_t* __restrict__ partial, uint32_t* __restrict__ gthr, uint32_t dbg) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t base = smem_u32(smem);
@@ -462,7 +463,7 @@ void launch_tf32(const CUtensorMap& map, const IndexView& ix, const float* q, ui
         const char* e = getenv("PLAID_TF32_DBG");
         return e ? uint32_t(atoi(e)) : 0u;
     }();
-    scores_tf32_kernel<NP><<<grid, kThreads, kSmemBytes, st>>>(map, ix.K, q, rows, t_cs, S, keep, partial, gthr, dbg);
+    ::plaid::launch::pdl(scores_tf32_kernel<NP>, grid, kThreads, kSmemBytes, st, map, ix.K, q, rows, t_cs, S, keep, partial, gthr, dbg);
     launch::count_launch();
 }
 

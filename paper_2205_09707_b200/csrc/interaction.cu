@@ -82,6 +82,7 @@ ci_warp_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ 
                const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ keep_bits,
                uint64_t* __restrict__ out_keys, float* __restrict__ out_scores,
                unsigned long long* __restrict__ d_rows) {
+    dev::pdl_wait();
     const uint64_t n = *d_n;
     const uint32_t lane = dev::lane_id();
     const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
@@ -111,6 +112,7 @@ ci_masked_flat_kernel(const uint32_t* __restrict__ codes, const uint64_t* __rest
                       const uint32_t* __restrict__ keep_bits, const uint32_t* __restrict__ owners,
                       uint64_t* __restrict__ out_keys, float* __restrict__ out_scores,
                       unsigned long long* __restrict__ d_rows) {
+    dev::pdl_wait();
     __shared__ uint64_t off_s[kCB];
     __shared__ uint32_t start_s[kCB + 1];
     __shared__ uint32_t acc_s[kCB * kAccPitch];
@@ -248,6 +250,7 @@ ci_masked_flat_kernel(const uint32_t* __restrict__ codes, const uint64_t* __rest
 __global__ void kept_owners_kernel(const uint32_t* __restrict__ keep_bits, uint64_t K,
                                    const uint64_t* __restrict__ ivf_offsets,
                                    const uint32_t* __restrict__ postings, uint32_t* __restrict__ owners) {
+    dev::pdl_wait();
     const uint32_t lane = dev::lane_id();
     const uint64_t words = (K + 31) / 32;
     const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
@@ -293,6 +296,7 @@ __global__ void kept_owners_kernel(const uint32_t* __restrict__ keep_bits, uint6
 __global__ void keep_list_kernel(const uint32_t* __restrict__ keep_bits, uint64_t K,
                                  const uint64_t* __restrict__ ivf_offsets, uint32_t* __restrict__ list,
                                  unsigned long long* __restrict__ counts /* [0] kept, [1] postings */) {
+    dev::pdl_wait();
     const uint32_t lane = dev::lane_id();
     const uint64_t words = (K + 31) / 32;
     for (uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; w0 < words;
@@ -332,6 +336,7 @@ __device__ __forceinline__ bool use_lists(const unsigned long long* counts, uint
 
 __global__ void slot_scatter_kernel(const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
                                     uint32_t* __restrict__ slot_of) {
+    dev::pdl_wait();
     const uint64_t n = *d_n1;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         slot_of[c1[i]] = uint32_t(i);
@@ -346,6 +351,7 @@ ivf_accumulate_kernel(const uint32_t* __restrict__ list, const unsigned long lon
                       const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ doclens,
                       uint32_t* __restrict__ acc, uint32_t* __restrict__ used_bits,
                       unsigned long long* __restrict__ d_rows) {
+    dev::pdl_wait();
     if (!use_lists(counts, *d_n1)) return;
     const uint64_t kept = counts[0];
     const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -394,6 +400,7 @@ __global__ void stage2_finalize_kernel(const uint32_t* __restrict__ c1, const ui
                                        const unsigned long long* __restrict__ counts, uint32_t rows,
                                        uint32_t* __restrict__ acc, const uint32_t* __restrict__ used_bits,
                                        uint64_t* __restrict__ keys_out) {
+    dev::pdl_wait();
     const uint64_t n = *d_n1;
     if (!use_lists(counts, n)) return;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -422,6 +429,7 @@ ci_all_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ o
               const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
               const unsigned long long* __restrict__ counts, const uint32_t* __restrict__ keep_bits,
               uint64_t* __restrict__ keys_out, unsigned long long* __restrict__ d_rows) {
+    dev::pdl_wait();
     const uint64_t n = *d_n1;
     if (use_lists(counts, n)) return;
     const uint32_t lane = dev::lane_id();
@@ -455,7 +463,7 @@ void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_o
     const uint64_t tasks = ((ix.K + 31) / 32 + 31) / 32;  // one warp per 32 keep words
     uint64_t blocks = (tasks + 7) / 8;
     if (blocks == 0) blocks = 1;
-    kept_owners_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_keep_bits, ix.K, ix.ivf_offsets, ix.ivf_postings,
+    ::plaid::launch::pdl(kept_owners_kernel, uint32_t(blocks), 256, 0, st, d_keep_bits, ix.K, ix.ivf_offsets, ix.ivf_postings,
                                                          d_owners);
     count_launch();
 }
@@ -468,21 +476,21 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
     const uint64_t words = (ix.K + 31) / 32;
     uint64_t kb = (words + 255) / 256;
     if (kb == 0) kb = 1;
-    keep_list_kernel<<<uint32_t(kb), 256, 0, st>>>(d_keep_bits, ix.K, ix.ivf_offsets, d_kept_list, d_counts2);
+    ::plaid::launch::pdl(keep_list_kernel, uint32_t(kb), 256, 0, st, d_keep_bits, ix.K, ix.ivf_offsets, d_kept_list, d_counts2);
     count_launch();
     if (nmax == 0) return;
     uint64_t sb = (nmax + 255) / 256;
     if (sb > uint64_t(sms) * 8) sb = uint64_t(sms) * 8;
-    slot_scatter_kernel<<<uint32_t(sb), 256, 0, st>>>(d_c1, d_n1, d_slot_of);
+    ::plaid::launch::pdl(slot_scatter_kernel, uint32_t(sb), 256, 0, st, d_c1, d_n1, d_slot_of);
     count_launch();
-    ivf_accumulate_kernel<<<sms * 8, 256, 0, st>>>(d_kept_list, d_counts2, d_n1, ix.ivf_offsets, ix.ivf_postings,
+    ::plaid::launch::pdl(ivf_accumulate_kernel, sms * 8, 256, 0, st, d_kept_list, d_counts2, d_n1, ix.ivf_offsets, ix.ivf_postings,
                                                    ix.ivf_mult, d_cand_bits, d_slot_of, d_scores, rows, ix.codes,
                                                    ix.offsets, ix.doclens, d_acc, d_used_bits, d_rows);
     count_launch();
-    stage2_finalize_kernel<<<uint32_t(sb), 256, 0, st>>>(d_c1, d_n1, d_counts2, rows, d_acc, d_used_bits,
+    ::plaid::launch::pdl(stage2_finalize_kernel, uint32_t(sb), 256, 0, st, d_c1, d_n1, d_counts2, rows, d_acc, d_used_bits,
                                                          d_out_keys);
     count_launch();
-    ci_all_kernel<<<sms * 8, 256, 0, st>>>(ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_c1, d_n1, d_counts2,
+    ::plaid::launch::pdl(ci_all_kernel, sms * 8, 256, 0, st, ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_c1, d_n1, d_counts2,
                                            d_keep_bits, d_out_keys, d_rows);
     count_launch();
 }
@@ -497,14 +505,14 @@ void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t r
         uint64_t blocks = (nmax + kCB - 1) / kCB;
         const uint64_t cap = uint64_t(sm_count()) * 4;
         if (blocks > cap) blocks = cap;
-        ci_masked_flat_kernel<<<uint32_t(blocks), kCB, 0, st>>>(
+        ::plaid::launch::pdl(ci_masked_flat_kernel, uint32_t(blocks), kCB, 0, st, 
             ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_ids, d_keys, d_n, d_keep_bits, d_owners,
             d_out_keys, d_out_scores, d_rows);
     } else {
         uint64_t blocks = (nmax + 7) / 8;
         const uint64_t cap = uint64_t(sm_count()) * 8;
         if (blocks > cap) blocks = cap;
-        ci_warp_kernel<<<uint32_t(blocks), 256, 0, st>>>(ix.codes, ix.offsets, ix.doclens, d_scores,
+        ::plaid::launch::pdl(ci_warp_kernel, uint32_t(blocks), 256, 0, st, ix.codes, ix.offsets, ix.doclens, d_scores,
                                                         rows, d_ids, d_keys, d_n, d_keep_bits,
                                                         d_out_keys, d_out_scores, d_rows);
     }

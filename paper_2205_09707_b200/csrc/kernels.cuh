@@ -56,6 +56,24 @@ constexpr int kScoresPitch = 32;  // S rows padded to 32 floats (128 B)
 
 namespace launch {
 
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while the previous kernel in the stream drains; every kernel
+// starts with dev::pdl_wait(), so no data dependence is relaxed.
+template <typename... KArgs, typename... Args>
+inline void pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---- stage 1 -----------------------------------------------------------------
 // S = C . Q^T (in-order fp32, bit-exact), row max, keep bits (row max >= t_cs),
 // and per-warp top-NP keys per query token written to `partial`

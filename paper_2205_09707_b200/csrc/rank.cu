@@ -75,6 +75,7 @@ rank_exact_kernel(const float* __restrict__ C, const uint32_t* __restrict__ code
                   const float* __restrict__ Q, uint32_t rows, const uint32_t* __restrict__ ids,
                   const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
                   uint64_t* __restrict__ out_keys) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) float sm[];
     const uint32_t pitch = dim + 4;
     float* q_s = sm;                    // 32 x pitch
@@ -173,6 +174,7 @@ rank128_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
                const uint64_t* __restrict__ offsets, Weights W, const float* __restrict__ Q, uint32_t rows,
                const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
                const uint64_t* __restrict__ d_n, uint64_t* __restrict__ out_keys) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) float sm[];
     __shared__ float w_s[16];
     constexpr uint32_t kBpt = NB * 128 / 8;  // residual bytes per token
@@ -285,6 +287,7 @@ rank128_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
 
 __global__ void unpack_kernel(const uint8_t* __restrict__ packed, uint64_t n, uint32_t nbits,
                               uint8_t* __restrict__ out) {
+    dev::pdl_wait();
     const uint32_t per = 8 / nbits, mask = (1u << nbits) - 1;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -297,6 +300,7 @@ __global__ void unpack_kernel(const uint8_t* __restrict__ packed, uint64_t n, ui
 __global__ void reconstruct_kernel(const float* __restrict__ C, uint32_t dim, uint32_t nbits, Weights W,
                                    const uint32_t* __restrict__ codes, uint64_t n,
                                    const uint8_t* __restrict__ residuals, float* __restrict__ out) {
+    dev::pdl_wait();
     const uint64_t bpt = uint64_t(nbits) * dim / 8;
     const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t t = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); t < n; t += nw) {
@@ -315,6 +319,7 @@ __global__ void reconstruct_kernel(const float* __restrict__ C, uint32_t dim, ui
 __global__ void maxsim_packed_kernel(const float* __restrict__ scores, uint32_t nq,
                                      const uint64_t* __restrict__ offsets, uint64_t np,
                                      float* __restrict__ out) {
+    dev::pdl_wait();
     const uint32_t lane = dev::lane_id();
     const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); p < np; p += nw) {
@@ -332,6 +337,7 @@ __global__ void maxsim_embeddings_kernel(const float* __restrict__ Q, uint32_t r
                                          const float* __restrict__ emb,
                                          const uint64_t* __restrict__ offsets, uint64_t np,
                                          float* __restrict__ out) {
+    dev::pdl_wait();
     const uint32_t lane = dev::lane_id();
     const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
     const float* q = Q + uint64_t(lane < rows ? lane : 0) * dim;
@@ -384,7 +390,7 @@ void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint
         uint64_t blocks = uint64_t(sm_count()) * 3;
         if (blocks > nmax) blocks = nmax;
         auto k = ix.nbits == 1 ? rank128_kernel<1> : ix.nbits == 2 ? rank128_kernel<2> : rank128_kernel<4>;
-        k<<<uint32_t(blocks), kR128Warps * 32, smem, st>>>(ix.centroids, ix.codes, ix.residuals, ix.doclens,
+        ::plaid::launch::pdl(k, uint32_t(blocks), kR128Warps * 32, smem, st, ix.centroids, ix.codes, ix.residuals, ix.doclens,
                                                            ix.offsets, W, d_q, rows, d_ids, d_keys, d_n,
                                                            d_out_keys);
         count_launch();
@@ -399,7 +405,7 @@ void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint
     uint64_t blocks = nmax;
     const uint64_t cap = uint64_t(sm_count()) * 16;
     if (blocks > cap) blocks = cap;
-    rank_exact_kernel<<<uint32_t(blocks), kThreads, smem, st>>>(
+    ::plaid::launch::pdl(rank_exact_kernel, uint32_t(blocks), kThreads, smem, st, 
         ix.centroids, ix.codes, ix.residuals, ix.doclens, ix.offsets, ix.dim, ix.nbits, W, d_q, rows,
         d_ids, d_keys, d_n, d_out_keys);
     count_launch();
@@ -409,7 +415,7 @@ void unpack_via_lut(const uint8_t* d_packed, uint64_t n, uint32_t nbits, uint8_t
                     cudaStream_t st) {
     if (!n) return;
     uint64_t b = (n + 255) / 256;
-    unpack_kernel<<<uint32_t(b > 4096 ? 4096 : b), 256, 0, st>>>(d_packed, n, nbits, d_out);
+    ::plaid::launch::pdl(unpack_kernel, uint32_t(b > 4096 ? 4096 : b), 256, 0, st, d_packed, n, nbits, d_out);
     count_launch();
 }
 
@@ -419,7 +425,7 @@ void reconstruct(const IndexView& ix, const uint32_t* d_codes, uint64_t n, const
     Weights W;
     for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
     uint64_t b = (n + 7) / 8;
-    reconstruct_kernel<<<uint32_t(b > 4096 ? 4096 : b), 256, 0, st>>>(ix.centroids, ix.dim, ix.nbits, W,
+    ::plaid::launch::pdl(reconstruct_kernel, uint32_t(b > 4096 ? 4096 : b), 256, 0, st, ix.centroids, ix.dim, ix.nbits, W,
                                                                       d_codes, n, d_residuals, d_out);
     count_launch();
 }
@@ -428,7 +434,7 @@ void maxsim_packed(const float* d_scores, uint32_t nq, const uint64_t* d_offsets
                    float* d_out, cudaStream_t st) {
     if (!np) return;
     uint64_t b = (np + 7) / 8;
-    maxsim_packed_kernel<<<uint32_t(b > 4096 ? 4096 : b), 256, 0, st>>>(d_scores, nq, d_offsets, np, d_out);
+    ::plaid::launch::pdl(maxsim_packed_kernel, uint32_t(b > 4096 ? 4096 : b), 256, 0, st, d_scores, nq, d_offsets, np, d_out);
     count_launch();
 }
 
@@ -436,7 +442,7 @@ void maxsim_embeddings(const float* d_q, uint32_t rows, uint32_t dim, const floa
                        const uint64_t* d_offsets, uint64_t np, float* d_out, cudaStream_t st) {
     if (!np) return;
     uint64_t b = (np + 7) / 8;
-    maxsim_embeddings_kernel<<<uint32_t(b > 4096 ? 4096 : b), 256, 0, st>>>(d_q, rows, dim, d_emb,
+    ::plaid::launch::pdl(maxsim_embeddings_kernel, uint32_t(b > 4096 ? 4096 : b), 256, 0, st, d_q, rows, dim, d_emb,
                                                                             d_offsets, np, d_out);
     count_launch();
 }

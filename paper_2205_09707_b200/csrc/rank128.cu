@@ -64,6 +64,7 @@ finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restric
                      const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ doclens,
                      const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pref,
                      uint64_t* __restrict__ fin_base) {
+    dev::pdl_wait();
     __shared__ uint32_t warp_sums[32];
     const uint32_t n = uint32_t(*d_n);
     const uint32_t per = (n + 1023) / 1024;
@@ -130,6 +131,7 @@ stream_decompress_kernel(const float* __restrict__ C, const uint32_t* __restrict
                          const uint8_t* __restrict__ residuals, Weights16 W, const uint64_t* __restrict__ d_n,
                          const uint32_t* __restrict__ pref, const uint64_t* __restrict__ fin_base,
                          float* __restrict__ vhat, uint32_t* __restrict__ tok_pass) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) float sm[];
     __shared__ float w_s[16];
     constexpr uint32_t kBpt = NB * 128 / 8;
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(kMsWarps * 32)
 stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict__ tok_pass,
                      const uint32_t* __restrict__ pref, const uint64_t* __restrict__ d_n,
                      const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) float sm[];
     // query pairs interleaved: qp[g][d] = (q_{2g}[d], q_{2g+1}[d]) so one
     // FMUL2 forms both products of a token dim with a query pair
@@ -307,6 +310,7 @@ stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict_
 __global__ void finalize_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
                                 const uint64_t* __restrict__ d_n, uint32_t rows, uint32_t* __restrict__ run,
                                 uint64_t* __restrict__ out_keys) {
+    dev::pdl_wait();
     const uint64_t n = *d_n;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x) {
         uint4* r4 = reinterpret_cast<uint4*>(run + p * 32);
@@ -357,22 +361,22 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
         cudaFuncSetAttribute(stream_maxsim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(msm));
         cfg = true;
     }
-    finalist_scan_kernel<<<1, 1024, 0, st>>>(d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref, s.fin_base);
+    ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref, s.fin_base);
     count_launch();
     const uint64_t max_tiles = (nmax * ix.max_doclen + 31) / 32;
     uint64_t db = (max_tiles + kDecWarps - 1) / kDecWarps;
     if (db > uint64_t(sm_count()) * 3) db = uint64_t(sm_count()) * 3;
     auto dk = ix.nbits == 1 ? stream_decompress_kernel<1>
                             : ix.nbits == 2 ? stream_decompress_kernel<2> : stream_decompress_kernel<4>;
-    dk<<<uint32_t(db), kDecWarps * 32, dsm, st>>>(ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref, s.fin_base,
+    ::plaid::launch::pdl(dk, uint32_t(db), kDecWarps * 32, dsm, st, ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref, s.fin_base,
                                                   s.vhat, s.tok_pass);
     count_launch();
     uint64_t mb = (nmax * ix.max_doclen + kMsTile - 1) / kMsTile;
     if (mb > uint64_t(sm_count()) * 4) mb = uint64_t(sm_count()) * 4;
-    stream_maxsim_kernel<<<uint32_t(mb), kMsWarps * 32, msm, st>>>(s.vhat, s.tok_pass, s.pref, d_n, d_q, rows, s.run);
+    ::plaid::launch::pdl(stream_maxsim_kernel, uint32_t(mb), kMsWarps * 32, msm, st, s.vhat, s.tok_pass, s.pref, d_n, d_q, rows, s.run);
     count_launch();
     const uint32_t fb = uint32_t((nmax + 255) / 256);
-    finalize_kernel<<<fb, 256, 0, st>>>(d_ids, d_keys, d_n, rows, s.run, d_out_keys);
+    ::plaid::launch::pdl(finalize_kernel, fb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
     count_launch();
     return true;
 }

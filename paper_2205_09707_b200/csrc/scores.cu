@@ -33,6 +33,7 @@ scores_exact_kernel(const float* __restrict__ C, uint64_t K, uint32_t dim,
                     const float* __restrict__ Q, uint32_t rows, float t_cs,
                     float* __restrict__ S, float* __restrict__ rowmax,
                     uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ partial) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) float smem[];
     const uint32_t qpitch = dim + 4;
     float* q_s = smem;                                   // 32 x (dim+4)
@@ -112,6 +113,7 @@ scores_exact_kernel(const float* __restrict__ C, uint64_t K, uint32_t dim,
 template <int NP>
 __global__ void topn_merge_kernel(const uint64_t* __restrict__ partial, uint32_t nwarps,
                                   uint32_t nprobe, uint32_t* __restrict__ sel) {
+    dev::pdl_wait();
     extern __shared__ uint64_t lists[];  // blockDim x NP
     const uint32_t i = blockIdx.x;
     uint64_t top[NP];
@@ -150,6 +152,7 @@ __global__ void topn_merge_kernel(const uint64_t* __restrict__ partial, uint32_t
 
 __global__ void token_keys_kernel(const float* __restrict__ S, uint64_t K, uint32_t i,
                                   uint64_t* __restrict__ keys) {
+    dev::pdl_wait();
     for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < K;
          c += uint64_t(gridDim.x) * blockDim.x)
         keys[c] = dev::make_key(S[c * kScoresPitch + i], uint32_t(c));
@@ -157,6 +160,7 @@ __global__ void token_keys_kernel(const float* __restrict__ S, uint64_t K, uint3
 
 __global__ void keys_to_ids_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ n,
                                    uint32_t* __restrict__ ids) {
+    dev::pdl_wait();
     const uint64_t cnt = *n;
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < cnt;
          j += uint64_t(gridDim.x) * blockDim.x)
@@ -165,6 +169,7 @@ __global__ void keys_to_ids_kernel(const uint64_t* __restrict__ keys, const uint
 
 __global__ void keep_bits_kernel(const float* __restrict__ rowmax, uint64_t K, float t_cs,
                                  uint32_t* __restrict__ bits) {
+    dev::pdl_wait();
     const uint64_t words = (K + 31) / 32;
     for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < words;
          w += uint64_t(gridDim.x) * blockDim.x) {
@@ -188,6 +193,7 @@ template <int NP>
 __global__ void __launch_bounds__(256)
 topn_from_scores_kernel(const float* __restrict__ S, uint64_t K, uint32_t rows, uint64_t* __restrict__ partial,
                         uint32_t* __restrict__ gthr) {
+    dev::pdl_wait();
     const uint32_t lane = dev::lane_id();
     const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -226,6 +232,7 @@ topn_from_scores_kernel(const float* __restrict__ S, uint64_t K, uint32_t rows, 
 }
 
 __global__ void iota_kernel(uint32_t* __restrict__ out, uint64_t n) {
+    dev::pdl_wait();
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x)
         out[i] = uint32_t(i);
@@ -252,7 +259,7 @@ void launch_scores(const IndexView& ix, const float* q, uint32_t rows, float t_c
                              227 * 1024);
         configured = true;
     }
-    scores_exact_kernel<NP><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+    ::plaid::launch::pdl(scores_exact_kernel<NP>, blocks, kWarpsPerBlock * 32, smem, st, 
         ix.centroids, ix.K, ix.dim, q, rows, t_cs, S, rowmax, keep, partial);
     launch::count_launch();
 }
@@ -267,7 +274,7 @@ void launch_merge(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint3
         cudaFuncSetAttribute(topn_merge_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         configured = true;
     }
-    topn_merge_kernel<NP><<<rows, threads, smem, st>>>(partial, nwarps, nprobe, sel);
+    ::plaid::launch::pdl(topn_merge_kernel<NP>, rows, threads, smem, st, partial, nwarps, nprobe, sel);
     launch::count_launch();
 }
 
@@ -311,7 +318,7 @@ void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucke
 void token_keys(const float* d_scores, uint64_t K, uint32_t i, uint64_t* d_keys, cudaStream_t st) {
     uint64_t blocks = (K + 255) / 256;
     if (blocks > 4096) blocks = 4096;
-    token_keys_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_scores, K, i, d_keys);
+    ::plaid::launch::pdl(token_keys_kernel, uint32_t(blocks), 256, 0, st, d_scores, K, i, d_keys);
     count_launch();
 }
 
@@ -320,7 +327,7 @@ void keys_to_ids(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uin
     uint64_t blocks = (nmax + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     if (blocks == 0) blocks = 1;
-    keys_to_ids_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_keys, d_n, d_ids);
+    ::plaid::launch::pdl(keys_to_ids_kernel, uint32_t(blocks), 256, 0, st, d_keys, d_n, d_ids);
     count_launch();
 }
 
@@ -329,7 +336,7 @@ void keep_bits_from_rowmax(const float* d_rowmax, uint64_t K, float t_cs, uint32
     uint64_t words = (K + 31) / 32;
     uint64_t blocks = (words + 255) / 256;
     if (blocks > 4096) blocks = 4096;
-    keep_bits_kernel<<<uint32_t(blocks), 256, 0, st>>>(d_rowmax, K, t_cs, d_keep_bits);
+    ::plaid::launch::pdl(keep_bits_kernel, uint32_t(blocks), 256, 0, st, d_rowmax, K, t_cs, d_keep_bits);
     count_launch();
 }
 
@@ -338,12 +345,12 @@ uint32_t topn_from_scores(const float* d_scores, uint64_t K, uint32_t rows, uint
     const uint32_t blocks = uint32_t(sm_count()) * kBlocksPerSm;
     const uint32_t threads = kWarpsPerBlock * 32;
     switch (np_bucket) {
-        case 1: topn_from_scores_kernel<1><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
-        case 2: topn_from_scores_kernel<2><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
-        case 4: topn_from_scores_kernel<4><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
-        case 8: topn_from_scores_kernel<8><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
-        case 16: topn_from_scores_kernel<16><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
-        default: topn_from_scores_kernel<32><<<blocks, threads, 0, st>>>(d_scores, K, rows, d_partial, d_gthr); break;
+        case 1: ::plaid::launch::pdl(topn_from_scores_kernel<1>, blocks, threads, 0, st, d_scores, K, rows, d_partial, d_gthr); break;
+        case 2: ::plaid::launch::pdl(topn_from_scores_kernel<2>, blocks, threads, 0, st, d_scores, K, rows, d_partial, d_gthr); break;
+        case 4: ::plaid::launch::pdl(topn_from_scores_kernel<4>, blocks, threads, 0, st, d_scores, K, rows, d_partial, d_gthr); break;
+        case 8: ::plaid::launch::pdl(topn_from_scores_kernel<8>, blocks, threads, 0, st, d_scores, K, rows, d_partial, d_gthr); break;
+        case 16: ::plaid::launch::pdl(topn_from_scores_kernel<16>, blocks, threads, 0, st, d_scores, K, rows, d_partial, d_gthr); break;
+        default: ::plaid::launch::pdl(topn_from_scores_kernel<32>, blocks, threads, 0, st, d_scores, K, rows, d_partial, d_gthr); break;
     }
     count_launch();
     return blocks * kWarpsPerBlock;
@@ -351,7 +358,7 @@ uint32_t topn_from_scores(const float* d_scores, uint64_t K, uint32_t rows, uint
 
 void iota(uint32_t* d_out, uint64_t n, cudaStream_t st) {
     uint64_t b = (n + 255) / 256;
-    iota_kernel<<<uint32_t(b > 4096 ? 4096 : (b ? b : 1)), 256, 0, st>>>(d_out, n);
+    ::plaid::launch::pdl(iota_kernel, uint32_t(b > 4096 ? 4096 : (b ? b : 1)), 256, 0, st, d_out, n);
     count_launch();
 }
 

@@ -52,6 +52,7 @@ __device__ __forceinline__ void grid_sync(unsigned int* count, unsigned int* gen
 __global__ void __launch_bounds__(kSelThreads)
 radix_select_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
                     SelectState* st, uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
+    dev::pdl_wait();
     __shared__ __align__(16) uint32_t h[kBins];
     __shared__ uint32_t part[kSelThreads];
     __shared__ unsigned long long s_prefix, s_mask, s_rem;
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(1024)
 sort_small_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint32_t npad,
                   uint64_t want, uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, uint64_t* __restrict__ out_n, uint32_t id_base) {
+    dev::pdl_wait();
     extern __shared__ uint64_t s[];
     const uint64_t n = *d_n;
     for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) s[i] = i < n ? keys[i] : 0ull;
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(kRankThreads)
 sort_rank_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
                  uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids, float* __restrict__ out_scores,
                  uint64_t* __restrict__ out_n, uint32_t id_base) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) uint64_t s[];
     const uint32_t n = uint32_t(*d_n);
     if (blockIdx.x == 0 && threadIdx.x == 0 && out_n) *out_n = n < want ? n : want;
@@ -271,6 +274,7 @@ sort_rank_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
 
 __global__ void pad_copy_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
                                 uint64_t npad, uint64_t* __restrict__ tmp) {
+    dev::pdl_wait();
     const uint64_t n = *d_n;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < npad;
          i += uint64_t(gridDim.x) * blockDim.x)
@@ -278,6 +282,7 @@ __global__ void pad_copy_kernel(const uint64_t* __restrict__ keys, const uint64_
 }
 
 __global__ void bitonic_step_kernel(uint64_t* __restrict__ s, uint64_t npad, uint64_t j, uint64_t k) {
+    dev::pdl_wait();
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < npad / 2;
          p += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
@@ -294,6 +299,7 @@ __global__ void bitonic_step_kernel(uint64_t* __restrict__ s, uint64_t npad, uin
 __global__ void emit_kernel(const uint64_t* __restrict__ sorted, const uint64_t* __restrict__ d_n,
                             uint64_t want, uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids,
                             float* __restrict__ out_scores, uint64_t* __restrict__ out_n, uint32_t id_base) {
+    dev::pdl_wait();
     const uint64_t n = *d_n;
     const uint64_t m = n < want ? n : want;
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < m;
@@ -304,6 +310,7 @@ __global__ void emit_kernel(const uint64_t* __restrict__ sorted, const uint64_t*
 
 __global__ void make_keys_kernel(const uint32_t* __restrict__ ids, const float* __restrict__ scores,
                                  uint64_t n, uint64_t* __restrict__ keys) {
+    dev::pdl_wait();
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x)
         keys[i] = dev::make_key(scores[i], ids[i]);
@@ -314,6 +321,7 @@ __global__ void make_keys_kernel(const uint32_t* __restrict__ ids, const float* 
 __global__ void merge_keys_kernel(const uint32_t* __restrict__ pids, const float* __restrict__ scores,
                                   const uint64_t* __restrict__ counts, uint64_t shards, uint64_t stride,
                                   uint64_t* __restrict__ keys, uint64_t* __restrict__ d_n) {
+    dev::pdl_wait();
     const uint64_t total = shards * stride;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -324,12 +332,14 @@ __global__ void merge_keys_kernel(const uint32_t* __restrict__ pids, const float
 }
 
 __global__ void copy_count_kernel(const uint64_t* src, uint64_t* dst, uint64_t cap) {
+    dev::pdl_wait();
     const uint64_t v = *src;
     *dst = v < cap ? v : cap;
 }
 
 __global__ void validate_query_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
                                       int* __restrict__ status) {
+    dev::pdl_wait();
     const uint32_t r = threadIdx.x;
     if (r >= rows) return;
     double acc = 0.0;
@@ -373,6 +383,7 @@ constexpr uint32_t kZeroBucket = 0x8000u;
 
 __global__ void hist16_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
                               SelectHist* __restrict__ st) {
+    dev::pdl_wait();
     __shared__ uint32_t zeros;
     if (threadIdx.x == 0) zeros = 0;
     __syncthreads();
@@ -397,6 +408,7 @@ __global__ void hist16_kernel(const uint64_t* __restrict__ keys, const uint64_t*
 // range holds the target walks it from the top, 32 buckets per step.
 __global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restrict__ d_n, uint64_t want,
                                                          SelectHist* __restrict__ st) {
+    dev::pdl_wait();
     __shared__ unsigned long long warp_tot[32];
     const uint64_t n = *d_n;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -443,6 +455,7 @@ __global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restr
 __global__ void hist_compact_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
                                     SelectHist* __restrict__ st, uint64_t* __restrict__ bkeys,
                                     uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
+    dev::pdl_wait();
     const uint64_t n = *d_n;
     const bool all = st->take_all;
     const uint32_t bucket = st->bucket;
@@ -477,6 +490,7 @@ __global__ void hist_compact_kernel(const uint64_t* __restrict__ keys, const uin
 __global__ void __launch_bounds__(128)
 hist_resolve_kernel(SelectHist* __restrict__ st, const uint64_t* __restrict__ bkeys, uint64_t* __restrict__ out,
                     uint64_t* __restrict__ out_n) {
+    dev::pdl_wait();
     extern __shared__ __align__(16) uint64_t s[];
     if (st->take_all) return;
     const uint32_t nb = uint32_t(st->bcount);
@@ -542,11 +556,11 @@ void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax,
     cudaMemsetAsync(d_out_n, 0, sizeof(uint64_t), st);
     if (nmax == 0) return;
     const uint32_t grid = grid_for(nmax, 256, uint32_t(sm_count()) * 8);
-    hist16_kernel<<<grid, 256, 0, st>>>(d_keys, d_n, d_st);
+    ::plaid::launch::pdl(hist16_kernel, grid, 256, 0, st, d_keys, d_n, d_st);
     count_launch();
-    hist_find_kernel<<<1, 1024, 0, st>>>(d_n, want, d_st);
+    ::plaid::launch::pdl(hist_find_kernel, 1, 1024, 0, st, d_n, want, d_st);
     count_launch();
-    hist_compact_kernel<<<grid, 256, 0, st>>>(d_keys, d_n, d_st, d_bkeys, d_out_keys, d_out_n);
+    ::plaid::launch::pdl(hist_compact_kernel, grid, 256, 0, st, d_keys, d_n, d_st, d_bkeys, d_out_keys, d_out_n);
     count_launch();
     static bool cfg = false;
     if (!cfg) {
@@ -555,7 +569,7 @@ void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax,
         cfg = true;
     }
     const uint64_t rb = std::min<uint64_t>((std::min<uint64_t>(nmax, kRankCap) + 31) / 32, kRankCap / 32);
-    hist_resolve_kernel<<<uint32_t(rb ? rb : 1), 128, kRankCap * sizeof(uint64_t), st>>>(d_st, d_bkeys, d_out_keys,
+    ::plaid::launch::pdl(hist_resolve_kernel, uint32_t(rb ? rb : 1), 128, kRankCap * sizeof(uint64_t), st, d_st, d_bkeys, d_out_keys,
                                                                                        d_out_n);
     count_launch();
 }
@@ -593,7 +607,7 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
             rank_cfg = true;
         }
         const uint32_t grid = uint32_t((nmax + kRankPerCta - 1) / kRankPerCta);
-        sort_rank_kernel<<<grid, kRankThreads, smem, st>>>(d_keys, d_n, want, d_out_keys, d_out_ids, d_out_scores,
+        ::plaid::launch::pdl(sort_rank_kernel, grid, kRankThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_ids, d_out_scores,
                                                           d_out_n, id_base);
         count_launch();
         return;
@@ -608,28 +622,28 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
             configured = true;
         }
         const uint32_t threads = npad / 2 < 1024 ? (npad / 2 < 32 ? 32 : npad / 2) : 1024;
-        sort_small_kernel<<<1, threads, smem, st>>>(d_keys, d_n, npad, want, d_out_keys, d_out_ids,
+        ::plaid::launch::pdl(sort_small_kernel, 1, threads, smem, st, d_keys, d_n, npad, want, d_out_keys, d_out_ids,
                                                     d_out_scores, d_out_n, id_base);
         count_launch();
         return;
     }
     const uint64_t npad = next_pow2(nmax);
     const uint32_t grid = grid_for(npad, 256, uint32_t(sm_count()) * 8);
-    pad_copy_kernel<<<grid, 256, 0, st>>>(d_keys, d_n, npad, d_tmp);
+    ::plaid::launch::pdl(pad_copy_kernel, grid, 256, 0, st, d_keys, d_n, npad, d_tmp);
     count_launch();
     for (uint64_t k = 2; k <= npad; k <<= 1)
         for (uint64_t j = k >> 1; j > 0; j >>= 1) {
-            bitonic_step_kernel<<<grid, 256, 0, st>>>(d_tmp, npad, j, k);
+            ::plaid::launch::pdl(bitonic_step_kernel, grid, 256, 0, st, d_tmp, npad, j, k);
             count_launch();
         }
-    emit_kernel<<<grid_for(want, 256, 4096), 256, 0, st>>>(d_tmp, d_n, want, d_out_keys, d_out_ids,
+    ::plaid::launch::pdl(emit_kernel, grid_for(want, 256, 4096), 256, 0, st, d_tmp, d_n, want, d_out_keys, d_out_ids,
                                                           d_out_scores, d_out_n, id_base);
     count_launch();
 }
 
 void make_keys(const uint32_t* d_ids, const float* d_scores, uint64_t n, uint64_t* d_keys,
                cudaStream_t st) {
-    make_keys_kernel<<<grid_for(n, 256, 4096), 256, 0, st>>>(d_ids, d_scores, n, d_keys);
+    ::plaid::launch::pdl(make_keys_kernel, grid_for(n, 256, 4096), 256, 0, st, d_ids, d_scores, n, d_keys);
     count_launch();
 }
 
@@ -637,7 +651,7 @@ void merge_topk(const uint32_t* d_pids, const float* d_scores, const uint64_t* d
                 uint64_t shards, uint64_t stride, uint64_t k, uint64_t* d_tmp_keys, uint64_t* d_tmp_n,
                 uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n, uint64_t* d_sort_tmp,
                 cudaStream_t st) {
-    merge_keys_kernel<<<grid_for(shards * stride, 256, 4096), 256, 0, st>>>(
+    ::plaid::launch::pdl(merge_keys_kernel, grid_for(shards * stride, 256, 4096), 256, 0, st, 
         d_pids, d_scores, d_counts, shards, stride, d_tmp_keys, d_tmp_n);
     count_launch();
     sort_top(d_tmp_keys, d_tmp_n, shards * stride, k, nullptr, d_out_pids, d_out_scores, d_out_n, 0,
@@ -645,12 +659,12 @@ void merge_topk(const uint32_t* d_pids, const float* d_scores, const uint64_t* d
 }
 
 void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st) {
-    copy_count_kernel<<<1, 1, 0, st>>>(src, dst, cap);
+    ::plaid::launch::pdl(copy_count_kernel, 1, 1, 0, st, src, dst, cap);
     count_launch();
 }
 
 void validate_query(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, cudaStream_t st) {
-    validate_query_kernel<<<1, 32, 0, st>>>(d_q, rows, dim, d_status);
+    ::plaid::launch::pdl(validate_query_kernel, 1, 32, 0, st, d_q, rows, dim, d_status);
     count_launch();
 }
 
