@@ -424,21 +424,15 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
     keys3_.ensure(nd);
     sel3_.ensure(n3);
     if (ix.dim == 128 && n3 <= launch::kStreamMaxPassages) {
-        const uint64_t toks = n3 * ix.max_doclen;
-        vhat_.ensure(toks * 128);
-        tok_pass_.ensure(toks);
         pref_.ensure(n3 + 1);
         if (run_.n < n3 * 32) {
             run_.ensure(n3 * 32);
             PLAID_CUDA(cudaMemset(run_.p, 0, run_.n * sizeof(uint32_t)));
         }
         fin_base_.ensure(n3);
-        rank_scratch_.vhat = vhat_.p;
-        rank_scratch_.tok_pass = tok_pass_.p;
         rank_scratch_.pref = pref_.p;
         rank_scratch_.run = run_.p;
         rank_scratch_.fin_base = fin_base_.p;
-        rank_scratch_.tok_cap = std::min<uint64_t>(vhat_.n / 128, tok_pass_.n);
         rank_scratch_.pass_cap =
             std::min<uint64_t>({pref_.n - 1, run_.n / 32, fin_base_.n, launch::kStreamMaxPassages});
     }

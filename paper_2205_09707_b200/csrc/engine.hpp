@@ -138,8 +138,8 @@ private:
     uint64_t last_launches_ = 0;
 
     // scratch
-    DevBuf<float> q_, scores_, rowmax_, out_scores_, vhat_;
-    DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, out_pids_, ids_tmp_, tok_pass_, pref_, run_, slot_of_,
+    DevBuf<float> q_, scores_, rowmax_, out_scores_;
+    DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, out_pids_, ids_tmp_, pref_, run_, slot_of_,
         kept_list_, acc2_;
     launch::RankScratch rank_scratch_;
     DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_, bkeys_,

@@ -169,12 +169,10 @@ uint64_t sort_tmp_capacity(uint64_t nmax);
 // With d = 128 and a finalist list that fits `scratch` (rank128.cu: the
 // packed token-stream path), otherwise one fused kernel per finalist.
 struct RankScratch {
-    float* vhat = nullptr;        // tok_cap x 128 decompressed rows
-    uint32_t* tok_pass = nullptr; // tok_cap: finalist of each stream token
     uint32_t* pref = nullptr;     // pass_cap + 1: stream offset of each finalist
     uint32_t* run = nullptr;      // pass_cap x 32 running maxima; all zero between searches
     uint64_t* fin_base = nullptr; // pass_cap: index token of stream position g is fin_base[p] + g
-    uint64_t tok_cap = 0, pass_cap = 0;
+    uint64_t pass_cap = 0;
 };
 constexpr uint64_t kStreamMaxPassages = 16384;
 void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,

@@ -1,32 +1,32 @@
 // rank128.cu — stage 4 for d = 128 (pipeline.cpp:165-225): residual
-// decompression (residual_codec.cpp:97-132) and exact MaxSim
+// decompression (residual_codec.cpp:97-132) fused with exact MaxSim
 // (maxsim.cpp:66-104) over the finalists' tokens as ONE packed stream.
 //
-// The finalists' tokens are laid end to end (passage p's tokens start at
-// pref[p], an exclusive scan of their doclens), and every kernel works on
-// full 32-token tiles of that stream, so no lane idles on a passage tail and
-// the grid is sized by tokens, not passages:
-//   K1 finalist_scan   one CTA: pref[] over the (<= 16384) finalists;
-//   K2 decompress      warp per tile: centroid rows fetched with cp.async
-//                      (lane = 16 bytes of every row), the token's packed
-//                      residual row in registers, then lane = token: v =
-//                      C + w[idx], the in-order fp64 norm and v *= inv —
-//                      bit-for-bit the reference arithmetic; rows written
-//                      to vhat[stream position] (coalesced 512-byte rows) and
-//                      tok_pass[g] = finalist of stream token g;
-//   K3 maxsim          CTA per tile (persistent, double-buffered cp.async
-//                      tile loads): lane = token, warp w = query tokens
-//                      8w..8w+7, eight independent in-order fp32 dot chains
-//                      per lane (q broadcast from shared memory); then a
-//                      segmented max across the lanes of each passage and one
-//                      atomicMax per (passage, query) segment into run[p][i]
-//                      (order-preserving uint image of the float);
-//   K4 finalize        thread per finalist: score = in-order fp32 sum of
-//                      run[p][i] over i, the 64-bit (score, pid) key, and
-//                      run[p][*] reset to 0 for the next search.
-// HBM/L2 traffic per finalist token: 4 B code + 16*b B residuals + 512 B
-// centroid row (shared rows hit L2) + a 512-byte vhat row written and read
-// back (L2-resident at these sizes).
+// The finalists' tokens are laid end to end (finalist p's tokens start at
+// pref[p], an exclusive scan of their doclens) and processed in full 64-token
+// tiles, so no lane idles on a passage tail and the grid is sized by tokens:
+//   K1 finalist_scan   one CTA: pref[] over the (<= 16384) finalists and the
+//                      index-token base of each;
+//   K2 stream_fused    persistent CTAs, warp-specialised around a 2-deep ring
+//                      of tiles in shared memory:
+//                      * 2 producer warps decompress the next tile: centroid
+//                        rows by cp.async (lane = 16 bytes of a row), the
+//                        token's packed residual row in registers, then lane =
+//                        token: v = C + w[idx], the in-order fp64 norm and
+//                        v *= inv — bit for bit the reference's arithmetic;
+//                      * 4 consumer warps score the ready tile: lane = token
+//                        (two per lane), warp w = query tokens 8w..8w+7,
+//                        in-order fp32 dot chains with FMUL2 products over
+//                        query pairs and separately rounded adds; then a
+//                        segmented max across the lanes of each finalist and
+//                        one atomicMax per (finalist, query) into run[p][i]
+//                        (order-preserving uint image of the float);
+//   K3 finalize        thread per finalist: score = in-order fp32 sum of
+//                      run[p][i], the 64-bit (score, pid) key, run reset to 0.
+// HBM traffic per finalist token: 4 B code + 16*b B residuals + the 512-byte
+// centroid row (rows shared by tokens hit L2); the decompressed rows never
+// leave shared memory.  The bound is the exact fp32 issue rate (FMA and
+// tensor cores would change the rounding), see DESIGN.md §3.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -37,10 +37,12 @@
 namespace plaid {
 namespace {
 
-constexpr uint32_t kPitch = 132;  // floats per shared-memory row (conflict-free LDS.128 both ways)
-constexpr uint32_t kDecWarps = 4;
-constexpr uint32_t kMsWarps = 4;  // x 8 query tokens = 32
-constexpr uint32_t kMsTile = 64;  // stream tokens per maxsim tile (two per lane)
+constexpr uint32_t kPitch = 132;   // floats per shared-memory row (conflict-free LDS.128 both ways)
+constexpr uint32_t kTile = 64;     // stream tokens per tile (two per consumer lane)
+constexpr uint32_t kConsumers = 4; // x 8 query tokens = 32
+constexpr uint32_t kProducers = 2; // x 32 tokens = one tile
+constexpr uint32_t kFusedThreads = (kConsumers + kProducers) * 32;
+constexpr uint32_t kSmemFloats = 16 * 128 * 2 + 2 * kTile * kPitch;  // query pairs + 2 tiles
 
 struct Weights16 {
     float w[16];
@@ -52,6 +54,22 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 __device__ __forceinline__ uint32_t finalist_pid(const uint32_t* ids, const uint64_t* keys, uint64_t p) {
@@ -100,13 +118,13 @@ finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restric
     if (threadIdx.x == 1023) pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)
 }
 
-// Warp-cooperative: the finalist of stream token g (this lane's) for a tile
-// starting at g0.  A 32-ary search finds p0 (pref[p0] <= g0 < pref[p0 + 1])
-// in ceil(log32 n) rounds of one load per lane; the tile's 32 tokens then lie
-// in finalists p0 .. p0 + 31 (each has >= 1 token), whose ends one load per
-// lane brings in.
-__device__ __forceinline__ uint32_t tile_finalists(const uint32_t* __restrict__ pref, uint32_t n, uint32_t g0,
-                                                   uint32_t g) {
+// Warp-cooperative: the finalist of stream token g (this lane's) for a
+// 32-token run starting at g0.  A 32-ary search finds p0 (pref[p0] <= g0 <
+// pref[p0 + 1]) in ceil(log32 n) rounds of one load per lane; the run's tokens
+// then lie in finalists p0 .. p0 + 31 (each has >= 1 token), whose ends one
+// load per lane brings in.
+__device__ __forceinline__ uint32_t run_finalists(const uint32_t* __restrict__ pref, uint32_t n, uint32_t g0,
+                                                  uint32_t g) {
     const uint32_t lane = dev::lane_id();
     uint32_t lo = 0, span = n;  // pref[lo] <= g0 < pref[lo + span]
     while (span > 1) {
@@ -124,106 +142,37 @@ __device__ __forceinline__ uint32_t tile_finalists(const uint32_t* __restrict__ 
     return p;
 }
 
-// ---- K2: decompress + normalise the token stream ------------------------------------
+// ---- K2: fused decompression + exact MaxSim ---------------------------------------------
 template <int NB>
-__global__ void __launch_bounds__(kDecWarps * 32)
-stream_decompress_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
-                         const uint8_t* __restrict__ residuals, Weights16 W, const uint64_t* __restrict__ d_n,
-                         const uint32_t* __restrict__ pref, const uint64_t* __restrict__ fin_base,
-                         float* __restrict__ vhat, uint32_t* __restrict__ tok_pass) {
+__global__ void __launch_bounds__(kFusedThreads)
+stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
+                    const uint8_t* __restrict__ residuals, Weights16 W, const uint64_t* __restrict__ d_n,
+                    const uint32_t* __restrict__ pref, const uint64_t* __restrict__ fin_base,
+                    const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
     dev::pdl_wait();
     extern __shared__ __align__(16) float sm[];
     __shared__ float w_s[16];
+    __shared__ uint32_t pass_s[2][kTile];
+    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
     constexpr uint32_t kBpt = NB * 128 / 8;
-    const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5;
-    float* tile = sm + warp * 32 * kPitch;
-    if (threadIdx.x < 16) w_s[threadIdx.x] = W.w[threadIdx.x];
-    __syncthreads();
-    const uint32_t n = uint32_t(*d_n);
-    const uint32_t T = pref[n];
-    const uint32_t ntiles = (T + 31) / 32;
-    for (uint32_t tl = blockIdx.x * kDecWarps + warp; tl < ntiles; tl += gridDim.x * kDecWarps) {
-        const uint32_t g = tl * 32 + lane;
-        const bool valid = g < T;
-        uint64_t tok = 0;
-        uint32_t code = 0;
-        const uint32_t p = tile_finalists(pref, n, tl * 32, g);
-        if (valid) {
-            tok_pass[g] = p;
-            tok = fin_base[p] + g;
-            code = __ldg(codes + tok);
-        }
-        const uint32_t nv = T - tl * 32 < 32 ? T - tl * 32 : 32;
-        for (uint32_t t = 0; t < nv; ++t) {
-            const uint32_t ct = __shfl_sync(0xffffffffu, code, t);
-            cp_async16(tile + t * kPitch + 4 * lane, C + uint64_t(ct) * 128 + 4 * lane);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        uint32_t rb[kBpt / 4];
-        if (valid) {
-            const uint4* src = reinterpret_cast<const uint4*>(residuals + tok * kBpt);
-#pragma unroll
-            for (uint32_t i = 0; i < kBpt / 16; ++i) {
-                const uint4 x = __ldg(src + i);
-                rb[4 * i] = x.x, rb[4 * i + 1] = x.y, rb[4 * i + 2] = x.z, rb[4 * i + 3] = x.w;
-            }
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        if (valid) {
-            float4* row = reinterpret_cast<float4*>(tile + lane * kPitch);
-            constexpr uint32_t mask = (1u << NB) - 1;
-            double acc = 0.0;
-#pragma unroll
-            for (int d4 = 0; d4 < 32; ++d4) {
-                // dims 4*d4 .. 4*d4+3 <- 4*NB bits from bit 4*d4*NB (LSB-first packing)
-                const uint32_t word = rb[(4 * d4 * NB) / 32] >> ((4 * d4 * NB) % 32);
-                float4 x = row[d4];
-                x.x = __fadd_rn(x.x, w_s[(word >> (0 * NB)) & mask]);
-                x.y = __fadd_rn(x.y, w_s[(word >> (1 * NB)) & mask]);
-                x.z = __fadd_rn(x.z, w_s[(word >> (2 * NB)) & mask]);
-                x.w = __fadd_rn(x.w, w_s[(word >> (3 * NB)) & mask]);
-                row[d4] = x;
-                acc = __dadd_rn(acc, __dmul_rn(double(x.x), double(x.x)));
-                acc = __dadd_rn(acc, __dmul_rn(double(x.y), double(x.y)));
-                acc = __dadd_rn(acc, __dmul_rn(double(x.z), double(x.z)));
-                acc = __dadd_rn(acc, __dmul_rn(double(x.w), double(x.w)));
-            }
-            if (acc > 0.0) {
-                const float inv = float(1.0 / sqrt(acc));
-#pragma unroll
-                for (int d4 = 0; d4 < 32; ++d4) {
-                    float4 x = row[d4];
-                    x.x = __fmul_rn(x.x, inv), x.y = __fmul_rn(x.y, inv);
-                    x.z = __fmul_rn(x.z, inv), x.w = __fmul_rn(x.w, inv);
-                    row[d4] = x;
-                }
-            }
-        }
-        __syncwarp();
-        float4* dst = reinterpret_cast<float4*>(vhat + uint64_t(tl) * 32 * 128);
-        for (uint32_t t = 0; t < nv; ++t) dst[t * 32 + lane] = reinterpret_cast<const float4*>(tile + t * kPitch)[lane];
-        __syncwarp();
-    }
-}
-
-// ---- K3: exact MaxSim over stream tiles ----------------------------------------------
-__global__ void __launch_bounds__(kMsWarps * 32)
-stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict__ tok_pass,
-                     const uint32_t* __restrict__ pref, const uint64_t* __restrict__ d_n,
-                     const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
-    dev::pdl_wait();
-    extern __shared__ __align__(16) float sm[];
-    // query pairs interleaved: qp[g][d] = (q_{2g}[d], q_{2g+1}[d]) so one
+    // query pairs interleaved: qp[g][d] = (q_{2g}[d], q_{2g+1}[d]), so one
     // FMUL2 forms both products of a token dim with a query pair
     float2* qp = reinterpret_cast<float2*>(sm);  // 16 x 128 float2
-    float* tile = sm + 32 * kPitch;              // kMsTile x kPitch
+    float* tiles = sm + 16 * 128 * 2;            // 2 x kTile x kPitch
     const uint32_t lane = dev::lane_id(), warp = threadIdx.x >> 5;
     const uint32_t n = uint32_t(*d_n);
     const uint32_t T = pref[n];
-    const uint32_t ntiles = (T + kMsTile - 1) / kMsTile;
+    const uint32_t ntiles = (T + kTile - 1) / kTile;
     if (blockIdx.x >= ntiles) return;
-    for (uint32_t i = threadIdx.x; i < 16 * 32; i += kMsWarps * 32) {
+    if (threadIdx.x < 16) w_s[threadIdx.x] = W.w[threadIdx.x];
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&full_bar[b], kProducers * 32);
+            mbar_init(&empty_bar[b], kConsumers * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t i = threadIdx.x; i < 16 * 32; i += kFusedThreads) {
         const uint32_t g = i >> 5, d4 = i & 31;
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 x = 2 * g < rows ? __ldg(reinterpret_cast<const float4*>(Q + 2 * g * 128) + d4) : z;
@@ -232,31 +181,97 @@ stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict_
         dst[0] = make_float4(x.x, y.x, x.y, y.y);
         dst[1] = make_float4(x.z, y.z, x.w, y.w);
     }
-    const uint32_t i0 = warp * 8;
-    for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-        const uint32_t g0 = tl * kMsTile;
-        const uint32_t nv = T - g0 < kMsTile ? T - g0 : kMsTile;
-        {
-            const float* src = vhat + uint64_t(g0) * 128;
-            for (uint32_t i = threadIdx.x; i < nv * 32; i += kMsWarps * 32) {
-                const uint32_t r = i >> 5, c = i & 31;
-                cp_async16(tile + r * kPitch + 4 * c, src + r * 128 + 4 * c);
+    __syncthreads();
+
+    if (warp >= kConsumers) {
+        // ---------------- producers: decompress tiles into the ring
+        const uint32_t pw = warp - kConsumers;  // tokens [32 pw, 32 pw + 32) of each tile
+        constexpr uint32_t mask = (1u << NB) - 1;
+        uint32_t k = 0;
+        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++k) {
+            const uint32_t b = k & 1;
+            mbar_wait(&empty_bar[b], ((k >> 1) & 1) ^ 1);
+            float* tile = tiles + b * kTile * kPitch + pw * 32 * kPitch;
+            const uint32_t g0 = tl * kTile + pw * 32;
+            const uint32_t g = g0 + lane;
+            const bool valid = g < T;
+            uint64_t tok = 0;
+            uint32_t code = 0, p = 0xFFFFFFFFu;
+            if (g0 < T) p = run_finalists(pref, n, g0, g);
+            if (valid) {
+                tok = fin_base[p] + g;
+                code = __ldg(codes + tok);
+            } else {
+                p = 0xFFFFFFFFu - pw;  // never equal to a real finalist or to the other half's pad
+            }
+            pass_s[b][pw * 32 + lane] = p;
+            const uint32_t nv = g0 < T ? (T - g0 < 32 ? T - g0 : 32) : 0;
+            for (uint32_t t = 0; t < nv; ++t) {
+                const uint32_t ct = __shfl_sync(0xffffffffu, code, t);
+                cp_async16(tile + t * kPitch + 4 * lane, C + uint64_t(ct) * 128 + 4 * lane);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
+            uint32_t rb[kBpt / 4];
+            if (valid) {
+                const uint4* src = reinterpret_cast<const uint4*>(residuals + tok * kBpt);
+#pragma unroll
+                for (uint32_t i = 0; i < kBpt / 16; ++i) {
+                    const uint4 x = __ldg(src + i);
+                    rb[4 * i] = x.x, rb[4 * i + 1] = x.y, rb[4 * i + 2] = x.z, rb[4 * i + 3] = x.w;
+                }
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            if (valid) {
+                float4* row = reinterpret_cast<float4*>(tile + lane * kPitch);
+                double acc = 0.0;
+#pragma unroll
+                for (int d4 = 0; d4 < 32; ++d4) {
+                    // dims 4*d4 .. 4*d4+3 <- 4*NB bits from bit 4*d4*NB (LSB-first packing)
+                    const uint32_t word = rb[(4 * d4 * NB) / 32] >> ((4 * d4 * NB) % 32);
+                    float4 x = row[d4];
+                    x.x = __fadd_rn(x.x, w_s[(word >> (0 * NB)) & mask]);
+                    x.y = __fadd_rn(x.y, w_s[(word >> (1 * NB)) & mask]);
+                    x.z = __fadd_rn(x.z, w_s[(word >> (2 * NB)) & mask]);
+                    x.w = __fadd_rn(x.w, w_s[(word >> (3 * NB)) & mask]);
+                    row[d4] = x;
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.x), double(x.x)));
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.y), double(x.y)));
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.z), double(x.z)));
+                    acc = __dadd_rn(acc, __dmul_rn(double(x.w), double(x.w)));
+                }
+                if (acc > 0.0) {
+                    const float inv = float(1.0 / sqrt(acc));
+#pragma unroll
+                    for (int d4 = 0; d4 < 32; ++d4) {
+                        float4 x = row[d4];
+                        x.x = __fmul_rn(x.x, inv), x.y = __fmul_rn(x.y, inv);
+                        x.z = __fmul_rn(x.z, inv), x.w = __fmul_rn(x.w, inv);
+                        row[d4] = x;
+                    }
+                }
+            }
+            mbar_arrive(&full_bar[b]);
         }
-        // lane scores tokens g0 + lane and g0 + 32 + lane
-        const bool valid0 = lane < nv, valid1 = 32 + lane < nv;
-        const uint32_t p0 = valid0 ? tok_pass[g0 + lane] : 0xFFFFFFFFu;
-        const uint32_t p1 = valid1 ? tok_pass[g0 + 32 + lane] : 0xFFFFFFFEu;
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
+        return;
+    }
+
+    // ---------------- consumers: exact MaxSim over ready tiles
+    const uint32_t i0 = warp * 8;
+    const float4* q4 = reinterpret_cast<const float4*>(qp + (i0 / 2) * 128);
+    uint32_t k = 0;
+    for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++k) {
+        const uint32_t b = k & 1;
+        mbar_wait(&full_bar[b], (k >> 1) & 1);
+        const float* tile = tiles + b * kTile * kPitch;
+        const uint32_t p0 = pass_s[b][lane], p1 = pass_s[b][32 + lane];
+        const bool valid0 = p0 < 0xFFFFFFF0u, valid1 = p1 < 0xFFFFFFF0u;
         if (i0 < rows) {
             float a[8], c[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) a[u] = 0.0f, c[u] = 0.0f;
             const float4* vr0 = reinterpret_cast<const float4*>(tile + lane * kPitch);
             const float4* vr1 = reinterpret_cast<const float4*>(tile + (32 + lane) * kPitch);
-            const float4* q4 = reinterpret_cast<const float4*>(qp + (i0 / 2) * 128);
 #pragma unroll 2
             for (uint32_t d4 = 0; d4 < 32; ++d4) {
                 const float4 v = vr0[d4], w = vr1[d4];
@@ -270,11 +285,11 @@ stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict_
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         // products rounded once each (FMUL2), then the in-order adds
-                        const float2 p0 = dev::mul2_rn(qq[e], vv[e]), p1 = dev::mul2_rn(qq[e], ww[e]);
-                        a[2 * gp] = __fadd_rn(a[2 * gp], p0.x);
-                        a[2 * gp + 1] = __fadd_rn(a[2 * gp + 1], p0.y);
-                        c[2 * gp] = __fadd_rn(c[2 * gp], p1.x);
-                        c[2 * gp + 1] = __fadd_rn(c[2 * gp + 1], p1.y);
+                        const float2 q0 = dev::mul2_rn(qq[e], vv[e]), q1 = dev::mul2_rn(qq[e], ww[e]);
+                        a[2 * gp] = __fadd_rn(a[2 * gp], q0.x);
+                        a[2 * gp + 1] = __fadd_rn(a[2 * gp + 1], q0.y);
+                        c[2 * gp] = __fadd_rn(c[2 * gp], q1.x);
+                        c[2 * gp + 1] = __fadd_rn(c[2 * gp + 1], q1.y);
                     }
                 }
             }
@@ -291,10 +306,10 @@ stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict_
                 for (int o = 1; o < 32; o <<= 1) {
                     const float y0 = __shfl_up_sync(0xffffffffu, m0, o);
                     const float y1 = __shfl_up_sync(0xffffffffu, m1, o);
-                    const uint32_t q0 = __shfl_up_sync(0xffffffffu, p0, o);
-                    const uint32_t q1 = __shfl_up_sync(0xffffffffu, p1, o);
-                    if (lane >= uint32_t(o) && q0 == p0) m0 = dev::max_gt(m0, y0);
-                    if (lane >= uint32_t(o) && q1 == p1) m1 = dev::max_gt(m1, y1);
+                    const uint32_t s0 = __shfl_up_sync(0xffffffffu, p0, o);
+                    const uint32_t s1 = __shfl_up_sync(0xffffffffu, p1, o);
+                    if (lane >= uint32_t(o) && s0 == p0) m0 = dev::max_gt(m0, y0);
+                    if (lane >= uint32_t(o) && s1 == p1) m1 = dev::max_gt(m1, y1);
                 }
                 if (i0 + u < rows) {
                     if (tail0) atomicMax(run + uint64_t(p0) * 32 + i0 + u, dev::ord_f32(m0));
@@ -302,11 +317,11 @@ stream_maxsim_kernel(const float* __restrict__ vhat, const uint32_t* __restrict_
                 }
             }
         }
-        __syncthreads();  // tile fully read before it is refilled
+        mbar_arrive(&empty_bar[b]);
     }
 }
 
-// ---- K4: per-finalist score ---------------------------------------------------------
+// ---- K3: per-finalist score ---------------------------------------------------------
 __global__ void finalize_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
                                 const uint64_t* __restrict__ d_n, uint32_t rows, uint32_t* __restrict__ run,
                                 uint64_t* __restrict__ out_keys) {
@@ -346,37 +361,28 @@ namespace launch {
 bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
                     const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
                     const RankScratch& s, cudaStream_t st) {
-    if (ix.dim != 128 || rows > 32 || nmax > s.pass_cap || nmax * ix.max_doclen > s.tok_cap ||
-        nmax * ix.max_doclen >= (1ull << 32))
-        return false;
+    if (ix.dim != 128 || rows > 32 || nmax > s.pass_cap || nmax * ix.max_doclen >= (1ull << 32)) return false;
     Weights16 W;
     for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
+    const size_t fsm = size_t(kSmemFloats) * sizeof(float);
     static bool cfg = false;
-    const size_t dsm = size_t(kDecWarps) * 32 * kPitch * sizeof(float);
-    const size_t msm = size_t(32 + kMsTile) * kPitch * sizeof(float);
     if (!cfg) {
-        cudaFuncSetAttribute(stream_decompress_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
-        cudaFuncSetAttribute(stream_decompress_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
-        cudaFuncSetAttribute(stream_decompress_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
-        cudaFuncSetAttribute(stream_maxsim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(msm));
+        cudaFuncSetAttribute(stream_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
+        cudaFuncSetAttribute(stream_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
+        cudaFuncSetAttribute(stream_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
         cfg = true;
     }
-    ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref, s.fin_base);
+    ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref,
+                         s.fin_base);
     count_launch();
-    const uint64_t max_tiles = (nmax * ix.max_doclen + 31) / 32;
-    uint64_t db = (max_tiles + kDecWarps - 1) / kDecWarps;
-    if (db > uint64_t(sm_count()) * 3) db = uint64_t(sm_count()) * 3;
-    auto dk = ix.nbits == 1 ? stream_decompress_kernel<1>
-                            : ix.nbits == 2 ? stream_decompress_kernel<2> : stream_decompress_kernel<4>;
-    ::plaid::launch::pdl(dk, uint32_t(db), kDecWarps * 32, dsm, st, ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref, s.fin_base,
-                                                  s.vhat, s.tok_pass);
+    uint64_t fb = (nmax * ix.max_doclen + kTile - 1) / kTile;
+    if (fb > uint64_t(sm_count()) * 2) fb = uint64_t(sm_count()) * 2;  // two CTAs (12 warps) per SM
+    auto fk = ix.nbits == 1 ? stream_fused_kernel<1> : ix.nbits == 2 ? stream_fused_kernel<2> : stream_fused_kernel<4>;
+    ::plaid::launch::pdl(fk, uint32_t(fb), kFusedThreads, fsm, st, ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref,
+                         s.fin_base, d_q, rows, s.run);
     count_launch();
-    uint64_t mb = (nmax * ix.max_doclen + kMsTile - 1) / kMsTile;
-    if (mb > uint64_t(sm_count()) * 4) mb = uint64_t(sm_count()) * 4;
-    ::plaid::launch::pdl(stream_maxsim_kernel, uint32_t(mb), kMsWarps * 32, msm, st, s.vhat, s.tok_pass, s.pref, d_n, d_q, rows, s.run);
-    count_launch();
-    const uint32_t fb = uint32_t((nmax + 255) / 256);
-    ::plaid::launch::pdl(finalize_kernel, fb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
+    const uint32_t nb = uint32_t((nmax + 255) / 256);
+    ::plaid::launch::pdl(finalize_kernel, nb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
     count_launch();
     return true;
 }
