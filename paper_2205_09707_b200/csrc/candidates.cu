@@ -62,7 +62,7 @@ __global__ void chunk_count_kernel(const uint32_t* __restrict__ bitmap, uint64_t
 
 __global__ void chunk_write_kernel(const uint32_t* __restrict__ bitmap, uint64_t N,
                                    const uint32_t* __restrict__ counts, uint32_t* __restrict__ out,
-                                   uint64_t* __restrict__ out_n) {
+                                   uint64_t* __restrict__ out_n, uint32_t* __restrict__ slot_of) {
     dev::pdl_wait();
     __shared__ uint64_t red[kThreads / 32];
     __shared__ uint32_t scan[kThreads / 32];
@@ -102,7 +102,9 @@ __global__ void chunk_write_kernel(const uint32_t* __restrict__ bitmap, uint64_t
         while (v) {
             const uint32_t b = __ffs(v) - 1;
             v &= v - 1;
-            out[pos++] = uint32_t((w0 + j) * 32 + b);
+            const uint32_t pid = uint32_t((w0 + j) * 32 + b);
+            if (slot_of) slot_of[pid] = uint32_t(pos);
+            out[pos++] = pid;
         }
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kThreads - 1) *out_n = pos;
@@ -126,10 +128,11 @@ uint32_t bitmap_chunks(uint64_t N) {
 }
 
 void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_counts,
-                    uint32_t* d_out_ids, uint64_t* d_out_n, cudaStream_t st) {
+                    uint32_t* d_out_ids, uint64_t* d_out_n, uint32_t* d_slot_of, cudaStream_t st) {
     const uint32_t chunks = bitmap_chunks(N);
     ::plaid::launch::pdl(chunk_count_kernel, chunks, kThreads, 0, st, d_bitmap, N, d_chunk_counts);
-    ::plaid::launch::pdl(chunk_write_kernel, chunks, kThreads, 0, st, d_bitmap, N, d_chunk_counts, d_out_ids, d_out_n);
+    ::plaid::launch::pdl(chunk_write_kernel, chunks, kThreads, 0, st, d_bitmap, N, d_chunk_counts, d_out_ids, d_out_n,
+                         d_slot_of);
     count_launch();
     count_launch();
 }

@@ -373,6 +373,7 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         slot_of_.ensure(ix.N);
         bkeys_.ensure(ix.N);
         sel_hist_.ensure(1);
+        PLAID_CUDA(cudaMemset(sel_hist_.p, 0, sizeof(SelectHist)));  // re-zeroed by every select after
         kept_list_.ensure(ix.K);
         acc2_.ensure(ix.N * 32);
         PLAID_CUDA(cudaMemset(acc2_.p, 0, acc2_.n * sizeof(uint32_t)));
@@ -494,7 +495,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         nsel = uint64_t(rows) * p.nprobe;
     }
     launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap, st);
-    launch::bitmap_compact(bitmap, N, chunk_counts_.p, c1_.p, c + kN1, st);
+    launch::bitmap_compact(bitmap, N, chunk_counts_.p, c1_.p, c + kN1, slot_of_.p, st);
     record(2, st, times);
 
     const uint64_t want_final = p.k;
@@ -516,7 +517,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
         launch::stage2_masked(ix, scores_.p, rows, c1_.p, c + kN1, N, keep_.p, bitmap, owners, kept_list_.p,
                               slot_of_.p, acc2_.p, reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p,
-                              reinterpret_cast<unsigned long long*>(c + kRows2), st);
+                              reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, st);
         record(3, st, times);
         launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st);
         record(4, st, times);
@@ -725,7 +726,7 @@ void Searcher::generate_candidates(const float* scores, uint64_t rows, uint64_t 
         nsel = rows * nprobe;
     }
     launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap_.p, stream_);
-    launch::bitmap_compact(bitmap_.p, ix.N, chunk_counts_.p, c1_.p, c + kN1, stream_);
+    launch::bitmap_compact(bitmap_.p, ix.N, chunk_counts_.p, c1_.p, c + kN1, nullptr, stream_);
     uint64_t n = 0;
     d2h(&n, c + kN1, 1, stream_);
     PLAID_CUDA(cudaStreamSynchronize(stream_));

@@ -281,15 +281,16 @@ __global__ void kept_owners_kernel(const uint32_t* __restrict__ keep_bits, uint6
 // when p is in postings(c) (IVF content invariant, index.cpp:64-83).  So the
 // stage is driven by the kept centroids' posting lists, never reading codes:
 //   keep_list        kept centroid ids + the total length of their lists;
-//   slot_scatter     slot_of[pid] = position of pid in C1;
-//   ivf_accumulate   a block per kept centroid: S[c] in registers (lane =
-//                    query token), for each posting in C1 one warp-wide
-//                    atomicMax of the 32 order-preserving score images into
-//                    acc[slot], the slot's used bit, and the posting's token
-//                    multiplicity (index-derived ivf_mult) into the
-//                    gathered-row counter;
+//   ivf_accumulate   blocks over the kept lists: S[c] in registers (lane =
+//                    query token), for each posting in C1 (slot_of[pid] =
+//                    position in C1, written by the candidate compaction) one
+//                    warp-wide atomicMax of the 32 order-preserving score
+//                    images into acc[slot], the slot's used bit, and the
+//                    posting's token multiplicity (index-derived ivf_mult)
+//                    into the gathered-row counter;
 //   stage2_finalize  thread per candidate: in-order fp32 sum of acc[slot]
-//                    (exactly 0 when unused), the key, acc reset to 0.
+//                    (exactly 0 when unused), the key, acc reset to 0, and
+//                    the key histogram the stage-2 select starts from.
 // Work is proportional to the kept (centroid, candidate) pairs.  When the kept
 // lists are long (t_cs near -1 keeps most centroids) a warp-per-candidate
 // pass over the codes (ci_all) takes over; the choice is made on the device.
@@ -332,14 +333,6 @@ __global__ void keep_list_kernel(const uint32_t* __restrict__ keep_bits, uint64_
 
 __device__ __forceinline__ bool use_lists(const unsigned long long* counts, uint64_t n1) {
     return counts[1] <= kListsPerCandidate * (n1 + 1024);
-}
-
-__global__ void slot_scatter_kernel(const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
-                                    uint32_t* __restrict__ slot_of) {
-    dev::pdl_wait();
-    const uint64_t n = *d_n1;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-        slot_of[c1[i]] = uint32_t(i);
 }
 
 __global__ void __launch_bounds__(256)
@@ -396,16 +389,35 @@ ivf_accumulate_kernel(const uint32_t* __restrict__ list, const unsigned long lon
     if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
 }
 
+// Key histogram for the stage-2 select (select_top_hist): bucket = top 16
+// key bits; warp-aggregated, the score-0 bucket of the all-masked candidates
+// counted per block.
+__device__ __forceinline__ void hist_key(SelectHist* hs, uint64_t key, bool valid, uint32_t* zeros) {
+    const uint32_t lane = dev::lane_id();
+    const uint32_t b = valid ? uint32_t(key >> kHistShift) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    if (valid && lane == uint32_t(__ffs(peers) - 1)) {
+        if (b == kHistZeroBucket) atomicAdd(zeros, uint32_t(__popc(peers)));
+        else atomicAdd(&hs->hist[b], uint32_t(__popc(peers)));
+    }
+}
+
 __global__ void stage2_finalize_kernel(const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
                                        const unsigned long long* __restrict__ counts, uint32_t rows,
                                        uint32_t* __restrict__ acc, const uint32_t* __restrict__ used_bits,
-                                       uint64_t* __restrict__ keys_out) {
+                                       uint64_t* __restrict__ keys_out, SelectHist* __restrict__ hs) {
     dev::pdl_wait();
+    __shared__ uint32_t zeros;
     const uint64_t n = *d_n1;
     if (!use_lists(counts, n)) return;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    if (threadIdx.x == 0) zeros = 0;
+    __syncthreads();
+    for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
+         i0 += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = i0 + dev::lane_id();
         float sc = 0.0f;
-        if ((used_bits[i >> 5] >> (i & 31)) & 1u) {
+        uint64_t key = 0;
+        if (i < n && ((used_bits[i >> 5] >> (i & 31)) & 1u)) {
             uint4* a4 = reinterpret_cast<uint4*>(acc + i * 32);
             uint32_t v[32];
 #pragma unroll
@@ -418,8 +430,14 @@ __global__ void stage2_finalize_kernel(const uint32_t* __restrict__ c1, const ui
             for (int q = 0; q < 32; ++q)
                 if (uint32_t(q) < rows) sc = __fadd_rn(sc, dev::unord_f32(v[q]));
         }
-        keys_out[i] = dev::make_key(sc, c1[i]);
+        if (i < n) {
+            key = dev::make_key(sc, c1[i]);
+            keys_out[i] = key;
+        }
+        hist_key(hs, key, i < n, &zeros);
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && zeros) atomicAdd(&hs->hist[kHistZeroBucket], zeros);
 }
 
 // fallback when the kept lists are long: warp per candidate over its codes
@@ -428,7 +446,7 @@ ci_all_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ o
               const uint32_t* __restrict__ doclens, const float* __restrict__ S, uint32_t rows,
               const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
               const unsigned long long* __restrict__ counts, const uint32_t* __restrict__ keep_bits,
-              uint64_t* __restrict__ keys_out, unsigned long long* __restrict__ d_rows) {
+              uint64_t* __restrict__ keys_out, unsigned long long* __restrict__ d_rows, SelectHist* __restrict__ hs) {
     dev::pdl_wait();
     const uint64_t n = *d_n1;
     if (use_lists(counts, n)) return;
@@ -439,7 +457,11 @@ ci_all_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ o
         const uint32_t pid = c1[i];
         uint32_t used;
         const float total = score_passage_warp<true>(codes, offsets[pid], doclens[pid], S, rows, keep_bits, &used);
-        if (lane == 0) keys_out[i] = dev::make_key(total, pid);
+        if (lane == 0) {
+            const uint64_t key = dev::make_key(total, pid);
+            keys_out[i] = key;
+            atomicAdd(&hs->hist[uint32_t(key >> kHistShift)], 1u);
+        }
         rows_local += used;
     }
     if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
@@ -470,28 +492,28 @@ void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_o
 
 void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, const uint32_t* d_c1,
                    const uint64_t* d_n1, uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_cand_bits,
-                   uint32_t* d_used_bits, uint32_t* d_kept_list, uint32_t* d_slot_of, uint32_t* d_acc,
-                   unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows, cudaStream_t st) {
+                   uint32_t* d_used_bits, uint32_t* d_kept_list, const uint32_t* d_slot_of, uint32_t* d_acc,
+                   unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows,
+                   SelectHist* d_hist, cudaStream_t st) {
     const uint32_t sms = uint32_t(sm_count());
     const uint64_t words = (ix.K + 31) / 32;
     uint64_t kb = (words + 255) / 256;
     if (kb == 0) kb = 1;
-    ::plaid::launch::pdl(keep_list_kernel, uint32_t(kb), 256, 0, st, d_keep_bits, ix.K, ix.ivf_offsets, d_kept_list, d_counts2);
+    ::plaid::launch::pdl(keep_list_kernel, uint32_t(kb), 256, 0, st, d_keep_bits, ix.K, ix.ivf_offsets, d_kept_list,
+                         d_counts2);
     count_launch();
     if (nmax == 0) return;
     uint64_t sb = (nmax + 255) / 256;
     if (sb > uint64_t(sms) * 8) sb = uint64_t(sms) * 8;
-    ::plaid::launch::pdl(slot_scatter_kernel, uint32_t(sb), 256, 0, st, d_c1, d_n1, d_slot_of);
+    ::plaid::launch::pdl(ivf_accumulate_kernel, sms * 8, 256, 0, st, d_kept_list, d_counts2, d_n1, ix.ivf_offsets,
+                         ix.ivf_postings, ix.ivf_mult, d_cand_bits, d_slot_of, d_scores, rows, ix.codes, ix.offsets,
+                         ix.doclens, d_acc, d_used_bits, d_rows);
     count_launch();
-    ::plaid::launch::pdl(ivf_accumulate_kernel, sms * 8, 256, 0, st, d_kept_list, d_counts2, d_n1, ix.ivf_offsets, ix.ivf_postings,
-                                                   ix.ivf_mult, d_cand_bits, d_slot_of, d_scores, rows, ix.codes,
-                                                   ix.offsets, ix.doclens, d_acc, d_used_bits, d_rows);
+    ::plaid::launch::pdl(stage2_finalize_kernel, uint32_t(sb), 256, 0, st, d_c1, d_n1, d_counts2, rows, d_acc,
+                         d_used_bits, d_out_keys, d_hist);
     count_launch();
-    ::plaid::launch::pdl(stage2_finalize_kernel, uint32_t(sb), 256, 0, st, d_c1, d_n1, d_counts2, rows, d_acc, d_used_bits,
-                                                         d_out_keys);
-    count_launch();
-    ::plaid::launch::pdl(ci_all_kernel, sms * 8, 256, 0, st, ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_c1, d_n1, d_counts2,
-                                           d_keep_bits, d_out_keys, d_rows);
+    ::plaid::launch::pdl(ci_all_kernel, sms * 2, 256, 0, st, ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_c1, d_n1,
+                         d_counts2, d_keep_bits, d_out_keys, d_rows, d_hist);
     count_launch();
 }
 

@@ -41,7 +41,10 @@ struct SelectState {
 constexpr size_t kSelectStateZeroBytes = offsetof(SelectState, bnd);
 
 // Histogram select scratch (select_top_hist): a 65536-bin histogram of the
-// keys' top 16 bits and the control words; zeroed by the launcher.
+// keys' top 16 bits (built by the kernel that produces the keys; all zero
+// between selects — the compaction re-zeroes it) and the control words.
+constexpr uint32_t kHistShift = 48;          // bucket = key >> 48: sign, exponent, 7 mantissa bits of the score
+constexpr uint32_t kHistZeroBucket = 0x8000u; // bucket of score 0 (the all-masked stage-2 candidates)
 struct SelectHist {
     unsigned int hist[65536];
     unsigned long long above;   // keys in buckets above the boundary bucket
@@ -117,8 +120,9 @@ void postings_to_bitmap(const IndexView& ix, const uint32_t* d_sel, uint32_t nse
                         uint32_t* d_bitmap, cudaStream_t st);
 // Bitmap (N bits) -> ascending ids + count.  chunk_counts has bitmap_chunks(N) entries.
 uint32_t bitmap_chunks(uint64_t N);
+// d_slot_of (optional, N): slot_of[pid] = position of pid in the output.
 void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_counts,
-                    uint32_t* d_out_ids, uint64_t* d_out_n, cudaStream_t st);
+                    uint32_t* d_out_ids, uint64_t* d_out_n, uint32_t* d_slot_of, cudaStream_t st);
 
 // ---- centroid interaction (stages 2 and 3) -----------------------------------------
 // Candidates are either ids (d_ids) or keys (d_keys, id in the low word).
@@ -139,8 +143,9 @@ void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_o
 // (nmax x 32, all zero between calls).
 void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, const uint32_t* d_c1,
                    const uint64_t* d_n1, uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_cand_bits,
-                   uint32_t* d_used_bits, uint32_t* d_kept_list, uint32_t* d_slot_of, uint32_t* d_acc,
-                   unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows, cudaStream_t st);
+                   uint32_t* d_used_bits, uint32_t* d_kept_list, const uint32_t* d_slot_of, uint32_t* d_acc,
+                   unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows,
+                   SelectHist* d_hist, cudaStream_t st);
 
 // ---- selection -----------------------------------------------------------------------
 // Top `want` of keys[0..*d_n) (largest first).  Result: d_out_keys unsorted
@@ -148,10 +153,12 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
 void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
                       SelectState* d_state, uint64_t* d_out_keys, uint64_t* d_out_n,
                       cudaStream_t st);
-// Same result as select_top_large without grid barriers: histogram of the top
-// 16 key bits, one-CTA bucket search, compaction (keys above the boundary
-// bucket -> out, bucket keys -> d_bkeys, capacity nmax), exact resolution of
-// the bucket by rank (<= 8192 keys) or a one-CTA radix pass (larger).
+// Same result as select_top_large without grid barriers, from the key
+// histogram d_st->hist built by the keys' producer (stage2_finalize /
+// ci_all): one-CTA bucket search, compaction (keys above the boundary bucket
+// -> out, bucket keys -> d_bkeys, capacity nmax; histogram re-zeroed), exact
+// resolution of the bucket by rank (<= 8192 keys) or a one-CTA radix pass
+// (larger).  *d_out_n must be zero on entry.
 void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, SelectHist* d_st,
                      uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st);
 // Sort keys[0..*d_n) descending (n <= nmax) and emit the first min(want, n):

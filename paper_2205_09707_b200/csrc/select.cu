@@ -374,48 +374,29 @@ uint64_t next_pow2(uint64_t v) {
 }
 
 // ---- histogram select (no grid barriers) ----------------------------------------------
-constexpr uint32_t kHistBucketShift = 48;  // top 16 key bits = sign, exponent, 7 mantissa bits of the score
-constexpr uint32_t kRankCap = 8192;       // boundary buckets up to this size are ranked in parallel
-
-// The bucket of score 0 (all-masked stage-2 candidates): counted per block in
-// shared memory so that bucket costs one global atomic per block.
-constexpr uint32_t kZeroBucket = 0x8000u;
-
-__global__ void hist16_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
-                              SelectHist* __restrict__ st) {
-    dev::pdl_wait();
-    __shared__ uint32_t zeros;
-    if (threadIdx.x == 0) zeros = 0;
-    __syncthreads();
-    const uint64_t n = *d_n;
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
-         i0 += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t i = i0 + lane;
-        const uint32_t b = i < n ? uint32_t(__ldcg(keys + i) >> kHistBucketShift) : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, b);
-        if (i < n && lane == uint32_t(__ffs(peers) - 1)) {
-            if (b == kZeroBucket) atomicAdd(&zeros, uint32_t(__popc(peers)));
-            else atomicAdd(&st->hist[b], uint32_t(__popc(peers)));
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && zeros) atomicAdd(&st->hist[kZeroBucket], zeros);
-}
+constexpr uint32_t kHistBucketShift = kHistShift;
+constexpr uint32_t kRankCap = 8192;  // boundary buckets up to this size are ranked in parallel
 
 // One CTA: the bucket (from the top) holding the want-th largest key.  Warp
 // w sums buckets [2048 w, 2048 w + 2048) with coalesced loads; the warp whose
-// range holds the target walks it from the top, 32 buckets per step.
+// range holds the target walks it from the top, 32 buckets per step.  Also
+// (re)initialises the control words for this select.
 __global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restrict__ d_n, uint64_t want,
                                                          SelectHist* __restrict__ st) {
     dev::pdl_wait();
     __shared__ unsigned long long warp_tot[32];
     const uint64_t n = *d_n;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    if (n <= want) {
-        if (t == 0) st->take_all = 1;
-        return;
+    if (t == 0) {
+        st->take_all = n <= want;
+        st->bn = 0;
+        st->bcount = 0;
+        st->rem = 0;
+        st->above = 0;
+        st->bucket = 0;
     }
+    if (n <= want) return;
+    __syncthreads();
     const uint32_t* hw = st->hist + warp * 2048;
     unsigned long long mine = 0;
 #pragma unroll 8
@@ -460,6 +441,8 @@ __global__ void hist_compact_kernel(const uint64_t* __restrict__ keys, const uin
     const bool all = st->take_all;
     const uint32_t bucket = st->bucket;
     const uint32_t lane = threadIdx.x & 31;
+    // hist_find has consumed the histogram: leave it zero for the next select
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < 65536; b += gridDim.x * blockDim.x) st->hist[b] = 0;
     for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
          i0 += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = i0 + lane;
@@ -552,12 +535,8 @@ namespace launch {
 
 void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, SelectHist* d_st,
                      uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st) {
-    cudaMemsetAsync(d_st, 0, sizeof(SelectHist), st);
-    cudaMemsetAsync(d_out_n, 0, sizeof(uint64_t), st);
     if (nmax == 0) return;
     const uint32_t grid = grid_for(nmax, 256, uint32_t(sm_count()) * 8);
-    ::plaid::launch::pdl(hist16_kernel, grid, 256, 0, st, d_keys, d_n, d_st);
-    count_launch();
     ::plaid::launch::pdl(hist_find_kernel, 1, 1024, 0, st, d_n, want, d_st);
     count_launch();
     ::plaid::launch::pdl(hist_compact_kernel, grid, 256, 0, st, d_keys, d_n, d_st, d_bkeys, d_out_keys, d_out_n);
