@@ -190,6 +190,33 @@ plaid_status plaid_merge_topk_device(plaid_searcher* s, const uint32_t* d_pids,
                                      uint64_t shards, uint64_t stride, uint64_t k, uint32_t* d_out_pids,
                                      float* d_out_scores, uint64_t* d_out_n, uint64_t stream);
 
+/* ---- global-exact passage-sharded search ----------------------------
+ * The reference searches one index (pipeline.cpp:232-283); a passage-range
+ * shard alone cannot know the global stage-2 (top-ndocs) and stage-3
+ * (top-stage3_width) cuts.  Each shard runs three enqueue-only phases on its
+ * searcher; between them the caller all-gathers every shard's exported key row
+ * (u64, zero-padded to a stride common to all shards, e.g. NCCL all-gather):
+ *   phase1: stages 1-2 -> d_x2[stride2] = this shard's top-ndocs keys
+ *           (stride2 >= min(ndocs, shard N); the global min(ndocs, N) works)
+ *   phase2: d_g2[shards * stride2] -> keep only the global top-ndocs members,
+ *           stage 3 -> d_x3[stride3] (stride3 >= min(stage3_width, shard N))
+ *   phase3: d_g3[shards * stride3] -> keep the global stage-3 members, stage 4,
+ *           this shard's top-k (global pids) into d_pids/d_scores/d_n.
+ * Merging the shards' top-k (plaid_merge_topk_device) then equals lir::search
+ * over the unsharded index, and the per-shard trace counters
+ * (plaid_searcher_trace_counters_device) sum to its StageTrace counters.
+ * With disable_filter the exports are skipped (nothing is cut before stage 4). */
+plaid_status plaid_shard_phase1_device(plaid_searcher* s, const float* d_q, uint64_t rows, uint64_t dim,
+                                       const plaid_params* params, uint64_t* d_x2, uint64_t stride2,
+                                       uint64_t stream);
+plaid_status plaid_shard_phase2_device(plaid_searcher* s, const uint64_t* d_g2, uint64_t shards,
+                                       uint64_t* d_x3, uint64_t stride3, uint64_t stream);
+plaid_status plaid_shard_phase3_device(plaid_searcher* s, const uint64_t* d_g3, uint64_t shards,
+                                       uint32_t* d_pids, float* d_scores, uint64_t* d_n, uint64_t stream);
+/* d_out[6] <- [stage1_candidates, stage2_out, stage3_out, final_out (host path
+ * only), stage2_rows_gathered, stage3_rows_gathered] of the last query. */
+plaid_status plaid_searcher_trace_counters_device(plaid_searcher* s, uint64_t* d_out, uint64_t stream);
+
 /* ---- per-stage entry points (host buffers in/out, computed on the GPU) ------------ */
 /* pipeline.cpp:26-50: scores K x rows (centroid-major), row_max K */
 plaid_status plaid_compute_centroid_scores(plaid_searcher* s, const float* q, uint64_t rows,

@@ -69,6 +69,13 @@ SIGNATURES = {
                                      u32p, f32p, u64p, C.POINTER(Trace)]),
     "plaid_search_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                       C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "plaid_shard_phase1_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(Params),
+                                            C.c_void_p, C.c_uint64, C.c_uint64]),
+    "plaid_shard_phase2_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                            C.c_uint64]),
+    "plaid_shard_phase3_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_uint64]),
+    "plaid_searcher_trace_counters_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "plaid_searcher_sync": (C.c_int, [C.c_void_p]),
     "plaid_searcher_last_launches": (C.c_uint64, [C.c_void_p]),
     "plaid_searcher_phase_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),

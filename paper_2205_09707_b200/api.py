@@ -283,6 +283,21 @@ class Searcher:
         _check(N.load().plaid_merge_topk_device(self._h, d_pids, d_scores, d_counts, shards, stride, k,
                                                 d_out_pids, d_out_scores, d_out_n, stream))
 
+    # ---- global-exact passage sharding (include/plaid.h)
+    def shard_phase1(self, d_q: int, rows: int, dim: int, params: SearchParams, d_x2: int, stride2: int,
+                     stream: int = 0, options: SearchOptions = SearchOptions()) -> None:
+        p = params._c(options.disable_filter)
+        _check(N.load().plaid_shard_phase1_device(self._h, d_q, rows, dim, C.byref(p), d_x2, stride2, stream))
+
+    def shard_phase2(self, d_g2: int, shards: int, d_x3: int, stride3: int, stream: int = 0) -> None:
+        _check(N.load().plaid_shard_phase2_device(self._h, d_g2, shards, d_x3, stride3, stream))
+
+    def shard_phase3(self, d_g3: int, shards: int, d_pids: int, d_scores: int, d_n: int, stream: int = 0) -> None:
+        _check(N.load().plaid_shard_phase3_device(self._h, d_g3, shards, d_pids, d_scores, d_n, stream))
+
+    def trace_counters_device(self, d_out: int, stream: int = 0) -> None:
+        _check(N.load().plaid_searcher_trace_counters_device(self._h, d_out, stream))
+
     def sync(self) -> None:
         _check(N.load().plaid_searcher_sync(self._h))
 

@@ -261,6 +261,39 @@ plaid_status plaid_search_device(plaid_searcher* s, const float* d_q, uint64_t n
     });
 }
 
+plaid_status plaid_shard_phase1_device(plaid_searcher* s, const float* d_q, uint64_t rows, uint64_t dim,
+                                       const plaid_params* params, uint64_t* d_x2, uint64_t stride2,
+                                       uint64_t stream) {
+    return guarded([&] {
+        need(s, "searcher");
+        need(params, "params");
+        s->impl->shard_phase1(d_q, rows, dim, *params, d_x2, stride2, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+plaid_status plaid_shard_phase2_device(plaid_searcher* s, const uint64_t* d_g2, uint64_t shards,
+                                       uint64_t* d_x3, uint64_t stride3, uint64_t stream) {
+    return guarded([&] {
+        need(s, "searcher");
+        s->impl->shard_phase2(d_g2, shards, d_x3, stride3, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+plaid_status plaid_shard_phase3_device(plaid_searcher* s, const uint64_t* d_g3, uint64_t shards,
+                                       uint32_t* d_pids, float* d_scores, uint64_t* d_n, uint64_t stream) {
+    return guarded([&] {
+        need(s, "searcher");
+        s->impl->shard_phase3(d_g3, shards, d_pids, d_scores, d_n, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+plaid_status plaid_searcher_trace_counters_device(plaid_searcher* s, uint64_t* d_out, uint64_t stream) {
+    return guarded([&] {
+        need(s, "searcher");
+        s->impl->trace_counters_device(d_out, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
 plaid_status plaid_searcher_sync(plaid_searcher* s) {
     return guarded([&] {
         need(s, "searcher");

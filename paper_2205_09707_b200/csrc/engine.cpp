@@ -463,6 +463,16 @@ void Searcher::record(int slot, cudaStream_t st, bool times) {
 // The four stages of lir::search (pipeline.cpp:232-283) as one launch sequence.
 void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
                        float* d_scores, uint64_t* d_n, cudaStream_t st, bool times) {
+    pending_rows_ = rows;
+    enqueue_front(d_q, rows, p, st, times);
+    enqueue_stage3(p, st, times);
+    enqueue_back(d_q, rows, p, d_pids, d_scores, d_n, st, times);
+}
+
+// Stage 1 (S_cq, candidates) and stage 2 (pruned interaction + top-ndocs
+// select): survivors in sel2_ (keys, count counters[kN2]).
+void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st,
+                             bool times) {
     const IndexView& ix = index_->view();
     const uint64_t K = ix.K, N = ix.N;
     uint64_t* c = counters_.p;
@@ -497,7 +507,43 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
     launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap, st);
     launch::bitmap_compact(bitmap, N, chunk_counts_.p, c1_.p, c + kN1, slot_of_.p, st);
     record(2, st, times);
+    if (p.disable_filter) {
+        record(3, st, times);
+        record(4, st, times);
+        return;
+    }
+    // Stage 2: pruned centroid interaction over C1, keep ndocs.  Only the
+    // candidates owning a kept token are read (see kept_owners).
+    launch::stage2_masked(ix, scores_.p, rows, c1_.p, c + kN1, N, keep_.p, bitmap, owners, kept_list_.p,
+                          slot_of_.p, acc2_.p, reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p,
+                          reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, st);
+    record(3, st, times);
+    launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st);
+    record(4, st, times);
+}
 
+// Stage 3: full centroid interaction over sel2_, keep max(ceil(ndocs/4), k)
+// into sel3_ (sorted, count counters[kN3]).
+void Searcher::enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times) {
+    if (p.disable_filter) {
+        record(5, st, times);
+        return;
+    }
+    const IndexView& ix = index_->view();
+    uint64_t* c = counters_.p;
+    const uint64_t nd = std::min<uint64_t>(p.ndocs, ix.N);
+    launch::centroid_interaction(ix, scores_.p, pending_rows_, nullptr, sel2_.p, c + kN2, nd, nullptr, nullptr,
+                                 keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
+    launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
+                     sort_tmp_.p, st);
+    record(5, st, times);
+}
+
+// Stage 4: decompress + exact MaxSim of the finalists, top-k (global ids).
+void Searcher::enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
+                            float* d_scores, uint64_t* d_n, cudaStream_t st, bool times) {
+    const IndexView& ix = index_->view();
+    uint64_t* c = counters_.p;
     const uint64_t want_final = p.k;
     const uint64_t* fin_keys = nullptr;
     const uint32_t* fin_ids = nullptr;
@@ -507,32 +553,12 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
         // pipeline.cpp:255-258: every stage-1 candidate goes to stage 4
         fin_ids = c1_.p;
         fin_n = c + kN1;
-        fin_max = N;
-        record(3, st, times);
-        record(4, st, times);
-        record(5, st, times);
+        fin_max = ix.N;
     } else {
-        // Stage 2: pruned centroid interaction over C1, keep ndocs.  Only the
-        // candidates owning a kept token are read (see kept_owners).
-        const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
-        launch::stage2_masked(ix, scores_.p, rows, c1_.p, c + kN1, N, keep_.p, bitmap, owners, kept_list_.p,
-                              slot_of_.p, acc2_.p, reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p,
-                              reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, st);
-        record(3, st, times);
-        launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st);
-        record(4, st, times);
-        // Stage 3: full centroid interaction, keep max(ceil(ndocs/4), k).
-        const uint64_t n3 = std::min<uint64_t>(stage3_width(p), N);
-        launch::centroid_interaction(ix, scores_.p, rows, nullptr, sel2_.p, c + kN2, nd, nullptr, nullptr,
-                                     keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
-        launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
-                         sort_tmp_.p, st);
-        record(5, st, times);
         fin_keys = sel3_.p;
         fin_n = c + kN3;
-        fin_max = n3;
+        fin_max = std::min<uint64_t>(stage3_width(p), ix.N);
     }
-    // Stage 4: decompress + exact MaxSim, top-k.
     launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, &rank_scratch_, st);
     record(6, st, times);
     const uint32_t base = uint32_t(index_->pid_base());
@@ -547,6 +573,85 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
                          sort_tmp_.p, st);
     }
     record(7, st, times);
+}
+
+// ---- global-exact passage sharding -------------------------------------
+// Three device phases; between them the caller all-gathers the exported key
+// rows of every shard (zero-padded to a common stride).  The survivors of
+// each threshold filter are exactly this shard's members of the reference's
+// single-index stage-2 / stage-3 selections, so the merged top-k — and the
+// summed trace counters — equal lir::search over the unsharded index.
+void Searcher::shard_phase1(const float* d_q, uint64_t rows, uint64_t dim, const plaid_params& p, uint64_t* d_x2,
+                            uint64_t stride2, cudaStream_t st) {
+    require_index();
+    const IndexView& ix = index_->view();
+    if (dim != ix.dim) fail(PLAID_DIMENSION_MISMATCH, "query dim does not match index dim");
+    if (rows == 0) fail(PLAID_INVALID_PARAMS, "query must contain at least one token");
+    if (rows > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32 query tokens");
+    validate_params_host(p, ix.K);
+    if (!p.disable_filter && stride2 < std::min<uint64_t>(p.ndocs, ix.N))
+        fail(PLAID_INVALID_PARAMS, "exchange stride below this shard's stage-2 width");
+    DeviceGuard g(device_);
+    ensure_param_buffers(p);
+    if (!st) st = stream_;
+    launch::reset_launches();
+    pending_ = p;
+    pending_q_ = d_q;
+    pending_rows_ = uint32_t(rows);
+    pending_stride2_ = stride2;
+    pending_stride3_ = 0;
+    phase_ = 1;
+    const bool times = cfg_.record_times != 0;
+    launch::validate_query(d_q, uint32_t(rows), uint32_t(dim), status_.p, st);
+    enqueue_front(d_q, uint32_t(rows), p, st, times);
+    if (!p.disable_filter)
+        launch::export_keys(sel2_.p, counters_.p + kN2, stride2, uint32_t(index_->pid_base()), d_x2, st);
+    PLAID_CUDA(cudaGetLastError());
+}
+
+void Searcher::shard_phase2(const uint64_t* d_g2, uint64_t shards, uint64_t* d_x3, uint64_t stride3,
+                            cudaStream_t st) {
+    if (phase_ != 1) fail(PLAID_INVALID_PARAMS, "shard_phase2 without a preceding shard_phase1");
+    const plaid_params& p = pending_;
+    if (!p.disable_filter && stride3 < std::min<uint64_t>(stage3_width(p), index_->view().N))
+        fail(PLAID_INVALID_PARAMS, "exchange stride below this shard's stage-3 width");
+    DeviceGuard g(device_);
+    if (!st) st = stream_;
+    const bool times = cfg_.record_times != 0;
+    const uint32_t base = uint32_t(index_->pid_base());
+    if (!p.disable_filter) {
+        launch::threshold_filter(d_g2, shards * pending_stride2_, p.ndocs, sel2_.p, counters_.p + kN2, base, st);
+        enqueue_stage3(p, st, times);
+        launch::export_keys(sel3_.p, counters_.p + kN3, stride3, base, d_x3, st);
+    }
+    pending_stride3_ = stride3;
+    phase_ = 2;
+    PLAID_CUDA(cudaGetLastError());
+}
+
+void Searcher::shard_phase3(const uint64_t* d_g3, uint64_t shards, uint32_t* d_pids, float* d_scores,
+                            uint64_t* d_n, cudaStream_t st) {
+    if (phase_ != 2) fail(PLAID_INVALID_PARAMS, "shard_phase3 without a preceding shard_phase2");
+    const plaid_params& p = pending_;
+    DeviceGuard g(device_);
+    if (!st) st = stream_;
+    const bool times = cfg_.record_times != 0;
+    if (!p.disable_filter)
+        launch::threshold_filter(d_g3, shards * pending_stride3_, stage3_width(p), sel3_.p, counters_.p + kN3,
+                                 uint32_t(index_->pid_base()), st);
+    enqueue_back(pending_q_, pending_rows_, p, d_pids, d_scores, d_n, st, times);
+    phase_ = 0;
+    PLAID_CUDA(cudaGetLastError());
+    last_launches_ = launch::launches();
+}
+
+// Trace counters of the last enqueued query, on the device: [stage1_candidates,
+// stage2_out, stage3_out, final_out (host path only), stage2_rows_gathered,
+// stage3_rows_gathered].
+void Searcher::trace_counters_device(uint64_t* d_out, cudaStream_t st) {
+    DeviceGuard g(device_);
+    if (!st) st = stream_;
+    PLAID_CUDA(cudaMemcpyAsync(d_out, counters_.p, 6 * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
 }
 
 // Phase durations of the last enqueued query (record_times): K1, candidate

@@ -94,6 +94,13 @@ public:
     void search_device(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim,
                        const plaid_params& p, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
                        cudaStream_t st);
+    // Global-exact sharded search: phases separated by the caller's all-gathers.
+    void shard_phase1(const float* d_q, uint64_t rows, uint64_t dim, const plaid_params& p, uint64_t* d_x2,
+                      uint64_t stride2, cudaStream_t st);
+    void shard_phase2(const uint64_t* d_g2, uint64_t shards, uint64_t* d_x3, uint64_t stride3, cudaStream_t st);
+    void shard_phase3(const uint64_t* d_g3, uint64_t shards, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
+                      cudaStream_t st);
+    void trace_counters_device(uint64_t* d_out, cudaStream_t st);
     void sync();
     uint64_t last_launches() const { return last_launches_; }
     void phase_ms(double* out);
@@ -128,6 +135,10 @@ private:
     // given device buffers (pids are global: local + pid_base).
     void enqueue(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
                  float* d_scores, uint64_t* d_n, cudaStream_t st, bool times);
+    void enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st, bool times);
+    void enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times);
+    void enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,
+                      uint64_t* d_n, cudaStream_t st, bool times);
     void ensure_param_buffers(const plaid_params& p);
     void record(int slot, cudaStream_t st, bool times);
 
@@ -136,6 +147,12 @@ private:
     plaid_searcher_config cfg_;
     cudaStream_t stream_ = nullptr;
     uint64_t last_launches_ = 0;
+    // sharded-search state between shard_phase calls
+    plaid_params pending_{};
+    const float* pending_q_ = nullptr;
+    uint32_t pending_rows_ = 0;
+    uint64_t pending_stride2_ = 0, pending_stride3_ = 0;
+    int phase_ = 0;
 
     // scratch
     DevBuf<float> q_, scores_, rowmax_, out_scores_;

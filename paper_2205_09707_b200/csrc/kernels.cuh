@@ -171,6 +171,15 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
               uint32_t id_base, uint64_t* d_tmp, cudaStream_t st);
 uint64_t sort_tmp_capacity(uint64_t nmax);
 
+// Global-exact shard exchange (select.cu): export keys[0..*d_n) in global
+// form (ids + base) into a zero-padded row of `stride`; then, from the
+// all-gathered rows of every shard (total keys), keep in place only the local
+// keys at or above the global want-th largest key (*d_n updated).
+void export_keys(const uint64_t* d_keys, const uint64_t* d_n, uint64_t stride, uint32_t base, uint64_t* d_out,
+                 cudaStream_t st);
+void threshold_filter(const uint64_t* d_gathered, uint64_t total, uint64_t want, uint64_t* d_keys, uint64_t* d_n,
+                      uint32_t base, cudaStream_t st);
+
 // ---- stage 4 ----------------------------------------------------------------------
 // Decompress + exact MaxSim per candidate (ids from keys or ids); writes keys.
 // With d = 128 and a finalist list that fits `scratch` (rank128.cu: the

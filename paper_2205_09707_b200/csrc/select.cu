@@ -337,16 +337,32 @@ __global__ void copy_count_kernel(const uint64_t* src, uint64_t* dst, uint64_t c
     *dst = v < cap ? v : cap;
 }
 
-__global__ void validate_query_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
-                                      int* __restrict__ status) {
+// types.cpp:10-19 check_unit_rows: norm^2 = sum of double(v)^2 in order.  The
+// products are exact in fp64 (24-bit mantissas), so only the adds must stay
+// in order: 32-dim chunks of Q are staged coalesced in shared memory and
+// thread r runs row r's dependent add chain from there.
+__global__ void __launch_bounds__(256) validate_query_kernel(const float* __restrict__ q, uint32_t rows,
+                                                              uint32_t dim, int* __restrict__ status) {
     dev::pdl_wait();
-    const uint32_t r = threadIdx.x;
-    if (r >= rows) return;
+    __shared__ float tile[32][33];
+    const uint32_t t = threadIdx.x;
     double acc = 0.0;
-    for (uint32_t d = 0; d < dim; ++d) {
-        const double v = double(q[r * dim + d]);
-        acc = __dadd_rn(acc, __dmul_rn(v, v));
+    for (uint32_t d0 = 0; d0 < dim; d0 += 32) {
+        for (uint32_t i = t; i < 32 * 32; i += blockDim.x) {
+            const uint32_t r = i >> 5, d = d0 + (i & 31);
+            tile[r][i & 31] = r < rows && d < dim ? q[size_t(r) * dim + d] : 0.f;
+        }
+        __syncthreads();
+        if (t < rows) {
+            const uint32_t m = dim - d0 < 32 ? dim - d0 : 32;
+            for (uint32_t j = 0; j < m; ++j) {
+                const double v = double(tile[t][j]);
+                acc = __dadd_rn(acc, __dmul_rn(v, v));
+            }
+        }
+        __syncthreads();
     }
+    if (t >= rows) return;
     const double norm = sqrt(acc);
     if (fabs(norm - 1.0) > double(1e-3f)) atomicExch(status, 2);  // NotNormalized + 1
 }
@@ -529,6 +545,111 @@ hist_resolve_kernel(SelectHist* __restrict__ st, const uint64_t* __restrict__ bk
     }
 }
 
+
+// ---- global-exact shard exchange ---------------------------------------
+// A key in GLOBAL form carries the global passage id: (score image << 32) |
+// ~(local id + base).  Within one shard the map is monotone, so local and
+// global forms order the shard's keys identically; across shards only the
+// global form is comparable.
+__device__ __forceinline__ uint64_t globalize(uint64_t key, uint32_t base) {
+    return (key & 0xffffffff00000000ull) | uint64_t(~(dev::key_id(key) + base));
+}
+
+// out[j] = global form of keys[j] for j < min(*d_n, stride), 0 (below every
+// real key) for the rest of the stride.
+__global__ void export_keys_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
+                                   uint64_t stride, uint32_t base, uint64_t* __restrict__ out) {
+    dev::pdl_wait();
+    const uint64_t n = *d_n;
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < stride;
+         j += uint64_t(gridDim.x) * blockDim.x)
+        out[j] = j < n ? globalize(keys[j], base) : 0ull;
+}
+
+// One CTA.  (1) t = the want-th largest non-zero key of the gathered global
+// keys g[0..total) by an MSB-first 8-bit radix select (t = 1, keep all, when
+// fewer than `want` are non-zero); (2) keys[0..*d_n) (local form, this
+// shard) keep exactly those whose global form is >= t, compacted in place in
+// their original order; *d_n becomes the survivor count.  Because every
+// shard's exported list holds its local top-`want`, the gathered union holds
+// the global top-`want`, so the survivors are the global selection's members
+// on this shard — the reference's single-index select_top (pipeline.cpp:139-163).
+constexpr uint32_t kThrThreads = 1024;
+__global__ void __launch_bounds__(kThrThreads)
+threshold_filter_kernel(const uint64_t* __restrict__ g, uint64_t total, uint64_t want,
+                        uint64_t* __restrict__ keys, uint64_t* __restrict__ d_n, uint32_t base) {
+    dev::pdl_wait();
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t s_prefix, s_rem;
+    __shared__ uint32_t s_warp[kThrThreads / 32];
+    __shared__ uint32_t s_out;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        s_prefix = 0;
+        s_rem = want;
+        s_out = 0;
+    }
+    // the first histogram pass also counts the non-zero gathered keys
+    uint64_t prefix = 0;  // digits fixed so far (high bits), shifted into place
+    bool keep_all = false;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (uint32_t i = tid; i < 256; i += kThrThreads) hist[i] = 0;
+        __syncthreads();
+        const uint64_t hi_mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
+        for (uint64_t i = tid; i < total; i += kThrThreads) {
+            const uint64_t x = __ldcg(g + i);
+            if (x != 0ull && (x & hi_mask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint64_t rem = s_rem;
+            if (pass == 0) {
+                uint64_t nz = 0;
+                for (int b = 0; b < 256; ++b) nz += hist[b];
+                if (nz < want) rem = 0;  // keep all
+            }
+            if (rem == 0) {
+                s_rem = 0;
+            } else {
+                int b = 255;
+                for (; b > 0; --b) {
+                    if (hist[b] >= rem) break;
+                    rem -= hist[b];
+                }
+                s_prefix = prefix | (uint64_t(b) << shift);
+                s_rem = rem;
+            }
+        }
+        __syncthreads();
+        if (s_rem == 0) {
+            keep_all = true;
+            break;
+        }
+        prefix = s_prefix;
+    }
+    const uint64_t t = keep_all ? 1ull : prefix;
+    // (2) order-preserving in-place compaction, one 1024-key chunk at a time
+    const uint64_t n = *d_n;
+    const uint32_t lane = tid & 31u, warp = tid >> 5;
+    for (uint64_t c0 = 0; c0 < n; c0 += kThrThreads) {
+        const uint64_t i = c0 + tid;
+        const uint64_t x = i < n ? keys[i] : 0ull;
+        const bool ok = i < n && globalize(x, base) >= t;
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0;
+        for (uint32_t w = 0; w < warp; ++w) before += s_warp[w];
+        const uint32_t base_out = s_out;
+        __syncthreads();
+        if (ok) keys[base_out + before + __popc(bal & ((1u << lane) - 1u))] = x;
+        if (tid == kThrThreads - 1) s_out = base_out + before + __popc(bal);
+        __syncthreads();
+    }
+    if (tid == 0) *d_n = s_out;
+}
+
 }  // namespace
 
 namespace launch {
@@ -643,7 +764,20 @@ void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t s
 }
 
 void validate_query(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, cudaStream_t st) {
-    ::plaid::launch::pdl(validate_query_kernel, 1, 32, 0, st, d_q, rows, dim, d_status);
+    ::plaid::launch::pdl(validate_query_kernel, 1, 256, 0, st, d_q, rows, dim, d_status);
+    count_launch();
+}
+
+void export_keys(const uint64_t* d_keys, const uint64_t* d_n, uint64_t stride, uint32_t base, uint64_t* d_out,
+                 cudaStream_t st) {
+    if (!stride) return;
+    ::plaid::launch::pdl(export_keys_kernel, grid_for(stride, 256, 1024), 256, 0, st, d_keys, d_n, stride, base, d_out);
+    count_launch();
+}
+
+void threshold_filter(const uint64_t* d_gathered, uint64_t total, uint64_t want, uint64_t* d_keys, uint64_t* d_n,
+                      uint32_t base, cudaStream_t st) {
+    ::plaid::launch::pdl(threshold_filter_kernel, 1, kThrThreads, 0, st, d_gathered, total, want, d_keys, d_n, base);
     count_launch();
 }
 

@@ -12,8 +12,21 @@ the same global top-k.  Messages are k x 8 B per rank, so they are
 latency-bound: three small all-gathers of fixed size, no host sync between
 the search and the merge.
 
-This is the "shard-local" mode of SURVEY.md §8e: its result equals the
-reference run on each shard followed by the same merge.
+Two modes:
+
+* "global-exact" (default): two more all-gathers make every shard apply the
+  GLOBAL stage-2 (top-ndocs) and stage-3 (top-stage3_width) cuts
+  (plaid_shard_phase{1,2,3}_device): after stage 2 each shard exports its
+  local top-ndocs keys (score image, ~global pid), the union holds the global
+  top-ndocs, and each shard keeps only its keys at or above the global
+  ndocs-th key; the same after stage 3.  The merged top-k then equals
+  lir::search over the UNSHARDED index (pipeline.cpp:232-283), and the
+  shards' trace counters sum to its StageTrace.  Messages: ndocs x 8 B and
+  stage3_width x 8 B per shard (256 KiB + 64 KiB per query at cfg2, 8 GPUs).
+* "shard-local": the search runs to completion on every shard and only the
+  top-k lists are merged — equal to the reference run on each shard followed
+  by the same merge (a shard may admit passages the global stage-2 cut
+  drops).
 """
 from __future__ import annotations
 
@@ -40,20 +53,41 @@ def _all_gather(out: torch.Tensor, inp: torch.Tensor, group) -> None:
         dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp, group=group)
 
 
+MODES = ("global-exact", "shard-local")
+
+
+def exchange_strides(params, num_passages: int, disable_filter: bool = False) -> tuple[int, int]:
+    """Common row lengths of the two key exchanges: min(ndocs, N) and
+    min(stage3_width, N) over the GLOBAL passage count (>= every shard's)."""
+    if disable_filter:
+        return 0, 0
+    n3 = max(-(-int(params.ndocs) // 4), int(params.k))  # pipeline.cpp:227-230
+    return min(int(params.ndocs), int(num_passages)), min(n3, int(num_passages))
+
+
 class ShardedSearcher:
     """Global top-k over passage-sharded searchers.
 
     `searcher` is this rank's Searcher (over a DeviceIndex made with
     DeviceIndex.from_host_at(shard, pid_base) so it emits global ids).
-    Buffers live on `device`; `stream` is the CUDA stream handle both the
-    search and the merge are enqueued on (0 = legacy default stream)."""
+    `num_passages` is the global passage count (required for global-exact).
+    Buffers live on `device`; `stream` is the CUDA stream handle every phase
+    and the merge are enqueued on (0 = legacy default stream)."""
 
-    def __init__(self, searcher, k: int, group=None, device: Optional[torch.device] = None):
+    def __init__(self, searcher, k: int, group=None, device: Optional[torch.device] = None,
+                 mode: str = "global-exact", num_passages: Optional[int] = None):
+        if mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}")
+        if mode == "global-exact" and num_passages is None:
+            raise ValueError("global-exact mode needs the global passage count")
         self.s = searcher
         self.k = int(k)
         self.group = group
+        self.mode = mode
+        self.num_passages = num_passages
         self.world = dist.get_world_size(group)
-        dev = device if device is not None else torch.device("cpu")
+        self.dev = dev = device if device is not None else torch.device("cpu")
+        self._x = {}
         z = lambda *shape, dt: torch.zeros(*shape, dtype=dt, device=dev)  # noqa: E731
         self.pids, self.scores, self.n = z(self.k, dt=torch.int32), z(self.k, dt=torch.float32), z(1, dt=torch.int64)
         self.g_pids = z(self.world * self.k, dt=torch.int32)
@@ -62,14 +96,51 @@ class ShardedSearcher:
         self.out_pids, self.out_scores = z(self.k, dt=torch.int32), z(self.k, dt=torch.float32)
         self.out_n = z(1, dt=torch.int64)
 
-    def search(self, q: torch.Tensor, params, stream: int = 0):
+    def _xbuf(self, name: str, n: int) -> torch.Tensor:
+        t = self._x.get(name)
+        if t is None or t.numel() != n:
+            t = self._x[name] = torch.zeros(max(n, 1), dtype=torch.int64, device=self.dev)
+        return t
+
+    def search(self, q: torch.Tensor, params, stream: int = 0, options=None):
         """q: [rows, dim] float32 on this rank's device.  Returns device views
-        (pids, scores) of the global top-k (length out_n)."""
+        (pids, scores, n) of the global top-k (length out_n).  Every phase and
+        collective is ordered on `stream` (default: torch's current stream,
+        which the NCCL all-gathers use too)."""
         if int(params.k) != self.k:
             raise ValueError(f"params.k {params.k} != {self.k}")
+        if self.dev.type == "cuda":
+            if not stream:
+                stream = torch.cuda.current_stream(self.dev).cuda_stream
+            if not stream:
+                # the legacy default stream does not order the searcher's own
+                # (non-blocking) stream: run the phases and the collectives on
+                # one private stream instead
+                if getattr(self, "_side", None) is None:
+                    self._side = torch.cuda.Stream(self.dev)
+                self._side.wait_stream(torch.cuda.current_stream(self.dev))
+                with torch.cuda.stream(self._side):
+                    out = self.search(q, params, self._side.cuda_stream, options)
+                torch.cuda.current_stream(self.dev).wait_stream(self._side)
+                return out
         rows, dim = q.shape
-        self.s.search_device(q.data_ptr(), 1, rows, dim, params, self.pids.data_ptr(), self.scores.data_ptr(),
-                             self.n.data_ptr(), stream=stream)
+        df = bool(options.disable_filter) if options is not None else False
+        kw = {"options": options} if options is not None else {}
+        if self.mode == "shard-local":
+            self.s.search_device(q.data_ptr(), 1, rows, dim, params, self.pids.data_ptr(), self.scores.data_ptr(),
+                                 self.n.data_ptr(), stream=stream, **kw)
+        else:
+            s2, s3 = exchange_strides(params, self.num_passages, df)
+            x2, g2 = self._xbuf("x2", s2), self._xbuf("g2", self.world * s2)
+            x3, g3 = self._xbuf("x3", s3), self._xbuf("g3", self.world * s3)
+            self.s.shard_phase1(q.data_ptr(), rows, dim, params, x2.data_ptr(), s2, stream=stream, **kw)
+            if s2:
+                _all_gather(g2[: self.world * s2], x2[:s2], self.group)
+            self.s.shard_phase2(g2.data_ptr(), self.world, x3.data_ptr(), s3, stream=stream)
+            if s3:
+                _all_gather(g3[: self.world * s3], x3[:s3], self.group)
+            self.s.shard_phase3(g3.data_ptr(), self.world, self.pids.data_ptr(), self.scores.data_ptr(),
+                                self.n.data_ptr(), stream=stream)
         _all_gather(self.g_pids, self.pids, self.group)
         _all_gather(self.g_scores, self.scores, self.group)
         _all_gather(self.g_n, self.n, self.group)
@@ -77,3 +148,56 @@ class ShardedSearcher:
                                  self.k, self.k, self.out_pids.data_ptr(), self.out_scores.data_ptr(),
                                  self.out_n.data_ptr(), stream=stream)
         return self.out_pids, self.out_scores, self.out_n
+
+    def trace_counters(self, stream: int = 0) -> dict:
+        """StageTrace counters of the last search summed over the shards
+        (global-exact: equal to the unsharded reference's).  Host sync."""
+        c = torch.zeros(6, dtype=torch.int64, device=self.dev)
+        self.s.trace_counters_device(c.data_ptr(), stream=stream)
+        if self.dev.type == "cuda":
+            torch.cuda.current_stream(self.dev).synchronize()
+        dist.all_reduce(c, group=self.group)
+        v = c.cpu().tolist()
+        return {"stage1_candidates": v[0], "stage2_out": v[1], "stage3_out": v[2],
+                "stage2_rows_gathered": v[4], "stage3_rows_gathered": v[5]}
+
+
+def search_local_shards(searchers, q, params, num_passages: int, stream: int = 0, options=None):
+    """Global-exact search over G shard searchers driven from ONE process (e.g.
+    G shards on one GPU for the parity tests): the same three phases as
+    ShardedSearcher, with the all-gathers done by device copies.  Returns
+    (pids, scores) of the merged global top-k as numpy arrays."""
+    import numpy as np
+
+    G = len(searchers)
+    dev = q.device
+    side = None
+    if dev.type == "cuda" and not stream:
+        # one stream for every shard (handle 0 would mean "each searcher's
+        # own stream"): phase 2 of shard i reads rows other shards exported
+        side = torch.cuda.Stream(dev)
+        stream = side.cuda_stream
+    df = bool(options.disable_filter) if options is not None else False
+    kw = {"options": options} if options is not None else {}
+    rows, dim = q.shape
+    k = int(params.k)
+    s2, s3 = exchange_strides(params, num_passages, df)
+    z = lambda n, dt=torch.int64: torch.zeros(max(n, 1), dtype=dt, device=dev)  # noqa: E731
+    g2, g3 = z(G * s2), z(G * s3)
+    pids, scores, ns = z(G * k, torch.int32), z(G * k, torch.float32), z(G)
+    op, os_, on = z(k, torch.int32), z(k, torch.float32), z(1)
+    if side is not None:
+        torch.cuda.synchronize(dev)  # buffers zeroed on the current stream
+    for i, s in enumerate(searchers):
+        s.shard_phase1(q.data_ptr(), rows, dim, params, g2.data_ptr() + 8 * i * s2, s2, stream=stream, **kw)
+    for i, s in enumerate(searchers):
+        s.shard_phase2(g2.data_ptr(), G, g3.data_ptr() + 8 * i * s3, s3, stream=stream)
+    for i, s in enumerate(searchers):
+        s.shard_phase3(g3.data_ptr(), G, pids.data_ptr() + 4 * i * k, scores.data_ptr() + 4 * i * k,
+                       ns.data_ptr() + 8 * i, stream=stream)
+    searchers[0].merge_topk_device(pids.data_ptr(), scores.data_ptr(), ns.data_ptr(), G, k, k, op.data_ptr(),
+                                   os_.data_ptr(), on.data_ptr(), stream=stream)
+    if dev.type == "cuda":
+        torch.cuda.synchronize(dev)
+    m = int(on[0])
+    return op[:m].cpu().numpy().view(np.uint32), os_[:m].cpu().numpy()

@@ -241,3 +241,49 @@ def test_stage2_select_massive_ties(port):
             assert np.array_equal(got.topk.passage_ids, ids)
             assert np.array_equal(bits(got.topk.scores), bits(sc))
             assert got.trace.counters() == tr
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_global_exact_shards_bit_exact(port, G):
+    """Global-exact passage sharding with G shards resident on
+    one GPU: the three device phases + key exchanges + merge reproduce the
+    UNSHARDED reference search bit for bit, and the summed trace counters
+    equal its StageTrace."""
+    import torch
+
+    from paper_2205_09707_b200.sharded import search_local_shards, shard_range
+
+    N, K = 6000, 512
+    whole = P.generate_index(N, K, dim=128, nbits=2, mean_len=40, seed=4)
+    qs = P.generate_queries(whole, 4, seed=21)
+    shards = []
+    for g in range(G):
+        a, b = shard_range(N, G, g)
+        hs = P.generate_index(b - a, K, dim=128, nbits=2, mean_len=40, seed=4, pid_base=a)
+        ix = P.DeviceIndex.from_host_at(hs, pid_base=a)
+        shards.append((ix, P.Searcher(ix, score_mode=P.ScoreMode.EXACT)))
+    ss = [s for _, s in shards]
+    cases = [P.default_params_for_k(k) for k in (10, 100)] + [P.SearchParams(20, 8, -1.0, 300),
+                                                               P.SearchParams(50, 4, 0.3, 64)]
+    for p in cases:
+        for q in qs:
+            dq = torch.from_numpy(q.copy()).cuda()
+            ids, sc = search_local_shards(ss, dq, p, N)
+            eids, esc, tr = port.search(whole, q, p)
+            assert np.array_equal(ids, eids), (G, p)
+            assert np.array_equal(bits(sc), bits(esc)), (G, p)
+            c = torch.zeros(6, dtype=torch.int64, device="cuda")
+            tot = np.zeros(6, np.int64)
+            for s in ss:
+                s.trace_counters_device(c.data_ptr())
+                torch.cuda.synchronize()
+                tot += c.cpu().numpy()
+            assert tot[0] == tr["stage1_candidates"] and tot[1] == tr["stage2_out"]
+            assert tot[2] == tr["stage3_out"]
+            assert tot[4] == tr["stage2_rows_gathered"] and tot[5] == tr["stage3_rows_gathered"]
+    # disable_filter: nothing is cut before stage 4
+    p = P.default_params_for_k(10)
+    dq = torch.from_numpy(qs[0].copy()).cuda()
+    ids, sc = search_local_shards(ss, dq, p, N, options=P.SearchOptions(disable_filter=True))
+    eids, esc, _ = port.search(whole, qs[0], p, disable_filter=True)
+    assert np.array_equal(ids, eids) and np.array_equal(bits(sc), bits(esc))
