@@ -196,7 +196,8 @@ def config_block(cfg, params, args, world):
             "passages_total": cfg["N"] * world, "centroids": cfg["K"], "nbits": cfg["nbits"], "dim": DIM,
             "query_tokens": QLEN, "k": params.k, "nprobe": params.nprobe, "t_cs": params.t_cs,
             "ndocs": params.ndocs, "batch": 1, "l2_flush": "256 MiB write before every step (untimed)",
-            "score_mode": args.score_mode, "parallelism": f"passage-range shards x{world}"}
+            "score_mode": args.score_mode, "parallelism": f"passage-range shards x{world}",
+            "shard_merge": args.shard_mode if world > 1 else None}
 
 
 def run_plaid(args, cfg):
@@ -207,12 +208,20 @@ def run_plaid(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PLAID_DIST_BACKEND", "nccl") != "nccl":
+        local = 0  # several ranks share one GPU (test of the multi-rank path)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # PLAID_DIST_BACKEND=gloo lets a 1-GPU box run several ranks on one GPU
+        # (exercise of the multi-rank path only; NCCL is the product backend)
+        backend = os.environ.get("PLAID_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     h = make_index(cfg, rank)
     params = params_for(cfg)
@@ -245,14 +254,18 @@ def run_plaid(args, cfg):
     if world > 1:
         from paper_2205_09707_b200.sharded import ShardedSearcher
 
-        ss = ShardedSearcher(s, k, device=torch.device("cuda", local))
+        ss = ShardedSearcher(s, k, device=torch.device("cuda", local), mode=args.shard_mode,
+                             num_passages=cfg["N"] * world)
         m_pids, m_scores = ss.out_pids, ss.out_scores
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step(i):
         q = dq[i % nq]
         if world > 1:
-            ss.search(q, params, stream=sh)  # local search, all-gather of k (pid, score), merge
+            # global-exact: stages 1-2, all-gather of the top-ndocs keys, filter +
+            # stage 3, all-gather of the stage-3 keys, filter + stage 4, then
+            # all-gather of k (pid, score) and the merge
+            ss.search(q, params, stream=sh)
         else:
             s.search_device(q.data_ptr(), 1, QLEN, DIM, params, d_pids.data_ptr(), d_scores.data_ptr(),
                             d_n.data_ptr(), stream=sh)
@@ -395,6 +408,8 @@ def main():
     ap.add_argument("--score-mode", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard-mode", default="global-exact", choices=["global-exact", "shard-local"],
+                    help="multi-GPU exchange (SURVEY.md §8e): global cuts after stages 2 and 3, or top-k merge only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

@@ -52,7 +52,7 @@ namespace {
 
 constexpr int kRaw = 9;                      // TMA ring depth
 constexpr int kOps = 6;                      // TMEM operand slots
-constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 32 fp32
+constexpr uint32_t kChunkBytes = 128 * 128;  // one TMA box: 32 centroids x 128 fp32 (16 KB contiguous in HBM)
 constexpr uint32_t kQChunkBytes = 64 * 128;  // [Q_hi; Q_lo] 64 rows x 32 fp32
 constexpr int kThreads = 512;
 constexpr int kEpiWarps = 8;                 // warps 8..15
@@ -80,6 +80,8 @@ constexpr uint32_t kIdesc32 = idesc_tf32(32);
 
 // Debug timeline (PLAID_TF32_DBG=16): globaltimer stamps of CTA 0's pipeline
 // events and every CTA's begin/end (read back with plaid_debug_tf32_trace).
+// Pipeline experiments (results wrong): dbg & 1 skips the MMAs, & 2 the S
+// stores, & 4 the TMEM operand stores.
 __device__ unsigned long long g_tf32_trace[8 * 256];
 __device__ unsigned long long g_tf32_cta[2 * 256];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -120,11 +122,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
             dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z)
         : "memory");
 }
 
@@ -216,7 +218,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRaw; ++s) {
             mbar_init(raw_full(s), 1);
-            mbar_init(raw_empty(s), 4);  // one arrive per converter warp
+            mbar_init(raw_empty(s), 1);  // the converter warp of the box's lane quarter
         }
         for (int s = 0; s < kOps; ++s) {
             mbar_init(ops_full(s), 4);
@@ -256,14 +258,16 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
     if (warp == 0) {
         // ---------------- TMA producer
         if (lane == 0) {
+            // box (t, w) = centroids [128 t + 32 w, +32), all 128 dims: 16 KB
+            // contiguous in HBM, landing as [chunk][centroid][32 fp32]
             uint32_t g = 0;
             for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-                for (int kc = 0; kc < kChunks; ++kc, ++g) {
+                for (int w = 0; w < 4; ++w, ++g) {
                     const int s = g % kRaw;
                     mbar_wait(raw_empty(s), ((g / kRaw) & 1) ^ 1);
                     trace_stamp(dbg, 0, g);
                     mbar_expect_tx(raw_full(s), kChunkBytes);
-                    tma_load_2d(base + kOffRaw + s * kChunkBytes, &cmap, kc * 32, int(t * 128), raw_full(s));
+                    tma_load_3d(base + kOffRaw + s * kChunkBytes, &cmap, 0, int(t * 128 + w * 32), 0, raw_full(s));
                 }
         }
     } else if (warp == 1) {
@@ -279,7 +283,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                 mbar_wait(ops_full(s), (g / kOps) & 1);
                 if (lane == 0) trace_stamp(dbg, 4, g);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lane == 0) {
+                if (lane == 0 && !(dbg & 1)) {
                     const uint32_t ahi = tmem_base + kOpsCol0 + s * 64, alo = ahi + 32;
                     const uint32_t bq = base + kOffQ + kc * kQChunkBytes;
 #pragma unroll
@@ -291,26 +295,33 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                     }
                     mma_commit(ops_empty(s));
                     if (kc == kChunks - 1) mma_commit(tfull_bar(acc));
+                } else if (lane == 0) {  // dbg & 1: no MMAs (pipeline experiment)
+                    mbar_arrive(ops_empty(s));
+                    if (kc == kChunks - 1) mbar_arrive(tfull_bar(acc));
                 }
                 __syncwarp();
             }
         }
     } else if (warp >= 4 && warp < 8) {
-        // ---------------- converters: thread = row (TMEM lane quarter warp % 4)
-        const uint32_t row = (warp & 3) * 32 + lane;
-        const uint32_t lane_off = ((warp & 3) * 32) << 16;
-        uint32_t g = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-            for (int kc = 0; kc < kChunks; ++kc, ++g) {
-                const int s = g % kRaw, o = g % kOps;
-                mbar_wait(raw_full(s), (g / kRaw) & 1);
-                if (warp == 4 && lane == 0) trace_stamp(dbg, 1, g);
-                // the row's 8 granules, un-swizzled: granule j at (j ^ (row & 7))
-                const uint4* src = reinterpret_cast<const uint4*>(smem + kOffRaw + s * kChunkBytes + row * 128);
+        // ---------------- converters: warp = lane quarter q, thread = centroid
+        // row 32 q + lane; the warp owns box (t, q) of every tile
+        const uint32_t q = warp & 3;
+        const uint32_t lane_off = (q * 32) << 16;
+        uint32_t go = 0, lt = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+            const uint32_t gb = lt * 4 + q;
+            const int s = gb % kRaw;
+            mbar_wait(raw_full(s), (gb / kRaw) & 1);
+            if (warp == 4 && lane == 0) trace_stamp(dbg, 1, lt * 4);
+            for (int kc = 0; kc < kChunks; ++kc, ++go) {
+                const int o = go % kOps;
+                // the row's 8 granules of chunk kc, un-swizzled: granule j at (j ^ (lane & 7))
+                const uint4* src =
+                    reinterpret_cast<const uint4*>(smem + kOffRaw + s * kChunkBytes + (kc * 32 + lane) * 128);
                 uint32_t hi[32], lo[32];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const uint4 v = src[j ^ (row & 7)];
+                    const uint4 v = src[j ^ (lane & 7)];
                     hi[4 * j + 0] = split_hi(v.x);
                     hi[4 * j + 1] = split_hi(v.y);
                     hi[4 * j + 2] = split_hi(v.z);
@@ -320,20 +331,25 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                     lo[4 * j + 2] = split_lo(v.z);
                     lo[4 * j + 3] = split_lo(v.w);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(raw_empty(s));  // slot consumed
-                mbar_wait(ops_empty(o), ((g / kOps) & 1) ^ 1);
-                if (warp == 4 && lane == 0) trace_stamp(dbg, 2, g);
+                if (kc == kChunks - 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(raw_empty(s));  // box consumed
+                }
+                mbar_wait(ops_empty(o), ((go / kOps) & 1) ^ 1);
+                if (warp == 4 && lane == 0) trace_stamp(dbg, 2, go);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t col = tmem_base + lane_off + kOpsCol0 + o * 64;
-                tmem_st32(col, hi);
-                tmem_st32(col + 32, lo);
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                if (!(dbg & 4)) {  // dbg & 4: no TMEM stores (pipeline experiment)
+                    tmem_st32(col, hi);
+                    tmem_st32(col + 32, lo);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(ops_full(o));
-                if (warp == 4 && lane == 0) trace_stamp(dbg, 3, g);
+                if (warp == 4 && lane == 0) trace_stamp(dbg, 3, go);
             }
+        }
     } else if (warp >= 8) {
         // ---------------- epilogue: two groups of 4 warps take alternate tiles
         // (group = accumulator); thread = centroid row (lane quarter q)
@@ -395,7 +411,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             for (int r = 0; r < 32; ++r) {
                 const float sc = tr[r * 33 + lane];
                 cand |= (uint32_t(r) < nv && tok && sc > thr0 && sc >= gb) ? (1u << r) : 0u;
-                if (uint32_t(r) < nv) S[(c0 + r) * kScoresPitch + lane] = sc;
+                if (uint32_t(r) < nv && !(dbg & 2)) S[(c0 + r) * kScoresPitch + lane] = sc;
             }
             // per-lane inserts, rare once the bounds have risen
             while (cand) {
@@ -475,10 +491,13 @@ bool tensor_scores_supported(const IndexView& ix) { return ix.dim == kDim && ix.
 
 void make_centroid_tensor_map(const IndexView& ix, void* out_map) {
     CUtensorMap* map = static_cast<CUtensorMap*>(out_map);
-    const cuuint64_t dims[2] = {cuuint64_t(kDim), cuuint64_t(ix.K)};
-    const cuuint64_t strides[1] = {cuuint64_t(kDim) * sizeof(float)};
-    const cuuint32_t box[2] = {32, 128};
-    const cuuint32_t estr[2] = {1, 1};
+    // 3-D view (32 fp32, centroid, 32-dim chunk): one box = 32 centroids x
+    // 4 chunks = 16 KB contiguous in HBM, laid out [chunk][centroid][32] in
+    // shared memory (128-B rows, SWIZZLE_128B by centroid & 7)
+    const cuuint64_t dims[3] = {32, cuuint64_t(ix.K), cuuint64_t(kDim / 32)};
+    const cuuint64_t strides[2] = {cuuint64_t(kDim) * sizeof(float), 32 * sizeof(float)};
+    const cuuint32_t box[3] = {32, 32, kDim / 32};
+    const cuuint32_t estr[3] = {1, 1, 1};
     // through the runtime's driver entry point: the library does not link
     // libcuda, so it loads (and exports its ABI) on hosts without a driver
     using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -493,7 +512,7 @@ void make_centroid_tensor_map(const IndexView& ix, void* out_map) {
         return reinterpret_cast<EncodeFn>(fn);
     }();
     if (!encode) fail_cuda_driver(int(CUDA_ERROR_NOT_FOUND), "cuGetProcAddress(cuTensorMapEncodeTiled)");
-    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ix.centroids), dims,
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ix.centroids), dims,
                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail_cuda_driver(int(r), "cuTensorMapEncodeTiled");

@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -43,6 +44,18 @@ constexpr uint32_t kConsumers = 4; // x 8 query tokens = 32
 constexpr uint32_t kProducers = 2; // x 32 tokens = one tile
 constexpr uint32_t kFusedThreads = (kConsumers + kProducers) * 32;
 constexpr uint32_t kSmemFloats = 16 * 128 * 2 + 2 * kTile * kPitch;  // query pairs + 2 tiles
+
+// Debug timeline (PLAID_RANK_DBG=1): globaltimer stamps of CTA 0's tiles
+// [event][tile]: 0 producer start, 1 producer rows landed, 2 producer done,
+// 3 consumer start, 4 consumer done (read with plaid_debug_rank_trace).
+__device__ unsigned long long g_rank_trace[5 * 64];
+__device__ __forceinline__ void rank_stamp(uint32_t dbg, int ev, uint32_t k) {
+    if (dbg && blockIdx.x == 0 && k < 64 && dev::lane_id() == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_rank_trace[ev * 64 + k] = t;
+    }
+}
 
 struct Weights16 {
     float w[16];
@@ -148,7 +161,7 @@ __global__ void __launch_bounds__(kFusedThreads)
 stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
                     const uint8_t* __restrict__ residuals, Weights16 W, const uint64_t* __restrict__ d_n,
                     const uint32_t* __restrict__ pref, const uint64_t* __restrict__ fin_base,
-                    const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
+                    const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run, uint32_t dbg) {
     dev::pdl_wait();
     extern __shared__ __align__(16) float sm[];
     __shared__ float w_s[16];
@@ -191,6 +204,7 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
         for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++k) {
             const uint32_t b = k & 1;
             mbar_wait(&empty_bar[b], ((k >> 1) & 1) ^ 1);
+            if (pw == 0) rank_stamp(dbg, 0, k);
             float* tile = tiles + b * kTile * kPitch + pw * 32 * kPitch;
             const uint32_t g0 = tl * kTile + pw * 32;
             const uint32_t g = g0 + lane;
@@ -222,6 +236,7 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
+            if (pw == 0) rank_stamp(dbg, 1, k);
             if (valid) {
                 float4* row = reinterpret_cast<float4*>(tile + lane * kPitch);
                 double acc = 0.0;
@@ -251,6 +266,7 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
                     }
                 }
             }
+            if (pw == 0) rank_stamp(dbg, 2, k);
             mbar_arrive(&full_bar[b]);
         }
         return;
@@ -263,6 +279,7 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
     for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++k) {
         const uint32_t b = k & 1;
         mbar_wait(&full_bar[b], (k >> 1) & 1);
+        if (warp == 0) rank_stamp(dbg, 3, k);
         const float* tile = tiles + b * kTile * kPitch;
         const uint32_t p0 = pass_s[b][lane], p1 = pass_s[b][32 + lane];
         const bool valid0 = p0 < 0xFFFFFFF0u, valid1 = p1 < 0xFFFFFFF0u;
@@ -317,6 +334,7 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
                 }
             }
         }
+        if (warp == 0) rank_stamp(dbg, 4, k);
         mbar_arrive(&empty_bar[b]);
     }
 }
@@ -378,8 +396,12 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
     uint64_t fb = (nmax * ix.max_doclen + kTile - 1) / kTile;
     if (fb > uint64_t(sm_count()) * 2) fb = uint64_t(sm_count()) * 2;  // two CTAs (12 warps) per SM
     auto fk = ix.nbits == 1 ? stream_fused_kernel<1> : ix.nbits == 2 ? stream_fused_kernel<2> : stream_fused_kernel<4>;
+    static const uint32_t dbg = [] {
+        const char* e = getenv("PLAID_RANK_DBG");
+        return e ? uint32_t(atoi(e)) : 0u;
+    }();
     ::plaid::launch::pdl(fk, uint32_t(fb), kFusedThreads, fsm, st, ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref,
-                         s.fin_base, d_q, rows, s.run);
+                         s.fin_base, d_q, rows, s.run, dbg);
     count_launch();
     const uint32_t nb = uint32_t((nmax + 255) / 256);
     ::plaid::launch::pdl(finalize_kernel, nb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
@@ -389,3 +411,8 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
 
 }  // namespace launch
 }  // namespace plaid
+
+// Debug: CTA 0's stage-4 tile timeline (see rank_stamp), 5 x 64 stamps.
+extern "C" int plaid_debug_rank_trace(unsigned long long* out) {
+    return int(cudaMemcpyFromSymbol(out, plaid::g_rank_trace, sizeof(plaid::g_rank_trace)));
+}

@@ -16,7 +16,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr) {
     return d;
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int CONT = 0, int NACC = 2>
 __global__ void bench(unsigned long long* out, int iters) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint32_t tslot;
@@ -35,10 +35,25 @@ __global__ void bench(unsigned long long* out, int iters) {
     const uint32_t tm = tslot;
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t(N) >> 3) << 17) | ((128u >> 4) << 24);
     const uint32_t a = smem_u32(sm), b = smem_u32(sm + 128 * 128 * 4);
+    __shared__ volatile int stop;
+    if (threadIdx.x == 0) stop = 0;
+    __syncthreads();
+    if (CONT && warp >= 1 && warp < 1 + CONT) {
+        // TMEM traffic on columns [384, 448) of this warp's lane quarter
+        uint32_t r[32];
+        for (int j = 0; j < 32; ++j) r[j] = j;
+        const uint32_t ta = tm + ((warp & 3) * 32 << 16) + 384;
+        while (!stop) {
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+                "r"(r[0]),"r"(r[1]),"r"(r[2]),"r"(r[3]),"r"(r[4]),"r"(r[5]),"r"(r[6]),"r"(r[7]),"r"(r[8]),"r"(r[9]),"r"(r[10]),"r"(r[11]),"r"(r[12]),"r"(r[13]),"r"(r[14]),"r"(r[15]),
+                "r"(r[16]),"r"(r[17]),"r"(r[18]),"r"(r[19]),"r"(r[20]),"r"(r[21]),"r"(r[22]),"r"(r[23]),"r"(r[24]),"r"(r[25]),"r"(r[26]),"r"(r[27]),"r"(r[28]),"r"(r[29]),"r"(r[30]),"r"(r[31]) : "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+    }
     if (threadIdx.x == 0) {
         long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
-            const uint32_t d = tm + (it & 1) * 256;  // two accumulators (<= 256 cols each)
+            const uint32_t d = NACC == 1 ? tm : NACC == 2 ? tm + (it & 1) * 256 : tm + (it & 3) * 64;
             if (TS) {
                 asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                              "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
@@ -53,21 +68,22 @@ __global__ void bench(unsigned long long* out, int iters) {
         asm volatile("{\n\t.reg .pred p;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W;\n\t}" ::"r"(smem_u32(&bar)));
         long long t1 = clock64();
         out[blockIdx.x] = t1 - t0;
+        stop = 1;
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512));
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int CONT = 0, int NACC = 2>
 void run(unsigned long long* d, int iters) {
     const int smem = 128 * 128 * 4 + 256 * 128 * 4 + 2048;
-    cudaFuncSetAttribute(bench<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    bench<N, TS><<<1, 128, smem>>>(d, iters);
+    cudaFuncSetAttribute(bench<N, TS, CONT, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench<N, TS, CONT, NACC><<<1, 128, smem>>>(d, iters);
     cudaDeviceSynchronize();
     unsigned long long h = 0;
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    printf("N=%3d %s: %.1f cycles/MMA (%s)\n", N, TS ? "TS" : "SS", double(h) / iters,
+    printf("N=%3d %s cont=%d nacc=%d: %.1f cycles/MMA (%s)\n", N, TS ? "TS" : "SS", CONT, NACC, double(h) / iters,
            cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -78,8 +94,22 @@ int main() {
     run<32, false>(d, it);
     run<32, true>(d, it);
     run<64, false>(d, it);
+    run<64, true>(d, it);
+    run<96, false>(d, it);
+    run<96, true>(d, it);
     run<128, false>(d, it);
+    run<128, true>(d, it);
     run<256, false>(d, it);
     run<256, true>(d, it);
+    run<64, true, 1>(d, it);
+    run<64, true, 3>(d, it);
+    run<32, true, 3>(d, it);
+    run<64, false, 3>(d, it);
+    run<64, true, 0, 1>(d, it);
+    run<32, true, 0, 1>(d, it);
+    run<64, true, 0, 4>(d, it);
+    run<32, true, 0, 4>(d, it);
+    run<128, true, 0, 1>(d, it);
+    run<64, true, 3, 1>(d, it);
     return 0;
 }
