@@ -44,8 +44,8 @@ CONFIGS = {
     "cfg2": dict(N=8_800_000, K=1 << 18, nbits=2, mean_len=68, k=1000,
                  desc="synthetic MS MARCO v1-scale: 8.8M passages (~600M embeddings), 2^18 centroids, "
                       "nbits=2, k=1000, single-query latency"),
-    "cfg3": dict(N=8_800_000, K=1 << 18, nbits=1, mean_len=68, k=100,
-                 desc="same MS MARCO-scale index, nbits=1, k=100"),
+    "cfg3": dict(N=8_800_000, K=1 << 18, nbits=1, mean_len=68, k=100, batch=1024,
+                 desc="same MS MARCO-scale index, nbits=1, batched 1024-query throughput, k=100"),
     "cfg4": dict(N=2_400_000, K=1 << 16, nbits=2, mean_len=136, k=10,
                  desc="synthetic LoTTE-pooled-scale: 2.4M passages, 2^16 centroids, nbits=2, k=10, ndocs=256"),
     "small": dict(N=200_000, K=1 << 14, nbits=2, mean_len=68, k=1000, desc="smoke-size index"),
@@ -174,9 +174,26 @@ def run_reference(args, cfg):
     qs = P.generate_queries(h, max(args.steps + args.warmup, 1), qlen=QLEN, seed=1234)
     params = params_for(cfg)
     threads = os.cpu_count() or 1
-    lat = cpu_reference_run(h, qs, params, args.steps, args.warmup, threads)
-    total = sum(lat)
-    qps = args.steps / total
+    B = int(cfg.get("batch", 1))
+    if B > 1:
+        # throughput mode: `threads` workers x SearchOptions.threads=1;
+        # each step is a bounded sample of the batch (~1 s of CPU work)
+        ref = oracle.get("ref")
+        qb = P.generate_queries(h, threads * 4, qlen=QLEN, seed=1234)
+        ref.search_many(h, qb[:threads], params, 1, threads)  # warm-up (+ index build)
+        lat = []
+        for i in range(args.steps):
+            t0 = time.perf_counter()
+            ref.search_many(h, qb, params, 1, threads)
+            lat.append(time.perf_counter() - t0)
+        total = sum(lat)
+        qps = len(qb) * args.steps / total
+        sample = f"{len(qb)} queries per step, lir::search throughput mode ({threads} workers x threads=1)"
+    else:
+        lat = cpu_reference_run(h, qs, params, args.steps, args.warmup, threads)
+        total = sum(lat)
+        qps = args.steps / total
+        sample = f"{args.steps} sequential queries, lir::search latency mode, SearchOptions.threads={threads}"
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
@@ -184,8 +201,7 @@ def run_reference(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 generator, SURVEY.md §8d)",
         "config": config_block(cfg, params, args, 1),
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} sequential queries, lir::search latency mode, "
-                                   f"SearchOptions.threads={threads}"},
+                         "sample": sample},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -195,7 +211,9 @@ def config_block(cfg, params, args, world):
     return {"workload": f"{args.config}: {cfg['desc']}", "passages_per_gpu": cfg["N"],
             "passages_total": cfg["N"] * world, "centroids": cfg["K"], "nbits": cfg["nbits"], "dim": DIM,
             "query_tokens": QLEN, "k": params.k, "nprobe": params.nprobe, "t_cs": params.t_cs,
-            "ndocs": params.ndocs, "batch": 1, "l2_flush": "256 MiB write before every step (untimed)",
+            "ndocs": params.ndocs, "batch": cfg.get("batch", 1),
+            "lanes": args.lanes if cfg.get("batch", 1) > 1 else None,
+            "l2_flush": "256 MiB write before every step (untimed)",
             "score_mode": args.score_mode, "parallelism": f"passage-range shards x{world}",
             "shard_merge": args.shard_mode if world > 1 else None}
 
@@ -398,6 +416,180 @@ def run_plaid(args, cfg):
         dist.destroy_process_group()
 
 
+def run_plaid_batch(args, cfg):
+    """Throughput mode (BASELINE configs[2]): one step = one batch of B queries
+    through BatchSearcher (L concurrent lanes); value = queries / job time.
+    Multi-GPU: every rank searches its passage shard (shard-local), the [B][k]
+    results are all-gathered once per batch and merged per query."""
+    import torch
+
+    import paper_2205_09707_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("PLAID_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = 0
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    B = int(cfg["batch"])
+    h = make_index(cfg, rank)
+    params = params_for(cfg)
+    k = params.k
+    nb = 2  # distinct batches, alternated
+    if rank == 0:
+        qs = P.generate_queries(h, nb * B, qlen=QLEN, seed=1234).reshape(nb, B, QLEN, DIM)
+    else:
+        qs = np.zeros((nb, B, QLEN, DIM), dtype=np.float32)
+    dq = torch.from_numpy(qs).cuda()
+    if dist is not None:
+        dist.broadcast(dq, 0)
+        qs = dq.cpu().numpy()
+    idx = P.DeviceIndex.from_host_at(h, pid_base=rank * cfg["N"], device=local)
+    mode = P.ScoreMode.EXACT if args.score_mode == "exact" else P.ScoreMode.TENSOR
+    bs = P.BatchSearcher(idx, lanes=args.lanes, device=local, score_mode=mode)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sh = stream.cuda_stream
+    d_pids = torch.zeros(B * k, dtype=torch.int32, device="cuda")
+    d_scores = torch.zeros(B * k, dtype=torch.float32, device="cuda")
+    d_n = torch.zeros(B, dtype=torch.int64, device="cuda")
+    if dist is not None:
+        g_pids = torch.zeros(world * B * k, dtype=torch.int32, device="cuda")
+        g_scores = torch.zeros(world * B * k, dtype=torch.float32, device="cuda")
+        g_n = torch.zeros(world * B, dtype=torch.int64, device="cuda")
+        m_pids = torch.zeros(B * k, dtype=torch.int32, device="cuda")
+        m_scores = torch.zeros(B * k, dtype=torch.float32, device="cuda")
+        m_n = torch.zeros(B, dtype=torch.int64, device="cuda")
+        merger = P.Searcher(None, device=local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(i):
+        q = dq[i % nb]
+        bs.search_device(q.data_ptr(), B, QLEN, DIM, params, d_pids.data_ptr(), d_scores.data_ptr(),
+                         d_n.data_ptr(), stream=sh)
+        if dist is not None:
+            from paper_2205_09707_b200.sharded import _all_gather
+
+            _all_gather(g_pids, d_pids, None)
+            _all_gather(g_scores, d_scores, None)
+            _all_gather(g_n, d_n, None)
+            # shard g's query j list at g*B*k + j*k (stride B*k per shard); counts
+            # regrouped per query: cnt[j][g]
+            cnt = g_n.view(world, B).t().contiguous()
+            for j in range(B):
+                merger.merge_topk_device(g_pids.data_ptr() + 4 * j * k, g_scores.data_ptr() + 4 * j * k,
+                                         cnt.data_ptr() + 8 * j * world, world, B * k, k,
+                                         m_pids.data_ptr() + 4 * j * k, m_scores.data_ptr() + 4 * j * k,
+                                         m_n.data_ptr() + 8 * j, stream=sh)
+
+    for i in range(args.warmup):
+        flush.zero_()
+        step(i)
+    torch.cuda.synchronize()
+    bs.sync()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches = 0
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step(args.warmup + i)
+        ev[i][1].record(stream)
+        launches += bs.last_launches()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    bs.sync()
+    step_ms = torch.tensor([a.elapsed_time(b) for a, b in ev], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
+    step_ms = step_ms.cpu().numpy()
+    total_s = float(step_ms.sum()) / 1e3
+    value = B * args.steps / total_s
+
+    # e2e through the host API (H2D of the batch, D2H of [B][k] results inside)
+    e2e_lat = []
+    if world == 1:
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            bs.search(qs[i % nb], params)
+            e2e_lat.append(time.perf_counter() - t0)
+        e2e_value = B * args.steps / sum(e2e_lat)
+    else:
+        e2e_value = None
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # S_cq kernel alone (one single-query search with phase events) for the roofline
+    s1 = P.Searcher(idx, device=local, score_mode=mode, record_times=True)
+    sc_ms = []
+    for i in range(5):
+        flush.zero_()
+        torch.cuda.synchronize()
+        s1.search(qs[0][i], params)
+        sc_ms.append(s1.phase_ms()["scores"])
+    sc = float(np.median(sc_ms[1:]))
+    hbm_peak, _, peak_kind = measured_peaks()
+    K = cfg["K"]
+    ab = 512 * K + 128 * K + K // 8 + QLEN * DIM * 4
+    kname = "scores_tf32_kernel" if args.score_mode == "tensor" else "scores_exact_kernel"
+    roof = {"bound": "hbm", "kernel": kname, "achieved": ab / (sc * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ab / (sc * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+            "peak_kind": f"{peak_kind} (copy bandwidth, burst)", "algorithmic_bytes_per_launch": ab,
+            "mean_ms": sc, "share_of_step": sc * B / (1e3 * total_s / args.steps),
+            "note": "one S_cq launch per query (single-query kernel; the batch's launches serialise)"}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            import oracle
+
+            threads = os.cpu_count() or 1
+            ref = oracle.get("ref")
+            ns = max(threads, min(256, int(args.cpu_seconds / (0.5 / threads))))
+            ref.search_many(h, qs[0][:threads], params, 1, threads)  # index build + warm-up
+            t0 = time.perf_counter()
+            ref.search_many(h, qs[0][:ns], params, 1, threads)
+            wall = time.perf_counter() - t0
+            cpu = {"value": ns / wall, "unit": "queries/s", "cores": threads, "kind": "reference",
+                   "sample": f"{ns} queries of the batch, lir::search throughput mode ({threads} workers x "
+                             f"SearchOptions.threads=1)"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
+        "p50_ms": float(np.median(step_ms)), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 generator, SURVEY.md §8d)",
+        "config": config_block(cfg, params, args, world),
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": B * QLEN * DIM * 4,
+                "d2h_bytes_per_step": B * (k * 8 + 8)},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -408,13 +600,19 @@ def main():
     ap.add_argument("--score-mode", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--lanes", type=int, default=8, help="throughput mode: concurrent searcher lanes")
+    ap.add_argument("--batch", type=int, default=0, help="queries per step (default: the config's)")
     ap.add_argument("--shard-mode", default="global-exact", choices=["global-exact", "shard-local"],
                     help="multi-GPU exchange (SURVEY.md §8e): global cuts after stages 2 and 3, or top-k merge only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.get("batch", 1) > 1:
+        run_plaid_batch(args, cfg)
     else:
         run_plaid(args, cfg)
 

@@ -190,6 +190,27 @@ plaid_status plaid_merge_topk_device(plaid_searcher* s, const uint32_t* d_pids,
                                      uint64_t shards, uint64_t stride, uint64_t k, uint32_t* d_out_pids,
                                      float* d_out_scores, uint64_t* d_out_n, uint64_t stream);
 
+/* ---- throughput mode (BASELINE configs[2]: batched queries) ---------------------------
+ * `lanes` searchers (own CUDA stream + scratch each) over one index; query j of
+ * a batch runs on lane j mod lanes, so the stages of different queries overlap
+ * on the GPU.  Results are identical to plaid_search per query. */
+typedef struct plaid_batch plaid_batch;
+plaid_status plaid_batch_create(plaid_index* index, int device, const plaid_searcher_config* cfg, uint32_t lanes,
+                                plaid_batch** out);
+void plaid_batch_destroy(plaid_batch* b);
+/* Host buffers: q [nq][rows][dim]; out_pids / out_scores [nq][k]; out_n [nq].
+ * Every query is validated before any work (types.cpp:61-99).  Synchronous. */
+plaid_status plaid_batch_search(plaid_batch* b, const float* q, uint64_t nq, uint64_t rows, uint64_t dim,
+                                const plaid_params* params, uint32_t* out_pids, float* out_scores, uint64_t* out_n);
+/* Device buffers, forked from and joined back to `stream` (0 = lane 0's);
+ * not synchronised (query norms are checked on the device, reported by
+ * plaid_batch_sync). */
+plaid_status plaid_batch_search_device(plaid_batch* b, const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim,
+                                       const plaid_params* params, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
+                                       uint64_t stream);
+plaid_status plaid_batch_sync(plaid_batch* b);
+uint64_t plaid_batch_last_launches(const plaid_batch* b);
+
 /* ---- global-exact passage-sharded search ----------------------------
  * The reference searches one index (pipeline.cpp:232-283); a passage-range
  * shard alone cannot know the global stage-2 (top-ndocs) and stage-3

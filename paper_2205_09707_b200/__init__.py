@@ -5,14 +5,14 @@ include/plaid.h); this package is the Python mirror of the reference's
 interface over that ABI, plus the host-side index container and the
 deterministic synthetic index generator used by tests and the bench.
 """
-from .api import (CandidateSet, DeviceIndex, ErrorCode, PlaidError, ScoreMode, SearchOptions,
+from .api import (BatchSearcher, CandidateSet, DeviceIndex, ErrorCode, PlaidError, ScoreMode, SearchOptions,
                   SearchParams, SearchResult, Searcher, StageTrace, default_params_for_k,
                   lut_build, pack_residual, search, stage3_width, validate_params, validate_query)
 from .hostindex import HostIndex, build_inverted_list, generate_index, generate_queries, quantizer
 
 __all__ = [
     "CandidateSet", "DeviceIndex", "ErrorCode", "PlaidError", "ScoreMode", "SearchOptions",
-    "SearchParams", "SearchResult", "Searcher", "StageTrace", "default_params_for_k", "lut_build",
+    "BatchSearcher", "SearchParams", "SearchResult", "Searcher", "StageTrace", "default_params_for_k", "lut_build",
     "pack_residual", "search", "stage3_width", "validate_params", "validate_query", "HostIndex",
     "build_inverted_list", "generate_index", "generate_queries", "quantizer",
 ]

@@ -69,6 +69,15 @@ SIGNATURES = {
                                      u32p, f32p, u64p, C.POINTER(Trace)]),
     "plaid_search_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                       C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "plaid_batch_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(SearcherConfig), C.c_uint32,
+                                     C.POINTER(C.c_void_p)]),
+    "plaid_batch_destroy": (None, [C.c_void_p]),
+    "plaid_batch_search": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(Params),
+                                     u32p, f32p, u64p]),
+    "plaid_batch_search_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                            C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "plaid_batch_sync": (C.c_int, [C.c_void_p]),
+    "plaid_batch_last_launches": (C.c_uint64, [C.c_void_p]),
     "plaid_shard_phase1_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(Params),
                                             C.c_void_p, C.c_uint64, C.c_uint64]),
     "plaid_shard_phase2_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,

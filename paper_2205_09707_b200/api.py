@@ -429,6 +429,59 @@ class Searcher:
         return oi[: n.value].copy(), os_[: n.value].copy()
 
 
+class BatchSearcher:
+    """Throughput mode (BASELINE configs[2], batched queries): `lanes`
+    searchers with their own streams over one index; query j runs on lane
+    j mod lanes so different queries' stages overlap (include/plaid.h)."""
+
+    def __init__(self, index: DeviceIndex, lanes: int = 8, device: int = 0,
+                 score_mode: ScoreMode = ScoreMode.TENSOR):
+        self.index = index
+        cfg = N.SearcherConfig(int(score_mode), 0, 0, 0)
+        out = C.c_void_p()
+        _check(N.load().plaid_batch_create(index._h, device, C.byref(cfg), int(lanes), C.byref(out)))
+        self._h = out
+        self.lanes = int(lanes)
+
+    def close(self) -> None:
+        if self._h:
+            N.load().plaid_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, q: np.ndarray, params: SearchParams, options: SearchOptions = SearchOptions()):
+        """q: [nq, rows, dim] float32 (host).  Returns a list of CandidateSet."""
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        if q.ndim != 3:
+            raise PlaidError(ErrorCode.DimensionMismatch, "queries must be nq x rows x dim")
+        nq, rows, dim = q.shape
+        k = max(int(params.k), 1)
+        ids = np.zeros((nq, k), dtype=np.uint32)
+        sc = np.zeros((nq, k), dtype=np.float32)
+        n = np.zeros(nq, dtype=np.uint64)
+        p = params._c(options.disable_filter)
+        _check(N.load().plaid_batch_search(self._h, N.ptr(q, C.c_float), nq, rows, dim, C.byref(p),
+                                           N.ptr(ids, C.c_uint32), N.ptr(sc, C.c_float), N.ptr(n, C.c_uint64)))
+        return [CandidateSet(ids[j, : n[j]].copy(), sc[j, : n[j]].copy()) for j in range(nq)]
+
+    def search_device(self, d_q: int, nq: int, rows: int, dim: int, params: SearchParams, d_pids: int,
+                      d_scores: int, d_n: int, stream: int = 0, options: SearchOptions = SearchOptions()) -> None:
+        p = params._c(options.disable_filter)
+        _check(N.load().plaid_batch_search_device(self._h, d_q, nq, rows, dim, C.byref(p), d_pids, d_scores, d_n,
+                                                  stream))
+
+    def sync(self) -> None:
+        _check(N.load().plaid_batch_sync(self._h))
+
+    def last_launches(self) -> int:
+        return int(N.load().plaid_batch_last_launches(self._h))
+
+
 def search(index: DeviceIndex, q: np.ndarray, params: SearchParams,
            options: SearchOptions = SearchOptions(), searcher: Optional[Searcher] = None) -> SearchResult:
     """lir::search (pipeline.hpp:86-87).  Creates a throwaway Searcher unless

@@ -15,6 +15,9 @@ struct plaid_index {
 struct plaid_searcher {
     std::unique_ptr<plaid::Searcher> impl;
 };
+struct plaid_batch {
+    std::unique_ptr<plaid::BatchSearcher> impl;
+};
 
 namespace {
 
@@ -260,6 +263,61 @@ plaid_status plaid_search_device(plaid_searcher* s, const float* d_q, uint64_t n
                                reinterpret_cast<cudaStream_t>(stream));
     });
 }
+
+plaid_status plaid_batch_create(plaid_index* index, int device, const plaid_searcher_config* cfg, uint32_t lanes,
+                                plaid_batch** out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        need(index, "index");
+        const plaid_searcher_config c = cfg ? *cfg : default_config();
+        auto* h = new plaid_batch();
+        try {
+            h->impl = std::make_unique<plaid::BatchSearcher>(index->impl.get(), device, c, lanes);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+void plaid_batch_destroy(plaid_batch* b) { delete b; }
+
+plaid_status plaid_batch_search(plaid_batch* b, const float* q, uint64_t nq, uint64_t rows, uint64_t dim,
+                                const plaid_params* params, uint32_t* out_pids, float* out_scores, uint64_t* out_n) {
+    return guarded([&] {
+        need(b, "batch");
+        need(params, "params");
+        if (nq) {
+            need(q, "q");
+            need(out_pids, "out_pids");
+            need(out_scores, "out_scores");
+            need(out_n, "out_n");
+        }
+        b->impl->search(q, nq, rows, dim, *params, out_pids, out_scores, out_n);
+    });
+}
+
+plaid_status plaid_batch_search_device(plaid_batch* b, const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim,
+                                       const plaid_params* params, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
+                                       uint64_t stream) {
+    return guarded([&] {
+        need(b, "batch");
+        need(params, "params");
+        b->impl->search_device(d_q, nq, rows, dim, *params, d_pids, d_scores, d_n,
+                               reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+plaid_status plaid_batch_sync(plaid_batch* b) {
+    return guarded([&] {
+        need(b, "batch");
+        b->impl->sync();
+    });
+}
+
+uint64_t plaid_batch_last_launches(const plaid_batch* b) { return b ? b->impl->last_launches() : 0; }
 
 plaid_status plaid_shard_phase1_device(plaid_searcher* s, const float* d_q, uint64_t rows, uint64_t dim,
                                        const plaid_params* params, uint64_t* d_x2, uint64_t stride2,

@@ -53,18 +53,6 @@ uint32_t np_bucket(uint64_t nprobe) {
     return b;
 }
 
-struct DeviceGuard {
-    int prev = 0;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) PLAID_CUDA(cudaSetDevice(dev));
-    }
-    ~DeviceGuard() {
-        int cur = 0;
-        cudaGetDevice(&cur);
-        if (cur != prev) cudaSetDevice(prev);
-    }
-};
 
 // Counter slots in Searcher::counters_.
 enum : int {
@@ -1076,6 +1064,109 @@ void Searcher::merge_topk(const uint32_t* pids, const float* scores, const uint6
     d2h(out_scores, os.p, n, stream_);
     PLAID_CUDA(cudaStreamSynchronize(stream_));
     *out_n = n;
+}
+
+// ---------------------------------------------------------------- throughput mode
+BatchSearcher::BatchSearcher(DeviceIndex* index, int device, const plaid_searcher_config& cfg, uint32_t lanes)
+    : index_(index), device_(device) {
+    if (!index) fail(PLAID_INVALID_PARAMS, "batch searcher needs an index");
+    if (lanes == 0 || lanes > 64) fail(PLAID_INVALID_PARAMS, "lanes must be in [1, 64]");
+    DeviceGuard g(device_);
+    plaid_searcher_config c = cfg;
+    c.record_times = 0;
+    for (uint32_t l = 0; l < lanes; ++l) {
+        lanes_.push_back(std::make_unique<Searcher>(index, device, c));
+        streams_.push_back(lanes_.back()->stream());
+        cudaEvent_t e;
+        PLAID_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        joins_.push_back(e);
+    }
+    PLAID_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+}
+
+BatchSearcher::~BatchSearcher() {
+    DeviceGuard g(device_);
+    cudaDeviceSynchronize();
+    for (auto e : joins_) cudaEventDestroy(e);
+    if (fork_) cudaEventDestroy(fork_);
+    if (h_q_) cudaFreeHost(h_q_);
+    if (h_pids_) cudaFreeHost(h_pids_);
+    if (h_scores_) cudaFreeHost(h_scores_);
+    if (h_n_) cudaFreeHost(h_n_);
+}
+
+void BatchSearcher::search_device(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim, const plaid_params& p,
+                                  uint32_t* d_pids, float* d_scores, uint64_t* d_n, cudaStream_t st) {
+    DeviceGuard g(device_);
+    if (!st) st = streams_[0];
+    const uint64_t L = lanes_.size();
+    PLAID_CUDA(cudaEventRecord(fork_, st));
+    for (uint64_t l = 0; l < L && l < nq; ++l)
+        if (streams_[l] != st) PLAID_CUDA(cudaStreamWaitEvent(streams_[l], fork_, 0));
+    uint64_t launches = 0;
+    for (uint64_t j = 0; j < nq; ++j) {
+        Searcher& s = *lanes_[j % L];
+        s.search_device(d_q + j * rows * dim, 1, rows, dim, p, d_pids + j * p.k, d_scores + j * p.k, d_n + j,
+                        streams_[j % L]);
+        launches += s.last_launches();
+    }
+    for (uint64_t l = 0; l < L && l < nq; ++l) {
+        if (streams_[l] == st) continue;
+        PLAID_CUDA(cudaEventRecord(joins_[l], streams_[l]));
+        PLAID_CUDA(cudaStreamWaitEvent(st, joins_[l], 0));
+    }
+    last_launches_ = launches;
+}
+
+void BatchSearcher::search(const float* q, uint64_t nq, uint64_t rows, uint64_t dim, const plaid_params& p,
+                           uint32_t* out_pids, float* out_scores, uint64_t* out_n) {
+    const IndexView& ix = index_->view();
+    for (uint64_t j = 0; j < nq; ++j) out_n[j] = 0;
+    for (uint64_t j = 0; j < nq; ++j) validate_query_host(q + j * rows * dim, rows, dim, ix.dim);
+    validate_params_host(p, ix.K);
+    if (rows > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32 query tokens");
+    if (nq == 0) return;
+    DeviceGuard g(device_);
+    const uint64_t nqf = nq * rows * dim, nout = nq * p.k;
+    q_.ensure(nqf);
+    pids_.ensure(nout);
+    scores_.ensure(nout);
+    n_.ensure(nq);
+    if (hq_cap_ < nqf) {
+        if (h_q_) cudaFreeHost(h_q_);
+        h_q_ = nullptr;
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_q_), nqf * sizeof(float)));
+        hq_cap_ = nqf;
+    }
+    if (ho_cap_ < nout + nq) {
+        if (h_pids_) cudaFreeHost(h_pids_);
+        if (h_scores_) cudaFreeHost(h_scores_);
+        if (h_n_) cudaFreeHost(h_n_);
+        h_pids_ = nullptr, h_scores_ = nullptr, h_n_ = nullptr;
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_pids_), (nout + nq) * sizeof(uint32_t)));
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_scores_), (nout + nq) * sizeof(float)));
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_n_), nq * sizeof(uint64_t)));
+        ho_cap_ = nout + nq;
+    }
+    std::memcpy(h_q_, q, nqf * sizeof(float));
+    cudaStream_t st = streams_[0];
+    PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, nqf * sizeof(float), cudaMemcpyHostToDevice, st));
+    search_device(q_.p, nq, rows, dim, p, pids_.p, scores_.p, n_.p, st);
+    PLAID_CUDA(cudaMemcpyAsync(h_n_, n_.p, nq * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    PLAID_CUDA(cudaMemcpyAsync(h_pids_, pids_.p, nout * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    PLAID_CUDA(cudaMemcpyAsync(h_scores_, scores_.p, nout * sizeof(float), cudaMemcpyDeviceToHost, st));
+    PLAID_CUDA(cudaStreamSynchronize(st));
+    sync();
+    for (uint64_t j = 0; j < nq; ++j) {
+        const uint64_t m = h_n_[j];
+        out_n[j] = m;
+        std::memcpy(out_pids + j * p.k, h_pids_ + j * p.k, m * sizeof(uint32_t));
+        std::memcpy(out_scores + j * p.k, h_scores_ + j * p.k, m * sizeof(float));
+    }
+}
+
+void BatchSearcher::sync() {
+    for (auto& s : lanes_) s->sync();  // also reports device-side query validation failures
 }
 
 }  // namespace plaid

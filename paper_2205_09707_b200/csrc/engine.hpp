@@ -33,6 +33,20 @@ private:
 void cuda_check(cudaError_t e, const char* what);
 #define PLAID_CUDA(x) ::plaid::cuda_check((x), #x)
 
+// Makes `dev` current for the scope.
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) PLAID_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != prev) cudaSetDevice(prev);
+    }
+};
+
 // Host-side validation mirroring types.cpp / index.cpp.
 void validate_query_host(const float* q, uint64_t rows, uint64_t dim, uint64_t index_dim);
 void validate_params_host(const plaid_params& p, uint64_t num_centroids);
@@ -103,6 +117,7 @@ public:
     void trace_counters_device(uint64_t* d_out, cudaStream_t st);
     void sync();
     uint64_t last_launches() const { return last_launches_; }
+    cudaStream_t stream() const { return stream_; }
     void phase_ms(double* out);
 
     // Per-stage entry points (host buffers).
@@ -186,6 +201,45 @@ private:
     alignas(64) unsigned char tmap_[128];   // CUtensorMap over the centroids
     // S_cq + row max + keep bits + per-warp top lists, in the configured mode
     uint32_t launch_scores(const float* d_q, uint32_t rows, float t_cs, uint32_t npb, cudaStream_t st);
+};
+
+// Throughput mode (BASELINE configs[2]: batched queries): L lanes, each a
+// full Searcher with its own stream and scratch over the shared index.
+// Query j runs on lane j mod L, so the latency-bound stage kernels of
+// different queries overlap on the GPU; a batch forks from and joins back
+// to the caller's stream with events.
+class BatchSearcher {
+public:
+    BatchSearcher(DeviceIndex* index, int device, const plaid_searcher_config& cfg, uint32_t lanes);
+    ~BatchSearcher();
+    uint32_t lanes() const { return uint32_t(lanes_.size()); }
+    // Host buffers: Q [nq][rows][dim], outputs [nq][k] + counts [nq].  Each
+    // query is validated host-side first (types.cpp:61-99 order).
+    void search(const float* q, uint64_t nq, uint64_t rows, uint64_t dim, const plaid_params& p,
+                uint32_t* out_pids, float* out_scores, uint64_t* out_n);
+    // Device buffers, enqueued on `st` (0 = lane 0's stream); not synchronised.
+    void search_device(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim, const plaid_params& p,
+                       uint32_t* d_pids, float* d_scores, uint64_t* d_n, cudaStream_t st);
+    void sync();
+    uint64_t last_launches() const { return last_launches_; }
+
+private:
+    DeviceIndex* index_;
+    int device_;
+    std::vector<std::unique_ptr<Searcher>> lanes_;
+    std::vector<cudaStream_t> streams_;
+    std::vector<cudaEvent_t> joins_;
+    cudaEvent_t fork_ = nullptr;
+    uint64_t last_launches_ = 0;
+    DevBuf<float> q_;
+    DevBuf<uint32_t> pids_;
+    DevBuf<float> scores_;
+    DevBuf<uint64_t> n_;
+    float* h_q_ = nullptr;
+    uint32_t* h_pids_ = nullptr;
+    float* h_scores_ = nullptr;
+    uint64_t* h_n_ = nullptr;
+    uint64_t hq_cap_ = 0, ho_cap_ = 0;
 };
 
 }  // namespace plaid

@@ -287,3 +287,25 @@ def test_global_exact_shards_bit_exact(port, G):
     ids, sc = search_local_shards(ss, dq, p, N, options=P.SearchOptions(disable_filter=True))
     eids, esc, _ = port.search(whole, qs[0], p, disable_filter=True)
     assert np.array_equal(ids, eids) and np.array_equal(bits(sc), bits(esc))
+
+
+@pytest.mark.parametrize("lanes", [1, 3, 8])
+def test_batch_searcher_bit_exact(small, port, lanes):
+    """Throughput mode: every query of a batch spread over `lanes` concurrent
+    streams returns exactly the reference's single-query result."""
+    h, qs, idx, _ = small
+    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.EXACT)
+    qb = np.concatenate([qs, qs[::-1], qs[:3]])
+    for k in (10, 1000):
+        p = P.default_params_for_k(k)
+        got = b.search(qb, p)
+        assert len(got) == len(qb)
+        for q, g in zip(qb, got):
+            ids, sc, _ = port.search(h, q, p)
+            assert np.array_equal(g.passage_ids, ids)
+            assert np.array_equal(bits(g.scores), bits(sc))
+    # one bad query rejects the whole batch before any work (types.cpp:61-72)
+    bad = qb.copy()
+    bad[2, 0, :] *= 2.0
+    with pytest.raises(P.PlaidError):
+        b.search(bad, P.default_params_for_k(10))
