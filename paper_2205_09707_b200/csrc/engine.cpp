@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -476,6 +477,18 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
     const uint32_t warps = launch_scores(d_q, rows, p.t_cs, npb, st);
     record(1, st, times);
+    front_after_scores(rows, p, warps, st, times);
+}
+
+// Stage 1 after S_cq (top-nprobe merge, candidate generation) and stage 2.
+void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t warps, cudaStream_t st,
+                                  bool times) {
+    const IndexView& ix = index_->view();
+    const uint64_t K = ix.K, N = ix.N;
+    uint64_t* c = counters_.p;
+    uint32_t* bitmap = bitmap_.p;
+    uint32_t* owners = bitmap_.p + (N + 31) / 32;
+    const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
     uint64_t nsel;
     if (p.nprobe == K) {
         launch::iota(sel_.p, K, st);
@@ -629,6 +642,48 @@ void Searcher::shard_phase3(const uint64_t* d_g3, uint64_t shards, uint32_t* d_p
                                  uint32_t(index_->pid_base()), st);
     enqueue_back(pending_q_, pending_rows_, p, d_pids, d_scores, d_n, st, times);
     phase_ = 0;
+    PLAID_CUDA(cudaGetLastError());
+    last_launches_ = launch::launches();
+}
+
+// ---- batched S_cq (BatchSearcher): the query's prologue on this lane's
+// stream, then the shared S_cq launch writes this lane's S / keep bits /
+// partial lists / bounds, then the rest of the pipeline.
+bool Searcher::batch_scores_ok(const plaid_params& p, uint64_t rows, uint64_t dim) const {
+    const IndexView& ix = index_->view();
+    return tensor_ && dim == ix.dim && rows <= 32 && p.nprobe < ix.K && p.nprobe <= 8;
+}
+
+void Searcher::batch_prepare(const float* d_q, uint64_t rows, uint64_t dim, const plaid_params& p,
+                             cudaStream_t st) {
+    require_index();
+    const IndexView& ix = index_->view();
+    if (dim != ix.dim) fail(PLAID_DIMENSION_MISMATCH, "query dim does not match index dim");
+    if (rows == 0) fail(PLAID_INVALID_PARAMS, "query must contain at least one token");
+    if (rows > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32 query tokens");
+    validate_params_host(p, ix.K);
+    DeviceGuard g(device_);
+    ensure_param_buffers(p);
+    launch::reset_launches();
+    launch::validate_query(d_q, uint32_t(rows), uint32_t(dim), status_.p, st);
+    PLAID_CUDA(cudaMemsetAsync(zero_.p, 0, zero_.n * sizeof(uint32_t), st));
+}
+
+void Searcher::batch_targets(TfOut& out, uint32_t qi, const float* d_q) {
+    out.Q[qi] = d_q;
+    out.S[qi] = scores_.p;
+    out.keep[qi] = keep_.p;
+    out.partial[qi] = partial_.p;
+    out.gthr[qi] = reinterpret_cast<uint32_t*>(counters_.p + kGthr);
+}
+
+void Searcher::batch_finish(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t warps, uint32_t* d_pids,
+                            float* d_scores, uint64_t* d_n, cudaStream_t st) {
+    DeviceGuard g(device_);
+    pending_rows_ = rows;
+    front_after_scores(rows, p, warps, st, false);
+    enqueue_stage3(p, st, false);
+    enqueue_back(d_q, rows, p, d_pids, d_scores, d_n, st, false);
     PLAID_CUDA(cudaGetLastError());
     last_launches_ = launch::launches();
 }
@@ -1082,12 +1137,23 @@ BatchSearcher::BatchSearcher(DeviceIndex* index, int device, const plaid_searche
         joins_.push_back(e);
     }
     PLAID_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+    for (uint32_t l = 0; l < lanes; ++l) {
+        cudaEvent_t e;
+        PLAID_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ready_.push_back(e);
+        PLAID_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        sdone_.push_back(e);
+    }
+    PLAID_CUDA(cudaStreamCreateWithFlags(&sstream_, cudaStreamNonBlocking));
 }
 
 BatchSearcher::~BatchSearcher() {
     DeviceGuard g(device_);
     cudaDeviceSynchronize();
     for (auto e : joins_) cudaEventDestroy(e);
+    for (auto e : ready_) cudaEventDestroy(e);
+    for (auto e : sdone_) cudaEventDestroy(e);
+    if (sstream_) cudaStreamDestroy(sstream_);
     if (fork_) cudaEventDestroy(fork_);
     if (h_q_) cudaFreeHost(h_q_);
     if (h_pids_) cudaFreeHost(h_pids_);
@@ -1104,11 +1170,42 @@ void BatchSearcher::search_device(const float* d_q, uint64_t nq, uint64_t rows, 
     for (uint64_t l = 0; l < L && l < nq; ++l)
         if (streams_[l] != st) PLAID_CUDA(cudaStreamWaitEvent(streams_[l], fork_, 0));
     uint64_t launches = 0;
-    for (uint64_t j = 0; j < nq; ++j) {
-        Searcher& s = *lanes_[j % L];
-        s.search_device(d_q + j * rows * dim, 1, rows, dim, p, d_pids + j * p.k, d_scores + j * p.k, d_n + j,
-                        streams_[j % L]);
-        launches += s.last_launches();
+    const bool batched = L >= 2 && lanes_[0]->batch_scores_ok(p, rows, dim);
+    if (batched) {
+        // pairs of queries share one S_cq pass over C (scores_tensor_batch) on
+        // the scores stream; each lane waits for it, then runs the rest
+        PLAID_CUDA(cudaStreamWaitEvent(sstream_, fork_, 0));
+        const uint32_t npb = np_bucket(p.nprobe);
+        const uint64_t step = kMaxScoreBatch;
+        for (uint64_t j0 = 0; j0 < nq; j0 += step) {
+            const uint32_t qb = uint32_t(std::min<uint64_t>(step, nq - j0));
+            TfOut out{};
+            for (uint32_t qi = 0; qi < qb; ++qi) {
+                const uint64_t j = j0 + qi, l = j % L;
+                const float* q = d_q + j * rows * dim;
+                lanes_[l]->batch_prepare(q, rows, dim, p, streams_[l]);
+                lanes_[l]->batch_targets(out, qi, q);
+                PLAID_CUDA(cudaEventRecord(ready_[l], streams_[l]));
+                PLAID_CUDA(cudaStreamWaitEvent(sstream_, ready_[l], 0));
+            }
+            const uint32_t warps = launch::scores_tensor_batch(lanes_[0]->tensor_map(), index_->view(), out, qb,
+                                                               uint32_t(rows), p.t_cs, npb, sstream_);
+            PLAID_CUDA(cudaEventRecord(sdone_[(j0 / step) % sdone_.size()], sstream_));
+            for (uint32_t qi = 0; qi < qb; ++qi) {
+                const uint64_t j = j0 + qi, l = j % L;
+                PLAID_CUDA(cudaStreamWaitEvent(streams_[l], sdone_[(j0 / step) % sdone_.size()], 0));
+                lanes_[l]->batch_finish(d_q + j * rows * dim, uint32_t(rows), p, warps, d_pids + j * p.k,
+                                        d_scores + j * p.k, d_n + j, streams_[l]);
+                launches += lanes_[l]->last_launches() + (qi == 0);
+            }
+        }
+    } else {
+        for (uint64_t j = 0; j < nq; ++j) {
+            Searcher& s = *lanes_[j % L];
+            s.search_device(d_q + j * rows * dim, 1, rows, dim, p, d_pids + j * p.k, d_scores + j * p.k, d_n + j,
+                            streams_[j % L]);
+            launches += s.last_launches();
+        }
     }
     for (uint64_t l = 0; l < L && l < nq; ++l) {
         if (streams_[l] == st) continue;

@@ -115,6 +115,13 @@ public:
     void shard_phase3(const uint64_t* d_g3, uint64_t shards, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
                       cudaStream_t st);
     void trace_counters_device(uint64_t* d_out, cudaStream_t st);
+    // Batched S_cq (BatchSearcher): prologue, this lane's S_cq outputs, the rest.
+    bool batch_scores_ok(const plaid_params& p, uint64_t rows, uint64_t dim) const;
+    void batch_prepare(const float* d_q, uint64_t rows, uint64_t dim, const plaid_params& p, cudaStream_t st);
+    void batch_targets(TfOut& out, uint32_t qi, const float* d_q);
+    void batch_finish(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t warps, uint32_t* d_pids,
+                      float* d_scores, uint64_t* d_n, cudaStream_t st);
+    const void* tensor_map() const { return tmap_; }
     void sync();
     uint64_t last_launches() const { return last_launches_; }
     cudaStream_t stream() const { return stream_; }
@@ -151,6 +158,7 @@ private:
     void enqueue(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
                  float* d_scores, uint64_t* d_n, cudaStream_t st, bool times);
     void enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st, bool times);
+    void front_after_scores(uint32_t rows, const plaid_params& p, uint32_t warps, cudaStream_t st, bool times);
     void enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times);
     void enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,
                       uint64_t* d_n, cudaStream_t st, bool times);
@@ -228,8 +236,9 @@ private:
     int device_;
     std::vector<std::unique_ptr<Searcher>> lanes_;
     std::vector<cudaStream_t> streams_;
-    std::vector<cudaEvent_t> joins_;
+    std::vector<cudaEvent_t> joins_, ready_, sdone_;
     cudaEvent_t fork_ = nullptr;
+    cudaStream_t sstream_ = nullptr;  // batched S_cq launches
     uint64_t last_launches_ = 0;
     DevBuf<float> q_;
     DevBuf<uint32_t> pids_;

@@ -50,33 +50,47 @@
 namespace plaid {
 namespace {
 
-constexpr int kRaw = 9;                      // TMA ring depth
-constexpr int kOps = 6;                      // TMEM operand slots
 constexpr uint32_t kChunkBytes = 128 * 128;  // one TMA box: 32 centroids x 128 fp32 (16 KB contiguous in HBM)
-constexpr uint32_t kQChunkBytes = 64 * 128;  // [Q_hi; Q_lo] 64 rows x 32 fp32
 constexpr int kThreads = 512;
 constexpr int kEpiWarps = 8;                 // warps 8..15
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAccCols = 64;            // 32 hi-product + 32 lo-product columns
-constexpr uint32_t kOpsCol0 = 128;           // first operand-slot column
 constexpr int kDim = 128;
 constexpr int kChunks = kDim / 32;
-
-// shared-memory carve-up (offsets from a 1024-B aligned base)
-constexpr uint32_t kOffRaw = 0;
-constexpr uint32_t kOffQ = kOffRaw + kRaw * kChunkBytes;
-constexpr uint32_t kOffTr = kOffQ + kChunks * kQChunkBytes;  // 4 warps x 32 x 33 floats
-constexpr uint32_t kOffBar = kOffTr + kEpiWarps * 32 * 33 * 4;
-constexpr uint32_t kNumBars = 2 * kRaw + 2 * kOps + 4;
-constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;  // tmem slot (16 B) + CTA bounds (128 B)
-constexpr uint32_t kSmemBytes = kOffMisc + 16 + 128 + 1024;  // + alignment slack
 
 // kind::tf32 instruction descriptors: D f32, A/B tf32, both K-major, M=128.
 constexpr uint32_t idesc_tf32(uint32_t n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
-constexpr uint32_t kIdesc64 = idesc_tf32(64);
-constexpr uint32_t kIdesc32 = idesc_tf32(32);
+
+// Per-batch-width layout: QB queries share one pass over C.  B operand rows
+// [0, 32 QB) = Q_hi of query r / 32, [32 QB, 64 QB) = Q_lo; accumulator
+// columns [32 qi, +32) = C_hi.Q_hi + C_lo.Q_hi of query qi and
+// [32 QB + 32 qi, +32) = C_hi.Q_lo of query qi.
+template <int QB>
+struct TfCfg {
+    // TMA ring depth.  Box gb (tile gb / 4, lane quarter gb % 4) shares its
+    // slot with box gb - kRaw; a converter warp can reach box gb once the MMA
+    // has consumed tile gb / 4 - 2, so box gb - kRaw must belong to that tile
+    // or earlier (else a parity wait two phases behind passes on a stale
+    // box): kRaw = 8 (same quarter) or kRaw >= 9.  7 is NOT safe.
+    static constexpr int kRaw = QB == 1 ? 9 : 8;
+    static constexpr int kOps = QB == 1 ? 6 : 4;        // TMEM operand slots (64 columns each)
+    static constexpr uint32_t kQChunkBytes = 64 * QB * 128;
+    static constexpr uint32_t kAccCols = 64 * QB;       // per accumulator (two, double-buffered)
+    static constexpr uint32_t kOpsCol0 = 2 * kAccCols;  // first operand-slot column
+    static_assert(kOpsCol0 + 64 * kOps <= kTmemCols, "TMEM budget");
+    // shared-memory carve-up (offsets from a 1024-B aligned base)
+    static constexpr uint32_t kOffRaw = 0;
+    static constexpr uint32_t kOffQ = kOffRaw + kRaw * kChunkBytes;
+    static constexpr uint32_t kOffTr = kOffQ + kChunks * kQChunkBytes;  // 8 warps x 32 x 33 floats
+    static constexpr uint32_t kOffBar = kOffTr + kEpiWarps * 32 * 33 * 4;
+    static constexpr uint32_t kNumBars = 2 * kRaw + 2 * kOps + 4;
+    static constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;  // tmem slot (16 B) + CTA bounds (128 B per query)
+    static constexpr uint32_t kSmemBytes = kOffMisc + 16 + 128 * QB + 1024;  // + alignment slack
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+    static constexpr uint32_t kIdescAll = idesc_tf32(64 * QB);  // C_hi . [Q_hi | Q_lo] of every query
+    static constexpr uint32_t kIdescHi = idesc_tf32(32 * QB);   // C_lo . Q_hi of every query
+};
 
 // Debug timeline (PLAID_TF32_DBG=16): globaltimer stamps of CTA 0's pipeline
 // events and every CTA's begin/end (read back with plaid_debug_tf32_trace).
@@ -192,11 +206,15 @@ __device__ __forceinline__ uint32_t split_lo(uint32_t x) {
     return (__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u;
 }
 
-template <int NP>
+template <int NP, int QB>
 __global__ void __launch_bounds__(kThreads, 1)
-scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const float* __restrict__ Q,
-                   uint32_t rows, float t_cs, float* __restrict__ S, uint32_t* __restrict__ keep_bits,
-                   uint64_t* __restrict__ partial, uint32_t* __restrict__ gthr, uint32_t dbg) {
+scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const __grid_constant__ TfOut out,
+                   uint32_t rows, float t_cs, uint32_t dbg) {
+    using Cf = TfCfg<QB>;
+    constexpr int kRaw = Cf::kRaw, kOps = Cf::kOps;
+    constexpr uint32_t kOffRaw = Cf::kOffRaw, kOffQ = Cf::kOffQ, kOffTr = Cf::kOffTr, kOffBar = Cf::kOffBar,
+                       kOffMisc = Cf::kOffMisc, kQChunkBytes = Cf::kQChunkBytes, kAccCols = Cf::kAccCols,
+                       kOpsCol0 = Cf::kOpsCol0;
     dev::pdl_wait();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -210,7 +228,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kRaw + 2 * kOps + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kRaw + 2 * kOps + 2 + a); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffMisc);
-    // CTA-wide per-token bound (ordered float bits, 0 = none)
+    // CTA-wide per-token bound per query, cthr[32 qi + token] (ordered float bits, 0 = none)
     volatile uint32_t* cthr = reinterpret_cast<volatile uint32_t*>(smem + kOffMisc + 16);
 
     const uint64_t ntiles = (K + 127) / 128;
@@ -231,23 +249,25 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&cmap)) : "memory");
     }
-    if (threadIdx.x < 32) cthr[threadIdx.x] = 0;
+    if (threadIdx.x < 32 * QB) cthr[threadIdx.x] = 0;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // B operand [Q_hi; Q_lo] (row n < 32: Q_hi of token n, else Q_lo of token
-    // n - 32; zero rows past `rows`), SWIZZLE_128B K-major: row n, 16-byte
-    // granule j of chunk kc at kc*8192 + n*128 + ((j ^ (n & 7)) << 4)
-    for (uint32_t e = threadIdx.x; e < 64 * (kDim / 4); e += kThreads) {
+    // B operand [Q_hi of every query; Q_lo of every query] (row n < 32 QB:
+    // Q_hi of query n / 32, token n % 32, else Q_lo; zero rows past `rows`),
+    // SWIZZLE_128B K-major: row n, 16-byte granule j of chunk kc at
+    // kc * kQChunkBytes + n*128 + ((j ^ (n & 7)) << 4)
+    for (uint32_t e = threadIdx.x; e < 64 * QB * (kDim / 4); e += kThreads) {
         const uint32_t n = e / (kDim / 4), g = e % (kDim / 4);
-        const uint32_t kc = g / 8, j = g % 8, tok = n & 31;
-        const uint4 v = tok < rows ? reinterpret_cast<const uint4*>(Q + uint64_t(tok) * kDim)[g] : make_uint4(0, 0, 0, 0);
+        const uint32_t kc = g / 8, j = g % 8, tok = n & 31, qi = (n % (32 * QB)) / 32;
+        const uint4 v = tok < rows ? reinterpret_cast<const uint4*>(out.Q[qi] + uint64_t(tok) * kDim)[g]
+                                   : make_uint4(0, 0, 0, 0);
         const uint32_t off = kc * kQChunkBytes + n * 128 + ((j ^ (n & 7)) << 4);
         *reinterpret_cast<uint4*>(smem + kOffQ + off) =
-            n < 32 ? make_uint4(split_hi(v.x), split_hi(v.y), split_hi(v.z), split_hi(v.w))
-                   : make_uint4(split_lo(v.x), split_lo(v.y), split_lo(v.z), split_lo(v.w));
+            n < 32 * QB ? make_uint4(split_hi(v.x), split_hi(v.y), split_hi(v.z), split_hi(v.w))
+                        : make_uint4(split_lo(v.x), split_lo(v.y), split_lo(v.z), split_lo(v.w));
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -288,10 +308,10 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                     const uint32_t bq = base + kOffQ + kc * kQChunkBytes;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        // D[:, 0:32] += C_hi.Q_hi, D[:, 32:64] += C_hi.Q_lo
-                        mma_ts(d, ahi + kk * 8, umma_desc(bq + kk * 32), kIdesc64, (kc | kk) != 0);
-                        // D[:, 0:32] += C_lo.Q_hi (B = the first 32 rows)
-                        mma_ts(d, alo + kk * 8, umma_desc(bq + kk * 32), kIdesc32, 1);
+                        // D[:, 0:32QB] += C_hi.Q_hi, D[:, 32QB:64QB] += C_hi.Q_lo
+                        mma_ts(d, ahi + kk * 8, umma_desc(bq + kk * 32), Cf::kIdescAll, (kc | kk) != 0);
+                        // D[:, 0:32QB] += C_lo.Q_hi (B = the first 32 QB rows)
+                        mma_ts(d, alo + kk * 8, umma_desc(bq + kk * 32), Cf::kIdescHi, 1);
                     }
                     mma_commit(ops_empty(s));
                     if (kc == kChunks - 1) mma_commit(tfull_bar(acc));
@@ -360,11 +380,15 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
         // larger score (reference tie order).  thr: the NP-th score (-inf
         // until full); gb: a bound some list in the grid already reached
         // (ties at gb are kept)
-        float top_s[NP];
-        uint32_t top_i[NP];
+        float top_s[QB][NP];
+        uint32_t top_i[QB][NP];
+        float gb[QB];
 #pragma unroll
-        for (int j = 0; j < NP; ++j) top_s[j] = -INFINITY, top_i[j] = 0;
-        float gb = -INFINITY;
+        for (int qi = 0; qi < QB; ++qi) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) top_s[qi][j] = -INFINITY, top_i[qi][j] = 0;
+            gb[qi] = -INFINITY;
+        }
         const bool tok = lane < rows;
         float* tr = reinterpret_cast<float*>(smem + kOffTr) + ew * 32 * 33;
         uint32_t lt = grp;
@@ -374,81 +398,89 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             if (ew == 0 && lane == 0) trace_stamp(dbg, 5, lt);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * kAccCols;
-            uint32_t rh[32], rl[32];
-            tmem_ld32(taddr, rh);
-            tmem_ld32(taddr + 32, rl);
-            tmem_ld_wait();
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(acc));
-
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(__uint_as_float(rh[j]), __uint_as_float(rl[j]));
             const uint64_t c0 = t * 128 + q * 32;
             const uint64_t c = c0 + lane;
             const bool valid = c < K;
-            float m = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (uint32_t(j) < rows) m = fmaxf(m, v[j]);
-            const uint32_t kw = __ballot_sync(0xffffffffu, valid && m >= t_cs);
-            if (lane == 0 && c0 < K) keep_bits[c0 >> 5] = kw;
-            // 32x32 transpose: tr[centroid][token], pitch 33 (conflict-free both ways)
-#pragma unroll
-            for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = v[j];
-            __syncwarp();
-            if (tok) {
-                const uint32_t cb = cthr[lane];
-                if (cb) gb = fmaxf(gb, dev::unord_f32(cb));
-            }
-            const float thr0 = top_s[NP - 1];
             const uint32_t nv = K - c0 < 32 ? uint32_t(K - c0) : 32u;
-            uint32_t cand = 0;
-            // S rows from the transposed tile: one coalesced 128-byte row per
-            // centroid (lane = token)
 #pragma unroll
-            for (int r = 0; r < 32; ++r) {
-                const float sc = tr[r * 33 + lane];
-                cand |= (uint32_t(r) < nv && tok && sc > thr0 && sc >= gb) ? (1u << r) : 0u;
-                if (uint32_t(r) < nv && !(dbg & 2)) S[(c0 + r) * kScoresPitch + lane] = sc;
-            }
-            // per-lane inserts, rare once the bounds have risen
-            while (cand) {
-                const int r = __ffs(cand) - 1;
-                cand &= cand - 1;
-                const float sc = tr[r * 33 + lane];
-                if (sc > top_s[NP - 1] && sc >= gb) {
-                    const uint32_t id = uint32_t(c0 + r);
-                    // shift-insert; every position reads only old values
-#pragma unroll
-                    for (int j = NP - 1; j > 0; --j) {
-                        const bool up = sc > top_s[j - 1], here = sc > top_s[j];
-                        top_i[j] = up ? top_i[j - 1] : (here ? id : top_i[j]);
-                        top_s[j] = up ? top_s[j - 1] : (here ? sc : top_s[j]);
-                    }
-                    if (sc > top_s[0]) top_s[0] = sc, top_i[0] = id;
+            for (int qi = 0; qi < QB; ++qi) {
+                uint32_t rh[32], rl[32];
+                tmem_ld32(taddr + 32 * qi, rh);
+                tmem_ld32(taddr + 32 * QB + 32 * qi, rl);
+                tmem_ld_wait();
+                if (qi == QB - 1) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty_bar(acc));
                 }
-            }
-            const float thr = top_s[NP - 1];
-            __syncwarp();
-            // bounds: CTA-wide in shared memory every tile; one warp trades it
-            // with the grid-wide `gthr` every 4th of its tiles (one L2 line
-            // that every CTA hits, so per-tile traffic there would serialise)
-            if (tok && thr > thr0 && thr > gb) {
-                atomicMax(const_cast<uint32_t*>(&cthr[lane]), dev::ord_f32(thr));
-                gb = thr;
-            }
-            if (ew == kEpiWarps - 1 && (lt & 7) == 7 && tok) {
-                const uint32_t mine = cthr[lane];
-                const uint32_t go = mine ? atomicMax(gthr + lane, mine) : __ldcg(gthr + lane);
-                if (go > mine) atomicMax(const_cast<uint32_t*>(&cthr[lane]), go);
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(__uint_as_float(rh[j]), __uint_as_float(rl[j]));
+                float m = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (uint32_t(j) < rows) m = fmaxf(m, v[j]);
+                const uint32_t kw = __ballot_sync(0xffffffffu, valid && m >= t_cs);
+                if (lane == 0 && c0 < K) out.keep[qi][c0 >> 5] = kw;
+                // 32x32 transpose: tr[centroid][token], pitch 33 (conflict-free both ways)
+                __syncwarp();  // the previous query's reads of tr are done
+#pragma unroll
+                for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = v[j];
+                __syncwarp();
+                if (tok) {
+                    const uint32_t cb = cthr[32 * qi + lane];
+                    if (cb) gb[qi] = fmaxf(gb[qi], dev::unord_f32(cb));
+                }
+                const float thr0 = top_s[qi][NP - 1];
+                uint32_t cand = 0;
+                float* Sq = out.S[qi];
+                // S rows from the transposed tile: one coalesced 128-byte row per
+                // centroid (lane = token)
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {
+                    const float sc = tr[r * 33 + lane];
+                    cand |= (uint32_t(r) < nv && tok && sc > thr0 && sc >= gb[qi]) ? (1u << r) : 0u;
+                    if (uint32_t(r) < nv && !(dbg & 2)) Sq[(c0 + r) * kScoresPitch + lane] = sc;
+                }
+                // per-lane inserts, rare once the bounds have risen
+                while (cand) {
+                    const int r = __ffs(cand) - 1;
+                    cand &= cand - 1;
+                    const float sc = tr[r * 33 + lane];
+                    if (sc > top_s[qi][NP - 1] && sc >= gb[qi]) {
+                        const uint32_t id = uint32_t(c0 + r);
+                        // shift-insert; every position reads only old values
+#pragma unroll
+                        for (int j = NP - 1; j > 0; --j) {
+                            const bool up = sc > top_s[qi][j - 1], here = sc > top_s[qi][j];
+                            top_i[qi][j] = up ? top_i[qi][j - 1] : (here ? id : top_i[qi][j]);
+                            top_s[qi][j] = up ? top_s[qi][j - 1] : (here ? sc : top_s[qi][j]);
+                        }
+                        if (sc > top_s[qi][0]) top_s[qi][0] = sc, top_i[qi][0] = id;
+                    }
+                }
+                const float thr = top_s[qi][NP - 1];
+                // bounds: CTA-wide in shared memory every tile; one warp trades it
+                // with the grid-wide `gthr` every 4th of its tiles (one L2 line
+                // that every CTA hits, so per-tile traffic there would serialise)
+                if (tok && thr > thr0 && thr > gb[qi]) {
+                    atomicMax(const_cast<uint32_t*>(&cthr[32 * qi + lane]), dev::ord_f32(thr));
+                    gb[qi] = thr;
+                }
+                if (ew == kEpiWarps - 1 && (lt & 7) == 7 && tok) {
+                    const uint32_t mine = cthr[32 * qi + lane];
+                    const uint32_t go = mine ? atomicMax(out.gthr[qi] + lane, mine) : __ldcg(out.gthr[qi] + lane);
+                    if (go > mine) atomicMax(const_cast<uint32_t*>(&cthr[32 * qi + lane]), go);
+                }
             }
             if (ew == 0 && lane == 0) trace_stamp(dbg, 6, lt);
         }
-        uint64_t* out = partial + ((uint64_t(blockIdx.x) * kEpiWarps + ew) * 32 + lane) * NP;
 #pragma unroll
-        for (int j = 0; j < NP; ++j) out[j] = top_s[j] == -INFINITY ? 0 : dev::make_key(top_s[j], top_i[j]);
+        for (int qi = 0; qi < QB; ++qi) {
+            uint64_t* po = out.partial[qi] + ((uint64_t(blockIdx.x) * kEpiWarps + ew) * 32 + lane) * NP;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) po[j] = top_s[qi][j] == -INFINITY ? 0 : dev::make_key(top_s[qi][j], top_i[qi][j]);
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -467,20 +499,45 @@ int sm_count() {
     return n;
 }
 
-template <int NP>
-void launch_tf32(const CUtensorMap& map, const IndexView& ix, const float* q, uint32_t rows, float t_cs, float* S,
-                 uint32_t* keep, uint64_t* partial, uint32_t* gthr, uint32_t grid, cudaStream_t st) {
+template <int NP, int QB>
+void launch_tf32(const CUtensorMap& map, const IndexView& ix, const TfOut& out, uint32_t rows, float t_cs,
+                 uint32_t grid, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(scores_tf32_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(scores_tf32_kernel<NP, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             TfCfg<QB>::kSmemBytes);
         configured = true;
     }
     static const uint32_t dbg = [] {
         const char* e = getenv("PLAID_TF32_DBG");
         return e ? uint32_t(atoi(e)) : 0u;
     }();
-    ::plaid::launch::pdl(scores_tf32_kernel<NP>, grid, kThreads, kSmemBytes, st, map, ix.K, q, rows, t_cs, S, keep, partial, gthr, dbg);
+    ::plaid::launch::pdl(scores_tf32_kernel<NP, QB>, grid, kThreads, TfCfg<QB>::kSmemBytes, st, map, ix.K, out, rows,
+                         t_cs, dbg);
     launch::count_launch();
+}
+
+template <int QB>
+void launch_tf32_np(const CUtensorMap& map, const IndexView& ix, const TfOut& out, uint32_t rows, float t_cs,
+                    uint32_t np_bucket, uint32_t grid, cudaStream_t st) {
+    switch (np_bucket) {
+        case 1: launch_tf32<1, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 2: launch_tf32<2, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 4: launch_tf32<4, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 8: launch_tf32<8, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 16: if constexpr (QB == 1) { launch_tf32<16, QB>(map, ix, out, rows, t_cs, grid, st); break; }
+        [[fallthrough]];
+        default:
+            if constexpr (QB == 1) launch_tf32<32, QB>(map, ix, out, rows, t_cs, grid, st);
+            else launch::fail_cuda_driver(1, "batched S_cq supports nprobe <= 8");
+            break;
+    }
+}
+
+uint32_t tf32_grid(const IndexView& ix) {
+    const uint64_t ntiles = (ix.K + 127) / 128;
+    uint32_t grid = uint32_t(ntiles < uint64_t(sm_count()) ? ntiles : uint64_t(sm_count()));
+    return grid ? grid : 1;
 }
 
 }  // namespace
@@ -524,17 +581,19 @@ uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, 
                        float* d_scores, uint32_t* d_keep_bits, uint64_t* d_partial, uint32_t np_bucket,
                        uint32_t* d_gthr, cudaStream_t st) {
     const CUtensorMap& map = *static_cast<const CUtensorMap*>(cmap);
-    const uint64_t ntiles = (ix.K + 127) / 128;
-    uint32_t grid = uint32_t(ntiles < uint64_t(sm_count()) ? ntiles : uint64_t(sm_count()));
-    if (grid == 0) grid = 1;
-    switch (np_bucket) {
-        case 1: launch_tf32<1>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 2: launch_tf32<2>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 4: launch_tf32<4>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 8: launch_tf32<8>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        case 16: launch_tf32<16>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
-        default: launch_tf32<32>(map, ix, d_q, rows, t_cs, d_scores, d_keep_bits, d_partial, d_gthr, grid, st); break;
-    }
+    TfOut out{};
+    out.Q[0] = d_q, out.S[0] = d_scores, out.keep[0] = d_keep_bits, out.partial[0] = d_partial, out.gthr[0] = d_gthr;
+    const uint32_t grid = tf32_grid(ix);
+    launch_tf32_np<1>(map, ix, out, rows, t_cs, np_bucket, grid, st);
+    return grid * kEpiWarps;
+}
+
+uint32_t scores_tensor_batch(const void* cmap, const IndexView& ix, const TfOut& out, uint32_t qb, uint32_t rows,
+                             float t_cs, uint32_t np_bucket, cudaStream_t st) {
+    const CUtensorMap& map = *static_cast<const CUtensorMap*>(cmap);
+    const uint32_t grid = tf32_grid(ix);
+    if (qb == 1) launch_tf32_np<1>(map, ix, out, rows, t_cs, np_bucket, grid, st);
+    else launch_tf32_np<2>(map, ix, out, rows, t_cs, np_bucket, grid, st);
     return grid * kEpiWarps;
 }
 

@@ -57,11 +57,22 @@ struct SelectHist {
 
 constexpr int kScoresPitch = 32;  // S rows padded to 32 floats (128 B)
 
+// Per-query outputs of the (batched) tensor S_cq kernel, query qi < qb.
+constexpr uint32_t kMaxScoreBatch = 2;
+struct TfOut {
+    const float* Q[kMaxScoreBatch];
+    float* S[kMaxScoreBatch];
+    uint32_t* keep[kMaxScoreBatch];
+    uint64_t* partial[kMaxScoreBatch];
+    uint32_t* gthr[kMaxScoreBatch];
+};
+
 namespace launch {
 
 // Launch with programmatic stream serialization (PDL): the kernel may be
 // scheduled while the previous kernel in the stream drains; every kernel
 // starts with dev::pdl_wait(), so no data dependence is relaxed.
+bool pdl_enabled();  // false when PLAID_NO_PDL is set (ordering experiments)
 template <typename... KArgs, typename... Args>
 inline void pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg{};
@@ -71,7 +82,7 @@ inline void pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
@@ -97,6 +108,11 @@ uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, 
                        float* d_scores, uint32_t* d_keep_bits, uint64_t* d_partial, uint32_t np_bucket,
                        uint32_t* d_gthr, cudaStream_t st);
 uint32_t scores_tensor_max_warps();
+// Batched variant: qb (<= kMaxScoreBatch) queries share one pass over C
+// (B operand = every query's Q_hi and Q_lo, N = 64 qb); per-query outputs as
+// above.  nprobe bucket <= 8.  Returns the number of partial lists per query.
+uint32_t scores_tensor_batch(const void* cmap, const IndexView& ix, const TfOut& out, uint32_t qb, uint32_t rows,
+                             float t_cs, uint32_t np_bucket, cudaStream_t st);
 [[noreturn]] void fail_cuda_driver(int code, const char* what);
 // Merge per-warp partial top-NP lists into sel[rows][nprobe] centroid ids.
 void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,

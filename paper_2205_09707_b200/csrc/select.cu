@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -761,6 +762,11 @@ void merge_topk(const uint32_t* d_pids, const float* d_scores, const uint64_t* d
 void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st) {
     ::plaid::launch::pdl(copy_count_kernel, 1, 1, 0, st, src, dst, cap);
     count_launch();
+}
+
+bool pdl_enabled() {
+    static const bool on = getenv("PLAID_NO_PDL") == nullptr;
+    return on;
 }
 
 void validate_query(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, cudaStream_t st) {

@@ -309,3 +309,21 @@ def test_batch_searcher_bit_exact(small, port, lanes):
     bad[2, 0, :] *= 2.0
     with pytest.raises(P.PlaidError):
         b.search(bad, P.default_params_for_k(10))
+
+
+@pytest.mark.parametrize("lanes", [2, 5])
+def test_batch_tensor_scores_match_single(small, lanes):
+    """Batched S_cq (two queries per pass over C, N = 128 MMAs) gives the same
+    results as the single-query tensor kernel, query by query; odd batch
+    sizes end with a one-query pass."""
+    h, qs, idx, _ = small
+    single = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.TENSOR)
+    qb = np.concatenate([qs, qs[1:4]])  # 9 queries
+    for k in (10, 100, 1000):
+        p = P.default_params_for_k(k)
+        got = b.search(qb, p)
+        for q, g in zip(qb, got):
+            r = single.search(q, p)
+            assert np.array_equal(g.passage_ids, r.topk.passage_ids), k
+            assert np.array_equal(bits(g.scores), bits(r.topk.scores)), k
