@@ -7,7 +7,9 @@
 One step = one query through all four stages (single-query latency mode,
 BASELINE.json configs[1]: synthetic MS MARCO v1 scale, 8.8M passages, 2^18
 centroids, nbits=2, k=1000 with default_params_for_k).  Inputs are resident in
-HBM when the timed region starts; L2 is flushed (256 MiB write) before every
+HBM when the timed region starts; L2 is flushed (256 MiB write; --flush
+write+read adds a 256 MiB read sweep so no dirty line of the flush is written
+back inside the timed region — measured to make no difference) before every
 step, outside the timed interval.  Each step is bracketed by CUDA events on
 the launching stream; the job time is the max over ranks of the summed step
 times, `value` = queries / that time.
@@ -119,6 +121,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class L2Flush:
+    """Untimed cold-L2 reset before every step: write a 256 MiB buffer (twice
+    the 126 MB L2), then (mode "write+read") read a second 256 MiB buffer so
+    the dirty lines of the write are evicted before the timed region instead
+    of being written back during it."""
+
+    def __init__(self, mode: str):
+        import torch
+
+        self.mode = mode
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(64 << 20, dtype=torch.int32, device="cuda") if mode == "write+read" else None
+
+    def __call__(self):
+        self.w.zero_()
+        if self.r is not None:
+            self.r.max()
+
+    def describe(self) -> str:
+        return self.describe_mode(self.mode)
+
+    @staticmethod
+    def describe_mode(mode: str) -> str:
+        return ("256 MiB write + 256 MiB read sweep before every step (untimed; L2 cold and clean)"
+                if mode == "write+read" else "256 MiB write before every step (untimed)")
+
+
 def make_index(cfg: dict, rank: int, seed: int = 0):
     import paper_2205_09707_b200 as P
 
@@ -213,7 +242,7 @@ def config_block(cfg, params, args, world):
             "query_tokens": QLEN, "k": params.k, "nprobe": params.nprobe, "t_cs": params.t_cs,
             "ndocs": params.ndocs, "batch": cfg.get("batch", 1),
             "lanes": args.lanes if cfg.get("batch", 1) > 1 else None,
-            "l2_flush": "256 MiB write before every step (untimed)",
+            "l2_flush": L2Flush.describe_mode(args.flush),
             "score_mode": args.score_mode, "parallelism": f"passage-range shards x{world}",
             "shard_merge": args.shard_mode if world > 1 else None}
 
@@ -275,7 +304,7 @@ def run_plaid(args, cfg):
         ss = ShardedSearcher(s, k, device=torch.device("cuda", local), mode=args.shard_mode,
                              num_passages=cfg["N"] * world)
         m_pids, m_scores = ss.out_pids, ss.out_scores
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush(args.flush)
 
     def step(i):
         q = dq[i % nq]
@@ -289,7 +318,7 @@ def run_plaid(args, cfg):
                             d_n.data_ptr(), stream=sh)
 
     for i in range(args.warmup):
-        flush.zero_()
+        flush()
         step(i)
     torch.cuda.synchronize()
     s.sync()
@@ -303,7 +332,7 @@ def run_plaid(args, cfg):
     torch.cuda.synchronize()
     clocks.start()
     for i in range(args.steps):
-        flush.zero_()
+        flush()
         ev[i][0].record(stream)
         step(args.warmup + i)
         ev[i][1].record(stream)
@@ -326,7 +355,7 @@ def run_plaid(args, cfg):
     e2e_lat = []
     if world == 1:
         for i in range(args.steps):
-            flush.zero_()
+            flush()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             r = s.search(qs[(args.warmup + i) % nq], params)
@@ -337,7 +366,7 @@ def run_plaid(args, cfg):
         hp = torch.zeros(k, dtype=torch.int32).pin_memory()
         hs = torch.zeros(k, dtype=torch.float32).pin_memory()
         for i in range(args.steps):
-            flush.zero_()
+            flush()
             torch.cuda.synchronize()
             dist.barrier()
             t0 = time.perf_counter()
@@ -470,7 +499,7 @@ def run_plaid_batch(args, cfg):
         m_scores = torch.zeros(B * k, dtype=torch.float32, device="cuda")
         m_n = torch.zeros(B, dtype=torch.int64, device="cuda")
         merger = P.Searcher(None, device=local)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush(args.flush)
 
     def step(i):
         q = dq[i % nb]
@@ -492,7 +521,7 @@ def run_plaid_batch(args, cfg):
                                          m_n.data_ptr() + 8 * j, stream=sh)
 
     for i in range(args.warmup):
-        flush.zero_()
+        flush()
         step(i)
     torch.cuda.synchronize()
     bs.sync()
@@ -504,7 +533,7 @@ def run_plaid_batch(args, cfg):
     clocks.start()
     launches = 0
     for i in range(args.steps):
-        flush.zero_()
+        flush()
         ev[i][0].record(stream)
         step(args.warmup + i)
         ev[i][1].record(stream)
@@ -523,7 +552,7 @@ def run_plaid_batch(args, cfg):
     e2e_lat = []
     if world == 1:
         for i in range(args.steps):
-            flush.zero_()
+            flush()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             bs.search(qs[i % nb], params)
@@ -540,7 +569,7 @@ def run_plaid_batch(args, cfg):
     s1 = P.Searcher(idx, device=local, score_mode=mode, record_times=True)
     sc_ms = []
     for i in range(5):
-        flush.zero_()
+        flush()
         torch.cuda.synchronize()
         s1.search(qs[0][i], params)
         sc_ms.append(s1.phase_ms()["scores"])
@@ -600,6 +629,8 @@ def main():
     ap.add_argument("--score-mode", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--flush", default="write", choices=["write", "write+read"],
+                    help="untimed L2 reset between steps")
     ap.add_argument("--lanes", type=int, default=8, help="throughput mode: concurrent searcher lanes")
     ap.add_argument("--batch", type=int, default=0, help="queries per step (default: the config's)")
     ap.add_argument("--shard-mode", default="global-exact", choices=["global-exact", "shard-local"],
