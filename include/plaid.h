@@ -132,6 +132,21 @@ uint64_t plaid_stage3_width(const plaid_params* p);
  * index.cpp:7-10).  validate != 0 runs validate_index's invariants (index.cpp:12-84). */
 plaid_status plaid_index_from_host(const plaid_index_desc* desc, int device, int validate,
                                    plaid_index** out);
+/* ---- on-disk index (SPEC.md storage module; layout in FORMAT.md) ----
+ * plaid_index_save writes manifest.json + centroids.f32, codes.u32,
+ * residuals.bin, doclens.u32, ivf_offsets.u64, ivf_postings.u32 (little
+ * endian) with per-file checksums; on any write error the partial files are
+ * removed (IoError).  Host-only: needs no GPU.
+ * plaid_index_open maps the files, uploads them once to HBM and verifies every
+ * checksum ON THE GPU over the uploaded arrays (ChecksumMismatch names the
+ * file); UnsupportedVersion / HeaderMismatch / LengthMismatch for a bad
+ * manifest; PLAID_OPEN_VALIDATE adds validate_index (index.cpp:12-84). */
+enum { PLAID_OPEN_VALIDATE = 1, PLAID_OPEN_NO_CHECKSUMS = 2 };
+plaid_status plaid_index_save(const plaid_index_desc* desc, const char* dir, uint64_t rng_seed);
+plaid_status plaid_index_open(const char* dir, int device, uint32_t flags, plaid_index** out);
+/* FORMAT.md digest of a host buffer (the manifest's per-file checksum). */
+uint64_t plaid_checksum(const void* data, uint64_t bytes);
+
 /* Same, for a desc that already is one passage-range shard of a larger index
  * (local ids, local IVF): results report local id + pid_base. */
 plaid_status plaid_index_from_host_at(const plaid_index_desc* desc, uint64_t pid_base, int device,

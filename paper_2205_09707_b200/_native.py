@@ -69,6 +69,9 @@ SIGNATURES = {
                                      u32p, f32p, u64p, C.POINTER(Trace)]),
     "plaid_search_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                       C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "plaid_index_save": (C.c_int, [C.POINTER(IndexDesc), C.c_char_p, C.c_uint64]),
+    "plaid_index_open": (C.c_int, [C.c_char_p, C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "plaid_checksum": (C.c_uint64, [C.c_void_p, C.c_uint64]),
     "plaid_batch_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(SearcherConfig), C.c_uint32,
                                      C.POINTER(C.c_void_p)]),
     "plaid_batch_destroy": (None, [C.c_void_p]),

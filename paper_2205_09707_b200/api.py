@@ -171,6 +171,18 @@ def _desc(h: HostIndex) -> N.IndexDesc:
                        N.ptr(h.bucket_cutoffs, C.c_float), N.ptr(h.bucket_weights, C.c_float))
 
 
+def save_index(h: HostIndex, path: str, rng_seed: int = 0) -> None:
+    """Write `h` in the on-disk format (FORMAT.md; SPEC.md storage module)."""
+    d = _desc(h)
+    _check(N.load().plaid_index_save(C.byref(d), str(path).encode(), int(rng_seed)))
+
+
+def checksum(buf: np.ndarray) -> int:
+    """FORMAT.md digest of a host array (the manifest's per-file checksum)."""
+    b = np.ascontiguousarray(buf)
+    return int(N.load().plaid_checksum(b.ctypes.data_as(C.c_void_p), b.nbytes))
+
+
 class DeviceIndex:
     """The compressed index resident in HBM (index.hpp:60-85).  Immutable and
     shareable between searchers (index.hpp:57-59)."""
@@ -202,6 +214,15 @@ class DeviceIndex:
         out = C.c_void_p()
         d = _desc(h)
         _check(N.load().plaid_index_from_host_shard(C.byref(d), pid_begin, pid_end, device, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def open(cls, path: str, device: int = 0, validate: bool = False, checksums: bool = True) -> "DeviceIndex":
+        """Load an on-disk index (FORMAT.md): mmap, one upload to HBM, every
+        file checksum verified on the GPU over the uploaded arrays."""
+        out = C.c_void_p()
+        flags = (1 if validate else 0) | (0 if checksums else 2)
+        _check(N.load().plaid_index_open(str(path).encode(), device, flags, C.byref(out)))
         return cls(out.value)
 
     def validate(self) -> None:  # index.cpp:12-84

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "storage.hpp"
 
 struct plaid_index {
     std::unique_ptr<plaid::DeviceIndex> impl;
@@ -225,6 +226,34 @@ plaid_status plaid_searcher_create(plaid_index* index, int device, const plaid_s
 }
 
 void plaid_searcher_destroy(plaid_searcher* s) { delete s; }
+
+plaid_status plaid_index_save(const plaid_index_desc* desc, const char* dir, uint64_t rng_seed) {
+    return guarded([&] {
+        need(desc, "desc");
+        need(dir, "dir");
+        plaid::save_index(*desc, dir, rng_seed);
+    });
+}
+
+plaid_status plaid_index_open(const char* dir, int device, uint32_t flags, plaid_index** out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        need(dir, "dir");
+        auto* h = new plaid_index();
+        try {
+            h->impl.reset(plaid::open_index(dir, device, flags));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+uint64_t plaid_checksum(const void* data, uint64_t bytes) { return plaid::checksum_host(data, bytes); }
+
+
 
 plaid_status plaid_search(plaid_searcher* s, const float* q, uint64_t rows, uint64_t dim,
                           const plaid_params* params, uint32_t* out_pids, float* out_scores,

@@ -174,3 +174,67 @@ def generate_queries(index: HostIndex, num_queries: int, qlen: int = 32, noise: 
                       _p(index.bucket_weights), _p(index.doclens), _p(index.passage_offsets),
                       index.num_passages, num_queries, qlen, float(noise), seed, _p(out))
     return out
+
+
+# ---- on-disk format (FORMAT.md): host-side reader with an independent numpy
+# implementation of the checksum (the GPU loader is DeviceIndex.open) -------------
+_FNV_BASIS = np.uint64(0xCBF29CE484222325)
+_FNV_PRIME = np.uint64(0x100000001B3)
+_FILES = ("centroids.f32", "codes.u32", "residuals.bin", "doclens.u32", "ivf_offsets.u64", "ivf_postings.u32")
+
+
+def fnv_digest(buf: bytes | np.ndarray) -> int:
+    """FORMAT.md digest: 64 KiB blocks, word i of a block -> lane i % 32,
+    FNV-1a 64 over 64-bit little-endian words (tail zero-padded), lanes folded
+    into the block digest, block digests + byte length into the file digest."""
+    raw = np.frombuffer(bytes(buf) if not isinstance(buf, np.ndarray) else np.ascontiguousarray(buf).tobytes(),
+                        dtype=np.uint8)
+    nbytes = raw.size
+    block = 64 * 1024
+    nb = (nbytes + block - 1) // block
+    with np.errstate(over="ignore"):
+        digests = []
+        if nb:
+            padded = np.zeros(nb * block, dtype=np.uint8)
+            padded[:nbytes] = raw
+            words = padded.view("<u8").reshape(nb, block // 8 // 32, 32)  # [block, step, lane]
+            nwords = np.full(nb, block // 8, dtype=np.int64)
+            nwords[-1] = (nbytes - (nb - 1) * block + 7) // 8
+            lanes = np.full((nb, 32), _FNV_BASIS, dtype=np.uint64)
+            for s in range(words.shape[1]):
+                active = (s * 32 + np.arange(32))[None, :] < nwords[:, None]
+                lanes = np.where(active, (lanes ^ words[:, s, :]) * _FNV_PRIME, lanes)
+            d = np.full(nb, _FNV_BASIS, dtype=np.uint64)
+            for l in range(32):
+                d = (d ^ lanes[:, l]) * _FNV_PRIME
+            digests = list(d)
+        h = _FNV_BASIS
+        for x in digests:
+            h = (h ^ np.uint64(x)) * _FNV_PRIME
+        h = (h ^ np.uint64(nbytes)) * _FNV_PRIME
+    return int(h)
+
+
+def load_index_host(path, verify: bool = True) -> HostIndex:
+    """Read an index written by save_index (FORMAT.md) into host memory."""
+    import json
+    import os
+
+    from .api import ErrorCode, PlaidError
+
+    with open(os.path.join(path, "manifest.json")) as f:
+        m = json.load(f)
+    if m.get("format_version") != 1:
+        raise PlaidError(ErrorCode.UnsupportedVersion, f"format_version {m.get('format_version')}")
+    arrays = {}
+    for name, dt in zip(_FILES, ("<f4", "<u4", "u1", "<u4", "<u8", "<u4")):
+        data = np.fromfile(os.path.join(path, name), dtype=np.uint8)
+        if verify and f"{fnv_digest(data):016x}" != m["checksums"][name]:
+            raise PlaidError(ErrorCode.ChecksumMismatch, f"{name}: checksum mismatch")
+        arrays[name] = data.view(dt)
+    dim, K = int(m["dim"]), int(m["num_centroids"])
+    cut = np.array(m["bucket_cutoffs_bits"], dtype=np.uint32).view(np.float32)
+    wts = np.array(m["bucket_weights_bits"], dtype=np.uint32).view(np.float32)
+    return HostIndex(dim, int(m["nbits"]), arrays["centroids.f32"].reshape(K, dim), arrays["codes.u32"],
+                     arrays["residuals.bin"], arrays["doclens.u32"], arrays["ivf_offsets.u64"],
+                     arrays["ivf_postings.u32"], cut, wts)

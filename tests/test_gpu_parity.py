@@ -327,3 +327,29 @@ def test_batch_tensor_scores_match_single(small, lanes):
             r = single.search(q, p)
             assert np.array_equal(g.passage_ids, r.topk.passage_ids), k
             assert np.array_equal(bits(g.scores), bits(r.topk.scores)), k
+
+
+def test_index_open_gpu_checksums(tmp_path, small, port):
+    """On-disk index -> DeviceIndex.open (mmap, one upload, checksums verified
+    on the GPU over the HBM copies) searches exactly like the in-memory index;
+    a flipped byte is a ChecksumMismatch naming the file."""
+    h, qs, idx, s = small
+    P.save_index(h, tmp_path)
+    ix2 = P.DeviceIndex.open(tmp_path, validate=True)
+    s2 = P.Searcher(ix2)
+    p = P.default_params_for_k(100)
+    for q in qs[:3]:
+        a, b = s.search(q, p), s2.search(q, p)
+        assert np.array_equal(a.topk.passage_ids, b.topk.passage_ids)
+        assert np.array_equal(bits(a.topk.scores), bits(b.topk.scores))
+    f = tmp_path / "codes.u32"
+    raw = bytearray(f.read_bytes())
+    raw[123] ^= 0x10
+    f.write_bytes(bytes(raw))
+    with pytest.raises(P.PlaidError) as e:
+        P.DeviceIndex.open(tmp_path)
+    assert e.value.code == P.ErrorCode.ChecksumMismatch and "codes.u32" in str(e.value)
+    (tmp_path / "doclens.u32").write_bytes(b"\0" * 8)
+    with pytest.raises(P.PlaidError) as e:
+        P.DeviceIndex.open(tmp_path)
+    assert e.value.code == P.ErrorCode.LengthMismatch
