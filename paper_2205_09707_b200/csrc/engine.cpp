@@ -1144,7 +1144,12 @@ BatchSearcher::BatchSearcher(DeviceIndex* index, int device, const plaid_searche
         PLAID_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         sdone_.push_back(e);
     }
-    PLAID_CUDA(cudaStreamCreateWithFlags(&sstream_, cudaStreamNonBlocking));
+    // the S_cq pass needs whole SMs (215 KB of shared memory, the full register
+    // file): give its stream the highest priority so freed SMs go to it before
+    // the lanes' small kernels refill them
+    int lo = 0, hi = 0;
+    PLAID_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    PLAID_CUDA(cudaStreamCreateWithPriority(&sstream_, cudaStreamNonBlocking, hi));
 }
 
 BatchSearcher::~BatchSearcher() {
