@@ -316,17 +316,24 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
             const uint32_t pn1 = __shfl_down_sync(0xffffffffu, p1, 1);
             const bool tail0 = valid0 && (lane == 31 || pn0 != p0);
             const bool tail1 = valid1 && (lane == 31 || pn1 != p1);
+            // segment membership of the lane `o` below, per scan step (same for every query)
+            uint32_t same0 = 0, same1 = 0;
+#pragma unroll
+            for (int l = 0, o = 1; l < 5; ++l, o <<= 1) {
+                const uint32_t s0 = __shfl_up_sync(0xffffffffu, p0, o);  // every lane takes part
+                const uint32_t s1 = __shfl_up_sync(0xffffffffu, p1, o);
+                same0 |= uint32_t(lane >= uint32_t(o) && s0 == p0) << l;
+                same1 |= uint32_t(lane >= uint32_t(o) && s1 == p1) << l;
+            }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 float m0 = a[u], m1 = c[u];
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
+                for (int l = 0, o = 1; l < 5; ++l, o <<= 1) {
                     const float y0 = __shfl_up_sync(0xffffffffu, m0, o);
                     const float y1 = __shfl_up_sync(0xffffffffu, m1, o);
-                    const uint32_t s0 = __shfl_up_sync(0xffffffffu, p0, o);
-                    const uint32_t s1 = __shfl_up_sync(0xffffffffu, p1, o);
-                    if (lane >= uint32_t(o) && s0 == p0) m0 = dev::max_gt(m0, y0);
-                    if (lane >= uint32_t(o) && s1 == p1) m1 = dev::max_gt(m1, y1);
+                    if ((same0 >> l) & 1u) m0 = dev::max_gt(m0, y0);
+                    if ((same1 >> l) & 1u) m1 = dev::max_gt(m1, y1);
                 }
                 if (i0 + u < rows) {
                     if (tail0) atomicMax(run + uint64_t(p0) * 32 + i0 + u, dev::ord_f32(m0));
