@@ -410,6 +410,27 @@ def run_plaid(args, cfg):
             "algorithmic_bytes_per_launch": ab, "mean_ms": mean_ph["scores"],
             "share_of_step": mean_ph["scores"] / (1e3 * total_s / args.steps)}
 
+    # ---- stage 4 (decompress + exact MaxSim) against its own bound: exactness
+    # forbids FMA and tensor cores, so every (token, query token, dim) is one
+    # rounded multiply and one rounded add on the FP32 pipe;
+    # peak = SMs x 128 lanes x max SM clock.  Duration = the stage-4 phase
+    # (scan + fused decompress/MaxSim + finalize), i.e. conservative.
+    roof4 = None
+    t4 = trace.decompressed_tokens if trace is not None else 0
+    if t4:
+        import torch as _t
+
+        props = _t.cuda.get_device_properties(local)
+        clk_mhz = (clk or {}).get("sm_max_mhz") or 1965.0
+        peak_ops = props.multi_processor_count * 128 * clk_mhz * 1e6 / 1e12
+        ops = 2.0 * QLEN * DIM * t4
+        ach = ops / (mean_ph["stage4_rank"] * 1e-3) / 1e12
+        bytes4 = t4 * (4 + DIM * cfg["nbits"] // 8)
+        roof4 = {"bound": "fp32", "kernel": "stream_fused_kernel (+ scan, finalize)", "achieved": ach,
+                 "peak": peak_ops, "unit": "Tops/s (fp32 lane-ops: separate mul + add)", "frac": ach / peak_ops,
+                 "tokens": t4, "ops_per_launch": ops, "code_and_residual_bytes": bytes4,
+                 "mean_ms": mean_ph["stage4_rank"]}
+
     # ---- CPU baseline: the reference's own searcher on this host, bounded sample
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -435,6 +456,7 @@ def run_plaid(args, cfg):
                 "d2h_bytes_per_step": k * 8 + 128, "p50_ms": 1e3 * statistics.median(e2e_lat)},
         "gpu_launches": launches,
         "roofline": roof,
+        "roofline_stage4": roof4,
         "phases_ms": mean_ph,
         "trace": tr,
         "cpu_baseline": cpu,

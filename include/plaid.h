@@ -105,6 +105,7 @@ typedef struct plaid_trace {
     double decompression_ms;
     double scoring_ms;
     double total_ms;
+    uint64_t decompressed_tokens;  /* stage-4 tokens (sum of the finalists' doclens; not a lir counter) */
 } plaid_trace;
 
 typedef struct plaid_searcher_config {

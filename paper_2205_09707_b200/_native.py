@@ -37,7 +37,7 @@ class Trace(C.Structure):
         "stage2_rows_gathered", "stage3_rows_gathered", "decompressed_passages")] + \
         [(n, C.c_double) for n in (
             "candidate_generation_ms", "stage2_ms", "stage3_ms", "lookup_ms", "decompression_ms",
-            "scoring_ms", "total_ms")]
+            "scoring_ms", "total_ms")] + [("decompressed_tokens", C.c_uint64)]
 
 
 class SearcherConfig(C.Structure):

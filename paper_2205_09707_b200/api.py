@@ -106,6 +106,7 @@ class StageTrace:  # pipeline.hpp:23-43
     stage2_rows_gathered: int = 0
     stage3_rows_gathered: int = 0
     decompressed_passages: int = 0
+    decompressed_tokens: int = 0  # stage-4 tokens (engine extra, not a lir counter)
 
     @classmethod
     def _from_c(cls, t: N.Trace) -> "StageTrace":

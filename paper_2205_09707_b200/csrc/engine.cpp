@@ -67,6 +67,7 @@ enum : int {
     kKConst = 7,    // K (for generic selects)
     kTmpN = 8,      // scratch count
     kEntryN = 9,    // entry-point input count
+    kT4 = 13,       // stage-4 stream tokens (trace.decompressed_tokens)
     kKeptN = 10,    // stage 2: kept centroids, their postings, queued owners (3 slots)
     kGthr = 16,     // 32 u32 per-token top-nprobe bounds (tensor S_cq kernel)
     kNumCounters = 32
@@ -423,6 +424,7 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
         rank_scratch_.pref = pref_.p;
         rank_scratch_.run = run_.p;
         rank_scratch_.fin_base = fin_base_.p;
+        rank_scratch_.tokens = counters_.p + kT4;
         rank_scratch_.pass_cap =
             std::min<uint64_t>({pref_.n - 1, run_.n / 32, fin_base_.n, launch::kStreamMaxPassages});
     }
@@ -748,6 +750,7 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
             trace->stage2_rows_gathered = h_counters_[kRows2];
             trace->stage3_rows_gathered = h_counters_[kRows3];
             trace->decompressed_passages = trace->stage3_out;
+            trace->decompressed_tokens = h_counters_[kT4];
         }
         if (times) {
             double ms[7];

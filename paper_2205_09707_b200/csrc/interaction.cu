@@ -53,18 +53,18 @@ __device__ float score_passage_warp(const uint32_t* __restrict__ codes, uint64_t
         if (MASKED) valid = valid && kept(keep_bits, code);
         uint32_t bits = __ballot_sync(0xffffffffu, valid);
         used += __popc(bits);
-        while (bits) {
-            float s[8];
+        // all (up to 32) S-row gathers of the chunk in flight at once, then
+        // the maxima in token order (`if (s > acc)`, pipeline.cpp:121-123)
+        float s[32];
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                const int b = bits ? __ffs(bits) - 1 : 0;
-                const uint32_t c = __shfl_sync(0xffffffffu, code, b);
-                s[v] = bits ? __ldg(S + uint64_t(c) * kScoresPitch + lane) : -INFINITY;
-                bits &= bits - 1;
-            }
-#pragma unroll
-            for (int v = 0; v < 8; ++v) acc = dev::max_gt(acc, s[v]);
+        for (int v = 0; v < 32; ++v) {
+            const int b = bits ? __ffs(bits) - 1 : 0;
+            const uint32_t c = __shfl_sync(0xffffffffu, code, b);
+            s[v] = bits ? __ldg(S + uint64_t(c) * kScoresPitch + lane) : -INFINITY;
+            bits &= bits - 1;
         }
+#pragma unroll
+        for (int v = 0; v < 32; ++v) acc = dev::max_gt(acc, s[v]);
     }
     float total = 0.0f;
     if (used > 0) {

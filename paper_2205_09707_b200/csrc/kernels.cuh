@@ -204,6 +204,7 @@ struct RankScratch {
     uint32_t* pref = nullptr;     // pass_cap + 1: stream offset of each finalist
     uint32_t* run = nullptr;      // pass_cap x 32 running maxima; all zero between searches
     uint64_t* fin_base = nullptr; // pass_cap: index token of stream position g is fin_base[p] + g
+    uint64_t* tokens = nullptr;   // 1 counter: stage-4 stream length (trace)
     uint64_t pass_cap = 0;
 };
 constexpr uint64_t kStreamMaxPassages = 16384;

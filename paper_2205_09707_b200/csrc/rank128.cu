@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(1024)
 finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
                      const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ doclens,
                      const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pref,
-                     uint64_t* __restrict__ fin_base) {
+                     uint64_t* __restrict__ fin_base, uint64_t* __restrict__ tokens) {
     dev::pdl_wait();
     __shared__ uint32_t warp_sums[32];
     const uint32_t n = uint32_t(*d_n);
@@ -128,7 +128,10 @@ finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restric
         fin_base[p] = offsets[pid] - run;  // index token = fin_base[p] + stream position
         run += doclens[pid];
     }
-    if (threadIdx.x == 1023) pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)
+    if (threadIdx.x == 1023) {
+        pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)
+        if (tokens) *tokens = pref[n];
+    }
 }
 
 // Warp-cooperative: the finalist of stream token g (this lane's) for a
@@ -398,7 +401,7 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
         cfg = true;
     }
     ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref,
-                         s.fin_base);
+                         s.fin_base, s.tokens);
     count_launch();
     uint64_t fb = (nmax * ix.max_doclen + kTile - 1) / kTile;
     if (fb > uint64_t(sm_count()) * 2) fb = uint64_t(sm_count()) * 2;  // two CTAs (12 warps) per SM
