@@ -340,7 +340,7 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
     PLAID_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     for (auto& e : ev_) PLAID_CUDA(cudaEventCreate(&e));
     const uint64_t words = index_ ? (index_->view().N + 31) / 32 : 0;
-    zero_.ensure(2 * kNumCounters + 2 * words);
+    zero_.ensure((2 * kNumCounters + 2 * words + 3) / 4 * 4);  // whole 16-byte units (query_prologue)
     PLAID_CUDA(cudaMemset(zero_.p, 0, zero_.n * sizeof(uint32_t)));
     counters_.p = reinterpret_cast<uint64_t*>(zero_.p);
     bitmap_.p = zero_.p + 2 * kNumCounters;
@@ -453,9 +453,9 @@ void Searcher::record(int slot, cudaStream_t st, bool times) {
 
 // The four stages of lir::search (pipeline.cpp:232-283) as one launch sequence.
 void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
-                       float* d_scores, uint64_t* d_n, cudaStream_t st, bool times) {
+                       float* d_scores, uint64_t* d_n, cudaStream_t st, bool times, bool validate) {
     pending_rows_ = rows;
-    enqueue_front(d_q, rows, p, st, times);
+    enqueue_front(d_q, rows, p, st, times, validate);
     enqueue_stage3(p, st, times);
     enqueue_back(d_q, rows, p, d_pids, d_scores, d_n, st, times);
 }
@@ -463,16 +463,17 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
 // Stage 1 (S_cq, candidates) and stage 2 (pruned interaction + top-ndocs
 // select): survivors in sel2_ (keys, count counters[kN2]).
 void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st,
-                             bool times) {
+                             bool times, bool validate) {
     const IndexView& ix = index_->view();
     const uint64_t K = ix.K, N = ix.N;
     uint64_t* c = counters_.p;
     uint32_t* bitmap = bitmap_.p;
     uint32_t* owners = bitmap_.p + (N + 31) / 32;
-    // one memset clears the per-query counters, the candidate bitmap and the
-    // stage-2 used bitmap (contiguous in zero_); the "scores" phase then
-    // brackets the S_cq kernel alone
-    PLAID_CUDA(cudaMemsetAsync(zero_.p, 0, zero_.n * sizeof(uint32_t), st));
+    // one PDL-chained prologue kernel validates the query rows on the device
+    // (device-resident queries) and clears the per-query counters, the
+    // candidate bitmap and the stage-2 used bitmap (contiguous in zero_); the
+    // "scores" phase then brackets the S_cq kernel alone
+    launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, st);
     record(0, st, times);
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
@@ -605,8 +606,7 @@ void Searcher::shard_phase1(const float* d_q, uint64_t rows, uint64_t dim, const
     pending_stride3_ = 0;
     phase_ = 1;
     const bool times = cfg_.record_times != 0;
-    launch::validate_query(d_q, uint32_t(rows), uint32_t(dim), status_.p, st);
-    enqueue_front(d_q, uint32_t(rows), p, st, times);
+    enqueue_front(d_q, uint32_t(rows), p, st, times, true);
     if (!p.disable_filter)
         launch::export_keys(sel2_.p, counters_.p + kN2, stride2, uint32_t(index_->pid_base()), d_x2, st);
     PLAID_CUDA(cudaGetLastError());
@@ -667,8 +667,7 @@ void Searcher::batch_prepare(const float* d_q, uint64_t rows, uint64_t dim, cons
     DeviceGuard g(device_);
     ensure_param_buffers(p);
     launch::reset_launches();
-    launch::validate_query(d_q, uint32_t(rows), uint32_t(dim), status_.p, st);
-    PLAID_CUDA(cudaMemsetAsync(zero_.p, 0, zero_.n * sizeof(uint32_t), st));
+    launch::query_prologue(d_q, uint32_t(rows), uint32_t(dim), status_.p, zero_.p, zero_.n, st);
 }
 
 void Searcher::batch_targets(TfOut& out, uint32_t qi, const float* d_q) {
@@ -727,7 +726,7 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
     std::memcpy(h_q_, q, rows * dim * sizeof(float));
     const bool times = trace && cfg_.record_times;
     PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, rows * dim * sizeof(float), cudaMemcpyHostToDevice, stream_));
-    enqueue(q_.p, uint32_t(rows), p, out_pids_.p, out_scores_.p, counters_.p + kNOut, stream_, times);
+    enqueue(q_.p, uint32_t(rows), p, out_pids_.p, out_scores_.p, counters_.p + kNOut, stream_, times, false);
     PLAID_CUDA(cudaMemcpyAsync(h_counters_, counters_.p, kNumCounters * sizeof(uint64_t),
                                cudaMemcpyDeviceToHost, stream_));
     PLAID_CUDA(cudaMemcpyAsync(h_pids_, out_pids_.p, p.k * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_));
@@ -781,9 +780,8 @@ void Searcher::search_device(const float* d_q, uint64_t nq, uint64_t rows, uint6
     launch::reset_launches();
     for (uint64_t j = 0; j < nq; ++j) {
         const float* q = d_q + j * rows * dim;
-        launch::validate_query(q, uint32_t(rows), uint32_t(dim), status_.p, st);
         enqueue(q, uint32_t(rows), p, d_pids + j * p.k, d_scores + j * p.k, d_n + j, st,
-                cfg_.record_times != 0);
+                cfg_.record_times != 0, true);
     }
     PLAID_CUDA(cudaGetLastError());
     last_launches_ = launch::launches();

@@ -156,8 +156,9 @@ private:
     // Enqueue one query whose rows already sit at d_q; results go to the
     // given device buffers (pids are global: local + pid_base).
     void enqueue(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
-                 float* d_scores, uint64_t* d_n, cudaStream_t st, bool times);
-    void enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st, bool times);
+                 float* d_scores, uint64_t* d_n, cudaStream_t st, bool times, bool validate);
+    void enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st, bool times,
+                       bool validate);
     void front_after_scores(uint32_t rows, const plaid_params& p, uint32_t warps, cudaStream_t st, bool times);
     void enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times);
     void enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,

@@ -368,6 +368,40 @@ __global__ void __launch_bounds__(256) validate_query_kernel(const float* __rest
     if (fabs(norm - 1.0) > double(1e-3f)) atomicExch(status, 2);  // NotNormalized + 1
 }
 
+// Per-query prologue, one PDL-chained launch instead of a memset plus the
+// validation kernel: CTA 0 checks the query rows (as validate_query_kernel,
+// when q != nullptr) and every CTA zeroes its share of the per-query
+// counters and bitmaps.
+__global__ void __launch_bounds__(256) query_prologue_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
+                                                              int* __restrict__ status, uint4* __restrict__ zero,
+                                                              uint64_t n16) {
+    dev::pdl_wait();
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * blockDim.x)
+        zero[i] = make_uint4(0, 0, 0, 0);
+    if (blockIdx.x != 0 || q == nullptr) return;
+    __shared__ float tile[32][33];
+    const uint32_t t = threadIdx.x;
+    double acc = 0.0;
+    for (uint32_t d0 = 0; d0 < dim; d0 += 32) {
+        for (uint32_t i = t; i < 32 * 32; i += blockDim.x) {
+            const uint32_t r = i >> 5, d = d0 + (i & 31);
+            tile[r][i & 31] = r < rows && d < dim ? q[size_t(r) * dim + d] : 0.f;
+        }
+        __syncthreads();
+        if (t < rows) {
+            const uint32_t m = dim - d0 < 32 ? dim - d0 : 32;
+            for (uint32_t j = 0; j < m; ++j) {
+                const double v = double(tile[t][j]);
+                acc = __dadd_rn(acc, __dmul_rn(v, v));
+            }
+        }
+        __syncthreads();
+    }
+    if (t >= rows) return;
+    const double norm = sqrt(acc);
+    if (fabs(norm - 1.0) > double(1e-3f)) atomicExch(status, 2);  // NotNormalized + 1
+}
+
 int sm_count() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -761,6 +795,15 @@ void merge_topk(const uint32_t* d_pids, const float* d_scores, const uint64_t* d
 
 void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st) {
     ::plaid::launch::pdl(copy_count_kernel, 1, 1, 0, st, src, dst, cap);
+    count_launch();
+}
+
+void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
+                    cudaStream_t st) {
+    const uint64_t n16 = nwords / 4;  // the zero region is a multiple of 16 bytes
+    const uint32_t grid = grid_for(n16, 256, uint32_t(sm_count()));
+    ::plaid::launch::pdl(query_prologue_kernel, grid, 256, 0, st, d_q, rows, dim, d_status,
+                         reinterpret_cast<uint4*>(d_zero), n16);
     count_launch();
 }
 
