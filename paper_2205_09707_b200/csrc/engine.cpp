@@ -340,16 +340,15 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
     PLAID_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     for (auto& e : ev_) PLAID_CUDA(cudaEventCreate(&e));
     const uint64_t words = index_ ? (index_->view().N + 31) / 32 : 0;
-    zero_.ensure((2 * kNumCounters + 2 * words + 3) / 4 * 4);  // whole 16-byte units (query_prologue)
+    zero_.ensure((2 * words + 3) / 4 * 4 + 4);  // bitmaps, whole 16-byte units (query_prologue)
     PLAID_CUDA(cudaMemset(zero_.p, 0, zero_.n * sizeof(uint32_t)));
-    counters_.p = reinterpret_cast<uint64_t*>(zero_.p);
-    bitmap_.p = zero_.p + 2 * kNumCounters;
+    bitmap_.p = zero_.p;
+    ensure_result_block(1);
     kconst_.ensure(1);
     status_.ensure(1);
     PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
     sel_state_.ensure(1);
     PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_q_), 32 * 256 * sizeof(float)));
-    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_counters_), kNumCounters * sizeof(uint64_t)));
     q_.ensure(32 * 256);
     if (index_) {
         const IndexView& ix = index_->view();
@@ -392,9 +391,7 @@ Searcher::~Searcher() {
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     if (h_q_) cudaFreeHost(h_q_);
-    if (h_counters_) cudaFreeHost(h_counters_);
-    if (h_pids_) cudaFreeHost(h_pids_);
-    if (h_scores_) cudaFreeHost(h_scores_);
+    if (h_res_) cudaFreeHost(h_res_);
     if (stream_) cudaStreamDestroy(stream_);
     cudaSetDevice(prev);
 }
@@ -429,22 +426,28 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
             std::min<uint64_t>({pref_.n - 1, run_.n / 32, fin_base_.n, launch::kStreamMaxPassages});
     }
     tmp_keys_.ensure(std::max<uint64_t>(std::min<uint64_t>(p.k, N), std::min<uint64_t>(p.nprobe, K)));
-    out_pids_.ensure(p.k);
-    out_scores_.ensure(p.k);
+    ensure_result_block(p.k);
     uint64_t tmp = 0;
     tmp = std::max(tmp, launch::sort_tmp_capacity(nd));
     tmp = std::max(tmp, launch::sort_tmp_capacity(std::min<uint64_t>(p.k, N)));
     tmp = std::max(tmp, launch::sort_tmp_capacity(n3));
     if (tmp) sort_tmp_.ensure(tmp);
-    if (h_cap_ < p.k) {
-        if (h_pids_) cudaFreeHost(h_pids_);
-        if (h_scores_) cudaFreeHost(h_scores_);
-        h_pids_ = nullptr;
-        h_scores_ = nullptr;
-        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_pids_), p.k * sizeof(uint32_t)));
-        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_scores_), p.k * sizeof(float)));
-        h_cap_ = p.k;
-    }
+}
+
+// res_ = [32 u64 counters | k u32 pids | k f32 scores] (16-byte aligned
+// parts): the host path reads counters and results back with ONE copy.
+void Searcher::ensure_result_block(uint64_t k) {
+    const uint64_t kk = (std::max<uint64_t>(k, 1) + 3) / 4 * 4;
+    if (res_.p && res_k_ >= kk) return;
+    res_.ensure(2 * kNumCounters + 2 * kk);
+    PLAID_CUDA(cudaMemset(res_.p, 0, res_.n * sizeof(uint32_t)));
+    res_k_ = kk;
+    counters_.p = reinterpret_cast<uint64_t*>(res_.p);
+    out_pids_p_ = res_.p + 2 * kNumCounters;
+    out_scores_p_ = reinterpret_cast<float*>(res_.p + 2 * kNumCounters + kk);
+    if (h_res_) cudaFreeHost(h_res_);
+    h_res_ = nullptr;
+    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_res_), res_.n * sizeof(uint32_t)));
 }
 
 void Searcher::record(int slot, cudaStream_t st, bool times) {
@@ -473,7 +476,8 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     // (device-resident queries) and clears the per-query counters, the
     // candidate bitmap and the stage-2 used bitmap (contiguous in zero_); the
     // "scores" phase then brackets the S_cq kernel alone
-    launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, st);
+    launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, res_.p,
+                           2 * kNumCounters, st);
     record(0, st, times);
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
@@ -667,7 +671,8 @@ void Searcher::batch_prepare(const float* d_q, uint64_t rows, uint64_t dim, cons
     DeviceGuard g(device_);
     ensure_param_buffers(p);
     launch::reset_launches();
-    launch::query_prologue(d_q, uint32_t(rows), uint32_t(dim), status_.p, zero_.p, zero_.n, st);
+    launch::query_prologue(d_q, uint32_t(rows), uint32_t(dim), status_.p, zero_.p, zero_.n, res_.p, 2 * kNumCounters,
+                           st);
 }
 
 void Searcher::batch_targets(TfOut& out, uint32_t qi, const float* d_q) {
@@ -726,18 +731,19 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
     std::memcpy(h_q_, q, rows * dim * sizeof(float));
     const bool times = trace && cfg_.record_times;
     PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, rows * dim * sizeof(float), cudaMemcpyHostToDevice, stream_));
-    enqueue(q_.p, uint32_t(rows), p, out_pids_.p, out_scores_.p, counters_.p + kNOut, stream_, times, false);
-    PLAID_CUDA(cudaMemcpyAsync(h_counters_, counters_.p, kNumCounters * sizeof(uint64_t),
-                               cudaMemcpyDeviceToHost, stream_));
-    PLAID_CUDA(cudaMemcpyAsync(h_pids_, out_pids_.p, p.k * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_));
-    PLAID_CUDA(cudaMemcpyAsync(h_scores_, out_scores_.p, p.k * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    enqueue(q_.p, uint32_t(rows), p, out_pids_p_, out_scores_p_, counters_.p + kNOut, stream_, times, false);
+    // one read-back: counters, then the k pids, then the k scores
+    const uint64_t kk = res_k_;
+    const uint64_t words = 2 * kNumCounters + kk + p.k;
+    PLAID_CUDA(cudaMemcpyAsync(h_res_, res_.p, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_));
     PLAID_CUDA(cudaStreamSynchronize(stream_));
     PLAID_CUDA(cudaGetLastError());
     last_launches_ = launch::launches();
+    const uint64_t* h_counters_ = reinterpret_cast<const uint64_t*>(h_res_);
     const uint64_t n = h_counters_[kNOut];
     *out_n = n;
-    std::memcpy(out_pids, h_pids_, n * sizeof(uint32_t));
-    std::memcpy(out_scores, h_scores_, n * sizeof(float));
+    std::memcpy(out_pids, h_res_ + 2 * kNumCounters, n * sizeof(uint32_t));
+    std::memcpy(out_scores, h_res_ + 2 * kNumCounters + kk, n * sizeof(float));
     if (trace) {
         trace->stage1_candidates = h_counters_[kN1];
         trace->centroid_matmul_count = 1;

@@ -164,6 +164,7 @@ private:
     void enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,
                       uint64_t* d_n, cudaStream_t st, bool times);
     void ensure_param_buffers(const plaid_params& p);
+    void ensure_result_block(uint64_t k);
     void record(int slot, cudaStream_t st, bool times);
 
     DeviceIndex* index_;
@@ -179,9 +180,14 @@ private:
     int phase_ = 0;
 
     // scratch
-    DevBuf<float> q_, scores_, rowmax_, out_scores_;
-    DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, out_pids_, ids_tmp_, pref_, run_, slot_of_,
-        kept_list_, acc2_;
+    DevBuf<float> q_, scores_, rowmax_;
+    DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, ids_tmp_, pref_, run_, slot_of_, kept_list_, acc2_;
+    // result block [32 u64 counters | k pids | k scores] (ensure_result_block)
+    DevBuf<uint32_t> res_;
+    uint64_t res_k_ = 0;
+    uint32_t* out_pids_p_ = nullptr;
+    float* out_scores_p_ = nullptr;
+    uint32_t* h_res_ = nullptr;
     launch::RankScratch rank_scratch_;
     DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_, bkeys_,
         tmp_keys_, kconst_;
@@ -200,10 +206,6 @@ private:
     DevBuf<int> status_;
     // pinned staging
     float* h_q_ = nullptr;
-    uint64_t* h_counters_ = nullptr;
-    uint32_t* h_pids_ = nullptr;
-    float* h_scores_ = nullptr;
-    uint64_t h_cap_ = 0;
     cudaEvent_t ev_[8] = {};
     uint64_t npartial_warps_ = 0;
     bool tensor_ = false;                   // tcgen05 S_cq path active

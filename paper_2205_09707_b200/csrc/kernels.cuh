@@ -218,10 +218,10 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
 // ---- misc ---------------------------------------------------------------------------
 // Device-side query validation (types.cpp:61-72): status 0 or NotNormalized+1.
 void validate_query(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, cudaStream_t st);
-// validate_query (when d_q != nullptr) + zero nwords u32 at d_zero (a multiple
-// of 4 words, 16-byte aligned): one launch.
+// validate_query (when d_q != nullptr) + zero nwords u32 at d_zero and nwords2
+// at d_zero2 (multiples of 4 words, 16-byte aligned): one launch.
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
-                    cudaStream_t st);
+                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st);
 // Stage counters: min() bookkeeping done on device.
 void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st);
 // Merge G shard top-k lists into the global top-k.

@@ -374,10 +374,13 @@ __global__ void __launch_bounds__(256) validate_query_kernel(const float* __rest
 // counters and bitmaps.
 __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
                                                               int* __restrict__ status, uint4* __restrict__ zero,
-                                                              uint64_t n16) {
+                                                              uint64_t n16, uint4* __restrict__ zero2, uint64_t m16) {
     dev::pdl_wait();
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * blockDim.x)
-        zero[i] = make_uint4(0, 0, 0, 0);
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16 + m16;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        if (i < n16) zero[i] = make_uint4(0, 0, 0, 0);
+        else zero2[i - n16] = make_uint4(0, 0, 0, 0);
+    }
     if (blockIdx.x != 0 || q == nullptr) return;
     __shared__ float tile[32][33];
     const uint32_t t = threadIdx.x;
@@ -799,11 +802,11 @@ void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t s
 }
 
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
-                    cudaStream_t st) {
-    const uint64_t n16 = nwords / 4;  // the zero region is a multiple of 16 bytes
-    const uint32_t grid = grid_for(n16, 256, uint32_t(sm_count()));
+                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st) {
+    const uint64_t n16 = nwords / 4, m16 = nwords2 / 4;  // both regions are multiples of 16 bytes
+    const uint32_t grid = grid_for(n16 + m16, 256, uint32_t(sm_count()));
     ::plaid::launch::pdl(query_prologue_kernel, grid, 256, 0, st, d_q, rows, dim, d_status,
-                         reinterpret_cast<uint4*>(d_zero), n16);
+                         reinterpret_cast<uint4*>(d_zero), n16, reinterpret_cast<uint4*>(d_zero2), m16);
     count_launch();
 }
 
