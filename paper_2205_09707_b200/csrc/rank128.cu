@@ -208,6 +208,11 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
             const uint32_t b = k & 1;
             mbar_wait(&empty_bar[b], ((k >> 1) & 1) ^ 1);
             if (pw == 0) rank_stamp(dbg, 0, k);
+            if (dbg & 2) {  // experiment: no decompression (consumers score stale tiles)
+                if (k < 2) pass_s[b][pw * 32 + lane] = 0xFFFFFFFFu - pw;
+                mbar_arrive(&full_bar[b]);
+                continue;
+            }
             float* tile = tiles + b * kTile * kPitch + pw * 32 * kPitch;
             const uint32_t g0 = tl * kTile + pw * 32;
             const uint32_t g = g0 + lane;
