@@ -497,12 +497,14 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
     uint32_t* owners = bitmap_.p + (N + 31) / 32;
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
     uint64_t nsel;
+    bool bitmap_done = false;
     if (p.nprobe == K) {
         launch::iota(sel_.p, K, st);
         nsel = K;
     } else if (p.nprobe <= 32) {
-        launch::topn_merge(partial_.p, warps, npb, rows, uint32_t(p.nprobe), sel_.p, st);
+        launch::topn_postings(partial_.p, warps, npb, rows, uint32_t(p.nprobe), ix, sel_.p, bitmap, st);
         nsel = uint64_t(rows) * p.nprobe;
+        bitmap_done = true;
     } else {
         for (uint32_t i = 0; i < rows; ++i) {
             launch::token_keys(scores_.p, K, i, tok_keys_.p, st);
@@ -512,7 +514,7 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
         }
         nsel = uint64_t(rows) * p.nprobe;
     }
-    launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap, st);
+    if (!bitmap_done) launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap, st);
     launch::bitmap_compact(bitmap, N, chunk_counts_.p, c1_.p, c + kN1, slot_of_.p, st);
     record(2, st, times);
     if (p.disable_filter) {

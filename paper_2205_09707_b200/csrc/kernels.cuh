@@ -114,6 +114,9 @@ uint32_t scores_tensor_max_warps();
 uint32_t scores_tensor_batch(const void* cmap, const IndexView& ix, const TfOut& out, uint32_t qb, uint32_t rows,
                              float t_cs, uint32_t np_bucket, cudaStream_t st);
 [[noreturn]] void fail_cuda_driver(int code, const char* what);
+// topn_merge + postings_to_bitmap in one launch (rows x nprobe CTAs).
+void topn_postings(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows, uint32_t nprobe,
+                   const IndexView& ix, uint32_t* d_sel, uint32_t* d_bitmap, cudaStream_t st);
 // Merge per-warp partial top-NP lists into sel[rows][nprobe] centroid ids.
 void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,
                 uint32_t nprobe, uint32_t* d_sel, cudaStream_t st);

@@ -110,12 +110,11 @@ scores_exact_kernel(const float* __restrict__ C, uint64_t K, uint32_t dim,
 }
 
 // One block per query token: merge every warp's top-NP list for that token.
+// One CTA: token i's best NP keys over the nwarps partial lists, left
+// descending in lists[0..NP).
 template <int NP>
-__global__ void topn_merge_kernel(const uint64_t* __restrict__ partial, uint32_t nwarps,
-                                  uint32_t nprobe, uint32_t* __restrict__ sel) {
-    dev::pdl_wait();
-    extern __shared__ uint64_t lists[];  // blockDim x NP
-    const uint32_t i = blockIdx.x;
+__device__ void merge_token_lists(const uint64_t* __restrict__ partial, uint32_t nwarps, uint32_t i,
+                                  uint64_t* lists) {
     uint64_t top[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) top[j] = 0;
@@ -147,7 +146,37 @@ __global__ void topn_merge_kernel(const uint64_t* __restrict__ partial, uint32_t
         }
         __syncthreads();
     }
+}
+
+template <int NP>
+__global__ void topn_merge_kernel(const uint64_t* __restrict__ partial, uint32_t nwarps,
+                                  uint32_t nprobe, uint32_t* __restrict__ sel) {
+    dev::pdl_wait();
+    extern __shared__ uint64_t lists[];  // blockDim x NP
+    const uint32_t i = blockIdx.x;
+    merge_token_lists<NP>(partial, nwarps, i, lists);
     if (threadIdx.x < nprobe) sel[i * nprobe + threadIdx.x] = dev::key_id(lists[threadIdx.x]);
+}
+
+// Candidate generation in one launch (pipeline.cpp:52-87): CTA (i, j) merges
+// token i's partial lists (every CTA of the token redundantly — a few tens
+// of KB from L2) and ORs the postings of the token's j-th best centroid into
+// the N-bit candidate bitmap.
+template <int NP>
+__global__ void topn_postings_kernel(const uint64_t* __restrict__ partial, uint32_t nwarps, uint32_t nprobe,
+                                     const uint64_t* __restrict__ ivf_offsets, const uint32_t* __restrict__ postings,
+                                     uint32_t* __restrict__ sel, uint32_t* __restrict__ bitmap) {
+    dev::pdl_wait();
+    extern __shared__ uint64_t lists[];  // blockDim x NP
+    const uint32_t i = blockIdx.x / nprobe, j = blockIdx.x % nprobe;
+    merge_token_lists<NP>(partial, nwarps, i, lists);
+    const uint32_t c = dev::key_id(lists[j]);
+    if (threadIdx.x == 0) sel[i * nprobe + j] = c;
+    const uint64_t b = ivf_offsets[c], e = ivf_offsets[c + 1];
+    for (uint64_t t = b + threadIdx.x; t < e; t += blockDim.x) {
+        const uint32_t p = __ldg(postings + t);
+        atomicOr(bitmap + (p >> 5), 1u << (p & 31));
+    }
 }
 
 __global__ void token_keys_kernel(const float* __restrict__ S, uint64_t K, uint32_t i,
@@ -278,6 +307,21 @@ void launch_merge(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint3
     launch::count_launch();
 }
 
+template <int NP>
+void launch_topn_postings(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint32_t nprobe,
+                          const IndexView& ix, uint32_t* sel, uint32_t* bitmap, cudaStream_t st) {
+    const uint32_t threads = 256;
+    const size_t smem = threads * NP * sizeof(uint64_t);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(topn_postings_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = true;
+    }
+    ::plaid::launch::pdl(topn_postings_kernel<NP>, rows * nprobe, threads, smem, st, partial, nwarps, nprobe,
+                         ix.ivf_offsets, ix.ivf_postings, sel, bitmap);
+    launch::count_launch();
+}
+
 }  // namespace
 
 namespace launch {
@@ -301,6 +345,18 @@ uint32_t scores_exact(const IndexView& ix, const float* d_q, uint32_t rows, floa
         default: launch_scores<32>(ix, d_q, rows, t_cs, d_scores, d_rowmax, d_keep_bits, d_partial, blocks, st); break;
     }
     return blocks * kWarpsPerBlock;
+}
+
+void topn_postings(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows, uint32_t nprobe,
+                   const IndexView& ix, uint32_t* d_sel, uint32_t* d_bitmap, cudaStream_t st) {
+    switch (np_bucket) {
+        case 1: launch_topn_postings<1>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
+        case 2: launch_topn_postings<2>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
+        case 4: launch_topn_postings<4>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
+        case 8: launch_topn_postings<8>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
+        case 16: launch_topn_postings<16>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
+        default: launch_topn_postings<32>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
+    }
 }
 
 void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,
