@@ -111,7 +111,7 @@ typedef struct plaid_trace {
 typedef struct plaid_searcher_config {
     int32_t score_mode;     /* plaid_score_mode */
     int32_t record_times;   /* fill the *_ms fields of plaid_trace (adds events) */
-    int32_t use_graphs;     /* replay captured CUDA graphs per parameter set */
+    int32_t use_graphs;     /* plaid_search: capture H2D + launches + read-back as one CUDA graph per (rows, params), replay after */
     int32_t reserved;
 } plaid_searcher_config;
 

@@ -5,6 +5,7 @@
 #include "device.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -175,9 +176,12 @@ void validate_index_host(const plaid_index_desc& d) {
 }
 
 // ---------------------------------------------------------------- DevBuf
+std::atomic<uint64_t> g_alloc_generation{0};  // bumped by every reallocation (captured graphs go stale)
+
 template <typename T>
 void DevBuf<T>::ensure(uint64_t count) {
     if (count <= n && p) return;
+    g_alloc_generation.fetch_add(1);
     release();
     const uint64_t c = count ? count : 1;
     PLAID_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), c * sizeof(T)));
@@ -388,6 +392,7 @@ Searcher::~Searcher() {
     cudaGetDevice(&prev);
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& e : graphs_) cudaGraphExecDestroy(e.exec);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     if (h_q_) cudaFreeHost(h_q_);
@@ -732,15 +737,56 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
     launch::reset_launches();
     std::memcpy(h_q_, q, rows * dim * sizeof(float));
     const bool times = trace && cfg_.record_times;
-    PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, rows * dim * sizeof(float), cudaMemcpyHostToDevice, stream_));
-    enqueue(q_.p, uint32_t(rows), p, out_pids_p_, out_scores_p_, counters_.p + kNOut, stream_, times, false);
-    // one read-back: counters, then the k pids, then the k scores
     const uint64_t kk = res_k_;
     const uint64_t words = 2 * kNumCounters + kk + p.k;
-    PLAID_CUDA(cudaMemcpyAsync(h_res_, res_.p, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_));
+    // H2D of Q, the launch sequence, one read-back of [counters | pids | scores]
+    auto body = [&] {
+        PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, rows * dim * sizeof(float), cudaMemcpyHostToDevice, stream_));
+        enqueue(q_.p, uint32_t(rows), p, out_pids_p_, out_scores_p_, counters_.p + kNOut, stream_, times, false);
+        PLAID_CUDA(cudaMemcpyAsync(h_res_, res_.p, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_));
+    };
+    if (cfg_.use_graphs && !times) {
+        // one CUDA graph per (rows, params): captured on first use, replayed
+        // after; every buffer it touches is owned by this searcher, and any
+        // reallocation (g_alloc_generation) makes the cached graphs stale
+        GraphKey key{rows, p.k, p.nprobe, p.ndocs, p.disable_filter, 0};
+        std::memcpy(&key.t_cs_bits, &p.t_cs, 4);
+        const uint64_t gen = g_alloc_generation.load();
+        GraphEntry* hit = nullptr;
+        for (auto& e : graphs_)
+            if (e.key == key) hit = &e;
+        if (hit && hit->gen != gen) {
+            cudaGraphExecDestroy(hit->exec);
+            *hit = graphs_.back();
+            graphs_.pop_back();
+            hit = nullptr;
+        }
+        if (!hit) {
+            cudaGraph_t graph = nullptr;
+            PLAID_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+            try {
+                body();
+            } catch (...) {
+                cudaStreamEndCapture(stream_, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            PLAID_CUDA(cudaStreamEndCapture(stream_, &graph));
+            GraphEntry e{key, gen, nullptr, launch::launches()};
+            const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+            cudaGraphDestroy(graph);
+            PLAID_CUDA(ie);
+            graphs_.push_back(e);
+            hit = &graphs_.back();
+        }
+        PLAID_CUDA(cudaGraphLaunch(hit->exec, stream_));
+        last_launches_ = hit->launches;
+    } else {
+        body();
+        last_launches_ = launch::launches();
+    }
     PLAID_CUDA(cudaStreamSynchronize(stream_));
     PLAID_CUDA(cudaGetLastError());
-    last_launches_ = launch::launches();
     const uint64_t* h_counters_ = reinterpret_cast<const uint64_t*>(h_res_);
     const uint64_t n = h_counters_[kNOut];
     *out_n = n;

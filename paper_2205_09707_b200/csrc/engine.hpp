@@ -172,6 +172,23 @@ private:
     plaid_searcher_config cfg_;
     cudaStream_t stream_ = nullptr;
     uint64_t last_launches_ = 0;
+    // captured host-path graphs (plaid_searcher_config.use_graphs)
+    struct GraphKey {
+        uint64_t rows, k, nprobe, ndocs;
+        int32_t disable_filter;
+        uint32_t t_cs_bits;
+        bool operator==(const GraphKey& o) const {
+            return rows == o.rows && k == o.k && nprobe == o.nprobe && ndocs == o.ndocs &&
+                   disable_filter == o.disable_filter && t_cs_bits == o.t_cs_bits;
+        }
+    };
+    struct GraphEntry {
+        GraphKey key;
+        uint64_t gen;
+        cudaGraphExec_t exec;
+        uint64_t launches;
+    };
+    std::vector<GraphEntry> graphs_;
     // sharded-search state between shard_phase calls
     plaid_params pending_{};
     const float* pending_q_ = nullptr;

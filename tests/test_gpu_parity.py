@@ -353,3 +353,20 @@ def test_index_open_gpu_checksums(tmp_path, small, port):
     with pytest.raises(P.PlaidError) as e:
         P.DeviceIndex.open(tmp_path)
     assert e.value.code == P.ErrorCode.LengthMismatch
+
+
+def test_graph_replay_matches_eager(small, port):
+    """use_graphs: the host path captured as one CUDA graph per (rows, params)
+    and replayed returns exactly the eager results; growing k re-allocates
+    the result block, so the cached graphs are re-captured."""
+    h, qs, idx, s = small
+    g = P.Searcher(idx, score_mode=P.ScoreMode.EXACT, use_graphs=True)
+    for k in (10, 100, 10, 1000, 100):
+        p = P.default_params_for_k(k)
+        for q in qs:
+            a, b = s.search(q, p), g.search(q, p)
+            assert np.array_equal(a.topk.passage_ids, b.topk.passage_ids), k
+            assert np.array_equal(bits(a.topk.scores), bits(b.topk.scores)), k
+            assert a.trace.counters() == b.trace.counters()
+        ids, sc, _ = port.search(h, qs[0], p)
+        assert np.array_equal(g.search(qs[0], p).topk.passage_ids, ids)
