@@ -206,6 +206,26 @@ plaid_status plaid_merge_topk_device(plaid_searcher* s, const uint32_t* d_pids,
                                      uint64_t shards, uint64_t stride, uint64_t k, uint32_t* d_out_pids,
                                      float* d_out_scores, uint64_t* d_out_n, uint64_t stream);
 
+/* ---- encode on the GPU -----------------------------------------
+ * Given trained centroids and quantizer, what lir::build_index derives from
+ * them (indexer.cpp:197-282): codes = assign_codes (exact in-order fp32 dots,
+ * first max wins), residuals = quantise + LSB-first pack, the IVF =
+ * build_inverted_list.  Bit-identical to the reference.  Host buffers in and
+ * out; the embeddings are T x dim unit rows (NotNormalized otherwise). */
+typedef struct plaid_encode_desc {
+    uint32_t dim;
+    uint32_t nbits;
+    uint64_t num_centroids;       /* K */
+    uint64_t num_passages;        /* N */
+    uint64_t num_embeddings;      /* T = sum(doclens) */
+    const float* embeddings;      /* T x dim */
+    const uint32_t* doclens;      /* N */
+    const float* centroids;       /* K x dim */
+    const float* bucket_cutoffs;  /* 2^nbits - 1 */
+} plaid_encode_desc;
+plaid_status plaid_encode(const plaid_encode_desc* in, int device, uint32_t* codes, uint8_t* residuals,
+                          uint64_t* ivf_offsets, uint32_t* ivf_postings, uint64_t postings_cap, uint64_t* num_postings);
+
 /* ---- throughput mode (BASELINE configs[2]: batched queries) ---------------------------
  * `lanes` searchers (own CUDA stream + scratch each) over one index; query j of
  * a batch runs on lane j mod lanes, so the stages of different queries overlap

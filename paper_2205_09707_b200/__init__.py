@@ -7,7 +7,7 @@ deterministic synthetic index generator used by tests and the bench.
 """
 from .api import (BatchSearcher, CandidateSet, DeviceIndex, ErrorCode, PlaidError, ScoreMode, SearchOptions,
                   SearchParams, SearchResult, Searcher, StageTrace, default_params_for_k,
-                  checksum, lut_build, pack_residual, save_index, search, stage3_width, validate_params,
+                  checksum, encode_corpus, lut_build, pack_residual, save_index, search, stage3_width, validate_params,
                   validate_query)
 from .hostindex import (HostIndex, build_inverted_list, fnv_digest, generate_index, generate_queries,
                         load_index_host, quantizer)
@@ -16,6 +16,6 @@ __all__ = [
     "CandidateSet", "DeviceIndex", "ErrorCode", "PlaidError", "ScoreMode", "SearchOptions",
     "BatchSearcher", "SearchParams", "SearchResult", "Searcher", "StageTrace", "default_params_for_k", "lut_build",
     "pack_residual", "search", "stage3_width", "validate_params", "validate_query", "HostIndex",
-    "build_inverted_list", "generate_index", "generate_queries", "quantizer", "save_index", "checksum",
+    "build_inverted_list", "generate_index", "generate_queries", "quantizer", "save_index", "checksum", "encode_corpus",
     "fnv_digest", "load_index_host",
 ]

@@ -40,6 +40,12 @@ class Trace(C.Structure):
             "scoring_ms", "total_ms")] + [("decompressed_tokens", C.c_uint64)]
 
 
+class EncodeDesc(C.Structure):
+    _fields_ = [("dim", C.c_uint32), ("nbits", C.c_uint32), ("num_centroids", C.c_uint64),
+                ("num_passages", C.c_uint64), ("num_embeddings", C.c_uint64), ("embeddings", C.c_void_p),
+                ("doclens", C.c_void_p), ("centroids", C.c_void_p), ("bucket_cutoffs", C.c_void_p)]
+
+
 class SearcherConfig(C.Structure):
     _fields_ = [("score_mode", C.c_int32), ("record_times", C.c_int32),
                 ("use_graphs", C.c_int32), ("reserved", C.c_int32)]
@@ -69,6 +75,7 @@ SIGNATURES = {
                                      u32p, f32p, u64p, C.POINTER(Trace)]),
     "plaid_search_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                       C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "plaid_encode": (C.c_int, [C.POINTER(EncodeDesc), C.c_int, u32p, u8p, u64p, u32p, C.c_uint64, u64p]),
     "plaid_index_save": (C.c_int, [C.POINTER(IndexDesc), C.c_char_p, C.c_uint64]),
     "plaid_index_open": (C.c_int, [C.c_char_p, C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
     "plaid_checksum": (C.c_uint64, [C.c_void_p, C.c_uint64]),

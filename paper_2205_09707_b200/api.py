@@ -172,6 +172,30 @@ def _desc(h: HostIndex) -> N.IndexDesc:
                        N.ptr(h.bucket_cutoffs, C.c_float), N.ptr(h.bucket_weights, C.c_float))
 
 
+def encode_corpus(embeddings: np.ndarray, doclens: np.ndarray, centroids: np.ndarray, bucket_cutoffs: np.ndarray,
+                  bucket_weights: np.ndarray, nbits: int, device: int = 0) -> HostIndex:
+    """The encode half of lir::build_index on the GPU (indexer.cpp:197-282):
+    codes (exact assign_codes), packed residuals and the IVF for trained
+    centroids + quantizer; returns the HostIndex (bit-identical to the
+    reference's)."""
+    emb = np.ascontiguousarray(embeddings, dtype=np.float32)
+    dl = np.ascontiguousarray(doclens, dtype=np.uint32)
+    cents = np.ascontiguousarray(centroids, dtype=np.float32)
+    cut = np.ascontiguousarray(bucket_cutoffs, dtype=np.float32)
+    T, dim = emb.shape
+    K = cents.shape[0]
+    d = N.EncodeDesc(dim, nbits, K, dl.size, T, emb.ctypes.data, dl.ctypes.data, cents.ctypes.data, cut.ctypes.data)
+    codes = np.zeros(max(T, 1), dtype=np.uint32)
+    res = np.zeros(max(T * nbits * dim // 8, 1), dtype=np.uint8)
+    ivo = np.zeros(K + 1, dtype=np.uint64)
+    post = np.zeros(max(T, 1), dtype=np.uint32)
+    n = C.c_uint64()
+    _check(N.load().plaid_encode(C.byref(d), device, N.ptr(codes, C.c_uint32), N.ptr(res, C.c_uint8),
+                                 N.ptr(ivo, C.c_uint64), N.ptr(post, C.c_uint32), post.size, C.byref(n)))
+    return HostIndex(dim, nbits, cents, codes[:T], res[: T * nbits * dim // 8], dl, ivo, post[: n.value], cut,
+                     np.ascontiguousarray(bucket_weights, dtype=np.float32))
+
+
 def save_index(h: HostIndex, path: str, rng_seed: int = 0) -> None:
     """Write `h` in the on-disk format (FORMAT.md; SPEC.md storage module)."""
     d = _desc(h)

@@ -9,6 +9,7 @@
 
 #include "engine.hpp"
 #include "storage.hpp"
+#include "encode.hpp"
 
 struct plaid_index {
     std::unique_ptr<plaid::DeviceIndex> impl;
@@ -252,6 +253,16 @@ plaid_status plaid_index_open(const char* dir, int device, uint32_t flags, plaid
 }
 
 uint64_t plaid_checksum(const void* data, uint64_t bytes) { return plaid::checksum_host(data, bytes); }
+
+plaid_status plaid_encode(const plaid_encode_desc* in, int device, uint32_t* codes, uint8_t* residuals,
+                          uint64_t* ivf_offsets, uint32_t* ivf_postings, uint64_t postings_cap, uint64_t* num_postings) {
+    return guarded([&] {
+        need(in, "in");
+        need(num_postings, "num_postings");
+        *num_postings = 0;
+        plaid::encode_host(*in, device, codes, residuals, ivf_offsets, ivf_postings, postings_cap, num_postings);
+    });
+}
 
 
 

@@ -370,3 +370,44 @@ def test_graph_replay_matches_eager(small, port):
             assert a.trace.counters() == b.trace.counters()
         ids, sc, _ = port.search(h, qs[0], p)
         assert np.array_equal(g.search(qs[0], p).topk.passage_ids, ids)
+
+
+@pytest.mark.parametrize("dim,nbits,K", [(64, 2, 96), (128, 1, 300), (32, 4, 17)])
+def test_encode_matches_reference_build(dim, nbits, K):
+    """GPU encode (assign_codes, quantise + pack, build_inverted_list) of a
+    corpus against the centroids and quantizer the reference's build_index
+    trained on it: codes, residual bytes and the IVF are bit-identical."""
+    import oracle
+
+    if not oracle.available("ref"):
+        pytest.skip("compiled reference not available")
+    ref = oracle.get("ref")
+    rng = np.random.default_rng(dim + K)
+    doclens = rng.integers(1, 40, 250).astype(np.uint32)
+    x = rng.standard_normal((int(doclens.sum()), dim)).astype(np.float32)
+    x /= np.linalg.norm(x.astype(np.float64), axis=1, keepdims=True).astype(np.float32)
+    x = (x / np.linalg.norm(x.astype(np.float64), axis=1, keepdims=True)).astype(np.float32)
+    d = ref.build_index(x, doclens, dim, nbits, K, iters=3, seed=5)
+    h = P.encode_corpus(x, doclens, d["centroids"], d["bucket_cutoffs"], d["bucket_weights"], nbits)
+    assert np.array_equal(h.codes, d["codes"])
+    assert np.array_equal(h.residuals, d["residuals"])
+    assert np.array_equal(h.ivf_offsets, d["ivf_offsets"])
+    assert np.array_equal(h.ivf_postings, d["ivf_postings"])
+    # and the encoded index searches like the reference-built one
+    port = oracle.get("port")
+    hr = P.HostIndex(dim, nbits, d["centroids"], d["codes"], d["residuals"], d["doclens"], d["ivf_offsets"],
+                     d["ivf_postings"], d["bucket_cutoffs"], d["bucket_weights"])
+    q = x[:32] if dim >= 32 else x[:32]
+    s = P.Searcher(P.DeviceIndex.from_host(h), score_mode=P.ScoreMode.EXACT)
+    p = P.SearchParams(10, 2, 0.3, 64)
+    got = s.search(q, p)
+    ids, sc, _ = port.search(hr, q, p)
+    assert np.array_equal(got.topk.passage_ids, ids)
+
+
+def test_encode_rejects_bad_corpus():
+    x = np.ones((4, 8), np.float32)
+    with pytest.raises(P.PlaidError) as e:
+        P.encode_corpus(x, np.array([2, 2], np.uint32), np.eye(8, dtype=np.float32)[:2], np.zeros(3, np.float32),
+                        np.zeros(4, np.float32), 2)
+    assert e.value.code == P.ErrorCode.NotNormalized
