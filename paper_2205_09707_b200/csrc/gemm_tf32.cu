@@ -401,7 +401,8 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
             const uint64_t c0 = t * 128 + q * 32;
             const uint64_t c = c0 + lane;
             const bool valid = c < K;
-            const uint32_t nv = K - c0 < 32 ? uint32_t(K - c0) : 32u;
+            // centroids of this lane quarter (0 past the end of a partial last tile)
+            const uint32_t nv = c0 >= K ? 0u : (K - c0 < 32 ? uint32_t(K - c0) : 32u);
 #pragma unroll
             for (int qi = 0; qi < QB; ++qi) {
                 uint32_t rh[32], rl[32];

@@ -168,6 +168,10 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
     dev::pdl_wait();
     extern __shared__ __align__(16) float sm[];
     __shared__ float w_s[16];
+    // the 4 bucket weights of every (4 NB)-bit residual group (NB <= 2): one
+    // LDS.128 per 4 dims instead of 4 index extractions and 4 lookups
+    constexpr uint32_t kLutN = NB <= 2 ? (1u << (4 * NB)) : 1u;
+    __shared__ float4 w_lut[kLutN];
     __shared__ uint32_t pass_s[2][kTile];
     __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
     constexpr uint32_t kBpt = NB * 128 / 8;
@@ -181,6 +185,11 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
     const uint32_t ntiles = (T + kTile - 1) / kTile;
     if (blockIdx.x >= ntiles) return;
     if (threadIdx.x < 16) w_s[threadIdx.x] = W.w[threadIdx.x];
+    if (NB <= 2) {
+        constexpr uint32_t m = (1u << NB) - 1;
+        for (uint32_t e = threadIdx.x; e < kLutN; e += blockDim.x)
+            w_lut[e] = make_float4(W.w[e & m], W.w[(e >> NB) & m], W.w[(e >> (2 * NB)) & m], W.w[(e >> (3 * NB)) & m]);
+    }
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; ++b) {
             mbar_init(&full_bar[b], kProducers * 32);
@@ -253,15 +262,26 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
                     // dims 4*d4 .. 4*d4+3 <- 4*NB bits from bit 4*d4*NB (LSB-first packing)
                     const uint32_t word = rb[(4 * d4 * NB) / 32] >> ((4 * d4 * NB) % 32);
                     float4 x = row[d4];
-                    x.x = __fadd_rn(x.x, w_s[(word >> (0 * NB)) & mask]);
-                    x.y = __fadd_rn(x.y, w_s[(word >> (1 * NB)) & mask]);
-                    x.z = __fadd_rn(x.z, w_s[(word >> (2 * NB)) & mask]);
-                    x.w = __fadd_rn(x.w, w_s[(word >> (3 * NB)) & mask]);
+                    if (NB <= 2) {
+                        const float4 w4 = w_lut[word & (kLutN - 1)];
+                        x.x = __fadd_rn(x.x, w4.x);
+                        x.y = __fadd_rn(x.y, w4.y);
+                        x.z = __fadd_rn(x.z, w4.z);
+                        x.w = __fadd_rn(x.w, w4.w);
+                    } else {
+                        x.x = __fadd_rn(x.x, w_s[(word >> (0 * NB)) & mask]);
+                        x.y = __fadd_rn(x.y, w_s[(word >> (1 * NB)) & mask]);
+                        x.z = __fadd_rn(x.z, w_s[(word >> (2 * NB)) & mask]);
+                        x.w = __fadd_rn(x.w, w_s[(word >> (3 * NB)) & mask]);
+                    }
                     row[d4] = x;
-                    acc = __dadd_rn(acc, __dmul_rn(double(x.x), double(x.x)));
-                    acc = __dadd_rn(acc, __dmul_rn(double(x.y), double(x.y)));
-                    acc = __dadd_rn(acc, __dmul_rn(double(x.z), double(x.z)));
-                    acc = __dadd_rn(acc, __dmul_rn(double(x.w), double(x.w)));
+                    // norm^2 += double(x)^2 in order (residual_codec.cpp:113-130): the
+                    // square of a float is exact in double (48 <= 53 significand bits),
+                    // so one fused multiply-add rounds exactly like the separate add
+                    acc = __fma_rn(double(x.x), double(x.x), acc);
+                    acc = __fma_rn(double(x.y), double(x.y), acc);
+                    acc = __fma_rn(double(x.z), double(x.z), acc);
+                    acc = __fma_rn(double(x.w), double(x.w), acc);
                 }
                 if (acc > 0.0) {
                     const float inv = float(1.0 / sqrt(acc));

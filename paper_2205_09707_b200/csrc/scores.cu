@@ -61,7 +61,8 @@ scores_exact_kernel(const float* __restrict__ C, uint64_t K, uint32_t dim,
         uint32_t keep_word = 0;
         for (int g = 0; g < 32 / kG; ++g) {
             const uint64_t c0 = chunk * 32 + g * kG;
-            const uint32_t nc = uint32_t(K - c0 < kG ? K - c0 : kG);
+            // centroids of this group (0 past the end of a partial last chunk)
+            const uint32_t nc = c0 >= K ? 0u : uint32_t(K - c0 < kG ? K - c0 : kG);
             // stage the group's rows (contiguous in HBM) into shared memory
             const float4* src = reinterpret_cast<const float4*>(C + c0 * dim);
             float4* dst = reinterpret_cast<float4*>(c_s);

@@ -411,3 +411,24 @@ def test_encode_rejects_bad_corpus():
         P.encode_corpus(x, np.array([2, 2], np.uint32), np.eye(8, dtype=np.float32)[:2], np.zeros(3, np.float32),
                         np.zeros(4, np.float32), 2)
     assert e.value.code == P.ErrorCode.NotNormalized
+
+
+@pytest.mark.parametrize("K", [300, 129, 33])
+def test_partial_last_tile(port, K):
+    """K not a multiple of the S_cq tile (128 centroids, 32 per lane group):
+    both score modes must ignore the rows past K (regression: an unsigned
+    underflow let the last tile write S rows and candidate ids beyond K)."""
+    h = P.generate_index(1500, K, dim=128, nbits=2, mean_len=30, seed=K)
+    qs = P.generate_queries(h, 3, seed=1)
+    idx = P.DeviceIndex.from_host(h)
+    for mode in (P.ScoreMode.EXACT, P.ScoreMode.TENSOR):
+        s = P.Searcher(idx, score_mode=mode)
+        for q in qs:
+            S, mx = s.compute_centroid_scores(q)
+            S0, mx0 = port.compute_centroid_scores(h, q)
+            assert np.abs(S - S0).max() < 5e-6
+            got = s.search(q, P.default_params_for_k(10))
+            if mode == P.ScoreMode.EXACT:
+                ids, sc, _ = port.search(h, q, P.default_params_for_k(10))
+                assert np.array_equal(got.topk.passage_ids, ids)
+            assert np.all(got.topk.passage_ids < h.num_passages)
