@@ -432,3 +432,31 @@ def test_partial_last_tile(port, K):
                 ids, sc, _ = port.search(h, q, P.default_params_for_k(10))
                 assert np.array_equal(got.topk.passage_ids, ids)
             assert np.all(got.topk.passage_ids < h.num_passages)
+
+
+def test_edge_cases(port):
+    """Empty stage-1 candidate set (pipeline.cpp:249-252: empty result), the
+    generic nprobe > 32 path, short queries (|Q| < 32), k above the corpus."""
+    rng = np.random.default_rng(3)
+    base = P.generate_index(400, 64, dim=64, nbits=2, mean_len=12, spread=4, seed=8)
+    # move every token onto centroids 0..31: centroids 32..63 own no passages
+    codes = (base.codes % 32).astype(np.uint32)
+    ivf_off, post = P.build_inverted_list(codes, base.doclens, 64)
+    h = P.HostIndex(base.dim, base.nbits, base.centroids, codes, base.residuals, base.doclens, ivf_off, post,
+                    base.bucket_cutoffs, base.bucket_weights)
+    s = P.Searcher(P.DeviceIndex.from_host(h), score_mode=P.ScoreMode.EXACT)
+    q = np.repeat(h.centroids[63:64], 4, axis=0)  # its only top-1 centroid is empty
+    for p in (P.SearchParams(10, 1, 0.5, 64), P.SearchParams(5, 1, -1.0, 64)):
+        got = s.search(q, p)
+        ids, sc, tr = port.search(h, q, p)
+        assert len(got.topk) == 0 == len(ids) and got.trace.counters() == tr
+    qs = P.generate_queries(h, 3, seed=4)
+    for rows in (1, 8, 32):
+        for p in (P.SearchParams(10, 40, 0.4, 256), P.SearchParams(500, 6, 0.3, 2000), P.SearchParams(3, 63, 0.5, 12)):
+            for q in qs:
+                qq = q[:rows] if rows < 32 else q
+                got = s.search(qq, p)
+                ids, sc, tr = port.search(h, qq, p)
+                assert np.array_equal(got.topk.passage_ids, ids), (rows, p)
+                assert np.array_equal(bits(got.topk.scores), bits(sc))
+                assert got.trace.counters() == tr
