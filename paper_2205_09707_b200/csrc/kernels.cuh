@@ -219,9 +219,8 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
                     const RankScratch& s, cudaStream_t st);
 
 // ---- misc ---------------------------------------------------------------------------
-// Device-side query validation (types.cpp:61-72): status 0 or NotNormalized+1.
-void validate_query(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, cudaStream_t st);
-// validate_query (when d_q != nullptr) + zero nwords u32 at d_zero and nwords2
+// Device-side query validation (types.cpp:61-72, status 0 or NotNormalized+1)
+// query validation (when d_q != nullptr) + zero nwords u32 at d_zero and nwords2
 // at d_zero2 (multiples of 4 words, 16-byte aligned): one launch.
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
                     uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st);

@@ -338,40 +338,13 @@ __global__ void copy_count_kernel(const uint64_t* src, uint64_t* dst, uint64_t c
     *dst = v < cap ? v : cap;
 }
 
-// types.cpp:10-19 check_unit_rows: norm^2 = sum of double(v)^2 in order.  The
-// products are exact in fp64 (24-bit mantissas), so only the adds must stay
-// in order: 32-dim chunks of Q are staged coalesced in shared memory and
-// thread r runs row r's dependent add chain from there.
-__global__ void __launch_bounds__(256) validate_query_kernel(const float* __restrict__ q, uint32_t rows,
-                                                              uint32_t dim, int* __restrict__ status) {
-    dev::pdl_wait();
-    __shared__ float tile[32][33];
-    const uint32_t t = threadIdx.x;
-    double acc = 0.0;
-    for (uint32_t d0 = 0; d0 < dim; d0 += 32) {
-        for (uint32_t i = t; i < 32 * 32; i += blockDim.x) {
-            const uint32_t r = i >> 5, d = d0 + (i & 31);
-            tile[r][i & 31] = r < rows && d < dim ? q[size_t(r) * dim + d] : 0.f;
-        }
-        __syncthreads();
-        if (t < rows) {
-            const uint32_t m = dim - d0 < 32 ? dim - d0 : 32;
-            for (uint32_t j = 0; j < m; ++j) {
-                const double v = double(tile[t][j]);
-                acc = __dadd_rn(acc, __dmul_rn(v, v));
-            }
-        }
-        __syncthreads();
-    }
-    if (t >= rows) return;
-    const double norm = sqrt(acc);
-    if (fabs(norm - 1.0) > double(1e-3f)) atomicExch(status, 2);  // NotNormalized + 1
-}
-
-// Per-query prologue, one PDL-chained launch instead of a memset plus the
-// validation kernel: CTA 0 checks the query rows (as validate_query_kernel,
-// when q != nullptr) and every CTA zeroes its share of the per-query
-// counters and bitmaps.
+// Per-query prologue, one PDL-chained launch instead of a memset plus a
+// validation kernel: every CTA zeroes its share of the per-query counters and
+// bitmaps; when q != nullptr CTA 0 also checks the query rows
+// (check_unit_rows, types.cpp:10-19: norm^2 = sum of double(v)^2 in order —
+// the products are exact in fp64, so only the adds must stay in order: 32-dim
+// chunks are staged coalesced in shared memory and thread r runs row r's add
+// chain from there).
 __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
                                                               int* __restrict__ status, uint4* __restrict__ zero,
                                                               uint64_t n16, uint4* __restrict__ zero2, uint64_t m16) {
@@ -813,11 +786,6 @@ void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status
 bool pdl_enabled() {
     static const bool on = getenv("PLAID_NO_PDL") == nullptr;
     return on;
-}
-
-void validate_query(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, cudaStream_t st) {
-    ::plaid::launch::pdl(validate_query_kernel, 1, 256, 0, st, d_q, rows, dim, d_status);
-    count_launch();
 }
 
 void export_keys(const uint64_t* d_keys, const uint64_t* d_n, uint64_t stride, uint32_t base, uint64_t* d_out,
