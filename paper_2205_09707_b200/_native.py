@@ -69,8 +69,10 @@ SIGNATURES = {
     "plaid_index_info": (None, [C.c_void_p, u64p]),
     "plaid_searcher_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(SearcherConfig), C.POINTER(C.c_void_p)]),
     "plaid_searcher_destroy": (None, [C.c_void_p]),
-    "plaid_search": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_uint64, C.POINTER(Params), u32p, f32p,
-                               u64p, C.POINTER(Trace)]),
+    # hot host path: array arguments as raw addresses (a ctypes POINTER per
+    # argument costs several microseconds per call)
+    "plaid_search": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(Params), C.c_void_p,
+                               C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(Trace)]),
     "plaid_search_batch": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(Params),
                                      u32p, f32p, u64p, C.POINTER(Trace)]),
     "plaid_search_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,

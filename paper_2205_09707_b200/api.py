@@ -294,14 +294,16 @@ class Searcher:
         if q.ndim != 2:
             raise PlaidError(ErrorCode.DimensionMismatch, "query must be rows x dim")
         k = max(int(params.k), 1)
-        ids = np.zeros(k, dtype=np.uint32)
-        sc = np.zeros(k, dtype=np.float32)
+        ids = np.empty(k, dtype=np.uint32)
+        sc = np.empty(k, dtype=np.float32)
         n = C.c_uint64()
         tr = N.Trace()
         p = params._c(options.disable_filter)
-        _check(N.load().plaid_search(self._h, N.ptr(q, C.c_float), q.shape[0], q.shape[1], C.byref(p),
-                                     N.ptr(ids, C.c_uint32), N.ptr(sc, C.c_float), C.byref(n), C.byref(tr)))
-        return SearchResult(CandidateSet(ids[: n.value].copy(), sc[: n.value].copy()), StageTrace._from_c(tr))
+        _check(N.load().plaid_search(self._h, q.__array_interface__["data"][0], q.shape[0], q.shape[1], C.byref(p),
+                                     ids.__array_interface__["data"][0], sc.__array_interface__["data"][0],
+                                     C.byref(n), C.byref(tr)))
+        m = n.value
+        return SearchResult(CandidateSet(ids[:m], sc[:m]), StageTrace._from_c(tr))
 
     def search_batch(self, q: np.ndarray, params: SearchParams, options: SearchOptions = SearchOptions()):
         q = np.ascontiguousarray(q, dtype=np.float32)
