@@ -420,6 +420,21 @@ def run_plaid(args, cfg):
             "frac": ach / hbm_peak, "traffic": traffic, "peak_kind": f"{peak_kind} (copy bandwidth, burst)",
             "algorithmic_bytes_per_launch": ab, "mean_ms": mean_ph["scores"],
             "share_of_step": mean_ph["scores"] / (1e3 * total_s / args.steps)}
+    # context: the live-measured rate of a plain one-pass read of C's size on
+    # this GPU (event-timed like the kernel) — the practical floor of a kernel
+    # that streams C once
+    try:
+        import ctypes as _C
+
+        from paper_2205_09707_b200 import _native as _N
+
+        g = _C.c_double()
+        if _N.load().plaid_measure_read_gbs(local, 512 * K, 5, _C.byref(g)) == 0 and g.value > 0:
+            roof["read_floor_gbs"] = g.value
+            roof["read_floor_note"] = f"plain coalesced read of {512 * K >> 20} MiB (C's size), L2 flushed, best of 5"
+            roof["frac_of_read_floor"] = ach / g.value  # same algorithmic bytes as `achieved`
+    except Exception:  # noqa: BLE001
+        pass
 
     # ---- stage 4 (decompress + exact MaxSim) against its own bound: exactness
     # forbids FMA and tensor cores, so every (token, query token, dim) is one

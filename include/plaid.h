@@ -145,6 +145,11 @@ plaid_status plaid_index_from_host(const plaid_index_desc* desc, int device, int
 enum { PLAID_OPEN_VALIDATE = 1, PLAID_OPEN_NO_CHECKSUMS = 2 };
 plaid_status plaid_index_save(const plaid_index_desc* desc, const char* dir, uint64_t rng_seed);
 plaid_status plaid_index_open(const char* dir, int device, uint32_t flags, plaid_index** out);
+/* Best-of-iters GB/s of a plain coalesced HBM read of `bytes` (L2 flushed
+ * before each pass): the achievable streaming rate for a one-pass kernel of
+ * that size (bench.py reports the S_cq kernel against it and against the copy
+ * peak).  Returns a cudaError_t value (0 = ok). */
+int plaid_measure_read_gbs(int device, uint64_t bytes, int iters, double* out_gbs);
 /* FORMAT.md digest of a host buffer (the manifest's per-file checksum). */
 uint64_t plaid_checksum(const void* data, uint64_t bytes);
 

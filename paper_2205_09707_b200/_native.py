@@ -81,6 +81,7 @@ SIGNATURES = {
     "plaid_index_save": (C.c_int, [C.POINTER(IndexDesc), C.c_char_p, C.c_uint64]),
     "plaid_index_open": (C.c_int, [C.c_char_p, C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
     "plaid_checksum": (C.c_uint64, [C.c_void_p, C.c_uint64]),
+    "plaid_measure_read_gbs": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_double)]),
     "plaid_batch_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(SearcherConfig), C.c_uint32,
                                      C.POINTER(C.c_void_p)]),
     "plaid_batch_destroy": (None, [C.c_void_p]),

@@ -95,7 +95,7 @@ struct TfCfg {
 // Debug timeline (PLAID_TF32_DBG=16): globaltimer stamps of CTA 0's pipeline
 // events and every CTA's begin/end (read back with plaid_debug_tf32_trace).
 // Pipeline experiments (results wrong): dbg & 1 skips the MMAs, & 2 the S
-// stores, & 4 the TMEM operand stores.
+// stores, & 4 the TMEM operand stores, & 8 the converters' reads.
 __device__ unsigned long long g_tf32_trace[8 * 256];
 __device__ unsigned long long g_tf32_cta[2 * 256];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -333,6 +333,17 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
             const int s = gb % kRaw;
             mbar_wait(raw_full(s), (gb / kRaw) & 1);
             if (warp == 4 && lane == 0) trace_stamp(dbg, 1, lt * 4);
+            if (dbg & 8) {  // experiment: pure TMA stream (box released unread, no MMA input)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(raw_empty(s));
+                for (int kc = 0; kc < kChunks; ++kc, ++go) {
+                    const int o = go % kOps;
+                    mbar_wait(ops_empty(o), ((go / kOps) & 1) ^ 1);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(ops_full(o));
+                }
+                continue;
+            }
             for (int kc = 0; kc < kChunks; ++kc, ++go) {
                 const int o = go % kOps;
                 // the row's 8 granules of chunk kc, un-swizzled: granule j at (j ^ (lane & 7))

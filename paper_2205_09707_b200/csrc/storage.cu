@@ -406,3 +406,58 @@ DeviceIndex* open_index(const std::string& dir, int device, uint32_t flags) {
 }
 
 }  // namespace plaid
+
+// ---- measured read floor (bench.py's roofline context) ---------------------------------
+namespace plaid {
+namespace {
+__global__ void read_stream_kernel(const uint4* __restrict__ src, uint64_t n16, unsigned long long* sink) {
+    unsigned long long acc = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint4 v = __ldcs(src + i);
+        acc += v.x ^ v.w;
+    }
+    if (acc == 0x9e3779b97f4a7c15ull) *sink = acc;  // keeps the loads alive
+}
+}  // namespace
+}  // namespace plaid
+
+// Best-of-`iters` GB/s of a plain coalesced read of `bytes` from HBM (L2
+// flushed by a 256 MiB write before each pass): the achievable streaming rate
+// of a one-pass kernel of that size, next to the copy peak of MEASURED_PEAKS.
+extern "C" int plaid_measure_read_gbs(int device, uint64_t bytes, int iters, double* out_gbs) {
+    using namespace plaid;
+    *out_gbs = 0;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    uint8_t *src = nullptr, *flush = nullptr;
+    unsigned long long* sink = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    int rc = int(cudaMalloc(&src, bytes));
+    if (!rc) rc = int(cudaMalloc(&flush, 256ull << 20));
+    if (!rc) rc = int(cudaMalloc(&sink, 8));
+    if (!rc) rc = int(cudaMemset(src, 1, bytes));
+    if (!rc) rc = int(cudaEventCreate(&a));
+    if (!rc) rc = int(cudaEventCreate(&b));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    float best = 1e30f;
+    for (int it = 0; !rc && it < iters + 1; ++it) {
+        cudaMemset(flush, it, 256ull << 20);
+        cudaEventRecord(a);
+        read_stream_kernel<<<sms * 32, 256>>>(reinterpret_cast<const uint4*>(src), bytes / 16, sink);
+        cudaEventRecord(b);
+        rc = int(cudaEventSynchronize(b));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (it > 0 && ms < best) best = ms;
+    }
+    if (!rc) *out_gbs = double(bytes) / (double(best) * 1e-3) / 1e9;
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    cudaFree(src);
+    cudaFree(flush);
+    cudaFree(sink);
+    cudaSetDevice(prev);
+    return rc;
+}
