@@ -279,6 +279,14 @@ plaid_status plaid_shard_phase3_device(plaid_searcher* s, const uint64_t* d_g3, 
  * only), stage2_rows_gathered, stage3_rows_gathered] of the last query. */
 plaid_status plaid_searcher_trace_counters_device(plaid_searcher* s, uint64_t* d_out, uint64_t stream);
 
+/* Same from packed rows, one all-gather per query: row g (of `shards`) at
+ * d_rows + g * (2k + 2) u32 words = [k u32 pids | k f32 scores | u64 count]
+ * (what plaid_shard_phase3_device / plaid_search_device write when given
+ * pids = row, scores = row + k, n = (uint64_t*)(row + 2k)). */
+plaid_status plaid_merge_topk_rows_device(plaid_searcher* s, const uint32_t* d_rows, uint64_t shards, uint64_t k,
+                                          uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
+                                          uint64_t stream);
+
 /* ---- per-stage entry points (host buffers in/out, computed on the GPU) ------------ */
 /* pipeline.cpp:26-50: scores K x rows (centroid-major), row_max K */
 plaid_status plaid_compute_centroid_scores(plaid_searcher* s, const float* q, uint64_t rows,

@@ -106,6 +106,8 @@ SIGNATURES = {
     "plaid_merge_topk_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                           C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_uint64]),
+    "plaid_merge_topk_rows_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
+                                               C.c_void_p, C.c_void_p, C.c_uint64]),
     "plaid_compute_centroid_scores": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_uint64, f32p, f32p]),
     "plaid_generate_candidates": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_uint64, u32p, u64p]),
     "plaid_prune_centroids": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_float, u8p]),

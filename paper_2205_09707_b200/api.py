@@ -346,6 +346,12 @@ class Searcher:
     def trace_counters_device(self, d_out: int, stream: int = 0) -> None:
         _check(N.load().plaid_searcher_trace_counters_device(self._h, d_out, stream))
 
+    def merge_topk_rows_device(self, d_rows: int, shards: int, k: int, d_out_pids: int, d_out_scores: int,
+                               d_out_n: int, stream: int = 0) -> None:
+        """Merge packed per-shard rows [k pids | k scores | u64 count] (one all-gather per query)."""
+        _check(N.load().plaid_merge_topk_rows_device(self._h, d_rows, shards, k, d_out_pids, d_out_scores,
+                                                     d_out_n, stream))
+
     def sync(self) -> None:
         _check(N.load().plaid_searcher_sync(self._h))
 

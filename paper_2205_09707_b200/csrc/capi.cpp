@@ -359,6 +359,16 @@ plaid_status plaid_batch_sync(plaid_batch* b) {
 
 uint64_t plaid_batch_last_launches(const plaid_batch* b) { return b ? b->impl->last_launches() : 0; }
 
+plaid_status plaid_merge_topk_rows_device(plaid_searcher* s, const uint32_t* d_rows, uint64_t shards, uint64_t k,
+                                          uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
+                                          uint64_t stream) {
+    return guarded([&] {
+        need(s, "searcher");
+        s->impl->merge_topk_rows_device(d_rows, shards, k, d_out_pids, d_out_scores, d_out_n,
+                                        reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
 plaid_status plaid_shard_phase1_device(plaid_searcher* s, const float* d_q, uint64_t rows, uint64_t dim,
                                        const plaid_params* params, uint64_t* d_x2, uint64_t stride2,
                                        uint64_t stream) {

@@ -1145,8 +1145,25 @@ void Searcher::merge_topk_device(const uint32_t* d_pids, const float* d_scores, 
     tmp_keys_.ensure(std::max<uint64_t>(total, 1));
     const uint64_t cap = launch::sort_tmp_capacity(total);
     if (cap) sort_tmp_.ensure(cap);
-    launch::merge_topk(d_pids, d_scores, d_counts, shards, stride, k, tmp_keys_.p, counters_.p + kTmpN,
+    launch::merge_topk(d_pids, d_scores, d_counts, shards, stride, 1, stride, k, tmp_keys_.p, counters_.p + kTmpN,
                        d_out_pids, d_out_scores, d_out_n, sort_tmp_.p, st);
+}
+
+// Packed rows (one all-gather per query): row g = [k u32 pids | k f32 scores |
+// u64 count] at d_rows + g * (2k + 2) words.
+void Searcher::merge_topk_rows_device(const uint32_t* d_rows, uint64_t shards, uint64_t k, uint32_t* d_out_pids,
+                                      float* d_out_scores, uint64_t* d_out_n, cudaStream_t st) {
+    if (k < 1) fail(PLAID_INVALID_PARAMS, "k must be >= 1");
+    DeviceGuard g(device_);
+    if (!st) st = stream_;
+    const uint64_t total = shards * k;
+    tmp_keys_.ensure(std::max<uint64_t>(total, 1));
+    const uint64_t cap = launch::sort_tmp_capacity(total);
+    if (cap) sort_tmp_.ensure(cap);
+    const uint64_t row = 2 * k + 2;
+    launch::merge_topk(d_rows, reinterpret_cast<const float*>(d_rows + k),
+                       reinterpret_cast<const uint64_t*>(d_rows + 2 * k), shards, row, row / 2, k, k, tmp_keys_.p,
+                       counters_.p + kTmpN, d_out_pids, d_out_scores, d_out_n, sort_tmp_.p, st);
 }
 
 void Searcher::merge_topk(const uint32_t* pids, const float* scores, const uint64_t* counts, uint64_t shards,

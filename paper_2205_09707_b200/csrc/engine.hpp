@@ -150,6 +150,8 @@ public:
     void merge_topk_device(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts,
                            uint64_t shards, uint64_t stride, uint64_t k, uint32_t* d_out_pids,
                            float* d_out_scores, uint64_t* d_out_n, cudaStream_t st);
+    void merge_topk_rows_device(const uint32_t* d_rows, uint64_t shards, uint64_t k, uint32_t* d_out_pids,
+                                float* d_out_scores, uint64_t* d_out_n, cudaStream_t st);
 
 private:
     void require_index() const;

@@ -227,10 +227,12 @@ void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status
 // Stage counters: min() bookkeeping done on device.
 void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st);
 // Merge G shard top-k lists into the global top-k.
+// Shard g's list: pids[g * stride + j], scores[g * stride + j] for j <
+// min(per, counts[g * count_stride]) (count_stride 1 = a separate count array).
 void merge_topk(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts,
-                uint64_t shards, uint64_t stride, uint64_t k, uint64_t* d_tmp_keys,
-                uint64_t* d_tmp_n, uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
-                uint64_t* d_sort_tmp, cudaStream_t st);
+                uint64_t shards, uint64_t stride, uint64_t count_stride, uint64_t per, uint64_t k,
+                uint64_t* d_tmp_keys, uint64_t* d_tmp_n, uint32_t* d_out_pids, float* d_out_scores,
+                uint64_t* d_out_n, uint64_t* d_sort_tmp, cudaStream_t st);
 // Build keys from (ids, scores) arrays (select_top entry point).
 void make_keys(const uint32_t* d_ids, const float* d_scores, uint64_t n, uint64_t* d_keys,
                cudaStream_t st);

@@ -319,15 +319,19 @@ __global__ void make_keys_kernel(const uint32_t* __restrict__ ids, const float* 
 
 // Per shard g, entries [0, counts[g]) of row g (stride) become keys; the rest
 // of the G*stride slots are 0 (below every real key).
+// (rows may be packed: shard g's pids at pids + g * stride, its count at
+// counts[g * count_stride]; only the first `k` entries of a row are read)
 __global__ void merge_keys_kernel(const uint32_t* __restrict__ pids, const float* __restrict__ scores,
                                   const uint64_t* __restrict__ counts, uint64_t shards, uint64_t stride,
-                                  uint64_t* __restrict__ keys, uint64_t* __restrict__ d_n) {
+                                  uint64_t count_stride, uint64_t k, uint64_t* __restrict__ keys,
+                                  uint64_t* __restrict__ d_n) {
     dev::pdl_wait();
-    const uint64_t total = shards * stride;
+    const uint64_t total = shards * k;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t g = i / stride, j = i % stride;
-        keys[i] = j < counts[g] ? dev::make_key(scores[i], pids[i]) : 0ull;
+        const uint64_t g = i / k, j = i % k;
+        const uint64_t at = g * stride + j;
+        keys[i] = j < counts[g * count_stride] ? dev::make_key(scores[at], pids[at]) : 0ull;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *d_n = total;
 }
@@ -759,13 +763,13 @@ void make_keys(const uint32_t* d_ids, const float* d_scores, uint64_t n, uint64_
 }
 
 void merge_topk(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts,
-                uint64_t shards, uint64_t stride, uint64_t k, uint64_t* d_tmp_keys, uint64_t* d_tmp_n,
-                uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n, uint64_t* d_sort_tmp,
-                cudaStream_t st) {
-    ::plaid::launch::pdl(merge_keys_kernel, grid_for(shards * stride, 256, 4096), 256, 0, st, 
-        d_pids, d_scores, d_counts, shards, stride, d_tmp_keys, d_tmp_n);
+                uint64_t shards, uint64_t stride, uint64_t count_stride, uint64_t per, uint64_t k,
+                uint64_t* d_tmp_keys, uint64_t* d_tmp_n, uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
+                uint64_t* d_sort_tmp, cudaStream_t st) {
+    ::plaid::launch::pdl(merge_keys_kernel, grid_for(shards * per, 256, 4096), 256, 0, st,
+        d_pids, d_scores, d_counts, shards, stride, count_stride, per, d_tmp_keys, d_tmp_n);
     count_launch();
-    sort_top(d_tmp_keys, d_tmp_n, shards * stride, k, nullptr, d_out_pids, d_out_scores, d_out_n, 0,
+    sort_top(d_tmp_keys, d_tmp_n, shards * per, k, nullptr, d_out_pids, d_out_scores, d_out_n, 0,
              d_sort_tmp, st);
 }
 

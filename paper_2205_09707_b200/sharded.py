@@ -6,10 +6,10 @@ GPU box, gloo for the CPU tests).  Rank r holds the passages
 replicated, so stage 1 is exact per shard.  Each rank runs the whole
 four-stage search on its shard and emits its top-k with GLOBAL passage ids;
 the one exchange step is an all-gather of the k (pid, score) pairs plus the
-count, followed by the device-side final select (merge_topk, the
+count (one packed row per rank, one collective), followed by the device-side final select (merge_topk, the
 (score desc, pid asc) order of pipeline.cpp:139-163) — every rank ends with
 the same global top-k.  Messages are k x 8 B per rank, so they are
-latency-bound: three small all-gathers of fixed size, no host sync between
+latency-bound: one all-gather of a packed row, no host sync between
 the search and the merge.
 
 Two modes:
@@ -89,10 +89,14 @@ class ShardedSearcher:
         self.dev = dev = device if device is not None else torch.device("cpu")
         self._x = {}
         z = lambda *shape, dt: torch.zeros(*shape, dtype=dt, device=dev)  # noqa: E731
-        self.pids, self.scores, self.n = z(self.k, dt=torch.int32), z(self.k, dt=torch.float32), z(1, dt=torch.int64)
-        self.g_pids = z(self.world * self.k, dt=torch.int32)
-        self.g_scores = z(self.world * self.k, dt=torch.float32)
-        self.g_n = z(self.world, dt=torch.int64)
+        # this rank's result row, packed for ONE all-gather per query:
+        # [k u32 pids | k f32 scores | u64 count] (plaid_merge_topk_rows_device)
+        self.row_words = 2 * self.k + 2
+        self.row = z(self.row_words, dt=torch.int32)
+        self.g_rows = z(self.world * self.row_words, dt=torch.int32)
+        self.pids = self.row[: self.k]
+        self.scores = self.row[self.k: 2 * self.k].view(torch.float32)
+        self.n = self.row[2 * self.k:].view(torch.int64)
         self.out_pids, self.out_scores = z(self.k, dt=torch.int32), z(self.k, dt=torch.float32)
         self.out_n = z(1, dt=torch.int64)
 
@@ -141,12 +145,9 @@ class ShardedSearcher:
                 _all_gather(g3[: self.world * s3], x3[:s3], self.group)
             self.s.shard_phase3(g3.data_ptr(), self.world, self.pids.data_ptr(), self.scores.data_ptr(),
                                 self.n.data_ptr(), stream=stream)
-        _all_gather(self.g_pids, self.pids, self.group)
-        _all_gather(self.g_scores, self.scores, self.group)
-        _all_gather(self.g_n, self.n, self.group)
-        self.s.merge_topk_device(self.g_pids.data_ptr(), self.g_scores.data_ptr(), self.g_n.data_ptr(), self.world,
-                                 self.k, self.k, self.out_pids.data_ptr(), self.out_scores.data_ptr(),
-                                 self.out_n.data_ptr(), stream=stream)
+        _all_gather(self.g_rows, self.row, self.group)
+        self.s.merge_topk_rows_device(self.g_rows.data_ptr(), self.world, self.k, self.out_pids.data_ptr(),
+                                      self.out_scores.data_ptr(), self.out_n.data_ptr(), stream=stream)
         return self.out_pids, self.out_scores, self.out_n
 
     def trace_counters(self, stream: int = 0) -> dict:

@@ -460,3 +460,34 @@ def test_edge_cases(port):
                 assert np.array_equal(got.topk.passage_ids, ids), (rows, p)
                 assert np.array_equal(bits(got.topk.scores), bits(sc))
                 assert got.trace.counters() == tr
+
+
+def test_merge_topk_rows_device(port):
+    """Packed per-shard rows [k pids | k scores | u64 count] (one all-gather
+    per query) merge like the separate arrays."""
+    import torch
+
+    rng = np.random.default_rng(9)
+    s = P.Searcher(None)
+    G, k = 5, 64
+    counts = [64, 10, 0, 64, 33]
+    rows = np.zeros((G, 2 * k + 2), np.uint32)
+    allp, alls = [], []
+    for g in range(G):
+        c = counts[g]
+        p = (rng.permutation(5000)[:c] + g * 5000).astype(np.uint32)
+        v = np.sort(rng.standard_normal(c).astype(np.float32))[::-1].copy()
+        rows[g, :c] = p
+        rows[g, k:k + c] = v.view(np.uint32)
+        rows[g, 2 * k:].view(np.uint64)[0] = c
+        allp.append(p), alls.append(v)
+    d = torch.from_numpy(rows.reshape(-1).view(np.int32)).cuda()
+    op = torch.zeros(k, dtype=torch.int32, device="cuda")
+    os_ = torch.zeros(k, dtype=torch.float32, device="cuda")
+    on = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s.merge_topk_rows_device(d.data_ptr(), G, k, op.data_ptr(), os_.data_ptr(), on.data_ptr())
+    torch.cuda.synchronize()
+    b = port.select_top(np.concatenate(allp), np.concatenate(alls), k)
+    m = int(on[0])
+    assert np.array_equal(op[:m].cpu().numpy().view(np.uint32), b[0])
+    assert np.array_equal(os_[:m].cpu().numpy(), b[1])

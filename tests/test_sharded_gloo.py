@@ -50,6 +50,17 @@ class OracleShard:
         view(d_scores, params.k, C.c_float, np.float32)[:n] = sc
         view(d_n, 1, C.c_int64, np.int64)[0] = n
 
+    def merge_topk_rows_device(self, g_rows, shards, k, o_pids, o_scores, o_n, stream=0):
+        row = 2 * k + 2
+        r = view(g_rows, shards * row, C.c_int32, np.uint32).reshape(shards, row)
+        allp = np.concatenate([r[g, :k][: int(r[g, 2 * k:].view(np.uint64)[0])] for g in range(shards)])
+        alls = np.concatenate([r[g, k:2 * k].view(np.float32)[: int(r[g, 2 * k:].view(np.uint64)[0])]
+                               for g in range(shards)])
+        mp_, ms = merge(allp, alls, k)
+        view(o_pids, k, C.c_int32, np.uint32)[: len(mp_)] = mp_
+        view(o_scores, k, C.c_float, np.float32)[: len(ms)] = ms
+        view(o_n, 1, C.c_int64, np.int64)[0] = len(mp_)
+
     def merge_topk_device(self, g_pids, g_scores, g_n, shards, stride, k, o_pids, o_scores, o_n, stream=0):
         pids = view(g_pids, shards * stride, C.c_int32, np.uint32).reshape(shards, stride)
         sc = view(g_scores, shards * stride, C.c_float, np.float32).reshape(shards, stride)
