@@ -549,8 +549,12 @@ void Searcher::enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times
     const uint64_t nd = std::min<uint64_t>(p.ndocs, ix.N);
     launch::centroid_interaction(ix, scores_.p, pending_rows_, nullptr, sel2_.p, c + kN2, nd, nullptr, nullptr,
                                  keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
-    launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
-                     sort_tmp_.p, st);
+    // stage 4 needs only the top-stage3_width SET (the final select orders it)
+    if (nd <= launch::kSmallSortMax)
+        launch::select_set(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, c + kN3, st);
+    else
+        launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
+                         sort_tmp_.p, st);
     record(5, st, times);
 }
 

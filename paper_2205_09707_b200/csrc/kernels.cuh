@@ -189,6 +189,10 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
               uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
               uint32_t id_base, uint64_t* d_tmp, cudaStream_t st);
 uint64_t sort_tmp_capacity(uint64_t nmax);
+// The top-`want` SET of keys[0..*d_n) (unordered), nmax <= kSmallSortMax, one
+// CTA (shared-memory radix select); *d_out_n = min(n, want).
+void select_set(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, uint64_t* d_out_keys,
+                uint64_t* d_out_n, cudaStream_t st);
 
 // Global-exact shard exchange (select.cu): export keys[0..*d_n) in global
 // form (ids + base) into a zero-padded row of `stride`; then, from the

@@ -665,6 +665,84 @@ threshold_filter_kernel(const uint64_t* __restrict__ g, uint64_t total, uint64_t
     if (tid == 0) *d_n = s_out;
 }
 
+
+// Top-`want` SET (unordered) of keys[0..*d_n), n <= kSmallSortMax, in one CTA:
+// the keys are staged in shared memory, an MSB-first 8-bit radix select finds
+// the want-th largest key t (keys are unique), and every key >= t is written
+// to out (order unspecified; *d_out_n = min(n, want)).  Stage 3 needs only
+// the set — stage 4 scores it and the final select orders the result.
+constexpr uint32_t kSelCtaThreads = 1024;
+__global__ void __launch_bounds__(kSelCtaThreads)
+select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
+                      uint64_t* __restrict__ out, uint64_t* __restrict__ d_out_n) {
+    dev::pdl_wait();
+    extern __shared__ uint64_t sk[];
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t s_prefix, s_rem, s_mask;
+    __shared__ uint32_t s_done, s_cnt;
+    const uint32_t t = threadIdx.x;
+    const uint32_t n = uint32_t(*d_n);
+    for (uint32_t i = t; i < n; i += kSelCtaThreads) sk[i] = __ldcg(keys + i);
+    if (t == 0) {
+        s_prefix = 0, s_rem = want, s_mask = 0, s_done = n <= want, s_cnt = 0;
+    }
+    __syncthreads();
+    if (s_done) {  // everything survives
+        for (uint32_t i = t; i < n; i += kSelCtaThreads) out[i] = sk[i];
+        if (t == 0) *d_out_n = n;
+        return;
+    }
+    for (int shift = 56; shift >= 0 && !s_done; shift -= 8) {
+        for (uint32_t b = t; b < 256; b += kSelCtaThreads) hist[b] = 0;
+        __syncthreads();
+        const uint64_t mask = s_mask, prefix = s_prefix;
+        for (uint32_t i = t; i < n; i += kSelCtaThreads)
+            if ((sk[i] & mask) == prefix) atomicAdd(&hist[(sk[i] >> shift) & 255u], 1u);
+        __syncthreads();
+        if (t < 32) {
+            // bins 255 - 8 t .. 248 - 8 t per lane (lane 0 the highest), prefix from the top
+            uint32_t c[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sum += (c[j] = hist[255 - 8 * t - j]);
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (t >= uint32_t(o)) incl += y;
+            }
+            const uint64_t rem = s_rem;
+            uint64_t above = incl - sum;
+            if (above < rem && rem <= above + sum) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (above < rem && rem <= above + c[j]) {
+                        const uint32_t b = 255 - 8 * t - j;
+                        s_prefix = prefix | (uint64_t(b) << shift);
+                        s_mask = mask | (uint64_t(255) << shift);
+                        s_rem = rem - above;
+                        s_done = c[j] == rem - above;  // the whole bucket is taken
+                    }
+                    above += c[j];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // the threshold: the bucket prefix when the whole bucket is taken, else
+    // the fully resolved key (64 bits of prefix) — keys >= it survive
+    const uint64_t thr = s_prefix;
+    for (uint32_t i0 = 0; i0 < n; i0 += kSelCtaThreads) {
+        const uint32_t i = i0 + t;
+        const bool ok = i < n && sk[i] >= thr;
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        uint32_t base = 0;
+        if ((t & 31) == 0 && bal) base = atomicAdd(&s_cnt, uint32_t(__popc(bal)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (ok) out[base + __popc(bal & ((1u << (t & 31)) - 1u))] = sk[i];
+    }
+    if (t == 0) *d_out_n = want;
+}
+
 }  // namespace
 
 namespace launch {
@@ -802,6 +880,19 @@ void export_keys(const uint64_t* d_keys, const uint64_t* d_n, uint64_t stride, u
 void threshold_filter(const uint64_t* d_gathered, uint64_t total, uint64_t want, uint64_t* d_keys, uint64_t* d_n,
                       uint32_t base, cudaStream_t st) {
     ::plaid::launch::pdl(threshold_filter_kernel, 1, kThrThreads, 0, st, d_gathered, total, want, d_keys, d_n, base);
+    count_launch();
+}
+
+void select_set(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, uint64_t* d_out_keys,
+                uint64_t* d_out_n, cudaStream_t st) {
+    const size_t smem = std::max<uint64_t>(nmax, 1) * sizeof(uint64_t);
+    static bool cfg = false;
+    if (!cfg) {
+        cudaFuncSetAttribute(select_set_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kSmallSortMax * sizeof(uint64_t)));
+        cfg = true;
+    }
+    ::plaid::launch::pdl(select_set_cta_kernel, 1, kSelCtaThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_n);
     count_launch();
 }
 
