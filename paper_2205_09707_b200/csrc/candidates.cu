@@ -4,8 +4,9 @@
 // (atomicOr per posting; duplicates across query tokens collapse for free),
 // then compacted into ascending passage ids.  Scanning the bitmap in order is
 // exactly the reference's `std::sort` of the unique ids (pipeline.cpp:83), so
-// the output is bit-identical.  Two launches: per-chunk popcounts, then each
-// chunk re-derives its base from the preceding chunk counts and writes its ids.
+// the output is bit-identical.  The search path compacts in one pass
+// (decoupled look-back over published chunk counts); the standalone entry
+// point uses two launches (per-chunk popcounts, then the writes).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -110,6 +111,75 @@ __global__ void chunk_write_kernel(const uint32_t* __restrict__ bitmap, uint64_t
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kThreads - 1) *out_n = pos;
 }
 
+
+// Single pass (decoupled look-back): every chunk publishes its popcount with
+// a ready flag, then sums its predecessors' published counts (spinning on
+// their flags — all chunks are resident: <= 2^32 / 65536 CTAs of 256 threads)
+// and writes its ids in order.  `status` (one u64 per chunk) must be zero on
+// entry (the per-query prologue clears it).
+__global__ void chunk_compact_kernel(const uint32_t* __restrict__ bitmap, uint64_t N,
+                                     unsigned long long* __restrict__ status, uint32_t* __restrict__ out,
+                                     uint64_t* __restrict__ out_n, uint32_t* __restrict__ slot_of) {
+    dev::pdl_wait();
+    __shared__ uint64_t red[kThreads / 32];
+    __shared__ uint32_t scan[kThreads / 32];
+    constexpr unsigned long long kReady = 1ull << 63;
+    const uint64_t w0 = uint64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
+    uint32_t words[kWordsPerThread];
+    uint32_t mine = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kWordsPerThread; ++j) {
+        words[j] = masked_word(bitmap, w0 + j, N);
+        mine += __popc(words[j]);
+    }
+    // block inclusive scan of `mine`
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += v;
+    }
+    if (lane == 31) scan[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t k = 0; k < kThreads / 32; ++k) {
+        if (k < warp) before += scan[k];
+        total += scan[k];
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(status + blockIdx.x), "l"(kReady | total) : "memory");
+    }
+    // look back: the counts of every earlier chunk
+    uint64_t part = 0;
+    for (uint32_t c = threadIdx.x; c < blockIdx.x; c += kThreads) {
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(status + c) : "memory");
+        } while (!(v & kReady));
+        part += v & ~kReady;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    uint64_t base = 0;
+    for (uint32_t k = 0; k < kThreads / 32; ++k) base += red[k];
+    uint64_t pos = base + before + incl - mine;
+#pragma unroll
+    for (uint32_t j = 0; j < kWordsPerThread; ++j) {
+        uint32_t v = words[j];
+        while (v) {
+            const uint32_t b = __ffs(v) - 1;
+            v &= v - 1;
+            const uint32_t pid = uint32_t((w0 + j) * 32 + b);
+            if (slot_of) slot_of[pid] = uint32_t(pos);
+            out[pos++] = pid;
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kThreads - 1) *out_n = pos;
+}
+
 }  // namespace
 
 namespace launch {
@@ -125,6 +195,13 @@ uint32_t bitmap_chunks(uint64_t N) {
     const uint64_t words = (N + 31) / 32;
     uint64_t c = (words + kChunkWords - 1) / kChunkWords;
     return uint32_t(c ? c : 1);
+}
+
+void bitmap_compact_1pass(const uint32_t* d_bitmap, uint64_t N, unsigned long long* d_status, uint32_t* d_out_ids,
+                          uint64_t* d_out_n, uint32_t* d_slot_of, cudaStream_t st) {
+    ::plaid::launch::pdl(chunk_compact_kernel, bitmap_chunks(N), kThreads, 0, st, d_bitmap, N, d_status, d_out_ids,
+                         d_out_n, d_slot_of);
+    count_launch();
 }
 
 void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_counts,

@@ -344,9 +344,14 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
     PLAID_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     for (auto& e : ev_) PLAID_CUDA(cudaEventCreate(&e));
     const uint64_t words = index_ ? (index_->view().N + 31) / 32 : 0;
-    zero_.ensure((2 * words + 3) / 4 * 4 + 4);  // bitmaps, whole 16-byte units (query_prologue)
+    // [candidate bitmap | used bitmap | per-chunk compaction status (u64)],
+    // whole 16-byte units, cleared per query by the prologue kernel
+    const uint64_t chunks = index_ ? launch::bitmap_chunks(index_->view().N) : 1;
+    const uint64_t bm_words = (2 * words + 3) / 4 * 4;
+    zero_.ensure(bm_words + (2 * chunks + 3) / 4 * 4);
     PLAID_CUDA(cudaMemset(zero_.p, 0, zero_.n * sizeof(uint32_t)));
     bitmap_.p = zero_.p;
+    compact_status_ = reinterpret_cast<unsigned long long*>(zero_.p + bm_words);
     ensure_result_block(1);
     kconst_.ensure(1);
     status_.ensure(1);
@@ -520,7 +525,7 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
         nsel = uint64_t(rows) * p.nprobe;
     }
     if (!bitmap_done) launch::postings_to_bitmap(ix, sel_.p, uint32_t(nsel), bitmap, st);
-    launch::bitmap_compact(bitmap, N, chunk_counts_.p, c1_.p, c + kN1, slot_of_.p, st);
+    launch::bitmap_compact_1pass(bitmap, N, compact_status_, c1_.p, c + kN1, slot_of_.p, st);
     record(2, st, times);
     if (p.disable_filter) {
         record(3, st, times);

@@ -213,6 +213,7 @@ private:
     // zero_ = [16 u64 counters | candidate bitmap (N bits) | kept-owner bitmap
     // (N bits)], cleared by a single memset per query.
     DevBuf<uint32_t> zero_;
+    unsigned long long* compact_status_ = nullptr;  // inside zero_ (bitmap_compact_1pass)
     template <typename T>
     struct View {
         T* p = nullptr;
