@@ -64,6 +64,8 @@ def filter_speedup(s: Searcher, queries: np.ndarray, params: SearchParams) -> di
     """Stage-4 time (ms, mean over the queries) with and without stages 2-3
     and whether the top-k agree.  `s` must record phase times."""
     on, off, same = [], [], 0
+    s.search(queries[0], params)  # warm-up: buffers sized, kernels configured
+    s.search(queries[0], params, SearchOptions(disable_filter=True))
     for q in queries:
         a = s.search(q, params)
         on.append(a.trace.decompression_ms)

@@ -514,11 +514,10 @@ int sm_count() {
 template <int NP, int QB>
 void launch_tf32(const CUtensorMap& map, const IndexView& ix, const TfOut& out, uint32_t rows, float t_cs,
                  uint32_t grid, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
+    static launch::PerDeviceOnce configured;
+    if (configured.first()) {
         cudaFuncSetAttribute(scores_tf32_kernel<NP, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TfCfg<QB>::kSmemBytes);
-        configured = true;
     }
     static const uint32_t dbg = [] {
         const char* e = getenv("PLAID_TF32_DBG");

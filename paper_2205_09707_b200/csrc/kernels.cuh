@@ -5,6 +5,7 @@
 // launch sequence that can be captured in a CUDA graph with no host sync.
 #pragma once
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -68,6 +69,19 @@ struct TfOut {
 };
 
 namespace launch {
+
+// True the first time per (call site, current device): kernel attributes
+// (e.g. the dynamic shared-memory limit) are per device, so a process that
+// drives several GPUs must set them on each.
+struct PerDeviceOnce {
+    std::atomic<unsigned long long> mask{0};
+    bool first() {
+        int d = 0;
+        cudaGetDevice(&d);
+        const unsigned long long bit = 1ull << (d & 63);
+        return !(mask.fetch_or(bit) & bit);
+    }
+};
 
 // Launch with programmatic stream serialization (PDL): the kernel may be
 // scheduled while the previous kernel in the stream drains; every kernel

@@ -379,12 +379,11 @@ void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint
         return;
     if (ix.dim == 128 && rows <= 32) {
         const size_t smem = size_t(kR128Warps) * kR128Chunk * kR128Pitch * sizeof(float);
-        static bool cfg128 = false;
-        if (!cfg128) {
+        static launch::PerDeviceOnce cfg128;
+        if (cfg128.first()) {
             cudaFuncSetAttribute(rank128_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             cudaFuncSetAttribute(rank128_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             cudaFuncSetAttribute(rank128_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            cfg128 = true;
         }
         // 3 CTAs (12 warps) per SM, one warp per finalist
         uint64_t blocks = uint64_t(sm_count()) * 3;
@@ -397,10 +396,9 @@ void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint
         return;
     }
     const size_t smem = size_t(32 + kTile) * (ix.dim + 4) * sizeof(float);
-    static bool configured = false;
-    if (!configured) {
+    static launch::PerDeviceOnce configured;
+    if (configured.first()) {
         cudaFuncSetAttribute(rank_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
     }
     uint64_t blocks = nmax;
     const uint64_t cap = uint64_t(sm_count()) * 16;

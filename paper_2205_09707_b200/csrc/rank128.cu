@@ -418,12 +418,11 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
     Weights16 W;
     for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
     const size_t fsm = size_t(kSmemFloats) * sizeof(float);
-    static bool cfg = false;
-    if (!cfg) {
+    static launch::PerDeviceOnce cfg;
+    if (cfg.first()) {
         cudaFuncSetAttribute(stream_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
         cudaFuncSetAttribute(stream_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
         cudaFuncSetAttribute(stream_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
-        cfg = true;
     }
     ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref,
                          s.fin_base, s.tokens);

@@ -283,11 +283,10 @@ void launch_scores(const IndexView& ix, const float* q, uint32_t rows, float t_c
                    float* rowmax, uint32_t* keep, uint64_t* partial, uint32_t blocks,
                    cudaStream_t st) {
     const size_t smem = size_t(32) * (ix.dim + 4) * 4 + size_t(kWarpsPerBlock) * kG * ix.dim * 4;
-    static bool configured = false;
-    if (!configured) {
+    static launch::PerDeviceOnce configured;
+    if (configured.first()) {
         cudaFuncSetAttribute(scores_exact_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024);
-        configured = true;
     }
     ::plaid::launch::pdl(scores_exact_kernel<NP>, blocks, kWarpsPerBlock * 32, smem, st, 
         ix.centroids, ix.K, ix.dim, q, rows, t_cs, S, rowmax, keep, partial);
@@ -299,10 +298,9 @@ void launch_merge(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint3
                   uint32_t* sel, cudaStream_t st) {
     const uint32_t threads = 256;
     const size_t smem = threads * NP * sizeof(uint64_t);
-    static bool configured = false;
-    if (!configured) {
+    static launch::PerDeviceOnce configured;
+    if (configured.first()) {
         cudaFuncSetAttribute(topn_merge_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = true;
     }
     ::plaid::launch::pdl(topn_merge_kernel<NP>, rows, threads, smem, st, partial, nwarps, nprobe, sel);
     launch::count_launch();
@@ -313,10 +311,9 @@ void launch_topn_postings(const uint64_t* partial, uint32_t nwarps, uint32_t row
                           const IndexView& ix, uint32_t* sel, uint32_t* bitmap, cudaStream_t st) {
     const uint32_t threads = 256;
     const size_t smem = threads * NP * sizeof(uint64_t);
-    static bool configured = false;
-    if (!configured) {
+    static launch::PerDeviceOnce configured;
+    if (configured.first()) {
         cudaFuncSetAttribute(topn_postings_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = true;
     }
     ::plaid::launch::pdl(topn_postings_kernel<NP>, rows * nprobe, threads, smem, st, partial, nwarps, nprobe,
                          ix.ivf_offsets, ix.ivf_postings, sel, bitmap);

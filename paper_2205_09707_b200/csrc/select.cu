@@ -755,11 +755,10 @@ void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax,
     count_launch();
     ::plaid::launch::pdl(hist_compact_kernel, grid, 256, 0, st, d_keys, d_n, d_st, d_bkeys, d_out_keys, d_out_n);
     count_launch();
-    static bool cfg = false;
-    if (!cfg) {
+    static launch::PerDeviceOnce cfg;
+    if (cfg.first()) {
         cudaFuncSetAttribute(hist_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(kRankCap * sizeof(uint64_t)));
-        cfg = true;
     }
     const uint64_t rb = std::min<uint64_t>((std::min<uint64_t>(nmax, kRankCap) + 31) / 32, kRankCap / 32);
     ::plaid::launch::pdl(hist_resolve_kernel, uint32_t(rb ? rb : 1), 128, kRankCap * sizeof(uint64_t), st, d_st, d_bkeys, d_out_keys,
@@ -793,11 +792,10 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
               uint32_t id_base, uint64_t* d_tmp, cudaStream_t st) {
     if (nmax <= kSmallSortMax && nmax >= 256) {
         const size_t smem = size_t(4) * (rank_quarter_pairs(uint32_t(nmax)) + 1) * 16;
-        static bool rank_cfg = false;
-        if (!rank_cfg) {
+        static launch::PerDeviceOnce rank_cfg;
+        if (rank_cfg.first()) {
             cudaFuncSetAttribute(sort_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(4 * (rank_quarter_pairs(uint32_t(kSmallSortMax)) + 1) * 16));
-            rank_cfg = true;
         }
         const uint32_t grid = uint32_t((nmax + kRankPerCta - 1) / kRankPerCta);
         ::plaid::launch::pdl(sort_rank_kernel, grid, kRankThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_ids, d_out_scores,
@@ -808,11 +806,10 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
     if (nmax <= kSmallSortMax) {
         const uint32_t npad = uint32_t(next_pow2(nmax < 2 ? 2 : nmax));
         const size_t smem = size_t(npad) * sizeof(uint64_t);
-        static bool configured = false;
-        if (!configured) {
+        static launch::PerDeviceOnce configured;
+        if (configured.first()) {
             cudaFuncSetAttribute(sort_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kSmallSortMax * sizeof(uint64_t)));
-            configured = true;
         }
         const uint32_t threads = npad / 2 < 1024 ? (npad / 2 < 32 ? 32 : npad / 2) : 1024;
         ::plaid::launch::pdl(sort_small_kernel, 1, threads, smem, st, d_keys, d_n, npad, want, d_out_keys, d_out_ids,
@@ -886,11 +883,10 @@ void threshold_filter(const uint64_t* d_gathered, uint64_t total, uint64_t want,
 void select_set(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, uint64_t* d_out_keys,
                 uint64_t* d_out_n, cudaStream_t st) {
     const size_t smem = std::max<uint64_t>(nmax, 1) * sizeof(uint64_t);
-    static bool cfg = false;
-    if (!cfg) {
+    static launch::PerDeviceOnce cfg;
+    if (cfg.first()) {
         cudaFuncSetAttribute(select_set_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(kSmallSortMax * sizeof(uint64_t)));
-        cfg = true;
     }
     ::plaid::launch::pdl(select_set_cta_kernel, 1, kSelCtaThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_n);
     count_launch();
