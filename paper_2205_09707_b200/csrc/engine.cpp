@@ -469,7 +469,7 @@ void Searcher::enqueue(const float* d_q, uint32_t rows, const plaid_params& p, u
                        float* d_scores, uint64_t* d_n, cudaStream_t st, bool times, bool validate) {
     pending_rows_ = rows;
     enqueue_front(d_q, rows, p, st, times, validate);
-    enqueue_stage3(p, st, times);
+    enqueue_stage3(p, st, times, true);
     enqueue_back(d_q, rows, p, d_pids, d_scores, d_n, st, times);
 }
 
@@ -507,12 +507,16 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
     uint32_t* owners = bitmap_.p + (N + 31) / 32;
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
     uint64_t nsel;
-    bool bitmap_done = false;
+    bool bitmap_done = false, kept_ready = false;
     if (p.nprobe == K) {
         launch::iota(sel_.p, K, st);
         nsel = K;
     } else if (p.nprobe <= 32) {
-        launch::topn_postings(partial_.p, warps, npb, rows, uint32_t(p.nprobe), ix, sel_.p, bitmap, st);
+        // the kept-centroid list rides in the same launch unless stage 2 is skipped
+        launch::KeepListArgs kl{keep_.p, kept_list_.p, reinterpret_cast<unsigned long long*>(c + kKeptN)};
+        kept_ready = !p.disable_filter;
+        launch::topn_postings(partial_.p, warps, npb, rows, uint32_t(p.nprobe), ix, sel_.p, bitmap,
+                              kept_ready ? &kl : nullptr, st);
         nsel = uint64_t(rows) * p.nprobe;
         bitmap_done = true;
     } else {
@@ -536,7 +540,7 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
     // candidates owning a kept token are read (see kept_owners).
     launch::stage2_masked(ix, scores_.p, rows, c1_.p, c + kN1, N, keep_.p, bitmap, owners, kept_list_.p,
                           slot_of_.p, acc2_.p, reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p,
-                          reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, st);
+                          reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, kept_ready, st);
     record(3, st, times);
     launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st);
     record(4, st, times);
@@ -544,7 +548,8 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
 
 // Stage 3: full centroid interaction over sel2_, keep max(ceil(ndocs/4), k)
 // into sel3_ (sorted, count counters[kN3]).
-void Searcher::enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times) {
+void Searcher::enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times, bool fuse_scan) {
+    scan_fused_ = false;
     if (p.disable_filter) {
         record(5, st, times);
         return;
@@ -555,8 +560,14 @@ void Searcher::enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times
     launch::centroid_interaction(ix, scores_.p, pending_rows_, nullptr, sel2_.p, c + kN2, nd, nullptr, nullptr,
                                  keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
     // stage 4 needs only the top-stage3_width SET (the final select orders it)
+    // unsharded, stage 4's finalist scan runs in the select's own CTA
+    const uint64_t fin_max = std::min<uint64_t>(stage3_width(p), ix.N);
+    scan_fused_ = fuse_scan && nd <= launch::kSmallSortMax && rank_scratch_.pref &&
+                  launch::rank_stream128_ok(ix, pending_rows_, fin_max, rank_scratch_);
+    launch::FinalistScanArgs fs{ix.doclens, ix.offsets, rank_scratch_.pref, rank_scratch_.fin_base,
+                                rank_scratch_.tokens};
     if (nd <= launch::kSmallSortMax)
-        launch::select_set(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, c + kN3, st);
+        launch::select_set(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, c + kN3, scan_fused_ ? &fs : nullptr, st);
     else
         launch::sort_top(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, nullptr, nullptr, c + kN3, 0,
                          sort_tmp_.p, st);
@@ -583,7 +594,9 @@ void Searcher::enqueue_back(const float* d_q, uint32_t rows, const plaid_params&
         fin_n = c + kN3;
         fin_max = std::min<uint64_t>(stage3_width(p), ix.N);
     }
+    rank_scratch_.prescanned = scan_fused_ && !p.disable_filter;
     launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, &rank_scratch_, st);
+    rank_scratch_.prescanned = scan_fused_ = false;
     record(6, st, times);
     const uint32_t base = uint32_t(index_->pid_base());
     if (fin_max <= launch::kSmallSortMax) {
@@ -644,7 +657,7 @@ void Searcher::shard_phase2(const uint64_t* d_g2, uint64_t shards, uint64_t* d_x
     const uint32_t base = uint32_t(index_->pid_base());
     if (!p.disable_filter) {
         launch::threshold_filter(d_g2, shards * pending_stride2_, p.ndocs, sel2_.p, counters_.p + kN2, base, st);
-        enqueue_stage3(p, st, times);
+        enqueue_stage3(p, st, times, false);
         launch::export_keys(sel3_.p, counters_.p + kN3, stride3, base, d_x3, st);
     }
     pending_stride3_ = stride3;
@@ -704,7 +717,7 @@ void Searcher::batch_finish(const float* d_q, uint32_t rows, const plaid_params&
     DeviceGuard g(device_);
     pending_rows_ = rows;
     front_after_scores(rows, p, warps, st, false);
-    enqueue_stage3(p, st, false);
+    enqueue_stage3(p, st, false, true);
     enqueue_back(d_q, rows, p, d_pids, d_scores, d_n, st, false);
     PLAID_CUDA(cudaGetLastError());
     last_launches_ = launch::launches();

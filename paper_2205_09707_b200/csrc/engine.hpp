@@ -162,7 +162,7 @@ private:
     void enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st, bool times,
                        bool validate);
     void front_after_scores(uint32_t rows, const plaid_params& p, uint32_t warps, cudaStream_t st, bool times);
-    void enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times);
+    void enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times, bool fuse_scan);
     void enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,
                       uint64_t* d_n, cudaStream_t st, bool times);
     void ensure_param_buffers(const plaid_params& p);
@@ -208,6 +208,7 @@ private:
     float* out_scores_p_ = nullptr;
     uint32_t* h_res_ = nullptr;
     launch::RankScratch rank_scratch_;
+    bool scan_fused_ = false;  // stage 3's select ran stage 4's finalist scan
     DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_, bkeys_,
         tmp_keys_, kconst_;
     // zero_ = [16 u64 counters | candidate bitmap (N bits) | kept-owner bitmap

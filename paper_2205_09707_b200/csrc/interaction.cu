@@ -19,6 +19,7 @@
 #include <cstdint>
 
 #include "device.cuh"
+#include "fused.cuh"
 #include "kernels.cuh"
 
 namespace plaid {
@@ -298,37 +299,7 @@ __global__ void keep_list_kernel(const uint32_t* __restrict__ keep_bits, uint64_
                                  const uint64_t* __restrict__ ivf_offsets, uint32_t* __restrict__ list,
                                  unsigned long long* __restrict__ counts /* [0] kept, [1] postings */) {
     dev::pdl_wait();
-    const uint32_t lane = dev::lane_id();
-    const uint64_t words = (K + 31) / 32;
-    for (uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; w0 < words;
-         w0 += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t w = w0 + lane;
-        uint32_t bits = w < words ? keep_bits[w] : 0u;
-        if (w == words - 1 && (K & 31)) bits &= (1u << (K & 31)) - 1;
-        const uint32_t cnt = __popc(bits);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= uint32_t(o)) incl += y;
-        }
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        if (!tot) continue;
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(counts, (unsigned long long)tot);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        uint32_t slot = uint32_t(base) + incl - cnt;
-        unsigned long long post = 0;
-        while (bits) {
-            const uint32_t c = uint32_t(w * 32 + (__ffs(bits) - 1));
-            bits &= bits - 1;
-            list[slot++] = c;
-            post += ivf_offsets[c + 1] - ivf_offsets[c];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) post += __shfl_xor_sync(0xffffffffu, post, o);
-        if (lane == 0) atomicAdd(counts + 1, post);
-    }
+    fused::keep_list(blockIdx.x, gridDim.x, keep_bits, K, ivf_offsets, list, counts);
 }
 
 __device__ __forceinline__ bool use_lists(const unsigned long long* counts, uint64_t n1) {
@@ -402,14 +373,10 @@ __device__ __forceinline__ void hist_key(SelectHist* hs, uint64_t key, bool vali
     }
 }
 
-__global__ void stage2_finalize_kernel(const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
-                                       const unsigned long long* __restrict__ counts, uint32_t rows,
-                                       uint32_t* __restrict__ acc, const uint32_t* __restrict__ used_bits,
-                                       uint64_t* __restrict__ keys_out, SelectHist* __restrict__ hs) {
-    dev::pdl_wait();
+__device__ __forceinline__ void stage2_finalize(const uint32_t* __restrict__ c1, uint64_t n, uint32_t rows,
+                                                uint32_t* __restrict__ acc, const uint32_t* __restrict__ used_bits,
+                                                uint64_t* __restrict__ keys_out, SelectHist* __restrict__ hs) {
     __shared__ uint32_t zeros;
-    const uint64_t n = *d_n1;
-    if (!use_lists(counts, n)) return;
     if (threadIdx.x == 0) zeros = 0;
     __syncthreads();
     for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
@@ -441,15 +408,11 @@ __global__ void stage2_finalize_kernel(const uint32_t* __restrict__ c1, const ui
 }
 
 // fallback when the kept lists are long: warp per candidate over its codes
-__global__ void __launch_bounds__(256)
-ci_all_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
-              const uint32_t* __restrict__ doclens, const float* __restrict__ S, uint32_t rows,
-              const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
-              const unsigned long long* __restrict__ counts, const uint32_t* __restrict__ keep_bits,
-              uint64_t* __restrict__ keys_out, unsigned long long* __restrict__ d_rows, SelectHist* __restrict__ hs) {
-    dev::pdl_wait();
-    const uint64_t n = *d_n1;
-    if (use_lists(counts, n)) return;
+__device__ __forceinline__ void ci_all(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
+                                       const uint32_t* __restrict__ doclens, const float* __restrict__ S,
+                                       uint32_t rows, const uint32_t* __restrict__ c1, uint64_t n,
+                                       const uint32_t* __restrict__ keep_bits, uint64_t* __restrict__ keys_out,
+                                       unsigned long long* __restrict__ d_rows, SelectHist* __restrict__ hs) {
     const uint32_t lane = dev::lane_id();
     const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
     unsigned long long rows_local = 0;
@@ -465,6 +428,24 @@ ci_all_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ o
         rows_local += used;
     }
     if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+}
+
+// The stage-2 keys: the list finalize or, when the kept lists are long, the
+// per-candidate fallback — one launch, the branch taken on the device.
+__global__ void __launch_bounds__(256)
+stage2_keys_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
+                   const uint32_t* __restrict__ doclens, const float* __restrict__ S, uint32_t rows,
+                   const uint32_t* __restrict__ c1, const uint64_t* __restrict__ d_n1,
+                   const unsigned long long* __restrict__ counts, const uint32_t* __restrict__ keep_bits,
+                   uint32_t* __restrict__ acc, const uint32_t* __restrict__ used_bits,
+                   uint64_t* __restrict__ keys_out, unsigned long long* __restrict__ d_rows,
+                   SelectHist* __restrict__ hs) {
+    dev::pdl_wait();
+    const uint64_t n = *d_n1;
+    if (use_lists(counts, n))
+        stage2_finalize(c1, n, rows, acc, used_bits, keys_out, hs);
+    else
+        ci_all(codes, offsets, doclens, S, rows, c1, n, keep_bits, keys_out, d_rows, hs);
 }
 
 int sm_count() {
@@ -494,14 +475,13 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
                    const uint64_t* d_n1, uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_cand_bits,
                    uint32_t* d_used_bits, uint32_t* d_kept_list, const uint32_t* d_slot_of, uint32_t* d_acc,
                    unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows,
-                   SelectHist* d_hist, cudaStream_t st) {
+                   SelectHist* d_hist, bool kept_ready, cudaStream_t st) {
     const uint32_t sms = uint32_t(sm_count());
-    const uint64_t words = (ix.K + 31) / 32;
-    uint64_t kb = (words + 255) / 256;
-    if (kb == 0) kb = 1;
-    ::plaid::launch::pdl(keep_list_kernel, uint32_t(kb), 256, 0, st, d_keep_bits, ix.K, ix.ivf_offsets, d_kept_list,
-                         d_counts2);
-    count_launch();
+    if (!kept_ready) {
+        ::plaid::launch::pdl(keep_list_kernel, keep_list_blocks(ix.K), 256, 0, st, d_keep_bits, ix.K, ix.ivf_offsets,
+                             d_kept_list, d_counts2);
+        count_launch();
+    }
     if (nmax == 0) return;
     uint64_t sb = (nmax + 255) / 256;
     if (sb > uint64_t(sms) * 8) sb = uint64_t(sms) * 8;
@@ -509,11 +489,9 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
                          ix.ivf_postings, ix.ivf_mult, d_cand_bits, d_slot_of, d_scores, rows, ix.codes, ix.offsets,
                          ix.doclens, d_acc, d_used_bits, d_rows);
     count_launch();
-    ::plaid::launch::pdl(stage2_finalize_kernel, uint32_t(sb), 256, 0, st, d_c1, d_n1, d_counts2, rows, d_acc,
-                         d_used_bits, d_out_keys, d_hist);
-    count_launch();
-    ::plaid::launch::pdl(ci_all_kernel, sms * 2, 256, 0, st, ix.codes, ix.offsets, ix.doclens, d_scores, rows, d_c1, d_n1,
-                         d_counts2, d_keep_bits, d_out_keys, d_rows, d_hist);
+    if (sb < uint64_t(sms) * 2) sb = uint64_t(sms) * 2;  // the fallback's warp-per-candidate width
+    ::plaid::launch::pdl(stage2_keys_kernel, uint32_t(sb), 256, 0, st, ix.codes, ix.offsets, ix.doclens, d_scores, rows,
+                         d_c1, d_n1, d_counts2, d_keep_bits, d_acc, d_used_bits, d_out_keys, d_rows, d_hist);
     count_launch();
 }
 

@@ -128,9 +128,22 @@ uint32_t scores_tensor_max_warps();
 uint32_t scores_tensor_batch(const void* cmap, const IndexView& ix, const TfOut& out, uint32_t qb, uint32_t rows,
                              float t_cs, uint32_t np_bucket, cudaStream_t st);
 [[noreturn]] void fail_cuda_driver(int code, const char* what);
-// topn_merge + postings_to_bitmap in one launch (rows x nprobe CTAs).
+// Stage 2's kept-centroid list: list (K), counts[0] kept, counts[1] their
+// total posting count (both zeroed beforehand).
+struct KeepListArgs {
+    const uint32_t* keep_bits = nullptr;
+    uint32_t* list = nullptr;
+    unsigned long long* counts = nullptr;
+};
+inline uint32_t keep_list_blocks(uint64_t K) {
+    const uint64_t kb = ((K + 31) / 32 + 255) / 256;
+    return uint32_t(kb ? kb : 1);
+}
+// topn_merge + postings_to_bitmap in one launch (rows x nprobe CTAs), plus
+// the kept-centroid list when `kl` is given (then stage2_masked is called
+// with kept_ready).
 void topn_postings(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows, uint32_t nprobe,
-                   const IndexView& ix, uint32_t* d_sel, uint32_t* d_bitmap, cudaStream_t st);
+                   const IndexView& ix, uint32_t* d_sel, uint32_t* d_bitmap, const KeepListArgs* kl, cudaStream_t st);
 // Merge per-warp partial top-NP lists into sel[rows][nprobe] centroid ids.
 void topn_merge(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows,
                 uint32_t nprobe, uint32_t* d_sel, cudaStream_t st);
@@ -181,7 +194,7 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
                    const uint64_t* d_n1, uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_cand_bits,
                    uint32_t* d_used_bits, uint32_t* d_kept_list, const uint32_t* d_slot_of, uint32_t* d_acc,
                    unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows,
-                   SelectHist* d_hist, cudaStream_t st);
+                   SelectHist* d_hist, bool kept_ready, cudaStream_t st);
 
 // ---- selection -----------------------------------------------------------------------
 // Top `want` of keys[0..*d_n) (largest first).  Result: d_out_keys unsorted
@@ -206,10 +219,21 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
               uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
               uint32_t id_base, uint64_t* d_tmp, cudaStream_t st);
 uint64_t sort_tmp_capacity(uint64_t nmax);
+// Stage 4's finalist scan outputs (RankScratch pref / fin_base / tokens) and
+// the index arrays it reads.
+struct FinalistScanArgs {
+    const uint32_t* doclens = nullptr;
+    const uint64_t* offsets = nullptr;
+    uint32_t* pref = nullptr;
+    uint64_t* fin_base = nullptr;
+    uint64_t* tokens = nullptr;
+};
 // The top-`want` SET of keys[0..*d_n) (unordered), nmax <= kSmallSortMax, one
-// CTA (shared-memory radix select); *d_out_n = min(n, want).
+// CTA (shared-memory radix select); *d_out_n = min(n, want).  With `fs`, the
+// same CTA then runs stage 4's finalist scan over the set (rank_exact is
+// then called with RankScratch::prescanned).
 void select_set(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, uint64_t* d_out_keys,
-                uint64_t* d_out_n, cudaStream_t st);
+                uint64_t* d_out_n, const FinalistScanArgs* fs, cudaStream_t st);
 
 // Global-exact shard exchange (select.cu): export keys[0..*d_n) in global
 // form (ids + base) into a zero-padded row of `stride`; then, from the
@@ -230,11 +254,14 @@ struct RankScratch {
     uint64_t* fin_base = nullptr; // pass_cap: index token of stream position g is fin_base[p] + g
     uint64_t* tokens = nullptr;   // 1 counter: stage-4 stream length (trace)
     uint64_t pass_cap = 0;
+    bool prescanned = false;      // pref / fin_base / tokens already written (select_set)
 };
 constexpr uint64_t kStreamMaxPassages = 16384;
 void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
                 const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
                 const RankScratch* scratch, cudaStream_t st);
+// Whether rank_exact takes the streamed path (rank_stream128) for this shape.
+bool rank_stream128_ok(const IndexView& ix, uint32_t rows, uint64_t nmax, const RankScratch& s);
 bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
                     const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
                     const RankScratch& s, cudaStream_t st);

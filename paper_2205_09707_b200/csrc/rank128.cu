@@ -33,6 +33,7 @@
 #include <cstdlib>
 
 #include "device.cuh"
+#include "fused.cuh"
 #include "kernels.cuh"
 
 namespace plaid {
@@ -96,42 +97,7 @@ finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restric
                      const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pref,
                      uint64_t* __restrict__ fin_base, uint64_t* __restrict__ tokens) {
     dev::pdl_wait();
-    __shared__ uint32_t warp_sums[32];
-    const uint32_t n = uint32_t(*d_n);
-    const uint32_t per = (n + 1023) / 1024;
-    const uint32_t b = threadIdx.x * per, e = b + per < n ? b + per : n;
-    uint32_t local = 0;
-    for (uint32_t p = b; p < e; ++p) local += doclens[finalist_pid(ids, keys, p)];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= uint32_t(o)) incl += y;
-    }
-    if (lane == 31) warp_sums[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = warp_sums[lane], wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= uint32_t(o)) wi += y;
-        }
-        warp_sums[lane] = wi - w;  // exclusive
-    }
-    __syncthreads();
-    uint32_t run = warp_sums[warp] + incl - local;
-    for (uint32_t p = b; p < e; ++p) {
-        const uint32_t pid = finalist_pid(ids, keys, p);
-        pref[p] = run;
-        fin_base[p] = offsets[pid] - run;  // index token = fin_base[p] + stream position
-        run += doclens[pid];
-    }
-    if (threadIdx.x == 1023) {
-        pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)
-        if (tokens) *tokens = pref[n];
-    }
+    fused::finalist_scan(ids, keys, uint32_t(*d_n), doclens, offsets, pref, fin_base, tokens);
 }
 
 // Warp-cooperative: the finalist of stream token g (this lane's) for a
@@ -411,10 +377,14 @@ int sm_count() {
 
 namespace launch {
 
+bool rank_stream128_ok(const IndexView& ix, uint32_t rows, uint64_t nmax, const RankScratch& s) {
+    return ix.dim == 128 && rows <= 32 && nmax <= s.pass_cap && nmax * ix.max_doclen < (1ull << 32);
+}
+
 bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
                     const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
                     const RankScratch& s, cudaStream_t st) {
-    if (ix.dim != 128 || rows > 32 || nmax > s.pass_cap || nmax * ix.max_doclen >= (1ull << 32)) return false;
+    if (!rank_stream128_ok(ix, rows, nmax, s)) return false;
     Weights16 W;
     for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
     const size_t fsm = size_t(kSmemFloats) * sizeof(float);
@@ -424,9 +394,11 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
         cudaFuncSetAttribute(stream_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
         cudaFuncSetAttribute(stream_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fsm));
     }
-    ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref,
-                         s.fin_base, s.tokens);
-    count_launch();
+    if (!s.prescanned) {
+        ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref,
+                             s.fin_base, s.tokens);
+        count_launch();
+    }
     uint64_t fb = (nmax * ix.max_doclen + kTile - 1) / kTile;
     if (fb > uint64_t(sm_count()) * 2) fb = uint64_t(sm_count()) * 2;  // two CTAs (12 warps) per SM
     auto fk = ix.nbits == 1 ? stream_fused_kernel<1> : ix.nbits == 2 ? stream_fused_kernel<2> : stream_fused_kernel<4>;

@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "device.cuh"
+#include "fused.cuh"
 #include "kernels.cuh"
 
 namespace plaid {
@@ -163,11 +164,18 @@ __global__ void topn_merge_kernel(const uint64_t* __restrict__ partial, uint32_t
 // token i's partial lists (every CTA of the token redundantly — a few tens
 // of KB from L2) and ORs the postings of the token's j-th best centroid into
 // the N-bit candidate bitmap.
+// CTAs past rows x nprobe build stage 2's kept-centroid list (fused::keep_list)
+// when `kl` is given: it depends only on the S_cq keep bits, like this kernel.
 template <int NP>
 __global__ void topn_postings_kernel(const uint64_t* __restrict__ partial, uint32_t nwarps, uint32_t nprobe,
-                                     const uint64_t* __restrict__ ivf_offsets, const uint32_t* __restrict__ postings,
-                                     uint32_t* __restrict__ sel, uint32_t* __restrict__ bitmap) {
+                                     uint32_t ntopn, const uint64_t* __restrict__ ivf_offsets,
+                                     const uint32_t* __restrict__ postings, uint32_t* __restrict__ sel,
+                                     uint32_t* __restrict__ bitmap, launch::KeepListArgs kl, uint64_t K) {
     dev::pdl_wait();
+    if (blockIdx.x >= ntopn) {
+        fused::keep_list(blockIdx.x - ntopn, gridDim.x - ntopn, kl.keep_bits, K, ivf_offsets, kl.list, kl.counts);
+        return;
+    }
     extern __shared__ uint64_t lists[];  // blockDim x NP
     const uint32_t i = blockIdx.x / nprobe, j = blockIdx.x % nprobe;
     merge_token_lists<NP>(partial, nwarps, i, lists);
@@ -308,15 +316,18 @@ void launch_merge(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint3
 
 template <int NP>
 void launch_topn_postings(const uint64_t* partial, uint32_t nwarps, uint32_t rows, uint32_t nprobe,
-                          const IndexView& ix, uint32_t* sel, uint32_t* bitmap, cudaStream_t st) {
+                          const IndexView& ix, uint32_t* sel, uint32_t* bitmap, const launch::KeepListArgs* kl,
+                          cudaStream_t st) {
     const uint32_t threads = 256;
     const size_t smem = threads * NP * sizeof(uint64_t);
     static launch::PerDeviceOnce configured;
     if (configured.first()) {
         cudaFuncSetAttribute(topn_postings_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     }
-    ::plaid::launch::pdl(topn_postings_kernel<NP>, rows * nprobe, threads, smem, st, partial, nwarps, nprobe,
-                         ix.ivf_offsets, ix.ivf_postings, sel, bitmap);
+    const uint32_t ntopn = rows * nprobe;
+    const uint32_t nkb = kl ? launch::keep_list_blocks(ix.K) : 0;
+    ::plaid::launch::pdl(topn_postings_kernel<NP>, ntopn + nkb, threads, smem, st, partial, nwarps, nprobe, ntopn,
+                         ix.ivf_offsets, ix.ivf_postings, sel, bitmap, kl ? *kl : launch::KeepListArgs{}, ix.K);
     launch::count_launch();
 }
 
@@ -346,14 +357,15 @@ uint32_t scores_exact(const IndexView& ix, const float* d_q, uint32_t rows, floa
 }
 
 void topn_postings(const uint64_t* d_partial, uint32_t num_warps, uint32_t np_bucket, uint32_t rows, uint32_t nprobe,
-                   const IndexView& ix, uint32_t* d_sel, uint32_t* d_bitmap, cudaStream_t st) {
+                   const IndexView& ix, uint32_t* d_sel, uint32_t* d_bitmap, const KeepListArgs* kl,
+                   cudaStream_t st) {
     switch (np_bucket) {
-        case 1: launch_topn_postings<1>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
-        case 2: launch_topn_postings<2>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
-        case 4: launch_topn_postings<4>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
-        case 8: launch_topn_postings<8>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
-        case 16: launch_topn_postings<16>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
-        default: launch_topn_postings<32>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, st); break;
+        case 1: launch_topn_postings<1>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, kl, st); break;
+        case 2: launch_topn_postings<2>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, kl, st); break;
+        case 4: launch_topn_postings<4>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, kl, st); break;
+        case 8: launch_topn_postings<8>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, kl, st); break;
+        case 16: launch_topn_postings<16>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, kl, st); break;
+        default: launch_topn_postings<32>(d_partial, num_warps, rows, nprobe, ix, d_sel, d_bitmap, kl, st); break;
     }
 }
 

@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include "device.cuh"
+#include "fused.cuh"
 #include "kernels.cuh"
 
 namespace plaid {
@@ -674,7 +675,7 @@ threshold_filter_kernel(const uint64_t* __restrict__ g, uint64_t total, uint64_t
 constexpr uint32_t kSelCtaThreads = 1024;
 __global__ void __launch_bounds__(kSelCtaThreads)
 select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
-                      uint64_t* __restrict__ out, uint64_t* __restrict__ d_out_n) {
+                      uint64_t* out, uint64_t* __restrict__ d_out_n, launch::FinalistScanArgs fs) {
     dev::pdl_wait();
     extern __shared__ uint64_t sk[];
     __shared__ uint32_t hist[256];
@@ -690,6 +691,10 @@ select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
     if (s_done) {  // everything survives
         for (uint32_t i = t; i < n; i += kSelCtaThreads) out[i] = sk[i];
         if (t == 0) *d_out_n = n;
+        if (fs.pref) {
+            __syncthreads();
+            fused::finalist_scan(nullptr, out, n, fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens);
+        }
         return;
     }
     for (int shift = 56; shift >= 0 && !s_done; shift -= 8) {
@@ -741,6 +746,10 @@ select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
         if (ok) out[base + __popc(bal & ((1u << (t & 31)) - 1u))] = sk[i];
     }
     if (t == 0) *d_out_n = want;
+    if (fs.pref) {  // stage 4's finalist scan over the set just written, same CTA
+        __syncthreads();
+        fused::finalist_scan(nullptr, out, uint32_t(want), fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens);
+    }
 }
 
 }  // namespace
@@ -881,14 +890,15 @@ void threshold_filter(const uint64_t* d_gathered, uint64_t total, uint64_t want,
 }
 
 void select_set(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, uint64_t* d_out_keys,
-                uint64_t* d_out_n, cudaStream_t st) {
+                uint64_t* d_out_n, const FinalistScanArgs* fs, cudaStream_t st) {
     const size_t smem = std::max<uint64_t>(nmax, 1) * sizeof(uint64_t);
     static launch::PerDeviceOnce cfg;
     if (cfg.first()) {
         cudaFuncSetAttribute(select_set_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(kSmallSortMax * sizeof(uint64_t)));
     }
-    ::plaid::launch::pdl(select_set_cta_kernel, 1, kSelCtaThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_n);
+    ::plaid::launch::pdl(select_set_cta_kernel, 1, kSelCtaThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_n,
+                         fs ? *fs : FinalistScanArgs{});
     count_launch();
 }
 
