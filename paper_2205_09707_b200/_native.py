@@ -6,6 +6,7 @@ loudly when the in-tree build is missing.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _LIB_DIR = Path(__file__).resolve().parent / "_lib"
@@ -128,7 +129,8 @@ _lib = None
 
 
 def lib_path() -> Path:
-    return _LIB_DIR / "libplaid.so"
+    # PLAID_LIB: an alternative build of the same library (A/B timing runs)
+    return Path(os.environ["PLAID_LIB"]) if os.environ.get("PLAID_LIB") else _LIB_DIR / "libplaid.so"
 
 
 def load() -> C.CDLL:

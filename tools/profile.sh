@@ -11,6 +11,10 @@ mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu "$@" \
     > gpurun_out/${tag}_launches.log 2>&1
+# 1b. the same with caches left warm (L2 state as the previous kernel left it)
+ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 400 --csv \
+    --log-file gpurun_out/${tag}_launches_warm.csv python bench.py --steps 2 --warmup 3 --no-cpu "$@" \
+    > gpurun_out/${tag}_launches_warm.log 2>&1
 ncu --set full --clock-control none --import-source on -s 38 -c 40 \
     -o gpurun_out/${tag}_full -f python bench.py --steps 1 --warmup 3 --no-cpu "$@" \
     > gpurun_out/${tag}_full.log 2>&1
