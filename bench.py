@@ -290,7 +290,7 @@ def run_plaid(args, cfg):
     # the timed searcher records no phase events (an event between two kernels
     # breaks their programmatic-dependent-launch overlap); a second searcher
     # with phase events measures the per-stage breakdown after the timed loop
-    s = P.Searcher(idx, device=local, score_mode=mode, record_times=False)
+    s = P.Searcher(idx, device=local, score_mode=mode, record_times=False, use_graphs=args.graphs)
     s_ph = P.Searcher(idx, device=local, score_mode=mode, record_times=True)
 
     k = params.k
@@ -677,6 +677,7 @@ def main():
     ap.add_argument("--score-mode", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--graphs", action="store_true", help="host API search replays a captured CUDA graph (e2e)")
     ap.add_argument("--flush", default="write", choices=["write", "write+read"],
                     help="untimed L2 reset between steps")
     ap.add_argument("--lanes", type=int, default=8, help="throughput mode: concurrent searcher lanes")

@@ -84,12 +84,24 @@ void validate_query_host(const float* q, uint64_t rows, uint64_t dim, uint64_t i
         fail(PLAID_DIMENSION_MISMATCH, "query dim " + std::to_string(dim) +
                                            " does not match index dim " + std::to_string(index_dim));
     const double tol = double(1e-3f);
-    for (uint64_t r = 0; r < rows; ++r) {
-        double acc = 0.0;
-        for (uint64_t d = 0; d < dim; ++d) acc += double(q[r * dim + d]) * double(q[r * dim + d]);
-        const double norm = std::sqrt(acc);
-        if (std::fabs(norm - 1.0) > tol)
-            fail(PLAID_NOT_NORMALIZED, "query row " + std::to_string(r) + " has L2 norm " + std::to_string(norm));
+    // each row's sum in dim order, eight rows' chains interleaved (the
+    // search path's host cost; same per-row rounding as one row at a time)
+    constexpr uint64_t kR = 8;
+    for (uint64_t r0 = 0; r0 < rows; r0 += kR) {
+        const uint64_t nr = rows - r0 < kR ? rows - r0 : kR;
+        double acc[kR] = {};
+        for (uint64_t d = 0; d < dim; ++d)
+            for (uint64_t j = 0; j < kR; ++j)
+                if (j < nr) {
+                    const double x = double(q[(r0 + j) * dim + d]);
+                    acc[j] += x * x;
+                }
+        for (uint64_t j = 0; j < nr; ++j) {
+            const double norm = std::sqrt(acc[j]);
+            if (std::fabs(norm - 1.0) > tol)
+                fail(PLAID_NOT_NORMALIZED,
+                     "query row " + std::to_string(r0 + j) + " has L2 norm " + std::to_string(norm));
+        }
     }
 }
 
