@@ -83,6 +83,15 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Slot of key bucket b in SelectHist::hist: each 2048-bucket block is stored
+// transposed (bucket 32 j + l at 64 l + j), so the run of consecutive buckets
+// a query's scores fill is spread over 32 cache lines instead of a few — the
+// producers' histogram atomics otherwise queue on one L2 slice.  Block sums
+// are unchanged; hist_find walks a block through shared memory.
+__device__ __forceinline__ uint32_t hist_slot(uint32_t b) {
+    return (b & ~0x7FFu) | ((b & 31u) << 6) | ((b >> 5) & 63u);
+}
+
 // Branchless insertion of x into a descending list k[0..NP) of unique keys.
 template <int NP>
 __device__ __forceinline__ void topn_insert(uint64_t (&k)[NP], uint64_t x) {

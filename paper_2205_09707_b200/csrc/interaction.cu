@@ -369,7 +369,7 @@ __device__ __forceinline__ void hist_key(SelectHist* hs, uint64_t key, bool vali
     const uint32_t peers = __match_any_sync(0xffffffffu, b);
     if (valid && lane == uint32_t(__ffs(peers) - 1)) {
         if (b == kHistZeroBucket) atomicAdd(zeros, uint32_t(__popc(peers)));
-        else atomicAdd(&hs->hist[b], uint32_t(__popc(peers)));
+        else atomicAdd(&hs->hist[dev::hist_slot(b)], uint32_t(__popc(peers)));
     }
 }
 
@@ -404,7 +404,7 @@ __device__ __forceinline__ void stage2_finalize(const uint32_t* __restrict__ c1,
         hist_key(hs, key, i < n, &zeros);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && zeros) atomicAdd(&hs->hist[kHistZeroBucket], zeros);
+    if (threadIdx.x == 0 && zeros) atomicAdd(&hs->hist[dev::hist_slot(kHistZeroBucket)], zeros);
 }
 
 // fallback when the kept lists are long: warp per candidate over its codes
@@ -423,7 +423,7 @@ __device__ __forceinline__ void ci_all(const uint32_t* __restrict__ codes, const
         if (lane == 0) {
             const uint64_t key = dev::make_key(total, pid);
             keys_out[i] = key;
-            atomicAdd(&hs->hist[uint32_t(key >> kHistShift)], 1u);
+            atomicAdd(&hs->hist[dev::hist_slot(uint32_t(key >> kHistShift))], 1u);
         }
         rows_local += used;
     }

@@ -410,13 +410,15 @@ constexpr uint32_t kHistBucketShift = kHistShift;
 constexpr uint32_t kRankCap = 8192;  // boundary buckets up to this size are ranked in parallel
 
 // One CTA: the bucket (from the top) holding the want-th largest key.  Warp
-// w sums buckets [2048 w, 2048 w + 2048) with coalesced loads; the warp whose
-// range holds the target walks it from the top, 32 buckets per step.  Also
-// (re)initialises the control words for this select.
+// w sums buckets [2048 w, 2048 w + 2048) (one transposed block, see
+// dev::hist_slot) with coalesced loads; the warp whose range holds the target
+// stages its block in shared memory and walks it from the top, 32 buckets per
+// step.  Also (re)initialises the control words for this select.
 __global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restrict__ d_n, uint64_t want,
                                                          SelectHist* __restrict__ st) {
     dev::pdl_wait();
     __shared__ unsigned long long warp_tot[32];
+    __shared__ uint32_t blk[32 * 65];  // the target block, row l = buckets 32 j + l (padded)
     const uint64_t n = *d_n;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) {
@@ -441,8 +443,11 @@ __global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restr
     unsigned long long above = 0;
     for (uint32_t w = warp + 1; w < 32; ++w) above += warp_tot[w];
     if (!(above < want && want <= above + warp_tot[warp])) return;
+#pragma unroll 8
+    for (uint32_t a = lane; a < 2048; a += 32) blk[(a >> 6) * 65 + (a & 63)] = hw[a];
+    __syncwarp();
     for (int j = 63; j >= 0; --j) {
-        const uint32_t c = hw[j * 32 + lane];
+        const uint32_t c = blk[lane * 65 + j];  // bucket 32 j + lane
         // inclusive sum from the top lane down (bucket 32 j + 31 first)
         uint32_t incl = c;
 #pragma unroll
