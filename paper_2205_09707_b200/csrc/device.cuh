@@ -83,6 +83,18 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// *dst += the sum over the block's warps of lane 0's v: one global atomic per
+// CTA instead of one per warp (thousands of same-address atomics queue on one
+// L2 slice).  Every thread of the block must call it.
+__device__ __forceinline__ void block_add_lane0(unsigned long long* dst, unsigned long long v) {
+    __shared__ unsigned long long tot;
+    if (threadIdx.x == 0) tot = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31u) == 0 && v) atomicAdd(&tot, v);
+    __syncthreads();
+    if (threadIdx.x == 0 && tot) atomicAdd(dst, tot);
+}
+
 // Slot of key bucket b in SelectHist::hist: each 2048-bucket block is stored
 // transposed (bucket 32 j + l at 64 l + j), so the run of consecutive buckets
 // a query's scores fill is spread over 32 cache lines instead of a few — the

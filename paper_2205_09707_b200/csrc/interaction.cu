@@ -101,7 +101,7 @@ ci_warp_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ 
         }
         rows_local += used;
     }
-    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+    dev::block_add_lane0(d_rows, rows_local);
 }
 
 // Stage 2: masked, flattened over the block's concatenated token range.
@@ -241,7 +241,7 @@ ci_masked_flat_kernel(const uint32_t* __restrict__ codes, const uint64_t* __rest
     // block-level reduction of the gathered-row counter
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rows_local += __shfl_xor_sync(0xffffffffu, rows_local, o);
-    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+    dev::block_add_lane0(d_rows, rows_local);
 }
 
 // owners |= postings of every kept centroid: the passages that own at least
@@ -357,7 +357,7 @@ ivf_accumulate_kernel(const uint32_t* __restrict__ list, const unsigned long lon
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rows_local += __shfl_xor_sync(0xffffffffu, rows_local, o);
-    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+    dev::block_add_lane0(d_rows, rows_local);
 }
 
 // Key histogram for the stage-2 select (select_top_hist): bucket = top 16
@@ -427,7 +427,7 @@ __device__ __forceinline__ void ci_all(const uint32_t* __restrict__ codes, const
         }
         rows_local += used;
     }
-    if (lane == 0 && rows_local) atomicAdd(d_rows, rows_local);
+    dev::block_add_lane0(d_rows, rows_local);
 }
 
 // The stage-2 keys: the list finalize or, when the kept lists are long, the

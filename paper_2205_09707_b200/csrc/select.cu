@@ -480,25 +480,39 @@ __global__ void hist_compact_kernel(const uint64_t* __restrict__ keys, const uin
     const uint32_t lane = threadIdx.x & 31;
     // hist_find has consumed the histogram: leave it zero for the next select
     for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < 65536; b += gridDim.x * blockDim.x) st->hist[b] = 0;
-    for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
-         i0 += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t i = i0 + lane;
+    // one atomic per CTA and output (the CTA's warps take consecutive ranges):
+    // per-warp atomics on the two counters queue on one L2 slice
+    __shared__ uint32_t wa[32], wb[32];
+    __shared__ unsigned long long ca, cb;
+    const uint32_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (uint64_t b0 = uint64_t(blockIdx.x) * blockDim.x; b0 < n; b0 += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = b0 + threadIdx.x;
         const uint64_t k = i < n ? __ldcg(keys + i) : 0;
         const uint32_t b = uint32_t(k >> kHistBucketShift);
         const bool above = i < n && (all || b > bucket), inb = i < n && !all && b == bucket;
         const uint32_t ba = __ballot_sync(0xffffffffu, above), bb = __ballot_sync(0xffffffffu, inb);
-        if (ba) {
-            unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd((unsigned long long*)out_n, (unsigned long long)__popc(ba));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (above) out[base + __popc(ba & ((1u << lane) - 1))] = k;
+        if (lane == 0) wa[warp] = __popc(ba), wb[warp] = __popc(bb);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            // exclusive scans of the warp counts, one atomic per counter
+            const uint32_t xa = lane < nwarps ? wa[lane] : 0u, xb = lane < nwarps ? wb[lane] : 0u;
+            uint32_t ia = xa, ib = xb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o), yb = __shfl_up_sync(0xffffffffu, ib, o);
+                if (lane >= uint32_t(o)) ia += ya, ib += yb;
+            }
+            const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
+            if (lane == 0) {
+                ca = ta ? atomicAdd((unsigned long long*)out_n, (unsigned long long)ta) : 0ull;
+                cb = tb ? atomicAdd(&st->bn, (unsigned long long)tb) : 0ull;
+            }
+            if (lane < nwarps) wa[lane] = ia - xa, wb[lane] = ib - xb;
         }
-        if (bb) {
-            unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(&st->bn, (unsigned long long)__popc(bb));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (inb) bkeys[base + __popc(bb & ((1u << lane) - 1))] = k;
-        }
+        __syncthreads();
+        if (above) out[ca + wa[warp] + __popc(ba & ((1u << lane) - 1))] = k;
+        if (inb) bkeys[cb + wb[warp] + __popc(bb & ((1u << lane) - 1))] = k;
+        __syncthreads();  // wa / wb / ca / cb are rewritten by the next round
     }
 }
 
