@@ -54,14 +54,20 @@ __device__ float score_passage_warp(const uint32_t* __restrict__ codes, uint64_t
         if (MASKED) valid = valid && kept(keep_bits, code);
         uint32_t bits = __ballot_sync(0xffffffffu, valid);
         used += __popc(bits);
-        // all (up to 32) S-row gathers of the chunk in flight at once, then
-        // the maxima in token order (`if (s > acc)`, pipeline.cpp:121-123)
+        if (!bits) continue;  // every token of the chunk masked
+        // all 32 S-row gathers of the chunk in flight at once, then the
+        // maxima in token order (`if (s > acc)`, pipeline.cpp:121-123).  The
+        // loads are unpredicated (a predicated load holds one of the 7
+        // predicate registers until it lands, capping the loads in flight):
+        // slots past the chunk's valid tokens repeat the last valid one,
+        // which cannot change a strict running max
+        const int last = 31 - __clz(bits);
         float s[32];
 #pragma unroll
         for (int v = 0; v < 32; ++v) {
-            const int b = bits ? __ffs(bits) - 1 : 0;
+            const int b = bits ? __ffs(bits) - 1 : last;
             const uint32_t c = __shfl_sync(0xffffffffu, code, b);
-            s[v] = bits ? __ldg(S + uint64_t(c) * kScoresPitch + lane) : -INFINITY;
+            s[v] = __ldg(S + uint64_t(c) * kScoresPitch + lane);
             bits &= bits - 1;
         }
 #pragma unroll
