@@ -182,9 +182,19 @@ __global__ void topn_postings_kernel(const uint64_t* __restrict__ partial, uint3
     const uint32_t c = dev::key_id(lists[j]);
     if (threadIdx.x == 0) sel[i * nprobe + j] = c;
     const uint64_t b = ivf_offsets[c], e = ivf_offsets[c + 1];
-    for (uint64_t t = b + threadIdx.x; t < e; t += blockDim.x) {
-        const uint32_t p = __ldg(postings + t);
-        atomicOr(bitmap + (p >> 5), 1u << (p & 31));
+    // kU postings per thread in flight: unpredicated loads (index clamped into
+    // the list), so the ~2K-entry list costs ~3 HBM round trips, not ~9
+    constexpr uint32_t kU = 4;
+    for (uint64_t t0 = b + threadIdx.x; t0 < e; t0 += kU * blockDim.x) {
+        uint32_t p[kU];
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u) {
+            const uint64_t t = t0 + u * blockDim.x;
+            p[u] = __ldg(postings + (t < e ? t : e - 1));
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u)
+            if (t0 + u * blockDim.x < e) atomicOr(bitmap + (p[u] >> 5), 1u << (p[u] & 31));
     }
 }
 
