@@ -431,10 +431,18 @@ __global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restr
     }
     if (n <= want) return;
     __syncthreads();
-    const uint32_t* hw = st->hist + warp * 2048;
+    // the warp's 8 KB block as 16 x 16-byte loads per lane, 8 in flight at a
+    // time (the 64-register cap of a 1024-thread CTA): 2 L2 round trips
+    const uint4* hw4 = reinterpret_cast<const uint4*>(st->hist + warp * 2048);
     unsigned long long mine = 0;
-#pragma unroll 8
-    for (uint32_t j = 0; j < 64; ++j) mine += hw[j * 32 + lane];
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+        uint4 v[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) v[j] = __ldcg(hw4 + (h * 8 + j) * 32 + lane);
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) mine += uint64_t(v[j].x) + v[j].y + v[j].z + v[j].w;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     if (lane == 0) warp_tot[warp] = mine;
@@ -443,8 +451,18 @@ __global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restr
     unsigned long long above = 0;
     for (uint32_t w = warp + 1; w < 32; ++w) above += warp_tot[w];
     if (!(above < want && want <= above + warp_tot[warp])) return;
-#pragma unroll 8
-    for (uint32_t a = lane; a < 2048; a += 32) blk[(a >> 6) * 65 + (a & 63)] = hw[a];
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+        uint4 v[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) v[j] = __ldcg(hw4 + (h * 8 + j) * 32 + lane);
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            const uint32_t a = 4 * ((h * 8 + j) * 32 + lane);  // slots a .. a + 3 (one row of blk)
+            uint32_t* r = blk + (a >> 6) * 65 + (a & 63);
+            r[0] = v[j].x, r[1] = v[j].y, r[2] = v[j].z, r[3] = v[j].w;
+        }
+    }
     __syncwarp();
     for (int j = 63; j >= 0; --j) {
         const uint32_t c = blk[lane * 65 + j];  // bucket 32 j + lane
