@@ -13,10 +13,12 @@
 // and errors keep their lir::ErrorCode (a plaid_status is the ErrorCode + 1,
 // error.hpp:8-26); CUDA/NCCL failures and requests outside the engine's
 // envelope surface as std::runtime_error.  Timings in the returned StageTrace
-// come from CUDA events (pipeline.hpp:23-43 fields, in milliseconds).
+// come from CUDA events (pipeline.hpp:23-43 fields, in milliseconds) when the
+// Engine is created with record_times.
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -57,17 +59,27 @@ inline plaid_index_desc describe(const lir::CompressedIndex& ix) {
     return d;
 }
 
+// Thread safety: lir::search is a reentrant free function over an immutable
+// index (index.hpp:57-59).  An Engine owns ONE plaid_searcher (stream,
+// scratch, pinned staging), so Engine::search serialises its callers on a
+// mutex; for concurrent queries create one Engine per host thread (each
+// uploads its own index copy) or use the C ABI directly with one
+// plaid_searcher per thread over a shared plaid_index.
 class Engine {
 public:
     // Uploads the index to `device` (validate: re-run validate_index's
     // invariants on the way, index.cpp:12-84) and creates one searcher.
+    // record_times fills StageTrace's *_ms fields from CUDA events between
+    // the stages; it costs ~40 us per query (events break the programmatic
+    // dependent launch chain), so it is off unless asked for.
     explicit Engine(const lir::CompressedIndex& index, int device = 0,
-                    plaid_score_mode mode = PLAID_SCORES_TENSOR, bool validate = false) {
+                    plaid_score_mode mode = PLAID_SCORES_TENSOR, bool validate = false,
+                    bool record_times = false) {
         const plaid_index_desc d = describe(index);
         check(plaid_index_from_host(&d, device, validate ? 1 : 0, &index_));
         plaid_searcher_config cfg{};
         cfg.score_mode = mode;
-        cfg.record_times = 1;
+        cfg.record_times = record_times ? 1 : 0;
         const plaid_status st = plaid_searcher_create(index_, device, &cfg, &searcher_);
         if (st != PLAID_OK) {
             plaid_index_close(index_);
@@ -91,7 +103,10 @@ public:
         std::vector<float> scores(ids.size());
         uint64_t n = 0;
         plaid_trace t{};
-        check(plaid_search(searcher_, q.data.data(), q.rows, q.dim, &p, ids.data(), scores.data(), &n, &t));
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            check(plaid_search(searcher_, q.data.data(), q.rows, q.dim, &p, ids.data(), scores.data(), &n, &t));
+        }
         lir::SearchResult r;
         ids.resize(n);
         scores.resize(n);
@@ -118,6 +133,7 @@ public:
 private:
     plaid_index* index_ = nullptr;
     plaid_searcher* searcher_ = nullptr;
+    mutable std::mutex mu_;
 };
 
 }  // namespace plaid_lir

@@ -123,6 +123,8 @@ SIGNATURES = {
     "plaid_maxsim_packed": (C.c_int, [C.c_void_p, f32p, C.c_uint64, u64p, C.c_uint64, f32p]),
     "plaid_maxsim_embeddings": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_uint64, f32p, u64p, C.c_uint64,
                                           f32p]),
+    # test knobs (not part of include/plaid.h)
+    "plaid_debug_set_tf32_grid": (C.c_uint32, [C.c_uint32]),
 }
 
 _lib = None

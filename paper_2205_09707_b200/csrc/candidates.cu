@@ -114,17 +114,25 @@ __global__ void chunk_write_kernel(const uint32_t* __restrict__ bitmap, uint64_t
 
 // Single pass (decoupled look-back): every chunk publishes its popcount with
 // a ready flag, then sums its predecessors' published counts (spinning on
-// their flags — all chunks are resident: <= 2^32 / 65536 CTAs of 256 threads)
-// and writes its ids in order.  `status` (one u64 per chunk) must be zero on
-// entry (the per-query prologue clears it).
+// their flags) and writes its ids in order.  A CTA takes its chunk from a
+// ticket counter (status[nchunks]), not from blockIdx.x: CTAs are not
+// dispatched in blockIdx order, and with more chunks than resident CTAs a
+// CTA spinning on a lower chunk that was never scheduled would deadlock.
+// With tickets every lower chunk belongs to a CTA that is already running.
+// `status` (nchunks + 1 u64) must be zero on entry (the per-query prologue
+// clears it).
 __global__ void chunk_compact_kernel(const uint32_t* __restrict__ bitmap, uint64_t N,
                                      unsigned long long* __restrict__ status, uint32_t* __restrict__ out,
                                      uint64_t* __restrict__ out_n, uint32_t* __restrict__ slot_of) {
     dev::pdl_wait();
     __shared__ uint64_t red[kThreads / 32];
     __shared__ uint32_t scan[kThreads / 32];
+    __shared__ uint32_t ticket;
     constexpr unsigned long long kReady = 1ull << 63;
-    const uint64_t w0 = uint64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
+    if (threadIdx.x == 0) ticket = uint32_t(atomicAdd(status + gridDim.x, 1ull));
+    __syncthreads();
+    const uint32_t chunk = ticket;
+    const uint64_t w0 = uint64_t(chunk) * kChunkWords + threadIdx.x * kWordsPerThread;
     uint32_t words[kWordsPerThread];
     uint32_t mine = 0;
 #pragma unroll
@@ -148,11 +156,11 @@ __global__ void chunk_compact_kernel(const uint32_t* __restrict__ bitmap, uint64
         total += scan[k];
     }
     if (threadIdx.x == 0) {
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(status + blockIdx.x), "l"(kReady | total) : "memory");
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(status + chunk), "l"(kReady | total) : "memory");
     }
     // look back: the counts of every earlier chunk
     uint64_t part = 0;
-    for (uint32_t c = threadIdx.x; c < blockIdx.x; c += kThreads) {
+    for (uint32_t c = threadIdx.x; c < chunk; c += kThreads) {
         unsigned long long v;
         do {
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(status + c) : "memory");
@@ -177,7 +185,7 @@ __global__ void chunk_compact_kernel(const uint32_t* __restrict__ bitmap, uint64
             out[pos++] = pid;
         }
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kThreads - 1) *out_n = pos;
+    if (chunk == gridDim.x - 1 && threadIdx.x == kThreads - 1) *out_n = pos;
 }
 
 }  // namespace

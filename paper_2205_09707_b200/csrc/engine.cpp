@@ -356,11 +356,12 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
     PLAID_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     for (auto& e : ev_) PLAID_CUDA(cudaEventCreate(&e));
     const uint64_t words = index_ ? (index_->view().N + 31) / 32 : 0;
-    // [candidate bitmap | used bitmap | per-chunk compaction status (u64)],
-    // whole 16-byte units, cleared per query by the prologue kernel
+    // [candidate bitmap | used bitmap | per-chunk compaction status (u64) +
+    // the compaction's ticket counter], whole 16-byte units, cleared per
+    // query by the prologue kernel
     const uint64_t chunks = index_ ? launch::bitmap_chunks(index_->view().N) : 1;
     const uint64_t bm_words = (2 * words + 3) / 4 * 4;
-    zero_.ensure(bm_words + (2 * chunks + 3) / 4 * 4);
+    zero_.ensure(bm_words + (2 * (chunks + 1) + 3) / 4 * 4);
     PLAID_CUDA(cudaMemset(zero_.p, 0, zero_.n * sizeof(uint32_t)));
     bitmap_.p = zero_.p;
     compact_status_ = reinterpret_cast<unsigned long long*>(zero_.p + bm_words);

@@ -41,6 +41,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -545,9 +546,17 @@ void launch_tf32_np(const CUtensorMap& map, const IndexView& ix, const TfOut& ou
     }
 }
 
+// Test knob (plaid_debug_set_tf32_grid): cap the persistent grid so a small K
+// still runs many tiles per CTA (TMA ring wrap, both accumulator groups, the
+// grid-wide bound exchange).  0 = one CTA per SM.
+std::atomic<uint32_t> g_tf32_grid_cap{0};
+
 uint32_t tf32_grid(const IndexView& ix) {
     const uint64_t ntiles = (ix.K + 127) / 128;
-    uint32_t grid = uint32_t(ntiles < uint64_t(sm_count()) ? ntiles : uint64_t(sm_count()));
+    uint64_t cap = uint64_t(sm_count());
+    const uint32_t dbg_cap = g_tf32_grid_cap.load(std::memory_order_relaxed);
+    if (dbg_cap && dbg_cap < cap) cap = dbg_cap;
+    uint32_t grid = uint32_t(ntiles < cap ? ntiles : cap);
     return grid ? grid : 1;
 }
 
@@ -613,6 +622,9 @@ uint32_t scores_tensor_batch(const void* cmap, const IndexView& ix, const TfOut&
 
 // Debug: copy the pipeline timeline (see trace_stamp / cta_stamp) to the host:
 // out[0..2048) = CTA 0 events, out[2048..2560) = per-CTA begin/end.
+// Test knob: cap the S_cq grid at `ctas` CTAs (0 = one per SM); returns the old cap.
+extern "C" uint32_t plaid_debug_set_tf32_grid(uint32_t ctas) { return plaid::g_tf32_grid_cap.exchange(ctas); }
+
 extern "C" int plaid_debug_tf32_trace(unsigned long long* out) {
     int rc = int(cudaMemcpyFromSymbol(out, plaid::g_tf32_trace, sizeof(plaid::g_tf32_trace)));
     if (!rc) rc = int(cudaMemcpyFromSymbol(out + 8 * 256, plaid::g_tf32_cta, sizeof(plaid::g_tf32_cta)));

@@ -167,7 +167,7 @@ void postings_to_bitmap(const IndexView& ix, const uint32_t* d_sel, uint32_t nse
 // Bitmap (N bits) -> ascending ids + count.  chunk_counts has bitmap_chunks(N) entries.
 uint32_t bitmap_chunks(uint64_t N);
 // d_slot_of (optional, N): slot_of[pid] = position of pid in the output.
-// Same in one launch; d_status: bitmap_chunks(N) u64, zero on entry.
+// Same in one launch; d_status: bitmap_chunks(N) + 1 u64 (chunk flags + ticket counter), zero on entry.
 void bitmap_compact_1pass(const uint32_t* d_bitmap, uint64_t N, unsigned long long* d_status, uint32_t* d_out_ids,
                           uint64_t* d_out_n, uint32_t* d_slot_of, cudaStream_t st);
 void bitmap_compact(const uint32_t* d_bitmap, uint64_t N, uint32_t* d_chunk_counts,

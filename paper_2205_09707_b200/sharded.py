@@ -99,6 +99,7 @@ class ShardedSearcher:
         self.n = self.row[2 * self.k:].view(torch.int64)
         self.out_pids, self.out_scores = z(self.k, dt=torch.int32), z(self.k, dt=torch.float32)
         self.out_n = z(1, dt=torch.int64)
+        self._last_stream, self._last_df = 0, False
 
     def _xbuf(self, name: str, n: int) -> torch.Tensor:
         t = self._x.get(name)
@@ -130,6 +131,7 @@ class ShardedSearcher:
         rows, dim = q.shape
         df = bool(options.disable_filter) if options is not None else False
         kw = {"options": options} if options is not None else {}
+        self._last_stream, self._last_df = stream, df
         if self.mode == "shard-local":
             self.s.search_device(q.data_ptr(), 1, rows, dim, params, self.pids.data_ptr(), self.scores.data_ptr(),
                                  self.n.data_ptr(), stream=stream, **kw)
@@ -150,15 +152,25 @@ class ShardedSearcher:
                                       self.out_scores.data_ptr(), self.out_n.data_ptr(), stream=stream)
         return self.out_pids, self.out_scores, self.out_n
 
-    def trace_counters(self, stream: int = 0) -> dict:
+    def trace_counters(self) -> dict:
         """StageTrace counters of the last search summed over the shards
-        (global-exact: equal to the unsharded reference's).  Host sync."""
+        (global-exact: equal to the unsharded reference's).  Host sync.
+
+        The device copy runs on the stream the last search() used (recorded
+        there), after a device-wide sync so the counters are final and the
+        zero fill of the target is done; with disable_filter the reference
+        reports stage1_candidates as stage2_out and stage3_out
+        (pipeline.cpp:255-258)."""
         c = torch.zeros(6, dtype=torch.int64, device=self.dev)
-        self.s.trace_counters_device(c.data_ptr(), stream=stream)
         if self.dev.type == "cuda":
-            torch.cuda.current_stream(self.dev).synchronize()
+            torch.cuda.synchronize(self.dev)
+        self.s.trace_counters_device(c.data_ptr(), stream=self._last_stream)
+        if self.dev.type == "cuda":
+            torch.cuda.synchronize(self.dev)
         dist.all_reduce(c, group=self.group)
         v = c.cpu().tolist()
+        if self._last_df:
+            v[1] = v[2] = v[0]
         return {"stage1_candidates": v[0], "stage2_out": v[1], "stage3_out": v[2],
                 "stage2_rows_gathered": v[4], "stage3_rows_gathered": v[5]}
 

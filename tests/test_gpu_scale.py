@@ -1,0 +1,162 @@
+"""GPU parity of the PRODUCTION (TENSOR) path at the scale it is benchmarked at.
+
+* K = 2^18 centroids (BASELINE configs[1]'s centroid count): the persistent
+  tcgen05 S_cq kernel runs ~14 tiles per CTA, so its TMA ring wraps, both
+  accumulator groups run and the grid-wide top-nprobe bound exchange fires.
+* The same steady state forced at small K by capping the grid to a few CTAs.
+* cfg1 exactly (10k passages, K = 4096, nbits = 2, k = 10) in both modes.
+* TENSOR results against the unmodified reference (`oracle/_ref`, i.e.
+  lir::search) with the north_star comparator (oracle/compare.py): integer
+  sets exact except near t_cs / the nprobe, ndocs and top-k boundaries,
+  MaxSim within 1e-4 relative.
+* The two-queries-per-pass batched S_cq (throughput mode) against the oracle.
+"""
+import numpy as np
+import pytest
+
+import paper_2205_09707_b200 as P
+from oracle.compare import check_tensor_search
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def best():
+    """The compiled reference when present (faster, and it IS lir), else the C restatement."""
+    import oracle
+
+    return oracle.get("ref") if oracle.available("ref") else oracle.get("port")
+
+
+def _check(best, h, q, p, s_tensor, **kw):
+    r = s_tensor.search(q, p, **kw)
+    S, _ = s_tensor.compute_centroid_scores(q)
+    rep = check_tensor_search(best, h, q, p, r.topk.passage_ids, r.topk.scores, S,
+                              got_counters=r.trace.counters(),
+                              disable_filter=bool(kw.get("options") and kw["options"].disable_filter))
+    assert rep.ok, rep.as_dict()
+    return rep
+
+
+@pytest.fixture(scope="module")
+def bigk():
+    """K = 2^18 (cfg2's centroid table: 2048 S_cq tiles, ~14 per CTA), N = 150k."""
+    h = P.generate_index(150_000, 1 << 18, dim=128, nbits=2, mean_len=68, seed=17)
+    qs = P.generate_queries(h, 3, seed=5)
+    idx = P.DeviceIndex.from_host(h)
+    return h, qs, idx
+
+
+def test_bigk_tensor_scores(bigk, best):
+    h, qs, idx = bigk
+    s = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+    for q in qs:
+        S, mx = s.compute_centroid_scores(q)
+        S0, mx0 = best.compute_centroid_scores(h, q)
+        assert np.abs(S - S0).max() < 5e-6
+        assert np.abs(mx - mx0).max() < 5e-6
+
+
+@pytest.mark.parametrize("k", [10, 100, 1000])
+def test_bigk_exact_bit_exact(bigk, best, k):
+    h, qs, idx = bigk
+    s = P.Searcher(idx, score_mode=P.ScoreMode.EXACT)
+    p = P.default_params_for_k(k)
+    for q in qs[:2]:
+        got = s.search(q, p)
+        ids, sc, tr = best.search(h, q, p)
+        assert np.array_equal(got.topk.passage_ids, ids)
+        assert np.array_equal(bits(got.topk.scores), bits(sc))
+        assert got.trace.counters() == tr
+
+
+@pytest.mark.parametrize("k", [10, 100, 1000])
+def test_bigk_tensor_vs_reference(bigk, best, k):
+    """TENSOR (the benchmarked mode) vs lir::search at K = 2^18."""
+    h, qs, idx = bigk
+    s = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+    p = P.default_params_for_k(k)
+    for q in qs:
+        _check(best, h, q, p, s)
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 3, 7])
+def test_tensor_grid_capped(best, ctas):
+    """The S_cq steady state at small K: the grid capped to a few CTAs so
+    each runs many tiles (ring slots reused, accumulator 1, bound exchange
+    every 8th tile), including a partial last tile."""
+    from paper_2205_09707_b200 import _native as N
+
+    h = P.generate_index(6000, 4096 + 96, dim=128, nbits=2, mean_len=40, seed=ctas)
+    qs = P.generate_queries(h, 3, seed=2)
+    idx = P.DeviceIndex.from_host(h)
+    old = N.load().plaid_debug_set_tf32_grid(ctas)
+    try:
+        s = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+        for q in qs:
+            S, mx = s.compute_centroid_scores(q)
+            S0, _ = best.compute_centroid_scores(h, q)
+            assert np.abs(S - S0).max() < 5e-6
+            for k in (10, 1000):
+                _check(best, h, q, P.default_params_for_k(k), s)
+            _check(best, h, q, P.SearchParams(20, 32, 0.3, 200), s)
+    finally:
+        N.load().plaid_debug_set_tf32_grid(old)
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    """BASELINE configs[0]: 10k passages, ~64 tokens, dim 128, K = 4096, nbits = 2."""
+    h = P.generate_index(10_000, 4096, dim=128, nbits=2, mean_len=64, seed=0)
+    qs = P.generate_queries(h, 8, seed=1234)
+    return h, qs, P.DeviceIndex.from_host(h, validate=True)
+
+
+def test_cfg1_exact(cfg1, best):
+    h, qs, idx = cfg1
+    s = P.Searcher(idx, score_mode=P.ScoreMode.EXACT)
+    p = P.default_params_for_k(10)
+    for q in qs:
+        got = s.search(q, p)
+        ids, sc, tr = best.search(h, q, p)
+        assert np.array_equal(got.topk.passage_ids, ids)
+        assert np.array_equal(bits(got.topk.scores), bits(sc))
+        assert got.trace.counters() == tr
+
+
+def test_cfg1_tensor(cfg1, best):
+    h, qs, idx = cfg1
+    s = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+    same = 0
+    for q in qs:
+        rep = _check(best, h, q, P.default_params_for_k(10), s)
+        same += rep.ids_equal_reference
+    assert same >= len(qs) - 1  # near-ties are rare: at most one query may reorder
+
+
+def test_tensor_disable_filter_vs_reference(cfg1, best):
+    h, qs, idx = cfg1
+    s = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+    for q in qs[:3]:
+        _check(best, h, q, P.default_params_for_k(100), s, options=P.SearchOptions(disable_filter=True))
+
+
+@pytest.mark.parametrize("lanes", [2, 4])
+def test_batch_tensor_vs_reference(cfg1, best, lanes):
+    """Throughput mode with two queries per S_cq pass (TfCfg<2>) against the
+    reference, query by query."""
+    h, qs, idx = cfg1
+    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.TENSOR)
+    single = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+    qb = np.concatenate([qs, qs[:3]])
+    for k in (10, 100):
+        p = P.default_params_for_k(k)
+        got = b.search(qb, p)
+        for q, g in zip(qb, got):
+            S, _ = single.compute_centroid_scores(q)
+            rep = check_tensor_search(best, h, q, p, g.passage_ids, g.scores, S)
+            assert rep.ok, rep.as_dict()
