@@ -21,6 +21,11 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 PORT_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "liblir_ref.so"
+# the same reference sources at -O3 -march=native of the build host (Sapphire
+# Rapids here): the timed CPU baseline when the running host has every ISA
+# extension that build may use (native_isa_ok), else the portable build
+REF_NATIVE_SO = HERE / "_ref" / "liblir_ref_native.so"
+REF_NATIVE_ISA = HERE / "_ref" / "native_isa.txt"
 
 u8p, u32p, u64p, f32p = (C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
                          C.POINTER(C.c_float))
@@ -73,9 +78,10 @@ class CpuOracle:
 
     def __init__(self, kind: str):
         self.kind = kind
-        path = PORT_SO if kind == "port" else REF_SO
+        path = {"port": PORT_SO, "ref": REF_SO, "ref_native": REF_NATIVE_SO}[kind]
         if not path.exists():
             raise FileNotFoundError(f"{path} not built (make -C oracle)")
+        self.path = path
         self.lib = C.CDLL(str(path))
         self.pre = "orc_" if kind == "port" else "ref_"
         self._ref_handles = {}
@@ -371,4 +377,34 @@ def get(kind: str) -> CpuOracle:
 
 
 def available(kind: str) -> bool:
+    if kind == "ref_native":
+        return REF_NATIVE_SO.exists() and native_isa_ok()
     return (PORT_SO if kind == "port" else REF_SO).exists()
+
+
+def _cpu_flags() -> set:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("flags"):
+                return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def native_isa_ok() -> bool:
+    """True when this host has every SIMD extension of the host that built
+    liblir_ref_native.so (recorded next to it by oracle/Makefile)."""
+    if not REF_NATIVE_ISA.exists():
+        return False
+    need = set(REF_NATIVE_ISA.read_text().split())
+    return need <= _cpu_flags()
+
+
+def timed_reference() -> tuple:
+    """(oracle, flags note) for the timed CPU baseline: the -march=native build
+    when this host can run it, else the portable -march=x86-64-v3 build."""
+    if available("ref_native"):
+        return get("ref_native"), "g++ -O3 -march=native (build host: " + \
+            (HERE / "_ref" / "native_march.txt").read_text().strip() + ") -ffp-contract=off"
+    return get("ref"), "g++ -O3 -march=x86-64-v3 -ffp-contract=off (host lacks the native build's ISA)"

@@ -86,7 +86,7 @@ def build_synth(verbose: bool = False) -> Path:
 def build_oracle(verbose: bool = False) -> None:
     """oracle/liboracle.so always; oracle/_ref/liblir_ref.so when the reference
     sources are present (this container; the GPU box uses the shipped .so)."""
-    targets = ["liboracle.so"]
+    targets = ["liboracle.so", "libsynth_oracle.so"]
     if Path("/root/reference/proj/src").is_dir():
         targets.append("ref")
     _run(["make", "-s", "-C", str(ROOT / "oracle"), *targets], verbose)

@@ -51,3 +51,18 @@ def test_shard_is_slice_of_whole():
         w = w[(w >= a) & (w < b)] - a
         p = part.ivf_postings[part.ivf_offsets[c]:part.ivf_offsets[c + 1]]
         assert np.array_equal(w, p)
+
+
+@pytest.mark.parametrize("nbits,dim,K,pid_base", [(2, 128, 300, 0), (1, 64, 17, 1234), (4, 32, 64, 7)])
+def test_oracle_generator_equals_product(nbits, dim, K, pid_base):
+    """The checker-side restatement of the recipe (oracle/synth_oracle.c, the
+    reference arm's input generator) produces the product generator's bytes."""
+    from oracle import synth
+
+    a = P.generate_index(700, K, dim=dim, nbits=nbits, mean_len=30, seed=5, pid_base=pid_base)
+    ivf = (lambda c, d, k: (a.ivf_offsets, a.ivf_postings)) if not oracle.available("ref") else None
+    b = synth.generate_index(700, K, dim=dim, nbits=nbits, mean_len=30, seed=5, pid_base=pid_base, ivf=ivf)
+    for f in ("centroids", "codes", "residuals", "doclens", "passage_offsets", "ivf_offsets", "ivf_postings",
+              "bucket_cutoffs", "bucket_weights"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert np.array_equal(P.generate_queries(a, 3, seed=8), synth.generate_queries(b, 3, seed=8))
