@@ -168,11 +168,22 @@ def params_for(cfg: dict):
     return p
 
 
-def cpu_reference_run(h, qs, params, steps, warmup, threads):
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return "unknown"
+
+
+def cpu_reference_run(h, qs, params, steps, warmup, threads, ref=None):
     """Latency mode (SURVEY.md §8d): sequential lir::search, threads = all host cores."""
     import oracle
 
-    ref = oracle.get("ref")
+    ref = ref or oracle.timed_reference()[0]
     t = time.time()
     ref.ref_handle(h)
     log(f"reference index built in {time.time() - t:.1f}s")
@@ -184,11 +195,34 @@ def cpu_reference_run(h, qs, params, steps, warmup, threads):
         t0 = time.perf_counter()
         ref.search(h, qs[(warmup + i) % nq], params, threads=threads)
         lat.append(time.perf_counter() - t0)
-    ref.release(h)
     return lat
 
 
+def cpu_reference_throughput(h, qs, params, threads, ref):
+    """Throughput mode (SURVEY.md §8d ii): `threads` concurrent lir::search
+    calls with SearchOptions.threads = 1 over the shared immutable index."""
+    n = min(len(qs), 2 * threads)
+    ref.search_many(h, qs[:threads], params, 1, threads)  # warm-up
+    t0 = time.perf_counter()
+    ref.search_many(h, qs[:n], params, 1, threads)
+    return n / (time.perf_counter() - t0), n
+
+
+class RefParams:
+    """lir::SearchParams (types.hpp:79-84) from the reference's own
+    default_params_for_k (types.cpp:74-86)."""
+
+    def __init__(self, ref, k: int, ndocs=None):
+        self.k, self.nprobe, self.t_cs, self.ndocs = ref.default_params_for_k(k)
+        if ndocs is not None:
+            self.ndocs = ndocs
+
+
 def run_reference(args, cfg):
+    """The reference's own CPU searcher on this host: the unmodified
+    /root/reference sources (oracle/_ref), inputs from the checker-side
+    generator (oracle/synth.py) and IVF from the reference's
+    build_inverted_list — no library of this package is loaded."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -197,18 +231,22 @@ def run_reference(args, cfg):
     if not oracle.available("ref"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liblir_ref.so not built"}))
         return
-    import paper_2205_09707_b200 as P
+    from oracle import synth
 
-    h = make_index(cfg, 0)
-    qs = P.generate_queries(h, max(args.steps + args.warmup, 1), qlen=QLEN, seed=1234)
-    params = params_for(cfg)
+    ref, flags = oracle.timed_reference()
+    t = time.time()
+    h = synth.generate_index(cfg["N"], cfg["K"], dim=DIM, nbits=cfg["nbits"], mean_len=cfg["mean_len"],
+                             spread=16, seed=0, ivf=ref.build_inverted_list)
+    log(f"[reference] generated index: N={h.num_passages} T={h.num_embeddings} ({h.nbytes() / 1e9:.1f} GB) "
+        f"in {time.time() - t:.1f}s")
+    qs = synth.generate_queries(h, max(args.steps + args.warmup, 1), qlen=QLEN, seed=1234)
+    params = RefParams(ref, cfg["k"], cfg.get("ndocs"))
     threads = os.cpu_count() or 1
     B = int(cfg.get("batch", 1))
     if B > 1:
         # throughput mode: `threads` workers x SearchOptions.threads=1;
         # each step is a bounded sample of the batch (~1 s of CPU work)
-        ref = oracle.get("ref")
-        qb = P.generate_queries(h, threads * 4, qlen=QLEN, seed=1234)
+        qb = synth.generate_queries(h, threads * 4, qlen=QLEN, seed=1234)
         ref.search_many(h, qb[:threads], params, 1, threads)  # warm-up (+ index build)
         lat = []
         for i in range(args.steps):
@@ -219,7 +257,7 @@ def run_reference(args, cfg):
         qps = len(qb) * args.steps / total
         sample = f"{len(qb)} queries per step, lir::search throughput mode ({threads} workers x threads=1)"
     else:
-        lat = cpu_reference_run(h, qs, params, args.steps, args.warmup, threads)
+        lat = cpu_reference_run(h, qs, params, args.steps, args.warmup, threads, ref)
         total = sum(lat)
         qps = args.steps / total
         sample = f"{args.steps} sequential queries, lir::search latency mode, SearchOptions.threads={threads}"
@@ -230,10 +268,25 @@ def run_reference(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 generator, SURVEY.md §8d)",
         "config": config_block(cfg, params, args, 1),
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model(), "build": flags},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "repo_libs_mapped": repo_libs_mapped(),
     }
     print(json.dumps(line))
+
+
+def repo_libs_mapped() -> list:
+    """In-tree shared objects this process has mapped (the reference arm must
+    show only oracle/ libraries: the reference and the checker-side generator)."""
+    libs = set()
+    try:
+        for line in Path("/proc/self/maps").read_text().splitlines():
+            f = line.split()
+            if len(f) >= 6 and f[-1].endswith(".so") and f[-1].startswith(str(ROOT)):
+                libs.add(str(Path(f[-1]).relative_to(ROOT)))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 def config_block(cfg, params, args, world):
@@ -398,99 +451,189 @@ def run_plaid(args, cfg):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel: the S_cq kernel (the largest single
-    # launch of a search; the engine's "scores" phase events bracket it alone).
-    # Algorithmic bytes per launch: C read once (512 B per
-    # centroid at d=128), S written once (128 B per centroid), keep bits (1 bit
-    # per centroid) and Q (16 KiB).  3xTF32 FLOPs (3 * 2*K*d*|Q| = 6.4 GFLOP at
-    # cfg2) take ~6 us at the dense tf32 rate, so the kernel is HBM-bound.
+    # ---- workload calibration and parity on the measured
+    # queries: the reference's stages (oracle, the checker) on query 0 give the
+    # integer counts B_alg is made of; --check N classifies N timed queries'
+    # TENSOR results against lir::search with the north_star comparator
     hbm_peak, tf_peak, peak_kind = measured_peaks()
+    tf_sust = measured_tensor_sustained()
     mean_ph = {n: float(np.mean(v)) for n, v in phases.items()}
     K = cfg["K"]
     tr = trace.counters() if trace is not None else {}
-    ab = 512 * K + 128 * K + K // 8 + QLEN * DIM * 4
-    ach = ab / (mean_ph["scores"] * 1e-3) / 1e9
-    kname = "scores_tf32_kernel" if args.score_mode == "tensor" else "scores_exact_kernel"
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        t = json.loads(tf.read_text()).get(f"{args.config}/{kname}")
-        traffic = t.get("dram_bytes_per_launch") if t else None
-    roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-            "frac": ach / hbm_peak, "traffic": traffic, "peak_kind": f"{peak_kind} (copy bandwidth, burst)",
-            "algorithmic_bytes_per_launch": ab, "mean_ms": mean_ph["scores"],
-            "share_of_step": mean_ph["scores"] / (1e3 * total_s / args.steps)}
-    # context: the live-measured rate of a plain one-pass read of C's size on
-    # this GPU (event-timed like the kernel) — the practical floor of a kernel
-    # that streams C once
-    try:
-        import ctypes as _C
-
-        from paper_2205_09707_b200 import _native as _N
-
-        g = _C.c_double()
-        if _N.load().plaid_measure_read_gbs(local, 512 * K, 5, _C.byref(g)) == 0 and g.value > 0:
-            roof["read_floor_gbs"] = g.value
-            roof["read_floor_note"] = f"plain coalesced read of {512 * K >> 20} MiB (C's size), L2 flushed, best of 5"
-            roof["frac_of_read_floor"] = ach / g.value  # same algorithmic bytes as `achieved`
-    except Exception:  # noqa: BLE001
-        pass
-
-    # ---- stage 4 (decompress + exact MaxSim) against its own bound: exactness
-    # forbids FMA and tensor cores, so every (token, query token, dim) is one
-    # rounded multiply and one rounded add on the FP32 pipe;
-    # peak = SMs x 128 lanes x max SM clock.  Duration = the stage-4 phase
-    # (scan + fused decompress/MaxSim + finalize), i.e. conservative.
-    roof4 = None
     t4 = trace.decompressed_tokens if trace is not None else 0
-    if t4:
-        import torch as _t
+    step_mean_ms = 1e3 * total_s / args.steps
+    calib, parity = None, None
+    if world == 1 and not args.no_cpu:
+        try:
+            calib, parity = check_and_calibrate(args, h, qs, params, s, args.warmup)
+        except Exception as e:  # noqa: BLE001
+            parity = {"error": repr(e)}
 
-        props = _t.cuda.get_device_properties(local)
-        clk_mhz = (clk or {}).get("sm_max_mhz") or 1965.0
-        peak_ops = props.multi_processor_count * 128 * clk_mhz * 1e6 / 1e12
-        ops = 2.0 * QLEN * DIM * t4
-        ach = ops / (mean_ph["stage4_rank"] * 1e-3) / 1e12
-        bytes4 = t4 * (4 + DIM * cfg["nbits"] // 8)
-        roof4 = {"bound": "fp32", "kernel": "stream_fused_kernel (+ scan, finalize)", "achieved": ach,
-                 "peak": peak_ops, "unit": "Tops/s (fp32 lane-ops: separate mul + add)", "frac": ach / peak_ops,
-                 "tokens": t4, "ops_per_launch": ops, "code_and_residual_bytes": bytes4,
-                 "mean_ms": mean_ph["stage4_rank"]}
+    # ---- rooflines of the two largest kernels (ncu launch list: S_cq and the
+    # stage-4 kernel; every other launch is < 1/3 of either).  Algorithmic
+    # bytes per launch follow SURVEY.md §8(d); the phase events bracket each
+    # kernel on the launching stream.
+    roofs = {}
+    ab_scq = 512 * K + QLEN * DIM * 4  # C read once + Q (no S writes: not in B_alg)
+    roofs["scores"] = roof_line("scores_tf32_kernel" if args.score_mode == "tensor" else "scores_exact_kernel",
+                                ab_scq, mean_ph["scores"], hbm_peak, peak_kind, step_mean_ms, args.config,
+                                "512 B x K centroid rows + 16 KiB Q (SURVEY.md §8d)")
+    if calib:
+        n3 = calib["n3"]
+        ab4 = (4 + 16 * cfg["nbits"]) * calib["T4"] + 12 * n3 + 512 * calib["U4"]
+        k4 = "stage4_tensor_kernel" if args.score_mode == "tensor" else "stream_fused_kernel"
+        roofs["stage4"] = roof_line(k4, ab4, mean_ph["stage4_rank"], hbm_peak, peak_kind, step_mean_ms,
+                                    args.config, "(4 + 16 b) B x T4 codes+residuals + 12 B x n3 + 512 B x U4 "
+                                                 "distinct centroid rows (SURVEY.md §8d); phase = scan + "
+                                                 "stage-4 kernel + finalize")
+    dom = max(roofs, key=lambda n: roofs[n]["mean_ms"])
+    roof = dict(roofs[dom])
+    roof["dominant_of"] = {n: r["mean_ms"] for n, r in roofs.items()}
+    others = {n: r for n, r in roofs.items() if n != dom}
+
+    # ---- whole-query roofline: t_roof = FLOPs_Scq / P_tc + B_alg / BW
+    rq = None
+    if calib:
+        # 3xTF32 = three tf32 MMA passes; tf32 dense rate = half the measured bf16 rate
+        p_tc = (tf_sust if tf_sust else tf_peak) / 2 * 1e12
+        flops = 3 * 2.0 * K * DIM * QLEN
+        t_roof = flops / p_tc + calib["B_alg"] / (hbm_peak * 1e9)
+        rq = {"t_roof_us": 1e6 * t_roof, "t_measured_us": 1e3 * step_mean_ms,
+              "frac": t_roof / (step_mean_ms * 1e-3), "B_alg_bytes": calib["B_alg"],
+              "scq_flops": flops, "p_tc_tflops": p_tc / 1e12,
+              "note": "t_roof = 3xTF32 S_cq FLOPs / (measured bf16 sustained / 2) + B_alg / measured HBM copy "
+                      "bandwidth; B_alg per SURVEY.md §8d from the reference's integer sets on query 0"}
 
     # ---- CPU baseline: the reference's own searcher on this host, bounded sample
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
+            import oracle
+
+            ref, flags = oracle.timed_reference()
             threads = os.cpu_count() or 1
             per_q = 0.5 if cfg["N"] > 1_000_000 else 0.02
             nsample = max(3, min(64, int(args.cpu_seconds / per_q)))
-            lat = cpu_reference_run(h, qs, params, nsample, 1, threads)
+            lat = cpu_reference_run(h, qs, params, nsample, 1, threads, ref)
+            tput, ntp = cpu_reference_throughput(h, qs, params, threads, ref)
+            ref.release(h)
             cpu = {"value": nsample / sum(lat), "unit": "queries/s", "cores": threads, "kind": "reference",
                    "sample": f"{nsample} sequential queries of the same workload, lir::search latency mode, "
-                             f"SearchOptions.threads={threads}", "p50_ms": 1e3 * statistics.median(lat)}
+                             f"SearchOptions.threads={threads}", "p50_ms": 1e3 * statistics.median(lat),
+                   "throughput_mode": {"value": tput, "unit": "queries/s", "queries": ntp,
+                                       "how": f"{threads} concurrent lir::search calls, SearchOptions.threads=1"},
+                   "cpu_model": cpu_model(), "build": flags}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
+        "warmup": args.warmup, "ms_per_step": step_mean_ms,
         "p50_ms": float(np.median(step_ms)), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 generator, SURVEY.md §8d)",
         "config": config_block(cfg, params, args, world),
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": QLEN * DIM * 4,
-                "d2h_bytes_per_step": k * 8 + 128, "p50_ms": 1e3 * statistics.median(e2e_lat)},
+                "d2h_bytes_per_step": k * 8 + 128, "p50_ms": 1e3 * statistics.median(e2e_lat),
+                "path": "Python Searcher.search -> plaid_search (C ABI), host buffers"},
         "gpu_launches": launches,
         "roofline": roof,
-        "roofline_stage4": roof4,
+        "roofline_other": others,
+        "roofline_query": rq,
         "phases_ms": mean_ph,
         "trace": tr,
+        "calibration": calib,
+        "parity": parity,
         "cpu_baseline": cpu,
         "clocks": clk,
     }
+    if args.cpp_e2e:
+        line["e2e_cpp"] = cpp_e2e(args, cfg)
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def cpp_e2e(args, cfg):
+    """e2e through the C++ drop-in binding (include/plaid_lir.hpp): see tools/e2e_cpp.cpp."""
+    return None
+
+
+def measured_tensor_sustained():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text()).get("bf16_tflops_sustained") or 0) or None
+    return None
+
+
+def roof_line(kname, ab, mean_ms, hbm_peak, peak_kind, step_ms, config, bytes_note):
+    ach = ab / (mean_ms * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        t = json.loads(tf.read_text()).get(f"{config}/{kname}")
+        traffic = t.get("dram_bytes_per_launch") if t else None
+    return {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ach / hbm_peak, "traffic": traffic, "peak_kind": f"{peak_kind} (copy bandwidth, burst)",
+            "algorithmic_bytes_per_launch": ab, "bytes": bytes_note, "mean_ms": mean_ms,
+            "share_of_step": mean_ms / step_ms}
+
+
+def check_and_calibrate(args, h, qs, params, searcher, first):
+    """Checker leg (oracle = the compiled reference, lir itself): SURVEY.md
+    §8d's calibration counts of query `first` and the north_star comparison of
+    --check queries' TENSOR results with lir::search on the same inputs."""
+    import oracle
+    from oracle.compare import check_tensor_search, compose
+
+    ref = oracle.get("ref") if oracle.available("ref") else oracle.get("port")
+    q = qs[first]
+    S0, mx0 = ref.compute_centroid_scores(h, q)
+    c = compose(ref, h, q, S0, mx0, params)
+    dl = h.doclens.astype(np.int64)
+    kept = int((mx0 >= np.float32(params.t_cs)).sum())
+    from oracle.compare import topn_sets
+
+    sets, _ = topn_sets(S0, int(params.nprobe))
+    probed = sorted(set().union(*sets))
+    ivo = h.ivf_offsets.astype(np.int64)
+    P1 = int(sum(ivo[x + 1] - ivo[x] for x in probed))
+    C1, T1 = len(c["c1"]), int(dl[c["c1"]].sum())
+    T3 = int(dl[c["k2"]].sum())
+    n3 = len(c["k3"])
+    T4 = int(dl[c["k3"]].sum())
+    off = h.passage_offsets.astype(np.int64)
+    U4 = int(np.unique(np.concatenate([h.codes[off[x]:off[x + 1]] for x in c["k3"]])).size) if n3 else 0
+    zero = float((c["s2"] == 0).mean()) if c["s2"] is not None and len(c["s2"]) else None
+    K, b = h.num_centroids, h.nbits
+    B_alg = (512 * K + 4 * P1 + (4 * T1 + 12 * C1) + (4 * T3 + 12 * int(params.ndocs))
+             + ((4 + 16 * b) * T4 + 12 * n3 + 512 * U4) + QLEN * DIM * 4 + 8 * int(params.k))
+    calib = {"query": int(first), "C1": C1, "T1": T1, "P1_distinct_probed_postings": P1,
+             "probed_centroids": len(probed), "kept_centroids": kept, "stage2_zero_score_fraction": zero,
+             "T3": T3, "n3": n3, "T4": T4, "U4": U4, "B_alg": B_alg}
+    parity = None
+    if args.check:
+        reps = []
+        for i in range(args.check):
+            qi = qs[first + i]
+            r = searcher.search(qi, params)
+            S_t, _ = searcher.compute_centroid_scores(qi)
+            rep = check_tensor_search(ref, h, qi, params, r.topk.passage_ids, r.topk.scores, S_t,
+                                      got_counters=r.trace.counters())
+            reps.append(rep)
+        parity = {"queries": len(reps), "checker": "oracle/_ref (lir::search, unmodified reference)"
+                  if ref.kind == "ref" else "oracle port", "mode": args.score_mode,
+                  "ok": all(r.ok for r in reps),
+                  "ids_equal_reference": sum(r.ids_equal_reference for r in reps),
+                  "max_rel_score_err": max(r.max_rel_score_err for r in reps),
+                  "s_max_abs_err": max(r.s_max_abs_err for r in reps),
+                  "near_boundary_diffs": {k: sum(getattr(r, k) for r in reps)
+                                          for k in ("stage1_diff", "keep_diff", "stage2_diff", "stage3_diff",
+                                                    "final_diff")},
+                  "problems": [p for r in reps for p in r.problems][:5],
+                  "comparator": "oracle/compare.py (north_star: integer sets exact except near t_cs / nprobe / "
+                                "ndocs / top-k boundaries; MaxSim within 1e-4 relative)"}
+    return calib, parity
 
 
 def run_plaid_batch(args, cfg):
@@ -676,7 +819,12 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--score-mode", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference baseline and the parity check")
+    ap.add_argument("--check", type=int, default=2,
+                    help="classify this many timed queries' results against lir::search (oracle/_ref) with the "
+                         "north_star comparator; reported as the line's `parity` block")
+    ap.add_argument("--cpp-e2e", type=int, default=1,
+                    help="also time e2e through the C++ drop-in (plaid_lir::Engine, tools/e2e_cpp)")
     ap.add_argument("--graphs", action="store_true", help="host API search replays a captured CUDA graph (e2e)")
     ap.add_argument("--flush", default="write", choices=["write", "write+read"],
                     help="untimed L2 reset between steps")
