@@ -221,7 +221,7 @@ T* DeviceIndex::upload(const T* src, uint64_t count) {
     PLAID_CUDA(cudaMalloc(&p, bytes));
     allocs_.push_back(p);
     bytes_ += bytes;
-    if (count) PLAID_CUDA(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    if (count && src) PLAID_CUDA(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice));
     return static_cast<T*>(p);
 }
 
@@ -306,6 +306,14 @@ DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_bas
         view_.ivf_postings = upload(d.ivf_postings, view_.P);
         const std::vector<uint8_t> mult = posting_multiplicity(d, offsets);
         view_.ivf_mult = upload(mult.data(), mult.size());
+        if (d.dim == 128 && d.num_embeddings) {
+            // per-token 1/||v|| for the tensor-core stage 4 (TENSOR mode)
+            float* inv = upload<float>(nullptr, d.num_embeddings);
+            launch::token_inv_norms(view_, inv, 0);
+            PLAID_CUDA(cudaStreamSynchronize(0));
+            PLAID_CUDA(cudaGetLastError());
+            view_.tok_inv = inv;
+        }
     } catch (...) {
         for (void* p : allocs_) cudaFree(p);
         allocs_.clear();
@@ -443,6 +451,7 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
         fin_base_.ensure(n3);
         rank_scratch_.pref = pref_.p;
         rank_scratch_.run = run_.p;
+        rank_scratch_.tensor_S = tensor_ ? scores_.p : nullptr;
         rank_scratch_.fin_base = fin_base_.p;
         rank_scratch_.tokens = counters_.p + kT4;
         rank_scratch_.pass_cap =

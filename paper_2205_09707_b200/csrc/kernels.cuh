@@ -26,6 +26,7 @@ struct IndexView {
     const uint64_t* ivf_offsets = nullptr;
     const uint32_t* ivf_postings = nullptr;
     const uint8_t* ivf_mult = nullptr;  // P: tokens of the passage with the posting's code (<= 255, saturating)
+    const float* tok_inv = nullptr;     // T: 1 / ||C[code] + residual|| per token (d = 128; TENSOR stage 4)
     float weights[16] = {};
 };
 
@@ -255,7 +256,11 @@ struct RankScratch {
     uint64_t* tokens = nullptr;   // 1 counter: stage-4 stream length (trace)
     uint64_t pass_cap = 0;
     bool prescanned = false;      // pref / fin_base / tokens already written (select_set)
+    const float* tensor_S = nullptr;  // TENSOR mode: this query's S_cq table -> stage4_tensor_kernel
 };
+// inv_t = 1 / ||C[code_t] + r_t|| for every index token (d = 128), the
+// reference's arithmetic (residual_codec.cpp:113-130); index-load time.
+void token_inv_norms(const IndexView& ix, float* d_out, cudaStream_t st);
 constexpr uint64_t kStreamMaxPassages = 16384;
 void rank_exact(const IndexView& ix, const float* d_q, uint32_t rows, const uint32_t* d_ids,
                 const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,

@@ -27,8 +27,10 @@
 // centroid row (rows shared by tokens hit L2); the decompressed rows never
 // leave shared memory.  The bound is the exact fp32 issue rate (FMA and
 // tensor cores would change the rounding), see DESIGN.md §3.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -363,6 +365,327 @@ __global__ void finalize_kernel(const uint32_t* __restrict__ ids, const uint64_t
     }
 }
 
+// ---- K2': stage 4 on the tensor cores (PLAID_SCORES_TENSOR) ----------------------------
+// q_i . v_hat_t with v_t = C[c_t] + r_t (residual_codec.cpp:97-132) is
+//   (q_i . C[c_t] + q_i . r_t) * inv_t = (S[c_t][i] + (R Q^T)[t][i]) * inv_t,
+// where S is this query's S_cq table (3xTF32, |err| < 5e-6, already in L2 after
+// stage 1), inv_t = 1 / ||v_t|| is computed per token at index load
+// (token_inv_kernel: the reference's in-order fp64 norm), and only R Q^T —
+// the residual part, rows of 2^b distinct weights — is a GEMM: 128 finalist
+// tokens x 32 query tokens per tile on tcgen05 (kind::f16, split bf16:
+// R = R_hi + R_lo and Q = Q_hi + Q_lo, three products kept, ~2^-16 relative).
+// A token then costs 4 B code + 16 b B residuals + 4 B inv_t from HBM and one
+// 128-B S row from L2: the 512-B centroid row of the exact path is never read.
+//   warps 0-3  token group: thread = token = TMEM lane (warp w owns lanes
+//              32w..32w+31).  Producer: finalist lookup, loads, residual
+//              decode into bf16 hi/lo pairs (LUT), tcgen05.st of the A
+//              operand [R_hi | R_lo] (K = 256), cp.async of the S row; then
+//              epilogue: tcgen05.ld of D, a 32x32 transpose through shared
+//              memory, lane = query token: (S + D) * inv, segmented max per
+//              finalist and one 128-byte row of atomicMax per segment.
+//   warp 4     TMEM allocation and the MMA issuer: 16 x (M=128, N=64, K=16)
+//              with B = [[Q_hi; Q_hi] | [Q_lo; 0]] (SWIZZLE_128B K-major, 32 KB)
+//              -> D[:, i] + D[:, 32 + i] = R_hi.Q_hi + R_lo.Q_hi + R_hi.Q_lo.
+// Two CTAs per SM (256 TMEM columns each: A 128 + D 64), tiles round-robin.
+constexpr uint32_t kTcTile = 128;
+constexpr uint32_t kTcThreads = 160;
+constexpr uint32_t kTcTmemCols = 256;
+constexpr uint32_t kTcAccCol = 128;
+constexpr uint32_t kTcOffB = 0;                                  // 4 chunks x 64 rows x 128 B
+constexpr uint32_t kTcOffS = kTcOffB + 4 * 64 * 128;             // 128 tokens x 32 floats
+constexpr uint32_t kTcOffTr = kTcOffS + kTcTile * 32 * 4;        // 4 warps x 32 x 33 floats
+constexpr uint32_t kTcOffMeta = kTcOffTr + 4 * 32 * 33 * 4;      // pass[128], inv[128]
+constexpr uint32_t kTcOffLut = kTcOffMeta + 2 * kTcTile * 4;     // hi[256], lo[256] u32
+constexpr uint32_t kTcOffBar = kTcOffLut + 2 * 256 * 4;          // a_full, acc_full, tmem slot
+// padded so at most two CTAs share an SM (two 256-column TMEM allocations)
+constexpr uint32_t kTcSmemBytes = 100 * 1024;
+static_assert(kTcOffBar + 64 + 1024 <= kTcSmemBytes, "stage-4 tensor smem");
+
+// kind::f16 instruction descriptor: D f32, A and B bf16, both K-major, M = 128, N = 64.
+constexpr uint32_t kTcIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ uint64_t tc_desc(uint32_t addr) {
+    uint64_t d = uint64_t((addr >> 4) & 0x3FFFu);
+    d |= uint64_t(1) << 16;
+    d |= uint64_t(1024 >> 4) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+
+__device__ __forceinline__ void tc_mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void tc_mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ uint16_t bf16_rn_bits(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float bf16_val(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
+
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kTcThreads, 2)
+stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_inv, const uint32_t* __restrict__ codes,
+                     const uint8_t* __restrict__ residuals, Weights16 W, const uint64_t* __restrict__ d_n,
+                     const uint32_t* __restrict__ pref, const uint64_t* __restrict__ fin_base,
+                     const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
+    dev::pdl_wait();
+    extern __shared__ __align__(16) uint8_t tc_smem_raw[];
+    uint8_t* smem = tc_smem_raw + ((1024u - (smem_addr(tc_smem_raw) & 1023u)) & 1023u);
+    const uint32_t base = smem_addr(smem);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t a_full = base + kTcOffBar, acc_full = base + kTcOffBar + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTcOffBar + 16);
+    float* srow = reinterpret_cast<float*>(smem + kTcOffS);
+    float* trb = reinterpret_cast<float*>(smem + kTcOffTr);
+    uint32_t* pass_s = reinterpret_cast<uint32_t*>(smem + kTcOffMeta);
+    float* inv_s = reinterpret_cast<float*>(smem + kTcOffMeta + kTcTile * 4);
+    uint32_t* lut_hi = reinterpret_cast<uint32_t*>(smem + kTcOffLut);
+    uint32_t* lut_lo = lut_hi + 256;
+
+    const uint32_t n = uint32_t(*d_n);
+    const uint32_t T = pref[n];
+    const uint32_t ntiles = (T + kTcTile - 1) / kTcTile;
+    if (blockIdx.x >= ntiles) return;
+
+    // LUT: a residual bit group of two dims (2 NB bits, LSB first) -> the
+    // packed bf16 pair (low half = the even dim) of w_hi and of w_lo
+    constexpr uint32_t kPairBits = 2 * NB, kPairs = 1u << kPairBits, kMask = (1u << NB) - 1;
+    for (uint32_t e = threadIdx.x; e < kPairs; e += kTcThreads) {
+        const float wa = W.w[e & kMask], wb = W.w[(e >> NB) & kMask];
+        const uint16_t ha = bf16_rn_bits(wa), hb = bf16_rn_bits(wb);
+        const uint16_t la = bf16_rn_bits(wa - bf16_val(ha)), lb = bf16_rn_bits(wb - bf16_val(hb));
+        lut_hi[e] = uint32_t(ha) | (uint32_t(hb) << 16);
+        lut_lo[e] = uint32_t(la) | (uint32_t(lb) << 16);
+    }
+    // B operand: row n < 32 = [Q_hi | Q_hi] of query token n, row 32 + i =
+    // [Q_lo | 0] of token i (zero rows past `rows`); 16-byte granule j of
+    // chunk kc (64 bf16 of K) at kc * 8192 + n * 128 + ((j ^ (n & 7)) << 4)
+    for (uint32_t e = threadIdx.x; e < 64 * 32; e += kTcThreads) {
+        const uint32_t nrow = e >> 5, g = e & 31;   // g = granule over K = 256 (8 bf16 each)
+        const uint32_t i = nrow & 31, kc = g >> 3, j = g & 7;
+        const uint32_t d0 = (g * 8) & 127;          // query dim of the granule's first element
+        uint32_t v[4] = {0, 0, 0, 0};
+        const bool lo_row = nrow >= 32;
+        if (i < rows && !(lo_row && g >= 16)) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(Q + i * 128 + d0));
+            const float4 y = __ldg(reinterpret_cast<const float4*>(Q + i * 128 + d0 + 4));
+            const float f[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint16_t h0 = bf16_rn_bits(f[2 * u]), h1 = bf16_rn_bits(f[2 * u + 1]);
+                if (lo_row) {
+                    h0 = bf16_rn_bits(f[2 * u] - bf16_val(h0));
+                    h1 = bf16_rn_bits(f[2 * u + 1] - bf16_val(h1));
+                }
+                v[u] = uint32_t(h0) | (uint32_t(h1) << 16);
+            }
+        }
+        *reinterpret_cast<uint4*>(smem + kTcOffB + kc * 8192 + nrow * 128 + ((j ^ (nrow & 7)) << 4)) =
+            make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    if (threadIdx.x == 0) {
+        tc_mbar_init(a_full, 4);
+        tc_mbar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                     "r"(kTcTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // ---------------- MMA issuer
+        uint32_t lt = 0;
+        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++lt) {
+            tc_mbar_wait(a_full, lt & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lane == 0) {
+#pragma unroll
+                for (uint32_t s = 0; s < 16; ++s) {
+                    const uint64_t bd = tc_desc(base + kTcOffB + (s >> 2) * 8192 + (s & 3) * 32);
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "setp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + kTcAccCol),
+                        "r"(tmem + 8 * s), "l"(bd), "r"(kTcIdesc), "r"(s));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 acc_full)
+                             : "memory");
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- token group: produce a tile, then its epilogue
+        constexpr uint32_t kBpt = NB * 128 / 8;          // residual bytes per token
+        const uint32_t lane_off = (warp * 32) << 16;
+        const uint32_t tslot = warp * 32 + lane;          // token slot in the tile
+        float* tr = trb + warp * 32 * 33;
+        uint32_t lt = 0;
+        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++lt) {
+            const uint32_t g0 = tl * kTcTile + warp * 32, g = g0 + lane;
+            const bool valid = g < T;
+            uint32_t p = 0xFFFFFFFFu;
+            if (g0 < T) p = run_finalists(pref, n, g0, g);
+            uint32_t hi[64], lo[64];
+            if (valid) {
+                const uint64_t tok = fin_base[p] + g;
+                const uint32_t code = __ldg(codes + tok);
+                inv_s[tslot] = __ldg(tok_inv + tok);
+                const float* srcS = S + uint64_t(code) * kScoresPitch;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) cp_async16(srow + tslot * 32 + 4 * c, srcS + 4 * c);
+                uint32_t rb[kBpt / 4];
+                const uint4* src = reinterpret_cast<const uint4*>(residuals + tok * kBpt);
+#pragma unroll
+                for (uint32_t i = 0; i < kBpt / 16; ++i) {
+                    const uint4 x = __ldg(src + i);
+                    rb[4 * i] = x.x, rb[4 * i + 1] = x.y, rb[4 * i + 2] = x.z, rb[4 * i + 3] = x.w;
+                }
+#pragma unroll
+                for (uint32_t c = 0; c < 64; ++c) {
+                    const uint32_t bit = c * kPairBits;
+                    const uint32_t e = (rb[bit / 32] >> (bit % 32)) & (kPairs - 1);
+                    hi[c] = lut_hi[e];
+                    lo[c] = lut_lo[e];
+                }
+            } else {
+#pragma unroll
+                for (uint32_t c = 0; c < 64; ++c) hi[c] = 0u, lo[c] = 0u;
+            }
+            pass_s[tslot] = valid ? p : 0xFFFFFFFFu;
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            {
+                uint32_t (&h0)[32] = *reinterpret_cast<uint32_t(*)[32]>(hi);
+                uint32_t (&h1)[32] = *reinterpret_cast<uint32_t(*)[32]>(hi + 32);
+                uint32_t (&l0)[32] = *reinterpret_cast<uint32_t(*)[32]>(lo);
+                uint32_t (&l1)[32] = *reinterpret_cast<uint32_t(*)[32]>(lo + 32);
+                tc_st32(tmem + lane_off + 0, h0);
+                tc_st32(tmem + lane_off + 32, h1);
+                tc_st32(tmem + lane_off + 64, l0);
+                tc_st32(tmem + lane_off + 96, l1);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tc_mbar_arrive(a_full);
+
+            // ---- epilogue
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            tc_mbar_wait(acc_full, lt & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t x[32], y[32];
+            tc_ld32(tmem + lane_off + kTcAccCol, x);
+            tc_ld32(tmem + lane_off + kTcAccCol + 32, y);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = __uint_as_float(x[i]) + __uint_as_float(y[i]);
+            __syncwarp();
+            // lane = query token i: (S + D) * inv over the warp's 32 tokens in
+            // stream order, segmented max per finalist
+            const uint32_t i = lane;
+            const bool live = i < rows;
+            uint32_t cur = 0xFFFFFFFFu;
+            float m = 0.0f;
+            for (uint32_t t = 0; t < 32; ++t) {
+                const uint32_t pt = pass_s[warp * 32 + t];
+                if (pt == 0xFFFFFFFFu) break;  // past the stream end (tail of the last tile)
+                const float v = __fmul_rn(__fadd_rn(srow[(warp * 32 + t) * 32 + i], tr[t * 33 + i]),
+                                          inv_s[warp * 32 + t]);
+                if (pt != cur) {
+                    if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
+                    cur = pt;
+                    m = v;
+                } else {
+                    m = dev::max_gt(m, v);
+                }
+            }
+            if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 4)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcTmemCols));
+}
+
+// inv_t = 1 / ||C[c_t] + w[idx_t]|| per index token, with the reference's
+// arithmetic (residual_codec.cpp:113-130: fp32 adds, in-order fp64 norm,
+// float(1 / sqrt)); 1 for a zero vector (the reference leaves it unscaled).
+// Index-load time, one thread per token.
+template <int NB>
+__global__ void token_inv_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
+                                 const uint8_t* __restrict__ residuals, Weights16 W, uint64_t T,
+                                 float* __restrict__ out) {
+    constexpr uint32_t kBpt = NB * 128 / 8, kMask = (1u << NB) - 1;
+    __shared__ float w_s[16];
+    if (threadIdx.x < 16) w_s[threadIdx.x] = W.w[threadIdx.x];
+    __syncthreads();
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < T; t += uint64_t(gridDim.x) * blockDim.x) {
+        const float4* c4 = reinterpret_cast<const float4*>(C + uint64_t(__ldg(codes + t)) * 128);
+        uint32_t rb[kBpt / 4];
+        const uint4* src = reinterpret_cast<const uint4*>(residuals + t * kBpt);
+#pragma unroll
+        for (uint32_t i = 0; i < kBpt / 16; ++i) {
+            const uint4 x = __ldg(src + i);
+            rb[4 * i] = x.x, rb[4 * i + 1] = x.y, rb[4 * i + 2] = x.z, rb[4 * i + 3] = x.w;
+        }
+        double acc = 0.0;
+#pragma unroll 8
+        for (uint32_t d4 = 0; d4 < 32; ++d4) {
+            const float4 c = __ldg(c4 + d4);
+            const float cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                const uint32_t d = 4 * d4 + u, bit = d * NB;
+                const float v = __fadd_rn(cc[u], w_s[(rb[bit / 32] >> (bit % 32)) & kMask]);
+                acc = __fma_rn(double(v), double(v), acc);  // exact square + one rounding = the in-order add
+            }
+        }
+        out[t] = acc > 0.0 ? float(1.0 / sqrt(acc)) : 1.0f;
+    }
+}
+
 int sm_count() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -401,18 +724,45 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
     }
     uint64_t fb = (nmax * ix.max_doclen + kTile - 1) / kTile;
     if (fb > uint64_t(sm_count()) * 2) fb = uint64_t(sm_count()) * 2;  // two CTAs (12 warps) per SM
-    auto fk = ix.nbits == 1 ? stream_fused_kernel<1> : ix.nbits == 2 ? stream_fused_kernel<2> : stream_fused_kernel<4>;
-    static const uint32_t dbg = [] {
-        const char* e = getenv("PLAID_RANK_DBG");
-        return e ? uint32_t(atoi(e)) : 0u;
-    }();
-    ::plaid::launch::pdl(fk, uint32_t(fb), kFusedThreads, fsm, st, ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref,
-                         s.fin_base, d_q, rows, s.run, dbg);
-    count_launch();
+    if (s.tensor_S && ix.tok_inv) {
+        // TENSOR mode: residual products on tcgen05, S rows reused (stage4_tensor_kernel)
+        static launch::PerDeviceOnce tcfg;
+        if (tcfg.first()) {
+            cudaFuncSetAttribute(stage4_tensor_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemBytes));
+            cudaFuncSetAttribute(stage4_tensor_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemBytes));
+            cudaFuncSetAttribute(stage4_tensor_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemBytes));
+        }
+        uint64_t tb = (nmax * ix.max_doclen + kTcTile - 1) / kTcTile;
+        if (tb > uint64_t(sm_count()) * 2) tb = uint64_t(sm_count()) * 2;  // two CTAs (2 x 256 TMEM columns) per SM
+        if (tb == 0) tb = 1;
+        auto tk = ix.nbits == 1 ? stage4_tensor_kernel<1> : ix.nbits == 2 ? stage4_tensor_kernel<2> : stage4_tensor_kernel<4>;
+        ::plaid::launch::pdl(tk, uint32_t(tb), kTcThreads, kTcSmemBytes, st, s.tensor_S, ix.tok_inv, ix.codes,
+                             ix.residuals, W, d_n, s.pref, s.fin_base, d_q, rows, s.run);
+        count_launch();
+    } else {
+        auto fk = ix.nbits == 1 ? stream_fused_kernel<1> : ix.nbits == 2 ? stream_fused_kernel<2> : stream_fused_kernel<4>;
+        static const uint32_t dbg = [] {
+            const char* e = getenv("PLAID_RANK_DBG");
+            return e ? uint32_t(atoi(e)) : 0u;
+        }();
+        ::plaid::launch::pdl(fk, uint32_t(fb), kFusedThreads, fsm, st, ix.centroids, ix.codes, ix.residuals, W, d_n, s.pref,
+                             s.fin_base, d_q, rows, s.run, dbg);
+        count_launch();
+    }
     const uint32_t nb = uint32_t((nmax + 255) / 256);
     ::plaid::launch::pdl(finalize_kernel, nb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
     count_launch();
     return true;
+}
+
+void token_inv_norms(const IndexView& ix, float* d_out, cudaStream_t st) {
+    if (ix.dim != 128 || ix.T == 0) return;
+    Weights16 W;
+    for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
+    const uint64_t blocks = std::min<uint64_t>((ix.T + 255) / 256, uint64_t(sm_count()) * 16);
+    auto k = ix.nbits == 1 ? token_inv_kernel<1> : ix.nbits == 2 ? token_inv_kernel<2> : token_inv_kernel<4>;
+    k<<<uint32_t(blocks), 256, 0, st>>>(ix.centroids, ix.codes, ix.residuals, W, ix.T, d_out);
+    count_launch();
 }
 
 }  // namespace launch
