@@ -655,14 +655,19 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
 // Index-load time, one thread per token.
 template <int NB>
 __global__ void token_inv_kernel(const float* __restrict__ C, const uint32_t* __restrict__ codes,
-                                 const uint8_t* __restrict__ residuals, Weights16 W, uint64_t T,
+                                 const uint8_t* __restrict__ residuals, Weights16 W, uint64_t T, uint64_t K,
                                  float* __restrict__ out) {
     constexpr uint32_t kBpt = NB * 128 / 8, kMask = (1u << NB) - 1;
     __shared__ float w_s[16];
     if (threadIdx.x < 16) w_s[threadIdx.x] = W.w[threadIdx.x];
     __syncthreads();
     for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < T; t += uint64_t(gridDim.x) * blockDim.x) {
-        const float4* c4 = reinterpret_cast<const float4*>(C + uint64_t(__ldg(codes + t)) * 128);
+        const uint32_t code = __ldg(codes + t);
+        if (code >= K) {  // not yet validated (an on-disk index is checksummed after upload)
+            out[t] = 0.0f;
+            continue;
+        }
+        const float4* c4 = reinterpret_cast<const float4*>(C + uint64_t(code) * 128);
         uint32_t rb[kBpt / 4];
         const uint4* src = reinterpret_cast<const uint4*>(residuals + t * kBpt);
 #pragma unroll
@@ -761,7 +766,7 @@ void token_inv_norms(const IndexView& ix, float* d_out, cudaStream_t st) {
     for (int i = 0; i < 16; ++i) W.w[i] = ix.weights[i];
     const uint64_t blocks = std::min<uint64_t>((ix.T + 255) / 256, uint64_t(sm_count()) * 16);
     auto k = ix.nbits == 1 ? token_inv_kernel<1> : ix.nbits == 2 ? token_inv_kernel<2> : token_inv_kernel<4>;
-    k<<<uint32_t(blocks), 256, 0, st>>>(ix.centroids, ix.codes, ix.residuals, W, ix.T, d_out);
+    k<<<uint32_t(blocks), 256, 0, st>>>(ix.centroids, ix.codes, ix.residuals, W, ix.T, ix.K, d_out);
     count_launch();
 }
 
