@@ -402,6 +402,7 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         PLAID_CUDA(cudaMemcpy(kconst_.p, &K, sizeof K, cudaMemcpyHostToDevice));
         tensor_ = cfg_.score_mode == PLAID_SCORES_TENSOR && launch::tensor_scores_supported(ix);
         if (tensor_) launch::make_centroid_tensor_map(ix, tmap_);
+        if (tensor_ && ix.tok_inv) qimg_.ensure(launch::kQImgBytes / 4);
     }
 }
 
@@ -451,11 +452,16 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
         fin_base_.ensure(n3);
         rank_scratch_.pref = pref_.p;
         rank_scratch_.run = run_.p;
-        rank_scratch_.tensor_S = tensor_ ? scores_.p : nullptr;
+        rank_scratch_.tensor_S = tensor_ && ix.tok_inv ? scores_.p : nullptr;
         rank_scratch_.fin_base = fin_base_.p;
         rank_scratch_.tokens = counters_.p + kT4;
         rank_scratch_.pass_cap =
             std::min<uint64_t>({pref_.n - 1, run_.n / 32, fin_base_.n, launch::kStreamMaxPassages});
+        if (rank_scratch_.tensor_S) {
+            run_p0_.ensure((rank_scratch_.pass_cap * ix.max_doclen + 31) / 32 + 1);
+            rank_scratch_.run_p0 = run_p0_.p;
+            rank_scratch_.qimg = qimg_.p;
+        }
     }
     tmp_keys_.ensure(std::max<uint64_t>(std::min<uint64_t>(p.k, N), std::min<uint64_t>(p.nprobe, K)));
     ensure_result_block(p.k);
@@ -509,7 +515,7 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     // candidate bitmap and the stage-2 used bitmap (contiguous in zero_); the
     // "scores" phase then brackets the S_cq kernel alone
     launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, res_.p,
-                           2 * kNumCounters, st);
+                           2 * kNumCounters, st, d_q, rank_scratch_.qimg ? qimg_.p : nullptr);
     record(0, st, times);
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
@@ -587,7 +593,7 @@ void Searcher::enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times
     scan_fused_ = fuse_scan && nd <= launch::kSmallSortMax && rank_scratch_.pref &&
                   launch::rank_stream128_ok(ix, pending_rows_, fin_max, rank_scratch_);
     launch::FinalistScanArgs fs{ix.doclens, ix.offsets, rank_scratch_.pref, rank_scratch_.fin_base,
-                                rank_scratch_.tokens};
+                                rank_scratch_.tokens, rank_scratch_.run_p0};
     if (nd <= launch::kSmallSortMax)
         launch::select_set(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, c + kN3, scan_fused_ ? &fs : nullptr, st);
     else
@@ -723,7 +729,7 @@ void Searcher::batch_prepare(const float* d_q, uint64_t rows, uint64_t dim, cons
     ensure_param_buffers(p);
     launch::reset_launches();
     launch::query_prologue(d_q, uint32_t(rows), uint32_t(dim), status_.p, zero_.p, zero_.n, res_.p, 2 * kNumCounters,
-                           st);
+                           st, d_q, rank_scratch_.qimg ? qimg_.p : nullptr);
 }
 
 void Searcher::batch_targets(TfOut& out, uint32_t qi, const float* d_q) {

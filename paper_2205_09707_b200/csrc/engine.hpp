@@ -201,6 +201,7 @@ private:
     // scratch
     DevBuf<float> q_, scores_, rowmax_;
     DevBuf<uint32_t> keep_, sel_, chunk_counts_, c1_, ids_tmp_, pref_, run_, slot_of_, kept_list_, acc2_;
+    DevBuf<uint32_t> run_p0_, qimg_;  // TENSOR stage 4: finalist per 32 stream tokens, query B-operand image
     // result block [32 u64 counters | k pids | k scores] (ensure_result_block)
     DevBuf<uint32_t> res_;
     uint64_t res_k_ = 0;

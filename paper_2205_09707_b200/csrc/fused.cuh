@@ -52,12 +52,15 @@ __device__ __forceinline__ void keep_list(uint32_t blk, uint32_t nblk, const uin
 
 // Stage-4 finalist scan (rank128.cu), one CTA of exactly 1024 threads:
 // pref[p] = exclusive prefix of the finalists' doclens, fin_base[p] =
-// offsets[pid] - pref[p], pref[n] = total (also *tokens when given).  The
-// finalist pid is ids[p] or the id of keys[p].
+// offsets[pid] - pref[p], pref[n] = total (also *tokens when given), and
+// (run_p0 given) run_p0[r] = the finalist holding stream position 32 r, so a
+// warp of the tensor-core stage 4 finds the finalists of its 32-token run
+// with one load.  The finalist pid is ids[p] or the id of keys[p].
 __device__ __forceinline__ void finalist_scan(const uint32_t* __restrict__ ids, const uint64_t* keys, uint32_t n,
                                               const uint32_t* __restrict__ doclens,
                                               const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pref,
-                                              uint64_t* __restrict__ fin_base, uint64_t* __restrict__ tokens) {
+                                              uint64_t* __restrict__ fin_base, uint64_t* __restrict__ tokens,
+                                              uint32_t* __restrict__ run_p0 = nullptr) {
     __shared__ uint32_t warp_sums[32];
     auto pid_of = [&](uint32_t p) { return ids ? ids[p] : dev::key_id(keys[p]); };
     const uint32_t per = (n + 1023) / 1024;
@@ -88,7 +91,10 @@ __device__ __forceinline__ void finalist_scan(const uint32_t* __restrict__ ids, 
         const uint32_t pid = pid_of(p);
         pref[p] = run;
         fin_base[p] = offsets[pid] - run;  // index token = fin_base[p] + stream position
-        run += doclens[pid];
+        const uint32_t len = doclens[pid];
+        if (run_p0)
+            for (uint32_t r = (run + 31) / 32; 32 * r < run + len; ++r) run_p0[r] = p;
+        run += len;
     }
     if (threadIdx.x == 1023) {
         pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)

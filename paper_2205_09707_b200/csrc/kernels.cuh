@@ -228,6 +228,7 @@ struct FinalistScanArgs {
     uint32_t* pref = nullptr;
     uint64_t* fin_base = nullptr;
     uint64_t* tokens = nullptr;
+    uint32_t* run_p0 = nullptr;  // finalist of every 32nd stream position (TENSOR stage 4)
 };
 // The top-`want` SET of keys[0..*d_n) (unordered), nmax <= kSmallSortMax, one
 // CTA (shared-memory radix select); *d_out_n = min(n, want).  With `fs`, the
@@ -257,7 +258,12 @@ struct RankScratch {
     uint64_t pass_cap = 0;
     bool prescanned = false;      // pref / fin_base / tokens already written (select_set)
     const float* tensor_S = nullptr;  // TENSOR mode: this query's S_cq table -> stage4_tensor_kernel
+    uint32_t* run_p0 = nullptr;       // TENSOR mode: finalist of every 32nd stream position (scan output)
+    const void* qimg = nullptr;       // TENSOR mode: the query's bf16 B-operand image (query_prologue)
 };
+// Bytes of the stage-4 tensor kernel's B-operand image of a query (built by
+// query_prologue when given a destination).
+constexpr uint32_t kQImgBytes = 24 * 1024;
 // inv_t = 1 / ||C[code_t] + r_t|| for every index token (d = 128), the
 // reference's arithmetic (residual_codec.cpp:113-130); index-load time.
 void token_inv_norms(const IndexView& ix, float* d_out, cudaStream_t st);
@@ -275,8 +281,11 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
 // Device-side query validation (types.cpp:61-72, status 0 or NotNormalized+1)
 // query validation (when d_q != nullptr) + zero nwords u32 at d_zero and nwords2
 // at d_zero2 (multiples of 4 words, 16-byte aligned): one launch.
+// d_qimg (optional, kQImgBytes): also build the stage-4 tensor kernel's
+// B-operand image of the query at d_qsrc (rows x 128).
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
-                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st);
+                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc = nullptr,
+                    void* d_qimg = nullptr);
 // Stage counters: min() bookkeeping done on device.
 void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st);
 // Merge G shard top-k lists into the global top-k.

@@ -97,9 +97,9 @@ __global__ void __launch_bounds__(1024)
 finalist_scan_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
                      const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ doclens,
                      const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pref,
-                     uint64_t* __restrict__ fin_base, uint64_t* __restrict__ tokens) {
+                     uint64_t* __restrict__ fin_base, uint64_t* __restrict__ tokens, uint32_t* __restrict__ run_p0) {
     dev::pdl_wait();
-    fused::finalist_scan(ids, keys, uint32_t(*d_n), doclens, offsets, pref, fin_base, tokens);
+    fused::finalist_scan(ids, keys, uint32_t(*d_n), doclens, offsets, pref, fin_base, tokens, run_p0);
 }
 
 // Warp-cooperative: the finalist of stream token g (this lane's) for a
@@ -368,41 +368,44 @@ __global__ void finalize_kernel(const uint32_t* __restrict__ ids, const uint64_t
 // ---- K2': stage 4 on the tensor cores (PLAID_SCORES_TENSOR) ----------------------------
 // q_i . v_hat_t with v_t = C[c_t] + r_t (residual_codec.cpp:97-132) is
 //   (q_i . C[c_t] + q_i . r_t) * inv_t = (S[c_t][i] + (R Q^T)[t][i]) * inv_t,
-// where S is this query's S_cq table (3xTF32, |err| < 5e-6, already in L2 after
-// stage 1), inv_t = 1 / ||v_t|| is computed per token at index load
+// where S is this query's S_cq table (3xTF32, |err| < 5e-6, already in L2
+// after stage 1), inv_t = 1 / ||v_t|| is computed per token at index load
 // (token_inv_kernel: the reference's in-order fp64 norm), and only R Q^T —
 // the residual part, rows of 2^b distinct weights — is a GEMM: 128 finalist
-// tokens x 32 query tokens per tile on tcgen05 (kind::f16, split bf16:
-// R = R_hi + R_lo and Q = Q_hi + Q_lo, three products kept, ~2^-16 relative).
-// A token then costs 4 B code + 16 b B residuals + 4 B inv_t from HBM and one
+// tokens x 32 query tokens per tile on tcgen05 (kind::f16, split bf16,
+// R = R_hi + R_lo, Q = Q_hi + Q_lo, three products kept: ~2^-16 relative).
+// A token costs 4 B code + 16 b B residuals + 4 B inv_t from HBM and one
 // 128-B S row from L2: the 512-B centroid row of the exact path is never read.
-//   warps 0-3  token group: thread = token = TMEM lane (warp w owns lanes
-//              32w..32w+31).  Producer: finalist lookup, loads, residual
-//              decode into bf16 hi/lo pairs (LUT), tcgen05.st of the A
-//              operand [R_hi | R_lo] (K = 256), cp.async of the S row; then
-//              epilogue: tcgen05.ld of D, a 32x32 transpose through shared
-//              memory, lane = query token: (S + D) * inv, segmented max per
-//              finalist and one 128-byte row of atomicMax per segment.
-//   warp 4     TMEM allocation and the MMA issuer: 16 x (M=128, N=64, K=16)
-//              with B = [[Q_hi; Q_hi] | [Q_lo; 0]] (SWIZZLE_128B K-major, 32 KB)
-//              -> D[:, i] + D[:, 32 + i] = R_hi.Q_hi + R_lo.Q_hi + R_hi.Q_lo.
-// Two CTAs per SM (256 TMEM columns each: A 128 + D 64), tiles round-robin.
+//   warps 0-3  token group, thread = token = TMEM lane (warp w owns lanes
+//              32w..32w+31).  The metadata of the CTA's next two tiles is
+//              prefetched into registers (finalist via run_p0 and one fused
+//              (end, fin_base) load, then code, inv_t and the residual words
+//              in flight together); per tile: cp.async of the S rows of this
+//              and the next tile, residual decode into packed bf16 pairs
+//              (LUT), tcgen05.st of A = [R_hi | R_lo] (K = 256, 128 columns);
+//              then the epilogue: tcgen05.ld of D, a 32x32 transpose through
+//              shared memory, lane = query token: (S + D) * inv, segmented max
+//              per finalist, one 128-byte row of atomicMax per segment.
+//   warp 4     TMEM allocation, the B operand (the query image built by
+//              query_prologue, one 24 KB bulk copy) and the MMA issuer:
+//              16 x (M=128, N=32, K=16) of [R_hi | R_lo] . [Q_hi | Q_hi] and
+//              8 of R_hi . Q_lo into the same 32 accumulator columns.
+// Two CTAs per SM (256 TMEM columns each); tiles round-robin over the grid.
 constexpr uint32_t kTcTile = 128;
 constexpr uint32_t kTcThreads = 160;
 constexpr uint32_t kTcTmemCols = 256;
 constexpr uint32_t kTcAccCol = 128;
-constexpr uint32_t kTcOffB = 0;                                  // 4 chunks x 64 rows x 128 B
-constexpr uint32_t kTcOffS = kTcOffB + 4 * 64 * 128;             // 128 tokens x 32 floats
-constexpr uint32_t kTcOffTr = kTcOffS + kTcTile * 32 * 4;        // 4 warps x 32 x 33 floats
-constexpr uint32_t kTcOffMeta = kTcOffTr + 4 * 32 * 33 * 4;      // pass[128], inv[128]
-constexpr uint32_t kTcOffLut = kTcOffMeta + 2 * kTcTile * 4;     // hi[256], lo[256] u32
-constexpr uint32_t kTcOffBar = kTcOffLut + 2 * 256 * 4;          // a_full, acc_full, tmem slot
-// padded so at most two CTAs share an SM (two 256-column TMEM allocations)
-constexpr uint32_t kTcSmemBytes = 100 * 1024;
-static_assert(kTcOffBar + 64 + 1024 <= kTcSmemBytes, "stage-4 tensor smem");
+constexpr uint32_t kTcOffB = 0;                                   // query image (launch::kQImgBytes)
+constexpr uint32_t kTcOffS = kTcOffB + launch::kQImgBytes;                // 2 x 128 tokens x 32 floats
+constexpr uint32_t kTcOffTr = kTcOffS + 2 * kTcTile * 32 * 4;     // 4 warps x 32 x 33 floats
+constexpr uint32_t kTcOffMeta = kTcOffTr + 4 * 32 * 33 * 4;       // pass[128], inv[128]
+constexpr uint32_t kTcOffLut = kTcOffMeta + 2 * kTcTile * 4;      // hi[256], lo[256] u32
+constexpr uint32_t kTcOffBar = kTcOffLut + 2 * 256 * 4;           // b_full, a_full, acc_full, tmem slot
+constexpr uint32_t kTcSmemBytes = kTcOffBar + 64 + 1024;          // + alignment slack
+static_assert(2 * (kTcSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
 
-// kind::f16 instruction descriptor: D f32, A and B bf16, both K-major, M = 128, N = 64.
-constexpr uint32_t kTcIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+// kind::f16 instruction descriptor: D f32, A and B bf16, both K-major, M = 128, N = 32.
+constexpr uint32_t kTcIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ uint64_t tc_desc(uint32_t addr) {
     uint64_t d = uint64_t((addr >> 4) & 0x3FFFu);
@@ -432,7 +435,7 @@ __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ uint16_t bf16_rn_bits(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
 __device__ __forceinline__ float bf16_val(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
 
-__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* r) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
         "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
@@ -454,19 +457,159 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
 }
 
+// One lane's token of a tile: what the decode and the epilogue need, loaded
+// ahead of use (residual words, code, inv_t in flight).
+template <int NB>
+struct TcToken {
+    uint32_t rb[NB * 128 / 32];
+    uint32_t code;
+    float inv;
+    uint32_t p;  // finalist index, 0xFFFFFFFF past the stream end
+};
+
+// Finalists of the warp's 32-token run [g0, g0 + 32) of tile `tl` (g0 < T):
+// first the run's first finalist lo (run_p0), then lane j loads the end of
+// finalist lo + j and its token base in ONE step; the finalist of lane L is
+// lo + #{j : end_j <= g0 + L} (ends are distinct: each finalist has a token).
+template <int NB>
+__device__ __forceinline__ void tc_prefetch2(TcToken<NB>& a, TcToken<NB>& b, uint32_t tla, uint32_t tlb, uint32_t ntiles,
+                                             uint32_t T, uint32_t n, const uint32_t* __restrict__ pref,
+                                             const uint64_t* __restrict__ fin_base,
+                                             const uint32_t* __restrict__ run_p0, const uint32_t* __restrict__ codes,
+                                             const float* __restrict__ tok_inv, const uint8_t* __restrict__ residuals) {
+    constexpr uint32_t kBpt = NB * 128 / 8;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t g0a = tla * kTcTile + warp * 32, g0b = tlb * kTcTile + warp * 32;
+    const bool ha = tla < ntiles && g0a < T, hb = tlb < ntiles && g0b < T;
+    const uint32_t loa = ha ? __ldg(run_p0 + (g0a >> 5)) : 0u;
+    const uint32_t lob = hb ? __ldg(run_p0 + (g0b >> 5)) : 0u;
+    const bool ia = ha && loa + 1 + lane <= n, ib = hb && lob + 1 + lane <= n;
+    const uint32_t ea = ia ? __ldg(pref + loa + 1 + lane) : 0xFFFFFFFFu;
+    const uint32_t eb = ib ? __ldg(pref + lob + 1 + lane) : 0xFFFFFFFFu;
+    const uint64_t fa = ia ? __ldg(reinterpret_cast<const unsigned long long*>(fin_base) + loa + lane) : 0ull;
+    const uint64_t fb = ib ? __ldg(reinterpret_cast<const unsigned long long*>(fin_base) + lob + lane) : 0ull;
+    auto finish = [&](TcToken<NB>& x, bool has, uint32_t g0, uint32_t lo, uint32_t e, uint64_t f) {
+        const uint32_t rel = e - g0;  // > 0: finalist lo holds g0
+        const uint32_t mask = __reduce_or_sync(0xffffffffu, has && rel < 32 ? 1u << rel : 0u);
+        const uint32_t cnt = __popc(mask & (0xFFFFFFFFu >> (31 - lane)));  // ends at or before g0 + lane
+        const uint64_t base = __shfl_sync(0xffffffffu, f, cnt);
+        const uint32_t g = g0 + lane;
+        if (has && g < T) {
+            x.p = lo + cnt;
+            const uint64_t tok = base + g;
+            x.code = __ldg(codes + tok);
+            x.inv = __ldg(tok_inv + tok);
+            const uint4* src = reinterpret_cast<const uint4*>(residuals + tok * kBpt);
+#pragma unroll
+            for (uint32_t i = 0; i < kBpt / 16; ++i) {
+                const uint4 v = __ldg(src + i);
+                x.rb[4 * i] = v.x, x.rb[4 * i + 1] = v.y, x.rb[4 * i + 2] = v.z, x.rb[4 * i + 3] = v.w;
+            }
+        } else {
+            x.p = 0xFFFFFFFFu;
+            x.code = 0u;
+            x.inv = 0.0f;
+#pragma unroll
+            for (uint32_t i = 0; i < kBpt / 4; ++i) x.rb[i] = 0u;
+        }
+    };
+    finish(a, ha, g0a, loa, ea, fa);
+    finish(b, hb, g0b, lob, eb, fb);
+}
+
+// cp.async of the token's 128-byte S row into slot `slot` (skipped past the end)
+template <int NB>
+__device__ __forceinline__ void tc_fetch_srow(const TcToken<NB>& x, const float* __restrict__ S, float* srow_slot,
+                                              uint32_t tslot) {
+    if (x.p != 0xFFFFFFFFu) {
+        const float* src = S + uint64_t(x.code) * kScoresPitch;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) cp_async16(srow_slot + tslot * 32 + 4 * c, src + 4 * c);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int NB>
+__device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint32_t tmem, uint32_t a_full,
+                                        uint32_t acc_full, const uint32_t* lut_hi, const uint32_t* lut_lo,
+                                        uint32_t* pass_s, float* inv_s, const float* srow_slot, float* tr,
+                                        uint32_t rows, uint32_t* __restrict__ run, bool next_srow_pending) {
+    constexpr uint32_t kPairBits = 2 * NB, kPairs = 1u << kPairBits;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lane_off = (warp * 32) << 16;
+    const uint32_t tslot = warp * 32 + lane;
+    // A operand: columns [0, 64) packed bf16 pairs of R_hi, [64, 128) of R_lo
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (uint32_t c = 0; c < 32; ++c) {
+            const uint32_t bit = (32 * h + c) * kPairBits;
+            const uint32_t e = (x.rb[bit / 32] >> (bit % 32)) & (kPairs - 1);
+            hi[c] = lut_hi[e];
+            lo[c] = lut_lo[e];
+        }
+        tc_st32(tmem + lane_off + 32 * h, hi);
+        tc_st32(tmem + lane_off + 64 + 32 * h, lo);
+    }
+    pass_s[tslot] = x.p;
+    inv_s[tslot] = x.inv;
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) tc_mbar_arrive(a_full);
+
+    // ---- epilogue: S rows of this tile landed, D ready
+    if (next_srow_pending)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    tc_mbar_wait(acc_full, lt & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t d[32];
+    tc_ld32(tmem + lane_off + kTcAccCol, d);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = __uint_as_float(d[i]);
+    __syncwarp();
+    // lane = query token i: (S + D) * inv over the warp's 32 tokens in stream
+    // order, segmented max per finalist, one atomicMax row per segment
+    const uint32_t i = lane;
+    const bool live = i < rows;
+    uint32_t cur = 0xFFFFFFFFu;
+    float m = 0.0f;
+#pragma unroll 4
+    for (uint32_t t = 0; t < 32; ++t) {
+        const uint32_t pt = pass_s[warp * 32 + t];
+        if (pt == 0xFFFFFFFFu) break;  // past the stream end (tail of the last tile)
+        const float v = __fmul_rn(__fadd_rn(srow_slot[(warp * 32 + t) * 32 + i], tr[t * 33 + i]), inv_s[warp * 32 + t]);
+        if (pt != cur) {
+            if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
+            cur = pt;
+            m = v;
+        } else {
+            m = dev::max_gt(m, v);
+        }
+    }
+    if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kTcThreads, 2)
 stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_inv, const uint32_t* __restrict__ codes,
                      const uint8_t* __restrict__ residuals, Weights16 W, const uint64_t* __restrict__ d_n,
                      const uint32_t* __restrict__ pref, const uint64_t* __restrict__ fin_base,
-                     const float* __restrict__ Q, uint32_t rows, uint32_t* __restrict__ run) {
+                     const uint32_t* __restrict__ run_p0, const uint8_t* __restrict__ qimg, uint32_t rows,
+                     uint32_t* __restrict__ run) {
     dev::pdl_wait();
     extern __shared__ __align__(16) uint8_t tc_smem_raw[];
     uint8_t* smem = tc_smem_raw + ((1024u - (smem_addr(tc_smem_raw) & 1023u)) & 1023u);
     const uint32_t base = smem_addr(smem);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t a_full = base + kTcOffBar, acc_full = base + kTcOffBar + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTcOffBar + 16);
+    const uint32_t b_full = base + kTcOffBar, a_full = base + kTcOffBar + 8, acc_full = base + kTcOffBar + 16;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTcOffBar + 24);
     float* srow = reinterpret_cast<float*>(smem + kTcOffS);
     float* trb = reinterpret_cast<float*>(smem + kTcOffTr);
     uint32_t* pass_s = reinterpret_cast<uint32_t*>(smem + kTcOffMeta);
@@ -479,9 +622,9 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
     const uint32_t ntiles = (T + kTcTile - 1) / kTcTile;
     if (blockIdx.x >= ntiles) return;
 
-    // LUT: a residual bit group of two dims (2 NB bits, LSB first) -> the
-    // packed bf16 pair (low half = the even dim) of w_hi and of w_lo
-    constexpr uint32_t kPairBits = 2 * NB, kPairs = 1u << kPairBits, kMask = (1u << NB) - 1;
+    // LUT: a residual bit group of two dims (2 NB bits, LSB first) -> packed
+    // bf16 pairs (low half = the even dim) of w_hi and of w_lo = w - w_hi
+    constexpr uint32_t kPairs = 1u << (2 * NB), kMask = (1u << NB) - 1;
     for (uint32_t e = threadIdx.x; e < kPairs; e += kTcThreads) {
         const float wa = W.w[e & kMask], wb = W.w[(e >> NB) & kMask];
         const uint16_t ha = bf16_rn_bits(wa), hb = bf16_rn_bits(wb);
@@ -489,33 +632,8 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
         lut_hi[e] = uint32_t(ha) | (uint32_t(hb) << 16);
         lut_lo[e] = uint32_t(la) | (uint32_t(lb) << 16);
     }
-    // B operand: row n < 32 = [Q_hi | Q_hi] of query token n, row 32 + i =
-    // [Q_lo | 0] of token i (zero rows past `rows`); 16-byte granule j of
-    // chunk kc (64 bf16 of K) at kc * 8192 + n * 128 + ((j ^ (n & 7)) << 4)
-    for (uint32_t e = threadIdx.x; e < 64 * 32; e += kTcThreads) {
-        const uint32_t nrow = e >> 5, g = e & 31;   // g = granule over K = 256 (8 bf16 each)
-        const uint32_t i = nrow & 31, kc = g >> 3, j = g & 7;
-        const uint32_t d0 = (g * 8) & 127;          // query dim of the granule's first element
-        uint32_t v[4] = {0, 0, 0, 0};
-        const bool lo_row = nrow >= 32;
-        if (i < rows && !(lo_row && g >= 16)) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(Q + i * 128 + d0));
-            const float4 y = __ldg(reinterpret_cast<const float4*>(Q + i * 128 + d0 + 4));
-            const float f[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                uint16_t h0 = bf16_rn_bits(f[2 * u]), h1 = bf16_rn_bits(f[2 * u + 1]);
-                if (lo_row) {
-                    h0 = bf16_rn_bits(f[2 * u] - bf16_val(h0));
-                    h1 = bf16_rn_bits(f[2 * u + 1] - bf16_val(h1));
-                }
-                v[u] = uint32_t(h0) | (uint32_t(h1) << 16);
-            }
-        }
-        *reinterpret_cast<uint4*>(smem + kTcOffB + kc * 8192 + nrow * 128 + ((j ^ (nrow & 7)) << 4)) =
-            make_uint4(v[0], v[1], v[2], v[3]);
-    }
     if (threadIdx.x == 0) {
+        tc_mbar_init(b_full, 1);
         tc_mbar_init(a_full, 4);
         tc_mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -525,27 +643,45 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
                      "r"(kTcTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 4) {
-        // ---------------- MMA issuer
+        // ---------------- B operand + MMA issuer
+        if (lane == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b_full), "r"(launch::kQImgBytes)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    base + kTcOffB),
+                "l"(qimg), "r"(launch::kQImgBytes), "r"(b_full)
+                : "memory");
+        }
+        tc_mbar_wait(b_full, 0);
         uint32_t lt = 0;
         for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++lt) {
             tc_mbar_wait(a_full, lt & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
+                // D = [R_hi | R_lo] . [Q_hi | Q_hi]  (K = 256: B1 chunks 0-3)
 #pragma unroll
                 for (uint32_t s = 0; s < 16; ++s) {
-                    const uint64_t bd = tc_desc(base + kTcOffB + (s >> 2) * 8192 + (s & 3) * 32);
+                    const uint64_t bd = tc_desc(base + kTcOffB + (s >> 2) * 4096 + (s & 3) * 32);
                     asm volatile(
                         "{\n\t.reg .pred p;\n\t"
                         "setp.ne.b32 p, %4, 0;\n\t"
                         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + kTcAccCol),
                         "r"(tmem + 8 * s), "l"(bd), "r"(kTcIdesc), "r"(s));
+                }
+                // D += R_hi . Q_lo  (K = 128: B2 chunks 0-1)
+#pragma unroll
+                for (uint32_t s = 0; s < 8; ++s) {
+                    const uint64_t bd = tc_desc(base + kTcOffB + 16384 + (s >> 2) * 4096 + (s & 3) * 32);
+                    asm volatile(
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 1;" ::"r"(tmem + kTcAccCol),
+                        "r"(tmem + 8 * s), "l"(bd), "r"(kTcIdesc));
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  acc_full)
@@ -554,93 +690,36 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
             __syncwarp();
         }
     } else {
-        // ---------------- token group: produce a tile, then its epilogue
-        constexpr uint32_t kBpt = NB * 128 / 8;          // residual bytes per token
-        const uint32_t lane_off = (warp * 32) << 16;
-        const uint32_t tslot = warp * 32 + lane;          // token slot in the tile
+        // ---------------- token group
         float* tr = trb + warp * 32 * 33;
+        const uint32_t tslot = warp * 32 + lane;
+        TcToken<NB> x0, x1;
+        const uint32_t G = gridDim.x;
+        tc_prefetch2<NB>(x0, x1, blockIdx.x, blockIdx.x + G, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
+                         residuals);
+        tc_fetch_srow<NB>(x0, S, srow, tslot);
         uint32_t lt = 0;
-        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++lt) {
-            const uint32_t g0 = tl * kTcTile + warp * 32, g = g0 + lane;
-            const bool valid = g < T;
-            uint32_t p = 0xFFFFFFFFu;
-            if (g0 < T) p = run_finalists(pref, n, g0, g);
-            uint32_t hi[64], lo[64];
-            if (valid) {
-                const uint64_t tok = fin_base[p] + g;
-                const uint32_t code = __ldg(codes + tok);
-                inv_s[tslot] = __ldg(tok_inv + tok);
-                const float* srcS = S + uint64_t(code) * kScoresPitch;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) cp_async16(srow + tslot * 32 + 4 * c, srcS + 4 * c);
-                uint32_t rb[kBpt / 4];
-                const uint4* src = reinterpret_cast<const uint4*>(residuals + tok * kBpt);
-#pragma unroll
-                for (uint32_t i = 0; i < kBpt / 16; ++i) {
-                    const uint4 x = __ldg(src + i);
-                    rb[4 * i] = x.x, rb[4 * i + 1] = x.y, rb[4 * i + 2] = x.z, rb[4 * i + 3] = x.w;
-                }
-#pragma unroll
-                for (uint32_t c = 0; c < 64; ++c) {
-                    const uint32_t bit = c * kPairBits;
-                    const uint32_t e = (rb[bit / 32] >> (bit % 32)) & (kPairs - 1);
-                    hi[c] = lut_hi[e];
-                    lo[c] = lut_lo[e];
-                }
-            } else {
-#pragma unroll
-                for (uint32_t c = 0; c < 64; ++c) hi[c] = 0u, lo[c] = 0u;
+        for (uint32_t tl = blockIdx.x; tl < ntiles; tl += 2 * G, lt += 2) {
+            // tile lt (slot 0, metadata x0); the next tile's S rows go out now
+            const bool has1 = tl + G < ntiles;
+            if (has1) tc_fetch_srow<NB>(x1, S, srow + kTcTile * 32, tslot);
+            tc_tile<NB>(x0, lt, tmem, a_full, acc_full, lut_hi, lut_lo, pass_s, inv_s, srow, tr, rows, run, has1);
+            if (!has1) break;
+            // tile lt + 1 (slot 1, x1); refill x0 with tile lt + 2
+            TcToken<NB> dummy;
+            const bool has2 = tl + 2 * G < ntiles;
+            if (has2) {
+                tc_prefetch2<NB>(x0, dummy, tl + 2 * G, ntiles, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
+                                 residuals);
+                tc_fetch_srow<NB>(x0, S, srow, tslot);
             }
-            pass_s[tslot] = valid ? p : 0xFFFFFFFFu;
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            {
-                uint32_t (&h0)[32] = *reinterpret_cast<uint32_t(*)[32]>(hi);
-                uint32_t (&h1)[32] = *reinterpret_cast<uint32_t(*)[32]>(hi + 32);
-                uint32_t (&l0)[32] = *reinterpret_cast<uint32_t(*)[32]>(lo);
-                uint32_t (&l1)[32] = *reinterpret_cast<uint32_t(*)[32]>(lo + 32);
-                tc_st32(tmem + lane_off + 0, h0);
-                tc_st32(tmem + lane_off + 32, h1);
-                tc_st32(tmem + lane_off + 64, l0);
-                tc_st32(tmem + lane_off + 96, l1);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) tc_mbar_arrive(a_full);
-
-            // ---- epilogue
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            tc_mbar_wait(acc_full, lt & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t x[32], y[32];
-            tc_ld32(tmem + lane_off + kTcAccCol, x);
-            tc_ld32(tmem + lane_off + kTcAccCol + 32, y);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = __uint_as_float(x[i]) + __uint_as_float(y[i]);
-            __syncwarp();
-            // lane = query token i: (S + D) * inv over the warp's 32 tokens in
-            // stream order, segmented max per finalist
-            const uint32_t i = lane;
-            const bool live = i < rows;
-            uint32_t cur = 0xFFFFFFFFu;
-            float m = 0.0f;
-            for (uint32_t t = 0; t < 32; ++t) {
-                const uint32_t pt = pass_s[warp * 32 + t];
-                if (pt == 0xFFFFFFFFu) break;  // past the stream end (tail of the last tile)
-                const float v = __fmul_rn(__fadd_rn(srow[(warp * 32 + t) * 32 + i], tr[t * 33 + i]),
-                                          inv_s[warp * 32 + t]);
-                if (pt != cur) {
-                    if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
-                    cur = pt;
-                    m = v;
-                } else {
-                    m = dev::max_gt(m, v);
-                }
-            }
-            if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
+            tc_tile<NB>(x1, lt + 1, tmem, a_full, acc_full, lut_hi, lut_lo, pass_s, inv_s, srow + kTcTile * 32, tr,
+                        rows, run, has2);
+            if (!has2) break;
+            const bool has3 = tl + 3 * G < ntiles;
+            if (has3)
+                tc_prefetch2<NB>(x1, dummy, tl + 3 * G, ntiles, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
+                                 residuals);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -724,12 +803,12 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
     }
     if (!s.prescanned) {
         ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref,
-                             s.fin_base, s.tokens);
+                             s.fin_base, s.tokens, s.tensor_S ? s.run_p0 : static_cast<uint32_t*>(nullptr));
         count_launch();
     }
     uint64_t fb = (nmax * ix.max_doclen + kTile - 1) / kTile;
     if (fb > uint64_t(sm_count()) * 2) fb = uint64_t(sm_count()) * 2;  // two CTAs (12 warps) per SM
-    if (s.tensor_S && ix.tok_inv) {
+    if (s.tensor_S && ix.tok_inv && s.run_p0 && s.qimg) {
         // TENSOR mode: residual products on tcgen05, S rows reused (stage4_tensor_kernel)
         static launch::PerDeviceOnce tcfg;
         if (tcfg.first()) {
@@ -742,7 +821,8 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
         if (tb == 0) tb = 1;
         auto tk = ix.nbits == 1 ? stage4_tensor_kernel<1> : ix.nbits == 2 ? stage4_tensor_kernel<2> : stage4_tensor_kernel<4>;
         ::plaid::launch::pdl(tk, uint32_t(tb), kTcThreads, kTcSmemBytes, st, s.tensor_S, ix.tok_inv, ix.codes,
-                             ix.residuals, W, d_n, s.pref, s.fin_base, d_q, rows, s.run);
+                             ix.residuals, W, d_n, s.pref, s.fin_base, s.run_p0,
+                             static_cast<const uint8_t*>(s.qimg), rows, s.run);
         count_launch();
     } else {
         auto fk = ix.nbits == 1 ? stream_fused_kernel<1> : ix.nbits == 2 ? stream_fused_kernel<2> : stream_fused_kernel<4>;

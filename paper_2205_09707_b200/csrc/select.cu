@@ -350,15 +350,53 @@ __global__ void copy_count_kernel(const uint64_t* src, uint64_t* dst, uint64_t c
 // the products are exact in fp64, so only the adds must stay in order: 32-dim
 // chunks are staged coalesced in shared memory and thread r runs row r's add
 // chain from there).
+// bf16 bits of x rounded to nearest even (finite inputs)
+__device__ __forceinline__ uint32_t bf16_rn_u32(float x) {
+    const uint32_t u = __float_as_uint(x);
+    return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+
+// The stage-4 tensor kernel's B operand for a query (rank128.cu,
+// stage4_tensor_kernel): B1 = 32 rows [Q_hi | Q_hi] (K = 256), B2 = 32 rows
+// Q_lo (K = 128), Q_hi = bf16(q), Q_lo = bf16(q - Q_hi), zero rows past
+// `rows`; SWIZZLE_128B K-major chunks of 64 bf16: chunk c, row n, 16-byte
+// granule j at c * 4096 + n * 128 + ((j ^ (n & 7)) << 4); B2 at 16384.
+__device__ __forceinline__ void build_qimg(const float* __restrict__ q, uint32_t rows, uint4* __restrict__ img) {
+    for (uint32_t e = threadIdx.x; e < launch::kQImgBytes / 16; e += blockDim.x) {
+        const bool lo = e >= 1024;
+        const uint32_t e2 = lo ? e - 1024 : e;
+        const uint32_t c = e2 >> 8, n = (e2 >> 3) & 31, j = e2 & 7;
+        const uint32_t d0 = (c * 64 + j * 8) & 127;
+        uint32_t v[4] = {0, 0, 0, 0};
+        if (n < rows) {
+            const float4 a = reinterpret_cast<const float4*>(q + n * 128 + d0)[0];
+            const float4 b = reinterpret_cast<const float4*>(q + n * 128 + d0)[1];
+            const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t h0 = bf16_rn_u32(f[2 * u]), h1 = bf16_rn_u32(f[2 * u + 1]);
+                if (lo) {
+                    h0 = bf16_rn_u32(f[2 * u] - __uint_as_float(h0 << 16));
+                    h1 = bf16_rn_u32(f[2 * u + 1] - __uint_as_float(h1 << 16));
+                }
+                v[u] = h0 | (h1 << 16);
+            }
+        }
+        img[((lo ? 16384u : 0u) + c * 4096 + n * 128 + ((j ^ (n & 7)) << 4)) / 16] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
                                                               int* __restrict__ status, uint4* __restrict__ zero,
-                                                              uint64_t n16, uint4* __restrict__ zero2, uint64_t m16) {
+                                                              uint64_t n16, uint4* __restrict__ zero2, uint64_t m16,
+                                                              const float* __restrict__ qsrc, uint4* __restrict__ qimg) {
     dev::pdl_wait();
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16 + m16;
          i += uint64_t(gridDim.x) * blockDim.x) {
         if (i < n16) zero[i] = make_uint4(0, 0, 0, 0);
         else zero2[i - n16] = make_uint4(0, 0, 0, 0);
     }
+    if (qimg && blockIdx.x == gridDim.x - 1) build_qimg(qsrc, rows, qimg);
     if (blockIdx.x != 0 || q == nullptr) return;
     __shared__ float tile[32][33];
     const uint32_t t = threadIdx.x;
@@ -730,7 +768,7 @@ select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
         if (t == 0) *d_out_n = n;
         if (fs.pref) {
             __syncthreads();
-            fused::finalist_scan(nullptr, out, n, fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens);
+            fused::finalist_scan(nullptr, out, n, fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens, fs.run_p0);
         }
         return;
     }
@@ -785,7 +823,7 @@ select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
     if (t == 0) *d_out_n = want;
     if (fs.pref) {  // stage 4's finalist scan over the set just written, same CTA
         __syncthreads();
-        fused::finalist_scan(nullptr, out, uint32_t(want), fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens);
+        fused::finalist_scan(nullptr, out, uint32_t(want), fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens, fs.run_p0);
     }
 }
 
@@ -900,11 +938,13 @@ void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t s
 }
 
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
-                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st) {
+                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc, void* d_qimg) {
     const uint64_t n16 = nwords / 4, m16 = nwords2 / 4;  // both regions are multiples of 16 bytes
     const uint32_t grid = grid_for(n16 + m16, 256, uint32_t(sm_count()));
+    const bool img = d_qimg && d_qsrc && dim == 128 && rows <= 32;
     ::plaid::launch::pdl(query_prologue_kernel, grid, 256, 0, st, d_q, rows, dim, d_status,
-                         reinterpret_cast<uint4*>(d_zero), n16, reinterpret_cast<uint4*>(d_zero2), m16);
+                         reinterpret_cast<uint4*>(d_zero), n16, reinterpret_cast<uint4*>(d_zero2), m16,
+                         img ? d_qsrc : nullptr, img ? reinterpret_cast<uint4*>(d_qimg) : nullptr);
     count_launch();
 }
 
