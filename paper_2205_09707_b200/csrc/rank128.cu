@@ -457,6 +457,19 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
 }
 
+// Debug timeline (plaid_debug_s4_set(1)): globaltimer stamps per CTA (< 512):
+// 0 start, 1 prefetch done, 2 B landed (MMA warp), 3/6/9 tile 0/1/2 A stored,
+// 4/7/10 D ready, 5/8/11 epilogue done, 12 end (token warp 0, lane 0).
+__device__ unsigned long long g_s4_trace[512 * 16];
+__device__ uint32_t g_s4_dbg;
+__device__ __forceinline__ void s4_stamp(int ev) {
+    if (g_s4_dbg && blockIdx.x < 512 && (threadIdx.x & 31) == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_s4_trace[blockIdx.x * 16 + ev] = t;
+    }
+}
+
 // One lane's token of a tile: what the decode and the epilogue need, loaded
 // ahead of use (residual words, code, inv_t in flight).
 template <int NB>
@@ -558,6 +571,7 @@ __device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint3
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
     if (lane == 0) tc_mbar_arrive(a_full);
+    if (warp == 0 && lt < 3) s4_stamp(3 + 3 * lt);
 
     // ---- epilogue: S rows of this tile landed, D ready
     if (next_srow_pending)
@@ -565,6 +579,7 @@ __device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint3
     else
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     tc_mbar_wait(acc_full, lt & 1);
+    if (warp == 0 && lt < 3) s4_stamp(4 + 3 * lt);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     uint32_t d[32];
     tc_ld32(tmem + lane_off + kTcAccCol, d);
@@ -594,6 +609,7 @@ __device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint3
     if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
+    if (warp == 0 && lt < 3) s4_stamp(5 + 3 * lt);
 }
 
 template <int NB>
@@ -621,6 +637,7 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
     const uint32_t T = pref[n];
     const uint32_t ntiles = (T + kTcTile - 1) / kTcTile;
     if (blockIdx.x >= ntiles) return;
+    if (warp == 0) s4_stamp(0);
 
     // LUT: a residual bit group of two dims (2 NB bits, LSB first) -> packed
     // bf16 pairs (low half = the even dim) of w_hi and of w_lo = w - w_hi
@@ -660,6 +677,7 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
                 : "memory");
         }
         tc_mbar_wait(b_full, 0);
+        s4_stamp(2);
         uint32_t lt = 0;
         for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++lt) {
             tc_mbar_wait(a_full, lt & 1);
@@ -697,6 +715,7 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
         const uint32_t G = gridDim.x;
         tc_prefetch2<NB>(x0, x1, blockIdx.x, blockIdx.x + G, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
                          residuals);
+        if (warp == 0) s4_stamp(1);
         tc_fetch_srow<NB>(x0, S, srow, tslot);
         uint32_t lt = 0;
         for (uint32_t tl = blockIdx.x; tl < ntiles; tl += 2 * G, lt += 2) {
@@ -722,6 +741,7 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
                                  residuals);
         }
     }
+    if (warp == 0) s4_stamp(12);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 4)
@@ -856,4 +876,15 @@ void token_inv_norms(const IndexView& ix, float* d_out, cudaStream_t st) {
 // Debug: CTA 0's stage-4 tile timeline (see rank_stamp), 5 x 64 stamps.
 extern "C" int plaid_debug_rank_trace(unsigned long long* out) {
     return int(cudaMemcpyFromSymbol(out, plaid::g_rank_trace, sizeof(plaid::g_rank_trace)));
+}
+
+// Debug: the tensor-core stage-4 timeline (s4_stamp), 512 CTAs x 16 stamps.
+extern "C" int plaid_debug_s4_set(uint32_t on) {
+    int rc = int(cudaMemcpyToSymbol(plaid::g_s4_dbg, &on, sizeof on));
+    unsigned long long z[512 * 16] = {};
+    if (!rc) rc = int(cudaMemcpyToSymbol(plaid::g_s4_trace, z, sizeof z));
+    return rc;
+}
+extern "C" int plaid_debug_s4_trace(unsigned long long* out) {
+    return int(cudaMemcpyFromSymbol(out, plaid::g_s4_trace, sizeof(plaid::g_s4_trace)));
 }
