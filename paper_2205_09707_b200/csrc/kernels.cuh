@@ -263,7 +263,7 @@ struct RankScratch {
 };
 // Bytes of the stage-4 tensor kernel's B-operand image of a query (built by
 // query_prologue when given a destination).
-constexpr uint32_t kQImgBytes = 24 * 1024;
+constexpr uint32_t kQImgBytes = 32 * 1024;
 // inv_t = 1 / ||C[code_t] + r_t|| for every index token (d = 128), the
 // reference's arithmetic (residual_codec.cpp:113-130); index-load time.
 void token_inv_norms(const IndexView& ix, float* d_out, cudaStream_t st);

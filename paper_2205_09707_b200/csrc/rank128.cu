@@ -384,12 +384,14 @@ __global__ void finalize_kernel(const uint32_t* __restrict__ ids, const uint64_t
 //              and the next tile, residual decode into packed bf16 pairs
 //              (LUT), tcgen05.st of A = [R_hi | R_lo] (K = 256, 128 columns);
 //              then the epilogue: tcgen05.ld of D, a 32x32 transpose through
-//              shared memory, lane = query token: (S + D) * inv, segmented max
-//              per finalist, one 128-byte row of atomicMax per segment.
+//              shared memory, lane = query token: (S + D) * inv over the
+//              warp's 32 tokens, fully unrolled with the finalist segments
+//              known up front (ballots), one 128-byte row of atomicMax per
+//              segment end (warp-uniform).
 //   warp 4     TMEM allocation, the B operand (the query image built by
-//              query_prologue, one 24 KB bulk copy) and the MMA issuer:
-//              16 x (M=128, N=32, K=16) of [R_hi | R_lo] . [Q_hi | Q_hi] and
-//              8 of R_hi . Q_lo into the same 32 accumulator columns.
+//              query_prologue, one 32 KB bulk copy) and the MMA issuer:
+//              16 x (M=128, N=64, K=16): D[:, i] + D[:, 32 + i] =
+//              [R_hi | R_lo] . [Q_hi | Q_hi] + [R_hi | R_lo] . [Q_lo | 0].
 // Two CTAs per SM (256 TMEM columns each); tiles round-robin over the grid.
 constexpr uint32_t kTcTile = 128;
 constexpr uint32_t kTcThreads = 160;
@@ -398,14 +400,13 @@ constexpr uint32_t kTcAccCol = 128;
 constexpr uint32_t kTcOffB = 0;                                   // query image (launch::kQImgBytes)
 constexpr uint32_t kTcOffS = kTcOffB + launch::kQImgBytes;                // 2 x 128 tokens x 32 floats
 constexpr uint32_t kTcOffTr = kTcOffS + 2 * kTcTile * 32 * 4;     // 4 warps x 32 x 33 floats
-constexpr uint32_t kTcOffMeta = kTcOffTr + 4 * 32 * 33 * 4;       // pass[128], inv[128]
-constexpr uint32_t kTcOffLut = kTcOffMeta + 2 * kTcTile * 4;      // hi[256], lo[256] u32
+constexpr uint32_t kTcOffLut = kTcOffTr + 4 * 32 * 33 * 4;        // hi[256], lo[256] u32
 constexpr uint32_t kTcOffBar = kTcOffLut + 2 * 256 * 4;           // b_full, a_full, acc_full, tmem slot
 constexpr uint32_t kTcSmemBytes = kTcOffBar + 64 + 1024;          // + alignment slack
 static_assert(2 * (kTcSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
 
-// kind::f16 instruction descriptor: D f32, A and B bf16, both K-major, M = 128, N = 32.
-constexpr uint32_t kTcIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// kind::f16 instruction descriptor: D f32, A and B bf16, both K-major, M = 128, N = 64.
+constexpr uint32_t kTcIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ uint64_t tc_desc(uint32_t addr) {
     uint64_t d = uint64_t((addr >> 4) & 0x3FFFu);
@@ -545,12 +546,11 @@ __device__ __forceinline__ void tc_fetch_srow(const TcToken<NB>& x, const float*
 template <int NB>
 __device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint32_t tmem, uint32_t a_full,
                                         uint32_t acc_full, const uint32_t* lut_hi, const uint32_t* lut_lo,
-                                        uint32_t* pass_s, float* inv_s, const float* srow_slot, float* tr,
+                                        const float* srow_slot, float* tr,
                                         uint32_t rows, uint32_t* __restrict__ run, bool next_srow_pending) {
     constexpr uint32_t kPairBits = 2 * NB, kPairs = 1u << kPairBits;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t lane_off = (warp * 32) << 16;
-    const uint32_t tslot = warp * 32 + lane;
     // A operand: columns [0, 64) packed bf16 pairs of R_hi, [64, 128) of R_lo
 #pragma unroll
     for (uint32_t h = 0; h < 2; ++h) {
@@ -565,8 +565,6 @@ __device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint3
         tc_st32(tmem + lane_off + 32 * h, hi);
         tc_st32(tmem + lane_off + 64 + 32 * h, lo);
     }
-    pass_s[tslot] = x.p;
-    inv_s[tslot] = x.inv;
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
@@ -578,35 +576,41 @@ __device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint3
         asm volatile("cp.async.wait_group 1;" ::: "memory");
     else
         asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // the warp's finalist segments (lane = token): starts, ends, and the
+    // stream end (tokens past it only in the last tile's tail)
+    const uint32_t my_p = x.p;
+    const uint32_t prev_p = __shfl_up_sync(0xffffffffu, my_p, 1), next_p = __shfl_down_sync(0xffffffffu, my_p, 1);
+    const bool tok = my_p != 0xFFFFFFFFu;
+    const uint32_t starts = __ballot_sync(0xffffffffu, tok && (lane == 0 || prev_p != my_p));
+    const uint32_t ends = __ballot_sync(0xffffffffu, tok && (lane == 31 || next_p != my_p));
     tc_mbar_wait(acc_full, lt & 1);
     if (warp == 0 && lt < 3) s4_stamp(4 + 3 * lt);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    uint32_t d[32];
-    tc_ld32(tmem + lane_off + kTcAccCol, d);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    {
+        uint32_t d0[32], d1[32];
+        tc_ld32(tmem + lane_off + kTcAccCol, d0);
+        tc_ld32(tmem + lane_off + kTcAccCol + 32, d1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = __uint_as_float(d[i]);
+        for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = __uint_as_float(d0[i]) + __uint_as_float(d1[i]);
+    }
     __syncwarp();
-    // lane = query token i: (S + D) * inv over the warp's 32 tokens in stream
-    // order, segmented max per finalist, one atomicMax row per segment
+    // lane = query token i: (S + D) * inv over the warp's tokens in stream
+    // order; the max restarts at a segment start and is published (one
+    // coalesced row of atomicMax) at a segment end
     const uint32_t i = lane;
     const bool live = i < rows;
-    uint32_t cur = 0xFFFFFFFFu;
+    const float* sr = srow_slot + warp * 32 * 32 + i;
     float m = 0.0f;
-#pragma unroll 4
+#pragma unroll
     for (uint32_t t = 0; t < 32; ++t) {
-        const uint32_t pt = pass_s[warp * 32 + t];
-        if (pt == 0xFFFFFFFFu) break;  // past the stream end (tail of the last tile)
-        const float v = __fmul_rn(__fadd_rn(srow_slot[(warp * 32 + t) * 32 + i], tr[t * 33 + i]), inv_s[warp * 32 + t]);
-        if (pt != cur) {
-            if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
-            cur = pt;
-            m = v;
-        } else {
-            m = dev::max_gt(m, v);
+        const float v = __fmul_rn(__fadd_rn(sr[t * 32], tr[t * 33 + i]), __shfl_sync(0xffffffffu, x.inv, t));
+        m = ((starts >> t) & 1u) ? v : dev::max_gt(m, v);
+        if ((ends >> t) & 1u) {
+            const uint32_t pt = __shfl_sync(0xffffffffu, my_p, t);
+            if (live) atomicMax(run + uint64_t(pt) * 32 + i, dev::ord_f32(m));
         }
     }
-    if (cur != 0xFFFFFFFFu && live) atomicMax(run + uint64_t(cur) * 32 + i, dev::ord_f32(m));
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
     if (warp == 0 && lt < 3) s4_stamp(5 + 3 * lt);
@@ -628,8 +632,6 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTcOffBar + 24);
     float* srow = reinterpret_cast<float*>(smem + kTcOffS);
     float* trb = reinterpret_cast<float*>(smem + kTcOffTr);
-    uint32_t* pass_s = reinterpret_cast<uint32_t*>(smem + kTcOffMeta);
-    float* inv_s = reinterpret_cast<float*>(smem + kTcOffMeta + kTcTile * 4);
     uint32_t* lut_hi = reinterpret_cast<uint32_t*>(smem + kTcOffLut);
     uint32_t* lut_lo = lut_hi + 256;
 
@@ -683,23 +685,15 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
             tc_mbar_wait(a_full, lt & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
-                // D = [R_hi | R_lo] . [Q_hi | Q_hi]  (K = 256: B1 chunks 0-3)
+                // D[:, 0:32] = [R_hi | R_lo] . [Q_hi | Q_hi], D[:, 32:64] = [R_hi | R_lo] . [Q_lo | 0]
 #pragma unroll
                 for (uint32_t s = 0; s < 16; ++s) {
-                    const uint64_t bd = tc_desc(base + kTcOffB + (s >> 2) * 4096 + (s & 3) * 32);
+                    const uint64_t bd = tc_desc(base + kTcOffB + (s >> 2) * 8192 + (s & 3) * 32);
                     asm volatile(
                         "{\n\t.reg .pred p;\n\t"
                         "setp.ne.b32 p, %4, 0;\n\t"
                         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + kTcAccCol),
                         "r"(tmem + 8 * s), "l"(bd), "r"(kTcIdesc), "r"(s));
-                }
-                // D += R_hi . Q_lo  (K = 128: B2 chunks 0-1)
-#pragma unroll
-                for (uint32_t s = 0; s < 8; ++s) {
-                    const uint64_t bd = tc_desc(base + kTcOffB + 16384 + (s >> 2) * 4096 + (s & 3) * 32);
-                    asm volatile(
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 1;" ::"r"(tmem + kTcAccCol),
-                        "r"(tmem + 8 * s), "l"(bd), "r"(kTcIdesc));
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  acc_full)
@@ -722,7 +716,7 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
             // tile lt (slot 0, metadata x0); the next tile's S rows go out now
             const bool has1 = tl + G < ntiles;
             if (has1) tc_fetch_srow<NB>(x1, S, srow + kTcTile * 32, tslot);
-            tc_tile<NB>(x0, lt, tmem, a_full, acc_full, lut_hi, lut_lo, pass_s, inv_s, srow, tr, rows, run, has1);
+            tc_tile<NB>(x0, lt, tmem, a_full, acc_full, lut_hi, lut_lo, srow, tr, rows, run, has1);
             if (!has1) break;
             // tile lt + 1 (slot 1, x1); refill x0 with tile lt + 2
             TcToken<NB> dummy;
@@ -732,7 +726,7 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
                                  residuals);
                 tc_fetch_srow<NB>(x0, S, srow, tslot);
             }
-            tc_tile<NB>(x1, lt + 1, tmem, a_full, acc_full, lut_hi, lut_lo, pass_s, inv_s, srow + kTcTile * 32, tr,
+            tc_tile<NB>(x1, lt + 1, tmem, a_full, acc_full, lut_hi, lut_lo, srow + kTcTile * 32, tr,
                         rows, run, has2);
             if (!has2) break;
             const bool has3 = tl + 3 * G < ntiles;

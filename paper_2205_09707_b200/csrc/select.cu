@@ -357,20 +357,20 @@ __device__ __forceinline__ uint32_t bf16_rn_u32(float x) {
 }
 
 // The stage-4 tensor kernel's B operand for a query (rank128.cu,
-// stage4_tensor_kernel): B1 = 32 rows [Q_hi | Q_hi] (K = 256), B2 = 32 rows
-// Q_lo (K = 128), Q_hi = bf16(q), Q_lo = bf16(q - Q_hi), zero rows past
-// `rows`; SWIZZLE_128B K-major chunks of 64 bf16: chunk c, row n, 16-byte
-// granule j at c * 4096 + n * 128 + ((j ^ (n & 7)) << 4); B2 at 16384.
+// stage4_tensor_kernel): 64 rows x K = 256 bf16, row n < 32 = [Q_hi | Q_hi]
+// of query token n, row 32 + i = [Q_lo | 0] of token i (Q_hi = bf16(q),
+// Q_lo = bf16(q - Q_hi); zero rows past `rows`), SWIZZLE_128B K-major chunks
+// of 64 bf16: chunk c, row n, 16-byte granule j at c * 8192 + n * 128 +
+// ((j ^ (n & 7)) << 4).
 __device__ __forceinline__ void build_qimg(const float* __restrict__ q, uint32_t rows, uint4* __restrict__ img) {
-    for (uint32_t e = threadIdx.x; e < launch::kQImgBytes / 16; e += blockDim.x) {
-        const bool lo = e >= 1024;
-        const uint32_t e2 = lo ? e - 1024 : e;
-        const uint32_t c = e2 >> 8, n = (e2 >> 3) & 31, j = e2 & 7;
-        const uint32_t d0 = (c * 64 + j * 8) & 127;
+    for (uint32_t e = threadIdx.x; e < kQImgBytes / 16; e += blockDim.x) {
+        const uint32_t c = e >> 9, n = (e >> 3) & 63, j = e & 7;
+        const uint32_t i = n & 31, k0 = c * 64 + j * 8, d0 = k0 & 127;
+        const bool lo = n >= 32;
         uint32_t v[4] = {0, 0, 0, 0};
-        if (n < rows) {
-            const float4 a = reinterpret_cast<const float4*>(q + n * 128 + d0)[0];
-            const float4 b = reinterpret_cast<const float4*>(q + n * 128 + d0)[1];
+        if (i < rows && !(lo && k0 >= 128)) {
+            const float4 a = reinterpret_cast<const float4*>(q + i * 128 + d0)[0];
+            const float4 b = reinterpret_cast<const float4*>(q + i * 128 + d0)[1];
             const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -382,7 +382,7 @@ __device__ __forceinline__ void build_qimg(const float* __restrict__ q, uint32_t
                 v[u] = h0 | (h1 << 16);
             }
         }
-        img[((lo ? 16384u : 0u) + c * 4096 + n * 128 + ((j ^ (n & 7)) << 4)) / 16] = make_uint4(v[0], v[1], v[2], v[3]);
+        img[(c * 8192 + n * 128 + ((j ^ (n & 7)) << 4)) / 16] = make_uint4(v[0], v[1], v[2], v[3]);
     }
 }
 
