@@ -363,7 +363,7 @@ __device__ __forceinline__ uint32_t bf16_rn_u32(float x) {
 // of 64 bf16: chunk c, row n, 16-byte granule j at c * 8192 + n * 128 +
 // ((j ^ (n & 7)) << 4).
 __device__ __forceinline__ void build_qimg(const float* __restrict__ q, uint32_t rows, uint4* __restrict__ img) {
-    for (uint32_t e = threadIdx.x; e < kQImgBytes / 16; e += blockDim.x) {
+    for (uint32_t e = threadIdx.x; e < launch::kQImgBytes / 16; e += blockDim.x) {
         const uint32_t c = e >> 9, n = (e >> 3) & 63, j = e & 7;
         const uint32_t i = n & 31, k0 = c * 64 + j * 8, d0 = k0 & 127;
         const bool lo = n >= 32;
