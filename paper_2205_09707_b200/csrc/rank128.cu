@@ -398,8 +398,9 @@ constexpr uint32_t kTcThreads = 160;
 constexpr uint32_t kTcTmemCols = 256;
 constexpr uint32_t kTcAccCol = 128;
 constexpr uint32_t kTcOffB = 0;                                   // query image (launch::kQImgBytes)
-constexpr uint32_t kTcOffS = kTcOffB + launch::kQImgBytes;                // 2 x 128 tokens x 32 floats
-constexpr uint32_t kTcOffTr = kTcOffS + 2 * kTcTile * 32 * 4;     // 4 warps x 32 x 33 floats
+constexpr uint32_t kTcSPitch = 36;                                // floats per S row slot (conflict-free LDS.128)
+constexpr uint32_t kTcOffS = kTcOffB + launch::kQImgBytes;        // 2 x 128 tokens x 36 floats
+constexpr uint32_t kTcOffTr = kTcOffS + 2 * kTcTile * kTcSPitch * 4;  // 4 warps x 32 x 33 floats
 constexpr uint32_t kTcOffLut = kTcOffTr + 4 * 32 * 33 * 4;        // hi[256], lo[256] u32
 constexpr uint32_t kTcOffBar = kTcOffLut + 2 * 256 * 4;           // b_full, a_full, acc_full, tmem slot
 constexpr uint32_t kTcSmemBytes = kTcOffBar + 64 + 1024;          // + alignment slack
@@ -531,27 +532,27 @@ __device__ __forceinline__ void tc_prefetch2(TcToken<NB>& a, TcToken<NB>& b, uin
     finish(b, hb, g0b, lob, eb, fb);
 }
 
-// cp.async of the token's 128-byte S row into slot `slot` (skipped past the end)
+// cp.async of the token's 128-byte S row into its row of an S slot (skipped
+// past the stream end); one commit group per call
 template <int NB>
-__device__ __forceinline__ void tc_fetch_srow(const TcToken<NB>& x, const float* __restrict__ S, float* srow_slot,
-                                              uint32_t tslot) {
+__device__ __forceinline__ void tc_fetch_srow(const TcToken<NB>& x, const float* __restrict__ S, float* srow_slot) {
     if (x.p != 0xFFFFFFFFu) {
         const float* src = S + uint64_t(x.code) * kScoresPitch;
+        float* dst = srow_slot + threadIdx.x * kTcSPitch;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) cp_async16(srow_slot + tslot * 32 + 4 * c, src + 4 * c);
+        for (int c = 0; c < 8; ++c) cp_async16(dst + 4 * c, src + 4 * c);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// A operand of the token's TMEM lane: columns [0, 64) packed bf16 pairs of
+// R_hi, [64, 128) of R_lo; then the warp's arrival on a_full
 template <int NB>
-__device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint32_t tmem, uint32_t a_full,
-                                        uint32_t acc_full, const uint32_t* lut_hi, const uint32_t* lut_lo,
-                                        const float* srow_slot, float* tr,
-                                        uint32_t rows, uint32_t* __restrict__ run, bool next_srow_pending) {
+__device__ __forceinline__ void tc_store_a(const TcToken<NB>& x, uint32_t tmem, uint32_t a_full,
+                                           const uint32_t* lut_hi, const uint32_t* lut_lo) {
     constexpr uint32_t kPairBits = 2 * NB, kPairs = 1u << kPairBits;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t lane_off = (warp * 32) << 16;
-    // A operand: columns [0, 64) packed bf16 pairs of R_hi, [64, 128) of R_lo
 #pragma unroll
     for (uint32_t h = 0; h < 2; ++h) {
         uint32_t hi[32], lo[32];
@@ -569,51 +570,57 @@ __device__ __forceinline__ void tc_tile(const TcToken<NB>& x, uint32_t lt, uint3
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
     if (lane == 0) tc_mbar_arrive(a_full);
-    if (warp == 0 && lt < 3) s4_stamp(3 + 3 * lt);
+}
 
-    // ---- epilogue: S rows of this tile landed, D ready
-    if (next_srow_pending)
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-    // the warp's finalist segments (lane = token): starts, ends, and the
-    // stream end (tokens past it only in the last tile's tail)
-    const uint32_t my_p = x.p;
+// D of tile lt into registers: d[i] = D[:, i] + D[:, 32 + i] = q_i . r_t
+__device__ __forceinline__ void tc_read_d(uint32_t lt, uint32_t tmem, uint32_t acc_full, float (&d)[32]) {
+    const uint32_t warp = threadIdx.x >> 5;
+    tc_mbar_wait(acc_full, lt & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t d0[32], d1[32];
+    tc_ld32(tmem + ((warp * 32) << 16) + kTcAccCol, d0);
+    tc_ld32(tmem + ((warp * 32) << 16) + kTcAccCol + 32, d1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) d[i] = __uint_as_float(d0[i]) + __uint_as_float(d1[i]);
+}
+
+// Epilogue of a tile (its S rows landed): thread = token forms the 32 scores
+// (S + D) * inv, a transpose through shared memory puts lane = query token,
+// and the warp walks its 32 tokens in stream order: the max restarts at a
+// finalist's first token and is published (one coalesced 128-byte row of
+// atomicMax) at its last — segments known up front from two ballots.
+__device__ __forceinline__ void tc_epilogue(float (&d)[32], float inv, uint32_t my_p, const float* srow_slot,
+                                            float* tr, uint32_t rows, uint32_t* __restrict__ run) {
+    const uint32_t lane = threadIdx.x & 31;
+    const float4* s4 = reinterpret_cast<const float4*>(srow_slot + threadIdx.x * kTcSPitch);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float4 sv = s4[c];
+        tr[lane * 33 + 4 * c + 0] = __fmul_rn(__fadd_rn(sv.x, d[4 * c + 0]), inv);
+        tr[lane * 33 + 4 * c + 1] = __fmul_rn(__fadd_rn(sv.y, d[4 * c + 1]), inv);
+        tr[lane * 33 + 4 * c + 2] = __fmul_rn(__fadd_rn(sv.z, d[4 * c + 2]), inv);
+        tr[lane * 33 + 4 * c + 3] = __fmul_rn(__fadd_rn(sv.w, d[4 * c + 3]), inv);
+    }
     const uint32_t prev_p = __shfl_up_sync(0xffffffffu, my_p, 1), next_p = __shfl_down_sync(0xffffffffu, my_p, 1);
     const bool tok = my_p != 0xFFFFFFFFu;
     const uint32_t starts = __ballot_sync(0xffffffffu, tok && (lane == 0 || prev_p != my_p));
     const uint32_t ends = __ballot_sync(0xffffffffu, tok && (lane == 31 || next_p != my_p));
-    tc_mbar_wait(acc_full, lt & 1);
-    if (warp == 0 && lt < 3) s4_stamp(4 + 3 * lt);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    {
-        uint32_t d0[32], d1[32];
-        tc_ld32(tmem + lane_off + kTcAccCol, d0);
-        tc_ld32(tmem + lane_off + kTcAccCol + 32, d1);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = __uint_as_float(d0[i]) + __uint_as_float(d1[i]);
-    }
     __syncwarp();
-    // lane = query token i: (S + D) * inv over the warp's tokens in stream
-    // order; the max restarts at a segment start and is published (one
-    // coalesced row of atomicMax) at a segment end
     const uint32_t i = lane;
     const bool live = i < rows;
-    const float* sr = srow_slot + warp * 32 * 32 + i;
     float m = 0.0f;
 #pragma unroll
     for (uint32_t t = 0; t < 32; ++t) {
-        const float v = __fmul_rn(__fadd_rn(sr[t * 32], tr[t * 33 + i]), __shfl_sync(0xffffffffu, x.inv, t));
+        const float v = tr[t * 33 + i];
         m = ((starts >> t) & 1u) ? v : dev::max_gt(m, v);
         if ((ends >> t) & 1u) {
             const uint32_t pt = __shfl_sync(0xffffffffu, my_p, t);
             if (live) atomicMax(run + uint64_t(pt) * 32 + i, dev::ord_f32(m));
         }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
-    if (warp == 0 && lt < 3) s4_stamp(5 + 3 * lt);
 }
 
 template <int NB>
@@ -702,37 +709,68 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
             __syncwarp();
         }
     } else {
-        // ---------------- token group
+        // ---------------- token group: a two-stage software pipeline — while
+        // tile lt's epilogue runs, tile lt + 1's A operand is in TMEM and its
+        // MMAs are in flight
         float* tr = trb + warp * 32 * 33;
-        const uint32_t tslot = warp * 32 + lane;
         TcToken<NB> x0, x1;
         const uint32_t G = gridDim.x;
         tc_prefetch2<NB>(x0, x1, blockIdx.x, blockIdx.x + G, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
                          residuals);
         if (warp == 0) s4_stamp(1);
-        tc_fetch_srow<NB>(x0, S, srow, tslot);
+        float* srow1 = srow + kTcTile * kTcSPitch;
+        tc_store_a<NB>(x0, tmem, a_full, lut_hi, lut_lo);
+        if (warp == 0) s4_stamp(3);
+        tc_fetch_srow<NB>(x0, S, srow);
+        float d[32];
+        TcToken<NB> unused;
         uint32_t lt = 0;
         for (uint32_t tl = blockIdx.x; tl < ntiles; tl += 2 * G, lt += 2) {
-            // tile lt (slot 0, metadata x0); the next tile's S rows go out now
-            const bool has1 = tl + G < ntiles;
-            if (has1) tc_fetch_srow<NB>(x1, S, srow + kTcTile * 32, tslot);
-            tc_tile<NB>(x0, lt, tmem, a_full, acc_full, lut_hi, lut_lo, srow, tr, rows, run, has1);
-            if (!has1) break;
-            // tile lt + 1 (slot 1, x1); refill x0 with tile lt + 2
-            TcToken<NB> dummy;
-            const bool has2 = tl + 2 * G < ntiles;
-            if (has2) {
-                tc_prefetch2<NB>(x0, dummy, tl + 2 * G, ntiles, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
-                                 residuals);
-                tc_fetch_srow<NB>(x0, S, srow, tslot);
+            // tile lt: metadata x0, S slot 0; tile lt + 1: x1, slot 1; the
+            // metadata of tile lt + 2 is requested before tile lt's epilogue
+            const bool has1 = tl + G < ntiles, has2 = tl + 2 * G < ntiles;
+            tc_read_d(lt, tmem, acc_full, d);
+            if (warp == 0 && lt < 3) s4_stamp(4 + 3 * lt);
+            if (has1) {
+                tc_store_a<NB>(x1, tmem, a_full, lut_hi, lut_lo);
+                if (warp == 0 && lt + 1 < 3) s4_stamp(3 + 3 * (lt + 1));
+                tc_fetch_srow<NB>(x1, S, srow1);
             }
-            tc_tile<NB>(x1, lt + 1, tmem, a_full, acc_full, lut_hi, lut_lo, srow + kTcTile * 32, tr,
-                        rows, run, has2);
-            if (!has2) break;
-            const bool has3 = tl + 3 * G < ntiles;
-            if (has3)
-                tc_prefetch2<NB>(x1, dummy, tl + 3 * G, ntiles, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
+            float inv = x0.inv;
+            uint32_t pp = x0.p;
+            if (has2)
+                tc_prefetch2<NB>(x0, unused, tl + 2 * G, ntiles, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
                                  residuals);
+            if (has1)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            tc_epilogue(d, inv, pp, srow, tr, rows, run);
+            if (warp == 0 && lt < 3) s4_stamp(5 + 3 * lt);
+            if (!has1) break;
+            // tile lt + 1 (x1, slot 1); tile lt + 2 (x0, slot 0) goes to TMEM
+            const bool has3 = tl + 3 * G < ntiles;
+            tc_read_d(lt + 1, tmem, acc_full, d);
+            if (warp == 0 && lt + 1 < 3) s4_stamp(4 + 3 * (lt + 1));
+            if (has2) {
+                tc_store_a<NB>(x0, tmem, a_full, lut_hi, lut_lo);
+                if (warp == 0 && lt + 2 < 3) s4_stamp(3 + 3 * (lt + 2));
+                tc_fetch_srow<NB>(x0, S, srow);
+            }
+            inv = x1.inv;
+            pp = x1.p;
+            if (has3)
+                tc_prefetch2<NB>(x1, unused, tl + 3 * G, ntiles, ntiles, T, n, pref, fin_base, run_p0, codes, tok_inv,
+                                 residuals);
+            if (has2)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            tc_epilogue(d, inv, pp, srow1, tr, rows, run);
+            if (warp == 0 && lt + 1 < 3) s4_stamp(5 + 3 * (lt + 1));
+            if (!has2) break;
         }
     }
     if (warp == 0) s4_stamp(12);
