@@ -287,6 +287,35 @@ plaid_status plaid_merge_topk_rows_device(plaid_searcher* s, const uint32_t* d_r
                                           uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
                                           uint64_t stream);
 
+/* Batched form for throughput mode over passage shards: pids/scores
+ * [shards][B][k] and counts [shards][B] (e.g. one NCCL all-gather of every
+ * shard's [B][k] results) -> out [B][k] + out_n[B], one kernel for the whole
+ * batch.  shards * k <= 25600. */
+plaid_status plaid_merge_topk_batch_device(plaid_searcher* s, const uint32_t* d_pids, const float* d_scores,
+                                           const uint64_t* d_counts, uint64_t shards, uint64_t batch, uint64_t k,
+                                           uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
+                                           uint64_t stream);
+
+/* ---- single-process sharded search over several GPUs -------------
+ * The drop-in for lir::search (pipeline.hpp:86-87) over a passage-sharded
+ * index: `shards` are disjoint passage ranges (plaid_index_from_host_shard /
+ * _at, each on its own GPU or sharing one), searched by one searcher per
+ * shard on its device; the exchanges are on-device all-gathers that read the
+ * other shards' rows through NVLink peer access (no host round trip), and the
+ * final select runs on shards[0]'s device.  mode GLOBAL_EXACT reproduces
+ * lir::search over the unsharded index (ids, scores, trace counters summed);
+ * SHARD_LOCAL is the reference run per shard followed by the top-k merge.
+ * Synchronous, host buffers like plaid_search. */
+typedef struct plaid_sharded plaid_sharded;
+enum { PLAID_SHARD_GLOBAL_EXACT = 0, PLAID_SHARD_LOCAL = 1 };
+plaid_status plaid_sharded_create(plaid_index* const* shards, uint32_t num_shards, const plaid_searcher_config* cfg,
+                                  int32_t mode, plaid_sharded** out);
+void plaid_sharded_destroy(plaid_sharded* s);
+plaid_status plaid_sharded_search(plaid_sharded* s, const float* q, uint64_t rows, uint64_t dim,
+                                  const plaid_params* params, uint32_t* out_pids, float* out_scores, uint64_t* out_n,
+                                  plaid_trace* trace);
+uint64_t plaid_sharded_last_launches(const plaid_sharded* s);
+
 /* ---- per-stage entry points (host buffers in/out, computed on the GPU) ------------ */
 /* pipeline.cpp:26-50: scores K x rows (centroid-major), row_max K */
 plaid_status plaid_compute_centroid_scores(plaid_searcher* s, const float* q, uint64_t rows,

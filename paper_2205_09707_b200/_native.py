@@ -123,6 +123,15 @@ SIGNATURES = {
     "plaid_maxsim_packed": (C.c_int, [C.c_void_p, f32p, C.c_uint64, u64p, C.c_uint64, f32p]),
     "plaid_maxsim_embeddings": (C.c_int, [C.c_void_p, f32p, C.c_uint64, C.c_uint64, f32p, u64p, C.c_uint64,
                                           f32p]),
+    "plaid_merge_topk_batch_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                                C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_uint64]),
+    "plaid_sharded_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.POINTER(SearcherConfig), C.c_int32,
+                                       C.POINTER(C.c_void_p)]),
+    "plaid_sharded_destroy": (None, [C.c_void_p]),
+    "plaid_sharded_search": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(Params),
+                                       C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(Trace)]),
+    "plaid_sharded_last_launches": (C.c_uint64, [C.c_void_p]),
     # test knobs (not part of include/plaid.h)
     "plaid_debug_set_tf32_grid": (C.c_uint32, [C.c_uint32]),
 }

@@ -492,6 +492,13 @@ class Searcher:
                                                 N.ptr(out, C.c_float)))
         return out[:np_]
 
+    def merge_topk_batch_device(self, d_pids: int, d_scores: int, d_counts: int, shards: int, batch: int, k: int,
+                                d_out_pids: int, d_out_scores: int, d_out_n: int, stream: int = 0) -> None:
+        """[shards][B][k] shard lists (+ counts [shards][B]) -> [B][k] global
+        top-k per query, one kernel for the whole batch."""
+        _check(N.load().plaid_merge_topk_batch_device(self._h, d_pids, d_scores, d_counts, shards, batch, k,
+                                                      d_out_pids, d_out_scores, d_out_n, stream))
+
     def merge_topk(self, pids: np.ndarray, scores: np.ndarray, counts: np.ndarray, k: int):
         """Final select over G shard lists [G, stride]."""
         pids = np.ascontiguousarray(pids, dtype=np.uint32)
@@ -505,6 +512,56 @@ class Searcher:
                                          N.ptr(cnt, C.c_uint64), G, stride, k, N.ptr(oi, C.c_uint32),
                                          N.ptr(os_, C.c_float), C.byref(n)))
         return oi[: n.value].copy(), os_[: n.value].copy()
+
+
+class MultiGpuSearcher:
+    """lir::search over a passage-sharded index in ONE process
+    (plaid_sharded_*, include/plaid.h): one searcher per shard on the
+    shard's GPU, exchanges as on-device all-gathers over NVLink peer access,
+    final select on shards[0]'s device.  mode "global-exact" equals the
+    reference over the unsharded index; "shard-local" = reference per shard +
+    top-k merge."""
+
+    MODES = {"global-exact": 0, "shard-local": 1}
+
+    def __init__(self, shards, score_mode: ScoreMode = ScoreMode.TENSOR, mode: str = "global-exact"):
+        if mode not in self.MODES:
+            raise ValueError(f"mode must be one of {tuple(self.MODES)}")
+        self.shards = list(shards)
+        arr = (C.c_void_p * len(self.shards))(*[s._h.value if isinstance(s._h, C.c_void_p) else s._h
+                                                for s in self.shards])
+        cfg = N.SearcherConfig(int(score_mode), 0, 0, 0)
+        out = C.c_void_p()
+        _check(N.load().plaid_sharded_create(arr, len(self.shards), C.byref(cfg), self.MODES[mode], C.byref(out)))
+        self._h = out
+
+    def close(self) -> None:
+        if self._h:
+            N.load().plaid_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, q: np.ndarray, params: SearchParams, options: SearchOptions = SearchOptions()) -> SearchResult:
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        rows, dim = (q.shape if q.ndim == 2 else (0, 0))
+        k = max(int(params.k), 1)
+        ids = np.zeros(k, dtype=np.uint32)
+        sc = np.zeros(k, dtype=np.float32)
+        n = C.c_uint64()
+        tr = N.Trace()
+        p = params._c(options.disable_filter)
+        _check(N.load().plaid_sharded_search(self._h, _addr(q), rows, dim, C.byref(p), _addr(ids), _addr(sc),
+                                             C.byref(n), C.byref(tr)))
+        m = n.value
+        return SearchResult(CandidateSet(ids[:m].copy(), sc[:m].copy()), StageTrace._from_c(tr))
+
+    def last_launches(self) -> int:
+        return int(N.load().plaid_sharded_last_launches(self._h))
 
 
 class BatchSearcher:

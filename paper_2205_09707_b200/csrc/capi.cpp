@@ -20,6 +20,9 @@ struct plaid_searcher {
 struct plaid_batch {
     std::unique_ptr<plaid::BatchSearcher> impl;
 };
+struct plaid_sharded {
+    std::unique_ptr<plaid::ShardedSearcher> impl;
+};
 
 namespace {
 
@@ -518,5 +521,63 @@ plaid_status plaid_maxsim_embeddings(plaid_searcher* s, const float* q, uint64_t
                                      float* out) {
     return guarded([&] { s->impl->maxsim_embeddings(q, rows, dim, emb, offsets, np, out); });
 }
+
+plaid_status plaid_merge_topk_batch_device(plaid_searcher* s, const uint32_t* d_pids, const float* d_scores,
+                                           const uint64_t* d_counts, uint64_t shards, uint64_t batch, uint64_t k,
+                                           uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
+                                           uint64_t stream) {
+    return guarded([&] {
+        need(s, "searcher");
+        if (k < 1) plaid::fail(PLAID_INVALID_PARAMS, "k must be >= 1");
+        if (shards * k > 25600) plaid::fail(PLAID_UNSUPPORTED, "shards x k above 25600");
+        plaid::DeviceGuard g(s->impl->device());
+        cudaStream_t st = stream ? reinterpret_cast<cudaStream_t>(stream) : s->impl->stream();
+        plaid::launch::merge_batch(d_pids, d_scores, d_counts, uint32_t(shards), uint32_t(batch), uint32_t(k),
+                                   d_out_pids, d_out_scores, d_out_n, st);
+        PLAID_CUDA(cudaGetLastError());
+    });
+}
+
+plaid_status plaid_sharded_create(plaid_index* const* shards, uint32_t num_shards, const plaid_searcher_config* cfg,
+                                  int32_t mode, plaid_sharded** out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        need(shards, "shards");
+        std::vector<plaid::DeviceIndex*> v;
+        for (uint32_t g = 0; g < num_shards; ++g) {
+            need(shards[g], "shard index");
+            v.push_back(shards[g]->impl.get());
+        }
+        const plaid_searcher_config c = cfg ? *cfg : default_config();
+        auto* h = new plaid_sharded();
+        try {
+            h->impl = std::make_unique<plaid::ShardedSearcher>(v, c, mode);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+void plaid_sharded_destroy(plaid_sharded* s) { delete s; }
+
+plaid_status plaid_sharded_search(plaid_sharded* s, const float* q, uint64_t rows, uint64_t dim,
+                                  const plaid_params* params, uint32_t* out_pids, float* out_scores, uint64_t* out_n,
+                                  plaid_trace* trace) {
+    return guarded([&] {
+        need(s, "sharded searcher");
+        need(params, "params");
+        need(out_n, "out_n");
+        *out_n = 0;
+        need(q, "q");
+        need(out_pids, "out_pids");
+        need(out_scores, "out_scores");
+        s->impl->search(q, rows, dim, *params, out_pids, out_scores, out_n, trace);
+    });
+}
+
+uint64_t plaid_sharded_last_launches(const plaid_sharded* s) { return s ? s->impl->last_launches() : 0; }
 
 }  // extern "C"

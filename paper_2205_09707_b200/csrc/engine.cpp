@@ -1393,4 +1393,188 @@ void BatchSearcher::sync() {
     for (auto& s : lanes_) s->sync();  // also reports device-side query validation failures
 }
 
+// ---------------------------------------------------------------- sharded (single process)
+ShardedSearcher::ShardedSearcher(const std::vector<DeviceIndex*>& shards, const plaid_searcher_config& cfg, int mode)
+    : mode_(mode) {
+    if (shards.empty() || shards.size() > launch::kMaxShards)
+        fail(PLAID_INVALID_PARAMS, "shard count must be in [1, " + std::to_string(launch::kMaxShards) + "]");
+    if (mode != kGlobalExact && mode != kShardLocal) fail(PLAID_INVALID_PARAMS, "unknown shard mode");
+    sh_.resize(shards.size());
+    for (size_t g = 0; g < shards.size(); ++g) {
+        DeviceIndex* ix = shards[g];
+        if (!ix) fail(PLAID_INVALID_PARAMS, "shard index is NULL");
+        const IndexView& v = ix->view();
+        if (g == 0) {
+            dim_ = v.dim;
+            K_ = v.K;
+        } else if (v.dim != dim_ || v.K != K_) {
+            fail(PLAID_INVALID_PARAMS, "shards must share dim and the centroid table");
+        }
+        N_ += v.N;
+        Shard& s = sh_[g];
+        s.ix = ix;
+        s.dev = ix->device();
+        s.s = std::make_unique<Searcher>(ix, s.dev, cfg);
+        s.st = s.s->stream();
+        DeviceGuard dg(s.dev);
+        for (auto& e : s.ev) PLAID_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s.q.ensure(32 * 256);
+        s.cnt.ensure(8);
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s.h_cnt), 8 * sizeof(uint64_t)));
+    }
+    // every shard's exchange kernel reads every other shard's row: peer access
+    for (auto& a : sh_)
+        for (auto& b : sh_) {
+            if (a.dev == b.dev) continue;
+            int ok = 0;
+            PLAID_CUDA(cudaDeviceCanAccessPeer(&ok, a.dev, b.dev));
+            if (!ok) fail(PLAID_UNSUPPORTED, "no peer access between GPUs " + std::to_string(a.dev) + " and " +
+                                                std::to_string(b.dev));
+            DeviceGuard dg(a.dev);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b.dev, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else PLAID_CUDA(e);
+        }
+    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_q_), 32 * 256 * sizeof(float)));
+}
+
+ShardedSearcher::~ShardedSearcher() {
+    for (auto& s : sh_) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(s.dev);
+        if (s.st) cudaStreamSynchronize(s.st);
+        for (auto& e : s.ev)
+            if (e) cudaEventDestroy(e);
+        if (s.h_cnt) cudaFreeHost(s.h_cnt);
+        cudaSetDevice(prev);
+    }
+    if (h_q_) cudaFreeHost(h_q_);
+    if (h_out_) cudaFreeHost(h_out_);
+}
+
+// dst's stream waits for event `which` of every shard, then gathers their
+// rows (x2, x3 or result rows) into `out` on dst's device.
+void ShardedSearcher::gather(Shard& dst, int which, uint64_t words, uint64_t* out) {
+    launch::PeerRows src{};
+    for (size_t g = 0; g < sh_.size(); ++g) {
+        Shard& s = sh_[g];
+        if (&s != &dst) PLAID_CUDA(cudaStreamWaitEvent(dst.st, s.ev[which], 0));
+        src.p[g] = which == 0 ? s.x2.p : which == 1 ? s.x3.p : s.rows.p;
+    }
+    DeviceGuard dg(dst.dev);
+    launch::gather_rows(src, uint32_t(sh_.size()), words, out, dst.st);
+}
+
+void ShardedSearcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_params& p, uint32_t* out_pids,
+                             float* out_scores, uint64_t* out_n, plaid_trace* trace) {
+    *out_n = 0;
+    if (trace) std::memset(trace, 0, sizeof *trace);
+    validate_query_host(q, rows, dim, dim_);  // types.cpp:61-72, then :88-99
+    validate_params_host(p, K_);
+    if (rows > 32) fail(PLAID_UNSUPPORTED, "engine supports |Q| <= 32 query tokens");
+    const uint32_t G = uint32_t(sh_.size());
+    const uint64_t k = p.k;
+    // exchange strides over the GLOBAL passage count (>= every shard's width)
+    const bool df = p.disable_filter != 0;
+    const uint64_t s2 = mode_ == kGlobalExact && !df ? std::min<uint64_t>(p.ndocs, N_) : 0;
+    const uint64_t s3 = mode_ == kGlobalExact && !df ? std::min<uint64_t>(stage3_width(p), N_) : 0;
+    const uint64_t row_words = k + 1;  // [k u32 pids | k f32 scores | u64 n] as u64 words
+    std::memcpy(h_q_, q, rows * dim * sizeof(float));
+    uint64_t launches = 0;
+    for (auto& s : sh_) {
+        DeviceGuard dg(s.dev);
+        s.x2.ensure(std::max<uint64_t>(s2, 1));
+        s.g2.ensure(std::max<uint64_t>(G * s2, 1));
+        s.x3.ensure(std::max<uint64_t>(s3, 1));
+        s.g3.ensure(std::max<uint64_t>(G * s3, 1));
+        s.rows.ensure(row_words);
+        PLAID_CUDA(cudaMemcpyAsync(s.q.p, h_q_, rows * dim * sizeof(float), cudaMemcpyHostToDevice, s.st));
+    }
+    auto row_ptrs = [&](Shard& s, uint32_t*& pids, float*& scores, uint64_t*& n) {
+        uint32_t* r = reinterpret_cast<uint32_t*>(s.rows.p);
+        pids = r;
+        scores = reinterpret_cast<float*>(r + k);
+        n = reinterpret_cast<uint64_t*>(r + 2 * k);
+    };
+    if (mode_ == kShardLocal) {
+        for (auto& s : sh_) {
+            DeviceGuard dg(s.dev);
+            uint32_t* pp;
+            float* ps;
+            uint64_t* pn;
+            row_ptrs(s, pp, ps, pn);
+            s.s->search_device(s.q.p, 1, rows, dim, p, pp, ps, pn, s.st);
+            launches += s.s->last_launches();
+        }
+    } else {
+        for (auto& s : sh_) {
+            DeviceGuard dg(s.dev);
+            s.s->shard_phase1(s.q.p, rows, dim, p, s.x2.p, s2, s.st);
+            PLAID_CUDA(cudaEventRecord(s.ev[0], s.st));
+        }
+        for (auto& s : sh_) {
+            if (s2) gather(s, 0, s2, s.g2.p);
+            DeviceGuard dg(s.dev);
+            s.s->shard_phase2(s.g2.p, G, s.x3.p, s3, s.st);
+            PLAID_CUDA(cudaEventRecord(s.ev[1], s.st));
+        }
+        for (auto& s : sh_) {
+            if (s3) gather(s, 1, s3, s.g3.p);
+            DeviceGuard dg(s.dev);
+            uint32_t* pp;
+            float* ps;
+            uint64_t* pn;
+            row_ptrs(s, pp, ps, pn);
+            s.s->shard_phase3(s.g3.p, G, pp, ps, pn, s.st);
+            launches += s.s->last_launches();
+        }
+    }
+    for (auto& s : sh_) {
+        DeviceGuard dg(s.dev);
+        s.s->trace_counters_device(s.cnt.p, s.st);
+        PLAID_CUDA(cudaMemcpyAsync(s.h_cnt, s.cnt.p, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s.st));
+        PLAID_CUDA(cudaEventRecord(s.ev[2], s.st));
+    }
+    // merge on shard 0's device: gather every result row, one select
+    Shard& s0 = sh_[0];
+    DeviceGuard dg(s0.dev);
+    grows_.ensure(G * row_words);
+    gather(s0, 2, row_words, grows_.p);
+    const uint64_t kk = (k + 3) / 4 * 4;
+    out_.ensure(2 * kk + 2);
+    if (h_out_k_ < kk) {
+        if (h_out_) cudaFreeHost(h_out_);
+        h_out_ = nullptr;
+        PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_out_), (2 * kk + 2) * sizeof(uint32_t)));
+        h_out_k_ = kk;
+    }
+    uint64_t* d_n = reinterpret_cast<uint64_t*>(out_.p + 2 * kk);
+    s0.s->merge_topk_rows_device(reinterpret_cast<const uint32_t*>(grows_.p), G, k, out_.p,
+                                 reinterpret_cast<float*>(out_.p + kk), d_n, s0.st);
+    PLAID_CUDA(cudaMemcpyAsync(h_out_, out_.p, (2 * kk + 2) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s0.st));
+    PLAID_CUDA(cudaStreamSynchronize(s0.st));
+    for (auto& s : sh_) s.s->sync();  // device-side failures (e.g. query validation) surface here
+    last_launches_ = launches + G + 1;
+    const uint64_t n = *reinterpret_cast<const uint64_t*>(h_out_ + 2 * kk);
+    *out_n = n;
+    std::memcpy(out_pids, h_out_, n * sizeof(uint32_t));
+    std::memcpy(out_scores, h_out_ + kk, n * sizeof(float));
+    if (trace) {
+        uint64_t c[6] = {};
+        for (auto& s : sh_)
+            for (int j = 0; j < 6; ++j) c[j] += s.h_cnt[j];
+        trace->stage1_candidates = c[0];
+        trace->centroid_matmul_count = 1;
+        if (c[0] > 0) {  // pipeline.cpp:249-252
+            trace->stage2_out = df ? c[0] : c[1];  // pipeline.cpp:255-258
+            trace->stage3_out = df ? c[0] : c[2];
+            trace->final_out = n;
+            trace->stage2_rows_gathered = c[4];
+            trace->stage3_rows_gathered = c[5];
+            trace->decompressed_passages = trace->stage3_out;
+        }
+    }
+}
+
 }  // namespace plaid

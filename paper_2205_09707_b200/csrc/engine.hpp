@@ -125,6 +125,7 @@ public:
     void sync();
     uint64_t last_launches() const { return last_launches_; }
     cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
     void phase_ms(double* out);
 
     // Per-stage entry points (host buffers).
@@ -274,6 +275,46 @@ private:
     float* h_scores_ = nullptr;
     uint64_t* h_n_ = nullptr;
     uint64_t hq_cap_ = 0, ho_cap_ = 0;
+};
+
+// Single-process passage-sharded search over G shard indexes
+// on one or several GPUs: one Searcher per shard (on the shard's device, its
+// own stream), the global-exact protocol of Searcher::shard_phase{1,2,3} (or
+// shard-local: whole search per shard, merge only), every exchange an
+// on-device all-gather (launch::gather_rows) that reads the other shards'
+// exported rows through NVLink peer access, ordered by cross-device events;
+// the per-shard top-k rows are gathered and merged on shard 0's device.
+// Equals lir::search over the unsharded index (global-exact).
+class ShardedSearcher {
+public:
+    enum Mode { kGlobalExact = 0, kShardLocal = 1 };
+    ShardedSearcher(const std::vector<DeviceIndex*>& shards, const plaid_searcher_config& cfg, int mode);
+    ~ShardedSearcher();
+    void search(const float* q, uint64_t rows, uint64_t dim, const plaid_params& p, uint32_t* out_pids,
+                float* out_scores, uint64_t* out_n, plaid_trace* trace);
+    uint64_t last_launches() const { return last_launches_; }
+
+private:
+    struct Shard {
+        DeviceIndex* ix = nullptr;
+        std::unique_ptr<Searcher> s;
+        int dev = 0;
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev[3] = {};
+        DevBuf<float> q;
+        DevBuf<uint64_t> x2, g2, x3, g3, rows, cnt;
+        uint64_t* h_cnt = nullptr;  // pinned: this shard's 6 trace counters
+    };
+    void gather(Shard& dst, int which, uint64_t words, uint64_t* out);
+    std::vector<Shard> sh_;
+    int mode_;
+    uint64_t N_ = 0, dim_ = 0, K_ = 0;
+    DevBuf<uint64_t> grows_;   // shard 0: gathered result rows
+    DevBuf<uint32_t> out_;     // shard 0: merged [k pids | k scores | n]
+    uint32_t* h_out_ = nullptr;
+    uint64_t h_out_k_ = 0;
+    float* h_q_ = nullptr;
+    uint64_t last_launches_ = 0;
 };
 
 }  // namespace plaid

@@ -243,6 +243,18 @@ void select_set(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint
 // keys at or above the global want-th largest key (*d_n updated).
 void export_keys(const uint64_t* d_keys, const uint64_t* d_n, uint64_t stride, uint32_t base, uint64_t* d_out,
                  cudaStream_t st);
+// All-gather as one kernel on the calling stream's device: row g of d_dst
+// (`words` u64 each) <- src.p[g], read through peer access when the shards
+// live on other GPUs.
+constexpr uint32_t kMaxShards = 16;
+struct PeerRows {
+    const uint64_t* p[kMaxShards];
+};
+void gather_rows(const PeerRows& src, uint32_t shards, uint64_t words, uint64_t* d_dst, cudaStream_t st);
+// Batch merge of shard top-k lists ([shards][B][k] pids / scores, counts
+// [shards][B]) into [B][k] + out_n[B]; shards * k <= 25600.
+void merge_batch(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts, uint32_t shards, uint32_t B,
+                 uint32_t k, uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n, cudaStream_t st);
 void threshold_filter(const uint64_t* d_gathered, uint64_t total, uint64_t want, uint64_t* d_keys, uint64_t* d_n,
                       uint32_t base, cudaStream_t st);
 

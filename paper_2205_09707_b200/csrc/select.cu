@@ -657,6 +657,61 @@ __global__ void export_keys_kernel(const uint64_t* __restrict__ keys, const uint
         out[j] = j < n ? globalize(keys[j], base) : 0ull;
 }
 
+// Exchange step of the single-process sharded searcher (engine.cpp,
+// ShardedSearcher): row g of dst = `words` u64 of shard g's exported row,
+// read straight from that shard's device memory through NVLink peer access
+// (or locally when shards share a device) — the all-gather as one kernel.
+__global__ void gather_rows_kernel(launch::PeerRows src, uint32_t shards, uint64_t words, uint64_t* __restrict__ dst) {
+    dev::pdl_wait();
+    const uint64_t total = uint64_t(shards) * words;
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t g = e / words, j = e - g * words;
+        dst[e] = __ldcv(src.p[g] + j);  // volatile: the peer wrote it this query
+    }
+}
+
+// Per-query merge of shard top-k lists for a whole batch (throughput mode
+// over passage shards): CTA j merges query j's lists — shard g's at
+// pids/scores [g][B][k] with count counts[g][B] — into the global top-k by
+// (score desc, pid asc) (pipeline.cpp:139-163): keys staged in shared memory,
+// each key ranked against all (unique keys: rank = # greater).
+constexpr uint32_t kMergeThreads = 256;
+__global__ void __launch_bounds__(kMergeThreads)
+merge_batch_kernel(const uint32_t* __restrict__ pids, const float* __restrict__ scores,
+                   const uint64_t* __restrict__ counts, uint32_t shards, uint32_t B, uint32_t k,
+                   uint32_t* __restrict__ out_pids, float* __restrict__ out_scores, uint64_t* __restrict__ out_n) {
+    dev::pdl_wait();
+    extern __shared__ uint64_t mk[];
+    const uint32_t j = blockIdx.x;
+    const uint32_t total = shards * k;
+    for (uint32_t e = threadIdx.x; e < total; e += kMergeThreads) {
+        const uint32_t g = e / k, r = e - g * k;
+        const uint64_t off = (uint64_t(g) * B + j) * k + r;
+        const uint64_t c = counts[uint64_t(g) * B + j];
+        mk[e] = r < c ? dev::make_key(scores[off], pids[off]) : 0ull;
+    }
+    __syncthreads();
+    uint32_t nz = 0;
+    for (uint32_t e = threadIdx.x; e < total; e += kMergeThreads) {
+        const uint64_t x = mk[e];
+        if (!x) continue;
+        ++nz;
+        uint32_t rank = 0;
+        for (uint32_t f = 0; f < total; ++f) rank += mk[f] > x;
+        if (rank < k) {
+            out_pids[uint64_t(j) * k + rank] = dev::key_id(x);
+            out_scores[uint64_t(j) * k + rank] = dev::key_score(x);
+        }
+    }
+    __shared__ uint32_t s_nz;
+    if (threadIdx.x == 0) s_nz = 0;
+    __syncthreads();
+    atomicAdd(&s_nz, nz);
+    __syncthreads();
+    if (threadIdx.x == 0) out_n[j] = s_nz < k ? s_nz : k;
+}
+
 // One CTA.  (1) t = the want-th largest non-zero key of the gathered global
 // keys g[0..total) by an MSB-first 8-bit radix select (t = 1, keep all, when
 // fewer than `want` are non-zero); (2) keys[0..*d_n) (local form, this
@@ -957,6 +1012,25 @@ void export_keys(const uint64_t* d_keys, const uint64_t* d_n, uint64_t stride, u
                  cudaStream_t st) {
     if (!stride) return;
     ::plaid::launch::pdl(export_keys_kernel, grid_for(stride, 256, 1024), 256, 0, st, d_keys, d_n, stride, base, d_out);
+    count_launch();
+}
+
+void gather_rows(const PeerRows& src, uint32_t shards, uint64_t words, uint64_t* d_dst, cudaStream_t st) {
+    if (!words || !shards) return;
+    ::plaid::launch::pdl(gather_rows_kernel, grid_for(uint64_t(shards) * words, 256, 1024), 256, 0, st, src, shards,
+                         words, d_dst);
+    count_launch();
+}
+
+void merge_batch(const uint32_t* d_pids, const float* d_scores, const uint64_t* d_counts, uint32_t shards, uint32_t B,
+                 uint32_t k, uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n, cudaStream_t st) {
+    if (!B) return;
+    const size_t smem = size_t(shards) * k * sizeof(uint64_t);
+    static launch::PerDeviceOnce cfg;
+    if (cfg.first())
+        cudaFuncSetAttribute(merge_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    ::plaid::launch::pdl(merge_batch_kernel, B, kMergeThreads, smem, st, d_pids, d_scores, d_counts, shards, B, k,
+                         d_out_pids, d_out_scores, d_out_n);
     count_launch();
 }
 
