@@ -702,14 +702,9 @@ def run_plaid_batch(args, cfg):
             _all_gather(g_pids, d_pids, None)
             _all_gather(g_scores, d_scores, None)
             _all_gather(g_n, d_n, None)
-            # shard g's query j list at g*B*k + j*k (stride B*k per shard); counts
-            # regrouped per query: cnt[j][g]
-            cnt = g_n.view(world, B).t().contiguous()
-            for j in range(B):
-                merger.merge_topk_device(g_pids.data_ptr() + 4 * j * k, g_scores.data_ptr() + 4 * j * k,
-                                         cnt.data_ptr() + 8 * j * world, world, B * k, k,
-                                         m_pids.data_ptr() + 4 * j * k, m_scores.data_ptr() + 4 * j * k,
-                                         m_n.data_ptr() + 8 * j, stream=sh)
+            # [world][B][k] lists + [world][B] counts -> [B][k]: one kernel
+            merger.merge_topk_batch_device(g_pids.data_ptr(), g_scores.data_ptr(), g_n.data_ptr(), world, B, k,
+                                           m_pids.data_ptr(), m_scores.data_ptr(), m_n.data_ptr(), stream=sh)
 
     for i in range(args.warmup):
         flush()

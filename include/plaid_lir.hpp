@@ -98,7 +98,7 @@ public:
     // options.threads is accepted and ignored (the grid size is internal).
     lir::SearchResult search(const lir::QueryMatrix& q, const lir::SearchParams& params,
                              const lir::SearchOptions& options = {}) const {
-        plaid_params p{params.k, params.nprobe, params.t_cs, params.ndocs, options.disable_filter ? 1 : 0};
+        const plaid_params p{params.k, params.nprobe, params.t_cs, params.ndocs, options.disable_filter ? 1 : 0};
         std::vector<uint32_t> ids(params.k ? params.k : 1);
         std::vector<float> scores(ids.size());
         uint64_t n = 0;
@@ -107,6 +107,12 @@ public:
             std::lock_guard<std::mutex> lock(mu_);
             check(plaid_search(searcher_, q.data.data(), q.rows, q.dim, &p, ids.data(), scores.data(), &n, &t));
         }
+        return to_result(std::move(ids), std::move(scores), n, t);
+    }
+
+    // lir::SearchResult from the C ABI's outputs (pipeline.hpp:50-53).
+    static lir::SearchResult to_result(std::vector<uint32_t> ids, std::vector<float> scores, uint64_t n,
+                                       const plaid_trace& t) {
         lir::SearchResult r;
         ids.resize(n);
         scores.resize(n);
@@ -133,6 +139,64 @@ public:
 private:
     plaid_index* index_ = nullptr;
     plaid_searcher* searcher_ = nullptr;
+    mutable std::mutex mu_;
+};
+
+// lir::search over the same index split by passage range across several GPUs
+// of one node: shard g = passages [N g / G, N (g+1) / G) on
+// devices[g] (devices may repeat), searched by plaid_sharded_* (on-device
+// all-gathers over NVLink peer access).  global_exact = true gives exactly
+// lir::search's result and trace; false = per-shard search + top-k merge.
+class ShardedEngine {
+public:
+    ShardedEngine(const lir::CompressedIndex& index, const std::vector<int>& devices,
+                  plaid_score_mode mode = PLAID_SCORES_TENSOR, bool global_exact = true) {
+        if (devices.empty()) throw std::invalid_argument("ShardedEngine needs at least one device");
+        const plaid_index_desc d = describe(index);
+        const uint64_t N = d.num_passages, G = devices.size();
+        try {
+            for (uint64_t g = 0; g < G; ++g) {
+                plaid_index* ix = nullptr;
+                check(plaid_index_from_host_shard(&d, N * g / G, N * (g + 1) / G, devices[g], &ix));
+                shards_.push_back(ix);
+            }
+            plaid_searcher_config cfg{};
+            cfg.score_mode = mode;
+            check(plaid_sharded_create(shards_.data(), uint32_t(G), &cfg,
+                                       global_exact ? PLAID_SHARD_GLOBAL_EXACT : PLAID_SHARD_LOCAL, &sharded_));
+        } catch (...) {
+            release();
+            throw;
+        }
+    }
+    ~ShardedEngine() { release(); }
+    ShardedEngine(const ShardedEngine&) = delete;
+    ShardedEngine& operator=(const ShardedEngine&) = delete;
+
+    lir::SearchResult search(const lir::QueryMatrix& q, const lir::SearchParams& params,
+                             const lir::SearchOptions& options = {}) const {
+        const plaid_params p{params.k, params.nprobe, params.t_cs, params.ndocs, options.disable_filter ? 1 : 0};
+        std::vector<uint32_t> ids(params.k ? params.k : 1);
+        std::vector<float> scores(ids.size());
+        uint64_t n = 0;
+        plaid_trace t{};
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            check(plaid_sharded_search(sharded_, q.data.data(), q.rows, q.dim, &p, ids.data(), scores.data(), &n,
+                                       &t));
+        }
+        return Engine::to_result(std::move(ids), std::move(scores), n, t);
+    }
+
+private:
+    void release() {
+        if (sharded_) plaid_sharded_destroy(sharded_);
+        sharded_ = nullptr;
+        for (plaid_index* ix : shards_) plaid_index_close(ix);
+        shards_.clear();
+    }
+    std::vector<plaid_index*> shards_;
+    plaid_sharded* sharded_ = nullptr;
     mutable std::mutex mu_;
 };
 

@@ -6,7 +6,10 @@
 // no other change.  The program builds an index with the reference's own
 // offline builder (lir::build_index), runs both searchers on the same queries
 // and prints one line per query:  "<q> <k> <ids_equal> <score_bits_equal>
-// <trace_equal>", then "OK" when everything matched (EXACT score mode) —
+// <trace_equal> sharded <bit-exact> tensor <within tolerance>", then "OK"
+// when everything matched: plaid_lir::Engine in EXACT mode and
+// plaid_lir::ShardedEngine (three passage shards, global-exact) bit for bit,
+// the TENSOR default within north_star's tolerance —
 // tests/test_gpu_parity.py runs it on the GPU box.  Without a GPU the Engine
 // constructor throws (no CPU fallback) and the program prints "NOGPU".
 #include <cmath>
@@ -50,6 +53,10 @@ int main() {
 
     try {
         const plaid_lir::Engine engine(index, 0, PLAID_SCORES_EXACT, /*validate=*/true);
+        // the production default (tcgen05 S_cq + stage 4) and the multi-GPU
+        // drop-in (three passage shards; all on GPU 0 here)
+        const plaid_lir::Engine tensor(index, 0, PLAID_SCORES_TENSOR);
+        const plaid_lir::ShardedEngine sharded(index, {0, 0, 0}, PLAID_SCORES_EXACT, /*global_exact=*/true);
         bool all = true;
         for (int qi = 0; qi < 4; ++qi) {
             lir::QueryMatrix q;
@@ -81,8 +88,33 @@ int main() {
                                 x.stage2_rows_gathered == y.stage2_rows_gathered &&
                                 x.stage3_rows_gathered == y.stage3_rows_gathered &&
                                 x.decompressed_passages == y.decompressed_passages;
-                std::printf("%d %zu %d %d %d\n", qi, k, int(ids), int(sc), int(tr));
-                all = all && ids && sc && tr;
+                // sharded: the same bits and counters as lir::search
+                const lir::SearchResult c = sharded.search(q, p);
+                bool sh = c.topk.passage_ids == a.topk.passage_ids && c.topk.scores && a.topk.scores &&
+                          c.topk.scores->size() == a.topk.scores->size();
+                for (std::size_t j = 0; sh && j < a.topk.scores->size(); ++j)
+                    sh = std::memcmp(&(*a.topk.scores)[j], &(*c.topk.scores)[j], 4) == 0;
+                sh = sh && c.trace.stage1_candidates == x.stage1_candidates && c.trace.stage2_out == x.stage2_out &&
+                     c.trace.stage3_out == x.stage3_out && c.trace.stage2_rows_gathered == x.stage2_rows_gathered &&
+                     c.trace.stage3_rows_gathered == x.stage3_rows_gathered;
+                // tensor: every returned score within 1e-4 relative of the
+                // reference's score of the same pid, the top-k equal up to
+                // near-ties (at most 2 swapped at the boundary)
+                const lir::SearchResult t = tensor.search(q, p);
+                std::size_t common = 0;
+                bool tol = t.topk.scores && a.topk.scores;
+                for (std::size_t j = 0; tol && j < t.topk.passage_ids.size(); ++j)
+                    for (std::size_t m = 0; m < a.topk.passage_ids.size(); ++m)
+                        if (a.topk.passage_ids[m] == t.topk.passage_ids[j]) {
+                            ++common;
+                            const float ra = (*a.topk.scores)[m], rt = (*t.topk.scores)[j];
+                            tol = tol && std::fabs(rt - ra) <= 1e-4f * std::fabs(ra);
+                        }
+                const bool ten = tol && common + 2 >= a.topk.passage_ids.size() &&
+                                 t.topk.passage_ids.size() == a.topk.passage_ids.size();
+                std::printf("%d %zu %d %d %d sharded %d tensor %d\n", qi, k, int(ids), int(sc), int(tr), int(sh),
+                            int(ten));
+                all = all && ids && sc && tr && sh && ten;
             }
         }
         // errors keep their lir::ErrorCode across the boundary
