@@ -404,6 +404,9 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         if (tensor_) launch::make_centroid_tensor_map(ix, tmap_);
         if (tensor_ && ix.tok_inv) qimg_.ensure(launch::kQImgBytes / 4);
     }
+    // the zero fills above run on the legacy default stream, which does not
+    // order the searcher's non-blocking streams: finish them before any search
+    PLAID_CUDA(cudaDeviceSynchronize());
 }
 
 uint32_t Searcher::launch_scores(const float* d_q, uint32_t rows, float t_cs, uint32_t npb, cudaStream_t st) {
@@ -433,6 +436,15 @@ void Searcher::require_index() const {
 }
 
 void Searcher::ensure_param_buffers(const plaid_params& p) {
+    // buffers that grow here are zero-filled on the legacy default stream
+    // (cudaMemset), which does NOT order the non-blocking stream the search
+    // runs on: wait for the fills before enqueueing (growth is rare)
+    const uint64_t gen0 = g_alloc_generation.load();
+    ensure_param_buffers_impl(p);
+    if (g_alloc_generation.load() != gen0) PLAID_CUDA(cudaDeviceSynchronize());
+}
+
+void Searcher::ensure_param_buffers_impl(const plaid_params& p) {
     const IndexView& ix = index_->view();
     const uint64_t K = ix.K, N = ix.N;
     const uint64_t nsel = p.nprobe == K ? K : 32 * std::max<uint64_t>(p.nprobe, 32);
@@ -899,6 +911,7 @@ void Searcher::sync() {
     PLAID_CUDA(cudaMemcpy(&status, status_.p, sizeof(int), cudaMemcpyDeviceToHost));
     if (status) {
         PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
+        PLAID_CUDA(cudaDeviceSynchronize());
         fail(status, "device-side query validation failed (row not unit norm)");
     }
 }

@@ -167,6 +167,7 @@ private:
     void enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,
                       uint64_t* d_n, cudaStream_t st, bool times);
     void ensure_param_buffers(const plaid_params& p);
+    void ensure_param_buffers_impl(const plaid_params& p);
     void ensure_result_block(uint64_t k);
     void record(int slot, cudaStream_t st, bool times);
 
