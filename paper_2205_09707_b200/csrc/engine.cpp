@@ -445,6 +445,10 @@ void Searcher::ensure_param_buffers(const plaid_params& p) {
 }
 
 void Searcher::ensure_param_buffers_impl(const plaid_params& p) {
+    // first: the result block holds the counters, and pointers into it are
+    // cached below (rank_scratch_.tokens) — growing it later would leave them
+    // pointing at the freed block
+    ensure_result_block(p.k);
     const IndexView& ix = index_->view();
     const uint64_t K = ix.K, N = ix.N;
     const uint64_t nsel = p.nprobe == K ? K : 32 * std::max<uint64_t>(p.nprobe, 32);
@@ -476,7 +480,6 @@ void Searcher::ensure_param_buffers_impl(const plaid_params& p) {
         }
     }
     tmp_keys_.ensure(std::max<uint64_t>(std::min<uint64_t>(p.k, N), std::min<uint64_t>(p.nprobe, K)));
-    ensure_result_block(p.k);
     uint64_t tmp = 0;
     tmp = std::max(tmp, launch::sort_tmp_capacity(nd));
     tmp = std::max(tmp, launch::sort_tmp_capacity(std::min<uint64_t>(p.k, N)));

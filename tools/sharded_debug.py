@@ -33,4 +33,12 @@ for k in (10, 100, 1000):
                 bad += 1
                 diff = {kk: (c[kk], tr[kk]) for kk in tr if c[kk] != tr[kk]}
                 print(f"k={k} q={qi} rep={rep}: ids_equal={np.array_equal(got.topk.passage_ids, ids)} diff={diff}")
+                gi, gs = got.topk.passage_ids, got.topk.scores
+                print("  lens", len(gi), len(ids), "missing", sorted(set(ids.tolist()) - set(gi.tolist()))[:10],
+                      "extra", sorted(set(gi.tolist()) - set(ids.tolist()))[:10])
+                w = np.nonzero(gi[:min(len(gi), len(ids))] != ids[:min(len(gi), len(ids))])[0]
+                for j in w[:6]:
+                    print("   pos", j, "got", gi[j], gs[j], "exp", ids[j], sc[j])
+                for j in np.nonzero(gs[:len(sc)] != sc[:len(gs)])[0][:4]:
+                    print("   score pos", j, gs[j], sc[j])
 print("mismatches", bad)
