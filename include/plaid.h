@@ -161,6 +161,26 @@ plaid_status plaid_index_from_host_at(const plaid_index_desc* desc, uint64_t pid
  * local ids; search results report global ids (local + pid_begin). */
 plaid_status plaid_index_from_host_shard(const plaid_index_desc* desc, uint64_t pid_begin,
                                          uint64_t pid_end, int device, plaid_index** out);
+/* The synthetic benchmark corpus generated directly in HBM:
+ * passages [pid_base, pid_base + num_passages) of the corpus the host
+ * generator defines (same SplitMix64 streams: identical integer arrays),
+ * local IVF built on the device, results report global ids.  For corpora
+ * that do not fit host memory (BASELINE configs[4]: 140M passages, ~45 GB
+ * per shard of 8).  Fixture infrastructure, not part of the lir API. */
+typedef struct plaid_synth_desc {
+    uint64_t num_passages, num_centroids, pid_base, seed;
+    uint32_t dim, nbits, mean_len, spread;
+    double repeat;  /* probability that a token repeats an earlier code of its passage */
+} plaid_synth_desc;
+plaid_status plaid_index_synth(const plaid_synth_desc* desc, int device, plaid_index** out);
+/* nq x qlen x dim unit-norm queries near reconstructed tokens of the index
+ * (the host generator's query recipe), into host memory. */
+plaid_status plaid_index_synth_queries(plaid_index* index, uint64_t nq, uint32_t qlen, double noise, uint64_t seed,
+                                       float* out);
+/* Copies the device arrays back (any pointer may be NULL); sizes from plaid_index_info. */
+plaid_status plaid_index_export(plaid_index* index, float* centroids, uint32_t* codes, uint8_t* residuals,
+                                uint32_t* doclens, uint64_t* ivf_offsets, uint32_t* ivf_postings, float* cutoffs,
+                                float* weights);
 /* Re-checks validate_index's invariants on the device copy (index.cpp:12-84). */
 plaid_status plaid_index_validate(plaid_index* index);
 void plaid_index_close(plaid_index* index);

@@ -47,6 +47,12 @@ class EncodeDesc(C.Structure):
                 ("doclens", C.c_void_p), ("centroids", C.c_void_p), ("bucket_cutoffs", C.c_void_p)]
 
 
+class SynthDesc(C.Structure):
+    _fields_ = [("num_passages", C.c_uint64), ("num_centroids", C.c_uint64), ("pid_base", C.c_uint64),
+                ("seed", C.c_uint64), ("dim", C.c_uint32), ("nbits", C.c_uint32), ("mean_len", C.c_uint32),
+                ("spread", C.c_uint32), ("repeat", C.c_double)]
+
+
 class SearcherConfig(C.Structure):
     _fields_ = [("score_mode", C.c_int32), ("record_times", C.c_int32),
                 ("use_graphs", C.c_int32), ("reserved", C.c_int32)]
@@ -132,6 +138,10 @@ SIGNATURES = {
     "plaid_sharded_search": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(Params),
                                        C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(Trace)]),
     "plaid_sharded_last_launches": (C.c_uint64, [C.c_void_p]),
+    "plaid_index_synth": (C.c_int, [C.POINTER(SynthDesc), C.c_int, C.POINTER(C.c_void_p)]),
+    "plaid_index_synth_queries": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_double, C.c_uint64,
+                                            C.c_void_p]),
+    "plaid_index_export": (C.c_int, [C.c_void_p] + [C.c_void_p] * 8),
     # test knobs (not part of include/plaid.h)
     "plaid_debug_set_tf32_grid": (C.c_uint32, [C.c_uint32]),
 }

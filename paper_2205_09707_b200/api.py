@@ -268,6 +268,42 @@ class DeviceIndex:
         _check(N.load().plaid_index_open(str(path).encode(), device, flags, C.byref(out)))
         return cls(out.value)
 
+    @classmethod
+    def synth(cls, num_passages: int, num_centroids: int, dim: int = 128, nbits: int = 2, mean_len: int = 64,
+              spread: int = 16, repeat: float = 0.28, seed: int = 0, pid_base: int = 0,
+              device: int = 0) -> "DeviceIndex":
+        """The synthetic corpus of generate_index (same arguments, same integer
+        arrays) generated directly in HBM: passages [pid_base, pid_base + N)
+        with a local IVF and global ids in results (plaid_index_synth)."""
+        d = N.SynthDesc(int(num_passages), int(num_centroids), int(pid_base), int(seed), int(dim), int(nbits),
+                        int(mean_len), int(spread), float(repeat))
+        out = C.c_void_p()
+        _check(N.load().plaid_index_synth(C.byref(d), device, C.byref(out)))
+        return cls(out.value)
+
+    def synth_queries(self, num_queries: int, qlen: int = 32, noise: float = 0.03, seed: int = 1234) -> np.ndarray:
+        """generate_queries' recipe on the device-resident index."""
+        out = np.empty((num_queries, qlen, self.dim), dtype=np.float32)
+        _check(N.load().plaid_index_synth_queries(self._h, num_queries, qlen, float(noise), seed, out.ctypes.data))
+        return out
+
+    def to_host(self) -> HostIndex:
+        """Download the index arrays (plaid_index_export)."""
+        nb = 1 << self.nbits
+        a = dict(centroids=np.empty((self.num_centroids, self.dim), np.float32),
+                 codes=np.empty(self.num_embeddings, np.uint32),
+                 residuals=np.empty(self.num_embeddings * self.nbits * self.dim // 8, np.uint8),
+                 doclens=np.empty(self.num_passages, np.uint32),
+                 ivf_offsets=np.empty(self.num_centroids + 1, np.uint64),
+                 ivf_postings=np.empty(max(self.num_postings, 1), np.uint32),
+                 bucket_cutoffs=np.empty(max(nb - 1, 1), np.float32), bucket_weights=np.empty(nb, np.float32))
+        order = ("centroids", "codes", "residuals", "doclens", "ivf_offsets", "ivf_postings", "bucket_cutoffs",
+                 "bucket_weights")
+        _check(N.load().plaid_index_export(self._h, *[a[k].ctypes.data for k in order]))
+        return HostIndex(self.dim, self.nbits, a["centroids"], a["codes"], a["residuals"], a["doclens"],
+                         a["ivf_offsets"], a["ivf_postings"][: self.num_postings], a["bucket_cutoffs"][: nb - 1],
+                         a["bucket_weights"])
+
     def validate(self) -> None:  # index.cpp:12-84
         _check(N.load().plaid_index_validate(self._h))
 

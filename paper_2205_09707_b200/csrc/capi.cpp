@@ -580,4 +580,48 @@ plaid_status plaid_sharded_search(plaid_sharded* s, const float* q, uint64_t row
 
 uint64_t plaid_sharded_last_launches(const plaid_sharded* s) { return s ? s->impl->last_launches() : 0; }
 
+plaid_status plaid_index_synth(const plaid_synth_desc* desc, int device, plaid_index** out) {
+    return guarded([&] {
+        need(desc, "desc");
+        need(out, "out");
+        *out = nullptr;
+        plaid::SynthSpec sp;
+        sp.num_passages = desc->num_passages;
+        sp.num_centroids = desc->num_centroids;
+        sp.pid_base = desc->pid_base;
+        sp.seed = desc->seed;
+        sp.dim = desc->dim;
+        sp.nbits = desc->nbits;
+        sp.mean_len = desc->mean_len;
+        sp.spread = desc->spread;
+        sp.repeat = desc->repeat;
+        auto* h = new plaid_index();
+        try {
+            h->impl = std::make_unique<plaid::DeviceIndex>(sp, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+plaid_status plaid_index_synth_queries(plaid_index* index, uint64_t nq, uint32_t qlen, double noise, uint64_t seed,
+                                       float* out) {
+    return guarded([&] {
+        need(index, "index");
+        need(out, "out");
+        index->impl->synth_queries(nq, qlen, noise, seed, out);
+    });
+}
+
+plaid_status plaid_index_export(plaid_index* index, float* centroids, uint32_t* codes, uint8_t* residuals,
+                                uint32_t* doclens, uint64_t* ivf_offsets, uint32_t* ivf_postings, float* cutoffs,
+                                float* weights) {
+    return guarded([&] {
+        need(index, "index");
+        index->impl->export_host(centroids, codes, residuals, doclens, ivf_offsets, ivf_postings, cutoffs, weights);
+    });
+}
+
 }  // extern "C"

@@ -54,9 +54,22 @@ void default_params_for_k(uint64_t k, plaid_params* out);
 uint64_t stage3_width(const plaid_params& p);
 void validate_index_host(const plaid_index_desc& d);
 
+// The synthetic index recipe of SURVEY.md §8d (plaid_index_synth).
+struct SynthSpec {
+    uint64_t num_passages = 0, num_centroids = 0, pid_base = 0, seed = 0;
+    uint32_t dim = 128, nbits = 2, mean_len = 64, spread = 16;
+    double repeat = 0.28;
+};
+
 class DeviceIndex {
 public:
     DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_base);
+    // Generated in HBM (synth_device.cu): passages [pid_base, pid_base + N)
+    // of the synthetic corpus, local IVF, global ids in results.
+    DeviceIndex(const SynthSpec& spec, int device);
+    void synth_queries(uint64_t nq, uint32_t qlen, double noise, uint64_t seed, float* out_host) const;
+    void export_host(float* centroids, uint32_t* codes, uint8_t* residuals, uint32_t* doclens, uint64_t* ivf_offsets,
+                     uint32_t* ivf_postings, float* cutoffs, float* weights) const;
     ~DeviceIndex();
     DeviceIndex(const DeviceIndex&) = delete;
     DeviceIndex& operator=(const DeviceIndex&) = delete;
