@@ -51,6 +51,12 @@ CONFIGS = {
     "cfg4": dict(N=2_400_000, K=1 << 16, nbits=2, mean_len=136, k=10,
                  desc="synthetic LoTTE-pooled-scale: 2.4M passages, 2^16 centroids, nbits=2, k=10, ndocs=256"),
     "small": dict(N=200_000, K=1 << 14, nbits=2, mean_len=68, k=1000, desc="smoke-size index"),
+    # N is the WHOLE corpus here: 8 passage-range shards of 17.5M (~1.25B
+    # embeddings, ~56 GB each) generated in HBM; rank r holds shard r, so at
+    # N < 8 GPUs the line measures the per-GPU load of the 8-GPU deployment
+    "cfg5": dict(N=140_000_000, K=1 << 20, nbits=2, mean_len=71, k=1000, shards=8, slice_N=200_000,
+                 desc="synthetic MS MARCO v2-scale: 140M passages (~10B embeddings) in 8 passage shards of 17.5M, "
+                      "2^20 centroids, nbits=2, k=1000, NCCL top-k merge"),
 }
 METRIC = "queries/sec @k=1000 & p50 latency vs HBM/tensor roofline, 1/2/4/8 B200"
 QLEN, DIM = 32, 128
@@ -234,8 +240,20 @@ def run_reference(args, cfg):
     from oracle import synth
 
     ref, flags = oracle.timed_reference()
+    n_ref, note = cfg["N"], ""
+    if cfg.get("shards"):
+        # the whole corpus (~390 GB) does not fit host memory: the reference
+        # searches shard 0 of 8 (what one GPU holds), when that fits
+        n_ref = cfg["N"] // int(cfg["shards"])
+        need = 2.5 * n_ref * cfg["mean_len"] * (4 + 16 * cfg["nbits"] + 4)
+        avail = host_mem_available()
+        if avail < need:
+            print(json.dumps({"impl": "reference", "unavailable": f"{args.config} shard needs ~{need / 1e9:.0f} GB of "
+                                                                  f"host memory, {avail / 1e9:.0f} GB available"}))
+            return
+        note = f" (shard 0 of {cfg['shards']}: {n_ref} passages)"
     t = time.time()
-    h = synth.generate_index(cfg["N"], cfg["K"], dim=DIM, nbits=cfg["nbits"], mean_len=cfg["mean_len"],
+    h = synth.generate_index(n_ref, cfg["K"], dim=DIM, nbits=cfg["nbits"], mean_len=cfg["mean_len"],
                              spread=16, seed=0, ivf=ref.build_inverted_list)
     log(f"[reference] generated index: N={h.num_passages} T={h.num_embeddings} ({h.nbytes() / 1e9:.1f} GB) "
         f"in {time.time() - t:.1f}s")
@@ -261,6 +279,7 @@ def run_reference(args, cfg):
         total = sum(lat)
         qps = args.steps / total
         sample = f"{args.steps} sequential queries, lir::search latency mode, SearchOptions.threads={threads}"
+    sample += note
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
@@ -273,6 +292,16 @@ def run_reference(args, cfg):
         "repo_libs_mapped": repo_libs_mapped(),
     }
     print(json.dumps(line))
+
+
+def host_mem_available() -> float:
+    try:
+        for line in Path("/proc/meminfo").read_text().splitlines():
+            if line.startswith("MemAvailable:"):
+                return float(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0.0
 
 
 def repo_libs_mapped() -> list:
@@ -290,8 +319,16 @@ def repo_libs_mapped() -> list:
 
 
 def config_block(cfg, params, args, world):
-    return {"workload": f"{args.config}: {cfg['desc']}", "passages_per_gpu": cfg["N"],
-            "passages_total": cfg["N"] * world, "centroids": cfg["K"], "nbits": cfg["nbits"], "dim": DIM,
+    shards = int(cfg.get("shards", 0))
+    per_gpu = cfg["N"] // shards if shards else cfg["N"]
+    extra = {}
+    if shards:
+        extra = {"corpus_passages": cfg["N"], "corpus_shards": shards,
+                 "scaling_note": (f"rank r holds shard r of {shards} (generated in HBM); with {world} GPU(s) the "
+                                  f"line covers {world}/{shards} of the corpus at the per-GPU load of the "
+                                  f"{shards}-GPU deployment" if world < shards else "the whole corpus")}
+    return {"workload": f"{args.config}: {cfg['desc']}", "passages_per_gpu": per_gpu,
+            "passages_total": per_gpu * world, **extra, "centroids": cfg["K"], "nbits": cfg["nbits"], "dim": DIM,
             "query_tokens": QLEN, "k": params.k, "nprobe": params.nprobe, "t_cs": params.t_cs,
             "ndocs": params.ndocs, "batch": cfg.get("batch", 1),
             "lanes": args.lanes if cfg.get("batch", 1) > 1 else None,
@@ -323,22 +360,34 @@ def run_plaid(args, cfg):
         else:
             dist.init_process_group(backend)
 
-    h = make_index(cfg, rank)
     params = params_for(cfg)
     nq = max(args.steps + args.warmup, 8)
+    shards = int(cfg.get("shards", 0))
+    t = time.time()
+    if shards:
+        # a shard of a corpus too large for host memory: generated in HBM
+        if world > shards:
+            raise SystemExit(f"{args.config} has {shards} shards; run it on at most {shards} GPUs")
+        n_shard = cfg["N"] // shards
+        h = None
+        idx = P.DeviceIndex.synth(n_shard, cfg["K"], dim=DIM, nbits=cfg["nbits"], mean_len=cfg["mean_len"],
+                                  spread=16, seed=0, pid_base=rank * n_shard, device=local)
+        num_passages = world * n_shard
+    else:
+        h = make_index(cfg, rank)
+        idx = P.DeviceIndex.from_host_at(h, pid_base=rank * cfg["N"], device=local)
+        num_passages = cfg["N"] * world
+    log(f"[rank {rank}] index resident on cuda:{local}: {idx.device_bytes / 1e9:.1f} GB in {time.time() - t:.1f}s")
     # queries: generated from shard 0's passages, identical on every rank
     if rank == 0:
-        qs = P.generate_queries(h, nq, qlen=QLEN, seed=1234)
+        qs = (idx.synth_queries(nq, qlen=QLEN, seed=1234) if h is None
+              else P.generate_queries(h, nq, qlen=QLEN, seed=1234))
     else:
         qs = np.zeros((nq, QLEN, DIM), dtype=np.float32)
     dq = torch.from_numpy(qs).cuda()
     if dist is not None:
         dist.broadcast(dq, 0)
         qs = dq.cpu().numpy()
-
-    t = time.time()
-    idx = P.DeviceIndex.from_host_at(h, pid_base=rank * cfg["N"], device=local)
-    log(f"[rank {rank}] index resident on cuda:{local}: {idx.device_bytes / 1e9:.1f} GB in {time.time() - t:.1f}s")
     mode = P.ScoreMode.EXACT if args.score_mode == "exact" else P.ScoreMode.TENSOR
     # the timed searcher records no phase events (an event between two kernels
     # breaks their programmatic-dependent-launch overlap); a second searcher
@@ -359,7 +408,7 @@ def run_plaid(args, cfg):
         from paper_2205_09707_b200.sharded import ShardedSearcher
 
         ss = ShardedSearcher(s, k, device=torch.device("cuda", local), mode=args.shard_mode,
-                             num_passages=cfg["N"] * world)
+                             num_passages=num_passages)
         m_pids, m_scores = ss.out_pids, ss.out_scores
     flush = L2Flush(args.flush)
 
@@ -463,9 +512,23 @@ def run_plaid(args, cfg):
     t4 = trace.decompressed_tokens if trace is not None else 0
     step_mean_ms = 1e3 * total_s / args.steps
     calib, parity = None, None
+    h_chk, qs_chk, s_chk, first_chk = h, qs, s, args.warmup
+    if world == 1 and not args.no_cpu and h is None:
+        # the shard has no host copy: check and baseline on a slice of the
+        # same corpus (same K, generator and queries recipe), state it
+        ns = int(cfg["slice_N"])
+        ix_slice = P.DeviceIndex.synth(ns, cfg["K"], dim=DIM, nbits=cfg["nbits"], mean_len=cfg["mean_len"],
+                                       spread=16, seed=0, pid_base=0, device=local)
+        h_chk = ix_slice.to_host()
+        qs_chk = ix_slice.synth_queries(max(args.check, 1) + 3, qlen=QLEN, seed=1234)
+        s_chk = P.Searcher(ix_slice, device=local, score_mode=mode)
+        first_chk = 0
     if world == 1 and not args.no_cpu:
         try:
-            calib, parity = check_and_calibrate(args, h, qs, params, s, args.warmup)
+            calib, parity = check_and_calibrate(args, h_chk, qs_chk, params, s_chk, first_chk)
+            if h is None:
+                calib["scope"] = parity["scope"] = (f"slice: passages [0, {len(h_chk.doclens)}) of the same corpus, "
+                                                    f"K = {cfg['K']} (the measured shard has no host copy)")
         except Exception as e:  # noqa: BLE001
             parity = {"error": repr(e)}
 
@@ -478,7 +541,7 @@ def run_plaid(args, cfg):
     roofs["scores"] = roof_line("scores_tf32_kernel" if args.score_mode == "tensor" else "scores_exact_kernel",
                                 ab_scq, mean_ph["scores"], hbm_peak, peak_kind, step_mean_ms, args.config,
                                 "512 B x K centroid rows + 16 KiB Q (SURVEY.md §8d)")
-    if calib:
+    if calib and h is not None:
         n3 = calib["n3"]
         ab4 = (4 + 16 * cfg["nbits"]) * calib["T4"] + 12 * n3 + 512 * calib["U4"]
         k4 = "stage4_tensor_kernel" if args.score_mode == "tensor" else "stream_fused_kernel"
@@ -493,7 +556,7 @@ def run_plaid(args, cfg):
 
     # ---- whole-query roofline: t_roof = FLOPs_Scq / P_tc + B_alg / BW
     rq = None
-    if calib:
+    if calib and h is not None:
         # 3xTF32 = three tf32 MMA passes; tf32 dense rate = half the measured bf16 rate
         p_tc = (tf_sust if tf_sust else tf_peak) / 2 * 1e12
         flops = 3 * 2.0 * K * DIM * QLEN
@@ -514,15 +577,17 @@ def run_plaid(args, cfg):
             threads = os.cpu_count() or 1
             per_q = 0.5 if cfg["N"] > 1_000_000 else 0.02
             nsample = max(3, min(64, int(args.cpu_seconds / per_q)))
-            lat = cpu_reference_run(h, qs, params, nsample, 1, threads, ref)
-            tput, ntp = cpu_reference_throughput(h, qs, params, threads, ref)
-            ref.release(h)
+            lat = cpu_reference_run(h_chk, qs_chk, params, nsample, 1, threads, ref)
+            tput, ntp = cpu_reference_throughput(h_chk, qs_chk, params, threads, ref)
+            ref.release(h_chk)
             cpu = {"value": nsample / sum(lat), "unit": "queries/s", "cores": threads, "kind": "reference",
                    "sample": f"{nsample} sequential queries of the same workload, lir::search latency mode, "
                              f"SearchOptions.threads={threads}", "p50_ms": 1e3 * statistics.median(lat),
                    "throughput_mode": {"value": tput, "unit": "queries/s", "queries": ntp,
                                        "how": f"{threads} concurrent lir::search calls, SearchOptions.threads=1"},
                    "cpu_model": cpu_model(), "build": flags}
+            if h is None:
+                cpu["sample"] += f" ({calib['scope'] if calib else 'slice of the corpus'})"
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}

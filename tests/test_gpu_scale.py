@@ -160,3 +160,18 @@ def test_batch_tensor_vs_reference(cfg1, best, lanes):
             S, _ = single.compute_centroid_scores(q)
             rep = check_tensor_search(best, h, q, p, g.passage_ids, g.scores, S)
             assert rep.ok, rep.as_dict()
+
+
+def test_k2pow20_tensor_scores(best):
+    """BASELINE configs[4]'s centroid table (K = 2^20, ~55 tiles per CTA):
+    the tcgen05 S_cq within 5e-6 of the reference's in-order dots, and a
+    search through it classified against lir::search."""
+    h = P.generate_index(20_000, 1 << 20, dim=128, nbits=2, mean_len=71, seed=23)
+    qs = P.generate_queries(h, 2, seed=9)
+    idx = P.DeviceIndex.from_host(h)
+    s = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
+    for q in qs:
+        S, _ = s.compute_centroid_scores(q)
+        S0, _ = best.compute_centroid_scores(h, q)
+        assert np.abs(S - S0).max() < 5e-6
+    _check(best, h, qs[0], P.default_params_for_k(1000), s)
