@@ -620,8 +620,23 @@ def run_plaid(args, cfg):
 
 
 def cpp_e2e(args, cfg):
-    """e2e through the C++ drop-in binding (include/plaid_lir.hpp): see tools/e2e_cpp.cpp."""
-    return None
+    """e2e through the C++ drop-in (include/plaid_lir.hpp, tools/e2e_cpp.cpp):
+    a C++ program on lir types builds the same corpus and times
+    plaid_lir::Engine::search per query with host buffers (subprocess; the GPU
+    index of this process stays resident)."""
+    exe = ROOT / "oracle" / "_ref" / "e2e_cpp"
+    if not exe.exists() or cfg.get("shards") or cfg.get("batch", 1) > 1:
+        return None
+    cmd = [str(exe), str(cfg["N"]), str(cfg["K"]), str(cfg["nbits"]), str(cfg["mean_len"]), str(cfg["k"]),
+           str(args.steps), str(max(args.warmup, 3)), "1" if args.score_mode == "tensor" else "0"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        out["h2d_bytes_per_step"] = QLEN * DIM * 4
+        out["d2h_bytes_per_step"] = int(cfg["k"]) * 8 + 128
+        return out
+    except Exception as e:  # noqa: BLE001
+        return {"error": repr(e)[:200]}
 
 
 def measured_tensor_sustained():

@@ -98,7 +98,7 @@ def build_all(verbose: bool = False) -> None:
     build_plaid(verbose)
     if Path("/root/reference/proj/src").is_dir():
         # drop-in demonstration: reference lir code calling libplaid (test infra)
-        _run(["make", "-s", "-C", str(ROOT / "oracle"), "dropin"], verbose)
+        _run(["make", "-s", "-C", str(ROOT / "oracle"), "dropin", "e2e"], verbose)
 
 
 if __name__ == "__main__":
