@@ -251,6 +251,32 @@ typedef struct plaid_encode_desc {
 plaid_status plaid_encode(const plaid_encode_desc* in, int device, uint32_t* codes, uint8_t* residuals,
                           uint64_t* ivf_offsets, uint32_t* ivf_postings, uint64_t postings_cap, uint64_t* num_postings);
 
+/* ---- full index build on the GPU: lir::build_index (indexer.cpp:197-282) --------------
+ * Training sample (uniform, <= 2^20 rows, seeded partial Fisher-Yates), k-means++
+ * seeding and Lloyd iterations (kmeans.cpp:78-175), assign_codes, the quantizer
+ * fit (indexer.cpp:74-147), residual packing and the IVF — bit-identical to
+ * the reference's build for the same corpus, config and seed.  The heavy loops
+ * (seeding dots, every T x K assignment, the mean sums) run on the GPU; the
+ * seed-driven sequential choices (k-means++ picks, empty-cluster repair, the
+ * quantizer's pool statistics) stay on the host in the reference's order.
+ * num_centroids 0 = auto_num_centroids (2^ceil(log2(T)/2)); centroids_cap
+ * rows must hold the resulting K (checked); ivf_offsets has K + 1 entries. */
+typedef struct plaid_build_desc {
+    uint32_t dim;
+    uint32_t nbits;
+    uint64_t num_passages;     /* N */
+    uint64_t num_embeddings;   /* T = sum(doclens) */
+    const float* embeddings;   /* T x dim, unit rows */
+    const uint32_t* doclens;   /* N */
+    uint64_t num_centroids;    /* 0 = auto */
+    uint64_t kmeans_iters;     /* IndexConfig::kmeans_iters (reference default 20) */
+    uint64_t rng_seed;         /* IndexConfig::rng_seed (reference default 42) */
+} plaid_build_desc;
+plaid_status plaid_build_index(const plaid_build_desc* in, int device, float* centroids, uint64_t centroids_cap,
+                               uint64_t* num_centroids, float* bucket_cutoffs, float* bucket_weights, uint32_t* codes,
+                               uint8_t* residuals, uint64_t* ivf_offsets, uint32_t* ivf_postings, uint64_t postings_cap,
+                               uint64_t* num_postings);
+
 /* ---- throughput mode (BASELINE configs[2]: batched queries) ---------------------------
  * `lanes` searchers (own CUDA stream + scratch each) over one index; query j of
  * a batch runs on lane j mod lanes, so the stages of different queries overlap

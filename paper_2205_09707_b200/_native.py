@@ -53,6 +53,12 @@ class SynthDesc(C.Structure):
                 ("spread", C.c_uint32), ("repeat", C.c_double)]
 
 
+class BuildDesc(C.Structure):
+    _fields_ = [("dim", C.c_uint32), ("nbits", C.c_uint32), ("num_passages", C.c_uint64),
+                ("num_embeddings", C.c_uint64), ("embeddings", C.c_void_p), ("doclens", C.c_void_p),
+                ("num_centroids", C.c_uint64), ("kmeans_iters", C.c_uint64), ("rng_seed", C.c_uint64)]
+
+
 class SearcherConfig(C.Structure):
     _fields_ = [("score_mode", C.c_int32), ("record_times", C.c_int32),
                 ("use_graphs", C.c_int32), ("reserved", C.c_int32)]
@@ -142,6 +148,9 @@ SIGNATURES = {
     "plaid_index_synth_queries": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_double, C.c_uint64,
                                             C.c_void_p]),
     "plaid_index_export": (C.c_int, [C.c_void_p] + [C.c_void_p] * 8),
+    "plaid_build_index": (C.c_int, [C.POINTER(BuildDesc), C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_uint64, C.POINTER(C.c_uint64)]),
     # test knobs (not part of include/plaid.h)
     "plaid_debug_set_tf32_grid": (C.c_uint32, [C.c_uint32]),
 }

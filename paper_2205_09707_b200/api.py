@@ -214,6 +214,33 @@ def encode_corpus(embeddings: np.ndarray, doclens: np.ndarray, centroids: np.nda
                      np.ascontiguousarray(bucket_weights, dtype=np.float32))
 
 
+def build_index(embeddings: np.ndarray, doclens: np.ndarray, nbits: int = 2, num_centroids: int = 0,
+                iters: int = 20, seed: int = 42, device: int = 0) -> HostIndex:
+    """lir::build_index (indexer.cpp:197-282) on the GPU: k-means, quantizer,
+    codes, residuals and IVF, bit-identical to the reference for the same
+    corpus, IndexConfig (nbits, num_centroids 0 = auto, kmeans_iters,
+    rng_seed) — plaid_build_index."""
+    x = np.ascontiguousarray(embeddings, dtype=np.float32)
+    dl = np.ascontiguousarray(doclens, dtype=np.uint32)
+    T, dim = x.shape
+    k = int(num_centroids) if num_centroids else (min(1 << int(np.ceil(np.log2(T) / 2.0)), T) if T else 1)
+    cents = np.empty((max(k, 1), dim), np.float32)
+    nb = 1 << nbits
+    cut = np.zeros(16, np.float32)
+    w = np.zeros(16, np.float32)
+    codes = np.empty(max(T, 1), np.uint32)
+    res = np.empty(max(T * nbits * dim // 8, 1), np.uint8)
+    ivo = np.empty(k + 1, np.uint64)
+    post = np.empty(max(T, 1), np.uint32)
+    kk, P = C.c_uint64(), C.c_uint64()
+    d = N.BuildDesc(dim, nbits, dl.size, T, x.ctypes.data, dl.ctypes.data, int(num_centroids), int(iters), int(seed))
+    _check(N.load().plaid_build_index(C.byref(d), device, cents.ctypes.data, k, C.byref(kk), cut.ctypes.data,
+                                      w.ctypes.data, codes.ctypes.data, res.ctypes.data, ivo.ctypes.data,
+                                      post.ctypes.data, post.size, C.byref(P)))
+    return HostIndex(dim, nbits, cents[: kk.value], codes[:T], res[: T * nbits * dim // 8], dl, ivo[: kk.value + 1],
+                     post[: P.value], cut[: nb - 1], w[:nb])
+
+
 def save_index(h: HostIndex, path: str, rng_seed: int = 0) -> None:
     """Write `h` in the on-disk format (FORMAT.md; SPEC.md storage module)."""
     d = _desc(h)

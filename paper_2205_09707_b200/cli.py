@@ -1,0 +1,195 @@
+"""Command-line surface of the reference's cli-bench module
+(/root/reference/SPEC.md, MODULE cli-bench) over the B200 engine.
+
+    python -m paper_2205_09707_b200.cli search  --index DIR --queries Q.npy --k K [--nprobe N --tcs T --ndocs D]
+                                                [--score-mode tensor|exact] --out results.tsv
+    python -m paper_2205_09707_b200.cli metrics --results results.tsv --qrels qrels.tsv [--cuts 10,100]
+    python -m paper_2205_09707_b200.cli selfrecall --index DIR --queries Q.npy --out curve.csv
+    python -m paper_2205_09707_b200.cli cdf     --index DIR --queries Q.npy --out cdf.csv
+    python -m paper_2205_09707_b200.cli bench   --index DIR --queries Q.npy --k K [--trials 3]
+    python -m paper_2205_09707_b200.cli index   --embeddings E.npy --doclens L.npy --nbits B [--centroids K]
+                                                [--seed S] [--iters I] --out DIR
+
+Queries are .npy arrays [nq, |Q|, dim] (query id = row); results TSV rows are
+query_id, rank (1-based), passage_id, score (6 decimals) (SPEC cmd_search).
+Exit codes 0 ok, 1 user error (a lir ErrorCode), 2 internal error.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+
+import numpy as np
+
+from . import analysis
+from .api import DeviceIndex, PlaidError, ScoreMode, SearchParams, Searcher, default_params_for_k
+from .metrics import compute_metrics, read_qrels_tsv, read_results_tsv
+
+
+def _params(a) -> SearchParams:
+    p = default_params_for_k(a.k)  # types.cpp:74-86, then explicit overrides
+    if a.nprobe is not None:
+        p.nprobe = a.nprobe
+    if a.tcs is not None:
+        p.t_cs = a.tcs
+    if a.ndocs is not None:
+        p.ndocs = a.ndocs
+    return p
+
+
+def _searcher(a, record_times=False) -> Searcher:
+    ix = DeviceIndex.open(a.index, device=a.device, validate=a.validate)
+    mode = ScoreMode.EXACT if a.score_mode == "exact" else ScoreMode.TENSOR
+    return Searcher(ix, device=a.device, score_mode=mode, record_times=record_times)
+
+
+def _queries(path) -> np.ndarray:
+    q = np.load(path).astype(np.float32, copy=False)
+    if q.ndim == 2:
+        q = q[None]
+    if q.ndim != 3:
+        raise ValueError(f"{path}: queries must be [nq, rows, dim]")
+    return q
+
+
+def cmd_search(a) -> int:
+    s = _searcher(a)
+    p = _params(a)
+    qs = _queries(a.queries)
+    with open(a.out, "w") as f:
+        for qid, q in enumerate(qs):
+            r = s.search(q, p)
+            for rank, (pid, sc) in enumerate(zip(r.topk.passage_ids, r.topk.scores), start=1):
+                f.write(f"{qid}\t{rank}\t{int(pid)}\t{float(sc):.6f}\n")
+    return 0
+
+
+def cmd_metrics(a) -> int:
+    cuts = tuple(int(c) for c in a.cuts.split(",")) if a.cuts else (10, 100)
+    rep = compute_metrics(read_results_tsv(a.results), read_qrels_tsv(a.qrels), cuts)
+    print(json.dumps(rep))
+    return 0
+
+
+def cmd_selfrecall(a) -> int:
+    s = _searcher(a)
+    rows = analysis.self_recall(s, _queries(a.queries))
+    with open(a.out, "w") as f:
+        f.write("k,kprime,recall\n")
+        for k, kp, r in rows:
+            f.write(f"{k},{kp},{r:.6f}\n")
+    return 0
+
+
+def cmd_cdf(a) -> int:
+    s = _searcher(a)
+    with open(a.out, "w") as f:
+        f.write("query_id,score,cdf\n")
+        for qid, q in enumerate(_queries(a.queries)):
+            v, c = analysis.centroid_score_cdf(s, q)
+            for x, y in zip(v, c):
+                f.write(f"{qid},{float(x):.6f},{float(y):.6f}\n")
+    return 0
+
+
+def cmd_bench(a) -> int:
+    """LatencyBreakdown (SPEC cmd_bench): per stage, the minimum over trials of
+    the mean over queries (§6.1 protocol), from CUDA events on the stages."""
+    s = _searcher(a, record_times=True)
+    p = _params(a)
+    qs = _queries(a.queries)
+    s.search(qs[0], p)  # warm-up
+    fields = ("candidate_generation_ms", "stage2_ms", "stage3_ms", "lookup_ms", "decompression_ms", "scoring_ms",
+              "total_ms")
+    best = None
+    for _ in range(a.trials):
+        acc = {f: 0.0 for f in fields}
+        for q in qs:
+            tr = s.search(q, p).trace
+            for f in fields:
+                acc[f] += getattr(tr, f)
+        mean = {f: v / len(qs) for f, v in acc.items()}
+        best = mean if best is None else {f: min(best[f], mean[f]) for f in fields}
+    best["filtering_ms"] = best["stage2_ms"] + best["stage3_ms"]
+    best.update(trials=a.trials, queries=len(qs), k=p.k)
+    print(json.dumps(best))
+    return 0
+
+
+def cmd_index(a) -> int:
+    from .api import build_index, save_index
+
+    emb = np.load(a.embeddings).astype(np.float32, copy=False)
+    doclens = np.load(a.doclens).astype(np.uint32, copy=False)
+    h = build_index(emb, doclens, nbits=a.nbits, num_centroids=a.centroids, iters=a.iters, seed=a.seed,
+                    device=a.device)
+    save_index(h, a.out, rng_seed=a.seed)
+    print(json.dumps({"out": a.out, "passages": h.num_passages, "embeddings": h.num_embeddings,
+                      "centroids": h.num_centroids, "nbits": h.nbits, "postings": int(h.ivf_postings.size)}))
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="plaid")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+
+    def common(p, index=True):
+        if index:
+            p.add_argument("--index", required=True)
+            p.add_argument("--queries", required=True)
+            p.add_argument("--score-mode", default="tensor", choices=["tensor", "exact"])
+            p.add_argument("--validate", action="store_true")
+        p.add_argument("--device", type=int, default=0)
+
+    p = sub.add_parser("search")
+    common(p)
+    p.add_argument("--k", type=int, required=True)
+    p.add_argument("--nprobe", type=int)
+    p.add_argument("--tcs", type=float)
+    p.add_argument("--ndocs", type=int)
+    p.add_argument("--threads", type=int, help="accepted for compatibility; the grid size is internal")
+    p.add_argument("--out", required=True)
+    p = sub.add_parser("metrics")
+    p.add_argument("--results", required=True)
+    p.add_argument("--qrels", required=True)
+    p.add_argument("--cuts", default="10,100")
+    for name in ("selfrecall", "cdf"):
+        p = sub.add_parser(name)
+        common(p)
+        p.add_argument("--out", required=True)
+    p = sub.add_parser("bench")
+    common(p)
+    p.add_argument("--k", type=int, required=True)
+    p.add_argument("--nprobe", type=int)
+    p.add_argument("--tcs", type=float)
+    p.add_argument("--ndocs", type=int)
+    p.add_argument("--trials", type=int, default=3)
+    p.add_argument("--threads", type=int)
+    p = sub.add_parser("index")
+    common(p, index=False)
+    p.add_argument("--embeddings", required=True)
+    p.add_argument("--doclens", required=True)
+    p.add_argument("--nbits", type=int, required=True, choices=[1, 2, 4])
+    p.add_argument("--centroids", type=int, default=0, help="0 = the reference's 16 sqrt(T) rule")
+    p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--iters", type=int, default=10)
+    p.add_argument("--out", required=True)
+    a = ap.parse_args(argv)
+    fn = {"search": cmd_search, "metrics": cmd_metrics, "selfrecall": cmd_selfrecall, "cdf": cmd_cdf,
+          "bench": cmd_bench, "index": cmd_index}[a.cmd]
+    try:
+        return fn(a)
+    except PlaidError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+    except (ValueError, FileNotFoundError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+    except Exception as e:  # noqa: BLE001
+        print(f"internal error: {e}", file=sys.stderr)
+        return 2
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -3,6 +3,7 @@
 // plaid_status with a thread-local message (lir::Error carries the same code,
 // error.hpp:51-61).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -621,6 +622,27 @@ plaid_status plaid_index_export(plaid_index* index, float* centroids, uint32_t* 
     return guarded([&] {
         need(index, "index");
         index->impl->export_host(centroids, codes, residuals, doclens, ivf_offsets, ivf_postings, cutoffs, weights);
+    });
+}
+
+plaid_status plaid_build_index(const plaid_build_desc* in, int device, float* centroids, uint64_t centroids_cap,
+                               uint64_t* num_centroids, float* bucket_cutoffs, float* bucket_weights, uint32_t* codes,
+                               uint8_t* residuals, uint64_t* ivf_offsets, uint32_t* ivf_postings, uint64_t postings_cap,
+                               uint64_t* num_postings) {
+    return guarded([&] {
+        need(in, "desc");
+        need(in->embeddings, "embeddings");
+        need(in->doclens, "doclens");
+        need(num_centroids, "num_centroids");
+        uint64_t T = 0;
+        for (uint64_t p = 0; p < in->num_passages; ++p) T += in->doclens[p];
+        if (T != in->num_embeddings) plaid::fail(PLAID_LENGTH_MISMATCH, "doclens total does not match the embedding rows");
+        uint64_t k = in->num_centroids;
+        if (!k && T) k = std::min<uint64_t>(uint64_t(1) << uint64_t(std::ceil(std::log2(double(T)) / 2.0)), T);
+        if (k > centroids_cap) plaid::fail(PLAID_INVALID_PARAMS, "centroids capacity below K = " + std::to_string(k));
+        plaid::build_index_host(in->embeddings, in->doclens, in->num_passages, in->dim, in->nbits, in->num_centroids,
+                                in->kmeans_iters, in->rng_seed, device, centroids, bucket_cutoffs, bucket_weights,
+                                num_centroids, codes, residuals, ivf_offsets, ivf_postings, postings_cap, num_postings);
     });
 }
 
