@@ -83,7 +83,7 @@ def test_cli_index_search_metrics(tmp_path):
     x /= np.linalg.norm(x, axis=1, keepdims=True)
     np.save(tmp_path / "e.npy", x)
     np.save(tmp_path / "l.npy", dl)
-    off = np.concatenate([[0], np.cumsum(dl)])
+    off = np.concatenate([[0], np.cumsum(dl.astype(np.int64))])
     src = [3, 77, 150]
     qs = []
     for p in src:
