@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 
 import numpy as np
@@ -124,6 +125,7 @@ def cmd_index(a) -> int:
     doclens = np.load(a.doclens).astype(np.uint32, copy=False)
     h = build_index(emb, doclens, nbits=a.nbits, num_centroids=a.centroids, iters=a.iters, seed=a.seed,
                     device=a.device)
+    os.makedirs(a.out, exist_ok=True)
     save_index(h, a.out, rng_seed=a.seed)
     print(json.dumps({"out": a.out, "passages": h.num_passages, "embeddings": h.num_embeddings,
                       "centroids": h.num_centroids, "nbits": h.nbits, "postings": int(h.ivf_postings.size)}))
