@@ -216,7 +216,10 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
     constexpr uint32_t kOffRaw = Cf::kOffRaw, kOffQ = Cf::kOffQ, kOffTr = Cf::kOffTr, kOffBar = Cf::kOffBar,
                        kOffMisc = Cf::kOffMisc, kQChunkBytes = Cf::kQChunkBytes, kAccCols = Cf::kAccCols,
                        kOpsCol0 = Cf::kOpsCol0;
-    dev::pdl_wait();
+    // No griddepcontrol.wait yet: C is index data no earlier kernel writes,
+    // so the TMA producer starts streaming it while the previous kernel (the
+    // query prologue, which triggers its dependents at once) still runs;
+    // every other warp waits before it touches Q, the bounds or the outputs.
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t base = smem_u32(smem);
@@ -250,6 +253,22 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&cmap)) : "memory");
     }
+    // box gb of this CTA = tile blockIdx.x + (gb / 4) * gridDim.x, lane quarter gb % 4
+    const uint64_t my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint32_t nboxes = uint32_t(my_tiles * 4);
+    auto issue_box = [&](uint32_t g) {
+        const int s = g % kRaw;
+        mbar_wait(raw_empty(s), ((g / kRaw) & 1) ^ 1);
+        trace_stamp(dbg, 0, g);
+        mbar_expect_tx(raw_full(s), kChunkBytes);
+        const uint64_t t = blockIdx.x + uint64_t(g / 4) * gridDim.x;
+        tma_load_3d(base + kOffRaw + s * kChunkBytes, &cmap, 0, int(t * 128 + (g % 4) * 32), 0, raw_full(s));
+    };
+    // the ring's first fill goes out before anything waits on earlier kernels
+    const uint32_t pre = nboxes < uint32_t(kRaw) ? nboxes : uint32_t(kRaw);
+    if (threadIdx.x == 0)
+        for (uint32_t g = 0; g < pre; ++g) issue_box(g);
+    if (warp != 0) dev::pdl_wait();
     if (threadIdx.x < 32 * QB) cthr[threadIdx.x] = 0;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -260,7 +279,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
     // Q_hi of query n / 32, token n % 32, else Q_lo; zero rows past `rows`),
     // SWIZZLE_128B K-major: row n, 16-byte granule j of chunk kc at
     // kc * kQChunkBytes + n*128 + ((j ^ (n & 7)) << 4)
-    for (uint32_t e = threadIdx.x; e < 64 * QB * (kDim / 4); e += kThreads) {
+    for (uint32_t e = threadIdx.x - 32; warp != 0 && e < 64 * QB * (kDim / 4); e += kThreads - 32) {
         const uint32_t n = e / (kDim / 4), g = e % (kDim / 4);
         const uint32_t kc = g / 8, j = g % 8, tok = n & 31, qi = (n % (32 * QB)) / 32;
         const uint4 v = tok < rows ? reinterpret_cast<const uint4*>(out.Q[qi] + uint64_t(tok) * kDim)[g]
@@ -277,20 +296,11 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer
-        if (lane == 0) {
-            // box (t, w) = centroids [128 t + 32 w, +32), all 128 dims: 16 KB
-            // contiguous in HBM, landing as [chunk][centroid][32 fp32]
-            uint32_t g = 0;
-            for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-                for (int w = 0; w < 4; ++w, ++g) {
-                    const int s = g % kRaw;
-                    mbar_wait(raw_empty(s), ((g / kRaw) & 1) ^ 1);
-                    trace_stamp(dbg, 0, g);
-                    mbar_expect_tx(raw_full(s), kChunkBytes);
-                    tma_load_3d(base + kOffRaw + s * kChunkBytes, &cmap, 0, int(t * 128 + w * 32), 0, raw_full(s));
-                }
-        }
+        // ---------------- TMA producer: box (t, w) = centroids [128 t + 32 w,
+        // +32), all 128 dims: 16 KB contiguous in HBM, landing as
+        // [chunk][centroid][32 fp32]; the first `pre` boxes went out above
+        if (lane == 0)
+            for (uint32_t g = pre; g < nboxes; ++g) issue_box(g);
     } else if (warp == 1) {
         // ---------------- MMA issuer
         uint32_t g = 0, lt = 0;

@@ -391,6 +391,10 @@ __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __rest
                                                               uint64_t n16, uint4* __restrict__ zero2, uint64_t m16,
                                                               const float* __restrict__ qsrc, uint4* __restrict__ qimg) {
     dev::pdl_wait();
+    // let the S_cq kernel launch now: its TMA producer streams the centroid
+    // table (no dependence on this kernel) while the zero fill runs; its other
+    // warps still wait for this grid to complete
+    dev::pdl_trigger();
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16 + m16;
          i += uint64_t(gridDim.x) * blockDim.x) {
         if (i < n16) zero[i] = make_uint4(0, 0, 0, 0);
