@@ -1001,6 +1001,10 @@ void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status
     const uint64_t n16 = nwords / 4, m16 = nwords2 / 4;  // both regions are multiples of 16 bytes
     const uint32_t grid = grid_for(n16 + m16, 256, uint32_t(sm_count()));
     const bool img = d_qimg && d_qsrc && dim == 128 && rows <= 32;
+    static launch::PerDeviceOnce cfg;
+    if (cfg.first())  // keep the SMs' shared-memory partition at its maximum so the
+                      // S_cq CTAs (213 KB each) can become resident beside this grid
+        cudaFuncSetAttribute(query_prologue_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     ::plaid::launch::pdl(query_prologue_kernel, grid, 256, 0, st, d_q, rows, dim, d_status,
                          reinterpret_cast<uint4*>(d_zero), n16, reinterpret_cast<uint4*>(d_zero2), m16,
                          img ? d_qsrc : nullptr, img ? reinterpret_cast<uint4*>(d_qimg) : nullptr);
