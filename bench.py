@@ -613,7 +613,14 @@ def run_plaid(args, cfg):
         "clocks": clk,
     }
     if args.cpp_e2e:
-        line["e2e_cpp"] = cpp_e2e(args, cfg)
+        # the headline e2e goes through the reference-facing drop-in (C++
+        # plaid_lir::Engine over the C ABI); the Python-API number stays beside it
+        ec = cpp_e2e(args, cfg)
+        if ec and "value" in ec:
+            line["e2e_python"] = line["e2e"]
+            line["e2e"] = ec
+        else:
+            line["e2e_cpp"] = ec
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

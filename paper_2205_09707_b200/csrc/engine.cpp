@@ -379,6 +379,10 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
     PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
     sel_state_.ensure(1);
     PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_q_), 32 * 256 * sizeof(float)));
+    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_flag_), 64));
+    *h_flag_ = 0;
+    pub_seq_.ensure(1);
+    PLAID_CUDA(cudaMemset(pub_seq_.p, 0, sizeof(uint32_t)));
     q_.ensure(32 * 256);
     if (index_) {
         const IndexView& ix = index_->view();
@@ -427,6 +431,7 @@ Searcher::~Searcher() {
         if (e) cudaEventDestroy(e);
     if (h_q_) cudaFreeHost(h_q_);
     if (h_res_) cudaFreeHost(h_res_);
+    if (h_flag_) cudaFreeHost(h_flag_);
     if (stream_) cudaStreamDestroy(stream_);
     cudaSetDevice(prev);
 }
@@ -500,7 +505,7 @@ void Searcher::ensure_result_block(uint64_t k) {
     out_scores_p_ = reinterpret_cast<float*>(res_.p + 2 * kNumCounters + kk);
     if (h_res_) cudaFreeHost(h_res_);
     h_res_ = nullptr;
-    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_res_), res_.n * sizeof(uint32_t)));
+    PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_res_), (res_.n + 3) / 4 * 4 * sizeof(uint32_t)));
 }
 
 void Searcher::record(int slot, cudaStream_t st, bool times) {
@@ -529,8 +534,11 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     // (device-resident queries) and clears the per-query counters, the
     // candidate bitmap and the stage-2 used bitmap (contiguous in zero_); the
     // "scores" phase then brackets the S_cq kernel alone
+    // host path: the prologue also copies Q from the pinned staging buffer
+    const float* qsrc = host_q_ ? host_q_ : d_q;
     launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, res_.p,
-                           2 * kNumCounters, st, d_q, rank_scratch_.qimg ? qimg_.p : nullptr);
+                           2 * kNumCounters, st, qsrc, rank_scratch_.qimg ? qimg_.p : nullptr,
+                           host_q_ ? const_cast<float*>(d_q) : nullptr);
     record(0, st, times);
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
@@ -788,6 +796,24 @@ void Searcher::phase_ms(double* out) {
     }
 }
 
+// Spin on the publish kernel's flag (every search publishes exactly once, so
+// the host's count is the value to expect); poll the stream now and then so a
+// fault surfaces instead of a hang.
+void Searcher::wait_published() {
+    const unsigned int expect = ++pub_seq_host_;
+    volatile unsigned int* flag = h_flag_;
+    for (uint64_t spins = 1; *flag != expect; ++spins) {
+        if ((spins & 4095) == 0) {
+            const cudaError_t e = cudaStreamQuery(stream_);
+            if (e == cudaSuccess && *flag != expect) {
+                pub_seq_host_ = *flag;  // resynchronise before failing
+                fail(PLAID_CUDA_ERROR, "search finished without publishing its results");
+            }
+            if (e != cudaSuccess && e != cudaErrorNotReady) PLAID_CUDA(e);
+        }
+    }
+}
+
 void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_params& p,
                       uint32_t* out_pids, float* out_scores, uint64_t* out_n, plaid_trace* trace) {
     require_index();
@@ -804,11 +830,21 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
     const bool times = trace && cfg_.record_times;
     const uint64_t kk = res_k_;
     const uint64_t words = 2 * kNumCounters + kk + p.k;
-    // H2D of Q, the launch sequence, one read-back of [counters | pids | scores]
+    // the launch sequence with Q read from the pinned staging buffer by the
+    // prologue and [counters | pids | scores] written to pinned memory by a
+    // final publish kernel, which then raises a flag the host spins on: no
+    // copy-engine round trips and no stream-synchronize wake-up on the path
+    const uint64_t pub_words = (words + 3) / 4 * 4;
     auto body = [&] {
-        PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, rows * dim * sizeof(float), cudaMemcpyHostToDevice, stream_));
-        enqueue(q_.p, uint32_t(rows), p, out_pids_p_, out_scores_p_, counters_.p + kNOut, stream_, times, false);
-        PLAID_CUDA(cudaMemcpyAsync(h_res_, res_.p, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_));
+        host_q_ = h_q_;
+        try {
+            enqueue(q_.p, uint32_t(rows), p, out_pids_p_, out_scores_p_, counters_.p + kNOut, stream_, times, false);
+        } catch (...) {
+            host_q_ = nullptr;
+            throw;
+        }
+        host_q_ = nullptr;
+        launch::publish(res_.p, h_res_, pub_words, pub_seq_.p, h_flag_, stream_);
     };
     if (cfg_.use_graphs && !times) {
         // one CUDA graph per (rows, params): captured on first use, replayed
@@ -850,7 +886,7 @@ void Searcher::search(const float* q, uint64_t rows, uint64_t dim, const plaid_p
         body();
         last_launches_ = launch::launches();
     }
-    PLAID_CUDA(cudaStreamSynchronize(stream_));
+    wait_published();
     PLAID_CUDA(cudaGetLastError());
     const uint64_t* h_counters_ = reinterpret_cast<const uint64_t*>(h_res_);
     const uint64_t n = h_counters_[kNOut];

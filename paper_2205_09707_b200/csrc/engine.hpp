@@ -241,8 +241,13 @@ private:
     DevBuf<SelectState> sel_state_;
     DevBuf<SelectHist> sel_hist_;
     DevBuf<int> status_;
-    // pinned staging
+    // pinned staging (mapped: read / written by kernels directly on the host path)
     float* h_q_ = nullptr;
+    const float* host_q_ = nullptr;      // set while the host path enqueues
+    unsigned int* h_flag_ = nullptr;     // publish flag (pinned)
+    unsigned int pub_seq_host_ = 0;
+    DevBuf<uint32_t> pub_seq_;           // publish sequence on the device
+    void wait_published();
     cudaEvent_t ev_[8] = {};
     uint64_t npartial_warps_ = 0;
     bool tensor_ = false;                   // tcgen05 S_cq path active

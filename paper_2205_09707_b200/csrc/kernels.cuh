@@ -295,9 +295,15 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
 // at d_zero2 (multiples of 4 words, 16-byte aligned): one launch.
 // d_qimg (optional, kQImgBytes): also build the stage-4 tensor kernel's
 // B-operand image of the query at d_qsrc (rows x 128).
+// d_qcopy (optional): first copy the rows x dim query from d_qsrc (e.g. a
+// mapped pinned host buffer) to d_qcopy.
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
                     uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc = nullptr,
-                    void* d_qimg = nullptr);
+                    void* d_qimg = nullptr, float* d_qcopy = nullptr);
+// One CTA: words u32 (multiple of 4) d_src -> mapped host h_dst, then
+// *h_flag = ++*d_seq (system-scope fences between).
+void publish(const uint32_t* d_src, uint32_t* h_dst_mapped, uint64_t words, unsigned int* d_seq,
+             unsigned int* h_flag_mapped, cudaStream_t st);
 // Stage counters: min() bookkeeping done on device.
 void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t st);
 // Merge G shard top-k lists into the global top-k.

@@ -389,7 +389,8 @@ __device__ __forceinline__ void build_qimg(const float* __restrict__ q, uint32_t
 __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
                                                               int* __restrict__ status, uint4* __restrict__ zero,
                                                               uint64_t n16, uint4* __restrict__ zero2, uint64_t m16,
-                                                              const float* __restrict__ qsrc, uint4* __restrict__ qimg) {
+                                                              const float* __restrict__ qsrc, uint4* __restrict__ qimg,
+                                                              float* __restrict__ qcopy, uint32_t ncopy4) {
     dev::pdl_wait();
     // let the S_cq kernel launch now: its TMA producer streams the centroid
     // table (no dependence on this kernel) while the zero fill runs; its other
@@ -400,6 +401,11 @@ __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __rest
         if (i < n16) zero[i] = make_uint4(0, 0, 0, 0);
         else zero2[i - n16] = make_uint4(0, 0, 0, 0);
     }
+    // host path: the query rows come straight from the caller's pinned
+    // (mapped) staging buffer — no separate H2D copy ahead of this kernel
+    if (qcopy && blockIdx.x == 0)
+        for (uint32_t i = threadIdx.x; i < ncopy4; i += blockDim.x)
+            reinterpret_cast<float4*>(qcopy)[i] = reinterpret_cast<const float4*>(qsrc)[i];
     if (qimg && blockIdx.x == gridDim.x - 1) build_qimg(qsrc, rows, qimg);
     if (blockIdx.x != 0 || q == nullptr) return;
     __shared__ float tile[32][33];
@@ -996,8 +1002,26 @@ void copy_count(const uint64_t* src, uint64_t* dst, uint64_t cap, cudaStream_t s
     count_launch();
 }
 
+// Results of the host path straight into the caller's pinned (mapped)
+// buffer, then a sequence flag (the host spins on it instead of a stream
+// synchronize): one CTA after the final select.
+__global__ void __launch_bounds__(256) publish_kernel(const uint4* __restrict__ src, uint4* dst, uint64_t n16,
+                                                      unsigned int* dev_seq, volatile unsigned int* host_flag) {
+    dev::pdl_wait();
+    for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int seq = *dev_seq + 1;
+        *dev_seq = seq;
+        __threadfence_system();
+        *host_flag = seq;
+    }
+}
+
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
-                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc, void* d_qimg) {
+                    uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc, void* d_qimg,
+                    float* d_qcopy) {
     const uint64_t n16 = nwords / 4, m16 = nwords2 / 4;  // both regions are multiples of 16 bytes
     const uint32_t grid = grid_for(n16 + m16, 256, uint32_t(sm_count()));
     const bool img = d_qimg && d_qsrc && dim == 128 && rows <= 32;
@@ -1007,7 +1031,15 @@ void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status
         cudaFuncSetAttribute(query_prologue_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     ::plaid::launch::pdl(query_prologue_kernel, grid, 256, 0, st, d_q, rows, dim, d_status,
                          reinterpret_cast<uint4*>(d_zero), n16, reinterpret_cast<uint4*>(d_zero2), m16,
-                         img ? d_qsrc : nullptr, img ? reinterpret_cast<uint4*>(d_qimg) : nullptr);
+                         (img || d_qcopy) ? d_qsrc : nullptr, img ? reinterpret_cast<uint4*>(d_qimg) : nullptr,
+                         d_qcopy, d_qcopy ? rows * dim / 4 : 0u);
+    count_launch();
+}
+
+void publish(const uint32_t* d_src, uint32_t* h_dst_mapped, uint64_t words, unsigned int* d_seq,
+             unsigned int* h_flag_mapped, cudaStream_t st) {
+    ::plaid::launch::pdl(publish_kernel, 1, 256, 0, st, reinterpret_cast<const uint4*>(d_src),
+                         reinterpret_cast<uint4*>(h_dst_mapped), (words + 3) / 4, d_seq, h_flag_mapped);
     count_launch();
 }
 
