@@ -538,7 +538,7 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     const float* qsrc = host_q_ ? host_q_ : d_q;
     launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, res_.p,
                            2 * kNumCounters, st, qsrc, rank_scratch_.qimg ? qimg_.p : nullptr,
-                           host_q_ ? const_cast<float*>(d_q) : nullptr, run_.p, take_run_dirty());
+                           host_q_ ? const_cast<float*>(d_q) : nullptr);
     record(0, st, times);
 
     // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
@@ -646,22 +646,13 @@ void Searcher::enqueue_back(const float* d_q, uint32_t rows, const plaid_params&
         fin_max = std::min<uint64_t>(stage3_width(p), ix.N);
     }
     rank_scratch_.prescanned = scan_fused_ && !p.disable_filter;
-    // the packed-stream stage 4 leaves per-finalist maxima in run; with a
-    // small final select those become the select's keys directly (no
-    // separate finalize launch) and the next query's prologue re-zeroes run
-    const bool stream = launch::rank_stream128_ok(ix, rows, fin_max, rank_scratch_);
-    const bool defer = stream && fin_max <= launch::kSmallSortMax && !times;
-    rank_scratch_.defer_finalize = defer;
     launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, &rank_scratch_, st);
     rank_scratch_.prescanned = scan_fused_ = false;
-    rank_scratch_.defer_finalize = false;
-    if (defer) run_dirty_ = std::max<uint64_t>(run_dirty_, fin_max * 32);
     record(6, st, times);
     const uint32_t base = uint32_t(index_->pid_base());
     if (fin_max <= launch::kSmallSortMax) {
-        const launch::RunKeys rk{rank_scratch_.run, rows, fin_ids, fin_keys};
         launch::sort_top(keys4_.p, fin_n, fin_max, want_final, nullptr, d_pids, d_scores, d_n, base,
-                         sort_tmp_.p, st, defer ? &rk : nullptr);
+                         sort_tmp_.p, st);
     } else {
         launch::select_top_large(keys4_.p, fin_n, fin_max, want_final, sel_state_.p, tmp_keys_.p,
                                  c + kTmpN, st);
@@ -761,7 +752,7 @@ void Searcher::batch_prepare(const float* d_q, uint64_t rows, uint64_t dim, cons
     ensure_param_buffers(p);
     launch::reset_launches();
     launch::query_prologue(d_q, uint32_t(rows), uint32_t(dim), status_.p, zero_.p, zero_.n, res_.p, 2 * kNumCounters,
-                           st, d_q, rank_scratch_.qimg ? qimg_.p : nullptr, nullptr, run_.p, take_run_dirty());
+                           st, d_q, rank_scratch_.qimg ? qimg_.p : nullptr);
 }
 
 void Searcher::batch_targets(TfOut& out, uint32_t qi, const float* d_q) {

@@ -246,13 +246,6 @@ private:
     const float* host_q_ = nullptr;      // set while the host path enqueues
     unsigned int* h_flag_ = nullptr;     // publish flag (pinned)
     unsigned int pub_seq_host_ = 0;
-    // run words a deferred finalize left non-zero (the next prologue clears them)
-    uint64_t run_dirty_ = 0;
-    uint64_t take_run_dirty() {
-        const uint64_t w = (run_dirty_ + 3) / 4 * 4;
-        run_dirty_ = 0;
-        return w;
-    }
     DevBuf<uint32_t> pub_seq_;           // publish sequence on the device
     void wait_published();
     cudaEvent_t ev_[8] = {};

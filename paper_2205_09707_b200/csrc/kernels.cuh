@@ -216,18 +216,9 @@ void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax,
 // out_n (optional).  nmax <= kSmallSortMax uses one CTA; larger uses a
 // global bitonic sort in `d_tmp` (capacity next_pow2(nmax)).
 constexpr uint64_t kSmallSortMax = 8192;
-// Keys formed from stage 4's running maxima instead of read from d_keys
-// (rank128.cu's finalize folded into the final select): key of finalist p =
-// (in-order fp32 sum of run[p][i < rows], pid of ids[p] or of fkeys[p]).
-struct RunKeys {
-    const uint32_t* run = nullptr;
-    uint32_t rows = 0;
-    const uint32_t* ids = nullptr;
-    const uint64_t* fkeys = nullptr;
-};
 void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
               uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
-              uint32_t id_base, uint64_t* d_tmp, cudaStream_t st, const RunKeys* from_run = nullptr);
+              uint32_t id_base, uint64_t* d_tmp, cudaStream_t st);
 uint64_t sort_tmp_capacity(uint64_t nmax);
 // Stage 4's finalist scan outputs (RankScratch pref / fin_base / tokens) and
 // the index arrays it reads.
@@ -278,7 +269,6 @@ struct RankScratch {
     uint64_t* tokens = nullptr;   // 1 counter: stage-4 stream length (trace)
     uint64_t pass_cap = 0;
     bool prescanned = false;      // pref / fin_base / tokens already written (select_set)
-    bool defer_finalize = false;  // the final select forms the keys from run (RunKeys); run is zeroed by the next prologue
     const float* tensor_S = nullptr;  // TENSOR mode: this query's S_cq table -> stage4_tensor_kernel
     uint32_t* run_p0 = nullptr;       // TENSOR mode: finalist of every 32nd stream position (scan output)
     const void* qimg = nullptr;       // TENSOR mode: the query's bf16 B-operand image (query_prologue)
@@ -309,8 +299,7 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
 // mapped pinned host buffer) to d_qcopy.
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
                     uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc = nullptr,
-                    void* d_qimg = nullptr, float* d_qcopy = nullptr, uint32_t* d_zero3 = nullptr,
-                    uint64_t nwords3 = 0);
+                    void* d_qimg = nullptr, float* d_qcopy = nullptr);
 // One CTA: words u32 (multiple of 4) d_src -> mapped host h_dst, then
 // *h_flag = ++*d_seq (system-scope fences between).
 void publish(const uint32_t* d_src, uint32_t* h_dst_mapped, uint64_t words, unsigned int* d_seq,

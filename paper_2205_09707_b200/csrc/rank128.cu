@@ -886,11 +886,9 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
                              s.fin_base, d_q, rows, s.run, dbg);
         count_launch();
     }
-    if (!s.defer_finalize) {  // else the final select forms the keys from run (RunKeys)
-        const uint32_t nb = uint32_t((nmax + 255) / 256);
-        ::plaid::launch::pdl(finalize_kernel, nb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
-        count_launch();
-    }
+    const uint32_t nb = uint32_t((nmax + 255) / 256);
+    ::plaid::launch::pdl(finalize_kernel, nb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
+    count_launch();
     return true;
 }
 

@@ -190,21 +190,6 @@ __device__ __forceinline__ void emit(uint64_t j, uint64_t key, uint64_t* out_key
     if (out_scores) out_scores[j] = dev::key_score(key);
 }
 
-__device__ __forceinline__ uint64_t run_key(const launch::RunKeys& rk, uint64_t p) {
-    const uint4* r4 = reinterpret_cast<const uint4*>(rk.run + p * 32);
-    uint32_t v[32];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint4 x = __ldcg(r4 + j);
-        v[4 * j] = x.x, v[4 * j + 1] = x.y, v[4 * j + 2] = x.z, v[4 * j + 3] = x.w;
-    }
-    float total = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-        if (uint32_t(i) < rk.rows) total = __fadd_rn(total, dev::unord_f32(v[i]));
-    return dev::make_key(total, rk.ids ? rk.ids[p] : dev::key_id(rk.fkeys[p]));
-}
-
 // Bitonic network step over s[0..npad): comparator p (< npad/2) joins
 // i = insert a 0 bit at position log2(j) of p, and i + j.
 __device__ __forceinline__ void bitonic_pair(uint64_t* s, uint32_t p, uint32_t j, uint32_t k) {
@@ -221,13 +206,11 @@ __device__ __forceinline__ void bitonic_pair(uint64_t* s, uint32_t p, uint32_t j
 __global__ void __launch_bounds__(1024)
 sort_small_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint32_t npad,
                   uint64_t want, uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids,
-                  float* __restrict__ out_scores, uint64_t* __restrict__ out_n, uint32_t id_base,
-                  launch::RunKeys rk) {
+                  float* __restrict__ out_scores, uint64_t* __restrict__ out_n, uint32_t id_base) {
     dev::pdl_wait();
     extern __shared__ uint64_t s[];
     const uint64_t n = *d_n;
-    for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x)
-        s[i] = i < n ? (rk.run ? run_key(rk, i) : keys[i]) : 0ull;
+    for (uint32_t i = threadIdx.x; i < npad; i += blockDim.x) s[i] = i < n ? keys[i] : 0ull;
     __syncthreads();
     const uint32_t half = npad >> 1;
     for (uint32_t k = 2; k <= npad; k <<= 1) {
@@ -261,7 +244,7 @@ __host__ __device__ constexpr uint32_t rank_quarter_pairs(uint32_t n) {
 __global__ void __launch_bounds__(kRankThreads)
 sort_rank_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
                  uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_ids, float* __restrict__ out_scores,
-                 uint64_t* __restrict__ out_n, uint32_t id_base, launch::RunKeys rk) {
+                 uint64_t* __restrict__ out_n, uint32_t id_base) {
     dev::pdl_wait();
     extern __shared__ __align__(16) uint64_t s[];
     const uint32_t n = uint32_t(*d_n);
@@ -273,16 +256,12 @@ sort_rank_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
         const uint32_t q = i / (npq + 1), k = i % (npq + 1);
         const uint32_t e = 2 * (q * npq + k);
         const bool real = k < npq;
-        s[2 * i] = real && e < n ? (rk.run ? run_key(rk, e) : __ldcg(keys + e)) : 0ull;
-        s[2 * i + 1] = real && e + 1 < n ? (rk.run ? run_key(rk, e + 1) : __ldcg(keys + e + 1)) : 0ull;
+        s[2 * i] = real && e < n ? __ldcg(keys + e) : 0ull;
+        s[2 * i + 1] = real && e + 1 < n ? __ldcg(keys + e + 1) : 0ull;
     }
     __syncthreads();
     const uint32_t me = blockIdx.x * kRankPerCta + (threadIdx.x >> 2), q = threadIdx.x & 3;
-    uint64_t x = ~0ull;
-    if (me < n) {  // my key from the staged quarters (pair k of quarter q at q * (npq + 1) + k)
-        const uint32_t pair = me / 2, qq = pair / npq, kk = pair % npq;
-        x = s[2 * (qq * (npq + 1) + kk) + (me & 1)];
-    }
+    const uint64_t x = me < n ? __ldcg(keys + me) : ~0ull;
     uint32_t rank = 0;
     const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(s) + q * (npq + 1);
 #pragma unroll 8
@@ -411,18 +390,16 @@ __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __rest
                                                               int* __restrict__ status, uint4* __restrict__ zero,
                                                               uint64_t n16, uint4* __restrict__ zero2, uint64_t m16,
                                                               const float* __restrict__ qsrc, uint4* __restrict__ qimg,
-                                                              float* __restrict__ qcopy, uint32_t ncopy4,
-                                                              uint4* __restrict__ zero3, uint64_t k16) {
+                                                              float* __restrict__ qcopy, uint32_t ncopy4) {
     dev::pdl_wait();
     // let the S_cq kernel launch now: its TMA producer streams the centroid
     // table (no dependence on this kernel) while the zero fill runs; its other
     // warps still wait for this grid to complete
     dev::pdl_trigger();
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16 + m16 + k16;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16 + m16;
          i += uint64_t(gridDim.x) * blockDim.x) {
         if (i < n16) zero[i] = make_uint4(0, 0, 0, 0);
-        else if (i < n16 + m16) zero2[i - n16] = make_uint4(0, 0, 0, 0);
-        else zero3[i - n16 - m16] = make_uint4(0, 0, 0, 0);
+        else zero2[i - n16] = make_uint4(0, 0, 0, 0);
     }
     // host path: the query rows come straight from the caller's pinned
     // (mapped) staging buffer — no separate H2D copy ahead of this kernel
@@ -961,9 +938,7 @@ uint64_t sort_tmp_capacity(uint64_t nmax) { return nmax <= kSmallSortMax ? 0 : n
 
 void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
               uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
-              uint32_t id_base, uint64_t* d_tmp, cudaStream_t st, const RunKeys* from_run) {
-    const RunKeys rk = from_run ? *from_run : RunKeys{};
-    if (from_run && nmax > kSmallSortMax) fail_cuda_driver(1, "sort_top: run keys need nmax <= kSmallSortMax");
+              uint32_t id_base, uint64_t* d_tmp, cudaStream_t st) {
     if (nmax <= kSmallSortMax && nmax >= 256) {
         const size_t smem = size_t(4) * (rank_quarter_pairs(uint32_t(nmax)) + 1) * 16;
         static launch::PerDeviceOnce rank_cfg;
@@ -973,7 +948,7 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
         }
         const uint32_t grid = uint32_t((nmax + kRankPerCta - 1) / kRankPerCta);
         ::plaid::launch::pdl(sort_rank_kernel, grid, kRankThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_ids, d_out_scores,
-                                                          d_out_n, id_base, rk);
+                                                          d_out_n, id_base);
         count_launch();
         return;
     }
@@ -987,7 +962,7 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
         }
         const uint32_t threads = npad / 2 < 1024 ? (npad / 2 < 32 ? 32 : npad / 2) : 1024;
         ::plaid::launch::pdl(sort_small_kernel, 1, threads, smem, st, d_keys, d_n, npad, want, d_out_keys, d_out_ids,
-                                                    d_out_scores, d_out_n, id_base, rk);
+                                                    d_out_scores, d_out_n, id_base);
         count_launch();
         return;
     }
@@ -1046,9 +1021,9 @@ __global__ void __launch_bounds__(256) publish_kernel(const uint4* __restrict__ 
 
 void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status, uint32_t* d_zero, uint64_t nwords,
                     uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc, void* d_qimg,
-                    float* d_qcopy, uint32_t* d_zero3, uint64_t nwords3) {
-    const uint64_t n16 = nwords / 4, m16 = nwords2 / 4, k16 = d_zero3 ? nwords3 / 4 : 0;  // multiples of 16 bytes
-    const uint32_t grid = grid_for(n16 + m16 + k16, 256, uint32_t(sm_count()));
+                    float* d_qcopy) {
+    const uint64_t n16 = nwords / 4, m16 = nwords2 / 4;  // both regions are multiples of 16 bytes
+    const uint32_t grid = grid_for(n16 + m16, 256, uint32_t(sm_count()));
     const bool img = d_qimg && d_qsrc && dim == 128 && rows <= 32;
     static launch::PerDeviceOnce cfg;
     if (cfg.first())  // keep the SMs' shared-memory partition at its maximum so the
@@ -1057,7 +1032,7 @@ void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status
     ::plaid::launch::pdl(query_prologue_kernel, grid, 256, 0, st, d_q, rows, dim, d_status,
                          reinterpret_cast<uint4*>(d_zero), n16, reinterpret_cast<uint4*>(d_zero2), m16,
                          (img || d_qcopy) ? d_qsrc : nullptr, img ? reinterpret_cast<uint4*>(d_qimg) : nullptr,
-                         d_qcopy, d_qcopy ? rows * dim / 4 : 0u, reinterpret_cast<uint4*>(d_zero3), k16);
+                         d_qcopy, d_qcopy ? rows * dim / 4 : 0u);
     count_launch();
 }
 
