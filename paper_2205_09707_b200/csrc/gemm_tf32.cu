@@ -270,39 +270,31 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
         for (uint32_t g = 0; g < pre; ++g) issue_box(g);
     if (warp != 0) dev::pdl_wait();
     if (threadIdx.x < 32 * QB) cthr[threadIdx.x] = 0;
-    if (fold.flag && warp != 0) {
-        if (blockIdx.x == 0) {
-            // the folded prologue's serial part, by warps 1-15 of CTA 0: query
-            // rows (all loads in flight before any store: the source may be
-            // pinned host memory), counters (and the grid-wide bounds among
-            // them); then the flag every CTA's B-operand build waits for
-            const uint32_t t = threadIdx.x - 32, n4 = fold.q_copy ? fold.rows * fold.dim / 4 : 0;
-            float4 v[3];
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-                if (t + u * 480 < n4) v[u] = reinterpret_cast<const float4*>(fold.q_src)[t + u * 480];
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-                if (t + u * 480 < n4) reinterpret_cast<float4*>(fold.q_copy)[t + u * 480] = v[u];
-            for (uint32_t i = 3 * 480 + t; i < n4; i += 480)
+    if (fold.flag && blockIdx.x == 0 && (warp == 2 || warp == 3)) {
+        // the folded prologue's serial part: query rows, counters (and the
+        // grid-wide bounds among them), norm check; then the flag
+        const uint32_t t = threadIdx.x - 64;
+        if (fold.q_copy)
+            for (uint32_t i = t; i < fold.rows * fold.dim / 4; i += 64)
                 reinterpret_cast<float4*>(fold.q_copy)[i] = reinterpret_cast<const float4*>(fold.q_src)[i];
-            for (uint64_t i = t; i < fold.m16; i += 480) fold.zero2[i] = make_uint4(0, 0, 0, 0);
-            __threadfence();
-            asm volatile("bar.sync 1, 480;" ::: "memory");
-            if (t == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fold.flag), "r"(fold.seq) : "memory");
-            if (fold.q_check && t < fold.rows) {  // types.cpp:61-72 on the device
-                const float* r = fold.q_check + uint64_t(t) * fold.dim;
-                double acc = 0.0;
-                for (uint32_t d = 0; d < fold.dim; ++d) acc = __dadd_rn(acc, __dmul_rn(double(r[d]), double(r[d])));
-                if (fabs(sqrt(acc) - 1.0) > double(1e-3f)) atomicExch(fold.status, 2);  // NotNormalized + 1
-            }
-        } else if (threadIdx.x == 32) {
+        for (uint64_t i = t; i < fold.m16; i += 64) fold.zero2[i] = make_uint4(0, 0, 0, 0);
+        __threadfence();
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (t == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fold.flag), "r"(fold.seq) : "memory");
+        if (fold.q_check && t < fold.rows) {  // types.cpp:61-72 on the device
+            const float* r = fold.q_check + uint64_t(t) * fold.dim;
+            double acc = 0.0;
+            for (uint32_t d = 0; d < fold.dim; ++d) acc = __dadd_rn(acc, __dmul_rn(double(r[d]), double(r[d])));
+            if (fabs(sqrt(acc) - 1.0) > double(1e-3f)) atomicExch(fold.status, 2);  // NotNormalized + 1
+        }
+    }
+    if (fold.flag && warp != 0) {
+        // every CTA's B operand reads Q: wait for CTA 0's flag
+        if (threadIdx.x == 32) {
             unsigned int v;
-            for (;;) {
+            do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fold.flag) : "memory");
-                if (v == fold.seq) break;
-                __nanosleep(64);
-            }
+            } while (v != fold.seq);
         }
         asm volatile("bar.sync 2, 480;" ::: "memory");
     }
