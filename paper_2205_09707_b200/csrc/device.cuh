@@ -116,41 +116,5 @@ __device__ __forceinline__ void topn_insert(uint64_t (&k)[NP], uint64_t x) {
     k[0] = k[0] > x ? k[0] : x;
 }
 
-// bf16 bits of x rounded to nearest even (finite inputs)
-__device__ __forceinline__ uint32_t bf16_rn_u32(float x) {
-    const uint32_t u = __float_as_uint(x);
-    return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
-}
-
-// Granule e (16 bytes, e < 2048) of the stage-4 tensor kernel's B-operand
-// image of a query (rank128.cu stage4_tensor_kernel): 64 rows x K = 256 bf16,
-// row n < 32 = [Q_hi | Q_hi] of query token n, row 32 + i = [Q_lo | 0] of
-// token i (Q_hi = bf16(q), Q_lo = bf16(q - Q_hi); zero rows past `rows`),
-// SWIZZLE_128B K-major chunks of 64 bf16: granule (c, n, j) stored at
-// c * 8192 + n * 128 + ((j ^ (n & 7)) << 4) — this returns the VALUE for
-// storage slot e of that layout.
-__device__ __forceinline__ uint4 qimg_granule(const float* __restrict__ q, uint32_t rows, uint32_t e) {
-    const uint32_t c = e >> 9, n = (e >> 3) & 63, js = e & 7;  // stored position
-    const uint32_t j = js ^ (n & 7);                               // logical granule
-    const uint32_t i = n & 31, k0 = c * 64 + j * 8, d0 = k0 & 127;
-    const bool lo = n >= 32;
-    uint32_t v[4] = {0, 0, 0, 0};
-    if (i < rows && !(lo && k0 >= 128)) {
-        const float4 a = reinterpret_cast<const float4*>(q + i * 128 + d0)[0];
-        const float4 b = reinterpret_cast<const float4*>(q + i * 128 + d0)[1];
-        const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            uint32_t h0 = bf16_rn_u32(f[2 * u]), h1 = bf16_rn_u32(f[2 * u + 1]);
-            if (lo) {
-                h0 = bf16_rn_u32(f[2 * u] - __uint_as_float(h0 << 16));
-                h1 = bf16_rn_u32(f[2 * u + 1] - __uint_as_float(h1 << 16));
-            }
-            v[u] = h0 | (h1 << 16);
-        }
-    }
-    return make_uint4(v[0], v[1], v[2], v[3]);
-}
-
 }  // namespace dev
 }  // namespace plaid

@@ -381,8 +381,6 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
     PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_q_), 32 * 256 * sizeof(float)));
     PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_flag_), 64));
     *h_flag_ = 0;
-    fold_flag_.ensure(1);
-    PLAID_CUDA(cudaMemset(fold_flag_.p, 0, sizeof(uint32_t)));
     pub_seq_.ensure(1);
     PLAID_CUDA(cudaMemset(pub_seq_.p, 0, sizeof(uint32_t)));
     q_.ensure(32 * 256);
@@ -538,38 +536,14 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     // "scores" phase then brackets the S_cq kernel alone
     // host path: the prologue also copies Q from the pinned staging buffer
     const float* qsrc = host_q_ ? host_q_ : d_q;
+    launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, res_.p,
+                           2 * kNumCounters, st, qsrc, rank_scratch_.qimg ? qimg_.p : nullptr,
+                           host_q_ ? const_cast<float*>(d_q) : nullptr);
+    record(0, st, times);
+
+    // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
     const uint32_t npb = p.nprobe <= 32 ? np_bucket(p.nprobe) : 1;
-    uint32_t warps = 0;
-    if (tensor_ && !cfg_.use_graphs) {
-        // the prologue rides in the S_cq launch (TfFold): its idle warps zero
-        // the bitmaps, CTA 0 copies Q / clears the counters / checks the norms
-        // and raises a flag the other CTAs' B-operand builds wait for (a
-        // per-launch sequence number, so graph capture keeps the prologue)
-        TfFold f;
-        f.q_src = host_q_;
-        f.q_copy = host_q_ ? const_cast<float*>(d_q) : nullptr;
-        f.q_check = validate ? d_q : nullptr;
-        f.rows = rows;
-        f.dim = ix.dim;
-        f.status = status_.p;
-        f.zero = reinterpret_cast<uint4*>(zero_.p);
-        f.n16 = zero_.n / 4;
-        f.zero2 = reinterpret_cast<uint4*>(res_.p);
-        f.m16 = 2 * kNumCounters / 4;
-        f.qimg = rank_scratch_.qimg ? reinterpret_cast<uint4*>(qimg_.p) : nullptr;
-        f.flag = fold_flag_.p;
-        f.seq = ++fold_seq_;
-        record(0, st, times);
-        warps = launch::scores_tensor(tmap_, ix, d_q, rows, p.t_cs, scores_.p, keep_.p, partial_.p, npb,
-                                      reinterpret_cast<uint32_t*>(counters_.p + kGthr), st, &f);
-    } else {
-        launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, res_.p,
-                               2 * kNumCounters, st, qsrc, rank_scratch_.qimg ? qimg_.p : nullptr,
-                               host_q_ ? const_cast<float*>(d_q) : nullptr);
-        record(0, st, times);
-        // Stage 1: S_cq (+ row max, keep bits, per-warp top-nprobe), candidates.
-        warps = launch_scores(d_q, rows, p.t_cs, npb, st);
-    }
+    const uint32_t warps = launch_scores(d_q, rows, p.t_cs, npb, st);
     record(1, st, times);
     front_after_scores(rows, p, warps, st, times);
 }

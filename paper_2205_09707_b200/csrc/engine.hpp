@@ -247,8 +247,6 @@ private:
     unsigned int* h_flag_ = nullptr;     // publish flag (pinned)
     unsigned int pub_seq_host_ = 0;
     DevBuf<uint32_t> pub_seq_;           // publish sequence on the device
-    DevBuf<uint32_t> fold_flag_;         // TfFold: CTA 0's "query ready" flag
-    unsigned int fold_seq_ = 0;
     void wait_published();
     cudaEvent_t ev_[8] = {};
     uint64_t npartial_warps_ = 0;

@@ -210,7 +210,7 @@ __device__ __forceinline__ uint32_t split_lo(uint32_t x) {
 template <int NP, int QB>
 __global__ void __launch_bounds__(kThreads, 1)
 scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const __grid_constant__ TfOut out,
-                   uint32_t rows, float t_cs, uint32_t dbg, const __grid_constant__ TfFold fold) {
+                   uint32_t rows, float t_cs, uint32_t dbg) {
     using Cf = TfCfg<QB>;
     constexpr int kRaw = Cf::kRaw, kOps = Cf::kOps;
     constexpr uint32_t kOffRaw = Cf::kOffRaw, kOffQ = Cf::kOffQ, kOffTr = Cf::kOffTr, kOffBar = Cf::kOffBar,
@@ -270,34 +270,6 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
         for (uint32_t g = 0; g < pre; ++g) issue_box(g);
     if (warp != 0) dev::pdl_wait();
     if (threadIdx.x < 32 * QB) cthr[threadIdx.x] = 0;
-    if (fold.flag && blockIdx.x == 0 && (warp == 2 || warp == 3)) {
-        // the folded prologue's serial part: query rows, counters (and the
-        // grid-wide bounds among them), norm check; then the flag
-        const uint32_t t = threadIdx.x - 64;
-        if (fold.q_copy)
-            for (uint32_t i = t; i < fold.rows * fold.dim / 4; i += 64)
-                reinterpret_cast<float4*>(fold.q_copy)[i] = reinterpret_cast<const float4*>(fold.q_src)[i];
-        for (uint64_t i = t; i < fold.m16; i += 64) fold.zero2[i] = make_uint4(0, 0, 0, 0);
-        __threadfence();
-        asm volatile("bar.sync 1, 64;" ::: "memory");
-        if (t == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fold.flag), "r"(fold.seq) : "memory");
-        if (fold.q_check && t < fold.rows) {  // types.cpp:61-72 on the device
-            const float* r = fold.q_check + uint64_t(t) * fold.dim;
-            double acc = 0.0;
-            for (uint32_t d = 0; d < fold.dim; ++d) acc = __dadd_rn(acc, __dmul_rn(double(r[d]), double(r[d])));
-            if (fabs(sqrt(acc) - 1.0) > double(1e-3f)) atomicExch(fold.status, 2);  // NotNormalized + 1
-        }
-    }
-    if (fold.flag && warp != 0) {
-        // every CTA's B operand reads Q: wait for CTA 0's flag
-        if (threadIdx.x == 32) {
-            unsigned int v;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fold.flag) : "memory");
-            } while (v != fold.seq);
-        }
-        asm volatile("bar.sync 2, 480;" ::: "memory");
-    }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kTmemCols));
@@ -419,17 +391,6 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
                 if (lane == 0) mbar_arrive(ops_full(o));
                 if (warp == 4 && lane == 0) trace_stamp(dbg, 3, go);
             }
-        }
-    } else if (warp == 2 || warp == 3) {
-        // ---------------- folded prologue: the zero fills (no kernel reads
-        // them before the next launch) and the stage-4 query image
-        if (fold.flag) {
-            const uint64_t stride = uint64_t(gridDim.x) * 64;
-            for (uint64_t i = uint64_t(blockIdx.x) * 64 + threadIdx.x - 64; i < fold.n16; i += stride)
-                fold.zero[i] = make_uint4(0, 0, 0, 0);
-            if (fold.qimg && blockIdx.x == gridDim.x - 1)
-                for (uint32_t e = threadIdx.x - 64; e < launch::kQImgBytes / 16; e += 64)
-                    fold.qimg[e] = dev::qimg_granule(out.Q[0], rows, e);
         }
     } else if (warp >= 8) {
         // ---------------- epilogue: two groups of 4 warps take alternate tiles
@@ -563,7 +524,7 @@ int sm_count() {
 
 template <int NP, int QB>
 void launch_tf32(const CUtensorMap& map, const IndexView& ix, const TfOut& out, uint32_t rows, float t_cs,
-                 uint32_t grid, cudaStream_t st, const TfFold& fold) {
+                 uint32_t grid, cudaStream_t st) {
     static launch::PerDeviceOnce configured;
     if (configured.first()) {
         cudaFuncSetAttribute(scores_tf32_kernel<NP, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -574,22 +535,22 @@ void launch_tf32(const CUtensorMap& map, const IndexView& ix, const TfOut& out, 
         return e ? uint32_t(atoi(e)) : 0u;
     }();
     ::plaid::launch::pdl(scores_tf32_kernel<NP, QB>, grid, kThreads, TfCfg<QB>::kSmemBytes, st, map, ix.K, out, rows,
-                         t_cs, dbg, fold);
+                         t_cs, dbg);
     launch::count_launch();
 }
 
 template <int QB>
 void launch_tf32_np(const CUtensorMap& map, const IndexView& ix, const TfOut& out, uint32_t rows, float t_cs,
-                    uint32_t np_bucket, uint32_t grid, cudaStream_t st, const TfFold& fold = TfFold{}) {
+                    uint32_t np_bucket, uint32_t grid, cudaStream_t st) {
     switch (np_bucket) {
-        case 1: launch_tf32<1, QB>(map, ix, out, rows, t_cs, grid, st, fold); break;
-        case 2: launch_tf32<2, QB>(map, ix, out, rows, t_cs, grid, st, fold); break;
-        case 4: launch_tf32<4, QB>(map, ix, out, rows, t_cs, grid, st, fold); break;
-        case 8: launch_tf32<8, QB>(map, ix, out, rows, t_cs, grid, st, fold); break;
-        case 16: if constexpr (QB == 1) { launch_tf32<16, QB>(map, ix, out, rows, t_cs, grid, st, fold); break; }
+        case 1: launch_tf32<1, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 2: launch_tf32<2, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 4: launch_tf32<4, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 8: launch_tf32<8, QB>(map, ix, out, rows, t_cs, grid, st); break;
+        case 16: if constexpr (QB == 1) { launch_tf32<16, QB>(map, ix, out, rows, t_cs, grid, st); break; }
         [[fallthrough]];
         default:
-            if constexpr (QB == 1) launch_tf32<32, QB>(map, ix, out, rows, t_cs, grid, st, fold);
+            if constexpr (QB == 1) launch_tf32<32, QB>(map, ix, out, rows, t_cs, grid, st);
             else launch::fail_cuda_driver(1, "batched S_cq supports nprobe <= 8");
             break;
     }
@@ -648,12 +609,12 @@ uint32_t scores_tensor_max_warps() { return uint32_t(sm_count()) * kEpiWarps; }
 
 uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
                        float* d_scores, uint32_t* d_keep_bits, uint64_t* d_partial, uint32_t np_bucket,
-                       uint32_t* d_gthr, cudaStream_t st, const TfFold* fold) {
+                       uint32_t* d_gthr, cudaStream_t st) {
     const CUtensorMap& map = *static_cast<const CUtensorMap*>(cmap);
     TfOut out{};
     out.Q[0] = d_q, out.S[0] = d_scores, out.keep[0] = d_keep_bits, out.partial[0] = d_partial, out.gthr[0] = d_gthr;
     const uint32_t grid = tf32_grid(ix);
-    launch_tf32_np<1>(map, ix, out, rows, t_cs, np_bucket, grid, st, fold ? *fold : TfFold{});
+    launch_tf32_np<1>(map, ix, out, rows, t_cs, np_bucket, grid, st);
     return grid * kEpiWarps;
 }
 

@@ -69,26 +69,6 @@ struct TfOut {
     uint32_t* gthr[kMaxScoreBatch];
 };
 
-// The per-query prologue folded into the single-query tensor S_cq kernel
-// (gemm_tf32.cu): the kernel's idle warps do the zero fills, and CTA 0 copies
-// the query, clears the counters (incl. the grid-wide top-nprobe bounds), checks
-// the row norms and builds the stage-4 query image before raising `flag` =
-// `seq`, which every CTA's B-operand build waits for.
-struct TfFold {
-    const float* q_src = nullptr;    // query rows to copy into q_copy (pinned host or device)
-    float* q_copy = nullptr;         // device destination (the kernel's Q), nullptr = Q already there
-    const float* q_check = nullptr;  // validate these rows' norms (device), nullptr = no check
-    uint32_t rows = 0, dim = 0;
-    int* status = nullptr;
-    uint4* zero = nullptr;           // bitmaps + compaction status (idle warps, any CTA)
-    uint64_t n16 = 0;
-    uint4* zero2 = nullptr;          // counters (CTA 0, before the flag)
-    uint64_t m16 = 0;
-    uint4* qimg = nullptr;           // stage-4 B-operand image (nullptr = none)
-    unsigned int* flag = nullptr;    // nullptr = no fold
-    unsigned int seq = 0;
-};
-
 namespace launch {
 
 // True the first time per (call site, current device): kernel attributes
@@ -141,7 +121,7 @@ void make_centroid_tensor_map(const IndexView& ix, void* out_map);
 // the launch.  Returns the number of partial lists written.
 uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, uint32_t rows, float t_cs,
                        float* d_scores, uint32_t* d_keep_bits, uint64_t* d_partial, uint32_t np_bucket,
-                       uint32_t* d_gthr, cudaStream_t st, const TfFold* fold = nullptr);
+                       uint32_t* d_gthr, cudaStream_t st);
 uint32_t scores_tensor_max_warps();
 // Batched variant: qb (<= kMaxScoreBatch) queries share one pass over C
 // (B operand = every query's Q_hi and Q_lo, N = 64 qb); per-query outputs as

@@ -350,9 +350,40 @@ __global__ void copy_count_kernel(const uint64_t* src, uint64_t* dst, uint64_t c
 // the products are exact in fp64, so only the adds must stay in order: 32-dim
 // chunks are staged coalesced in shared memory and thread r runs row r's add
 // chain from there).
-// The stage-4 tensor kernel's B-operand image of a query (dev::qimg_granule).
+// bf16 bits of x rounded to nearest even (finite inputs)
+__device__ __forceinline__ uint32_t bf16_rn_u32(float x) {
+    const uint32_t u = __float_as_uint(x);
+    return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+
+// The stage-4 tensor kernel's B operand for a query (rank128.cu,
+// stage4_tensor_kernel): 64 rows x K = 256 bf16, row n < 32 = [Q_hi | Q_hi]
+// of query token n, row 32 + i = [Q_lo | 0] of token i (Q_hi = bf16(q),
+// Q_lo = bf16(q - Q_hi); zero rows past `rows`), SWIZZLE_128B K-major chunks
+// of 64 bf16: chunk c, row n, 16-byte granule j at c * 8192 + n * 128 +
+// ((j ^ (n & 7)) << 4).
 __device__ __forceinline__ void build_qimg(const float* __restrict__ q, uint32_t rows, uint4* __restrict__ img) {
-    for (uint32_t e = threadIdx.x; e < launch::kQImgBytes / 16; e += blockDim.x) img[e] = dev::qimg_granule(q, rows, e);
+    for (uint32_t e = threadIdx.x; e < launch::kQImgBytes / 16; e += blockDim.x) {
+        const uint32_t c = e >> 9, n = (e >> 3) & 63, j = e & 7;
+        const uint32_t i = n & 31, k0 = c * 64 + j * 8, d0 = k0 & 127;
+        const bool lo = n >= 32;
+        uint32_t v[4] = {0, 0, 0, 0};
+        if (i < rows && !(lo && k0 >= 128)) {
+            const float4 a = reinterpret_cast<const float4*>(q + i * 128 + d0)[0];
+            const float4 b = reinterpret_cast<const float4*>(q + i * 128 + d0)[1];
+            const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t h0 = bf16_rn_u32(f[2 * u]), h1 = bf16_rn_u32(f[2 * u + 1]);
+                if (lo) {
+                    h0 = bf16_rn_u32(f[2 * u] - __uint_as_float(h0 << 16));
+                    h1 = bf16_rn_u32(f[2 * u + 1] - __uint_as_float(h1 << 16));
+                }
+                v[u] = h0 | (h1 << 16);
+            }
+        }
+        img[(c * 8192 + n * 128 + ((j ^ (n & 7)) << 4)) / 16] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
 }
 
 __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
