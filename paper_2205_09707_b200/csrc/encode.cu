@@ -8,9 +8,9 @@
 //   IVF        build_inverted_list (indexer.cpp:149-195): per centroid the
 //              sorted unique ids of the passages owning it.
 // Bit-identical to the reference (tests/test_gpu_parity.py::test_encode_*).
-// k-means and the quantizer fit (kmeans.cpp, indexer.cpp:74-147) stay on the
-// host reference: they are order-sensitive sequential reductions that only
-// see a <= 2^20-row sample.
+// build_index_host (below) adds k-means and the quantizer fit (kmeans.cpp,
+// indexer.cpp:74-147): their seed-driven sequential choices stay on the host
+// in the reference's order, the dots and sums run on the GPU.
 //
 // assign_codes is the only heavy part (T x K x d multiply-adds).  Exactness
 // pins it to the FP32 pipe (a rounded multiply and a rounded add per term):
