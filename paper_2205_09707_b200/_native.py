@@ -153,6 +153,7 @@ SIGNATURES = {
                                     C.c_uint64, C.POINTER(C.c_uint64)]),
     # test knobs (not part of include/plaid.h)
     "plaid_debug_set_tf32_grid": (C.c_uint32, [C.c_uint32]),
+    "plaid_debug_set_launch_cap": (C.c_longlong, [C.c_longlong]),
 }
 
 _lib = None

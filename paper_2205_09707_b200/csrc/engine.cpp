@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <thread>
 
@@ -18,9 +19,16 @@ namespace plaid {
 namespace launch {
 namespace {
 thread_local uint64_t g_launches = 0;
+thread_local int64_t g_pdl_issued = 0;
+std::atomic<int64_t> g_launch_cap{-1};
 }
 uint64_t launches() { return g_launches; }
-void reset_launches() { g_launches = 0; }
+void reset_launches() { g_launches = 0; g_pdl_issued = 0; }
+bool pdl_skip() {
+    const int64_t cap = g_launch_cap.load(std::memory_order_relaxed);
+    return cap >= 0 && g_pdl_issued++ >= cap;
+}
+int64_t set_launch_cap(int64_t cap) { return g_launch_cap.exchange(cap); }
 // Every launcher calls this right after its <<<>>>: a failed launch (bad
 // config, missing smem opt-in) surfaces here instead of as stale results.
 void count_launch() {
@@ -293,6 +301,7 @@ DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_bas
     }
     if (offsets.back() != d.num_embeddings) fail(PLAID_LENGTH_MISMATCH, "doclens total does not match codes length");
     view_.max_doclen = max_doclen_;
+    set_list_bounds(d.ivf_offsets);
     const uint64_t nb = uint64_t(1) << d.nbits;
     for (uint64_t i = 0; i < nb; ++i) view_.weights[i] = d.bucket_weights[i];
     for (uint64_t i = 0; i + 1 < nb; ++i) cutoffs_[i] = d.bucket_cutoffs[i];
@@ -319,6 +328,22 @@ DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_bas
         allocs_.clear();
         throw;
     }
+}
+
+void DeviceIndex::set_list_bounds(const uint64_t* ivo) {
+    const uint64_t K = view_.K;
+    std::vector<uint64_t> len(K);
+    for (uint64_t c = 0; c < K; ++c) len[c] = ivo[c + 1] - ivo[c];
+    std::sort(len.begin(), len.end(), std::greater<uint64_t>());
+    longest_prefix_.assign(K + 1, 0);
+    for (uint64_t j = 0; j < K; ++j) longest_prefix_[j + 1] = longest_prefix_[j] + len[j];
+}
+
+uint64_t DeviceIndex::candidate_bound(uint64_t nprobe) const {
+    const uint64_t N = view_.N, K = view_.K;
+    if (longest_prefix_.size() != K + 1) return N;
+    const uint64_t lists = nprobe >= K / 32 ? K : 32 * nprobe;
+    return std::min<uint64_t>(N, longest_prefix_[std::min<uint64_t>(lists, K)]);
 }
 
 void DeviceIndex::validate_device() {
@@ -398,8 +423,6 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         sel_hist_.ensure(1);
         PLAID_CUDA(cudaMemset(sel_hist_.p, 0, sizeof(SelectHist)));  // re-zeroed by every select after
         kept_list_.ensure(ix.K);
-        acc2_.ensure(ix.N * 32);
-        PLAID_CUDA(cudaMemset(acc2_.p, 0, acc2_.n * sizeof(uint32_t)));
         keys2_.ensure(ix.N);
         keys4_.ensure(ix.N);
         const uint64_t K = ix.K;
@@ -461,6 +484,13 @@ void Searcher::ensure_param_buffers_impl(const plaid_params& p) {
     if (p.nprobe > 32 && p.nprobe < K) tok_keys_.ensure(K);
     const uint64_t nd = std::min<uint64_t>(p.ndocs, N);
     const uint64_t n3 = std::min<uint64_t>(stage3_width(p), N);
+    // stage-2 accumulators: [slot of a candidate][query token], slots < |C1|;
+    // every consumer re-zeroes the slots it read, so only growth is filled
+    const uint64_t n1cap = index_->candidate_bound(p.nprobe);
+    if (acc2_.n < n1cap * 32) {
+        acc2_.ensure(n1cap * 32);
+        PLAID_CUDA(cudaMemset(acc2_.p, 0, acc2_.n * sizeof(uint32_t)));
+    }
     sel2_.ensure(nd);
     keys3_.ensure(nd);
     sel3_.ensure(n3);
@@ -1630,3 +1660,9 @@ void ShardedSearcher::search(const float* q, uint64_t rows, uint64_t dim, const 
 }
 
 }  // namespace plaid
+
+// Profiling knob: stop every search after its first `cap` kernel launches
+// (-1 = off); returns the previous cap.  Not part of include/plaid.h.
+extern "C" long long plaid_debug_set_launch_cap(long long cap) {
+    return static_cast<long long>(plaid::launch::set_launch_cap(cap));
+}

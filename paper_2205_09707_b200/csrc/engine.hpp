@@ -83,6 +83,11 @@ public:
     const std::vector<uint32_t>& host_doclens() const { return h_doclens_; }
     // Downloads the device arrays and re-checks validate_index's invariants.
     void validate_device();
+    // Upper bound on |C1| for a query probing nprobe centroids per token:
+    // at most 32 * nprobe distinct lists, so at most the sum of the 32 *
+    // nprobe longest list lengths (and at most N).  Sizes the stage-2
+    // accumulators by the query's reach instead of the corpus.
+    uint64_t candidate_bound(uint64_t nprobe) const;
 
 private:
     template <typename T>
@@ -95,6 +100,8 @@ private:
     float cutoffs_[16] = {};
     std::vector<void*> allocs_;
     std::vector<uint32_t> h_doclens_;
+    std::vector<uint64_t> longest_prefix_;  // [K + 1]: sums of the j longest list lengths
+    void set_list_bounds(const uint64_t* ivf_offsets_host);
 };
 
 // Host-side pinned/device buffer helper.

@@ -88,8 +88,15 @@ struct PerDeviceOnce {
 // scheduled while the previous kernel in the stream drains; every kernel
 // starts with dev::pdl_wait(), so no data dependence is relaxed.
 bool pdl_enabled();  // false when PLAID_NO_PDL is set (ordering experiments)
+// Profiling knob (plaid_debug_set_launch_cap): true once this thread has
+// issued `cap` launches since reset_launches(), so a search stops after its
+// first `cap` kernels (tools/chain_profile.py: marginal cost of each kernel
+// inside the PDL chain).  Always false unless the cap is set.
+bool pdl_skip();
+int64_t set_launch_cap(int64_t cap);  // -1 = no cap; returns the old cap
 template <typename... KArgs, typename... Args>
 inline void pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    if (pdl_skip()) return;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;

@@ -334,6 +334,11 @@ DeviceIndex::DeviceIndex(const SynthSpec& sp, int device) : device_(device), pid
         view_.ivf_mult = mult8;
         h_doclens_.resize(N);
         PLAID_CUDA(cudaMemcpy(h_doclens_.data(), dl, N * 4, cudaMemcpyDeviceToHost));
+        {
+            std::vector<uint64_t> h_ivo(K + 1);
+            PLAID_CUDA(cudaMemcpy(h_ivo.data(), ivo, (K + 1) * 8, cudaMemcpyDeviceToHost));
+            set_list_bounds(h_ivo.data());
+        }
         for (uint32_t x : h_doclens_) max_doclen_ = std::max(max_doclen_, x);
         view_.max_doclen = max_doclen_;
         if (dim == 128 && T) {
