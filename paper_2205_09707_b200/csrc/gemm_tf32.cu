@@ -157,20 +157,57 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
     return d;
 }
 
-// D[tmem] (+)= A[tmem] . B[smem]
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
-                                       uint32_t accumulate) {
+// One 32-dim chunk of a tile, issued by the whole (converged) warp with the
+// elected lane predicated inside a single asm block: per 8-dim step
+// D[:, 0:32QB] += C_hi.Q_hi, D[:, 32QB:64QB] += C_hi.Q_lo (idesc_all) and
+// D[:, 0:32QB] += C_lo.Q_hi (idesc_hi), then a commit to `bar`.  Issued from a
+// `lane == 0` branch instead, every MMA was wrapped in its own waterfall loop
+// (ELECT / R2UR.BROADCAST / BRA.U.ANY) and the issuing warp, not the tensor
+// core, set the pace: ~0.45 us per chunk against ~0.2 us of MMA work
+// (tools/tf32_timeline.py).  Descriptor steps: +32 bytes of K = +2 in the
+// smem descriptor's address field, +8 TMEM columns.
+__device__ __forceinline__ void mma_chunk_tf32(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t b, uint32_t idesc_all,
+                                               uint32_t idesc_hi, uint32_t accumulate, uint32_t bar) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+        "{\n\t"
+        ".reg .pred e, pa, pt;\n\t"
+        ".reg .b32 rx, h1, h2, h3, l1, l2, l3;\n\t"
+        ".reg .b64 b1, b2, b3;\n\t"
+        "elect.sync rx|e, 0xffffffff;\n\t"
+        "setp.ne.b32 pa, %6, 0;\n\t"
+        "setp.eq.b32 pt, %6, %6;\n\t"
+        "add.s64 b1, %3, 2;\n\t"
+        "add.s64 b2, %3, 4;\n\t"
+        "add.s64 b3, %3, 6;\n\t"
+        "add.u32 h1, %1, 8;\n\t"
+        "add.u32 h2, %1, 16;\n\t"
+        "add.u32 h3, %1, 24;\n\t"
+        "add.u32 l1, %2, 8;\n\t"
+        "add.u32 l2, %2, 16;\n\t"
+        "add.u32 l3, %2, 24;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %4, pa;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [h1], b1, %4, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [l1], b1, %5, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [h2], b2, %4, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [l2], b2, %5, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [h3], b3, %4, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [l3], b3, %5, pt;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t"
+        "}" ::"r"(d),
+        "r"(ahi), "r"(alo), "l"(b), "r"(idesc_all), "r"(idesc_hi), "r"(accumulate), "r"(bar)
+        : "memory");
 }
 
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
+// tcgen05.commit by the elected lane of a converged warp.
+__device__ __forceinline__ void mma_commit_warp(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 rx;\n\t"
+        "elect.sync rx|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
 }
+
 
 // 32 consecutive TMEM columns of this warp's 32 lanes -> r[0..31] (no wait).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -314,18 +351,11 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
                 mbar_wait(ops_full(s), (g / kOps) & 1);
                 if (lane == 0) trace_stamp(dbg, 4, g);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lane == 0 && !(dbg & 1)) {
+                if (!(dbg & 1)) {
                     const uint32_t ahi = tmem_base + kOpsCol0 + s * 64, alo = ahi + 32;
                     const uint32_t bq = base + kOffQ + kc * kQChunkBytes;
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        // D[:, 0:32QB] += C_hi.Q_hi, D[:, 32QB:64QB] += C_hi.Q_lo
-                        mma_ts(d, ahi + kk * 8, umma_desc(bq + kk * 32), Cf::kIdescAll, (kc | kk) != 0);
-                        // D[:, 0:32QB] += C_lo.Q_hi (B = the first 32 QB rows)
-                        mma_ts(d, alo + kk * 8, umma_desc(bq + kk * 32), Cf::kIdescHi, 1);
-                    }
-                    mma_commit(ops_empty(s));
-                    if (kc == kChunks - 1) mma_commit(tfull_bar(acc));
+                    mma_chunk_tf32(d, ahi, alo, umma_desc(bq), Cf::kIdescAll, Cf::kIdescHi, uint32_t(kc), ops_empty(s));
+                    if (kc == kChunks - 1) mma_commit_warp(tfull_bar(acc));
                 } else if (lane == 0) {  // dbg & 1: no MMAs (pipeline experiment)
                     mbar_arrive(ops_empty(s));
                     if (kc == kChunks - 1) mbar_arrive(tfull_bar(acc));
@@ -390,6 +420,7 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
                 __syncwarp();
                 if (lane == 0) mbar_arrive(ops_full(o));
                 if (warp == 4 && lane == 0) trace_stamp(dbg, 3, go);
+                if (warp == 7 && lane == 0) trace_stamp(dbg, 7, go);
             }
         }
     } else if (warp >= 8) {

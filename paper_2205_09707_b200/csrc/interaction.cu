@@ -369,21 +369,36 @@ ivf_accumulate_kernel(const uint32_t* __restrict__ list, const unsigned long lon
 // Key histogram for the stage-2 select (select_top_hist): bucket = top 16
 // key bits; warp-aggregated, the score-0 bucket of the all-masked candidates
 // counted per block.
-__device__ __forceinline__ void hist_key(SelectHist* hs, uint64_t key, bool valid, uint32_t* zeros) {
+// Block sums (SelectHist::blk, one per 2048 buckets) are gathered per CTA in
+// shared memory and flushed once at its end (hist_flush).
+__device__ __forceinline__ void hist_key(SelectHist* hs, uint64_t key, bool valid, uint32_t* zeros,
+                                         uint32_t* blk_s) {
     const uint32_t lane = dev::lane_id();
     const uint32_t b = valid ? uint32_t(key >> kHistShift) : 0xFFFFFFFFu;
     const uint32_t peers = __match_any_sync(0xffffffffu, b);
     if (valid && lane == uint32_t(__ffs(peers) - 1)) {
         if (b == kHistZeroBucket) atomicAdd(zeros, uint32_t(__popc(peers)));
-        else atomicAdd(&hs->hist[dev::hist_slot(b)], uint32_t(__popc(peers)));
+        else {
+            atomicAdd(&hs->hist[dev::hist_slot(b)], uint32_t(__popc(peers)));
+            atomicAdd(&blk_s[b >> 11], uint32_t(__popc(peers)));
+        }
     }
+}
+
+__device__ __forceinline__ void hist_flush(SelectHist* hs, uint32_t zeros, const uint32_t* blk_s) {
+    if (threadIdx.x == 0 && zeros) {
+        atomicAdd(&hs->hist[dev::hist_slot(kHistZeroBucket)], zeros);
+        atomicAdd(&hs->blk[kHistZeroBucket >> 11], zeros);
+    }
+    if (threadIdx.x < 32 && blk_s[threadIdx.x]) atomicAdd(&hs->blk[threadIdx.x], blk_s[threadIdx.x]);
 }
 
 __device__ __forceinline__ void stage2_finalize(const uint32_t* __restrict__ c1, uint64_t n, uint32_t rows,
                                                 uint32_t* __restrict__ acc, const uint32_t* __restrict__ used_bits,
                                                 uint64_t* __restrict__ keys_out, SelectHist* __restrict__ hs) {
-    __shared__ uint32_t zeros;
+    __shared__ uint32_t zeros, blk_s[32];
     if (threadIdx.x == 0) zeros = 0;
+    if (threadIdx.x < 32) blk_s[threadIdx.x] = 0;
     __syncthreads();
     for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; i0 < n;
          i0 += uint64_t(gridDim.x) * blockDim.x) {
@@ -407,10 +422,10 @@ __device__ __forceinline__ void stage2_finalize(const uint32_t* __restrict__ c1,
             key = dev::make_key(sc, c1[i]);
             keys_out[i] = key;
         }
-        hist_key(hs, key, i < n, &zeros);
+        hist_key(hs, key, i < n, &zeros, blk_s);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && zeros) atomicAdd(&hs->hist[dev::hist_slot(kHistZeroBucket)], zeros);
+    hist_flush(hs, zeros, blk_s);
 }
 
 // fallback when the kept lists are long: warp per candidate over its codes
@@ -430,6 +445,7 @@ __device__ __forceinline__ void ci_all(const uint32_t* __restrict__ codes, const
             const uint64_t key = dev::make_key(total, pid);
             keys_out[i] = key;
             atomicAdd(&hs->hist[dev::hist_slot(uint32_t(key >> kHistShift))], 1u);
+            atomicAdd(&hs->blk[uint32_t(key >> kHistShift) >> 11], 1u);
         }
         rows_local += used;
     }

@@ -49,6 +49,7 @@ constexpr uint32_t kHistShift = 48;          // bucket = key >> 48: sign, expone
 constexpr uint32_t kHistZeroBucket = 0x8000u; // bucket of score 0 (the all-masked stage-2 candidates)
 struct SelectHist {
     unsigned int hist[65536];
+    unsigned int blk[32];       // per 2048-bucket block: the sum of its counts
     unsigned long long above;   // keys in buckets above the boundary bucket
     unsigned long long bcount;  // keys in the boundary bucket
     unsigned long long rem;     // boundary keys still to take

@@ -111,43 +111,97 @@ scores_exact_kernel(const float* __restrict__ C, uint64_t K, uint32_t dim,
     for (int j = 0; j < NP; ++j) out[j] = top[j];
 }
 
-// One block per query token: merge every warp's top-NP list for that token.
 // One CTA: token i's best NP keys over the nwarps partial lists, left
-// descending in lists[0..NP).
+// descending in lists[0..NP) (lists: blockDim x NP u64 of shared memory).
+// Latency-shaped: each thread has all of its lists' loads in flight at once
+// (the 8 epilogue warps of every S_cq CTA leave ~1200 lists per token), then
+// a butterfly of shuffles merges the warp's lists (the sets are disjoint at
+// every level, so the unique-key insert applies) and warp 0 merges the warps.
 template <int NP>
 __device__ void merge_token_lists(const uint64_t* __restrict__ partial, uint32_t nwarps, uint32_t i,
                                   uint64_t* lists) {
+    if constexpr (NP > 8) {  // long lists: tree of two-pointer merges
+        uint64_t top[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) top[j] = 0;
+        for (uint32_t w = threadIdx.x; w < nwarps; w += blockDim.x) {
+            const uint64_t* l = partial + (uint64_t(w) * 32 + i) * NP;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) dev::topn_insert<NP>(top, l[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < NP; ++j) lists[threadIdx.x * NP + j] = top[j];
+        __syncthreads();
+        for (uint32_t s = blockDim.x / 2; s > 0; s >>= 1) {
+            const bool active = threadIdx.x < s;
+            uint64_t out[NP];
+            if (active) {  // two-pointer merge of two descending lists, keep NP
+                const uint64_t* a = lists + threadIdx.x * NP;
+                const uint64_t* b = lists + (threadIdx.x + s) * NP;
+                int ia = 0, ib = 0;
+#pragma unroll
+                for (int j = 0; j < NP; ++j) {
+                    uint64_t va = ia < NP ? a[ia] : 0, vb = ib < NP ? b[ib] : 0;
+                    if (va > vb) { out[j] = va; ++ia; } else { out[j] = vb; ++ib; }
+                }
+            }
+            __syncthreads();
+            if (active) {
+#pragma unroll
+                for (int j = 0; j < NP; ++j) lists[threadIdx.x * NP + j] = out[j];
+            }
+            __syncthreads();
+        }
+        return;
+    }
     uint64_t top[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) top[j] = 0;
-    for (uint32_t w = threadIdx.x; w < nwarps; w += blockDim.x) {
-        const uint64_t* l = partial + (uint64_t(w) * 32 + i) * NP;
+    constexpr int kPer = NP <= 4 ? 8 : 2;  // lists per thread per round
+    for (uint32_t w0 = 0; w0 < nwarps; w0 += kPer * blockDim.x) {
+        uint64_t v[kPer][NP];
 #pragma unroll
-        for (int j = 0; j < NP; ++j) dev::topn_insert<NP>(top, l[j]);
+        for (int u = 0; u < kPer; ++u) {
+            const uint32_t w = w0 + u * blockDim.x + threadIdx.x;
+            const uint64_t* l = partial + (uint64_t(w < nwarps ? w : 0) * 32 + i) * NP;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) v[u][j] = w < nwarps ? __ldcg(l + j) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+#pragma unroll
+            for (int j = 0; j < NP; ++j) dev::topn_insert<NP>(top, v[u][j]);
     }
 #pragma unroll
-    for (int j = 0; j < NP; ++j) lists[threadIdx.x * NP + j] = top[j];
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t pv[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) pv[j] = __shfl_xor_sync(0xffffffffu, top[j], o);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) dev::topn_insert<NP>(top, pv[j]);
+    }
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) lists[warp * NP + j] = top[j];
     __syncthreads();
-    for (uint32_t s = blockDim.x / 2; s > 0; s >>= 1) {
-        const bool active = threadIdx.x < s;
-        uint64_t out[NP];
-        if (active) {  // two-pointer merge of two descending lists, keep NP
-            const uint64_t* a = lists + threadIdx.x * NP;
-            const uint64_t* b = lists + (threadIdx.x + s) * NP;
-            int ia = 0, ib = 0;
+    if (warp == 0) {
 #pragma unroll
-            for (int j = 0; j < NP; ++j) {
-                uint64_t va = ia < NP ? a[ia] : 0, vb = ib < NP ? b[ib] : 0;
-                if (va > vb) { out[j] = va; ++ia; } else { out[j] = vb; ++ib; }
-            }
-        }
-        __syncthreads();
-        if (active) {
+        for (int j = 0; j < NP; ++j) top[j] = lane < nw ? lists[lane * NP + j] : 0ull;
 #pragma unroll
-            for (int j = 0; j < NP; ++j) lists[threadIdx.x * NP + j] = out[j];
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t pv[NP];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) pv[j] = __shfl_xor_sync(0xffffffffu, top[j], o);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) dev::topn_insert<NP>(top, pv[j]);
         }
-        __syncthreads();
     }
+    __syncthreads();  // every warp's row of lists was read
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) lists[j] = top[j];
+    __syncthreads();
 }
 
 template <int NP>

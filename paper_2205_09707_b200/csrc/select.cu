@@ -345,11 +345,9 @@ __global__ void copy_count_kernel(const uint64_t* src, uint64_t* dst, uint64_t c
 
 // Per-query prologue, one PDL-chained launch instead of a memset plus a
 // validation kernel: every CTA zeroes its share of the per-query counters and
-// bitmaps; when q != nullptr CTA 0 also checks the query rows
+// bitmaps; when q != nullptr the last CTA also checks the query rows
 // (check_unit_rows, types.cpp:10-19: norm^2 = sum of double(v)^2 in order —
-// the products are exact in fp64, so only the adds must stay in order: 32-dim
-// chunks are staged coalesced in shared memory and thread r runs row r's add
-// chain from there).
+// the products are exact in fp64, so only the adds must stay in order).
 // bf16 bits of x rounded to nearest even (finite inputs)
 __device__ __forceinline__ uint32_t bf16_rn_u32(float x) {
     const uint32_t u = __float_as_uint(x);
@@ -362,30 +360,34 @@ __device__ __forceinline__ uint32_t bf16_rn_u32(float x) {
 // Q_lo = bf16(q - Q_hi); zero rows past `rows`), SWIZZLE_128B K-major chunks
 // of 64 bf16: chunk c, row n, 16-byte granule j at c * 8192 + n * 128 +
 // ((j ^ (n & 7)) << 4).
-__device__ __forceinline__ void build_qimg(const float* __restrict__ q, uint32_t rows, uint4* __restrict__ img) {
-    for (uint32_t e = threadIdx.x; e < launch::kQImgBytes / 16; e += blockDim.x) {
-        const uint32_t c = e >> 9, n = (e >> 3) & 63, j = e & 7;
-        const uint32_t i = n & 31, k0 = c * 64 + j * 8, d0 = k0 & 127;
-        const bool lo = n >= 32;
-        uint32_t v[4] = {0, 0, 0, 0};
-        if (i < rows && !(lo && k0 >= 128)) {
-            const float4 a = reinterpret_cast<const float4*>(q + i * 128 + d0)[0];
-            const float4 b = reinterpret_cast<const float4*>(q + i * 128 + d0)[1];
-            const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+// One 16-byte granule e of the image (e < kQImgBytes / 16).
+__device__ __forceinline__ void qimg_granule(const float* __restrict__ q, uint32_t rows, uint32_t e,
+                                             uint4* __restrict__ img) {
+    const uint32_t c = e >> 9, n = (e >> 3) & 63, j = e & 7;
+    const uint32_t i = n & 31, k0 = c * 64 + j * 8, d0 = k0 & 127;
+    const bool lo = n >= 32;
+    uint32_t v[4] = {0, 0, 0, 0};
+    if (i < rows && !(lo && k0 >= 128)) {
+        const float4 a = reinterpret_cast<const float4*>(q + i * 128 + d0)[0];
+        const float4 b = reinterpret_cast<const float4*>(q + i * 128 + d0)[1];
+        const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                uint32_t h0 = bf16_rn_u32(f[2 * u]), h1 = bf16_rn_u32(f[2 * u + 1]);
-                if (lo) {
-                    h0 = bf16_rn_u32(f[2 * u] - __uint_as_float(h0 << 16));
-                    h1 = bf16_rn_u32(f[2 * u + 1] - __uint_as_float(h1 << 16));
-                }
-                v[u] = h0 | (h1 << 16);
+        for (int u = 0; u < 4; ++u) {
+            uint32_t h0 = bf16_rn_u32(f[2 * u]), h1 = bf16_rn_u32(f[2 * u + 1]);
+            if (lo) {
+                h0 = bf16_rn_u32(f[2 * u] - __uint_as_float(h0 << 16));
+                h1 = bf16_rn_u32(f[2 * u + 1] - __uint_as_float(h1 << 16));
             }
+            v[u] = h0 | (h1 << 16);
         }
-        img[(c * 8192 + n * 128 + ((j ^ (n & 7)) << 4)) / 16] = make_uint4(v[0], v[1], v[2], v[3]);
     }
+    img[(c * 8192 + n * 128 + ((j ^ (n & 7)) << 4)) / 16] = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
+// Every piece of the prologue is spread over the whole grid (one element per
+// thread), so none of it is a serial chain of round trips on one CTA: the
+// query rows may sit in pinned host memory (host path), where each dependent
+// load costs a PCIe round trip, and the S_cq kernel waits for this grid.
 __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __restrict__ q, uint32_t rows, uint32_t dim,
                                                               int* __restrict__ status, uint4* __restrict__ zero,
                                                               uint64_t n16, uint4* __restrict__ zero2, uint64_t m16,
@@ -396,37 +398,47 @@ __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __rest
     // table (no dependence on this kernel) while the zero fill runs; its other
     // warps still wait for this grid to complete
     dev::pdl_trigger();
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16 + m16;
-         i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t gt = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x, nt = uint64_t(gridDim.x) * blockDim.x;
+    // host path: the query rows come straight from the caller's pinned
+    // (mapped) staging buffer — no separate H2D copy ahead of this kernel
+    if (qcopy)
+        for (uint64_t i = gt; i < ncopy4; i += nt)
+            reinterpret_cast<float4*>(qcopy)[i] = reinterpret_cast<const float4*>(qsrc)[i];
+    if (qimg)
+        for (uint64_t e = gt; e < launch::kQImgBytes / 16; e += nt) qimg_granule(qsrc, rows, uint32_t(e), qimg);
+    for (uint64_t i = gt; i < n16 + m16; i += nt) {
         if (i < n16) zero[i] = make_uint4(0, 0, 0, 0);
         else zero2[i - n16] = make_uint4(0, 0, 0, 0);
     }
-    // host path: the query rows come straight from the caller's pinned
-    // (mapped) staging buffer — no separate H2D copy ahead of this kernel
-    if (qcopy && blockIdx.x == 0)
-        for (uint32_t i = threadIdx.x; i < ncopy4; i += blockDim.x)
-            reinterpret_cast<float4*>(qcopy)[i] = reinterpret_cast<const float4*>(qsrc)[i];
-    if (qimg && blockIdx.x == gridDim.x - 1) build_qimg(qsrc, rows, qimg);
-    if (blockIdx.x != 0 || q == nullptr) return;
-    __shared__ float tile[32][33];
-    const uint32_t t = threadIdx.x;
+    // the norm check of row r (check_unit_rows, types.cpp:10-19) in the last
+    // CTA: 128-dim slabs of all rows staged with one coalesced round of loads,
+    // then thread r runs row r's in-order fp64 add chain from shared memory
+    // (the squares are exact in fp64)
+    if (q == nullptr || blockIdx.x != gridDim.x - 1) return;
+    __shared__ float slab[32][129];
     double acc = 0.0;
-    for (uint32_t d0 = 0; d0 < dim; d0 += 32) {
-        for (uint32_t i = t; i < 32 * 32; i += blockDim.x) {
-            const uint32_t r = i >> 5, d = d0 + (i & 31);
-            tile[r][i & 31] = r < rows && d < dim ? q[size_t(r) * dim + d] : 0.f;
+    for (uint32_t d0 = 0; d0 < dim; d0 += 128) {
+        const uint32_t w = dim - d0 < 128 ? dim - d0 : 128;
+        float v[16];  // 32 x 128 / 256 threads: every load in flight at once
+#pragma unroll
+        for (uint32_t k = 0; k < 16; ++k) {
+            const uint32_t i = threadIdx.x + k * 256, r = i >> 7, d = i & 127;
+            v[k] = r < rows && d < w ? q[size_t(r) * dim + d0 + d] : 0.f;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < 16; ++k) {
+            const uint32_t i = threadIdx.x + k * 256;
+            slab[i >> 7][i & 127] = v[k];
         }
         __syncthreads();
-        if (t < rows) {
-            const uint32_t m = dim - d0 < 32 ? dim - d0 : 32;
-            for (uint32_t j = 0; j < m; ++j) {
-                const double v = double(tile[t][j]);
+        if (threadIdx.x < rows)
+            for (uint32_t d = 0; d < w; ++d) {
+                const double v = double(slab[threadIdx.x][d]);
                 acc = __dadd_rn(acc, __dmul_rn(v, v));
             }
-        }
         __syncthreads();
     }
-    if (t >= rows) return;
+    if (threadIdx.x >= rows) return;
     const double norm = sqrt(acc);
     if (fabs(norm - 1.0) > double(1e-3f)) atomicExch(status, 2);  // NotNormalized + 1
 }
@@ -457,95 +469,99 @@ uint64_t next_pow2(uint64_t v) {
 constexpr uint32_t kHistBucketShift = kHistShift;
 constexpr uint32_t kRankCap = 8192;  // boundary buckets up to this size are ranked in parallel
 
-// One CTA: the bucket (from the top) holding the want-th largest key.  Warp
-// w sums buckets [2048 w, 2048 w + 2048) (one transposed block, see
-// dev::hist_slot) with coalesced loads; the warp whose range holds the target
-// stages its block in shared memory and walks it from the top, 32 buckets per
-// step.  Also (re)initialises the control words for this select.
-__global__ void __launch_bounds__(1024) hist_find_kernel(const uint64_t* __restrict__ d_n, uint64_t want,
-                                                         SelectHist* __restrict__ st) {
-    dev::pdl_wait();
-    __shared__ unsigned long long warp_tot[32];
-    __shared__ uint32_t blk[32 * 65];  // the target block, row l = buckets 32 j + l (padded)
-    const uint64_t n = *d_n;
+// The bucket (from the top) holding the want-th largest key, found by every
+// CTA of the compaction for itself (no separate single-CTA launch): the 32
+// block sums SelectHist::blk (one L2 round trip) give the block, then thread t
+// sums buckets [8 t, 8 t + 8) of that block (one more round trip) and a
+// block-wide suffix scan gives the bucket.  256 threads.
+struct HistBoundary {
+    unsigned long long above, bcount, rem;
+    uint32_t bucket, take_all;
+};
+
+__device__ __forceinline__ void hist_boundary(const SelectHist* __restrict__ st, uint64_t n, uint64_t want,
+                                              HistBoundary& hb /* shared */) {
+    __shared__ unsigned long long blk_above;
+    __shared__ uint32_t blk_id, wsum[8];
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    if (t == 0) {
-        st->take_all = n <= want;
-        st->bn = 0;
-        st->bcount = 0;
-        st->rem = 0;
-        st->above = 0;
-        st->bucket = 0;
+    if (t == 0) {  // defaults select nothing should the sums ever disagree with n
+        blk_id = 0, blk_above = 0;
+        hb.take_all = 0, hb.bucket = 0xFFFFFFFFu, hb.above = 0, hb.bcount = 0, hb.rem = 0;
     }
-    if (n <= want) return;
     __syncthreads();
-    // the warp's 8 KB block as 16 x 16-byte loads per lane, 8 in flight at a
-    // time (the 64-register cap of a 1024-thread CTA): 2 L2 round trips
-    const uint4* hw4 = reinterpret_cast<const uint4*>(st->hist + warp * 2048);
-    unsigned long long mine = 0;
-#pragma unroll
-    for (uint32_t h = 0; h < 2; ++h) {
-        uint4 v[8];
-#pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) v[j] = __ldcg(hw4 + (h * 8 + j) * 32 + lane);
-#pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) mine += uint64_t(v[j].x) + v[j].y + v[j].z + v[j].w;
+    if (n <= want) {
+        if (t == 0) hb.take_all = 1, hb.bucket = 0, hb.above = 0, hb.bcount = 0, hb.rem = 0;
+        __syncthreads();
+        return;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if (lane == 0) warp_tot[warp] = mine;
-    __syncthreads();
-    // keys in the warps' ranges above this one (higher buckets = higher warps)
-    unsigned long long above = 0;
-    for (uint32_t w = warp + 1; w < 32; ++w) above += warp_tot[w];
-    if (!(above < want && want <= above + warp_tot[warp])) return;
-#pragma unroll
-    for (uint32_t h = 0; h < 2; ++h) {
-        uint4 v[8];
-#pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) v[j] = __ldcg(hw4 + (h * 8 + j) * 32 + lane);
-#pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) {
-            const uint32_t a = 4 * ((h * 8 + j) * 32 + lane);  // slots a .. a + 3 (one row of blk)
-            uint32_t* r = blk + (a >> 6) * 65 + (a & 63);
-            r[0] = v[j].x, r[1] = v[j].y, r[2] = v[j].z, r[3] = v[j].w;
-        }
-    }
-    __syncwarp();
-    for (int j = 63; j >= 0; --j) {
-        const uint32_t c = blk[lane * 65 + j];  // bucket 32 j + lane
-        // inclusive sum from the top lane down (bucket 32 j + 31 first)
-        uint32_t incl = c;
+    if (warp == 0) {
+        const uint32_t c = __ldcg(&st->blk[lane]);
+        // inclusive suffix sum: keys in blocks >= lane (higher blocks = higher keys)
+        unsigned long long incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_down_sync(0xffffffffu, incl, o);
+            const unsigned long long y = __shfl_down_sync(0xffffffffu, incl, o);
             if (lane + o < 32) incl += y;
         }
-        const uint32_t chunk = __shfl_sync(0xffffffffu, incl, 0);
-        if (above + chunk >= want) {
-            const bool hit = above + incl >= want && above + incl - c < want;
-            if (hit) {
-                st->bucket = warp * 2048 + j * 32 + lane;
-                st->above = above + incl - c;
-                st->bcount = c;
-                st->rem = want - (above + incl - c);
-            }
-            return;
-        }
-        above += chunk;
+        if (incl >= want && incl - c < want) blk_id = lane, blk_above = incl - c;
     }
+    __syncthreads();
+    const uint32_t B = blk_id;
+    uint32_t v[8], mine = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        v[j] = __ldcg(&st->hist[dev::hist_slot(B * 2048 + 8 * t + j)]);
+        mine += v[j];
+    }
+    // suffix scan over the 256 threads (thread 255 holds the top buckets)
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += y;
+    }
+    if (lane == 0) wsum[warp] = incl;
+    __syncthreads();
+    unsigned long long above = blk_above;
+    for (uint32_t w = warp + 1; w < 8; ++w) above += wsum[w];
+    above += incl - mine;  // keys in this block above thread t's buckets
+    if (above < want && want <= above + mine) {
+        for (int j = 7; j >= 0; --j) {
+            if (above + v[j] >= want) {
+                hb.take_all = 0;
+                hb.bucket = B * 2048 + 8 * t + uint32_t(j);
+                hb.above = above;
+                hb.bcount = v[j];
+                hb.rem = want - above;
+                break;
+            }
+            above += v[j];
+        }
+    }
+    __syncthreads();
 }
 
-__global__ void hist_compact_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
-                                    SelectHist* __restrict__ st, uint64_t* __restrict__ bkeys,
-                                    uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
+// Keys above the boundary bucket go to out, the boundary bucket's keys to
+// bkeys (then hist_resolve).  CTA 0 records the boundary for hist_resolve,
+// which also re-zeroes the histogram for the next select.
+__global__ void __launch_bounds__(256) hist_compact_kernel(const uint64_t* __restrict__ keys,
+                                                           const uint64_t* __restrict__ d_n, uint64_t want,
+                                                           SelectHist* __restrict__ st, uint64_t* __restrict__ bkeys,
+                                                           uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
     dev::pdl_wait();
     const uint64_t n = *d_n;
-    const bool all = st->take_all;
-    const uint32_t bucket = st->bucket;
+    __shared__ HistBoundary hb;
+    hist_boundary(st, n, want, hb);
+    const bool all = hb.take_all;
+    const uint32_t bucket = hb.bucket;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->take_all = hb.take_all;
+        st->bucket = hb.bucket;
+        st->above = hb.above;
+        st->bcount = hb.bcount;
+        st->rem = hb.rem;
+    }
     const uint32_t lane = threadIdx.x & 31;
-    // hist_find has consumed the histogram: leave it zero for the next select
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < 65536; b += gridDim.x * blockDim.x) st->hist[b] = 0;
     // one atomic per CTA and output (the CTA's warps take consecutive ranges):
     // per-warp atomics on the two counters queue on one L2 slice
     __shared__ uint32_t wa[32], wb[32];
@@ -592,6 +608,14 @@ hist_resolve_kernel(SelectHist* __restrict__ st, const uint64_t* __restrict__ bk
                     uint64_t* __restrict__ out_n) {
     dev::pdl_wait();
     extern __shared__ __align__(16) uint64_t s[];
+    // the compaction has consumed the histogram: leave it (and the boundary
+    // counter) zero for the next select
+    {
+        uint4* h4 = reinterpret_cast<uint4*>(st->hist);
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (65536 + 32) / 4; i += gridDim.x * blockDim.x)
+            h4[i] = make_uint4(0, 0, 0, 0);  // hist and blk are contiguous
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->bn = 0;
+    }
     if (st->take_all) return;
     const uint32_t nb = uint32_t(st->bcount);
     const uint64_t rem = st->rem;
@@ -900,9 +924,8 @@ void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax,
                      uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st) {
     if (nmax == 0) return;
     const uint32_t grid = grid_for(nmax, 256, uint32_t(sm_count()) * 8);
-    ::plaid::launch::pdl(hist_find_kernel, 1, 1024, 0, st, d_n, want, d_st);
-    count_launch();
-    ::plaid::launch::pdl(hist_compact_kernel, grid, 256, 0, st, d_keys, d_n, d_st, d_bkeys, d_out_keys, d_out_n);
+    ::plaid::launch::pdl(hist_compact_kernel, grid, 256, 0, st, d_keys, d_n, want, d_st, d_bkeys, d_out_keys,
+                         d_out_n);
     count_launch();
     static launch::PerDeviceOnce cfg;
     if (cfg.first()) {

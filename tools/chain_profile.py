@@ -7,9 +7,10 @@ chain — unlike ncu's serialised launch list, overlap with its neighbours
 (PDL prologues, tails) is included.  Results of truncated searches are
 garbage; only the times are read.  Run under gpurun:
 
-    python tools/chain_profile.py [cfg2] [steps]
+    python tools/chain_profile.py [cfg2] [steps] [caps, e.g. 0,1,2]
 """
 import sys
+import time
 from pathlib import Path
 
 import numpy as np
@@ -20,6 +21,9 @@ import bench  # noqa: E402
 import paper_2205_09707_b200 as P  # noqa: E402
 from paper_2205_09707_b200 import _native  # noqa: E402
 
+import os
+
+PAD = int(os.environ.get("PAD_CYCLES", "0"))
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 cfg = dict(bench.CONFIGS[name])
@@ -48,25 +52,31 @@ def timed(cap):
     # a fresh searcher per cap: kernels that never run leave no stale state
     # behind for the ones that do
     t = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR, record_times=False, use_graphs=False)
-    ms = []
+    ms, host = [], []
     for i in range(steps + 5):
         flush.zero_()
+        if PAD:  # keep the GPU busy until the whole chain is enqueued (host-bound check)
+            torch.cuda._sleep(PAD)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
+        h0 = time.perf_counter()
         t.search_device(dq[i % 64].data_ptr(), 1, 32, 128, p, d_pids.data_ptr(), d_scores.data_ptr(),
                         d_n.data_ptr(), stream=sh)
+        h1 = time.perf_counter()
         b.record(stream)
         b.synchronize()
         if i >= 5:
             ms.append(a.elapsed_time(b) * 1e3)
+            host.append((h1 - h0) * 1e6)
     lib.plaid_debug_set_launch_cap(-1)
     t.close()
-    return float(np.median(ms)), float(np.min(ms))
+    return float(np.median(ms)), float(np.min(ms)), float(np.median(host))
 
 
 print(f"{name}: {full} launches per search; median / min step us with the chain cut after each launch")
 prev = 0.0
-for cap in list(range(1, full + 1)):
-    med, mn = timed(cap)
-    print(f"cap {cap:2d}: median {med:7.2f} us  min {mn:7.2f}  marginal {med - prev:+7.2f}")
+caps = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(0, full + 1))
+for cap in caps:
+    med, mn, hst = timed(cap)
+    print(f"cap {cap:2d}: median {med:7.2f} us  min {mn:7.2f}  marginal {med - prev:+7.2f}  (host enqueue {hst:6.1f} us)")
     prev = med

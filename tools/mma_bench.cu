@@ -16,11 +16,11 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr) {
     return d;
 }
 
-template <int N, bool TS, int CONT = 0, int NACC = 2>
+template <int N, bool TS, int CONT = 0, int NACC = 2, int MIX = 0, int CE = 0>
 __global__ void bench(unsigned long long* out, int iters) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint32_t tslot;
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar, bar2;
     const uint32_t warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < 128 * 128 + N * 128; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.001f;
     if (warp == 0) {
@@ -28,6 +28,7 @@ __global__ void bench(unsigned long long* out, int iters) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2)));
     asm volatile("fence.proxy.async.shared::cta;");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -54,7 +55,21 @@ __global__ void bench(unsigned long long* out, int iters) {
         long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
             const uint32_t d = NACC == 1 ? tm : NACC == 2 ? tm + (it & 1) * 256 : tm + (it & 3) * 64;
-            if (TS) {
+            if (MIX) {
+                // the S_cq pattern: C_hi . [Q_hi | Q_lo] (N) then C_lo . Q_hi (N/2 when MIX = 1) into one D
+                const uint32_t idesc2 = MIX == 1 ? ((1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t(N / 2) >> 3) << 17) |
+                                                    ((128u >> 4) << 24))
+                                                 : idesc;
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                             "r"(tm + 256 + 8 * (it & 3)), "l"(desc(b + (it & 3) * 32)), "r"(idesc), "r"(it > 1 ? 1 : 0));
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                             "r"(tm + 288 + 8 * (it & 3)), "l"(desc(b + (it & 3) * 32)), "r"(idesc2), "r"(1));
+                if (CE && (it % CE) == CE - 1)  // a commit every CE iterations (the S_cq loop commits per chunk)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_u32(&bar2)));
+            } else if (TS) {
                 asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                              "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
                              "r"(tm + 256 + 32 * 0), "l"(desc(b + (it & 3) * 32)), "r"(idesc), "r"(it > 1 ? 1 : 0));
@@ -75,15 +90,16 @@ __global__ void bench(unsigned long long* out, int iters) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512));
 }
 
-template <int N, bool TS, int CONT = 0, int NACC = 2>
+template <int N, bool TS, int CONT = 0, int NACC = 2, int MIX = 0, int CE = 0>
 void run(unsigned long long* d, int iters) {
     const int smem = 128 * 128 * 4 + 256 * 128 * 4 + 2048;
-    cudaFuncSetAttribute(bench<N, TS, CONT, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    bench<N, TS, CONT, NACC><<<1, 128, smem>>>(d, iters);
+    cudaFuncSetAttribute(bench<N, TS, CONT, NACC, MIX, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench<N, TS, CONT, NACC, MIX, CE><<<1, 128, smem>>>(d, iters);
     cudaDeviceSynchronize();
     unsigned long long h = 0;
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    printf("N=%3d %s cont=%d nacc=%d: %.1f cycles/MMA (%s)\n", N, TS ? "TS" : "SS", CONT, NACC, double(h) / iters,
+    printf("N=%3d %s cont=%d nacc=%d mix=%d commit/%d: %.1f cycles/MMA (%s)\n", N, TS ? "TS" : "SS", CONT, NACC, MIX, CE,
+           double(h) / iters / (MIX ? 2 : 1),
            cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -111,5 +127,14 @@ int main() {
     run<32, true, 0, 4>(d, it);
     run<128, true, 0, 1>(d, it);
     run<64, true, 3, 1>(d, it);
+    // the S_cq issue pattern (two MMAs per K step into one accumulator)
+    run<64, true, 0, 1, 1>(d, it);
+    run<64, true, 0, 1, 2>(d, it);
+    run<128, true, 0, 1, 1>(d, it);
+    run<128, true, 0, 1, 2>(d, it);
+    run<64, true, 3, 1, 1>(d, it);
+    run<64, true, 3, 1, 2>(d, it);
+    run<64, true, 0, 1, 1, 4>(d, it);
+    run<64, true, 0, 1, 1, 1>(d, it);
     return 0;
 }

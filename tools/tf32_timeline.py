@@ -36,7 +36,8 @@ cta = a[2048:].reshape(2, 256)
 t0 = ev[0, 0]
 names = ["issue", "rawfull", "opsfree", "conv_done", "mmastart"]
 for g in list(range(0, 8)) + list(range(48, 56)):
-    print(g, " ".join(f"{n}={(ev[i, g] - t0) / 1000:7.2f}" for i, n in enumerate(names)))
+    print(g, " ".join(f"{n}={(ev[i, g] - t0) / 1000:7.2f}" for i, n in enumerate(names)),
+          f"conv3_done={(ev[7, g] - t0) / 1000:7.2f}")
 for lt in range(16):
     print("tile", lt, f"tfull={(ev[5, lt] - t0) / 1000:7.2f} epidone={(ev[6, lt] - t0) / 1000:7.2f}")
 nz = cta[0] > 0
