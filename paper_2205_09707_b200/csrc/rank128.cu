@@ -691,22 +691,71 @@ stage4_tensor_kernel(const float* __restrict__ S, const float* __restrict__ tok_
         for (uint32_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++lt) {
             tc_mbar_wait(a_full, lt & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lane == 0) {
-                // D[:, 0:32] = [R_hi | R_lo] . [Q_hi | Q_hi], D[:, 32:64] = [R_hi | R_lo] . [Q_lo | 0]
-#pragma unroll
-                for (uint32_t s = 0; s < 16; ++s) {
-                    const uint64_t bd = tc_desc(base + kTcOffB + (s >> 2) * 8192 + (s & 3) * 32);
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\t"
-                        "setp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + kTcAccCol),
-                        "r"(tmem + 8 * s), "l"(bd), "r"(kTcIdesc), "r"(s));
-                }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 acc_full)
-                             : "memory");
-            }
-            __syncwarp();
+            // D[:, 0:32] = [R_hi | R_lo] . [Q_hi | Q_hi], D[:, 32:64] = [R_hi | R_lo] . [Q_lo | 0]:
+            // 16 K=16 steps (B chunk s >> 2, 32-byte step s & 3: +512 / +2 in the
+            // descriptor's address field; A +8 TMEM columns), issued by the
+            // converged warp with the elected lane predicated inside one asm
+            // block (no per-MMA waterfall loop, see gemm_tf32.cu mma_chunk_tf32)
+            asm volatile(
+                "{\n\t"
+                ".reg .pred e, pz, pt;\n\t"
+                ".reg .b32 rx, ta;\n\t"
+                ".reg .b64 bd;\n\t"
+                "elect.sync rx|e, 0xffffffff;\n\t"
+                "setp.ne.b32 pz, %1, %1;\n\t"
+                "setp.eq.b32 pt, %1, %1;\n\t"
+                "add.s64 bd, %2, 0;\n\t"
+                "add.u32 ta, %1, 0;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pz;\n\t"
+                "add.s64 bd, %2, 2;\n\t"
+                "add.u32 ta, %1, 8;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 4;\n\t"
+                "add.u32 ta, %1, 16;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 6;\n\t"
+                "add.u32 ta, %1, 24;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 512;\n\t"
+                "add.u32 ta, %1, 32;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 514;\n\t"
+                "add.u32 ta, %1, 40;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 516;\n\t"
+                "add.u32 ta, %1, 48;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 518;\n\t"
+                "add.u32 ta, %1, 56;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1024;\n\t"
+                "add.u32 ta, %1, 64;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1026;\n\t"
+                "add.u32 ta, %1, 72;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1028;\n\t"
+                "add.u32 ta, %1, 80;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1030;\n\t"
+                "add.u32 ta, %1, 88;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1536;\n\t"
+                "add.u32 ta, %1, 96;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1538;\n\t"
+                "add.u32 ta, %1, 104;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1540;\n\t"
+                "add.u32 ta, %1, 112;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "add.s64 bd, %2, 1542;\n\t"
+                "add.u32 ta, %1, 120;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, pt;\n\t"
+                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t"
+                "}" ::"r"(tmem + kTcAccCol),
+                "r"(tmem), "l"(tc_desc(base + kTcOffB)), "r"(kTcIdesc), "r"(acc_full)
+                : "memory");
         }
     } else {
         // ---------------- token group: a two-stage software pipeline — while
