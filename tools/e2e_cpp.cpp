@@ -9,7 +9,7 @@
 // lir::SearchResult construction; L2 is flushed (256 MiB write) before every
 // query, outside the timed region, as in bench.py.  Prints one JSON line.
 //
-//   e2e_cpp <N> <K> <nbits> <mean_len> <k> <steps> <warmup> [tensor=1]
+//   e2e_cpp <N> <K> <nbits> <mean_len> <k> <steps> <warmup> [tensor=1] [graphs=1]
 //
 // Built by oracle/Makefile (target e2e) because it needs the reference
 // headers; the binary travels to the GPU box in oracle/_ref/.
@@ -51,6 +51,7 @@ int main(int argc, char** argv) {
     const uint64_t k = std::strtoull(argv[5], nullptr, 10);
     const int steps = std::atoi(argv[6]), warmup = std::atoi(argv[7]);
     const bool tensor = argc < 9 || std::atoi(argv[8]) != 0;
+    const bool graphs = argc < 10 || std::atoi(argv[9]) != 0;
     const uint32_t dim = 128, spread = 16;
 
     // the synthetic corpus (same streams and seeds as bench.py / generate_index)
@@ -84,7 +85,7 @@ int main(int argc, char** argv) {
                  ix.doclens.data(), off.data(), N, nq, 32, 0.03, 1234, qs.data());
 
     try {
-        const plaid_lir::Engine engine(ix, 0, tensor ? PLAID_SCORES_TENSOR : PLAID_SCORES_EXACT);
+        const plaid_lir::Engine engine(ix, 0, tensor ? PLAID_SCORES_TENSOR : PLAID_SCORES_EXACT, false, false, graphs);
         const lir::SearchParams p = lir::default_params_for_k(k);
         std::vector<double> lat;
         uint64_t returned = 0;
@@ -109,9 +110,10 @@ int main(int argc, char** argv) {
         const double total = std::accumulate(lat.begin(), lat.end(), 0.0);
         std::printf("{\"value\": %.3f, \"unit\": \"queries/s\", \"p50_ms\": %.4f, \"mean_ms\": %.4f, \"steps\": %d, "
                     "\"results\": %llu, \"path\": \"C++ plaid_lir::Engine::search (lir::QueryMatrix in host memory "
-                    "-> lir::SearchResult), host clock per query, L2 flushed before each\", \"score_mode\": \"%s\"}\n",
+                    "-> lir::SearchResult), host clock per query, L2 flushed before each\", \"score_mode\": \"%s\", "
+                    "\"graphs\": %s}\n",
                     lat.size() / total, 1e3 * sorted[sorted.size() / 2], 1e3 * total / lat.size(), steps,
-                    (unsigned long long)returned, tensor ? "tensor" : "exact");
+                    (unsigned long long)returned, tensor ? "tensor" : "exact", graphs ? "true" : "false");
         return 0;
     } catch (const std::exception& e) {
         std::printf("{\"error\": \"%s\"}\n", e.what());
