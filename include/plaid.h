@@ -112,8 +112,14 @@ typedef struct plaid_searcher_config {
     int32_t score_mode;     /* plaid_score_mode */
     int32_t record_times;   /* fill the *_ms fields of plaid_trace (adds events) */
     int32_t use_graphs;     /* plaid_search: capture H2D + launches + read-back as one CUDA graph per (rows, params), replay after */
-    int32_t reserved;
+    int32_t batch_engine;   /* plaid_batch_*: plaid_batch_engine */
 } plaid_searcher_config;
+
+/* Throughput-mode engine of plaid_batch_*: waves (one S_cq pass per wave of
+ * queries + one CTA per query for stages 1b-4; used when the shape allows:
+ * d = 128, |Q| <= 32, nprobe <= 8, filter on, stage3_width <= 2048) with the
+ * lanes as fallback, or lanes only. */
+typedef enum plaid_batch_engine { PLAID_BATCH_AUTO = 0, PLAID_BATCH_LANES = 1 } plaid_batch_engine;
 
 /* ---- errors / host-side helpers ------------------------------------------------ */
 const char* plaid_last_error(void);
@@ -297,6 +303,15 @@ plaid_status plaid_batch_search_device(plaid_batch* b, const float* d_q, uint64_
                                        uint64_t stream);
 plaid_status plaid_batch_sync(plaid_batch* b);
 uint64_t plaid_batch_last_launches(const plaid_batch* b);
+/* After a batch that ran on the wave engine: per query [stage1_candidates,
+ * stage2_out, stage3_out, final_out] (lir::StageTrace counters), out[nq][4].
+ * Synchronises.  PLAID_INVALID_PARAMS when the last batch ran on lanes. */
+plaid_status plaid_batch_counters(plaid_batch* b, uint64_t* out, uint64_t nq);
+/* Test hook: the S_cq table (num_centroids x 32 floats, one row per
+ * centroid) the last wave computed for its j-th query (j < wave size). */
+plaid_status plaid_batch_wave_scores(plaid_batch* b, uint64_t j, float* out);
+/* 1 when the last batch ran on the wave engine, else 0. */
+int plaid_batch_last_was_wave(const plaid_batch* b);
 
 /* ---- global-exact passage-sharded search ----------------------------
  * The reference searches one index (pipeline.cpp:232-283); a passage-range

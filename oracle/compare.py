@@ -172,7 +172,7 @@ def check_tensor_search(oracle, h, q, p, got_ids, got_scores, S_t, got_counters=
     if got_counters is not None:
         exp = _counters(ten, disable_filter)
         for kk, v in exp.items():
-            if int(got_counters.get(kk, -1)) != int(v):
+            if kk in got_counters and int(got_counters[kk]) != int(v):
                 rep.fail(f"trace {kk}: GPU {got_counters.get(kk)} vs oracle-on-S_tensor {v}")
     # stages 2 and 3, where stage 1 agreed: differences only at the cut
     if not disable_filter and np.array_equal(ref["c1"], ten["c1"]) and len(ref["c1"]):

@@ -61,7 +61,7 @@ class BuildDesc(C.Structure):
 
 class SearcherConfig(C.Structure):
     _fields_ = [("score_mode", C.c_int32), ("record_times", C.c_int32),
-                ("use_graphs", C.c_int32), ("reserved", C.c_int32)]
+                ("use_graphs", C.c_int32), ("batch_engine", C.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/plaid.h
@@ -104,6 +104,9 @@ SIGNATURES = {
                                             C.POINTER(Params), C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     "plaid_batch_sync": (C.c_int, [C.c_void_p]),
     "plaid_batch_last_launches": (C.c_uint64, [C.c_void_p]),
+    "plaid_batch_counters": (C.c_int, [C.c_void_p, u64p, C.c_uint64]),
+    "plaid_batch_last_was_wave": (C.c_int, [C.c_void_p]),
+    "plaid_batch_wave_scores": (C.c_int, [C.c_void_p, C.c_uint64, f32p]),
     "plaid_shard_phase1_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(Params),
                                             C.c_void_p, C.c_uint64, C.c_uint64]),
     "plaid_shard_phase2_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
@@ -154,6 +157,7 @@ SIGNATURES = {
     # test knobs (not part of include/plaid.h)
     "plaid_debug_set_tf32_grid": (C.c_uint32, [C.c_uint32]),
     "plaid_debug_set_launch_cap": (C.c_longlong, [C.c_longlong]),
+    "plaid_debug_wave_trace": (C.c_int, [C.c_void_p, u64p, C.c_uint64]),
 }
 
 _lib = None

@@ -628,14 +628,18 @@ class MultiGpuSearcher:
 
 
 class BatchSearcher:
-    """Throughput mode (BASELINE configs[2], batched queries): `lanes`
-    searchers with their own streams over one index; query j runs on lane
-    j mod lanes so different queries' stages overlap (include/plaid.h)."""
+    """Throughput mode (BASELINE configs[2], batched queries).  Engine
+    "auto": waves of queries — one S_cq pass per wave (four queries per pass
+    over C in TENSOR mode) and one CTA per query for stages 1b-4 — whenever
+    the shape allows, else (and with engine="lanes") `lanes` searchers with
+    their own streams, query j on lane j mod lanes (include/plaid.h)."""
 
     def __init__(self, index: DeviceIndex, lanes: int = 8, device: int = 0,
-                 score_mode: ScoreMode = ScoreMode.TENSOR):
+                 score_mode: ScoreMode = ScoreMode.TENSOR, engine: str = "auto"):
         self.index = index
-        cfg = N.SearcherConfig(int(score_mode), 0, 0, 0)
+        if engine not in ("auto", "lanes"):
+            raise PlaidError(ErrorCode.InvalidParams, f"unknown batch engine {engine!r}")
+        cfg = N.SearcherConfig(int(score_mode), 0, 0, 1 if engine == "lanes" else 0)
         out = C.c_void_p()
         _check(N.load().plaid_batch_create(index._h, device, C.byref(cfg), int(lanes), C.byref(out)))
         self._h = out
@@ -678,6 +682,22 @@ class BatchSearcher:
 
     def last_launches(self) -> int:
         return int(N.load().plaid_batch_last_launches(self._h))
+
+    def last_was_wave(self) -> bool:
+        return bool(N.load().plaid_batch_last_was_wave(self._h))
+
+    def wave_scores(self, j: int) -> np.ndarray:
+        """Test hook: the [K, 32] S_cq table the last wave used for its j-th query."""
+        out = np.zeros((self.index.num_centroids, 32), dtype=np.float32)
+        _check(N.load().plaid_batch_wave_scores(self._h, j, N.ptr(out, C.c_float)))
+        return out
+
+    def counters(self, nq: int) -> np.ndarray:
+        """[nq, 4] StageTrace counters (stage1_candidates, stage2_out,
+        stage3_out, final_out) of the last batch (wave engine only)."""
+        out = np.zeros((nq, 4), dtype=np.uint64)
+        _check(N.load().plaid_batch_counters(self._h, N.ptr(out, C.c_uint64), nq))
+        return out
 
 
 def search(index: DeviceIndex, q: np.ndarray, params: SearchParams,

@@ -363,6 +363,33 @@ plaid_status plaid_batch_sync(plaid_batch* b) {
 
 uint64_t plaid_batch_last_launches(const plaid_batch* b) { return b ? b->impl->last_launches() : 0; }
 
+plaid_status plaid_batch_counters(plaid_batch* b, uint64_t* out, uint64_t nq) {
+    return guarded([&] {
+        need(b, "batch");
+        need(out, "out");
+        b->impl->wave_counters(out, nq);
+    });
+}
+
+plaid_status plaid_batch_wave_scores(plaid_batch* b, uint64_t j, float* out) {
+    return guarded([&] {
+        need(b, "batch");
+        need(out, "out");
+        b->impl->wave_scores(j, out);
+    });
+}
+
+// Debug: per-query phase timeline of the last wave batch (PLAID_WAVE_TRACE=1).
+plaid_status plaid_debug_wave_trace(plaid_batch* b, uint64_t* out, uint64_t nq) {
+    return guarded([&] {
+        need(b, "batch");
+        need(out, "out");
+        b->impl->wave_trace(out, nq);
+    });
+}
+
+int plaid_batch_last_was_wave(const plaid_batch* b) { return b && b->impl->last_was_wave() ? 1 : 0; }
+
 plaid_status plaid_merge_topk_rows_device(plaid_searcher* s, const uint32_t* d_rows, uint64_t shards, uint64_t k,
                                           uint32_t* d_out_pids, float* d_out_scores, uint64_t* d_out_n,
                                           uint64_t stream) {

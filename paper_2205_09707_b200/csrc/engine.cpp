@@ -1326,6 +1326,178 @@ void Searcher::merge_topk(const uint32_t* pids, const float* scores, const uint6
 }
 
 // ---------------------------------------------------------------- throughput mode
+// ---------------------------------------------------------------- throughput: waves
+WavePipeline::WavePipeline(DeviceIndex* index, int device, bool tensor)
+    : index_(index), device_(device), tensor_(tensor) {
+    DeviceGuard g(device_);
+    const IndexView& ix = index_->view();
+    if (tensor_ && launch::tensor_scores_supported(ix)) launch::make_wave_tensor_map(ix, tmap_);
+    else tensor_ = false;
+    status_.ensure(1);
+    PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
+    PLAID_CUDA(cudaDeviceSynchronize());
+    const char* tr = getenv("PLAID_WAVE_TRACE");
+    tracing_ = tr && *tr && *tr != '0';
+}
+
+WavePipeline::~WavePipeline() {
+    DeviceGuard g(device_);
+    cudaDeviceSynchronize();
+}
+
+bool WavePipeline::supports(const plaid_params& p, uint64_t rows, uint64_t dim) const {
+    const IndexView& ix = index_->view();
+    return ix.dim == 128 && dim == 128 && rows >= 1 && rows <= 32 && ix.tok_inv && !p.disable_filter &&
+           p.nprobe >= 1 && p.nprobe <= 8 && p.nprobe <= ix.K && ix.N < (1ull << 31) &&
+           std::min<uint64_t>(stage3_width(p), ix.N) <= launch::kWaveSortCap && p.ndocs <= (1ull << 24) &&
+           index_->candidate_bound(p.nprobe) < (1ull << 31);
+}
+
+// Scratch per slot: S (K x 32 f32), keep bits, partial lists, candidate
+// bitmap + word prefix (N bits each, padded to whole compaction rounds), C1
+// ids / keys / two side buffers / stage-2 accumulators (c1cap = the sum of
+// the 32 nprobe longest posting lists), stage-2/3 selections.  The number of
+// slots is the wave size: at most 512 (4 resident worker CTAs per SM hold a
+// whole wave) and at most half of the free device memory.
+void WavePipeline::ensure(uint64_t nq, const plaid_params& p) {
+    const IndexView& ix = index_->view();
+    const uint64_t K = ix.K, N = ix.N;
+    const uint64_t c1cap = std::max<uint64_t>(index_->candidate_bound(p.nprobe), 1);
+    const uint64_t nd = std::min<uint64_t>(p.ndocs, N), n3 = std::min<uint64_t>(stage3_width(p), N);
+    const uint64_t sel_stride = (nd + n3 + 1) / 2 * 2;
+    const uint64_t lists = std::max<uint64_t>(launch::wave_scores_lists(ix), launch::scores_max_warps());
+    const uint64_t partial_stride = lists * 32 * 8;
+    const uint64_t keep_stride = ((K + 31) / 32 + 3) / 4 * 4;
+    const uint64_t s_stride = K * kScoresPitch;
+    const uint64_t per_slot = s_stride * 4 + keep_stride * 4 + partial_stride * 8 + c1cap * (4 + 8 + 24) +
+                              nd * 128 + sel_stride * 8 + 32;
+    // a wave = the worker CTAs resident at once (one round of the worker)
+    static const uint64_t resident = [&] {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return uint64_t(sms) * launch::wave_worker_ctas_per_sm(ix.nbits);
+    }();
+    uint64_t want = std::min<uint64_t>(std::max<uint64_t>(nq, 1), std::min<uint64_t>(resident, 1024));
+    if (tensor_) want = (want + 3) / 4 * 4;
+    if (!range_tab_.p) {
+        // the worker's per-(centroid, pid range) posting offsets (index-side, once)
+        range_w_ = launch::kWaveRangeIds;
+        range_n_ = uint32_t((N + range_w_ - 1) / range_w_);
+        range_tab_.ensure(K * (range_n_ + 1));
+        launch::wave_range_table(ix, range_w_, range_n_, range_tab_.p, 0);
+        PLAID_CUDA(cudaDeviceSynchronize());
+        PLAID_CUDA(cudaGetLastError());
+    }
+    const bool fits = slots_ >= want && c1cap_ >= c1cap && sel_stride_ >= sel_stride && nd_cap_ >= nd;
+    if (fits) return;
+    // grow: release first so the free-memory estimate sees the old buffers
+    S_.release(), rowmax_.release(), keep_.release(), c1_.release(), acc_.release();
+    partial_.release(), keys_.release(), side_.release(), sel_.release(), counters_.release();
+    size_t free_b = 0, total_b = 0;
+    PLAID_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t cap = std::max<uint64_t>(uint64_t(free_b / 2) / per_slot, 1);
+    uint64_t slots = std::max<uint64_t>(want, slots_);
+    slots = std::min<uint64_t>(slots, cap);
+    if (tensor_ && slots >= 4) slots = slots / 4 * 4;
+    if (slots == 0) fail(PLAID_OUT_OF_MEMORY, "not enough device memory for one throughput-mode slot");
+    c1cap_ = std::max(c1cap_, c1cap);
+    sel_stride_ = std::max(sel_stride_, sel_stride);
+    partial_stride_ = partial_stride, keep_stride_ = keep_stride, s_stride_ = s_stride;
+    nd_cap_ = std::max(nd_cap_, nd);
+    slots_ = uint32_t(slots);
+    S_.ensure(slots * s_stride_);
+    rowmax_.ensure(K);
+    keep_.ensure(slots * keep_stride_);
+    partial_.ensure(slots * partial_stride_);
+    c1_.ensure(slots * c1cap_);
+    acc_.ensure(slots * nd_cap_ * 32);
+    keys_.ensure(slots * c1cap_);
+    side_.ensure(slots * c1cap_ * 3);
+    sel_.ensure(slots * sel_stride_);
+    counters_.ensure(std::max<uint64_t>(nq, slots) * 4);
+    if (tracing_) trace_.ensure(std::max<uint64_t>(nq, slots) * 16);
+    PLAID_CUDA(cudaMemset(acc_.p, 0, acc_.n * sizeof(uint32_t)));
+    PLAID_CUDA(cudaDeviceSynchronize());
+}
+
+void WavePipeline::run(const float* d_q, uint64_t nq, uint32_t rows, const plaid_params& p, uint32_t* d_pids,
+                       float* d_scores, uint64_t* d_n, bool validate, cudaStream_t st) {
+    DeviceGuard g(device_);
+    const IndexView& ix = index_->view();
+    ensure(nq, p);
+    if (counters_.n < nq * 4 || (tracing_ && trace_.n < nq * 16)) {
+        counters_.ensure(nq * 4);
+        if (tracing_) trace_.ensure(nq * 16);
+        PLAID_CUDA(cudaDeviceSynchronize());
+    }
+    launch::reset_launches();
+    const uint32_t npb = np_bucket(p.nprobe);
+    const uint64_t nd = std::min<uint64_t>(p.ndocs, ix.N), n3 = std::min<uint64_t>(stage3_width(p), ix.N);
+    for (uint64_t j0 = 0; j0 < nq; j0 += slots_) {
+        const uint32_t w = uint32_t(std::min<uint64_t>(slots_, nq - j0));
+        const float* q = d_q + j0 * rows * 128;
+        uint32_t lists = 0;
+        if (tensor_) {
+            lists = launch::wave_scores(tmap_, ix, q, w, rows, p.t_cs, npb, S_.p, s_stride_, keep_.p, keep_stride_,
+                                        partial_.p, partial_stride_, st);
+        } else {
+            for (uint32_t i = 0; i < w; ++i)
+                lists = launch::scores_exact(ix, q + uint64_t(i) * rows * 128, rows, p.t_cs, S_.p + i * s_stride_,
+                                             rowmax_.p, keep_.p + i * keep_stride_, partial_.p + i * partial_stride_,
+                                             npb, st);
+        }
+        launch::WaveArgs a;
+        a.Q = q;
+        a.rows = rows, a.nprobe = uint32_t(p.nprobe), a.ndocs = uint32_t(nd), a.n3 = uint32_t(n3);
+        a.k = uint32_t(p.k), a.nlists = lists, a.pid_base = uint32_t(index_->pid_base()), a.validate = validate ? 1 : 0;
+        a.S = S_.p, a.s_stride = s_stride_, a.keep = keep_.p, a.keep_stride = keep_stride_;
+        a.partial = partial_.p, a.partial_stride = partial_stride_;
+        a.range_tab = range_tab_.p, a.range_w = range_w_, a.range_n = range_n_;
+        a.c1 = c1_.p, a.acc = acc_.p, a.keys = keys_.p, a.side = side_.p, a.c1cap = c1cap_;
+        a.sel = sel_.p, a.sel_stride = sel_stride_;
+        a.out_pids = d_pids + j0 * p.k, a.out_scores = d_scores + j0 * p.k, a.out_n = d_n + j0;
+        a.counters = counters_.p + j0 * 4, a.status = status_.p;
+        a.trace = tracing_ ? reinterpret_cast<unsigned long long*>(trace_.p + j0 * 16) : nullptr;
+        launch::wave_worker(ix, a, w, npb, st);
+    }
+    PLAID_CUDA(cudaGetLastError());
+    last_launches_ = launch::launches();
+}
+
+void WavePipeline::counters(uint64_t* out_host, uint64_t nq) {
+    DeviceGuard g(device_);
+    PLAID_CUDA(cudaDeviceSynchronize());
+    if (nq * 4 > counters_.n) fail(PLAID_INVALID_PARAMS, "counter request exceeds the last batch");
+    PLAID_CUDA(cudaMemcpy(out_host, counters_.p, nq * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+}
+
+void WavePipeline::copy_scores(uint64_t j, float* out_host) {
+    DeviceGuard g(device_);
+    PLAID_CUDA(cudaDeviceSynchronize());
+    if (j >= slots_ || !S_.p) fail(PLAID_INVALID_PARAMS, "no such slot in the last wave");
+    PLAID_CUDA(cudaMemcpy(out_host, S_.p + j * s_stride_, s_stride_ * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+void WavePipeline::trace(uint64_t* out_host, uint64_t nq) {
+    DeviceGuard g(device_);
+    PLAID_CUDA(cudaDeviceSynchronize());
+    if (!tracing_ || nq * 16 > trace_.n) fail(PLAID_INVALID_PARAMS, "no wave trace (set PLAID_WAVE_TRACE=1)");
+    PLAID_CUDA(cudaMemcpy(out_host, trace_.p, nq * 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+}
+
+void WavePipeline::check_status() {
+    DeviceGuard g(device_);
+    PLAID_CUDA(cudaDeviceSynchronize());
+    int status = 0;
+    PLAID_CUDA(cudaMemcpy(&status, status_.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (status) {
+        PLAID_CUDA(cudaMemset(status_.p, 0, sizeof(int)));
+        PLAID_CUDA(cudaDeviceSynchronize());
+        fail(status, "device-side query validation failed (row not unit norm)");
+    }
+}
+
 BatchSearcher::BatchSearcher(DeviceIndex* index, int device, const plaid_searcher_config& cfg, uint32_t lanes)
     : index_(index), device_(device) {
     if (!index) fail(PLAID_INVALID_PARAMS, "batch searcher needs an index");
@@ -1354,6 +1526,8 @@ BatchSearcher::BatchSearcher(DeviceIndex* index, int device, const plaid_searche
     int lo = 0, hi = 0;
     PLAID_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     PLAID_CUDA(cudaStreamCreateWithPriority(&sstream_, cudaStreamNonBlocking, hi));
+    if (cfg.batch_engine != PLAID_BATCH_LANES)
+        wave_ = std::make_unique<WavePipeline>(index, device, cfg.score_mode == PLAID_SCORES_TENSOR);
 }
 
 BatchSearcher::~BatchSearcher() {
@@ -1372,8 +1546,38 @@ BatchSearcher::~BatchSearcher() {
 
 void BatchSearcher::search_device(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim, const plaid_params& p,
                                   uint32_t* d_pids, float* d_scores, uint64_t* d_n, cudaStream_t st) {
+    search_device_impl(d_q, nq, rows, dim, p, d_pids, d_scores, d_n, st, true);
+}
+
+void BatchSearcher::wave_counters(uint64_t* out_host, uint64_t nq) {
+    if (!wave_ || !last_wave_) fail(PLAID_INVALID_PARAMS, "the last batch did not run on the wave engine");
+    wave_->counters(out_host, nq);
+}
+
+void BatchSearcher::wave_scores(uint64_t j, float* out_host) {
+    if (!wave_ || !last_wave_) fail(PLAID_INVALID_PARAMS, "the last batch did not run on the wave engine");
+    wave_->copy_scores(j, out_host);
+}
+
+void BatchSearcher::wave_trace(uint64_t* out_host, uint64_t nq) {
+    if (!wave_ || !last_wave_) fail(PLAID_INVALID_PARAMS, "the last batch did not run on the wave engine");
+    wave_->trace(out_host, nq);
+}
+
+void BatchSearcher::search_device_impl(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim,
+                                       const plaid_params& p, uint32_t* d_pids, float* d_scores, uint64_t* d_n,
+                                       cudaStream_t st, bool validate) {
     DeviceGuard g(device_);
     if (!st) st = streams_[0];
+    last_wave_ = false;
+    if (wave_ && wave_->supports(p, rows, dim)) {
+        validate_params_host(p, index_->view().K);
+        if (nq == 0) return;
+        wave_->run(d_q, nq, uint32_t(rows), p, d_pids, d_scores, d_n, validate, st);
+        last_launches_ = wave_->last_launches();
+        last_wave_ = true;
+        return;
+    }
     const uint64_t L = lanes_.size();
     PLAID_CUDA(cudaEventRecord(fork_, st));
     for (uint64_t l = 0; l < L && l < nq; ++l)
@@ -1457,7 +1661,7 @@ void BatchSearcher::search(const float* q, uint64_t nq, uint64_t rows, uint64_t 
     std::memcpy(h_q_, q, nqf * sizeof(float));
     cudaStream_t st = streams_[0];
     PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, nqf * sizeof(float), cudaMemcpyHostToDevice, st));
-    search_device(q_.p, nq, rows, dim, p, pids_.p, scores_.p, n_.p, st);
+    search_device_impl(q_.p, nq, rows, dim, p, pids_.p, scores_.p, n_.p, st, false);  // validated above
     PLAID_CUDA(cudaMemcpyAsync(h_n_, n_.p, nq * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     PLAID_CUDA(cudaMemcpyAsync(h_pids_, pids_.p, nout * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     PLAID_CUDA(cudaMemcpyAsync(h_scores_, scores_.p, nout * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -1472,6 +1676,7 @@ void BatchSearcher::search(const float* q, uint64_t nq, uint64_t rows, uint64_t 
 }
 
 void BatchSearcher::sync() {
+    if (wave_) wave_->check_status();
     for (auto& s : lanes_) s->sync();  // also reports device-side query validation failures
 }
 

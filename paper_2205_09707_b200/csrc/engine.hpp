@@ -263,6 +263,49 @@ private:
     uint32_t launch_scores(const float* d_q, uint32_t rows, float t_cs, uint32_t npb, cudaStream_t st);
 };
 
+// Throughput mode, wave engine: a batch runs in waves of up to `slots`
+// queries; per wave ONE S_cq pass (TENSOR: wave_scores, four queries per
+// pass over C; EXACT: the exact kernel per query) and ONE worker launch with
+// a CTA per query for stages 1b-4 (wave_worker.cu).  Scratch is per slot,
+// sized from the index and the params (throughput mode).
+class WavePipeline {
+public:
+    WavePipeline(DeviceIndex* index, int device, bool tensor);
+    ~WavePipeline();
+    WavePipeline(const WavePipeline&) = delete;
+    WavePipeline& operator=(const WavePipeline&) = delete;
+    bool supports(const plaid_params& p, uint64_t rows, uint64_t dim) const;
+    // d_q [nq][rows][dim]; outputs [nq][k] + d_n[nq] (global ids); the
+    // per-query counters [stage1, stage2_out, stage3_out, final_out] stay in
+    // the pipeline (counters()).  validate: device-side query norm check.
+    void run(const float* d_q, uint64_t nq, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,
+             uint64_t* d_n, bool validate, cudaStream_t st);
+    void counters(uint64_t* out_host, uint64_t nq);
+    // S_cq (K x 32, row per centroid) the last wave computed for its query j
+    void copy_scores(uint64_t j, float* out_host);
+    // phase timeline of the last batch ([nq][16] globaltimer stamps; needs PLAID_WAVE_TRACE=1)
+    void trace(uint64_t* out_host, uint64_t nq);
+    void check_status();
+    uint64_t last_launches() const { return last_launches_; }
+    uint32_t slots() const { return slots_; }
+
+private:
+    void ensure(uint64_t nq, const plaid_params& p);
+    DeviceIndex* index_;
+    int device_;
+    bool tensor_;
+    alignas(64) unsigned char tmap_[128];
+    uint32_t slots_ = 0;
+    uint64_t c1cap_ = 0, sel_stride_ = 0, partial_stride_ = 0, keep_stride_ = 0, nd_cap_ = 0, s_stride_ = 0;
+    uint32_t range_w_ = 0, range_n_ = 0;
+    uint64_t last_launches_ = 0;
+    DevBuf<float> S_, rowmax_;
+    DevBuf<uint32_t> keep_, range_tab_, c1_, acc_;
+    DevBuf<uint64_t> partial_, keys_, side_, sel_, counters_, trace_;
+    DevBuf<int> status_;
+    bool tracing_ = false;
+};
+
 // Throughput mode (BASELINE configs[2]: batched queries): L lanes, each a
 // full Searcher with its own stream and scratch over the shared index.
 // Query j runs on lane j mod L, so the latency-bound stage kernels of
@@ -282,10 +325,21 @@ public:
                        uint32_t* d_pids, float* d_scores, uint64_t* d_n, cudaStream_t st);
     void sync();
     uint64_t last_launches() const { return last_launches_; }
+    // Which engine ran the last batch (1 = waves, 0 = lanes) and its per-query
+    // counters [nq][stage1, stage2_out, stage3_out, final_out] (waves only).
+    bool last_was_wave() const { return last_wave_; }
+    void wave_counters(uint64_t* out_host, uint64_t nq);
+    void wave_scores(uint64_t j, float* out_host);
+    void wave_trace(uint64_t* out_host, uint64_t nq);
+    uint32_t wave_slots() const { return wave_ ? wave_->slots() : 0; }
 
 private:
+    void search_device_impl(const float* d_q, uint64_t nq, uint64_t rows, uint64_t dim, const plaid_params& p,
+                            uint32_t* d_pids, float* d_scores, uint64_t* d_n, cudaStream_t st, bool validate);
     DeviceIndex* index_;
     int device_;
+    std::unique_ptr<WavePipeline> wave_;  // null when the config asks for lanes only
+    bool last_wave_ = false;
     std::vector<std::unique_ptr<Searcher>> lanes_;
     std::vector<cudaStream_t> streams_;
     std::vector<cudaEvent_t> joins_, ready_, sdone_;

@@ -297,6 +297,52 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
                     const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t* d_out_keys,
                     const RankScratch& s, cudaStream_t st);
 
+// ---- throughput mode: waves of queries (wave_scores.cu, wave_worker.cu) ------------
+// S_cq of a wave, 4 queries per pass over C (tcgen05, 3xTF32): S rows
+// [nq][s_stride], keep bits [nq][keep_stride], partial top-NP lists
+// [nq][partial_stride] as [wave_scores_lists()][32][np_bucket] (key 0 = empty).  Q: [nq][rows][128].
+void make_wave_tensor_map(const IndexView& ix, void* out_map);
+uint32_t wave_scores_lists(const IndexView& ix);
+uint32_t wave_scores(const void* cmap, const IndexView& ix, const float* d_q, uint32_t nq, uint32_t rows, float t_cs,
+                     uint32_t np_bucket, float* d_S, uint64_t s_stride, uint32_t* d_keep, uint64_t keep_stride,
+                     uint64_t* d_partial, uint64_t partial_stride, cudaStream_t st);
+constexpr uint32_t kWaveSortCap = 2048;     // max finalists (stage3_width) of the wave worker
+constexpr uint32_t kWaveRangeIds = 65536;   // pid range of the worker's shared-memory member bitmap
+// Index-side table of the wave worker: for centroid c and pid range r (ids
+// [r W, (r+1) W)), the offset in c's posting list of its first posting >= r W;
+// [K][R + 1] u32 with R = ceil(N / W).
+void wave_range_table(const IndexView& ix, uint32_t W, uint32_t R, uint32_t* d_tab, cudaStream_t st);
+// Per-wave buffers of the worker: slot q (= query q of the wave) owns c1 /
+// keys [c1cap], side [3 c1cap], acc [ndocs x 32] (zero between queries),
+// sel [sel_stride >= ndocs + n3].
+struct WaveArgs {
+    const float* Q = nullptr;
+    uint32_t rows = 0, nprobe = 0, ndocs = 0, n3 = 0, k = 0, nlists = 0, pid_base = 0, validate = 0;
+    const float* S = nullptr;
+    uint64_t s_stride = 0;
+    const uint32_t* keep = nullptr;
+    uint64_t keep_stride = 0;
+    const uint64_t* partial = nullptr;
+    uint64_t partial_stride = 0;
+    const uint32_t* range_tab = nullptr;
+    uint32_t range_w = 0, range_n = 0;
+    uint32_t* c1 = nullptr;
+    uint32_t* acc = nullptr;
+    uint64_t* keys = nullptr;
+    uint64_t* side = nullptr;
+    uint64_t c1cap = 0;
+    uint64_t* sel = nullptr;
+    uint64_t sel_stride = 0;
+    uint32_t* out_pids = nullptr;
+    float* out_scores = nullptr;
+    uint64_t* out_n = nullptr;
+    uint64_t* counters = nullptr;  // optional [nq][4]: stage1, stage2_out, stage3_out, final_out
+    int* status = nullptr;
+    unsigned long long* trace = nullptr;  // optional [nq][16] phase timestamps (globaltimer)
+};
+void wave_worker(const IndexView& ix, const WaveArgs& a, uint32_t nq, uint32_t np_stride, cudaStream_t st);
+uint32_t wave_worker_ctas_per_sm(uint32_t nbits);  // resident worker CTAs per SM (occupancy)
+
 // ---- misc ---------------------------------------------------------------------------
 // Device-side query validation (types.cpp:61-72, status 0 or NotNormalized+1)
 // query validation (when d_q != nullptr) + zero nwords u32 at d_zero and nwords2
