@@ -838,24 +838,67 @@ def run_plaid_batch(args, cfg):
             dist.destroy_process_group()
         return
 
-    # S_cq kernel alone (one single-query search with phase events) for the roofline
-    s1 = P.Searcher(idx, device=local, score_mode=mode, record_times=True)
-    sc_ms = []
-    for i in range(5):
-        flush()
-        torch.cuda.synchronize()
-        s1.search(qs[0][i], params)
-        sc_ms.append(s1.phase_ms()["scores"])
-    sc = float(np.median(sc_ms[1:]))
     hbm_peak, _, peak_kind = measured_peaks()
     K = cfg["K"]
-    ab = 512 * K + 128 * K + K // 8 + QLEN * DIM * 4
-    kname = "scores_tf32_kernel" if args.score_mode == "tensor" else "scores_exact_kernel"
-    roof = {"bound": "hbm", "kernel": kname, "achieved": ab / (sc * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-            "frac": ab / (sc * 1e-3) / 1e9 / hbm_peak, "traffic": None,
-            "peak_kind": f"{peak_kind} (copy bandwidth, burst)", "algorithmic_bytes_per_launch": ab,
-            "mean_ms": sc, "share_of_step": sc * B / (1e3 * total_s / args.steps),
-            "note": "one S_cq launch per query (single-query kernel; the batch's launches serialise)"}
+    wave = bs.last_was_wave()
+    if wave and args.score_mode == "tensor":
+        # the wave engine: time the first wave's S_cq launch alone and with its
+        # worker (launch cap: a batch stops after its first n kernels), events
+        # on the launching stream, L2 flushed before each
+        import ctypes as C
+
+        from paper_2205_09707_b200 import _native as Nv
+
+        lib = Nv.load()
+        slots = min(B, bs.wave_slots())
+
+        def capped(n):
+            old = lib.plaid_debug_set_launch_cap(n)
+            ts = []
+            for _ in range(3):
+                flush()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                bs.search_device(dq[0].data_ptr(), slots, QLEN, DIM, params, d_pids.data_ptr(),
+                                 d_scores.data_ptr(), d_n.data_ptr(), stream=sh)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            lib.plaid_debug_set_launch_cap(old)
+            return float(np.median(ts))
+
+        t_sc = capped(1)
+        t_wave = capped(2)
+        flops = 3 * 2 * K * DIM * QLEN * slots  # 3xTF32: three tf32 products per dot
+        tf32_peak = measured_peaks()[1] / 2.0
+        ab = 512 * K * ((slots + 3) // 4) + 128 * K * slots + slots * K // 8  # C per 4-query pass + S rows + keep bits
+        roof = {"bound": "tensor", "kernel": "wave_scores_kernel", "achieved": flops / (t_sc * 1e-3) / 1e12,
+                "peak": tf32_peak, "unit": "TFLOP/s", "frac": flops / (t_sc * 1e-3) / 1e12 / tf32_peak,
+                "traffic": None, "peak_kind": f"{peak_kind} dense bf16 (burst) / 2 = tf32 rate",
+                "algorithmic_flops_per_launch": flops, "queries_per_launch": slots, "mean_ms": t_sc,
+                "hbm": {"algorithmic_bytes_per_launch": ab, "achieved_gbs": ab / (t_sc * 1e-3) / 1e9,
+                        "frac": ab / (t_sc * 1e-3) / 1e9 / hbm_peak},
+                "share_of_step": t_sc * (B / slots) / (1e3 * total_s / args.steps),
+                "worker_ms_per_wave": t_wave - t_sc,
+                "note": "one wave = one S_cq launch (4 queries per pass over C) + one worker launch (a CTA per "
+                        "query, stages 1b-4); tensor-pipe activity from ncu in profiles/"}
+    else:
+        # S_cq kernel alone (one single-query search with phase events) for the roofline
+        s1 = P.Searcher(idx, device=local, score_mode=mode, record_times=True)
+        sc_ms = []
+        for i in range(5):
+            flush()
+            torch.cuda.synchronize()
+            s1.search(qs[0][i], params)
+            sc_ms.append(s1.phase_ms()["scores"])
+        sc = float(np.median(sc_ms[1:]))
+        ab = 512 * K + 128 * K + K // 8 + QLEN * DIM * 4
+        kname = "scores_tf32_kernel" if args.score_mode == "tensor" else "scores_exact_kernel"
+        roof = {"bound": "hbm", "kernel": kname, "achieved": ab / (sc * 1e-3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s", "frac": ab / (sc * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+                "peak_kind": f"{peak_kind} (copy bandwidth, burst)", "algorithmic_bytes_per_launch": ab,
+                "mean_ms": sc, "share_of_step": sc * B / (1e3 * total_s / args.steps),
+                "note": "one S_cq launch per query (single-query kernel; the batch's launches serialise)"}
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
@@ -887,6 +930,8 @@ def run_plaid_batch(args, cfg):
         "cpu_baseline": cpu,
         "clocks": clk,
     }
+    line["config"]["batch_engine"] = (f"waves of {bs.wave_slots()} queries (one S_cq pass + one worker launch "
+                                      f"each)" if wave else f"{args.lanes} lanes")
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

@@ -310,6 +310,8 @@ plaid_status plaid_batch_counters(plaid_batch* b, uint64_t* out, uint64_t nq);
 /* Test hook: the S_cq table (num_centroids x 32 floats, one row per
  * centroid) the last wave computed for its j-th query (j < wave size). */
 plaid_status plaid_batch_wave_scores(plaid_batch* b, uint64_t j, float* out);
+/* Queries per wave of the wave engine (0 before its first batch). */
+uint32_t plaid_batch_wave_slots(const plaid_batch* b);
 /* 1 when the last batch ran on the wave engine, else 0. */
 int plaid_batch_last_was_wave(const plaid_batch* b);
 

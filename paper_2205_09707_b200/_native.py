@@ -106,6 +106,7 @@ SIGNATURES = {
     "plaid_batch_last_launches": (C.c_uint64, [C.c_void_p]),
     "plaid_batch_counters": (C.c_int, [C.c_void_p, u64p, C.c_uint64]),
     "plaid_batch_last_was_wave": (C.c_int, [C.c_void_p]),
+    "plaid_batch_wave_slots": (C.c_uint32, [C.c_void_p]),
     "plaid_batch_wave_scores": (C.c_int, [C.c_void_p, C.c_uint64, f32p]),
     "plaid_shard_phase1_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(Params),
                                             C.c_void_p, C.c_uint64, C.c_uint64]),

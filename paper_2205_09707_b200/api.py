@@ -686,6 +686,10 @@ class BatchSearcher:
     def last_was_wave(self) -> bool:
         return bool(N.load().plaid_batch_last_was_wave(self._h))
 
+    def wave_slots(self) -> int:
+        """Queries per wave of the wave engine (0 before its first batch)."""
+        return int(N.load().plaid_batch_wave_slots(self._h))
+
     def wave_scores(self, j: int) -> np.ndarray:
         """Test hook: the [K, 32] S_cq table the last wave used for its j-th query."""
         out = np.zeros((self.index.num_centroids, 32), dtype=np.float32)

@@ -388,6 +388,8 @@ plaid_status plaid_debug_wave_trace(plaid_batch* b, uint64_t* out, uint64_t nq) 
     });
 }
 
+uint32_t plaid_batch_wave_slots(const plaid_batch* b) { return b ? b->impl->wave_slots() : 0; }
+
 int plaid_batch_last_was_wave(const plaid_batch* b) { return b && b->impl->last_was_wave() ? 1 : 0; }
 
 plaid_status plaid_merge_topk_rows_device(plaid_searcher* s, const uint32_t* d_rows, uint64_t shards, uint64_t k,

@@ -9,8 +9,8 @@
 //   A = [Q_hi | Q_lo] of the group in TMEM (256 columns, loaded once per
 //       group), B = the centroid tile from shared memory: the raw fp32 TMA box
 //       IS C_hi (the tensor core truncates fp32 operands to tf32), and
-//       converter warps write C_lo = tf32_rn(C - C_hi) beside it in the same
-//       swizzled layout.
+//       converter warps write C_lo = C - C_hi beside it in the same swizzled
+//       layout (truncated to tf32 by the tensor core in turn).
 //   D = Q_hi.C_hi + Q_lo.C_hi + Q_hi.C_lo (3xTF32, fp32 accumulate, ~2e-6
 //       absolute on unit-vector dots), two 128-column accumulators.
 // A TMA box is 128 centroids x 32 dims (16 KB, SWIZZLE_128B: K-major rows of
@@ -56,7 +56,8 @@ constexpr uint32_t kOffLo = kOffRaw + kRaw * kBoxBytes;
 constexpr uint32_t kOffBar = kOffLo + kLo * kBoxBytes;
 constexpr uint32_t kNumBars = 2 * kRaw + 2 * kLo + 4 + 2;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
-constexpr uint32_t kSmemBytes = kOffMisc + 16 + 1024;
+constexpr uint32_t kOffStage = (kOffMisc + 16 + 15) / 16 * 16;  // epilogue: 8 warps x 32 lanes x 33 f32
+constexpr uint32_t kSmemBytes = kOffStage + 8 * 32 * 33 * 4 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 constexpr uint32_t kTmemCols = 512;  // [0,256) two accumulators, [256,384) Q_hi, [384,512) Q_lo
 constexpr uint32_t kColA = 256;
@@ -101,6 +102,27 @@ __device__ __forceinline__ void mma_chunk(uint32_t d, uint32_t ahi, uint32_t alo
         "}" ::"r"(d),
         "r"(ahi), "r"(alo), "l"(braw), "l"(blo), "r"(accumulate), "r"(kIdesc)
         : "memory");
+}
+
+// C_lo = C - C_hi exactly (fp32), left for the tensor core to truncate: the
+// dropped bits are < 2^-22 |c| per element (a bias below 3e-7 on a unit dot
+// product, far inside the 3xTF32 error), and the converter saves the
+// rounding's two ALU operations per element — the ALU pipe, not the tensor
+// core or HBM, limited this kernel.
+__device__ __forceinline__ uint32_t lo_trunc(uint32_t x) {
+    return __float_as_uint(__fsub_rn(__uint_as_float(x), __uint_as_float(tc::split_hi(x))));
+}
+
+// 0xFFFFFFFF when a >= b (a > b), else 0: one FSET instead of a compare and a select
+__device__ __forceinline__ uint32_t fset_ge(float a, float b) {
+    uint32_t r;
+    asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t fset_gt(float a, float b) {
+    uint32_t r;
+    asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
 }
 
 template <int NP>
@@ -226,8 +248,8 @@ wave_scores_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                 for (int j = 0; j < 8; ++j) v[j] = src[j ^ (lane & 7)];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    dst[j ^ (lane & 7)] = make_uint4(tc::split_lo(v[j].x), tc::split_lo(v[j].y),
-                                                     tc::split_lo(v[j].z), tc::split_lo(v[j].w));
+                    dst[j ^ (lane & 7)] = make_uint4(lo_trunc(v[j].x), lo_trunc(v[j].y), lo_trunc(v[j].z),
+                                                     lo_trunc(v[j].w));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
@@ -238,27 +260,40 @@ wave_scores_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
             if (i == 0) {
                 // A of group g (after converting its first tile, so the MMA's
                 // wait for A is the only bubble at a group boundary)
-                if (g > 0) tc::mbar_wait(a_empty, (g - 1) & 1);
-                tc::fence_after();
+                // Q rows of the group, two 32-dim chunks per round trip; the
+                // first two are in flight before A is free (the MMA waits for
+                // A at every group boundary: the reload is the bubble).  A_hi
+                // is the raw fp32 row (the tensor core truncates it to tf32)
                 const uint32_t qi = g * 4 + q;
                 const bool live = qi < nq && lane < rows;
                 const uint4* qr = reinterpret_cast<const uint4*>(Q + (uint64_t(qi) * rows + lane) * 128);
-#pragma unroll 1
-                for (uint32_t kc = 0; kc < 4; ++kc) {
-                    uint32_t hi[32], lo[32];
+                auto load2 = [&](uint32_t kc, uint32_t (&x)[64]) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const uint4 x = live ? __ldg(qr + kc * 8 + j) : make_uint4(0, 0, 0, 0);
-                        hi[4 * j] = tc::split_hi(x.x), lo[4 * j] = tc::split_lo(x.x);
-                        hi[4 * j + 1] = tc::split_hi(x.y), lo[4 * j + 1] = tc::split_lo(x.y);
-                        hi[4 * j + 2] = tc::split_hi(x.z), lo[4 * j + 2] = tc::split_lo(x.z);
-                        hi[4 * j + 3] = tc::split_hi(x.w), lo[4 * j + 3] = tc::split_lo(x.w);
+                    for (int j = 0; j < 16; ++j) {
+                        const uint4 v = live ? __ldg(qr + kc * 8 + j) : make_uint4(0, 0, 0, 0);
+                        x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
                     }
+                };
+                auto store2 = [&](uint32_t kc, uint32_t (&x)[64]) {
                     const uint32_t col = tmem + ((q * 32) << 16) + kColA + kc * 32;
-                    tc::tmem_st32(col, hi);
-                    tc::tmem_st32(col + 128, lo);
-                }
-                tc::tmem_st_wait();
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t (&v)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[32 * h]);
+                        tc::tmem_st32(col + 32 * h, v);
+                        tc::tmem_st_wait();  // v is overwritten next
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) v[e] = tc::split_lo(v[e]);
+                        tc::tmem_st32(col + 128 + 32 * h, v);
+                        tc::tmem_st_wait();
+                    }
+                };
+                uint32_t xq[64];
+                load2(0, xq);
+                if (g > 0) tc::mbar_wait(a_empty, (g - 1) & 1);
+                tc::fence_after();
+                store2(0, xq);
+                load2(2, xq);
+                store2(2, xq);
                 tc::fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(a_full);
@@ -268,6 +303,7 @@ wave_scores_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
         // ---------------- epilogue: group grp takes the items of parity grp
         const uint32_t ew = warp - 8, grp = ew >> 2, q = warp & 3;
         const bool tok = lane < rows;
+        uint32_t* stage = reinterpret_cast<uint32_t*>(smem + kOffStage) + (ew * 32 + lane) * 33;
         float top_s[NP];
         uint32_t top_i[NP];
 #pragma unroll
@@ -295,26 +331,63 @@ wave_scores_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
                     const uint64_t c0 = t * 128 + jb * 32;
                     if (!live || c0 >= K) continue;
                     const uint32_t nv = K - c0 < 32 ? uint32_t(K - c0) : 32u;
-                    uint32_t kw = 0;
+                    // per lane (= token) bit masks over the 32 centroids, then one
+                    // OR-reduction across the tokens for the keep word: the ALU
+                    // pipe, not HBM, was the limit with a vote per centroid
                     const float thr0 = top_s[NP - 1];
-                    uint32_t cand = 0;
+                    uint32_t km = 0, cm = 0;
+                    float* Srow = Sq + c0 * kScoresPitch + lane;
+                    if (nv == 32) {  // whole tile column block: no per-centroid bound checks
 #pragma unroll
-                    for (int r = 0; r < 32; ++r) {
-                        const float v = __uint_as_float(raw[r]);
-                        if (uint32_t(r) < nv) Sq[(c0 + r) * kScoresPitch + lane] = v;
-                        kw |= (__any_sync(0xffffffffu, tok && v >= t_cs) ? 1u : 0u) << r;
-                        cand |= (tok && uint32_t(r) < nv && v > thr0) ? (1u << r) : 0u;
+                        for (int r = 0; r < 32; ++r) {
+                            const float v = __uint_as_float(raw[r]);
+                            Srow[r * kScoresPitch] = v;
+                            km |= fset_ge(v, t_cs) & (1u << r);
+                            cm |= fset_gt(v, thr0) & (1u << r);
+                        }
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < 32; ++r) {
+                            const float v = __uint_as_float(raw[r]);
+                            if (uint32_t(r) < nv) Srow[r * kScoresPitch] = v;
+                            km |= fset_ge(v, t_cs) & (1u << r);
+                            cm |= fset_gt(v, thr0) & (1u << r);
+                        }
                     }
-                    if (lane == 0) keep[uint64_t(qi) * keep_stride + (c0 >> 5)] = nv == 32 ? kw : kw & ((1u << nv) - 1);
+                    const uint32_t vmask = nv == 32 ? 0xFFFFFFFFu : (1u << nv) - 1u;
+                    const uint32_t kw = __reduce_or_sync(0xffffffffu, tok ? km : 0u);
+                    uint32_t cand = tok ? cm & vmask : 0u;
+                    if (lane == 0) keep[uint64_t(qi) * keep_stride + (c0 >> 5)] = kw & vmask;
                     // inserts (centroids arrive in increasing id order within a
-                    // tile; strict > keeps the lower id on ties)
+                    // tile; strict > keeps the lower id on ties).  Many
+                    // candidates (a group's first tiles, lists still short):
+                    // one static pass over the 32 values; few: extract each
+                    auto insert = [&](float sc, uint32_t id) {
+#pragma unroll
+                        for (int j = NP - 1; j > 0; --j) {
+                            const bool up = sc > top_s[j - 1], here = sc > top_s[j];
+                            top_i[j] = up ? top_i[j - 1] : (here ? id : top_i[j]);
+                            top_s[j] = up ? top_s[j - 1] : (here ? sc : top_s[j]);
+                        }
+                        if (sc > top_s[0]) top_s[0] = sc, top_i[0] = id;
+                    };
+                    if (__any_sync(0xffffffffu, __popc(cand) > 4)) {
+#pragma unroll
+                        for (int r = 0; r < 32; ++r) {
+                            const float sc = __uint_as_float(raw[r]);
+                            if (((cand >> r) & 1u) && sc > top_s[NP - 1]) insert(sc, uint32_t(c0 + r));
+                        }
+                        cand = 0;
+                    }
+                    if (__any_sync(0xffffffffu, cand != 0u)) {  // stage the row for the extractions
+#pragma unroll
+                        for (int r = 0; r < 32; ++r) stage[r] = raw[r];
+                        __syncwarp();
+                    }
                     while (cand) {
                         const int r = __ffs(cand) - 1;
                         cand &= cand - 1;
-                        float sc = 0.0f;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (j == r) sc = __uint_as_float(raw[j]);
+                        const float sc = __uint_as_float(stage[r]);
                         if (sc > top_s[NP - 1]) {
                             const uint32_t id = uint32_t(c0 + r);
 #pragma unroll

@@ -75,10 +75,11 @@ constexpr uint32_t kOffBm = kOffKS + kKeptLists * 33 * 4;          // kRangeWord
 constexpr uint32_t kOffWpre = kOffBm + kRangeWords * 4;            // kRangeWords u16
 constexpr uint32_t kOffMPid = kOffWpre + kRangeWords * 2;          // kMCap u16
 constexpr uint32_t kOffGOff = kOffMPid + kMCap * 2;                // kMCap + 1 u16
-constexpr uint32_t kOffGrp = kOffGOff + (kMCap + 8) * 2;           // kGCap u8
-constexpr uint32_t kOffUList = kOffGrp + kGCap;                    // kMCap u16: members with kept tokens
+constexpr uint32_t kOffGrp = kOffGOff + (kMCap + 8) * 2;           // kGCap u16
+constexpr uint32_t kOffUList = kOffGrp + kGCap * 2;                // kMCap u16: members with kept tokens
 constexpr uint32_t kOffTile = kOffUList + kMCap * 2;               // kWarps x 16 x 33 u32
 constexpr uint32_t kOffHist = kOffTile + kWarps * 16 * 33 * 4;    // 2048 u32 (A-F)
+constexpr uint32_t kMapCap = kWarps * 16 * 33 * 2;                 // u16 flat->list map entries (tile space)
 constexpr uint32_t kEndAE = kOffHist + 2048 * 4;
 constexpr uint32_t kOffQ = 0;                                      // 32 x kQPitch f32 (G)
 constexpr uint32_t kTok = 2;                                       // stage-4 tokens per warp step
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 3) wave_worker_kernel(const IndexVie
     uint16_t* goff = reinterpret_cast<uint16_t*>(smem + kOffGOff);    // member rank -> kept-token count, then offset
     uint16_t* ulist = reinterpret_cast<uint16_t*>(smem + kOffUList);  // members with a kept token (this range)
     uint32_t* tile = reinterpret_cast<uint32_t*>(smem + kOffTile) + warp * 16 * 33;
-    uint8_t* grp = reinterpret_cast<uint8_t*>(smem + kOffGrp);        // kept list of each kept token, by member
+    uint16_t* grp = reinterpret_cast<uint16_t*>(smem + kOffGrp);      // 33 x kept list of each kept token, by member
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kOffHist);
     uint64_t* keys_used = side0 + 2 * a.c1cap;                        // keys of the members with a kept token
     const uint32_t W = a.range_w, R = a.range_n, WW = W / 32;
@@ -449,14 +450,26 @@ __global__ void __launch_bounds__(kThreads, 3) wave_worker_kernel(const IndexVie
         if (tid * 2 < nl) lpref[tid * 2] = ex, rbeg[tid * 2] = tb[0];
         if (tid * 2 + 1 < nl) lpref[tid * 2 + 1] = ex + c0, rbeg[tid * 2 + 1] = tb[1];
         if (tid == 0) lpref[nl] = tot;
+        // flat posting index -> list, when the range's runs fit the map
+        // (shares the stage-2 tile's space, free until step 5)
+        const bool use_map = tot <= kMapCap;
+        if (use_map) {
+            uint16_t* map = reinterpret_cast<uint16_t*>(smem + kOffTile);
+            for (uint32_t i = 0; i < c0; ++i) map[ex + i] = uint16_t(tid * 2);
+            for (uint32_t i = 0; i < c1n; ++i) map[ex + c0 + i] = uint16_t(tid * 2 + 1);
+        }
         __syncthreads();
         const uint32_t total_p = lpref[nprobed], total = lpref[nl];
         const uint32_t base_pid = r * W;
         lap(0);
         auto locate = [&](uint32_t f, uint32_t lo, uint32_t hi) -> uint64_t {  // (list << 40) | posting index
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (lpref[mid] <= f) lo = mid; else hi = mid;
+            if (use_map) {
+                lo = reinterpret_cast<const uint16_t*>(smem + kOffTile)[f];
+            } else {
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (lpref[mid] <= f) lo = mid; else hi = mid;
+                }
             }
             return (uint64_t(lo) << 40) | (lstart[lo] + rbeg[lo] + (f - lpref[lo]));
         };
@@ -556,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 3) wave_worker_kernel(const IndexVie
             __syncthreads();
 #pragma unroll
             for (int x = 0; x < int(kPer); ++x)
-                if (rk[x] != 0xFFFFFFFFu) grp[goff[rk[x]] + at[x]] = uint8_t(kl[x]);
+                if (rk[x] != 0xFFFFFFFFu) grp[goff[rk[x]] + at[x]] = uint16_t(kl[x] * 33);
             __syncthreads();
             lap(4);
             // (5) members: stage-2 key = in-order sum over the query tokens of
@@ -578,7 +591,12 @@ __global__ void __launch_bounds__(kThreads, 3) wave_worker_kernel(const IndexVie
                     const uint32_t m = ulist[u0 + i];
                     const uint32_t gs = goff[m], ge = goff[m + 1];
                     uint32_t mx = 0;
-                    for (uint32_t g = gs; g < ge; ++g) mx = max(mx, ks[uint32_t(grp[g]) * 33 + lane]);
+                    uint32_t g = gs;
+                    for (; g + 4 <= ge; g += 4) {
+                        const uint32_t a0 = grp[g], a1 = grp[g + 1], a2 = grp[g + 2], a3 = grp[g + 3];
+                        mx = max(max(mx, ks[a0 + lane]), max(ks[a1 + lane], max(ks[a2 + lane], ks[a3 + lane])));
+                    }
+                    for (; g < ge; ++g) mx = max(mx, ks[grp[g] + lane]);
                     tile[i * 33 + lane] = mx;
                 }
                 __syncwarp();

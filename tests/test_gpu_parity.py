@@ -313,7 +313,7 @@ def test_batch_searcher_bit_exact(small, port, lanes):
     """Throughput mode: every query of a batch spread over `lanes` concurrent
     streams returns exactly the reference's single-query result."""
     h, qs, idx, _ = small
-    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.EXACT)
+    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.EXACT, engine="lanes")
     qb = np.concatenate([qs, qs[::-1], qs[:3]])
     for k in (10, 1000):
         p = P.default_params_for_k(k)
@@ -337,7 +337,7 @@ def test_batch_tensor_scores_match_single(small, lanes):
     sizes end with a one-query pass."""
     h, qs, idx, _ = small
     single = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
-    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.TENSOR)
+    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.TENSOR, engine="lanes")
     qb = np.concatenate([qs, qs[1:4]])  # 9 queries
     for k in (10, 100, 1000):
         p = P.default_params_for_k(k)

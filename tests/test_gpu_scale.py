@@ -150,7 +150,7 @@ def test_batch_tensor_vs_reference(cfg1, best, lanes):
     """Throughput mode with two queries per S_cq pass (TfCfg<2>) against the
     reference, query by query."""
     h, qs, idx = cfg1
-    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.TENSOR)
+    b = P.BatchSearcher(idx, lanes=lanes, score_mode=P.ScoreMode.TENSOR, engine="lanes")
     single = P.Searcher(idx, score_mode=P.ScoreMode.TENSOR)
     qb = np.concatenate([qs, qs[:3]])
     for k in (10, 100):
