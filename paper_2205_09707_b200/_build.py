@@ -26,7 +26,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
     "--expt-relaxed-constexpr", "-I", str(CSRC), "-I", str(ROOT / "include"),
 ]
-CU_SOURCES = ["scores.cu", "candidates.cu", "interaction.cu", "select.cu", "rank.cu", "rank128.cu", "gemm_tf32.cu", "wave_scores.cu", "wave_worker.cu", "storage.cu", "encode.cu", "synth_device.cu"]
+CU_SOURCES = ["scores.cu", "candidates.cu", "interaction.cu", "select.cu", "rank.cu", "rank128.cu", "gemm_tf32.cu", "range_stage2.cu", "wave_scores.cu", "wave_worker.cu", "storage.cu", "encode.cu", "synth_device.cu"]
 CPP_SOURCES = ["engine.cpp", "capi.cpp"]
 
 

@@ -222,6 +222,19 @@ template struct DevBuf<SelectHist>;
 template struct DevBuf<int>;
 
 // ---------------------------------------------------------------- DeviceIndex
+void DeviceIndex::build_range_table(cudaStream_t st) {
+    // per (centroid, pid range of launch::kWaveRangeIds ids): where the list's
+    // run in the range starts — index-side, once (binary searches on the GPU)
+    const uint64_t N = view_.N, K = view_.K;
+    if (!N || !K || N > 0xFFFFFFFFull) return;
+    const uint32_t W = launch::kWaveRangeIds, R = uint32_t((N + W - 1) / W);
+    uint32_t* tab = upload<uint32_t>(nullptr, K * (uint64_t(R) + 1));
+    launch::wave_range_table(view_, W, R, tab, st);
+    PLAID_CUDA(cudaStreamSynchronize(st));
+    PLAID_CUDA(cudaGetLastError());
+    view_.range_tab = tab, view_.range_w = W, view_.range_n = R;
+}
+
 template <typename T>
 T* DeviceIndex::upload(const T* src, uint64_t count) {
     void* p = nullptr;
@@ -323,6 +336,7 @@ DeviceIndex::DeviceIndex(const plaid_index_desc& d, int device, uint64_t pid_bas
             PLAID_CUDA(cudaGetLastError());
             view_.tok_inv = inv;
         }
+        build_range_table(0);
     } catch (...) {
         for (void* p : allocs_) cudaFree(p);
         allocs_.clear();
@@ -592,6 +606,21 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
     if (p.nprobe == K) {
         launch::iota(sel_.p, K, st);
         nsel = K;
+    } else if (p.nprobe <= 8 && !p.disable_filter && launch::range_stage2_ok(ix, rows, uint64_t(rows) * p.nprobe) &&
+               !getenv("PLAID_NO_RANGE_STAGE2")) {
+        // candidates + stage 2 in one launch, a CTA per pid range
+        // (range_stage2.cu): topn_postings only merges the top-nprobe lists
+        // and builds the kept list; no bitmap, no compaction, no slot map
+        launch::KeepListArgs kl{keep_.p, kept_list_.p, reinterpret_cast<unsigned long long*>(c + kKeptN)};
+        launch::topn_postings(partial_.p, warps, npb, rows, uint32_t(p.nprobe), ix, sel_.p, nullptr, &kl, st);
+        record(2, st, times);
+        launch::range_stage2(ix, scores_.p, rows, sel_.p, rows * uint32_t(p.nprobe), keep_.p, kept_list_.p,
+                             reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p, c + kN1,
+                             reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, st);
+        record(3, st, times);
+        launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st);
+        record(4, st, times);
+        return;
     } else if (p.nprobe <= 32) {
         // the kept-centroid list rides in the same launch unless stage 2 is skipped
         launch::KeepListArgs kl{keep_.p, kept_list_.p, reinterpret_cast<unsigned long long*>(c + kKeptN)};
@@ -1347,7 +1376,7 @@ WavePipeline::~WavePipeline() {
 
 bool WavePipeline::supports(const plaid_params& p, uint64_t rows, uint64_t dim) const {
     const IndexView& ix = index_->view();
-    return ix.dim == 128 && dim == 128 && rows >= 1 && rows <= 32 && ix.tok_inv && !p.disable_filter &&
+    return ix.dim == 128 && dim == 128 && rows >= 1 && rows <= 32 && ix.tok_inv && ix.range_tab && !p.disable_filter &&
            p.nprobe >= 1 && p.nprobe <= 8 && p.nprobe <= ix.K && ix.N < (1ull << 31) &&
            std::min<uint64_t>(stage3_width(p), ix.N) <= launch::kWaveSortCap && p.ndocs <= (1ull << 24) &&
            index_->candidate_bound(p.nprobe) < (1ull << 31);
@@ -1380,15 +1409,6 @@ void WavePipeline::ensure(uint64_t nq, const plaid_params& p) {
     }();
     uint64_t want = std::min<uint64_t>(std::max<uint64_t>(nq, 1), std::min<uint64_t>(resident, 1024));
     if (tensor_) want = (want + 3) / 4 * 4;
-    if (!range_tab_.p) {
-        // the worker's per-(centroid, pid range) posting offsets (index-side, once)
-        range_w_ = launch::kWaveRangeIds;
-        range_n_ = uint32_t((N + range_w_ - 1) / range_w_);
-        range_tab_.ensure(K * (range_n_ + 1));
-        launch::wave_range_table(ix, range_w_, range_n_, range_tab_.p, 0);
-        PLAID_CUDA(cudaDeviceSynchronize());
-        PLAID_CUDA(cudaGetLastError());
-    }
     const bool fits = slots_ >= want && c1cap_ >= c1cap && sel_stride_ >= sel_stride && nd_cap_ >= nd;
     if (fits) return;
     // grow: release first so the free-memory estimate sees the old buffers
@@ -1453,7 +1473,7 @@ void WavePipeline::run(const float* d_q, uint64_t nq, uint32_t rows, const plaid
         a.k = uint32_t(p.k), a.nlists = lists, a.pid_base = uint32_t(index_->pid_base()), a.validate = validate ? 1 : 0;
         a.S = S_.p, a.s_stride = s_stride_, a.keep = keep_.p, a.keep_stride = keep_stride_;
         a.partial = partial_.p, a.partial_stride = partial_stride_;
-        a.range_tab = range_tab_.p, a.range_w = range_w_, a.range_n = range_n_;
+        a.range_tab = ix.range_tab, a.range_w = ix.range_w, a.range_n = ix.range_n;
         a.c1 = c1_.p, a.acc = acc_.p, a.keys = keys_.p, a.side = side_.p, a.c1cap = c1cap_;
         a.sel = sel_.p, a.sel_stride = sel_stride_;
         a.out_pids = d_pids + j0 * p.k, a.out_scores = d_scores + j0 * p.k, a.out_n = d_n + j0;

@@ -102,6 +102,7 @@ private:
     std::vector<uint32_t> h_doclens_;
     std::vector<uint64_t> longest_prefix_;  // [K + 1]: sums of the j longest list lengths
     void set_list_bounds(const uint64_t* ivf_offsets_host);
+    void build_range_table(cudaStream_t st);
 };
 
 // Host-side pinned/device buffer helper.
@@ -297,10 +298,9 @@ private:
     alignas(64) unsigned char tmap_[128];
     uint32_t slots_ = 0;
     uint64_t c1cap_ = 0, sel_stride_ = 0, partial_stride_ = 0, keep_stride_ = 0, nd_cap_ = 0, s_stride_ = 0;
-    uint32_t range_w_ = 0, range_n_ = 0;
     uint64_t last_launches_ = 0;
     DevBuf<float> S_, rowmax_;
-    DevBuf<uint32_t> keep_, range_tab_, c1_, acc_;
+    DevBuf<uint32_t> keep_, c1_, acc_;
     DevBuf<uint64_t> partial_, keys_, side_, sel_, counters_, trace_;
     DevBuf<int> status_;
     bool tracing_ = false;

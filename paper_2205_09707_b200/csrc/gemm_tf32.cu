@@ -6,8 +6,9 @@
 // (pipeline.cpp:90-110).
 //
 // Precision: 3xTF32.  Each fp32 operand is split into hi = x with the low 13
-// mantissa bits cleared and lo = tf32_rn(x - hi) (rounded: the tensor core
-// truncates fp32 operands to tf32, tools/tf32_round.cu), and
+// mantissa bits cleared and lo = x - hi (the tensor core truncates fp32
+// operands to tf32, tools/tf32_round.cu: C_hi is the raw row, and C_lo is
+// truncated in turn — Q_lo is rounded, it is built once per query), and
 // S = C_hi.Q_hi + C_hi.Q_lo + C_lo.Q_hi is accumulated in fp32 in TMEM: ~2e-6
 // absolute on unit-vector dots (tests/test_gpu_parity.py), while HBM traffic
 // stays one fp32 read of C.
@@ -127,13 +128,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
+// suspend-time hint: a waiting warp sleeps until the phase completes instead
+// of re-polling (the polls were 16% of the issued instructions)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(0x100000)
         : "memory");
 }
 
@@ -236,6 +239,9 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 
 __device__ __forceinline__ uint32_t split_hi(uint32_t x) { return x & 0xFFFFE000u; }
+__device__ __forceinline__ uint32_t lo_trunc(uint32_t x) {
+    return __float_as_uint(__fsub_rn(__uint_as_float(x), __uint_as_float(split_hi(x))));
+}
 
 // x - trunc_tf32(x) rounded to the nearest tf32 (an unrounded lo would be
 // truncated again by the tensor core and bias every dot product downwards)
@@ -390,18 +396,23 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
                 // the row's 8 granules of chunk kc, un-swizzled: granule j at (j ^ (lane & 7))
                 const uint4* src =
                     reinterpret_cast<const uint4*>(smem + kOffRaw + s * kChunkBytes + (kc * 32 + lane) * 128);
+                // A_hi = the raw fp32 row (the tensor core truncates it to
+                // tf32), A_lo = C - trunc(C) exactly (truncated to tf32 by the
+                // tensor core in turn: < 2^-22 |c| per element, < 3e-7 on a
+                // unit dot).  The rounding split cost 4 ALU operations per
+                // element, and the converters were on the critical path.
                 uint32_t hi[32], lo[32];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const uint4 v = src[j ^ (lane & 7)];
-                    hi[4 * j + 0] = split_hi(v.x);
-                    hi[4 * j + 1] = split_hi(v.y);
-                    hi[4 * j + 2] = split_hi(v.z);
-                    hi[4 * j + 3] = split_hi(v.w);
-                    lo[4 * j + 0] = split_lo(v.x);
-                    lo[4 * j + 1] = split_lo(v.y);
-                    lo[4 * j + 2] = split_lo(v.z);
-                    lo[4 * j + 3] = split_lo(v.w);
+                    hi[4 * j + 0] = v.x;
+                    hi[4 * j + 1] = v.y;
+                    hi[4 * j + 2] = v.z;
+                    hi[4 * j + 3] = v.w;
+                    lo[4 * j + 0] = lo_trunc(v.x);
+                    lo[4 * j + 1] = lo_trunc(v.y);
+                    lo[4 * j + 2] = lo_trunc(v.z);
+                    lo[4 * j + 3] = lo_trunc(v.w);
                 }
                 if (kc == kChunks - 1) {
                     __syncwarp();
@@ -529,11 +540,38 @@ scores_tf32_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const _
             }
             if (ew == 0 && lane == 0) trace_stamp(dbg, 6, lt);
         }
+        if constexpr (NP <= 8) {
+            // one list per CTA and token: the 8 epilogue warps' lists merged
+            // here (through the transpose buffer, free once every epilogue
+            // warp is done), so the consumers merge 148 lists, not 1184
+            uint64_t* kx = reinterpret_cast<uint64_t*>(smem + kOffTr);  // [QB][8 warps][32 tokens][NP]
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
 #pragma unroll
-        for (int qi = 0; qi < QB; ++qi) {
-            uint64_t* po = out.partial[qi] + ((uint64_t(blockIdx.x) * kEpiWarps + ew) * 32 + lane) * NP;
+            for (int qi = 0; qi < QB; ++qi)
 #pragma unroll
-            for (int j = 0; j < NP; ++j) po[j] = top_s[qi][j] == -INFINITY ? 0 : dev::make_key(top_s[qi][j], top_i[qi][j]);
+                for (int j = 0; j < NP; ++j)
+                    kx[((qi * kEpiWarps + ew) * 32 + lane) * NP + j] =
+                        top_s[qi][j] == -INFINITY ? 0 : dev::make_key(top_s[qi][j], top_i[qi][j]);
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+            if (ew < uint32_t(QB)) {
+                uint64_t top[NP];
+#pragma unroll
+                for (int j = 0; j < NP; ++j) top[j] = 0;
+                for (uint32_t w = 0; w < kEpiWarps; ++w)
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) dev::topn_insert<NP>(top, kx[((ew * kEpiWarps + w) * 32 + lane) * NP + j]);
+                uint64_t* po = out.partial[ew] + (uint64_t(blockIdx.x) * 32 + lane) * NP;
+#pragma unroll
+                for (int j = 0; j < NP; ++j) po[j] = top[j];
+            }
+        } else {
+#pragma unroll
+            for (int qi = 0; qi < QB; ++qi) {
+                uint64_t* po = out.partial[qi] + ((uint64_t(blockIdx.x) * kEpiWarps + ew) * 32 + lane) * NP;
+#pragma unroll
+                for (int j = 0; j < NP; ++j)
+                    po[j] = top_s[qi][j] == -INFINITY ? 0 : dev::make_key(top_s[qi][j], top_i[qi][j]);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -646,7 +684,7 @@ uint32_t scores_tensor(const void* cmap, const IndexView& ix, const float* d_q, 
     out.Q[0] = d_q, out.S[0] = d_scores, out.keep[0] = d_keep_bits, out.partial[0] = d_partial, out.gthr[0] = d_gthr;
     const uint32_t grid = tf32_grid(ix);
     launch_tf32_np<1>(map, ix, out, rows, t_cs, np_bucket, grid, st);
-    return grid * kEpiWarps;
+    return np_bucket <= 8 ? grid : grid * kEpiWarps;  // one list per CTA (merged in the epilogue) up to NP = 8
 }
 
 uint32_t scores_tensor_batch(const void* cmap, const IndexView& ix, const TfOut& out, uint32_t qb, uint32_t rows,
@@ -655,7 +693,7 @@ uint32_t scores_tensor_batch(const void* cmap, const IndexView& ix, const TfOut&
     const uint32_t grid = tf32_grid(ix);
     if (qb == 1) launch_tf32_np<1>(map, ix, out, rows, t_cs, np_bucket, grid, st);
     else launch_tf32_np<2>(map, ix, out, rows, t_cs, np_bucket, grid, st);
-    return grid * kEpiWarps;
+    return np_bucket <= 8 ? grid : grid * kEpiWarps;
 }
 
 }  // namespace launch

@@ -27,6 +27,10 @@ struct IndexView {
     const uint32_t* ivf_postings = nullptr;
     const uint8_t* ivf_mult = nullptr;  // P: tokens of the passage with the posting's code (<= 255, saturating)
     const float* tok_inv = nullptr;     // T: 1 / ||C[code] + residual|| per token (d = 128; TENSOR stage 4)
+    // [K][range_n + 1]: offset in c's posting list of its first posting >= r
+    // range_w (wave_range_table); the range kernels' run locator
+    const uint32_t* range_tab = nullptr;
+    uint32_t range_w = 0, range_n = 0;
     float weights[16] = {};
 };
 
@@ -204,6 +208,17 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
                    uint32_t* d_used_bits, uint32_t* d_kept_list, const uint32_t* d_slot_of, uint32_t* d_acc,
                    unsigned long long* d_counts2, uint64_t* d_out_keys, unsigned long long* d_rows,
                    SelectHist* d_hist, bool kept_ready, cudaStream_t st);
+
+// Candidate generation + stage 2 in one launch, a CTA per pid range
+// (range_stage2.cu): from the probed centroids sel[nsel] and the kept list
+// (topn_postings' kl outputs), stage-2 keys of every C1 member into
+// d_keys[0..*d_n1) (order unspecified), the select histogram, the
+// stage1_candidates / stage2_rows_gathered counters.  Needs ix.range_tab.
+bool range_stage2_ok(const IndexView& ix, uint32_t rows, uint64_t nsel);
+void range_stage2(const IndexView& ix, const float* d_scores, uint32_t rows, const uint32_t* d_sel, uint32_t nsel,
+                  const uint32_t* d_keep_bits, const uint32_t* d_kept, const unsigned long long* d_kept_counts,
+                  uint64_t* d_keys, uint64_t* d_n1, unsigned long long* d_rows, SelectHist* d_hist,
+                  cudaStream_t st);
 
 // ---- selection -----------------------------------------------------------------------
 // Top `want` of keys[0..*d_n) (largest first).  Result: d_out_keys unsorted

@@ -235,6 +235,7 @@ __global__ void topn_postings_kernel(const uint64_t* __restrict__ partial, uint3
     merge_token_lists<NP>(partial, nwarps, i, lists);
     const uint32_t c = dev::key_id(lists[j]);
     if (threadIdx.x == 0) sel[i * nprobe + j] = c;
+    if (!bitmap) return;  // range_stage2 reads the probed lists itself
     const uint64_t b = ivf_offsets[c], e = ivf_offsets[c + 1];
     // kU postings per thread in flight: unpredicated loads (index clamped into
     // the list), so the ~2K-entry list costs ~3 HBM round trips, not ~9

@@ -346,6 +346,7 @@ DeviceIndex::DeviceIndex(const SynthSpec& sp, int device) : device_(device), pid
             launch::token_inv_norms(view_, inv, st);
             view_.tok_inv = inv;
         }
+        build_range_table(st);
         PLAID_CUDA(cudaStreamSynchronize(st));
         PLAID_CUDA(cudaGetLastError());
     } catch (...) {
