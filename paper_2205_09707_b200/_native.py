@@ -159,6 +159,7 @@ SIGNATURES = {
     "plaid_debug_set_tf32_grid": (C.c_uint32, [C.c_uint32]),
     "plaid_debug_set_launch_cap": (C.c_longlong, [C.c_longlong]),
     "plaid_debug_wave_trace": (C.c_int, [C.c_void_p, u64p, C.c_uint64]),
+    "plaid_debug_rs2_trace": (C.c_int, [C.c_int, C.c_void_p]),
 }
 
 _lib = None

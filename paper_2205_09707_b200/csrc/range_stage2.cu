@@ -13,11 +13,13 @@
 //   * compaction in id order gives each member its rank; one atomic reserves
 //     the range's slots in the stage-2 key array (key order is irrelevant to
 //     the select that follows, which ranks keys, not positions);
-//   * the kept lists' runs (t_cs keep bits, pipeline.cpp:89-95) are grouped
-//     by member with a counting sort; a warp scores eight members at a time,
-//     lane = query token: the max of the member's kept centroids' S rows
-//     (held in shared memory), then the in-order fp32 sum (0 without a kept
-//     token) — the same keys as the reference, bit for bit;
+//   * the kept lists' runs (t_cs keep bits, pipeline.cpp:89-95; at most 64
+//     kept lists) set one bit per (member, kept list) in a 64-bit mask per
+//     member — the member's set of distinct kept codes, all the max needs —
+//     and a thread per member forms the key: per query token the max of
+//     its kept lists' S rows (held in shared memory), then the in-order fp32
+//     sum (0 without a kept token) — the same keys as the reference, bit
+//     for bit (a warp-per-member grouping was latency-bound: ~14 us);
 //   * the key histogram the stage-2 select starts from (SelectHist), and the
 //     StageTrace counters (stage1_candidates, stage2_rows_gathered with the
 //     postings' token multiplicities).
@@ -34,16 +36,15 @@
 namespace plaid {
 namespace {
 
-constexpr uint32_t kThreads = 512;
+constexpr uint32_t kThreads = 1024;  // one CTA per SM: every warp hides the scoring's latency
 constexpr uint32_t kWarps = kThreads / 32;
 constexpr uint32_t kKeptLists = 64;
 constexpr uint32_t kMaxLists = 256 + kKeptLists;
 constexpr uint32_t kRangeWords = launch::kWaveRangeIds / 32;
 constexpr uint32_t kMCap = 4096;               // members per range
-constexpr uint32_t kPer = 8;                   // postings per thread per round
+constexpr uint32_t kPer = 4;                   // postings per thread per round
 constexpr uint32_t kGCap = kPer * kThreads;    // kept postings per range (one register round)
-constexpr uint32_t kTileM = 32;                // members per warp batch (lane i sums member i)
-constexpr uint32_t kMapCap = kWarps * kTileM * 33 * 2;  // u16 flat -> list entries (tile space)
+constexpr uint32_t kMapCap = 8192;            // u16 flat -> list entries (longer ranges: binary search)
 
 constexpr uint32_t kOffLCent = 0;
 constexpr uint32_t kOffLStart = kOffLCent + kMaxLists * 4;
@@ -53,12 +54,13 @@ constexpr uint32_t kOffKS = kOffRBeg + kMaxLists * 4;
 constexpr uint32_t kOffBm = kOffKS + kKeptLists * 33 * 4;
 constexpr uint32_t kOffWpre = kOffBm + kRangeWords * 4;
 constexpr uint32_t kOffMPid = kOffWpre + kRangeWords * 2;
-constexpr uint32_t kOffGOff = kOffMPid + kMCap * 2;
-constexpr uint32_t kOffGrp = kOffGOff + (kMCap + 8) * 2;
-constexpr uint32_t kOffUList = kOffGrp + kGCap * 2;
-constexpr uint32_t kOffTile = kOffUList + kMCap * 2;
-constexpr uint32_t kSmemBytes = kOffTile + kWarps * kTileM * 33 * 4;
+constexpr uint32_t kOffMask = kOffMPid + kMCap * 2;                 // kMCap x 2 u32: kept-list mask per member
+constexpr uint32_t kOffMap = kOffMask + kMCap * 8;                   // kMapCap u16: flat posting -> list
+constexpr uint32_t kOffUList = kOffMap + kMapCap * 2;                // kMCap u16: members with a kept token
+constexpr uint32_t kOffTile = kOffUList + kMCap * 2;                 // kWarps x 32 x 33 u32
+constexpr uint32_t kSmemBytes = kOffTile + kWarps * 32 * 33 * 4;
 static_assert(kRangeWords % kThreads == 0 && kMCap % kThreads == 0 && kThreads >= kMaxLists, "layout");
+static_assert(kSmemBytes + sizeof(uint32_t) * 256 <= 227 * 1024, "shared memory budget");
 
 struct Shared {
     uint32_t warp_tot[kWarps];
@@ -67,6 +69,18 @@ struct Shared {
     uint32_t rows32;
     uint32_t kept_s[kKeptLists];
 };
+
+// Debug timeline (plaid_debug_rs2_trace): globaltimer at the phase
+// boundaries of every CTA, when enabled.
+__device__ int g_rs2_on;
+__device__ unsigned long long g_rs2_t[512 * 8];
+__device__ __forceinline__ void rs2_stamp(bool on, int k) {  // `on`: g_rs2_on, read once per CTA
+    if (on && threadIdx.x == 0 && blockIdx.x < 512) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_rs2_t[blockIdx.x * 8 + k] = t;
+    }
+}
 
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t* total) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -146,7 +160,10 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
                     const unsigned long long* __restrict__ kept_counts, uint64_t* __restrict__ keys_out,
                     unsigned long long* __restrict__ d_n1, unsigned long long* __restrict__ d_rows,
                     SelectHist* __restrict__ hs) {
+    const bool trace_on = g_rs2_on != 0;  // one load, in flight with the PDL wait
+    rs2_stamp(trace_on, 6);  // CTA start (before the PDL wait)
     dev::pdl_wait();
+    rs2_stamp(trace_on, 0);
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ Shared sh;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -160,11 +177,10 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
     uint32_t* bm = reinterpret_cast<uint32_t*>(smem + kOffBm);
     uint16_t* wpre = reinterpret_cast<uint16_t*>(smem + kOffWpre);
     uint16_t* mpid = reinterpret_cast<uint16_t*>(smem + kOffMPid);
-    uint16_t* goff = reinterpret_cast<uint16_t*>(smem + kOffGOff);
-    uint16_t* grp = reinterpret_cast<uint16_t*>(smem + kOffGrp);
+    uint32_t* mmask = reinterpret_cast<uint32_t*>(smem + kOffMask);
+    uint16_t* map = reinterpret_cast<uint16_t*>(smem + kOffMap);
     uint16_t* ulist = reinterpret_cast<uint16_t*>(smem + kOffUList);
-    uint16_t* map = reinterpret_cast<uint16_t*>(smem + kOffTile);
-    uint32_t* tile = reinterpret_cast<uint32_t*>(smem + kOffTile) + warp * kTileM * 33;
+    uint32_t* tile = reinterpret_cast<uint32_t*>(smem + kOffTile) + warp * 32 * 33;
     uint32_t* kept_s = sh.kept_s;
 
     // the probed centroids (topn_postings: merge of the S_cq CTAs' top-nprobe
@@ -191,7 +207,7 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
     for (uint32_t j = warp; j < nk; j += kWarps)
         ks[j * 33 + lane] = dev::ord_f32(__ldg(S + uint64_t(kept_s[j]) * kScoresPitch + lane));
     for (uint32_t w = tid; w < kRangeWords; w += kThreads) bm[w] = 0u;
-    for (uint32_t m = tid; m < kMCap; m += kThreads) goff[m] = 0;
+    for (uint32_t m = tid; m < 2 * kMCap; m += kThreads) mmask[m] = 0u;
     if (tid < 32) sh.blk_s[tid] = 0;
     if (tid == 0) sh.zeros = 0, sh.ucount = 0, sh.rows32 = 0;
     uint32_t tot;
@@ -202,6 +218,7 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
     if (use_map && tid < nl)
         for (uint32_t i = 0; i < cnt; ++i) map[ex + i] = uint16_t(tid);
     __syncthreads();
+    rs2_stamp(trace_on, 1);
     const uint32_t total_p = lpref[nsel], total = lpref[nl];
     auto locate = [&](uint32_t f, uint32_t lo, uint32_t hi) -> uint64_t {  // (list << 40) | posting index
         if (use_map) {
@@ -243,6 +260,7 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
             }
     }
     __syncthreads();
+    rs2_stamp(trace_on, 2);
     // (3) compaction: member ranks in id order; the range's key slots
     uint32_t m_r;
     {
@@ -268,22 +286,22 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
         if (tid == 0) sh.base = m_r ? uint32_t(atomicAdd(d_n1, (unsigned long long)m_r)) : 0u;
     }
     __syncthreads();
+    rs2_stamp(trace_on, 3);
     const uint32_t kbase = sh.base;
     uint64_t* keys = keys_out + kbase;
     if (walk && m_r <= kMCap) {
-        // (4) kept postings -> their member: counting sort by rank
-        uint32_t rk[kPer], at[kPer];
+        // (4) kept postings -> a 64-bit mask per member over the kept lists
+        // (<= 64): the member's set of distinct kept codes is all the max
+        // needs (pipeline.cpp:112-131)
         unsigned long long rows_local = 0;
 #pragma unroll
         for (int x = 0; x < int(kPer); ++x) {
-            rk[x] = 0xFFFFFFFFu;
             if (total_p + x * kThreads + tid < total) {
                 const uint32_t o = kp[x] - base_pid;
                 const uint32_t wv = bm[o >> 5];
                 if ((wv >> (o & 31)) & 1u) {
-                    rk[x] = wpre[o >> 5] + __popc(wv & ((1u << (o & 31)) - 1u));
-                    at[x] = atomicAdd(reinterpret_cast<unsigned int*>(goff + (rk[x] & ~1u)), 1u << (16 * (rk[x] & 1u)));
-                    at[x] = (at[x] >> (16 * (rk[x] & 1u))) & 0xFFFFu;  // counts <= kGCap: no carry between halves
+                    const uint32_t rk = wpre[o >> 5] + __popc(wv & ((1u << (o & 31)) - 1u));
+                    atomicOr(mmask + 2 * rk + (kl[x] >> 5), 1u << (kl[x] & 31));
                     uint32_t m = km[x];
                     if (m == 255) {  // saturated multiplicity: recount from the codes
                         const uint32_t p = kp[x], c = lcent[nsel + kl[x]];
@@ -296,60 +314,61 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
                 }
             }
         }
-        // warp-reduced first: a 64-bit shared-memory atomic is a CAS loop, and
-        // 512 of them on one word were a quarter of this kernel's time
+        // warp-reduced first: a 64-bit shared-memory atomic is a CAS loop
         uint32_t rl = uint32_t(rows_local);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) rl += __shfl_xor_sync(0xffffffffu, rl, o);
         if (lane == 0 && rl) atomicAdd(&sh.rows32, rl);
         __syncthreads();
-        {  // exclusive scan of the per-member counts (in place)
-            constexpr uint32_t kPM = kMCap / kThreads;
-            uint32_t v[kPM], mine = 0;
-#pragma unroll
-            for (uint32_t j = 0; j < kPM; ++j) v[j] = goff[tid * kPM + j], mine += v[j];
-            uint32_t gt;
-            uint32_t run = block_excl_scan(mine, sh.warp_tot, &gt);
-#pragma unroll
-            for (uint32_t j = 0; j < kPM; ++j) goff[tid * kPM + j] = uint16_t(run), run += v[j];
-            if (tid == 0) goff[kMCap] = uint16_t(gt);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int x = 0; x < int(kPer); ++x)
-            if (rk[x] != 0xFFFFFFFFu) grp[goff[rk[x]] + at[x]] = uint16_t(kl[x] * 33);
+        rs2_stamp(trace_on, 4);
         // (5) members without a kept token: key 0; the others listed
         for (uint32_t m0 = 0; m0 < m_r; m0 += kThreads) {
             const uint32_t m = m0 + tid;
             bool z = false;
             uint64_t key = 0;
             if (m < m_r) {
-                if (goff[m + 1] > goff[m]) ulist[atomicAdd(&sh.ucount, 1u)] = uint16_t(m);
-                else {
+                if (!(mmask[2 * m] | mmask[2 * m + 1])) {
                     z = true;
                     key = dev::make_key(0.0f, base_pid + mpid[m]);
                     keys[m] = key;
                 }
             }
+            // the members with a kept token, listed (one shared atomic per warp)
+            const bool u = m < m_r && !z;
+            const uint32_t ub = __ballot_sync(0xffffffffu, u);
+            uint32_t b0 = 0;
+            if (lane == 0 && ub) b0 = atomicAdd(&sh.ucount, __popc(ub));
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if (u) ulist[b0 + __popc(ub & ((1u << lane) - 1u))] = uint16_t(m);
             hist_key(hs, key, z, sh);
         }
         __syncthreads();
-        // (6) warps score the listed members, eight at a time: lane = query
-        // token takes the max over the member's kept rows, lane i < 8 then
-        // sums member i's row in order (pipeline.cpp:125-131)
+        rs2_stamp(trace_on, 7);
+        // (6) a warp takes 32 listed members: lane = query token, the max over
+        // the member's kept lists (mask bits, four loads in flight) into a
+        // tile row; then lane i sums member i's row in order (pipeline.cpp:
+        // 125-131).  A thread per member (divergent mask loops) or a grouped
+        // list with dependent loads were both latency-bound
         const uint32_t nu = sh.ucount;
-        for (uint32_t u0 = warp * kTileM; u0 < nu; u0 += kWarps * kTileM) {
-            const uint32_t ub = nu - u0 < kTileM ? nu - u0 : kTileM;
+        // batches of kBatch members spread over all warps (a 32-member batch
+        // left half the warps idle and serialised 32 members per warp)
+        constexpr uint32_t kBatch = 8;
+        for (uint32_t u0 = warp * kBatch; u0 < nu; u0 += kWarps * kBatch) {
+            const uint32_t ub = nu - u0 < kBatch ? nu - u0 : kBatch;
             for (uint32_t i = 0; i < ub; ++i) {
                 const uint32_t m = ulist[u0 + i];
-                const uint32_t gs = goff[m], ge = goff[m + 1];
+                uint64_t x = (uint64_t(mmask[2 * m + 1]) << 32) | mmask[2 * m];
                 uint32_t mx = 0;
-                uint32_t g = gs;
-                for (; g + 4 <= ge; g += 4) {
-                    const uint32_t a0 = grp[g], a1 = grp[g + 1], a2 = grp[g + 2], a3 = grp[g + 3];
-                    mx = max(max(mx, ks[a0 + lane]), max(ks[a1 + lane], max(ks[a2 + lane], ks[a3 + lane])));
+                while (x) {
+                    uint32_t l[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        l[u] = x ? uint32_t(__ffsll(x) - 1) : l[0];
+                        x &= x - 1;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) mx = max(mx, ks[l[u] * 33 + lane]);
                 }
-                for (; g < ge; ++g) mx = max(mx, ks[grp[g] + lane]);
                 tile[i * 33 + lane] = mx;
             }
             __syncwarp();
@@ -357,16 +376,20 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
             const bool live = lane < ub;
             if (live) {
                 const uint32_t m = ulist[u0 + lane];
+                uint32_t v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = tile[lane * 33 + j];  // all loads in flight
                 float t = 0.0f;
-                for (uint32_t j = 0; j < rows; ++j) t = __fadd_rn(t, dev::unord_f32(tile[lane * 33 + j]));
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (uint32_t(j) < rows) t = __fadd_rn(t, dev::unord_f32(v[j]));
                 key = dev::make_key(t, base_pid + mpid[m]);
                 keys[m] = key;
             }
             hist_key(hs, key, live, sh);
             __syncwarp();
         }
-    } else {
-        // code scan: a warp per member (bitmap order), masked interaction
+    } else {        // code scan: a warp per member (bitmap order), masked interaction
         unsigned long long rows_local = 0;
         for (uint32_t w = warp; w < WW; w += kWarps) {
             uint32_t x = bm[w];
@@ -386,6 +409,7 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
         if (lane == 0 && rows_local) atomicAdd(&sh.rows32, uint32_t(rows_local));
     }
     __syncthreads();
+    rs2_stamp(trace_on, 5);
     if (tid == 0) {
         if (sh.zeros) {
             atomicAdd(&hs->hist[dev::hist_slot(kHistZeroBucket)], sh.zeros);
@@ -419,3 +443,11 @@ void range_stage2(const IndexView& ix, const float* d_scores, uint32_t rows, con
 
 }  // namespace launch
 }  // namespace plaid
+
+// Debug: enable (out == NULL) or read back the range_stage2 timeline
+// (out[512][8]: per CTA 0 start after the PDL wait, 1 runs located,
+// 2 postings in, 3 compacted, 4 kept grouped, 5 scored, 6 launch-resident).
+extern "C" int plaid_debug_rs2_trace(int enable, unsigned long long* out) {
+    if (!out) return int(cudaMemcpyToSymbol(plaid::g_rs2_on, &enable, sizeof(int)));
+    return int(cudaMemcpyFromSymbol(out, plaid::g_rs2_t, sizeof(plaid::g_rs2_t)));
+}
