@@ -77,6 +77,7 @@ enum : int {
     kTmpN = 8,      // scratch count
     kEntryN = 9,    // entry-point input count
     kT4 = 13,       // stage-4 stream tokens (trace.decompressed_tokens)
+    kUsedN = 14,    // range_stage2: keys of candidates owning a kept token (ukeys_)
     kKeptN = 10,    // stage 2: kept centroids, their postings, queued owners (3 slots)
     kGthr = 16,     // 32 u32 per-token top-nprobe bounds (tensor S_cq kernel)
     kNumCounters = 32
@@ -438,6 +439,7 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         PLAID_CUDA(cudaMemset(sel_hist_.p, 0, sizeof(SelectHist)));  // re-zeroed by every select after
         kept_list_.ensure(ix.K);
         keys2_.ensure(ix.N);
+        ukeys_.ensure(ix.N);
         keys4_.ensure(ix.N);
         const uint64_t K = ix.K;
         PLAID_CUDA(cudaMemcpy(kconst_.p, &K, sizeof K, cudaMemcpyHostToDevice));
@@ -616,9 +618,11 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
         record(2, st, times);
         launch::range_stage2(ix, scores_.p, rows, sel_.p, rows * uint32_t(p.nprobe), keep_.p, kept_list_.p,
                              reinterpret_cast<unsigned long long*>(c + kKeptN), keys2_.p, c + kN1,
-                             reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, st);
+                             reinterpret_cast<unsigned long long*>(c + kRows2), sel_hist_.p, ukeys_.p, c + kUsedN,
+                             st);
         record(3, st, times);
-        launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st);
+        launch::select_top_hist(keys2_.p, c + kN1, N, p.ndocs, sel_hist_.p, bkeys_.p, sel2_.p, c + kN2, st,
+                                ukeys_.p, c + kUsedN);
         record(4, st, times);
         return;
     } else if (p.nprobe <= 32) {

@@ -233,7 +233,7 @@ private:
     uint32_t* h_res_ = nullptr;
     launch::RankScratch rank_scratch_;
     bool scan_fused_ = false;  // stage 3's select ran stage 4's finalist scan
-    DevBuf<uint64_t> partial_, tok_keys_, keys2_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_, bkeys_,
+    DevBuf<uint64_t> partial_, tok_keys_, keys2_, ukeys_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_, bkeys_,
         tmp_keys_, kconst_;
     // zero_ = [16 u64 counters | candidate bitmap (N bits) | kept-owner bitmap
     // (N bits)], cleared by a single memset per query.

@@ -215,10 +215,12 @@ void stage2_masked(const IndexView& ix, const float* d_scores, uint32_t rows, co
 // d_keys[0..*d_n1) (order unspecified), the select histogram, the
 // stage1_candidates / stage2_rows_gathered counters.  Needs ix.range_tab.
 bool range_stage2_ok(const IndexView& ix, uint32_t rows, uint64_t nsel);
+// d_ukeys / d_nu (optional, *d_nu zero on entry): the keys of the candidates
+// owning a kept token again, compact — every positive stage-2 key is there.
 void range_stage2(const IndexView& ix, const float* d_scores, uint32_t rows, const uint32_t* d_sel, uint32_t nsel,
                   const uint32_t* d_keep_bits, const uint32_t* d_kept, const unsigned long long* d_kept_counts,
                   uint64_t* d_keys, uint64_t* d_n1, unsigned long long* d_rows, SelectHist* d_hist,
-                  cudaStream_t st);
+                  uint64_t* d_ukeys, uint64_t* d_nu, cudaStream_t st);
 
 // ---- selection -----------------------------------------------------------------------
 // Top `want` of keys[0..*d_n) (largest first).  Result: d_out_keys unsorted
@@ -231,9 +233,12 @@ void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax
 // ci_all): one-CTA bucket search, compaction (keys above the boundary bucket
 // -> out, bucket keys -> d_bkeys, capacity nmax; histogram re-zeroed), exact
 // resolution of the bucket by rank (<= 8192 keys) or a one-CTA radix pass
-// (larger).  *d_out_n must be zero on entry.
+// (larger).  *d_out_n must be zero on entry.  d_ukeys / d_nu (optional): the
+// keys with a positive-capable score (stage 2: candidates owning a kept
+// token), scanned instead of all keys when the boundary lies above score 0.
 void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, SelectHist* d_st,
-                     uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st);
+                     uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st,
+                     const uint64_t* d_ukeys = nullptr, const uint64_t* d_nu = nullptr);
 // Sort keys[0..*d_n) descending (n <= nmax) and emit the first min(want, n):
 // out_keys (optional), out_ids/out_scores (optional, ids offset by id_base),
 // out_n (optional).  nmax <= kSmallSortMax uses one CTA; larger uses a

@@ -159,7 +159,7 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
                     uint32_t nsel, const uint32_t* __restrict__ keep, const uint32_t* __restrict__ kept,
                     const unsigned long long* __restrict__ kept_counts, uint64_t* __restrict__ keys_out,
                     unsigned long long* __restrict__ d_n1, unsigned long long* __restrict__ d_rows,
-                    SelectHist* __restrict__ hs) {
+                    SelectHist* __restrict__ hs, uint64_t* __restrict__ ukeys, unsigned long long* __restrict__ d_nu) {
     const bool trace_on = g_rs2_on != 0;  // one load, in flight with the PDL wait
     rs2_stamp(trace_on, 6);  // CTA start (before the PDL wait)
     dev::pdl_wait();
@@ -355,6 +355,11 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
         constexpr uint32_t kBatch = 8;
         for (uint32_t u0 = warp * kBatch; u0 < nu; u0 += kWarps * kBatch) {
             const uint32_t ub = nu - u0 < kBatch ? nu - u0 : kBatch;
+            // the batch's slots in the list of keys with a kept token (read by
+            // the stage-2 select when its boundary lies above score 0); the
+            // atomic's latency overlaps the scoring below
+            unsigned long long ubase = 0;
+            if (ukeys && lane == 0) ubase = atomicAdd(d_nu, (unsigned long long)ub);
             for (uint32_t i = 0; i < ub; ++i) {
                 const uint32_t m = ulist[u0 + i];
                 uint64_t x = (uint64_t(mmask[2 * m + 1]) << 32) | mmask[2 * m];
@@ -386,6 +391,8 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
                 key = dev::make_key(t, base_pid + mpid[m]);
                 keys[m] = key;
             }
+            ubase = __shfl_sync(0xffffffffu, ubase, 0);
+            if (ukeys && live) ukeys[ubase + lane] = key;
             hist_key(hs, key, live, sh);
             __syncwarp();
         }
@@ -401,7 +408,10 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
                 const float t = score_masked(ix.codes, __ldg(ix.offsets + pid), __ldg(ix.doclens + pid), S, rows,
                                              keep, &used);
                 const uint64_t key = dev::make_key(t, pid);
-                if (lane == 0) keys[wpre[w] + __popc(bm[w] & ((1u << b) - 1u))] = key;
+                if (lane == 0) {
+                    keys[wpre[w] + __popc(bm[w] & ((1u << b) - 1u))] = key;
+                    if (ukeys) ukeys[atomicAdd(d_nu, 1ull)] = key;  // a superset of the positive keys
+                }
                 hist_key(hs, key, lane == 0, sh);
                 rows_local += used;
             }
@@ -431,13 +441,13 @@ bool range_stage2_ok(const IndexView& ix, uint32_t rows, uint64_t nsel) {
 void range_stage2(const IndexView& ix, const float* d_scores, uint32_t rows, const uint32_t* d_sel, uint32_t nsel,
                   const uint32_t* d_keep_bits, const uint32_t* d_kept, const unsigned long long* d_kept_counts,
                   uint64_t* d_keys, uint64_t* d_n1, unsigned long long* d_rows, SelectHist* d_hist,
-                  cudaStream_t st) {
+                  uint64_t* d_ukeys, uint64_t* d_nu, cudaStream_t st) {
     static PerDeviceOnce configured;
     if (configured.first())
         cudaFuncSetAttribute(range_stage2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     ::plaid::launch::pdl(range_stage2_kernel, ix.range_n, kThreads, kSmemBytes, st, ix, d_scores, rows, d_sel, nsel,
                          d_keep_bits, d_kept, d_kept_counts, d_keys, reinterpret_cast<unsigned long long*>(d_n1),
-                         d_rows, d_hist);
+                         d_rows, d_hist, d_ukeys, reinterpret_cast<unsigned long long*>(d_nu));
     count_launch();
 }
 

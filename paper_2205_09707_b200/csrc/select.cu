@@ -547,13 +547,21 @@ __device__ __forceinline__ void hist_boundary(const SelectHist* __restrict__ st,
 __global__ void __launch_bounds__(256) hist_compact_kernel(const uint64_t* __restrict__ keys,
                                                            const uint64_t* __restrict__ d_n, uint64_t want,
                                                            SelectHist* __restrict__ st, uint64_t* __restrict__ bkeys,
-                                                           uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
+                                                           uint64_t* __restrict__ out, uint64_t* __restrict__ out_n,
+                                                           const uint64_t* __restrict__ ukeys,
+                                                           const uint64_t* __restrict__ d_nu) {
     dev::pdl_wait();
-    const uint64_t n = *d_n;
+    const uint64_t n_all = *d_n;
     __shared__ HistBoundary hb;
-    hist_boundary(st, n, want, hb);
+    hist_boundary(st, n_all, want, hb);
     const bool all = hb.take_all;
     const uint32_t bucket = hb.bucket;
+    // a boundary above the score-0 bucket selects positive scores only, and
+    // every positive stage-2 score belongs to a candidate with a kept token:
+    // scan that (much shorter) list when the producer kept one
+    const bool use_u = ukeys && !all && bucket > kHistZeroBucket;
+    if (use_u) keys = ukeys;
+    const uint64_t n = use_u ? *d_nu : n_all;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->take_all = hb.take_all;
         st->bucket = hb.bucket;
@@ -921,11 +929,12 @@ select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
 namespace launch {
 
 void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, SelectHist* d_st,
-                     uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st) {
+                     uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st,
+                     const uint64_t* d_ukeys, const uint64_t* d_nu) {
     if (nmax == 0) return;
     const uint32_t grid = grid_for(nmax, 256, uint32_t(sm_count()) * 8);
     ::plaid::launch::pdl(hist_compact_kernel, grid, 256, 0, st, d_keys, d_n, want, d_st, d_bkeys, d_out_keys,
-                         d_out_n);
+                         d_out_n, d_ukeys, d_nu);
     count_launch();
     static launch::PerDeviceOnce cfg;
     if (cfg.first()) {
