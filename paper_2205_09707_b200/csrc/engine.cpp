@@ -224,11 +224,14 @@ template struct DevBuf<int>;
 
 // ---------------------------------------------------------------- DeviceIndex
 void DeviceIndex::build_range_table(cudaStream_t st) {
-    // per (centroid, pid range of launch::kWaveRangeIds ids): where the list's
-    // run in the range starts — index-side, once (binary searches on the GPU)
+    // per (centroid, pid range): where the list's run in the range starts —
+    // index-side, once (binary searches on the GPU).  Ranges of about N / SMs
+    // ids: range_stage2 runs one CTA per range, one wave
     const uint64_t N = view_.N, K = view_.K;
     if (!N || !K || N > 0xFFFFFFFFull) return;
-    const uint32_t W = launch::kWaveRangeIds, R = uint32_t((N + W - 1) / W);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
+    const uint32_t W = launch::range_width_for(N, uint32_t(sms)), R = uint32_t((N + W - 1) / W);
     uint32_t* tab = upload<uint32_t>(nullptr, K * (uint64_t(R) + 1));
     launch::wave_range_table(view_, W, R, tab, st);
     PLAID_CUDA(cudaStreamSynchronize(st));
@@ -1380,7 +1383,7 @@ WavePipeline::~WavePipeline() {
 
 bool WavePipeline::supports(const plaid_params& p, uint64_t rows, uint64_t dim) const {
     const IndexView& ix = index_->view();
-    return ix.dim == 128 && dim == 128 && rows >= 1 && rows <= 32 && ix.tok_inv && ix.range_tab && !p.disable_filter &&
+    return ix.dim == 128 && dim == 128 && rows >= 1 && rows <= 32 && ix.tok_inv && !p.disable_filter &&
            p.nprobe >= 1 && p.nprobe <= 8 && p.nprobe <= ix.K && ix.N < (1ull << 31) &&
            std::min<uint64_t>(stage3_width(p), ix.N) <= launch::kWaveSortCap && p.ndocs <= (1ull << 24) &&
            index_->candidate_bound(p.nprobe) < (1ull << 31);
@@ -1413,6 +1416,16 @@ void WavePipeline::ensure(uint64_t nq, const plaid_params& p) {
     }();
     uint64_t want = std::min<uint64_t>(std::max<uint64_t>(nq, 1), std::min<uint64_t>(resident, 1024));
     if (tensor_) want = (want + 3) / 4 * 4;
+    if (ix.range_w == launch::kWaveRangeIds) {
+        range_tab_p_ = ix.range_tab;  // the index's own table has the worker's range width
+    } else if (!range_tab_.p) {
+        const uint32_t W = launch::kWaveRangeIds, R = uint32_t((N + W - 1) / W);
+        range_tab_.ensure(K * (uint64_t(R) + 1));
+        launch::wave_range_table(ix, W, R, range_tab_.p, 0);
+        PLAID_CUDA(cudaDeviceSynchronize());
+        PLAID_CUDA(cudaGetLastError());
+        range_tab_p_ = range_tab_.p;
+    }
     const bool fits = slots_ >= want && c1cap_ >= c1cap && sel_stride_ >= sel_stride && nd_cap_ >= nd;
     if (fits) return;
     // grow: release first so the free-memory estimate sees the old buffers
@@ -1477,7 +1490,8 @@ void WavePipeline::run(const float* d_q, uint64_t nq, uint32_t rows, const plaid
         a.k = uint32_t(p.k), a.nlists = lists, a.pid_base = uint32_t(index_->pid_base()), a.validate = validate ? 1 : 0;
         a.S = S_.p, a.s_stride = s_stride_, a.keep = keep_.p, a.keep_stride = keep_stride_;
         a.partial = partial_.p, a.partial_stride = partial_stride_;
-        a.range_tab = ix.range_tab, a.range_w = ix.range_w, a.range_n = ix.range_n;
+        a.range_tab = range_tab_p_, a.range_w = launch::kWaveRangeIds;
+        a.range_n = uint32_t((ix.N + launch::kWaveRangeIds - 1) / launch::kWaveRangeIds);
         a.c1 = c1_.p, a.acc = acc_.p, a.keys = keys_.p, a.side = side_.p, a.c1cap = c1cap_;
         a.sel = sel_.p, a.sel_stride = sel_stride_;
         a.out_pids = d_pids + j0 * p.k, a.out_scores = d_scores + j0 * p.k, a.out_n = d_n + j0;

@@ -300,7 +300,8 @@ private:
     uint64_t c1cap_ = 0, sel_stride_ = 0, partial_stride_ = 0, keep_stride_ = 0, nd_cap_ = 0, s_stride_ = 0;
     uint64_t last_launches_ = 0;
     DevBuf<float> S_, rowmax_;
-    DevBuf<uint32_t> keep_, c1_, acc_;
+    DevBuf<uint32_t> keep_, c1_, acc_, range_tab_;  // range_tab_: 64K-id table when the index's differs
+    const uint32_t* range_tab_p_ = nullptr;
     DevBuf<uint64_t> partial_, keys_, side_, sel_, counters_, trace_;
     DevBuf<int> status_;
     bool tracing_ = false;

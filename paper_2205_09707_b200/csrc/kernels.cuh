@@ -328,6 +328,14 @@ uint32_t wave_scores(const void* cmap, const IndexView& ix, const float* d_q, ui
                      uint64_t* d_partial, uint64_t partial_stride, cudaStream_t st);
 constexpr uint32_t kWaveSortCap = 2048;     // max finalists (stage3_width) of the wave worker
 constexpr uint32_t kWaveRangeIds = 65536;   // pid range of the worker's shared-memory member bitmap
+constexpr uint32_t kRangeIdsMax = 131072;   // widest pid range of range_stage2 (its member bitmap)
+// range_stage2's pid range width for N passages: about one range per SM
+// (power of two, 1024 .. kRangeIdsMax ids)
+inline uint32_t range_width_for(uint64_t N, uint32_t sms) {
+    uint64_t w = 1024;
+    while (w < kRangeIdsMax && w * sms < N) w <<= 1;
+    return uint32_t(w);
+}
 // Index-side table of the wave worker: for centroid c and pid range r (ids
 // [r W, (r+1) W)), the offset in c's posting list of its first posting >= r W;
 // [K][R + 1] u32 with R = ceil(N / W).

@@ -1,7 +1,7 @@
 // range_stage2.cu — latency path: candidate generation (pipeline.cpp:52-87)
 // and the pruned stage-2 centroid interaction (pipeline.cpp:97-137) in ONE
-// launch, one CTA per pid range [r W, (r + 1) W), W = 64K ids (135 ranges at
-// 8.8M passages: one wave on 148 SMs).
+// launch, one CTA per pid range [r W, (r + 1) W), W ~ N / 148 (a power of two
+// in [1K, 256K] ids: 64K and 135 ranges at 8.8M passages, one wave on 148 SMs).
 //
 // It replaces three kernels of the PDL chain (bitmap compaction, the
 // kept-list accumulation into per-candidate rows, the stage-2 keys) and the
@@ -38,10 +38,11 @@ namespace {
 
 constexpr uint32_t kThreads = 1024;  // one CTA per SM: every warp hides the scoring's latency
 constexpr uint32_t kWarps = kThreads / 32;
-constexpr uint32_t kKeptLists = 64;
+constexpr uint32_t kKeptLists = 256;               // kept lists walked (more: code scan)
+constexpr uint32_t kMaskWords = kKeptLists / 32;  // kept-list mask words per member
 constexpr uint32_t kMaxLists = 256 + kKeptLists;
-constexpr uint32_t kRangeWords = launch::kWaveRangeIds / 32;
-constexpr uint32_t kMCap = 4096;               // members per range
+constexpr uint32_t kRangeWords = launch::kRangeIdsMax / 32;  // member bitmap words (widest range)
+constexpr uint32_t kMCap = 2048;               // members per range (more: code scan)
 constexpr uint32_t kPer = 4;                   // postings per thread per round
 constexpr uint32_t kGCap = kPer * kThreads;    // kept postings per range (one register round)
 constexpr uint32_t kMapCap = 8192;            // u16 flat -> list entries (longer ranges: binary search)
@@ -53,12 +54,13 @@ constexpr uint32_t kOffRBeg = kOffLPref + (kMaxLists + 4) * 4;
 constexpr uint32_t kOffKS = kOffRBeg + kMaxLists * 4;
 constexpr uint32_t kOffBm = kOffKS + kKeptLists * 33 * 4;
 constexpr uint32_t kOffWpre = kOffBm + kRangeWords * 4;
-constexpr uint32_t kOffMPid = kOffWpre + kRangeWords * 2;
-constexpr uint32_t kOffMask = kOffMPid + kMCap * 2;                 // kMCap x 2 u32: kept-list mask per member
-constexpr uint32_t kOffMap = kOffMask + kMCap * 8;                   // kMapCap u16: flat posting -> list
+constexpr uint32_t kOffMPid = kOffWpre + kRangeWords * 4;
+constexpr uint32_t kOffMask = kOffMPid + kMCap * 4;                 // kMCap x kMaskWords u32: kept lists per member
+constexpr uint32_t kOffMap = kOffMask + kMCap * kMaskWords * 4;      // kMapCap u16: flat posting -> list
 constexpr uint32_t kOffUList = kOffMap + kMapCap * 2;                // kMCap u16: members with a kept token
-constexpr uint32_t kOffTile = kOffUList + kMCap * 2;                 // kWarps x 32 x 33 u32
-constexpr uint32_t kSmemBytes = kOffTile + kWarps * 32 * 33 * 4;
+constexpr uint32_t kBatch = 8;                                      // members per warp batch (scoring)
+constexpr uint32_t kOffTile = kOffUList + kMCap * 2;                 // kWarps x kBatch x 33 u32
+constexpr uint32_t kSmemBytes = kOffTile + kWarps * kBatch * 33 * 4;
 static_assert(kRangeWords % kThreads == 0 && kMCap % kThreads == 0 && kThreads >= kMaxLists, "layout");
 static_assert(kSmemBytes + sizeof(uint32_t) * 256 <= 227 * 1024, "shared memory budget");
 
@@ -175,12 +177,12 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
     uint32_t* rbeg = reinterpret_cast<uint32_t*>(smem + kOffRBeg);
     uint32_t* ks = reinterpret_cast<uint32_t*>(smem + kOffKS);
     uint32_t* bm = reinterpret_cast<uint32_t*>(smem + kOffBm);
-    uint16_t* wpre = reinterpret_cast<uint16_t*>(smem + kOffWpre);
-    uint16_t* mpid = reinterpret_cast<uint16_t*>(smem + kOffMPid);
+    uint32_t* wpre = reinterpret_cast<uint32_t*>(smem + kOffWpre);
+    uint32_t* mpid = reinterpret_cast<uint32_t*>(smem + kOffMPid);
     uint32_t* mmask = reinterpret_cast<uint32_t*>(smem + kOffMask);
     uint16_t* map = reinterpret_cast<uint16_t*>(smem + kOffMap);
     uint16_t* ulist = reinterpret_cast<uint16_t*>(smem + kOffUList);
-    uint32_t* tile = reinterpret_cast<uint32_t*>(smem + kOffTile) + warp * 32 * 33;
+    uint32_t* tile = reinterpret_cast<uint32_t*>(smem + kOffTile) + warp * kBatch * 33;
     uint32_t* kept_s = sh.kept_s;
 
     // the probed centroids (topn_postings: merge of the S_cq CTAs' top-nprobe
@@ -206,8 +208,10 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
     __syncthreads();
     for (uint32_t j = warp; j < nk; j += kWarps)
         ks[j * 33 + lane] = dev::ord_f32(__ldg(S + uint64_t(kept_s[j]) * kScoresPitch + lane));
-    for (uint32_t w = tid; w < kRangeWords; w += kThreads) bm[w] = 0u;
-    for (uint32_t m = tid; m < 2 * kMCap; m += kThreads) mmask[m] = 0u;
+    for (uint32_t w = tid; w < WW; w += kThreads) bm[w] = 0u;
+    // mask words in use: one per 32 kept lists, laid out [word][member]
+    const uint32_t nwk = (nk + 31) / 32;
+    for (uint32_t m = tid; m < nwk * kMCap; m += kThreads) mmask[m] = 0u;
     if (tid < 32) sh.blk_s[tid] = 0;
     if (tid == 0) sh.zeros = 0, sh.ucount = 0, sh.rows32 = 0;
     uint32_t tot;
@@ -264,9 +268,9 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
     // (3) compaction: member ranks in id order; the range's key slots
     uint32_t m_r;
     {
-        constexpr uint32_t kPW = kRangeWords / kThreads;
+        constexpr uint32_t kPW = kRangeWords / kThreads;  // words per thread at the widest range
         uint32_t v[kPW], mine = 0;
-        const uint32_t w0 = tid * kPW;
+        const uint32_t w0 = tid * kPW;  // (narrower ranges: the high threads hold nothing)
 #pragma unroll
         for (uint32_t j = 0; j < kPW; ++j) {
             v[j] = w0 + j < WW ? bm[w0 + j] : 0u;
@@ -275,10 +279,10 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
         uint32_t pos = block_excl_scan(mine, sh.warp_tot, &m_r);
 #pragma unroll
         for (uint32_t j = 0; j < kPW; ++j) {
-            if (w0 + j < WW) wpre[w0 + j] = uint16_t(pos);  // <= 32 (W/32 - 1) < 65536
+            if (w0 + j < WW) wpre[w0 + j] = pos;
             uint32_t x = v[j];
             while (x) {
-                if (pos < kMCap) mpid[pos] = uint16_t((w0 + j) * 32 + (__ffs(x) - 1));
+                if (pos < kMCap) mpid[pos] = (w0 + j) * 32 + (__ffs(x) - 1);
                 ++pos;
                 x &= x - 1;
             }
@@ -301,7 +305,7 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
                 const uint32_t wv = bm[o >> 5];
                 if ((wv >> (o & 31)) & 1u) {
                     const uint32_t rk = wpre[o >> 5] + __popc(wv & ((1u << (o & 31)) - 1u));
-                    atomicOr(mmask + 2 * rk + (kl[x] >> 5), 1u << (kl[x] & 31));
+                    atomicOr(mmask + (kl[x] >> 5) * kMCap + rk, 1u << (kl[x] & 31));
                     uint32_t m = km[x];
                     if (m == 255) {  // saturated multiplicity: recount from the codes
                         const uint32_t p = kp[x], c = lcent[nsel + kl[x]];
@@ -327,7 +331,10 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
             bool z = false;
             uint64_t key = 0;
             if (m < m_r) {
-                if (!(mmask[2 * m] | mmask[2 * m + 1])) {
+                uint32_t any = 0;
+#pragma unroll
+                for (uint32_t q = 0; q < nwk; ++q) any |= mmask[q * kMCap + m];
+                if (!any) {
                     z = true;
                     key = dev::make_key(0.0f, base_pid + mpid[m]);
                     keys[m] = key;
@@ -352,7 +359,6 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
         const uint32_t nu = sh.ucount;
         // batches of kBatch members spread over all warps (a 32-member batch
         // left half the warps idle and serialised 32 members per warp)
-        constexpr uint32_t kBatch = 8;
         for (uint32_t u0 = warp * kBatch; u0 < nu; u0 += kWarps * kBatch) {
             const uint32_t ub = nu - u0 < kBatch ? nu - u0 : kBatch;
             // the batch's slots in the list of keys with a kept token (read by
@@ -362,17 +368,19 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
             if (ukeys && lane == 0) ubase = atomicAdd(d_nu, (unsigned long long)ub);
             for (uint32_t i = 0; i < ub; ++i) {
                 const uint32_t m = ulist[u0 + i];
-                uint64_t x = (uint64_t(mmask[2 * m + 1]) << 32) | mmask[2 * m];
                 uint32_t mx = 0;
-                while (x) {
-                    uint32_t l[4];
+                for (uint32_t q = 0; q < nwk; ++q) {
+                    uint32_t x = mmask[q * kMCap + m];
+                    while (x) {
+                        uint32_t l[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        l[u] = x ? uint32_t(__ffsll(x) - 1) : l[0];
-                        x &= x - 1;
+                        for (int u = 0; u < 4; ++u) {
+                            l[u] = x ? q * 32 + uint32_t(__ffs(x) - 1) : l[0];
+                            x &= x - 1;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) mx = max(mx, ks[l[u] * 33 + lane]);
                     }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) mx = max(mx, ks[l[u] * 33 + lane]);
                 }
                 tile[i * 33 + lane] = mx;
             }
