@@ -81,6 +81,18 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 // scheduling overlap the previous kernel's tail; it must not touch memory the
 // previous kernels write before this wait (a no-op without a PDL edge).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// "Last CTA out" ticket: one thread per CTA, after a __syncthreads that
+// follows the CTA's global reads and writes.  acq_rel at gpu scope: releases
+// this CTA's accesses (ordered before it by the barrier) and acquires every
+// earlier ticket holder's, without the sequentially consistent fence
+// (MEMBAR.SC + L1 invalidate) that __threadfence() costs.  True for the last
+// of `n` CTAs.
+__device__ __forceinline__ bool last_ticket(unsigned int* ticket, unsigned int n) {
+    unsigned int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ticket) : "memory");
+    return old == n - 1;
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // *dst += the sum over the block's warps of lane 0's v: one global atomic per

@@ -78,6 +78,7 @@ enum : int {
     kEntryN = 9,    // entry-point input count
     kT4 = 13,       // stage-4 stream tokens (trace.decompressed_tokens)
     kUsedN = 14,    // range_stage2: keys of candidates owning a kept token (ukeys_)
+    kFinTicket = 15,  // finalize_rank: CTAs done reading `run`
     kKeptN = 10,    // stage 2: kept centroids, their postings, queued owners (3 slots)
     kGthr = 16,     // 32 u32 per-token top-nprobe bounds (tensor S_cq kernel)
     kNumCounters = 32
@@ -585,7 +586,9 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     // "scores" phase then brackets the S_cq kernel alone
     // host path: the prologue also copies Q from the pinned staging buffer
     const float* qsrc = host_q_ ? host_q_ : d_q;
-    launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p, zero_.n, res_.p,
+    // the range path reads neither bitmap: only the counters are cleared
+    launch::query_prologue(validate ? d_q : nullptr, rows, ix.dim, status_.p, zero_.p,
+                           range_path(rows, p) ? 0 : zero_.n, res_.p,
                            2 * kNumCounters, st, qsrc, rank_scratch_.qimg ? qimg_.p : nullptr,
                            host_q_ ? const_cast<float*>(d_q) : nullptr);
     record(0, st, times);
@@ -595,6 +598,21 @@ void Searcher::enqueue_front(const float* d_q, uint32_t rows, const plaid_params
     const uint32_t warps = launch_scores(d_q, rows, p.t_cs, npb, st);
     record(1, st, times);
     front_after_scores(rows, p, warps, st, times);
+}
+
+bool Searcher::final_fused_ok(uint32_t rows, const plaid_params& p) const {
+    const IndexView& ix = index_->view();
+    if (p.disable_filter || !rank_scratch_.run || ix.dim != 128 || rows > 32) return false;
+    const uint64_t fin_max = std::min<uint64_t>(stage3_width(p), ix.N);
+    return fin_max >= launch::kFinalRankMin && fin_max <= launch::kSmallSortMax &&
+           launch::rank_stream128_ok(ix, rows, fin_max, rank_scratch_);
+}
+
+bool Searcher::range_path(uint32_t rows, const plaid_params& p) const {
+    static const bool off = getenv("PLAID_NO_RANGE_STAGE2") != nullptr;
+    const IndexView& ix = index_->view();
+    return !off && p.nprobe != ix.K && p.nprobe <= 8 && !p.disable_filter &&
+           launch::range_stage2_ok(ix, rows, uint64_t(rows) * p.nprobe);
 }
 
 // Stage 1 after S_cq (top-nprobe merge, candidate generation) and stage 2.
@@ -611,8 +629,7 @@ void Searcher::front_after_scores(uint32_t rows, const plaid_params& p, uint32_t
     if (p.nprobe == K) {
         launch::iota(sel_.p, K, st);
         nsel = K;
-    } else if (p.nprobe <= 8 && !p.disable_filter && launch::range_stage2_ok(ix, rows, uint64_t(rows) * p.nprobe) &&
-               !getenv("PLAID_NO_RANGE_STAGE2")) {
+    } else if (range_path(rows, p)) {
         // candidates + stage 2 in one launch, a CTA per pid range
         // (range_stage2.cu): topn_postings only merges the top-nprobe lists
         // and builds the kept list; no bitmap, no compaction, no slot map
@@ -712,10 +729,20 @@ void Searcher::enqueue_back(const float* d_q, uint32_t rows, const plaid_params&
         fin_max = std::min<uint64_t>(stage3_width(p), ix.N);
     }
     rank_scratch_.prescanned = scan_fused_ && !p.disable_filter;
+    const uint32_t base = uint32_t(index_->pid_base());
+    // finalize + top-k in one launch (the ticket slot was cleared by this query's prologue)
+    const launch::RankScratch::Final fin{want_final, d_pids, d_scores, d_n, base,
+                                         reinterpret_cast<unsigned int*>(c + kFinTicket)};
+    const bool fused_final = final_fused_ok(rows, p);
+    rank_scratch_.final_out = fused_final ? &fin : nullptr;
     launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, &rank_scratch_, st);
     rank_scratch_.prescanned = scan_fused_ = false;
+    rank_scratch_.final_out = nullptr;
     record(6, st, times);
-    const uint32_t base = uint32_t(index_->pid_base());
+    if (fused_final) {
+        record(7, st, times);
+        return;
+    }
     if (fin_max <= launch::kSmallSortMax) {
         launch::sort_top(keys4_.p, fin_n, fin_max, want_final, nullptr, d_pids, d_scores, d_n, base,
                          sort_tmp_.p, st);

@@ -184,6 +184,10 @@ private:
     void enqueue_front(const float* d_q, uint32_t rows, const plaid_params& p, cudaStream_t st, bool times,
                        bool validate);
     void front_after_scores(uint32_t rows, const plaid_params& p, uint32_t warps, cudaStream_t st, bool times);
+    // candidates + stage 2 through range_stage2 (no bitmaps to clear)
+    bool range_path(uint32_t rows, const plaid_params& p) const;
+    // stage 4 ends in one finalize_rank launch (else finalize_kernel + sort_top)
+    bool final_fused_ok(uint32_t rows, const plaid_params& p) const;
     void enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times, bool fuse_scan);
     void enqueue_back(const float* d_q, uint32_t rows, const plaid_params& p, uint32_t* d_pids, float* d_scores,
                       uint64_t* d_n, cudaStream_t st, bool times);

@@ -60,6 +60,7 @@ struct SelectHist {
     unsigned int bucket;        // boundary bucket (top 16 key bits)
     unsigned int take_all;      // n <= want
     unsigned long long bn;      // boundary keys written to the side buffer
+    unsigned int done;          // CTAs of the select finished (the last one resolves the bucket)
 };
 
 constexpr int kScoresPitch = 32;  // S rows padded to 32 floats (128 B)
@@ -248,6 +249,14 @@ void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64
               uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
               uint32_t id_base, uint64_t* d_tmp, cudaStream_t st);
 uint64_t sort_tmp_capacity(uint64_t nmax);
+// Stage 4's finalize (per-finalist sum of the running maxima `run`) fused with
+// the final top-k rank sort: one launch instead of finalize + sort_top.  For
+// kFinalRankMin <= nmax <= kSmallSortMax.  Leaves `run` zero like
+// finalize_kernel; *d_ticket must be 0 at launch.
+constexpr uint64_t kFinalRankMin = 256;
+void finalize_rank(const uint32_t* d_ids, const uint64_t* d_fkeys, const uint64_t* d_n, uint64_t nmax, uint32_t rows,
+                   uint32_t* d_run, uint64_t want, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
+                   uint32_t id_base, unsigned int* d_ticket, cudaStream_t st);
 // Stage 4's finalist scan outputs (RankScratch pref / fin_base / tokens) and
 // the index arrays it reads.
 struct FinalistScanArgs {
@@ -300,6 +309,17 @@ struct RankScratch {
     const float* tensor_S = nullptr;  // TENSOR mode: this query's S_cq table -> stage4_tensor_kernel
     uint32_t* run_p0 = nullptr;       // TENSOR mode: finalist of every 32nd stream position (scan output)
     const void* qimg = nullptr;       // TENSOR mode: the query's bf16 B-operand image (query_prologue)
+    // set: rank_stream128 ends with finalize_rank into these (top-k ids and
+    // scores) instead of finalize_kernel's keys; `run` must arrive zeroed
+    struct Final {
+        uint64_t want = 0;
+        uint32_t* ids = nullptr;
+        float* scores = nullptr;
+        uint64_t* n = nullptr;
+        uint32_t base = 0;
+        unsigned int* ticket = nullptr;  // zero at launch (a per-query counter)
+    };
+    const Final* final_out = nullptr;
 };
 // Bytes of the stage-4 tensor kernel's B-operand image of a query (built by
 // query_prologue when given a destination).

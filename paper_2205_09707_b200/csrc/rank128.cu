@@ -935,6 +935,11 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
                              s.fin_base, d_q, rows, s.run, dbg);
         count_launch();
     }
+    if (s.final_out) {  // finalize + top-k sort in one launch
+        const RankScratch::Final& f = *s.final_out;
+        finalize_rank(d_ids, d_keys, d_n, nmax, rows, s.run, f.want, f.ids, f.scores, f.n, f.base, f.ticket, st);
+        return true;
+    }
     const uint32_t nb = uint32_t((nmax + 255) / 256);
     ::plaid::launch::pdl(finalize_kernel, nb, 256, 0, st, d_ids, d_keys, d_n, rows, s.run, d_out_keys);
     count_launch();

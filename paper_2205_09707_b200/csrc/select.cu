@@ -274,6 +274,78 @@ sort_rank_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__
     if (q == 0 && me < n && rank < want) emit(rank, x, out_keys, out_ids, out_scores, id_base);
 }
 
+// Stage 4's last two launches in one (finalize_kernel + sort_rank_kernel):
+// every CTA sums the running maxima of ALL n finalists itself (n x 128 B of
+// `run`, L2-resident after stage 4; the same in-order fp32 adds as
+// finalize_kernel, rank128.cu) into a shared-memory key array, thread per
+// finalist so that every row load of the CTA is in flight at once, then warp
+// w ranks key 32 b + w (lane j counts the keys j, j + 32, ... above it).  The
+// redundant reads (n x 128 B per CTA, one L2 round trip) cost less than the
+// launch boundary they remove.  `run` must be zero again for the next stage
+// 4: the last CTA done reading it (a ticket counter, zero at launch) clears
+// the n rows.
+constexpr uint32_t kFinRankThreads = 1024;
+constexpr uint32_t kFinRankPerCta = kFinRankThreads / 32;
+constexpr uint32_t kFinTileWords = (kFinRankThreads / 32) * 32 * 33;  // one 32 x 33 float tile per warp
+__global__ void __launch_bounds__(kFinRankThreads)
+finalize_rank_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ fkeys,
+                     const uint64_t* __restrict__ d_n, uint32_t rows, uint32_t* __restrict__ run, uint64_t want,
+                     uint32_t* __restrict__ out_ids, float* __restrict__ out_scores, uint64_t* __restrict__ out_n,
+                     uint32_t id_base, unsigned int* __restrict__ ticket) {
+    dev::pdl_wait();
+    extern __shared__ __align__(16) uint64_t sm[];
+    uint64_t* s = sm + kFinTileWords / 2;  // keys after the warps' tiles
+    __shared__ uint32_t s_last;
+    const uint32_t n = uint32_t(*d_n);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && out_n) *out_n = n < want ? n : want;
+    // warp w takes rows [32 r, 32 r + 32) for r = w, w + 32, ...: coalesced
+    // 512-byte loads (4 rows per instruction) into a per-warp 32 x 33 tile,
+    // then lane = row: the in-order sum.  (A thread reading its own 128-byte
+    // row would touch 32 lines per instruction: 8 K L1 wavefronts per CTA.)
+    float* tile = reinterpret_cast<float*>(sm) + (threadIdx.x >> 5) * 32 * 33;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t r0 = (threadIdx.x >> 5) * 32; r0 < n; r0 += kFinRankThreads) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(run + uint64_t(r0) * 32);
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t row = 4 * j + lane / 8;
+            v[j] = r0 + row < n ? __ldcg(r4 + 32 * j + lane) : make_uint4(0, 0, 0, 0);
+        }
+        const uint32_t e = r0 + lane;
+        const uint32_t pid = e < n ? (ids ? __ldcg(ids + e) : dev::key_id(__ldcg(fkeys + e))) : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float* t = tile + (4 * j + lane / 8) * 33 + (lane % 8) * 4;
+            t[0] = dev::unord_f32(v[j].x), t[1] = dev::unord_f32(v[j].y);
+            t[2] = dev::unord_f32(v[j].z), t[3] = dev::unord_f32(v[j].w);
+        }
+        __syncwarp();
+        float total = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (uint32_t(i) < rows) total = __fadd_rn(total, tile[lane * 33 + i]);
+        if (e < n) s[e] = dev::make_key(total, pid);
+        __syncwarp();
+    }
+    __syncthreads();  // this CTA's reads of `run` are complete
+    if (threadIdx.x == 0) s_last = dev::last_ticket(ticket, gridDim.x);
+    __syncthreads();
+    if (s_last) {
+        uint4* r4 = reinterpret_cast<uint4*>(run);
+        for (uint32_t i = threadIdx.x; i < n * 8; i += kFinRankThreads) r4[i] = make_uint4(0, 0, 0, 0);
+    }
+    const uint32_t me = blockIdx.x * kFinRankPerCta + (threadIdx.x >> 5);
+    if (me >= n) return;
+    const uint64_t x = s[me];
+    uint32_t rank = 0;
+#pragma unroll 4
+    for (uint32_t j = lane; j < n; j += 32) rank += s[j] > x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (lane == 0 && rank < want) emit(rank, x, nullptr, out_ids, out_scores, id_base);
+}
+
 __global__ void pad_copy_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
                                 uint64_t npad, uint64_t* __restrict__ tmp) {
     dev::pdl_wait();
@@ -467,13 +539,12 @@ uint64_t next_pow2(uint64_t v) {
 
 // ---- histogram select (no grid barriers) ----------------------------------------------
 constexpr uint32_t kHistBucketShift = kHistShift;
-constexpr uint32_t kRankCap = 8192;  // boundary buckets up to this size are ranked in parallel
 
 // The bucket (from the top) holding the want-th largest key, found by every
 // CTA of the compaction for itself (no separate single-CTA launch): the 32
 // block sums SelectHist::blk (one L2 round trip) give the block, then thread t
 // sums buckets [8 t, 8 t + 8) of that block (one more round trip) and a
-// block-wide suffix scan gives the bucket.  256 threads.
+// block-wide suffix scan gives the bucket (threads 0-255 hold the buckets).
 struct HistBoundary {
     unsigned long long above, bcount, rem;
     uint32_t bucket, take_all;
@@ -507,10 +578,10 @@ __device__ __forceinline__ void hist_boundary(const SelectHist* __restrict__ st,
     }
     __syncthreads();
     const uint32_t B = blk_id;
-    uint32_t v[8], mine = 0;
+    uint32_t v[8], mine = 0;  // threads >= 256 (wider CTAs) hold no buckets
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        v[j] = __ldcg(&st->hist[dev::hist_slot(B * 2048 + 8 * t + j)]);
+        v[j] = t < 256 ? __ldcg(&st->hist[dev::hist_slot(B * 2048 + 8 * t + j)]) : 0u;
         mine += v[j];
     }
     // suffix scan over the 256 threads (thread 255 holds the top buckets)
@@ -520,7 +591,7 @@ __device__ __forceinline__ void hist_boundary(const SelectHist* __restrict__ st,
         const uint32_t y = __shfl_down_sync(0xffffffffu, incl, o);
         if (lane + o < 32) incl += y;
     }
-    if (lane == 0) wsum[warp] = incl;
+    if (lane == 0 && warp < 8) wsum[warp] = incl;
     __syncthreads();
     unsigned long long above = blk_above;
     for (uint32_t w = warp + 1; w < 8; ++w) above += wsum[w];
@@ -541,10 +612,78 @@ __device__ __forceinline__ void hist_boundary(const SelectHist* __restrict__ st,
     __syncthreads();
 }
 
+// The top `rem` keys of the boundary bucket (keys are unique) appended to
+// out, by one CTA of kHistThreads: an MSB-first 8-bit radix select over the
+// low 48 bits (the bucket fixes the top 16), each digit found by a
+// warp-parallel suffix scan of the 256 counts, stopping early once the
+// digit's whole bucket is taken; then every key >= the threshold is written.
+// `src` is shared memory (small buckets, staged) or global memory.
+constexpr uint32_t kHistThreads = 1024;
+constexpr uint32_t kResolveStage = 16384;  // boundary buckets staged in shared memory (dynamic) up to this size
+__device__ void resolve_bucket_cta(const uint64_t* src, uint32_t nb, uint64_t rem, uint32_t bucket,
+                                   uint64_t* __restrict__ out, uint64_t* __restrict__ out_n) {
+    __shared__ uint32_t h[256];
+    __shared__ unsigned long long s_prefix, s_rem;
+    __shared__ uint32_t s_done;
+    const uint32_t t = threadIdx.x, lane = t & 31;
+    if (t == 0) s_prefix = 0, s_rem = rem, s_done = 0;
+    uint64_t mask = 0;
+    for (int shift = 40; shift >= 0; shift -= 8) {
+        if (t < 256) h[t] = 0;
+        __syncthreads();
+        const uint64_t prefix = s_prefix;
+        for (uint32_t i = t; i < nb; i += kHistThreads) {
+            const uint64_t k = src[i] & 0xFFFFFFFFFFFFull;
+            if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (t < 32) {  // lane l: digits 255 - 8 l .. 248 - 8 l, suffix sums from the top
+            uint32_t c[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sum += (c[j] = h[255 - 8 * lane - j]);
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= uint32_t(o)) incl += y;
+            }
+            const uint64_t r = s_rem;
+            uint64_t above = incl - sum;
+            if (above < r && r <= above + sum) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (above < r && r <= above + c[j]) {
+                        s_prefix = prefix | (uint64_t(255 - 8 * lane - j) << shift);
+                        s_rem = r - above;
+                        s_done = c[j] == r - above;  // the digit's whole bucket is taken
+                    }
+                    above += c[j];
+                }
+            }
+        }
+        __syncthreads();
+        mask |= uint64_t(255) << shift;
+        if (s_done) break;
+    }
+    // exactly rem keys of the bucket are >= the threshold
+    const uint64_t thr = (uint64_t(bucket) << kHistBucketShift) | s_prefix;
+    for (uint32_t i0 = 0; i0 < nb; i0 += kHistThreads) {
+        const uint32_t i = i0 + t;
+        const uint64_t k = i < nb ? src[i] : 0ull;
+        const bool take = i < nb && k >= thr;
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        unsigned long long base = 0;
+        if (lane == 0 && bal) base = atomicAdd((unsigned long long*)out_n, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (take) out[base + __popc(bal & ((1u << lane) - 1))] = k;
+    }
+}
+
 // Keys above the boundary bucket go to out, the boundary bucket's keys to
-// bkeys (then hist_resolve).  CTA 0 records the boundary for hist_resolve,
-// which also re-zeroes the histogram for the next select.
-__global__ void __launch_bounds__(256) hist_compact_kernel(const uint64_t* __restrict__ keys,
+// bkeys; the last CTA to finish (a ticket in SelectHist) resolves the bucket
+// (resolve_bucket_cta) and re-zeroes the histogram for the next select — the
+// compaction and the boundary resolution in one launch.
+__global__ void __launch_bounds__(kHistThreads) hist_select_kernel(const uint64_t* __restrict__ keys,
                                                            const uint64_t* __restrict__ d_n, uint64_t want,
                                                            SelectHist* __restrict__ st, uint64_t* __restrict__ bkeys,
                                                            uint64_t* __restrict__ out, uint64_t* __restrict__ out_n,
@@ -562,13 +701,6 @@ __global__ void __launch_bounds__(256) hist_compact_kernel(const uint64_t* __res
     const bool use_u = ukeys && !all && bucket > kHistZeroBucket;
     if (use_u) keys = ukeys;
     const uint64_t n = use_u ? *d_nu : n_all;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        st->take_all = hb.take_all;
-        st->bucket = hb.bucket;
-        st->above = hb.above;
-        st->bcount = hb.bcount;
-        st->rem = hb.rem;
-    }
     const uint32_t lane = threadIdx.x & 31;
     // one atomic per CTA and output (the CTA's warps take consecutive ranges):
     // per-warp atomics on the two counters queue on one L2 slice
@@ -604,78 +736,37 @@ __global__ void __launch_bounds__(256) hist_compact_kernel(const uint64_t* __res
         if (inb) bkeys[cb + wb[warp] + __popc(bb & ((1u << lane) - 1))] = k;
         __syncthreads();  // wa / wb / ca / cb are rewritten by the next round
     }
-}
-
-// Boundary bucket: keys are unique, so the top `rem` are those with fewer
-// than `rem` bucket keys above them.  Up to kRankCap keys: every CTA stages
-// the bucket in shared memory and ranks 32 of them (4 threads per key).
-// Larger buckets (massive score ties, e.g. the all-masked zeros of stage 2):
-// CTA 0 runs an MSB radix select over the bucket's low 48 bits.
-__global__ void __launch_bounds__(128)
-hist_resolve_kernel(SelectHist* __restrict__ st, const uint64_t* __restrict__ bkeys, uint64_t* __restrict__ out,
-                    uint64_t* __restrict__ out_n) {
-    dev::pdl_wait();
-    extern __shared__ __align__(16) uint64_t s[];
-    // the compaction has consumed the histogram: leave it (and the boundary
-    // counter) zero for the next select
-    {
-        uint4* h4 = reinterpret_cast<uint4*>(st->hist);
-        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (65536 + 32) / 4; i += gridDim.x * blockDim.x)
-            h4[i] = make_uint4(0, 0, 0, 0);  // hist and blk are contiguous
-        if (blockIdx.x == 0 && threadIdx.x == 0) st->bn = 0;
-    }
-    if (st->take_all) return;
-    const uint32_t nb = uint32_t(st->bcount);
-    const uint64_t rem = st->rem;
-    const uint32_t t = threadIdx.x;
-    if (nb <= kRankCap) {
-        if (blockIdx.x * 32 >= nb) return;
-        for (uint32_t i = t; i < nb; i += 128) s[i] = __ldcg(bkeys + i);
-        __syncthreads();
-        const uint32_t me = blockIdx.x * 32 + (t >> 2), q = t & 3;
-        const uint64_t x = me < nb ? s[me] : ~0ull;
-        uint32_t rank = 0;
-        for (uint32_t j = q; j < nb; j += 4) rank += s[j] > x;
-        rank += __shfl_xor_sync(0xffffffffu, rank, 1);
-        rank += __shfl_xor_sync(0xffffffffu, rank, 2);
-        if (q == 0 && me < nb && rank < rem) out[atomicAdd((unsigned long long*)out_n, 1ull)] = x;
-        return;
-    }
-    if (blockIdx.x != 0) return;
-    // one-CTA radix over bits 47..0, 8 bits per pass
-    uint32_t* h = reinterpret_cast<uint32_t*>(s);
-    __shared__ unsigned long long s_prefix, s_rem;
-    unsigned long long prefix = 0, mask = 0;
-    if (t == 0) s_rem = rem;
-    for (int shift = 40; shift >= 0; shift -= 8) {
-        for (uint32_t b = t; b < 256; b += 128) h[b] = 0;
-        __syncthreads();
-        for (uint32_t i = t; i < nb; i += 128) {
-            const uint64_t k = __ldcg(bkeys + i) & 0xFFFFFFFFFFFFull;
-            if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & 255], 1u);
+    // ---- the last CTA: boundary bucket, then a clean histogram
+    __shared__ uint32_t s_last;
+    if (threadIdx.x == 0) s_last = dev::last_ticket(&st->done, gridDim.x);
+    __syncthreads();
+    if (!s_last) return;
+    const uint32_t nb = all ? 0u : uint32_t(__ldcg(&st->bn));
+    if (nb) {
+        if (nb <= kResolveStage) {
+            extern __shared__ __align__(16) uint64_t sk[];
+            for (uint32_t i = threadIdx.x; i < nb; i += kHistThreads) sk[i] = __ldcg(bkeys + i);
+            __syncthreads();
+            resolve_bucket_cta(sk, nb, hb.rem, bucket, out, out_n);
+        } else {
+            resolve_bucket_cta(bkeys, nb, hb.rem, bucket, out, out_n);
         }
-        __syncthreads();
-        if (t == 0) {
-            unsigned long long cum = 0, r = s_rem;
-            for (int b = 255; b >= 0; --b) {
-                if (cum + h[b] >= r) {
-                    s_prefix = prefix | (uint64_t(b) << shift);
-                    s_rem = r - cum;
-                    break;
-                }
-                cum += h[b];
-            }
-        }
-        __syncthreads();
-        prefix = s_prefix;
-        mask |= uint64_t(255) << shift;
     }
-    // threshold key (bucket bits + resolved low bits): exactly rem keys >= it
-    const uint64_t thr = (uint64_t(st->bucket) << kHistBucketShift) | prefix;
-    for (uint32_t i = t; i < nb; i += 128) {
-        const uint64_t k = __ldcg(bkeys + i);
-        if (k >= thr) out[atomicAdd((unsigned long long*)out_n, 1ull)] = k;
+    // every CTA read the histogram before taking its ticket: clear the
+    // non-empty blocks (their sums fetched in one round trip), then the sums
+    // and the counters
+    __shared__ uint32_t s_nz;
+    if (threadIdx.x < 32) {
+        const uint32_t nz = __ballot_sync(0xffffffffu, __ldcg(&st->blk[threadIdx.x]) != 0);
+        if (threadIdx.x == 0) s_nz = nz;
+        st->blk[threadIdx.x] = 0;
     }
+    __syncthreads();
+    for (uint32_t nz = s_nz; nz; nz &= nz - 1) {
+        uint4* h4 = reinterpret_cast<uint4*>(st->hist + (__ffs(nz) - 1) * 2048);
+        for (uint32_t i = threadIdx.x; i < 2048 / 4; i += kHistThreads) h4[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (threadIdx.x == 0) st->bn = 0, st->done = 0;
 }
 
 
@@ -932,18 +1023,14 @@ void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax,
                      uint64_t* d_bkeys, uint64_t* d_out_keys, uint64_t* d_out_n, cudaStream_t st,
                      const uint64_t* d_ukeys, const uint64_t* d_nu) {
     if (nmax == 0) return;
-    const uint32_t grid = grid_for(nmax, 256, uint32_t(sm_count()) * 8);
-    ::plaid::launch::pdl(hist_compact_kernel, grid, 256, 0, st, d_keys, d_n, want, d_st, d_bkeys, d_out_keys,
-                         d_out_n, d_ukeys, d_nu);
-    count_launch();
+    // one 1024-thread CTA per SM at most; the last one stages the boundary bucket
+    const uint32_t grid = grid_for(nmax, kHistThreads, uint32_t(sm_count()));
     static launch::PerDeviceOnce cfg;
-    if (cfg.first()) {
-        cudaFuncSetAttribute(hist_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kRankCap * sizeof(uint64_t)));
-    }
-    const uint64_t rb = std::min<uint64_t>((std::min<uint64_t>(nmax, kRankCap) + 31) / 32, kRankCap / 32);
-    ::plaid::launch::pdl(hist_resolve_kernel, uint32_t(rb ? rb : 1), 128, kRankCap * sizeof(uint64_t), st, d_st, d_bkeys, d_out_keys,
-                                                                                       d_out_n);
+    if (cfg.first())
+        cudaFuncSetAttribute(hist_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kResolveStage * sizeof(uint64_t)));
+    ::plaid::launch::pdl(hist_select_kernel, grid, kHistThreads, kResolveStage * sizeof(uint64_t), st, d_keys, d_n, want, d_st, d_bkeys, d_out_keys,
+                         d_out_n, d_ukeys, d_nu);
     count_launch();
 }
 
@@ -967,6 +1054,22 @@ void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax
 }
 
 uint64_t sort_tmp_capacity(uint64_t nmax) { return nmax <= kSmallSortMax ? 0 : next_pow2(nmax); }
+
+void finalize_rank(const uint32_t* d_ids, const uint64_t* d_fkeys, const uint64_t* d_n, uint64_t nmax, uint32_t rows,
+                   uint32_t* d_run, uint64_t want, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
+                   uint32_t id_base, unsigned int* d_ticket, cudaStream_t st) {
+    if (nmax < kFinalRankMin || nmax > kSmallSortMax) fail_cuda_driver(1, "finalize_rank: nmax out of range");
+    // one 32 x 33 float tile per warp, then the nmax keys
+    const size_t smem = kFinTileWords * sizeof(float) + size_t(nmax) * sizeof(uint64_t);
+    static launch::PerDeviceOnce cfg;
+    if (cfg.first())
+        cudaFuncSetAttribute(finalize_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kFinTileWords * sizeof(float) + kSmallSortMax * sizeof(uint64_t)));
+    const uint32_t grid = uint32_t((nmax + kFinRankPerCta - 1) / kFinRankPerCta);
+    ::plaid::launch::pdl(finalize_rank_kernel, grid, kFinRankThreads, smem, st, d_ids, d_fkeys, d_n, rows, d_run, want,
+                         d_out_ids, d_out_scores, d_out_n, id_base, d_ticket);
+    count_launch();
+}
 
 void sort_top(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want,
               uint64_t* d_out_keys, uint32_t* d_out_ids, float* d_out_scores, uint64_t* d_out_n,
@@ -1055,8 +1158,9 @@ void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status
                     uint32_t* d_zero2, uint64_t nwords2, cudaStream_t st, const float* d_qsrc, void* d_qimg,
                     float* d_qcopy) {
     const uint64_t n16 = nwords / 4, m16 = nwords2 / 4;  // both regions are multiples of 16 bytes
-    const uint32_t grid = grid_for(n16 + m16, 256, uint32_t(sm_count()));
     const bool img = d_qimg && d_qsrc && dim == 128 && rows <= 32;
+    // at least one thread per query-image granule (the rows may be in host memory)
+    const uint32_t grid = grid_for(std::max<uint64_t>(n16 + m16, img ? kQImgBytes / 16 : 0), 256, uint32_t(sm_count()));
     static launch::PerDeviceOnce cfg;
     if (cfg.first())  // keep the SMs' shared-memory partition at its maximum so the
                       // S_cq CTAs (213 KB each) can become resident beside this grid
