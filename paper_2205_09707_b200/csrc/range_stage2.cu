@@ -357,15 +357,16 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
         // 125-131).  A thread per member (divergent mask loops) or a grouped
         // list with dependent loads were both latency-bound
         const uint32_t nu = sh.ucount;
+        // the range's slots in the list of keys with a kept token (read by the
+        // stage-2 select when its boundary lies above score 0): one atomic per
+        // CTA — one per warp batch put ~9K atomics on one L2 address
+        if (tid == 0) sh.base = ukeys && nu ? uint32_t(atomicAdd(d_nu, (unsigned long long)nu)) : 0u;
+        __syncthreads();
+        const uint32_t ucta = sh.base;
         // batches of kBatch members spread over all warps (a 32-member batch
         // left half the warps idle and serialised 32 members per warp)
         for (uint32_t u0 = warp * kBatch; u0 < nu; u0 += kWarps * kBatch) {
             const uint32_t ub = nu - u0 < kBatch ? nu - u0 : kBatch;
-            // the batch's slots in the list of keys with a kept token (read by
-            // the stage-2 select when its boundary lies above score 0); the
-            // atomic's latency overlaps the scoring below
-            unsigned long long ubase = 0;
-            if (ukeys && lane == 0) ubase = atomicAdd(d_nu, (unsigned long long)ub);
             for (uint32_t i = 0; i < ub; ++i) {
                 const uint32_t m = ulist[u0 + i];
                 uint32_t mx = 0;
@@ -399,8 +400,7 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
                 key = dev::make_key(t, base_pid + mpid[m]);
                 keys[m] = key;
             }
-            ubase = __shfl_sync(0xffffffffu, ubase, 0);
-            if (ukeys && live) ukeys[ubase + lane] = key;
+            if (ukeys && live) ukeys[ucta + u0 + lane] = key;
             hist_key(hs, key, live, sh);
             __syncwarp();
         }
