@@ -1515,6 +1515,8 @@ void WavePipeline::run(const float* d_q, uint64_t nq, uint32_t rows, const plaid
         a.Q = q;
         a.rows = rows, a.nprobe = uint32_t(p.nprobe), a.ndocs = uint32_t(nd), a.n3 = uint32_t(n3);
         a.k = uint32_t(p.k), a.nlists = lists, a.pid_base = uint32_t(index_->pid_base()), a.validate = validate ? 1 : 0;
+        static const bool s4_exact = getenv("PLAID_WAVE_S4_EXACT") != nullptr;
+        a.s4_tensor = tensor_ && ix.tok_inv && !s4_exact ? 1u : 0u;
         a.S = S_.p, a.s_stride = s_stride_, a.keep = keep_.p, a.keep_stride = keep_stride_;
         a.partial = partial_.p, a.partial_stride = partial_stride_;
         a.range_tab = range_tab_p_, a.range_w = launch::kWaveRangeIds;

@@ -366,6 +366,7 @@ void wave_range_table(const IndexView& ix, uint32_t W, uint32_t R, uint32_t* d_t
 struct WaveArgs {
     const float* Q = nullptr;
     uint32_t rows = 0, nprobe = 0, ndocs = 0, n3 = 0, k = 0, nlists = 0, pid_base = 0, validate = 0;
+    uint32_t s4_tensor = 0;  // stage 4 as (S + R Q^T) * inv on mma.sync (TENSOR mode; else exact)
     const float* S = nullptr;
     uint64_t s_stride = 0;
     const uint32_t* keep = nullptr;

@@ -109,7 +109,9 @@ def test_wave_tensor_comparator(idx_small, ref, k):
         got = dict(zip(("stage1_candidates", "stage2_out", "stage3_out", "final_out"), (int(x) for x in cnt[j])))
         rep = check_tensor_search(ref, h, q, p, res[j].passage_ids, res[j].scores, S, got_counters=got)
         assert rep.ok, (j, rep.problems)
-        assert rep.max_rel_score_err == 0.0 or rep.max_rel_score_err < 1e-6  # stage 4 is exact given S
+        # stage 4 on mma.sync: (S + R Q^T) * inv with a three-way bf16 split of
+        # the residual product (~1e-6 relative observed; north_star allows 1e-4)
+        assert rep.max_rel_score_err < 2e-5
 
 
 def test_wave_tensor_many_tiles_per_cta(port):
