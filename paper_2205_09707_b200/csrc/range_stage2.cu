@@ -58,9 +58,7 @@ constexpr uint32_t kOffMPid = kOffWpre + kRangeWords * 4;
 constexpr uint32_t kOffMask = kOffMPid + kMCap * 4;                 // kMCap x kMaskWords u32: kept lists per member
 constexpr uint32_t kOffMap = kOffMask + kMCap * kMaskWords * 4;      // kMapCap u16: flat posting -> list
 constexpr uint32_t kOffUList = kOffMap + kMapCap * 2;                // kMCap u16: members with a kept token
-constexpr uint32_t kBatch = 8;                                      // members per warp batch (scoring)
-constexpr uint32_t kOffTile = kOffUList + kMCap * 2;                 // kWarps x kBatch x 33 u32
-constexpr uint32_t kSmemBytes = kOffTile + kWarps * kBatch * 33 * 4;
+constexpr uint32_t kSmemBytes = kOffUList + kMCap * 2;
 static_assert(kRangeWords % kThreads == 0 && kMCap % kThreads == 0 && kThreads >= kMaxLists, "layout");
 static_assert(kSmemBytes + sizeof(uint32_t) * 256 <= 227 * 1024, "shared memory budget");
 
@@ -182,7 +180,6 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
     uint32_t* mmask = reinterpret_cast<uint32_t*>(smem + kOffMask);
     uint16_t* map = reinterpret_cast<uint16_t*>(smem + kOffMap);
     uint16_t* ulist = reinterpret_cast<uint16_t*>(smem + kOffUList);
-    uint32_t* tile = reinterpret_cast<uint32_t*>(smem + kOffTile) + warp * kBatch * 33;
     uint32_t* kept_s = sh.kept_s;
 
     // the probed centroids (topn_postings: merge of the S_cq CTAs' top-nprobe
@@ -351,58 +348,45 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
         }
         __syncthreads();
         rs2_stamp(trace_on, 7);
-        // (6) a warp takes 32 listed members: lane = query token, the max over
-        // the member's kept lists (mask bits, four loads in flight) into a
-        // tile row; then lane i sums member i's row in order (pipeline.cpp:
-        // 125-131).  A thread per member (divergent mask loops) or a grouped
-        // list with dependent loads were both latency-bound
+        // (6) lane = listed member: the max over its kept lists' S rows (mask
+        // bits; two halves of 16 query tokens in registers) and the in-order
+        // sum (pipeline.cpp:125-131), all in the lane; the 32 members' row
+        // loads proceed side by side.  (Lane = query token with a warp's
+        // members one after another chained dependent loads per member.)
         const uint32_t nu = sh.ucount;
         // the range's slots in the list of keys with a kept token (read by the
         // stage-2 select when its boundary lies above score 0): one atomic per
-        // CTA — one per warp batch put ~9K atomics on one L2 address
+        // CTA — one per warp put thousands of atomics on one L2 address
         if (tid == 0) sh.base = ukeys && nu ? uint32_t(atomicAdd(d_nu, (unsigned long long)nu)) : 0u;
         __syncthreads();
         const uint32_t ucta = sh.base;
-        // batches of kBatch members spread over all warps (a 32-member batch
-        // left half the warps idle and serialised 32 members per warp)
-        for (uint32_t u0 = warp * kBatch; u0 < nu; u0 += kWarps * kBatch) {
-            const uint32_t ub = nu - u0 < kBatch ? nu - u0 : kBatch;
-            for (uint32_t i = 0; i < ub; ++i) {
-                const uint32_t m = ulist[u0 + i];
-                uint32_t mx = 0;
-                for (uint32_t q = 0; q < nwk; ++q) {
-                    uint32_t x = mmask[q * kMCap + m];
-                    while (x) {
-                        uint32_t l[4];
+        for (uint32_t u0 = warp * 32; u0 < nu; u0 += kWarps * 32) {
+            const bool live = u0 + lane < nu;
+            const uint32_t m = live ? ulist[u0 + lane] : 0u;
+            float t = 0.0f;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            l[u] = x ? q * 32 + uint32_t(__ffs(x) - 1) : l[0];
-                            x &= x - 1;
-                        }
+            for (uint32_t h = 0; h < 2; ++h) {
+                uint32_t mx[16];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) mx = max(mx, ks[l[u] * 33 + lane]);
+                for (int j = 0; j < 16; ++j) mx[j] = 0;
+                for (uint32_t q = 0; live && q < nwk; ++q) {
+                    for (uint32_t x = mmask[q * kMCap + m]; x; x &= x - 1) {
+                        const uint32_t* row = ks + (q * 32 + uint32_t(__ffs(x) - 1)) * 33 + 16 * h;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) mx[j] = max(mx[j], row[j]);
                     }
                 }
-                tile[i * 33 + lane] = mx;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (16 * h + j < rows) t = __fadd_rn(t, dev::unord_f32(mx[j]));
             }
-            __syncwarp();
             uint64_t key = 0;
-            const bool live = lane < ub;
             if (live) {
-                const uint32_t m = ulist[u0 + lane];
-                uint32_t v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = tile[lane * 33 + j];  // all loads in flight
-                float t = 0.0f;
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (uint32_t(j) < rows) t = __fadd_rn(t, dev::unord_f32(v[j]));
                 key = dev::make_key(t, base_pid + mpid[m]);
                 keys[m] = key;
+                if (ukeys) ukeys[ucta + u0 + lane] = key;
             }
-            if (ukeys && live) ukeys[ucta + u0 + lane] = key;
             hist_key(hs, key, live, sh);
-            __syncwarp();
         }
     } else {        // code scan: a warp per member (bitmap order), masked interaction
         unsigned long long rows_local = 0;
