@@ -513,6 +513,7 @@ void Searcher::ensure_param_buffers_impl(const plaid_params& p) {
     }
     sel2_.ensure(nd);
     keys3_.ensure(nd);
+    if (nd <= launch::kSmallSortMax) cand_len_.ensure(nd), cand_off_.ensure(nd);
     sel3_.ensure(n3);
     if (ix.dim == 128 && n3 <= launch::kStreamMaxPassages) {
         pref_.ensure(n3 + 1);
@@ -691,15 +692,19 @@ void Searcher::enqueue_stage3(const plaid_params& p, cudaStream_t st, bool times
     const IndexView& ix = index_->view();
     uint64_t* c = counters_.p;
     const uint64_t nd = std::min<uint64_t>(p.ndocs, ix.N);
-    launch::centroid_interaction(ix, scores_.p, pending_rows_, nullptr, sel2_.p, c + kN2, nd, nullptr, nullptr,
-                                 keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st);
     // stage 4 needs only the top-stage3_width SET (the final select orders it)
-    // unsharded, stage 4's finalist scan runs in the select's own CTA
+    // unsharded, stage 4's finalist scan runs in the select's own CTA, on the
+    // (doclen, offset) pairs the stage-3 scorer carries over
     const uint64_t fin_max = std::min<uint64_t>(stage3_width(p), ix.N);
     scan_fused_ = fuse_scan && nd <= launch::kSmallSortMax && rank_scratch_.pref &&
                   launch::rank_stream128_ok(ix, pending_rows_, fin_max, rank_scratch_);
+    const bool carry = scan_fused_ && cand_len_.n >= nd && cand_off_.n >= nd;
+    launch::centroid_interaction(ix, scores_.p, pending_rows_, nullptr, sel2_.p, c + kN2, nd, nullptr, nullptr,
+                                 keys3_.p, nullptr, reinterpret_cast<unsigned long long*>(c + kRows3), st,
+                                 carry ? cand_len_.p : nullptr, carry ? cand_off_.p : nullptr);
     launch::FinalistScanArgs fs{ix.doclens, ix.offsets, rank_scratch_.pref, rank_scratch_.fin_base,
-                                rank_scratch_.tokens, rank_scratch_.run_p0};
+                                rank_scratch_.tokens, rank_scratch_.run_p0,
+                                carry ? cand_len_.p : nullptr, carry ? cand_off_.p : nullptr};
     if (nd <= launch::kSmallSortMax)
         launch::select_set(keys3_.p, c + kN2, nd, stage3_width(p), sel3_.p, c + kN3, scan_fused_ ? &fs : nullptr, st);
     else

@@ -239,6 +239,8 @@ private:
     bool scan_fused_ = false;  // stage 3's select ran stage 4's finalist scan
     DevBuf<uint64_t> partial_, tok_keys_, keys2_, ukeys_, sel2_, keys3_, sel3_, keys4_, sel4_, sort_tmp_, fin_base_, bkeys_,
         tmp_keys_, kconst_;
+    DevBuf<uint32_t> cand_len_;  // stage-3 candidates' doclens, carried to the finalist scan
+    DevBuf<uint64_t> cand_off_;  // ... and their token offsets
     // zero_ = [16 u64 counters | candidate bitmap (N bits) | kept-owner bitmap
     // (N bits)], cleared by a single memset per query.
     DevBuf<uint32_t> zero_;

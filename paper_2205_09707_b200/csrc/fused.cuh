@@ -102,5 +102,51 @@ __device__ __forceinline__ void finalist_scan(const uint32_t* __restrict__ ids, 
     }
 }
 
+// finalist_scan with each finalist's (doclen, offset) already in shared
+// memory: finalist p is select input idx[p], whose doclen / offset are
+// len[idx[p]] / off[idx[p]] (carried from the stage-3 scorer).
+__device__ __forceinline__ void finalist_scan_carried(uint32_t n, const uint32_t* idx, const uint32_t* len,
+                                                      const uint64_t* off, uint32_t* __restrict__ pref,
+                                                      uint64_t* __restrict__ fin_base, uint64_t* __restrict__ tokens,
+                                                      uint32_t* __restrict__ run_p0) {
+    __shared__ uint32_t warp_sums[32];
+    const uint32_t per = (n + 1023) / 1024;
+    const uint32_t b = threadIdx.x * per, e = b + per < n ? b + per : n;
+    uint32_t local = 0;
+    for (uint32_t p = b; p < e; ++p) local += len[idx[p]];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += y;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = warp_sums[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= uint32_t(o)) wi += y;
+        }
+        warp_sums[lane] = wi - w;  // exclusive
+    }
+    __syncthreads();
+    uint32_t run = warp_sums[warp] + incl - local;
+    for (uint32_t p = b; p < e; ++p) {
+        const uint32_t i = idx[p], l = len[i];
+        pref[p] = run;
+        fin_base[p] = off[i] - run;  // index token = fin_base[p] + stream position
+        if (run_p0)
+            for (uint32_t r = (run + 31) / 32; 32 * r < run + l; ++r) run_p0[r] = p;
+        run += l;
+    }
+    if (threadIdx.x == 1023) {
+        pref[n] = warp_sums[31] + incl;  // total (last thread's inclusive)
+        if (tokens) *tokens = pref[n];
+    }
+}
+
 }  // namespace fused
 }  // namespace plaid

@@ -88,7 +88,8 @@ ci_warp_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ 
                const uint32_t* __restrict__ ids, const uint64_t* __restrict__ keys,
                const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ keep_bits,
                uint64_t* __restrict__ out_keys, float* __restrict__ out_scores,
-               unsigned long long* __restrict__ d_rows) {
+               unsigned long long* __restrict__ d_rows, uint32_t* __restrict__ out_len,
+               uint64_t* __restrict__ out_off) {
     dev::pdl_wait();
     const uint64_t n = *d_n;
     const uint32_t lane = dev::lane_id();
@@ -104,6 +105,7 @@ ci_warp_kernel(const uint32_t* __restrict__ codes, const uint64_t* __restrict__ 
         if (lane == 0) {
             out_keys[i] = dev::make_key(total, pid);
             if (out_scores) out_scores[i] = total;
+            if (out_len) out_len[i] = len, out_off[i] = off;
         }
         rows_local += used;
     }
@@ -521,8 +523,9 @@ void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t r
                           const uint32_t* d_ids, const uint64_t* d_keys, const uint64_t* d_n,
                           uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_owners,
                           uint64_t* d_out_keys, float* d_out_scores, unsigned long long* d_rows,
-                          cudaStream_t st) {
+                          cudaStream_t st, uint32_t* d_out_len, uint64_t* d_out_off) {
     if (nmax == 0) return;
+    if (d_keep_bits && d_out_len) fail_cuda_driver(1, "centroid_interaction: (len, off) outputs are unmasked-only");
     if (d_keep_bits) {
         uint64_t blocks = (nmax + kCB - 1) / kCB;
         const uint64_t cap = uint64_t(sm_count()) * 4;
@@ -536,7 +539,7 @@ void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t r
         if (blocks > cap) blocks = cap;
         ::plaid::launch::pdl(ci_warp_kernel, uint32_t(blocks), 256, 0, st, ix.codes, ix.offsets, ix.doclens, d_scores,
                                                         rows, d_ids, d_keys, d_n, d_keep_bits,
-                                                        d_out_keys, d_out_scores, d_rows);
+                                                        d_out_keys, d_out_scores, d_rows, d_out_len, d_out_off);
     }
     count_launch();
 }

@@ -196,7 +196,7 @@ void centroid_interaction(const IndexView& ix, const float* d_scores, uint32_t r
                           const uint32_t* d_ids, const uint64_t* d_keys, const uint64_t* d_n,
                           uint64_t nmax, const uint32_t* d_keep_bits, const uint32_t* d_owners,
                           uint64_t* d_out_keys, float* d_out_scores, unsigned long long* d_rows,
-                          cudaStream_t st);
+                          cudaStream_t st, uint32_t* d_out_len = nullptr, uint64_t* d_out_off = nullptr);
 // owners |= postings(c) for every kept centroid c (owners zeroed by the caller).
 void kept_owners(const IndexView& ix, const uint32_t* d_keep_bits, uint32_t* d_owners, cudaStream_t st);
 // Stage 2 over C1 (ids d_c1 ascending, count *d_n1 <= nmax, membership
@@ -266,6 +266,11 @@ struct FinalistScanArgs {
     uint64_t* fin_base = nullptr;
     uint64_t* tokens = nullptr;
     uint32_t* run_p0 = nullptr;  // finalist of every 32nd stream position (TENSOR stage 4)
+    // optional: (doclen, offset) of every select input (centroid_interaction's
+    // out_len / out_off), so the scan reads them from shared memory instead of
+    // two dependent L2 round trips per finalist
+    const uint32_t* cand_len = nullptr;
+    const uint64_t* cand_off = nullptr;
 };
 // The top-`want` SET of keys[0..*d_n) (unordered), nmax <= kSmallSortMax, one
 // CTA (shared-memory radix select); *d_out_n = min(n, want).  With `fs`, the

@@ -938,25 +938,37 @@ threshold_filter_kernel(const uint64_t* __restrict__ g, uint64_t total, uint64_t
 constexpr uint32_t kSelCtaThreads = 1024;
 __global__ void __launch_bounds__(kSelCtaThreads)
 select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n, uint64_t want,
-                      uint64_t* out, uint64_t* __restrict__ d_out_n, launch::FinalistScanArgs fs) {
+                      uint64_t* out, uint64_t* __restrict__ d_out_n, launch::FinalistScanArgs fs, uint32_t nmax) {
     dev::pdl_wait();
+    // [keys | (with fs.cand_len) offsets, doclens, input index of each output]
     extern __shared__ uint64_t sk[];
+    uint64_t* co = sk + nmax;
+    uint32_t* cl = reinterpret_cast<uint32_t*>(co + nmax);
+    uint32_t* sidx = cl + nmax;
+    const bool carry = fs.pref && fs.cand_len;
     __shared__ uint32_t hist[256];
     __shared__ uint64_t s_prefix, s_rem, s_mask;
     __shared__ uint32_t s_done, s_cnt;
     const uint32_t t = threadIdx.x;
     const uint32_t n = uint32_t(*d_n);
-    for (uint32_t i = t; i < n; i += kSelCtaThreads) sk[i] = __ldcg(keys + i);
+    for (uint32_t i = t; i < n; i += kSelCtaThreads) {
+        sk[i] = __ldcg(keys + i);
+        if (carry) co[i] = __ldcg(fs.cand_off + i), cl[i] = __ldcg(fs.cand_len + i);
+    }
     if (t == 0) {
         s_prefix = 0, s_rem = want, s_mask = 0, s_done = n <= want, s_cnt = 0;
     }
     __syncthreads();
     if (s_done) {  // everything survives
-        for (uint32_t i = t; i < n; i += kSelCtaThreads) out[i] = sk[i];
+        for (uint32_t i = t; i < n; i += kSelCtaThreads) {
+            out[i] = sk[i];
+            if (carry) sidx[i] = i;
+        }
         if (t == 0) *d_out_n = n;
         if (fs.pref) {
             __syncthreads();
-            fused::finalist_scan(nullptr, out, n, fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens, fs.run_p0);
+            if (carry) fused::finalist_scan_carried(n, sidx, cl, co, fs.pref, fs.fin_base, fs.tokens, fs.run_p0);
+            else fused::finalist_scan(nullptr, out, n, fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens, fs.run_p0);
         }
         return;
     }
@@ -1006,12 +1018,20 @@ select_set_cta_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restr
         uint32_t base = 0;
         if ((t & 31) == 0 && bal) base = atomicAdd(&s_cnt, uint32_t(__popc(bal)));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (ok) out[base + __popc(bal & ((1u << (t & 31)) - 1u))] = sk[i];
+        if (ok) {
+            const uint32_t pos = base + __popc(bal & ((1u << (t & 31)) - 1u));
+            out[pos] = sk[i];
+            if (carry) sidx[pos] = i;
+        }
     }
     if (t == 0) *d_out_n = want;
     if (fs.pref) {  // stage 4's finalist scan over the set just written, same CTA
         __syncthreads();
-        fused::finalist_scan(nullptr, out, uint32_t(want), fs.doclens, fs.offsets, fs.pref, fs.fin_base, fs.tokens, fs.run_p0);
+        if (carry)
+            fused::finalist_scan_carried(uint32_t(want), sidx, cl, co, fs.pref, fs.fin_base, fs.tokens, fs.run_p0);
+        else
+            fused::finalist_scan(nullptr, out, uint32_t(want), fs.doclens, fs.offsets, fs.pref, fs.fin_base,
+                                 fs.tokens, fs.run_p0);
     }
 }
 
@@ -1218,14 +1238,17 @@ void threshold_filter(const uint64_t* d_gathered, uint64_t total, uint64_t want,
 
 void select_set(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, uint64_t* d_out_keys,
                 uint64_t* d_out_n, const FinalistScanArgs* fs, cudaStream_t st) {
-    const size_t smem = std::max<uint64_t>(nmax, 1) * sizeof(uint64_t);
+    const uint64_t nm = std::max<uint64_t>(nmax, 1);
+    // keys, then (carried scan inputs) offsets, doclens and the output -> input map
+    const bool carry = fs && fs->pref && fs->cand_len;
+    const size_t smem = nm * (carry ? 24 : 8);
     static launch::PerDeviceOnce cfg;
     if (cfg.first()) {
         cudaFuncSetAttribute(select_set_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kSmallSortMax * sizeof(uint64_t)));
+                             int(kSmallSortMax * 24));
     }
     ::plaid::launch::pdl(select_set_cta_kernel, 1, kSelCtaThreads, smem, st, d_keys, d_n, want, d_out_keys, d_out_n,
-                         fs ? *fs : FinalistScanArgs{});
+                         fs ? *fs : FinalistScanArgs{}, uint32_t(nm));
     count_launch();
 }
 
