@@ -669,7 +669,8 @@ class BatchSearcher:
         p = params._c(options.disable_filter)
         _check(N.load().plaid_batch_search(self._h, N.ptr(q, C.c_float), nq, rows, dim, C.byref(p),
                                            N.ptr(ids, C.c_uint32), N.ptr(sc, C.c_float), N.ptr(n, C.c_uint64)))
-        return [CandidateSet(ids[j, : n[j]].copy(), sc[j, : n[j]].copy()) for j in range(nq)]
+        # views into this call's fresh arrays (no per-query copies)
+        return [CandidateSet(ids[j, :m], sc[j, :m]) for j, m in enumerate(n.tolist())]
 
     def search_device(self, d_q: int, nq: int, rows: int, dim: int, params: SearchParams, d_pids: int,
                       d_scores: int, d_n: int, stream: int = 0, options: SearchOptions = SearchOptions()) -> None:
