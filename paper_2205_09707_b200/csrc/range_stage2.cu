@@ -382,7 +382,8 @@ range_stage2_kernel(const IndexView ix, const float* __restrict__ S, uint32_t ro
             }
             uint64_t key = 0;
             if (live) {
-                key = dev::make_key(t, base_pid + mpid[m]);
+                const uint32_t pid = base_pid + mpid[m];
+                key = dev::make_key(t, pid);
                 keys[m] = key;
                 if (ukeys) ukeys[ucta + u0 + lane] = key;
             }

@@ -329,21 +329,27 @@ finalize_rank_kernel(const uint32_t* __restrict__ ids, const uint64_t* __restric
         __syncwarp();
     }
     __syncthreads();  // this CTA's reads of `run` are complete
-    if (threadIdx.x == 0) s_last = dev::last_ticket(ticket, gridDim.x);
+    // the ticket's round trip overlaps the ranking: issued here, its value
+    // first needed after the emit
+    unsigned int tk = 0;
+    if (threadIdx.x == 0)
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(tk) : "l"(ticket) : "memory");
+    const uint32_t me = blockIdx.x * kFinRankPerCta + (threadIdx.x >> 5);
+    if (me < n) {
+        const uint64_t x = s[me];
+        uint32_t rank = 0;
+#pragma unroll 4
+        for (uint32_t j = lane; j < n; j += 32) rank += s[j] > x;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+        if (lane == 0 && rank < want) emit(rank, x, nullptr, out_ids, out_scores, id_base);
+    }
+    if (threadIdx.x == 0) s_last = tk == gridDim.x - 1;
     __syncthreads();
-    if (s_last) {
+    if (s_last) {  // every CTA has read `run`: clear it for the next stage 4
         uint4* r4 = reinterpret_cast<uint4*>(run);
         for (uint32_t i = threadIdx.x; i < n * 8; i += kFinRankThreads) r4[i] = make_uint4(0, 0, 0, 0);
     }
-    const uint32_t me = blockIdx.x * kFinRankPerCta + (threadIdx.x >> 5);
-    if (me >= n) return;
-    const uint64_t x = s[me];
-    uint32_t rank = 0;
-#pragma unroll 4
-    for (uint32_t j = lane; j < n; j += 32) rank += s[j] > x;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
-    if (lane == 0 && rank < want) emit(rank, x, nullptr, out_ids, out_scores, id_base);
 }
 
 __global__ void pad_copy_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ d_n,
