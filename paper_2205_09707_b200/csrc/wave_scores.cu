@@ -341,7 +341,7 @@ wave_scores_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
 #pragma unroll
                         for (int r = 0; r < 32; ++r) {
                             const float v = __uint_as_float(raw[r]);
-                            Srow[r * kScoresPitch] = v;
+                            __stcs(Srow + r * kScoresPitch, v);  // evict-first: keep L2 for C's reuse
                             km |= fset_ge(v, t_cs) & (1u << r);
                             cm |= fset_gt(v, thr0) & (1u << r);
                         }
@@ -349,7 +349,7 @@ wave_scores_kernel(const __grid_constant__ CUtensorMap cmap, uint64_t K, const f
 #pragma unroll
                         for (int r = 0; r < 32; ++r) {
                             const float v = __uint_as_float(raw[r]);
-                            if (uint32_t(r) < nv) Srow[r * kScoresPitch] = v;
+                            if (uint32_t(r) < nv) __stcs(Srow + r * kScoresPitch, v);
                             km |= fset_ge(v, t_cs) & (1u << r);
                             cm |= fset_gt(v, thr0) & (1u << r);
                         }
