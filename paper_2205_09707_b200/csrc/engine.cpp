@@ -449,7 +449,7 @@ Searcher::Searcher(DeviceIndex* index, int device, const plaid_searcher_config& 
         PLAID_CUDA(cudaMemcpy(kconst_.p, &K, sizeof K, cudaMemcpyHostToDevice));
         tensor_ = cfg_.score_mode == PLAID_SCORES_TENSOR && launch::tensor_scores_supported(ix);
         if (tensor_) launch::make_centroid_tensor_map(ix, tmap_);
-        if (tensor_ && ix.tok_inv) qimg_.ensure(launch::kQImgBytes / 4);
+        if (tensor_ && ix.tok_inv) qimg_.ensure((launch::kQImgBytes + launch::kQFragImgBytes) / 4);
     }
     // the zero fills above run on the legacy default stream, which does not
     // order the searcher's non-blocking streams: finish them before any search
@@ -738,11 +738,14 @@ void Searcher::enqueue_back(const float* d_q, uint32_t rows, const plaid_params&
     // finalize + top-k in one launch (the ticket slot was cleared by this query's prologue)
     const launch::RankScratch::Final fin{want_final, d_pids, d_scores, d_n, base,
                                          reinterpret_cast<unsigned int*>(c + kFinTicket)};
-    const bool fused_final = final_fused_ok(rows, p);
+    static const bool s4_tiles = getenv("PLAID_S4_TILES") != nullptr;  // stage4_tensor_kernel instead
+    rank_scratch_.warp_s4 = !s4_tiles && rank_scratch_.tensor_S != nullptr;
+    const bool fused_final = !rank_scratch_.warp_s4 && final_fused_ok(rows, p);
     rank_scratch_.final_out = fused_final ? &fin : nullptr;
     launch::rank_exact(ix, d_q, rows, fin_ids, fin_keys, fin_n, fin_max, keys4_.p, &rank_scratch_, st);
     rank_scratch_.prescanned = scan_fused_ = false;
     rank_scratch_.final_out = nullptr;
+    rank_scratch_.warp_s4 = false;
     record(6, st, times);
     if (fused_final) {
         record(7, st, times);

@@ -325,10 +325,16 @@ struct RankScratch {
         unsigned int* ticket = nullptr;  // zero at launch (a per-query counter)
     };
     const Final* final_out = nullptr;
+    // TENSOR mode: stage 4 as a warp per finalist on mma.sync (s4_mma.cuh)
+    // writing the finalists' keys, instead of stage4_tensor_kernel's tiles
+    bool warp_s4 = false;
 };
 // Bytes of the stage-4 tensor kernel's B-operand image of a query (built by
 // query_prologue when given a destination).
 constexpr uint32_t kQImgBytes = 32 * 1024;
+// ... followed by the query's mma.sync B fragments (s4_mma.cuh layout,
+// [k-step][n-tile][hi, lo][lane] uint2) for stage4_warp_kernel
+constexpr uint32_t kQFragImgBytes = 8 * 4 * 2 * 32 * 8;
 // inv_t = 1 / ||C[code_t] + r_t|| for every index token (d = 128), the
 // reference's arithmetic (residual_codec.cpp:113-130); index-load time.
 void token_inv_norms(const IndexView& ix, float* d_out, cudaStream_t st);

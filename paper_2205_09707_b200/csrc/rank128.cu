@@ -37,6 +37,7 @@
 #include "device.cuh"
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "s4_mma.cuh"
 
 namespace plaid {
 namespace {
@@ -339,6 +340,41 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
         }
         if (warp == 0) rank_stamp(dbg, 4, k);
         mbar_arrive(&empty_bar[b]);
+    }
+}
+
+// ---- K2'': stage 4 on mma.sync (TENSOR mode), a warp per finalist -------------------
+// s4_mma.cuh's scorer over finalist f's tokens [fin_base[f] + pref[f],
+// + pref[f + 1] - pref[f]) (the finalist scan's outputs), the B fragments
+// read from the query image the prologue built (L1-resident after the first
+// tile), the finalist's key straight out — no running-maxima rows, no
+// finalize.  (A CTA per finalist with its tiles dealt over 4 warps, each CTA
+// building its own fragments: 17.9 us against 14.3 at cfg2.)
+constexpr uint32_t kS4wThreads = 128;
+template <int NB>
+__global__ void __launch_bounds__(kS4wThreads)
+stage4_warp_kernel(const IndexView ix, const float* __restrict__ S, const uint2* __restrict__ qf, uint32_t rows,
+                   const uint64_t* __restrict__ d_n, const uint32_t* __restrict__ pref,
+                   const uint64_t* __restrict__ fin_base, const uint32_t* __restrict__ ids,
+                   const uint64_t* __restrict__ keys, uint64_t* __restrict__ out_keys) {
+    dev::pdl_wait();
+    __shared__ uint32_t lut[2 * 256];
+    __shared__ float mrows[kS4wThreads];
+    constexpr uint32_t kPairs = 1u << (2 * NB), kMask = (1u << NB) - 1;
+    for (uint32_t e = threadIdx.x; e < kPairs; e += kS4wThreads) {
+        const float w0 = ix.weights[e & kMask], w1 = ix.weights[e >> NB];
+        lut[e] = s4mma::bf16_pair(w0, w1);
+        lut[256 + e] = s4mma::bf16_pair_lo(w0, w1);
+    }
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kS4wThreads / 32;
+    float* mrow = mrows + warp * 32;
+    const uint32_t n = uint32_t(*d_n);
+    for (uint32_t f = blockIdx.x * nw + warp; f < n; f += gridDim.x * nw) {
+        const uint32_t p0 = __ldcg(pref + f), p1 = __ldcg(pref + f + 1);
+        const uint64_t off = __ldcg(fin_base + f) + p0;
+        const float total = s4mma::finalist<NB>(ix, S, rows, off, p1 - p0, qf, lut, mrow);
+        if (lane == 0) out_keys[f] = dev::make_key(total, finalist_pid(ids, keys, f));
     }
 }
 
@@ -906,6 +942,17 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
         ::plaid::launch::pdl(finalist_scan_kernel, 1, 1024, 0, st, d_ids, d_keys, d_n, ix.doclens, ix.offsets, s.pref,
                              s.fin_base, s.tokens, s.tensor_S ? s.run_p0 : static_cast<uint32_t*>(nullptr));
         count_launch();
+    }
+    if (s.tensor_S && ix.tok_inv && s.warp_s4 && s.qimg) {
+        // TENSOR mode, a warp per finalist: keys straight out (no finalize)
+        const uint32_t nw = kS4wThreads / 32;
+        const uint32_t blocks = uint32_t(std::max<uint64_t>(1, (nmax + nw - 1) / nw));
+        auto wk = ix.nbits == 1 ? stage4_warp_kernel<1> : ix.nbits == 2 ? stage4_warp_kernel<2> : stage4_warp_kernel<4>;
+        const uint2* qf = reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.qimg) + kQImgBytes);
+        ::plaid::launch::pdl(wk, blocks, kS4wThreads, 0, st, ix, s.tensor_S, qf, rows, d_n, s.pref, s.fin_base,
+                             d_ids, d_keys, d_out_keys);
+        count_launch();
+        return true;
     }
     uint64_t fb = (nmax * ix.max_doclen + kTile - 1) / kTile;
     if (fb > uint64_t(sm_count()) * 2) fb = uint64_t(sm_count()) * 2;  // two CTAs (12 warps) per SM

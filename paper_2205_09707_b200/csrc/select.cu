@@ -20,6 +20,7 @@
 #include "device.cuh"
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "s4_mma.cuh"
 
 namespace plaid {
 namespace {
@@ -482,8 +483,23 @@ __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __rest
     if (qcopy)
         for (uint64_t i = gt; i < ncopy4; i += nt)
             reinterpret_cast<float4*>(qcopy)[i] = reinterpret_cast<const float4*>(qsrc)[i];
-    if (qimg)
+    if (qimg) {
         for (uint64_t e = gt; e < launch::kQImgBytes / 16; e += nt) qimg_granule(qsrc, rows, uint32_t(e), qimg);
+        // the mma.sync B fragments (s4_mma.cuh) after it
+        uint2* qf = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(qimg) + launch::kQImgBytes);
+        for (uint64_t e = gt; e < 8 * 4 * 32; e += nt) {
+            const uint32_t ln = uint32_t(e) & 31, j = (uint32_t(e) >> 5) & 3, ks = uint32_t(e) >> 7;
+            const uint32_t n = 8 * j + (ln >> 2), k0 = 16 * ks + 2 * (ln & 3);
+            float x[4] = {0.f, 0.f, 0.f, 0.f};
+            if (n < rows) {
+                const float* qr = qsrc + uint64_t(n) * 128 + k0;
+                x[0] = qr[0], x[1] = qr[1], x[2] = qr[8], x[3] = qr[9];
+            }
+            qf[((ks * 4 + j) * 2 + 0) * 32 + ln] = make_uint2(s4mma::bf16_pair(x[0], x[1]), s4mma::bf16_pair(x[2], x[3]));
+            qf[((ks * 4 + j) * 2 + 1) * 32 + ln] =
+                make_uint2(s4mma::bf16_pair_lo(x[0], x[1]), s4mma::bf16_pair_lo(x[2], x[3]));
+        }
+    }
     for (uint64_t i = gt; i < n16 + m16; i += nt) {
         if (i < n16) zero[i] = make_uint4(0, 0, 0, 0);
         else zero2[i - n16] = make_uint4(0, 0, 0, 0);

@@ -47,6 +47,7 @@
 
 #include "device.cuh"
 #include "kernels.cuh"
+#include "s4_mma.cuh"
 
 namespace plaid {
 namespace {
@@ -89,8 +90,8 @@ constexpr uint32_t kOffK4 = kOffV + kWarps * kTok * 128 * 4;       // kSortCap u
 constexpr uint32_t kEndGH = kOffK4 + kSortCap * 8;
 // G on the tensor cores (WaveArgs::s4_tensor): Q's bf16 hi/lo B fragments,
 // the residual-pair LUTs and a per-warp row of maxima, past the exact G/H layout
-constexpr uint32_t kOffQF = kEndGH;                                 // 8 k-steps x 4 n-tiles x 2 x 32 uint2
-constexpr uint32_t kOffLut = kOffQF + 8 * 4 * 2 * 32 * 8;           // 2 x 256 u32 (hi, lo)
+constexpr uint32_t kOffQF = kEndGH;                                 // s4mma::kQFragBytes
+constexpr uint32_t kOffLut = kOffQF + 8 * 4 * 2 * 32 * 8;           // s4mma::kLutBytes
 constexpr uint32_t kOffMaxRow = kOffLut + 2 * 256 * 4;              // kWarps x 32 f32
 constexpr uint32_t kEndG2 = kOffMaxRow + kWarps * 32 * 4;
 constexpr uint32_t kSmemBytes = kEndAE > kEndGH ? (kEndAE > kEndG2 ? kEndAE : kEndG2) : (kEndGH > kEndG2 ? kEndGH : kEndG2);
@@ -129,27 +130,6 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
         : "=l"(r)
         : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
     return *reinterpret_cast<float2*>(&r);
-}
-
-// D += A . B, m16n8k16, bf16 in, fp32 accumulate (the legacy warp-level
-// tensor path: the worker's 256-thread CTAs have no TMEM of their own)
-__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// (x, y) -> packed bf16 pair (x in the low half) rounded to nearest, and the
-// pair of what rounding left over
-__device__ __forceinline__ uint32_t bf16_pair(float x, float y) {
-    const __nv_bfloat162 v = __floats2bfloat162_rn(x, y);
-    return *reinterpret_cast<const uint32_t*>(&v);
-}
-__device__ __forceinline__ uint32_t bf16_pair_lo(float x, float y) {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
-    return bf16_pair(x - __low2float(h), y - __high2float(h));
 }
 
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t* total) {
@@ -280,52 +260,20 @@ __device__ __forceinline__ float score_passage(const uint32_t* __restrict__ code
     return total;
 }
 
-// Stage 4 on the tensor cores (TENSOR score mode): q_i . v_t with v_t =
-// (C[c_t] + r_t) * inv_t (residual_codec.cpp:97-132) is computed as
-// (S[c_t][i] + r_t . q_i) * inv_t — S is this query's S_cq table (3xTF32),
-// inv_t the per-token norm precomputed at index load, and only r_t . q_i, a
-// product with rows of 2^NB distinct weights, is a GEMM: 16 finalist tokens
-// x 32 query tokens per warp step on mma.sync (bf16 in, fp32 accumulate),
-// split three ways (R_hi Q_hi + R_hi Q_lo + R_lo Q_hi: ~2^-16 relative on
-// the residual term).  MaxSim then takes the max over the finalist's tokens
-// (a 16-row reduction across the fragment's lane groups) and the in-order
-// fp32 sum over the query tokens (maxsim.cpp:66-104).  Same role as the
-// latency path's stage4_tensor_kernel (rank128.cu); scores within 1e-4
-// relative of the exact MaxSim (oracle/compare.py).  A warp takes finalists
-// w, w + 8, ...; tiles never straddle two finalists.
+// Stage 4 on the tensor cores (TENSOR score mode): s4_mma.cuh's warp scorer
+// (r_t . q_i on mma.sync, (S + r.q) * inv, max over the tokens, in-order
+// sum), a warp per finalist w, w + 8, ...; keys into k4.
 template <int NB>
 __device__ __forceinline__ void stage4_tensor(const IndexView& ix, const launch::WaveArgs& a, const float* __restrict__ Q,
                                            const float* __restrict__ S, uint32_t rows, uint32_t n3,
                                            const uint64_t* __restrict__ sel3, uint64_t* f_off, uint32_t* f_len,
                                            uint8_t* smem) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q4 = lane & 3;
-    uint2* qf = reinterpret_cast<uint2*>(smem + kOffQF);  // [ks][j][hi, lo][lane]
-    uint32_t* lut = reinterpret_cast<uint32_t*>(smem + kOffLut);  // [hi, lo][pair index]
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint2* qf = reinterpret_cast<uint2*>(smem + kOffQF);
+    uint32_t* lut = reinterpret_cast<uint32_t*>(smem + kOffLut);
     float* mrow = reinterpret_cast<float*>(smem + kOffMaxRow) + warp * 32;
     uint64_t* k4 = reinterpret_cast<uint64_t*>(smem + kOffK4);
-    // B fragments of Q (n = query token, k = dim): lane ln holds
-    // (Q[n][k0], Q[n][k0 + 1]) and (Q[n][k0 + 8], Q[n][k0 + 9]), n = 8 j + ln / 4,
-    // k0 = 16 ks + 2 (ln % 4)
-    for (uint32_t e = tid; e < 8 * 4 * 32; e += kThreads) {
-        const uint32_t ln = e & 31, j = (e >> 5) & 3, ks = e >> 7;
-        const uint32_t n = 8 * j + (ln >> 2), k0 = 16 * ks + 2 * (ln & 3);
-        float x[4] = {0.f, 0.f, 0.f, 0.f};
-        if (n < rows) {
-            const float* qr = Q + uint64_t(n) * 128 + k0;
-            x[0] = __ldg(qr), x[1] = __ldg(qr + 1), x[2] = __ldg(qr + 8), x[3] = __ldg(qr + 9);
-        }
-        qf[((ks * 4 + j) * 2 + 0) * 32 + ln] = make_uint2(bf16_pair(x[0], x[1]), bf16_pair(x[2], x[3]));
-        qf[((ks * 4 + j) * 2 + 1) * 32 + ln] = make_uint2(bf16_pair_lo(x[0], x[1]), bf16_pair_lo(x[2], x[3]));
-    }
-    // residual pair (dims d, d + 1) -> bf16 pair of their bucket weights: index
-    // = bucket(d) | bucket(d + 1) << NB (dim d's bucket is bits [NB d, NB d + NB)
-    // of the token's little-endian residual row)
-    constexpr uint32_t kPairs = 1u << (2 * NB), kMask = (1u << NB) - 1;
-    for (uint32_t e = tid; e < kPairs; e += kThreads) {
-        const float w0 = ix.weights[e & kMask], w1 = ix.weights[e >> NB];
-        lut[e] = bf16_pair(w0, w1);
-        lut[256 + e] = bf16_pair_lo(w0, w1);
-    }
+    s4mma::setup<NB>(ix, Q, rows, qf, lut);
     for (uint32_t i = tid; i < n3; i += kThreads) {
         const uint32_t pid = dev::key_id(__ldcg(sel3 + i));
         f_off[i] = __ldg(ix.offsets + pid);
@@ -333,84 +281,9 @@ __device__ __forceinline__ void stage4_tensor(const IndexView& ix, const launch:
     }
     __threadfence_block();
     __syncthreads();
-    constexpr uint32_t kWordsPerRow = NB * 4;  // residual row: NB x 16 bytes
     for (uint32_t f = warp; f < n3; f += kWarps) {
-        const uint64_t off = f_off[f];
-        const uint32_t len = f_len[f];
-        float bm[8];
-#pragma unroll
-        for (int x = 0; x < 8; ++x) bm[x] = -INFINITY;
-        for (uint32_t t0 = 0; t0 < len; t0 += 16) {
-            const uint32_t ta = t0 + g, tb = t0 + g + 8;
-            const bool va = ta < len, vb = tb < len;
-            const uint64_t tka = off + (va ? ta : len - 1), tkb = off + (vb ? tb : len - 1);
-            const uint32_t ca = __ldg(ix.codes + tka), cb = __ldg(ix.codes + tkb);
-            const float ia = __ldg(ix.tok_inv + tka), ib = __ldg(ix.tok_inv + tkb);
-            uint32_t ra[kWordsPerRow], rb[kWordsPerRow];
-#pragma unroll
-            for (uint32_t x = 0; x < kWordsPerRow; x += 4) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(ix.residuals + tka * (NB * 16)) + x / 4);
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(ix.residuals + tkb * (NB * 16)) + x / 4);
-                ra[x] = u.x, ra[x + 1] = u.y, ra[x + 2] = u.z, ra[x + 3] = u.w;
-                rb[x] = v.x, rb[x + 1] = v.y, rb[x + 2] = v.z, rb[x + 3] = v.w;
-            }
-            float2 sa[4], sb[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                sa[j] = __ldg(reinterpret_cast<const float2*>(S + uint64_t(ca) * kScoresPitch + 8 * j + 2 * q4));
-                sb[j] = __ldg(reinterpret_cast<const float2*>(S + uint64_t(cb) * kScoresPitch + 8 * j + 2 * q4));
-            }
-            float acc[4][4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-#pragma unroll
-            for (uint32_t ks = 0; ks < 8; ++ks) {
-                // dims d0 = 16 ks + 2 q4 and d0 + 8: bit NB d0 of the row
-                const uint32_t p0 = NB * (16 * ks), sh0 = (p0 & 31) + NB * 2 * q4;
-                const uint32_t w0 = p0 >> 5, w1 = (p0 + NB * 8) >> 5, sh1 = ((p0 + NB * 8) & 31) + NB * 2 * q4;
-                const uint32_t ia0 = (ra[w0] >> sh0) & (kPairs - 1), ib0 = (rb[w0] >> sh0) & (kPairs - 1);
-                const uint32_t ia1 = (ra[w1] >> sh1) & (kPairs - 1), ib1 = (rb[w1] >> sh1) & (kPairs - 1);
-                const uint32_t ah[4] = {lut[ia0], lut[ib0], lut[ia1], lut[ib1]};
-                const uint32_t al[4] = {lut[256 + ia0], lut[256 + ib0], lut[256 + ia1], lut[256 + ib1]};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint2 bh = qf[((ks * 4 + j) * 2 + 0) * 32 + lane];
-                    const uint2 bl = qf[((ks * 4 + j) * 2 + 1) * 32 + lane];
-                    mma_bf16(acc[j], ah, bh.x, bh.y);
-                    mma_bf16(acc[j], ah, bl.x, bl.y);
-                    mma_bf16(acc[j], al, bh.x, bh.y);
-                }
-            }
-            // rows g (token ta) and g + 8 (tb), columns 8 j + 2 q4 + {0, 1}
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float xa0 = va ? __fmul_rn(__fadd_rn(sa[j].x, acc[j][0]), ia) : -INFINITY;
-                const float xa1 = va ? __fmul_rn(__fadd_rn(sa[j].y, acc[j][1]), ia) : -INFINITY;
-                const float xb0 = vb ? __fmul_rn(__fadd_rn(sb[j].x, acc[j][2]), ib) : -INFINITY;
-                const float xb1 = vb ? __fmul_rn(__fadd_rn(sb[j].y, acc[j][3]), ib) : -INFINITY;
-                float m0 = fmaxf(xa0, xb0), m1 = fmaxf(xa1, xb1);
-#pragma unroll
-                for (int o = 4; o < 32; o <<= 1) {
-                    m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-                    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-                }
-                bm[2 * j] = fmaxf(bm[2 * j], m0);
-                bm[2 * j + 1] = fmaxf(bm[2 * j + 1], m1);
-            }
-        }
-        // lanes 0-3 hold the maxima of columns 8 j + 2 q4 + {0, 1}: the
-        // in-order sum over the query tokens
-        if (lane < 4) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) mrow[8 * j + 2 * lane] = bm[2 * j], mrow[8 * j + 2 * lane + 1] = bm[2 * j + 1];
-        }
-        __syncwarp();
-        if (lane == 0) {
-            float total = 0.0f;
-            for (uint32_t i = 0; i < rows; ++i) total = __fadd_rn(total, mrow[i]);
-            k4[f] = dev::make_key(total, dev::key_id(__ldcg(sel3 + f)));
-        }
-        __syncwarp();
+        const float total = s4mma::finalist<NB>(ix, S, rows, f_off[f], f_len[f], qf, lut, mrow);
+        if (lane == 0) k4[f] = dev::make_key(total, dev::key_id(__ldcg(sel3 + f)));
     }
 }
 
