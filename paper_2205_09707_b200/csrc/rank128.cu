@@ -346,9 +346,8 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
 // ---- K2'': stage 4 on mma.sync (TENSOR mode), a warp per finalist -------------------
 // s4_mma.cuh's scorer over finalist f's tokens [fin_base[f] + pref[f],
 // + pref[f + 1] - pref[f]) (the finalist scan's outputs), the B fragments
-// read from the query image the prologue built (L1-resident after the first
-// tile), the finalist's key straight out — no running-maxima rows, no
-// finalize.  (A CTA per finalist with its tiles dealt over 4 warps, each CTA
+// copied from the query image the prologue built, the finalist's key straight
+// out — no running-maxima rows, no finalize.  (A CTA per finalist with its tiles dealt over 4 warps, each CTA
 // building its own fragments: 17.9 us against 14.3 at cfg2.)
 constexpr uint32_t kS4wThreads = 128;
 template <int NB>
@@ -360,11 +359,19 @@ stage4_warp_kernel(const IndexView ix, const float* __restrict__ S, const uint2*
     dev::pdl_wait();
     __shared__ uint32_t lut[2 * 256];
     __shared__ float mrows[kS4wThreads];
+    __shared__ __align__(16) uint2 qs[s4mma::kQFragBytes / 8];
     constexpr uint32_t kPairs = 1u << (2 * NB), kMask = (1u << NB) - 1;
     for (uint32_t e = threadIdx.x; e < kPairs; e += kS4wThreads) {
         const float w0 = ix.weights[e & kMask], w1 = ix.weights[e >> NB];
         lut[e] = s4mma::bf16_pair(w0, w1);
         lut[256 + e] = s4mma::bf16_pair_lo(w0, w1);
+    }
+    // the fragments into shared memory: one coalesced round of 16-byte loads
+    // (read from global inside the MMA loop they cost 14 -> 16 us)
+#pragma unroll
+    for (uint32_t u = 0; u < s4mma::kQFragBytes / 16 / kS4wThreads; ++u) {
+        const uint32_t e = u * kS4wThreads + threadIdx.x;
+        reinterpret_cast<uint4*>(qs)[e] = __ldg(reinterpret_cast<const uint4*>(qf) + e);
     }
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kS4wThreads / 32;
@@ -373,7 +380,7 @@ stage4_warp_kernel(const IndexView ix, const float* __restrict__ S, const uint2*
     for (uint32_t f = blockIdx.x * nw + warp; f < n; f += gridDim.x * nw) {
         const uint32_t p0 = __ldcg(pref + f), p1 = __ldcg(pref + f + 1);
         const uint64_t off = __ldcg(fin_base + f) + p0;
-        const float total = s4mma::finalist<NB>(ix, S, rows, off, p1 - p0, qf, lut, mrow);
+        const float total = s4mma::finalist<NB>(ix, S, rows, off, p1 - p0, qs, lut, mrow);
         if (lane == 0) out_keys[f] = dev::make_key(total, finalist_pid(ids, keys, f));
     }
 }
