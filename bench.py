@@ -544,11 +544,12 @@ def run_plaid(args, cfg):
     if calib and h is not None:
         n3 = calib["n3"]
         ab4 = (4 + 16 * cfg["nbits"]) * calib["T4"] + 12 * n3 + 512 * calib["U4"]
-        k4 = "stage4_tensor_kernel" if args.score_mode == "tensor" else "stream_fused_kernel"
+        k4 = "stage4_warp_kernel" if args.score_mode == "tensor" else "stream_fused_kernel"
         roofs["stage4"] = roof_line(k4, ab4, mean_ph["stage4_rank"], hbm_peak, peak_kind, step_mean_ms,
                                     args.config, "(4 + 16 b) B x T4 codes+residuals + 12 B x n3 + 512 B x U4 "
-                                                 "distinct centroid rows (SURVEY.md §8d); phase = scan + "
-                                                 "stage-4 kernel + finalize")
+                                                 "distinct centroid rows (SURVEY.md §8d); phase = the stage-4 "
+                                                 "kernel (TENSOR: the finalist scan rides in the stage-3 select, "
+                                                 "no finalize)")
     dom = max(roofs, key=lambda n: roofs[n]["mean_ms"])
     roof = dict(roofs[dom])
     roof["dominant_of"] = {n: r["mean_ms"] for n, r in roofs.items()}
