@@ -343,7 +343,7 @@ stream_fused_kernel(const float* __restrict__ C, const uint32_t* __restrict__ co
     }
 }
 
-// ---- K2'': stage 4 on mma.sync (TENSOR mode), a warp per finalist -------------------
+// ---- K2'': stage 4 on mma.sync (TENSOR mode), a warp pair per finalist --------------
 // s4_mma.cuh's scorer over finalist f's tokens [fin_base[f] + pref[f],
 // + pref[f + 1] - pref[f]) (the finalist scan's outputs), the B fragments
 // copied from the query image the prologue built, the finalist's key straight
@@ -374,14 +374,30 @@ stage4_warp_kernel(const IndexView ix, const float* __restrict__ S, const uint2*
         reinterpret_cast<uint4*>(qs)[e] = __ldg(reinterpret_cast<const uint4*>(qf) + e);
     }
     __syncthreads();
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kS4wThreads / 32;
+    // two warps per finalist (tiles alternate between them, the maxima meet
+    // in shared memory): a finalist is ~5 tiles, and one warp chained them
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp >> 1, sub = warp & 1;
+    constexpr uint32_t kPairs2 = kS4wThreads / 64;
     float* mrow = mrows + warp * 32;
     const uint32_t n = uint32_t(*d_n);
-    for (uint32_t f = blockIdx.x * nw + warp; f < n; f += gridDim.x * nw) {
-        const uint32_t p0 = __ldcg(pref + f), p1 = __ldcg(pref + f + 1);
-        const uint64_t off = __ldcg(fin_base + f) + p0;
-        const float total = s4mma::finalist<NB>(ix, S, rows, off, p1 - p0, qs, lut, mrow);
-        if (lane == 0) out_keys[f] = dev::make_key(total, finalist_pid(ids, keys, f));
+    for (uint32_t f0 = blockIdx.x * kPairs2; f0 < n; f0 += gridDim.x * kPairs2) {
+        const uint32_t f = f0 + pair;
+        if (f < n) {
+            const uint32_t p0 = __ldcg(pref + f), p1 = __ldcg(pref + f + 1);
+            const uint64_t off = __ldcg(fin_base + f) + p0;
+            s4mma::finalist_max<NB>(ix, S, off, p1 - p0, 16 * sub, 32, qs, lut, mrow);
+        }
+        __syncthreads();
+        if (f < n && sub == 0) {
+            mrow[lane] = fmaxf(mrow[lane], mrow[32 + lane]);
+            __syncwarp();
+            if (lane == 0) {
+                float total = 0.0f;
+                for (uint32_t i = 0; i < rows; ++i) total = __fadd_rn(total, mrow[i]);
+                out_keys[f] = dev::make_key(total, finalist_pid(ids, keys, f));
+            }
+        }
+        __syncthreads();  // the pair's rows are rewritten next round
     }
 }
 
@@ -952,8 +968,8 @@ bool rank_stream128(const IndexView& ix, const float* d_q, uint32_t rows, const 
     }
     if (s.tensor_S && ix.tok_inv && s.warp_s4 && s.qimg) {
         // TENSOR mode, a warp per finalist: keys straight out (no finalize)
-        const uint32_t nw = kS4wThreads / 32;
-        const uint32_t blocks = uint32_t(std::max<uint64_t>(1, (nmax + nw - 1) / nw));
+        const uint32_t per_cta = kS4wThreads / 64;  // finalists per CTA (two warps each)
+        const uint32_t blocks = uint32_t(std::max<uint64_t>(1, (nmax + per_cta - 1) / per_cta));
         auto wk = ix.nbits == 1 ? stage4_warp_kernel<1> : ix.nbits == 2 ? stage4_warp_kernel<2> : stage4_warp_kernel<4>;
         const uint2* qf = reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(s.qimg) + kQImgBytes);
         ::plaid::launch::pdl(wk, blocks, kS4wThreads, 0, st, ix, s.tensor_S, qf, rows, d_n, s.pref, s.fin_base,
