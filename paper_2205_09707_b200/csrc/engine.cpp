@@ -1739,29 +1739,40 @@ void BatchSearcher::search(const float* q, uint64_t nq, uint64_t rows, uint64_t 
         PLAID_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_n_), nq * sizeof(uint64_t)));
         ho_cap_ = nout + nq;
     }
-    // staging copy into pinned memory: large batches split over host threads
-    // (one core copies ~8 GB/s: 2 ms for 1024 queries)
-    const uint64_t qbytes = nqf * sizeof(float);
-    const uint32_t nthr = qbytes >= (4u << 20) ? std::min<uint32_t>(8, std::max(1u, std::thread::hardware_concurrency()))
-                                               : 1u;
-    if (nthr > 1) {
+    // staging copy into pinned memory, large batches split over host threads
+    // (one core copies ~8 GB/s: 2 ms for 1024 queries); with the wave engine
+    // one wave at a time, so that wave j + 1's staging and upload overlap wave
+    // j on the GPU
+    auto stage = [&](uint64_t b0, uint64_t bytes) {
+        const uint32_t nthr =
+            bytes >= (4u << 20) ? std::min<uint32_t>(8, std::max(1u, std::thread::hardware_concurrency())) : 1u;
+        char* dst = reinterpret_cast<char*>(h_q_) + b0;
+        const char* src = reinterpret_cast<const char*>(q) + b0;
+        if (nthr == 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
         std::vector<std::thread> pool;
-        const uint64_t per = (qbytes / nthr + 4095) & ~uint64_t(4095);
+        const uint64_t per = (bytes / nthr + 4095) & ~uint64_t(4095);
         for (uint32_t t = 0; t < nthr; ++t) {
-            const uint64_t b0 = uint64_t(t) * per;
-            if (b0 >= qbytes) break;
-            const uint64_t len = std::min(per, qbytes - b0);
-            pool.emplace_back([=] {
-                std::memcpy(reinterpret_cast<char*>(h_q_) + b0, reinterpret_cast<const char*>(q) + b0, len);
-            });
+            const uint64_t o = uint64_t(t) * per;
+            if (o >= bytes) break;
+            const uint64_t len = std::min(per, bytes - o);
+            pool.emplace_back([=] { std::memcpy(dst + o, src + o, len); });
         }
         for (auto& th : pool) th.join();
-    } else {
-        std::memcpy(h_q_, q, qbytes);
-    }
+    };
     cudaStream_t st = streams_[0];
-    PLAID_CUDA(cudaMemcpyAsync(q_.p, h_q_, qbytes, cudaMemcpyHostToDevice, st));
-    search_device_impl(q_.p, nq, rows, dim, p, pids_.p, scores_.p, n_.p, st, true);
+    const uint64_t per_q = rows * dim;
+    const uint64_t chunk = wave_ && wave_->supports(p, rows, dim) && wave_->slots() ? wave_->slots() : nq;
+    for (uint64_t j0 = 0; j0 < nq; j0 += chunk) {
+        const uint64_t m = std::min(chunk, nq - j0);
+        stage(j0 * per_q * sizeof(float), m * per_q * sizeof(float));
+        PLAID_CUDA(cudaMemcpyAsync(q_.p + j0 * per_q, h_q_ + j0 * per_q, m * per_q * sizeof(float),
+                                   cudaMemcpyHostToDevice, st));
+        search_device_impl(q_.p + j0 * per_q, m, rows, dim, p, pids_.p + j0 * p.k, scores_.p + j0 * p.k, n_.p + j0,
+                           st, true);
+    }
     PLAID_CUDA(cudaMemcpyAsync(h_n_, n_.p, nq * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     PLAID_CUDA(cudaMemcpyAsync(h_pids_, pids_.p, nout * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     PLAID_CUDA(cudaMemcpyAsync(h_scores_, scores_.p, nout * sizeof(float), cudaMemcpyDeviceToHost, st));
