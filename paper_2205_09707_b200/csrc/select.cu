@@ -477,7 +477,12 @@ __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __rest
     // table (no dependence on this kernel) while the zero fill runs; its other
     // warps still wait for this grid to complete
     dev::pdl_trigger();
-    const uint64_t gt = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x, nt = uint64_t(gridDim.x) * blockDim.x;
+    // with validation the last CTA only runs the norm check (its serial fp64
+    // chains then overlap the other CTAs' work instead of following its own)
+    const bool checker = q != nullptr && blockIdx.x == gridDim.x - 1;
+    const uint32_t work_ctas = q != nullptr ? gridDim.x - 1 : gridDim.x;
+    const uint64_t gt = checker ? ~0ull : blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint64_t nt = uint64_t(work_ctas) * blockDim.x;
     // host path: the query rows come straight from the caller's pinned
     // (mapped) staging buffer — no separate H2D copy ahead of this kernel
     if (qcopy)
@@ -508,7 +513,7 @@ __global__ void __launch_bounds__(256) query_prologue_kernel(const float* __rest
     // CTA: 128-dim slabs of all rows staged with one coalesced round of loads,
     // then thread r runs row r's in-order fp64 add chain from shared memory
     // (the squares are exact in fp64)
-    if (q == nullptr || blockIdx.x != gridDim.x - 1) return;
+    if (!checker) return;
     __shared__ float slab[32][129];
     double acc = 0.0;
     for (uint32_t d0 = 0; d0 < dim; d0 += 128) {
@@ -1202,7 +1207,9 @@ void query_prologue(const float* d_q, uint32_t rows, uint32_t dim, int* d_status
     const uint64_t n16 = nwords / 4, m16 = nwords2 / 4;  // both regions are multiples of 16 bytes
     const bool img = d_qimg && d_qsrc && dim == 128 && rows <= 32;
     // at least one thread per query-image granule (the rows may be in host memory)
-    const uint32_t grid = grid_for(std::max<uint64_t>(n16 + m16, img ? kQImgBytes / 16 : 0), 256, uint32_t(sm_count()));
+    // + one CTA for the norm check when validating
+    const uint32_t grid = grid_for(std::max<uint64_t>(n16 + m16, img ? kQImgBytes / 16 : 0), 256,
+                                   uint32_t(sm_count())) + (d_q ? 1u : 0u);
     static launch::PerDeviceOnce cfg;
     if (cfg.first())  // keep the SMs' shared-memory partition at its maximum so the
                       // S_cq CTAs (213 KB each) can become resident beside this grid
