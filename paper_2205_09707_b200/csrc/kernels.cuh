@@ -230,11 +230,12 @@ void select_top_large(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax
                       SelectState* d_state, uint64_t* d_out_keys, uint64_t* d_out_n,
                       cudaStream_t st);
 // Same result as select_top_large without grid barriers, from the key
-// histogram d_st->hist built by the keys' producer (stage2_finalize /
-// ci_all): one-CTA bucket search, compaction (keys above the boundary bucket
-// -> out, bucket keys -> d_bkeys, capacity nmax; histogram re-zeroed), exact
-// resolution of the bucket by rank (<= 8192 keys) or a one-CTA radix pass
-// (larger).  *d_out_n must be zero on entry.  d_ukeys / d_nu (optional): the
+// histogram d_st->hist built by the keys' producer (range_stage2 /
+// stage2_finalize / ci_all), in ONE launch: every CTA finds the boundary
+// bucket and compacts its share (keys above it -> out, bucket keys ->
+// d_bkeys, capacity nmax); the last CTA to finish (ticket d_st->done)
+// resolves the bucket by a shared-memory radix select (global memory past
+// 16384 keys) and re-zeroes the histogram.  *d_out_n must be zero on entry.  d_ukeys / d_nu (optional): the
 // keys with a positive-capable score (stage 2: candidates owning a kept
 // token), scanned instead of all keys when the boundary lies above score 0.
 void select_top_hist(const uint64_t* d_keys, const uint64_t* d_n, uint64_t nmax, uint64_t want, SelectHist* d_st,
