@@ -175,3 +175,48 @@ def test_k2pow20_tensor_scores(best):
         S0, _ = best.compute_centroid_scores(h, q)
         assert np.abs(S - S0).max() < 5e-6
     _check(best, h, qs[0], P.default_params_for_k(1000), s)
+
+
+_TILES_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_2205_09707_b200 as P
+import oracle
+from oracle.compare import check_tensor_search
+best = oracle.get("ref") if oracle.available("ref") else oracle.get("port")
+h = P.generate_index(20_000, 4096, dim=128, nbits=2, mean_len=64, seed=3)
+qs = P.generate_queries(h, 4, seed=9)
+s = P.Searcher(P.DeviceIndex.from_host(h), score_mode=P.ScoreMode.TENSOR)
+for k in (10, 100, 1000):
+    p = P.default_params_for_k(k)
+    for q in qs:
+        r = s.search(q, p)
+        S, _ = s.compute_centroid_scores(q)
+        rep = check_tensor_search(best, h, q, p, r.topk.passage_ids, r.topk.scores, S,
+                                  got_counters=r.trace.counters())
+        assert rep.ok, (k, rep.problems)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("tiles", ["0", "1"])
+def test_tensor_stage4_variants(tiles):
+    """Both TENSOR stage-4 kernels against the reference, each in a fresh
+    process (the switch is read once per process): the default warp-per-
+    finalist mma.sync kernel, and with PLAID_S4_TILES=1 the tcgen05 tile kernel
+    with its fused finalize + rank sort (run rows re-zeroed by the last CTA:
+    three k values in a row would expose stale rows)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ)
+    env.pop("PLAID_S4_TILES", None)
+    if tiles == "1":
+        env["PLAID_S4_TILES"] = "1"
+    r = subprocess.run([sys.executable, "-c", _TILES_SCRIPT.format(root=root)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
