@@ -224,7 +224,8 @@ template <int NP>
 __global__ void topn_postings_kernel(const uint64_t* __restrict__ partial, uint32_t nwarps, uint32_t nprobe,
                                      uint32_t ntopn, const uint64_t* __restrict__ ivf_offsets,
                                      const uint32_t* __restrict__ postings, uint32_t* __restrict__ sel,
-                                     uint32_t* __restrict__ bitmap, launch::KeepListArgs kl, uint64_t K) {
+                                     uint32_t* __restrict__ bitmap, launch::KeepListArgs kl, uint64_t K,
+                                     const uint32_t* __restrict__ range_tab, uint32_t range_rows) {
     dev::pdl_wait();
     if (blockIdx.x >= ntopn) {
         fused::keep_list(blockIdx.x - ntopn, gridDim.x - ntopn, kl.keep_bits, K, ivf_offsets, kl.list, kl.counts);
@@ -235,7 +236,17 @@ __global__ void topn_postings_kernel(const uint64_t* __restrict__ partial, uint3
     merge_token_lists<NP>(partial, nwarps, i, lists);
     const uint32_t c = dev::key_id(lists[j]);
     if (threadIdx.x == 0) sel[i * nprobe + j] = c;
-    if (!bitmap) return;  // range_stage2 reads the probed lists itself
+    if (!bitmap) {
+        // range_stage2 reads the probed lists itself, starting from this
+        // centroid's range-table row and list start: warm L2 for it
+        if (range_tab) {
+            const uint32_t* row = range_tab + uint64_t(c) * range_rows;
+            for (uint32_t o = threadIdx.x * 32; o < range_rows; o += blockDim.x * 32)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+            if (threadIdx.x == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(ivf_offsets + c));
+        }
+        return;
+    }
     const uint64_t b = ivf_offsets[c], e = ivf_offsets[c + 1];
     // kU postings per thread in flight: unpredicated loads (index clamped into
     // the list), so the ~2K-entry list costs ~3 HBM round trips, not ~9
@@ -392,7 +403,8 @@ void launch_topn_postings(const uint64_t* partial, uint32_t nwarps, uint32_t row
     const uint32_t ntopn = rows * nprobe;
     const uint32_t nkb = kl ? launch::keep_list_blocks(ix.K) : 0;
     ::plaid::launch::pdl(topn_postings_kernel<NP>, ntopn + nkb, threads, smem, st, partial, nwarps, nprobe, ntopn,
-                         ix.ivf_offsets, ix.ivf_postings, sel, bitmap, kl ? *kl : launch::KeepListArgs{}, ix.K);
+                         ix.ivf_offsets, ix.ivf_postings, sel, bitmap, kl ? *kl : launch::KeepListArgs{}, ix.K,
+                         ix.range_tab, ix.range_n + 1);
     launch::count_launch();
 }
 
