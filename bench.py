@@ -727,8 +727,10 @@ def check_and_calibrate(args, h, qs, params, searcher, first):
 def run_plaid_batch(args, cfg):
     """Throughput mode (BASELINE configs[2]): one step = one batch of B queries
     through BatchSearcher (L concurrent lanes); value = queries / job time.
-    Multi-GPU: every rank searches its passage shard (shard-local), the [B][k]
-    results are all-gathered once per batch and merged per query."""
+    Multi-GPU: every rank searches its passage shard.  shard-local: the [B][k]
+    results are all-gathered once per batch and merged per query (one kernel).
+    global-exact (default): BatchShardedSearcher reproduces the single-index
+    cuts (pipeline.cpp:260-275) with three all-gathers per wave of lanes."""
     import torch
 
     import paper_2205_09707_b200 as P
@@ -763,7 +765,17 @@ def run_plaid_batch(args, cfg):
         qs = dq.cpu().numpy()
     idx = P.DeviceIndex.from_host_at(h, pid_base=rank * cfg["N"], device=local)
     mode = P.ScoreMode.EXACT if args.score_mode == "exact" else P.ScoreMode.TENSOR
-    bs = P.BatchSearcher(idx, lanes=args.lanes, device=local, score_mode=mode)
+    gx = None
+    if dist is not None and args.shard_mode == "global-exact":
+        # global-exact throughput mode: lane Searchers run the three shard
+        # phases, three batched all-gathers per wave of lanes (sharded.py)
+        from paper_2205_09707_b200.sharded import BatchShardedSearcher
+
+        gx_lanes = [P.Searcher(idx, device=local, score_mode=mode, record_times=False) for _ in range(args.lanes)]
+        gx = BatchShardedSearcher(gx_lanes, k=k, num_passages=world * cfg["N"], device=torch.device("cuda", local))
+        bs = None
+    else:
+        bs = P.BatchSearcher(idx, lanes=args.lanes, device=local, score_mode=mode)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
@@ -782,6 +794,9 @@ def run_plaid_batch(args, cfg):
 
     def step(i):
         q = dq[i % nb]
+        if gx is not None:
+            gx.search(q, params, m_pids.view(B, k), m_scores.view(B, k), m_n)
+            return
         bs.search_device(q.data_ptr(), B, QLEN, DIM, params, d_pids.data_ptr(), d_scores.data_ptr(),
                          d_n.data_ptr(), stream=sh)
         if dist is not None:
@@ -798,7 +813,8 @@ def run_plaid_batch(args, cfg):
         flush()
         step(i)
     torch.cuda.synchronize()
-    bs.sync()
+    if bs is not None:
+        bs.sync()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     if dist is not None:
@@ -811,10 +827,11 @@ def run_plaid_batch(args, cfg):
         ev[i][0].record(stream)
         step(args.warmup + i)
         ev[i][1].record(stream)
-        launches += bs.last_launches()
+        launches += gx.launches if gx is not None else bs.last_launches()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    bs.sync()
+    if bs is not None:
+        bs.sync()
     step_ms = torch.tensor([a.elapsed_time(b) for a, b in ev], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
@@ -841,7 +858,7 @@ def run_plaid_batch(args, cfg):
 
     hbm_peak, _, peak_kind = measured_peaks()
     K = cfg["K"]
-    wave = bs.last_was_wave()
+    wave = bs.last_was_wave() if bs is not None else False
     if wave and args.score_mode == "tensor":
         # the wave engine: time the first wave's S_cq launch alone and with its
         # worker (launch cap: a batch stops after its first n kernels), events
@@ -931,8 +948,12 @@ def run_plaid_batch(args, cfg):
         "cpu_baseline": cpu,
         "clocks": clk,
     }
-    line["config"]["batch_engine"] = (f"waves of {bs.wave_slots()} queries (one S_cq pass + one worker launch "
-                                      f"each)" if wave else f"{args.lanes} lanes")
+    if gx is not None:
+        line["config"]["batch_engine"] = (f"global-exact: {args.lanes} lane Searchers, shard phases 1-3 per wave of "
+                                          f"{args.lanes} queries, 3 all-gathers per wave")
+    else:
+        line["config"]["batch_engine"] = (f"waves of {bs.wave_slots()} queries (one S_cq pass + one worker launch "
+                                          f"each)" if wave else f"{args.lanes} lanes")
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

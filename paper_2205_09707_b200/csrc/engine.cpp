@@ -784,6 +784,7 @@ void Searcher::shard_phase1(const float* d_q, uint64_t rows, uint64_t dim, const
     ensure_param_buffers(p);
     if (!st) st = stream_;
     launch::reset_launches();
+    const uint64_t l0 = launch::launches();
     pending_ = p;
     pending_q_ = d_q;
     pending_rows_ = uint32_t(rows);
@@ -795,6 +796,7 @@ void Searcher::shard_phase1(const float* d_q, uint64_t rows, uint64_t dim, const
     if (!p.disable_filter)
         launch::export_keys(sel2_.p, counters_.p + kN2, stride2, uint32_t(index_->pid_base()), d_x2, st);
     PLAID_CUDA(cudaGetLastError());
+    phase_launches_ = launch::launches() - l0;
 }
 
 void Searcher::shard_phase2(const uint64_t* d_g2, uint64_t shards, uint64_t* d_x3, uint64_t stride3,
@@ -807,6 +809,7 @@ void Searcher::shard_phase2(const uint64_t* d_g2, uint64_t shards, uint64_t* d_x
     if (!st) st = stream_;
     const bool times = cfg_.record_times != 0;
     const uint32_t base = uint32_t(index_->pid_base());
+    const uint64_t l0 = launch::launches();
     if (!p.disable_filter) {
         launch::threshold_filter(d_g2, shards * pending_stride2_, p.ndocs, sel2_.p, counters_.p + kN2, base, st);
         enqueue_stage3(p, st, times, false);
@@ -815,6 +818,7 @@ void Searcher::shard_phase2(const uint64_t* d_g2, uint64_t shards, uint64_t* d_x
     pending_stride3_ = stride3;
     phase_ = 2;
     PLAID_CUDA(cudaGetLastError());
+    phase_launches_ += launch::launches() - l0;
 }
 
 void Searcher::shard_phase3(const uint64_t* d_g3, uint64_t shards, uint32_t* d_pids, float* d_scores,
@@ -824,13 +828,14 @@ void Searcher::shard_phase3(const uint64_t* d_g3, uint64_t shards, uint32_t* d_p
     DeviceGuard g(device_);
     if (!st) st = stream_;
     const bool times = cfg_.record_times != 0;
+    const uint64_t l0 = launch::launches();
     if (!p.disable_filter)
         launch::threshold_filter(d_g3, shards * pending_stride3_, stage3_width(p), sel3_.p, counters_.p + kN3,
                                  uint32_t(index_->pid_base()), st);
     enqueue_back(pending_q_, pending_rows_, p, d_pids, d_scores, d_n, st, times);
     phase_ = 0;
     PLAID_CUDA(cudaGetLastError());
-    last_launches_ = launch::launches();
+    last_launches_ = phase_launches_ + (launch::launches() - l0);
 }
 
 // ---- batched S_cq (BatchSearcher): the query's prologue on this lane's
@@ -1364,9 +1369,11 @@ void Searcher::merge_topk_rows_device(const uint32_t* d_rows, uint64_t shards, u
     const uint64_t cap = launch::sort_tmp_capacity(total);
     if (cap) sort_tmp_.ensure(cap);
     const uint64_t row = 2 * k + 2;
+    const uint64_t l0 = launch::launches();
     launch::merge_topk(d_rows, reinterpret_cast<const float*>(d_rows + k),
                        reinterpret_cast<const uint64_t*>(d_rows + 2 * k), shards, row, row / 2, k, k, tmp_keys_.p,
                        counters_.p + kTmpN, d_out_pids, d_out_scores, d_out_n, sort_tmp_.p, st);
+    last_launches_ = launch::launches() - l0;
 }
 
 void Searcher::merge_topk(const uint32_t* pids, const float* scores, const uint64_t* counts, uint64_t shards,

@@ -201,6 +201,9 @@ private:
     plaid_searcher_config cfg_;
     cudaStream_t stream_ = nullptr;
     uint64_t last_launches_ = 0;
+    // launches of the shard phases of the pending query, counted per call so
+    // several searchers' phases may interleave on one host thread
+    uint64_t phase_launches_ = 0;
     // captured host-path graphs (plaid_searcher_config.use_graphs)
     struct GraphKey {
         uint64_t rows, k, nprobe, ndocs;

@@ -214,3 +214,122 @@ def search_local_shards(searchers, q, params, num_passages: int, stream: int = 0
         torch.cuda.synchronize(dev)
     m = int(on[0])
     return op[:m].cpu().numpy().view(np.uint32), os_[:m].cpu().numpy()
+
+
+class BatchShardedSearcher:
+    """Global-exact THROUGHPUT mode over passage shards: B queries per call,
+    the reference's single-index cuts (pipeline.cpp:260-275) reproduced
+    exactly, with the key exchanges batched per wave instead of per query.
+
+    `lanes` are this rank's Searchers over the same shard DeviceIndex (each
+    holds one query's state between the phases).  A wave = up to L queries,
+    one per lane: phase 1 on every lane, ONE all-gather of the [L][s2] keys,
+    a device transpose to per-lane [world][s2] rows, phase 2, ONE all-gather
+    of [L][s3], phase 3, ONE all-gather of the packed [L] result rows and a
+    per-lane merge.  Three collectives per wave of L queries (ShardedSearcher
+    pays three per query).  With CUDA, lane l runs its phases on its own
+    stream; the collectives and transposes run on the caller's stream and
+    the lanes are fenced to it on both sides of each exchange."""
+
+    def __init__(self, lanes, k: int, num_passages: int, group=None, device: Optional[torch.device] = None):
+        if not lanes:
+            raise ValueError("need at least one lane searcher")
+        self.lanes = list(lanes)
+        self.L = len(self.lanes)
+        self.k = int(k)
+        self.group = group
+        self.num_passages = int(num_passages)
+        self.world = dist.get_world_size(group)
+        self.dev = device if device is not None else torch.device("cpu")
+        self.row_words = 2 * self.k + 2
+        z = lambda n, dt=torch.int32: torch.zeros(max(n, 1), dtype=dt, device=self.dev)  # noqa: E731
+        self.rows = z(self.L * self.row_words)
+        self.g_rows = z(self.world * self.L * self.row_words)
+        self.t_rows = z(self.L * self.world * self.row_words)
+        self._x = {}
+        self.launches = 0  # kernels the last search() launched (phases + merges)
+        self._streams = None
+        if self.dev.type == "cuda":
+            self._streams = [torch.cuda.Stream(self.dev) for _ in range(self.L)]
+
+    def _buf(self, name: str, n: int) -> torch.Tensor:
+        t = self._x.get(name)
+        if t is None or t.numel() < max(n, 1):
+            t = self._x[name] = torch.zeros(max(n, 1), dtype=torch.int64, device=self.dev)
+        return t
+
+    def _fan_out(self, main):
+        if self._streams is not None:
+            for s in self._streams:
+                s.wait_stream(main)
+
+    def _fan_in(self, main):
+        if self._streams is not None:
+            for s in self._streams:
+                main.wait_stream(s)
+
+    def _lane_stream(self, l: int, main_handle: int) -> int:
+        return self._streams[l].cuda_stream if self._streams is not None else main_handle
+
+    def _exchange(self, x: torch.Tensor, g: torch.Tensor, t: torch.Tensor, n: int, stride: int) -> None:
+        """x [n][stride] (this rank) -> t [n][world][stride] (every rank's row
+        of each lane's query, rank-major as shard_phase{2,3} read it)."""
+        w = self.world
+        _all_gather(g[: w * self.L * stride], x[: self.L * stride], self.group)
+        gv = g[: w * self.L * stride].view(w, self.L, stride)[:, :n]
+        t[: n * w * stride].view(n, w, stride).copy_(gv.transpose(0, 1))
+
+    def search(self, qs: torch.Tensor, params, out_pids: torch.Tensor, out_scores: torch.Tensor,
+               out_n: torch.Tensor, options=None) -> None:
+        """qs: [B, rows, dim] float32 on this rank's device.  Writes the global
+        top-k of query b to out_pids[b, :out_n[b]] / out_scores[b, ...]
+        ([B, k] int32 / float32, out_n [B] int64), ordered on torch's current
+        stream.  Every rank must call with the same B and params."""
+        if int(params.k) != self.k:
+            raise ValueError(f"params.k {params.k} != {self.k}")
+        B, rows, dim = qs.shape
+        df = bool(options.disable_filter) if options is not None else False
+        kw = {"options": options} if options is not None else {}
+        s2, s3 = exchange_strides(params, self.num_passages, df)
+        w, L, k, rw = self.world, self.L, self.k, self.row_words
+        x2, g2, t2 = self._buf("x2", L * s2), self._buf("g2", w * L * s2), self._buf("t2", L * w * s2)
+        x3, g3, t3 = self._buf("x3", L * s3), self._buf("g3", w * L * s3), self._buf("t3", L * w * s3)
+        cuda = self.dev.type == "cuda"
+        main = torch.cuda.current_stream(self.dev) if cuda else None
+        mh = main.cuda_stream if cuda else 0
+        qrow = rows * dim * 4
+        count = lambda s: int(s.last_launches()) if hasattr(s, "last_launches") else 0  # noqa: E731
+        self.launches = 0
+        for b0 in range(0, B, L):
+            n = min(L, B - b0)
+            self._fan_out(main)
+            for l in range(n):
+                self.lanes[l].shard_phase1(qs.data_ptr() + (b0 + l) * qrow, rows, dim, params,
+                                           x2.data_ptr() + 8 * l * s2, s2, stream=self._lane_stream(l, mh), **kw)
+            self._fan_in(main)
+            if s2:
+                self._exchange(x2, g2, t2, n, s2)
+            self._fan_out(main)
+            for l in range(n):
+                self.lanes[l].shard_phase2(t2.data_ptr() + 8 * l * w * s2, w, x3.data_ptr() + 8 * l * s3, s3,
+                                           stream=self._lane_stream(l, mh))
+            self._fan_in(main)
+            if s3:
+                self._exchange(x3, g3, t3, n, s3)
+            self._fan_out(main)
+            base = self.rows.data_ptr()
+            for l in range(n):
+                r = base + 4 * l * rw
+                self.lanes[l].shard_phase3(t3.data_ptr() + 8 * l * w * s3, w, r, r + 4 * k, r + 8 * k,
+                                           stream=self._lane_stream(l, mh))
+                self.launches += count(self.lanes[l])
+            self._fan_in(main)
+            _all_gather(self.g_rows[: w * L * rw], self.rows[: L * rw], self.group)
+            gv = self.g_rows[: w * L * rw].view(w, L, rw)[:, :n]
+            self.t_rows[: n * w * rw].view(n, w, rw).copy_(gv.transpose(0, 1))
+            for l in range(n):
+                b = b0 + l
+                self.lanes[0].merge_topk_rows_device(
+                    self.t_rows.data_ptr() + 4 * l * w * rw, w, k, out_pids.data_ptr() + 4 * b * k,
+                    out_scores.data_ptr() + 4 * b * k, out_n.data_ptr() + 8 * b, stream=mh)
+                self.launches += count(self.lanes[0])

@@ -1,6 +1,8 @@
 """GPU parity: the CUDA engine (through the C ABI) against the CPU oracle on
 identical index bytes and queries.  Integer outputs and, in EXACT score mode,
 every fp32 score must be bit-identical to the reference arithmetic."""
+import os
+
 import numpy as np
 import pytest
 
@@ -510,3 +512,46 @@ def test_merge_topk_rows_device(port):
     m = int(on[0])
     assert np.array_equal(op[:m].cpu().numpy().view(np.uint32), b[0])
     assert np.array_equal(os_[:m].cpu().numpy(), b[1])
+
+
+@pytest.mark.gpu
+def test_batch_sharded_global_exact_world1(port):
+    """Global-exact throughput mode (sharded.BatchShardedSearcher) on one GPU
+    in a world-size-1 NCCL group: 7 queries through 3 lane Searchers (a
+    ragged last wave), each lane on its own stream, the exchanges and
+    rank-major transposes on the caller's stream.  Every [b][k] row equals
+    the reference search of query b, bit for bit."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_09707_b200.sharded import BatchShardedSearcher
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port_no = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        N, K = 6000, 512
+        h = P.generate_index(N, K, dim=128, nbits=2, mean_len=40, seed=4)
+        qs = P.generate_queries(h, 7, seed=21)
+        ix = P.DeviceIndex.from_host_at(h, pid_base=0)
+        for p in [P.default_params_for_k(10), P.default_params_for_k(100), P.SearchParams(50, 4, 0.3, 64)]:
+            lanes = [P.Searcher(ix, score_mode=P.ScoreMode.EXACT, record_times=False) for _ in range(3)]
+            bs = BatchShardedSearcher(lanes, k=p.k, num_passages=N, device=torch.device("cuda", 0))
+            dq = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+            op = torch.zeros(len(qs), p.k, dtype=torch.int32, device="cuda")
+            osc = torch.zeros(len(qs), p.k, dtype=torch.float32, device="cuda")
+            on = torch.zeros(len(qs), dtype=torch.int64, device="cuda")
+            bs.search(dq, p, op, osc, on)
+            torch.cuda.synchronize()
+            assert bs.launches > 0
+            for b, q in enumerate(qs):
+                ids, sc, _ = port.search(h, q, p)
+                m = int(on[b])
+                assert np.array_equal(op[b, :m].cpu().numpy().view(np.uint32), ids), (p, b)
+                assert np.array_equal(bits(osc[b, :m].cpu().numpy()), bits(sc)), (p, b)
+    finally:
+        dist.destroy_process_group()

@@ -274,3 +274,54 @@ def test_two_rank_gloo(tmp_path):
         alls += list(b_)
     ep, es = merge(allp, alls, 20)
     assert np.array_equal(ep, ids) and np.array_equal(es.view(np.uint32), sc.view(np.uint32))
+
+
+def worker_bgx(rank, world, port_no, out_dir):
+    from paper_2205_09707_b200.sharded import BatchShardedSearcher
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, b = shard_range(N, world, rank)
+    h = P.generate_index(b - a, K, dim=DIM, nbits=2, mean_len=16, spread=4, seed=SEED, pid_base=a)
+    whole = P.generate_index(N, K, dim=DIM, nbits=2, mean_len=16, spread=4, seed=SEED)
+    qs = torch.from_numpy(np.ascontiguousarray(P.generate_queries(whole, 5, seed=77)))
+    res = []
+    for p in GX_PARAMS:
+        lanes = []
+        for _ in range(2):
+            sh = OracleShardPhases(h, a)
+            sh.stride2, sh.stride3 = exchange_strides(p, N)
+            lanes.append(sh)
+        bs = BatchShardedSearcher(lanes, k=p.k, num_passages=N)
+        B = qs.shape[0]
+        op = torch.zeros(B, p.k, dtype=torch.int32)
+        osc = torch.zeros(B, p.k, dtype=torch.float32)
+        on = torch.zeros(B, dtype=torch.int64)
+        bs.search(qs, p, op, osc, on)
+        for i in range(B):
+            m = int(on[i])
+            res.append((op[i, :m].numpy().astype(np.uint32), osc[i, :m].numpy().copy()))
+    with open(os.path.join(out_dir, f"bgx{rank}.pkl"), "wb") as f:
+        pickle.dump(res, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_global_exact_gloo(tmp_path, world):
+    """Throughput mode, global-exact: 5 queries through 2 lanes (a ragged last
+    wave), three batched exchanges per wave; every rank's [B][k] equals the
+    UNSHARDED reference search of each query, bit for bit."""
+    mp.spawn(worker_bgx, args=(world, free_port(), str(tmp_path)), nprocs=world, join=True)
+    rs = [pickle.loads((tmp_path / f"bgx{r}.pkl").read_bytes()) for r in range(world)]
+    port = oracle.get("port")
+    whole = P.generate_index(N, K, dim=DIM, nbits=2, mean_len=16, spread=4, seed=SEED)
+    qs = P.generate_queries(whole, 5, seed=77)
+    i = 0
+    for p in GX_PARAMS:
+        for q in qs:
+            ids, sc, _ = port.search(whole, q, p)
+            for r in rs:
+                assert np.array_equal(r[i][0], ids), (p, i)
+                assert np.array_equal(r[i][1].view(np.uint32), sc.view(np.uint32)), (p, i)
+            i += 1
